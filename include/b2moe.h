@@ -1,0 +1,169 @@
+/*
+ * b2moe.h — C-ABI of the B200-native MoE expert path and EP-aware sharded AdamW.
+ *
+ * Drop-in boundary for the reference's hot path (arxiv 2604.00785, "Optimus";
+ * reference tree /root/reference/proj). Each entry point names the reference
+ * interface it replaces. All tensors are DEVICE pointers unless a parameter says
+ * "host"; shapes and layouts are the reference's row-major ones:
+ *   x [S,H]   router [H,N]   gate/up [NR,H,I]   down [NR,I,H]   (NR = N/EP local experts)
+ * Element type per call: B2_F32 (float) or B2_BF16 (bfloat16 bits); routing
+ * scores/weights are always fp32 and expert ids int64 on the host side.
+ *
+ * Every function returns a status: 0 ok, 1 contract violation (the reference's
+ * ContractError, common.hpp:19-21), 2 bad configuration (ConfigError,
+ * common.hpp:24-26), 3 CUDA error, 4 NCCL error; b2_last_error() has the message.
+ * Calls are asynchronous on the context's stream unless documented otherwise.
+ * There is no CPU fallback: without a B200 every compute call returns 3.
+ */
+#ifndef B2MOE_H
+#define B2MOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B2_OK 0
+#define B2_ERR_CONTRACT 1
+#define B2_ERR_CONFIG 2
+#define B2_ERR_CUDA 3
+#define B2_ERR_NCCL 4
+
+#define B2_F32 0
+#define B2_BF16 1
+
+/* replaces optimus::MoeConfig (include/optimus/moe.hpp:13-31) */
+typedef struct {
+    int64_t n_experts;
+    int64_t top_k;
+    int64_t hidden;
+    int64_t intermediate;
+    int32_t ep;
+    int32_t normalize_topk;
+    int64_t token_block;
+} b2_moe_cfg;
+
+/* replaces optimus::AdamWConfig (include/optimus/optim.hpp:11-25) */
+typedef struct {
+    double beta1, beta2, eps, weight_decay, peak_lr, min_lr;
+    int64_t warmup_steps, total_steps;
+    double clip_norm;
+    int32_t clip_after_warmup_only, round_weights_bf16;
+} b2_adamw_cfg;
+
+/* replaces optimus::ParamSlot (optim.hpp:43-49): non-owning device pointers */
+typedef struct {
+    void* weight;       /* [numel] weight_dtype, updated in place by b2_opt_step */
+    const void* grad;   /* [numel] grad_dtype, summed over replicas by b2_opt_step */
+    int64_t numel;
+    int32_t cls;        /* 0 non_expert, 1 expert (optim.hpp:32-35) */
+    int32_t tp_sharded;
+} b2_param;
+
+/* replaces optimus::StepStats (optim.hpp:89-94) */
+typedef struct {
+    int64_t step;
+    double lr, grad_norm, clip_scale;
+} b2_step_stats;
+
+typedef struct b2_ctx b2_ctx;
+typedef struct b2_moe b2_moe;
+typedef struct b2_opt b2_opt;
+
+const char* b2_last_error(void);
+const char* b2_version(void);
+/* 1 when the current device is an sm_100 B200 the tcgen05 kernels run on */
+int b2_device_ok(void);
+
+/* ---- rank context: replaces optimus::RankCtx (comm.hpp:205-231) --------------------
+ * rank layout rank = ((pp*DP + dp)*EP + ep)*TP + tp (comm.hpp:45-59). For world > 1,
+ * nccl_id is the 128-byte ncclUniqueId from b2_nccl_unique_id() on rank 0, shared
+ * by the caller; the DP, EP and DPxEP communicators are split from it. */
+int b2_nccl_unique_id(uint8_t out[128]);
+int b2_ctx_create(int device, void* stream, int rank, int dp, int ep, int tp, int pp, const uint8_t* nccl_id,
+                  b2_ctx** out);
+int b2_ctx_destroy(b2_ctx* ctx);
+int b2_ctx_sync(b2_ctx* ctx);
+
+/* ---- FastSparseMoE layer: replaces fast_moe_forward / fast_moe_backward
+ * (moe.hpp:344-466) and the state they share (FastMoeState, moe.hpp:302-316).
+ * max_tokens is the per-rank S capacity; the state owns its workspace. */
+int b2_moe_create(b2_ctx* ctx, const b2_moe_cfg* cfg, int dtype, int64_t max_tokens, b2_moe** out);
+int b2_moe_destroy(b2_moe* m);
+/* fast_moe_forward (moe.hpp:344-390): out [S,H] */
+int b2_moe_forward(b2_moe* m, const void* x, const void* router, const void* gate, const void* up,
+                   const void* down, int64_t s_tokens, int fur, void* out);
+/* fast_moe_backward (moe.hpp:392-466): aux_probs_grad [S,N] fp32 device or NULL;
+ * expert grads come out pre-scaled by 1/EP like the reference (moe.hpp:458-461). */
+int b2_moe_backward(b2_moe* m, const void* router, const void* gate, const void* up, const void* down,
+                    const void* dout, const float* aux_probs_grad, void* dx, void* drouter, void* dgate,
+                    void* dup, void* ddown);
+/* moe_aux_probs_grad (moe.hpp:331-342) into out [S,N] fp32 device */
+int b2_moe_aux_probs_grad(b2_moe* m, double coeff, float* out);
+/* moe_aux_loss (moe.hpp:320-328); synchronises */
+int b2_moe_aux_loss(b2_moe* m, double* out);
+/* host copies of the local routing (RouteResult, moe.hpp:50-56); synchronises */
+int b2_moe_routing(b2_moe* m, float* probs_host, float* weights_host, int64_t* indices_host);
+/* host copies of RoutingArtifacts (moe.hpp:106-120), same field order as
+ * routing_artifacts_json (moe.cpp:17-32); buffers sized for the maxima
+ * (NR*TH(+1), T, T*K). sizes_host = {t_total, th, rt, padded_rows}. Synchronises. */
+int b2_moe_artifacts(b2_moe* m, int64_t* sizes_host, int64_t* token_counts, int64_t* partial_token_counts,
+                     int64_t* partial_cum, int64_t* cum_token_counts, int64_t* expert_counts,
+                     int64_t* cum_expert_counts, int64_t* input_indices, int64_t* output_indices,
+                     int64_t* selected_k, int64_t* counter);
+/* MoE layer forward+backward with HOST input/output buffers (the reference's
+ * Tensor-in/Tensor-out façade): x_host/dout_host -> out_host/dx_host, weights and
+ * their grads device-resident. Copies run on a side stream overlapped with compute.
+ * Synchronises. */
+int b2_moe_fwd_bwd_host(b2_moe* m, const void* x_host, const void* dout_host, const void* router,
+                        const void* gate, const void* up, const void* down, double aux_coeff, void* out_host,
+                        void* dx_host, void* drouter, void* dgate, void* dup, void* ddown, int64_t s_tokens);
+
+/* ---- standalone routing stages (for identical-score parity checks) ---- */
+/* route (moe.hpp:58-80): logits/probs [S,N] f32, weights [S,K] f32, indices [S,K] int32, all device */
+int b2_route(b2_ctx* ctx, const b2_moe_cfg* cfg, int dtype, const void* x, const void* router, int64_t s_tokens,
+             float* logits, float* probs, float* weights, int32_t* indices);
+/* softmax (kernels.hpp:194-214) + topk (kernels.hpp:235-258) on given scores, device */
+int b2_softmax_topk(b2_ctx* ctx, const float* logits, int64_t rows, int64_t n, int64_t k, int normalize,
+                    float* probs, float* weights, int32_t* indices);
+/* count_tokens + generate_indices (moe.hpp:122-197) on a device [T,K] int32 table;
+ * outputs to host buffers like b2_moe_artifacts. Synchronises. */
+int b2_routing_artifacts(b2_ctx* ctx, const b2_moe_cfg* cfg, const int32_t* indices, int64_t t_total, int ep_rank,
+                         int64_t* sizes_host, int64_t* token_counts, int64_t* partial_token_counts,
+                         int64_t* partial_cum, int64_t* cum_token_counts, int64_t* expert_counts,
+                         int64_t* cum_expert_counts, int64_t* input_indices, int64_t* output_indices,
+                         int64_t* selected_k, int64_t* counter);
+
+/* ---- optimizer: replaces ShardedOptimizer (optim.hpp:98-121, optim.cpp:109-194) ---- */
+#define B2_DDP 0
+#define B2_SO 1
+#define B2_EPSO 2
+int b2_opt_create(b2_ctx* ctx, const b2_adamw_cfg* cfg, const b2_param* params, int nparams, int mode,
+                  int weight_dtype, int grad_dtype, b2_opt** out);
+int b2_opt_destroy(b2_opt* o);
+/* ShardedOptimizer::step (optim.cpp:130-194): reduce-scatter, global norm, clip,
+ * fused AdamW, all-gather. stats may be NULL (then the step does not synchronise). */
+int b2_opt_step(b2_opt* o, b2_step_stats* stats);
+int64_t b2_opt_state_bytes(b2_opt* o);
+/* owned slice [begin,end) of param p (ShardPlan::Entry::own, optim.hpp:62-69) */
+int b2_opt_owned(b2_opt* o, int p, int64_t* begin, int64_t* end);
+/* host copies of the fp32 master / exp_avg / exp_avg_sq of param p's owned slice */
+int b2_opt_get_state(b2_opt* o, int p, float* master, float* exp_avg, float* exp_avg_sq);
+int b2_opt_set_step_count(b2_opt* o, int64_t n);
+/* adamw_update (optim.cpp:88-107) on device slices */
+int b2_adamw_update(b2_ctx* ctx, float* master, float* exp_avg, float* exp_avg_sq, const void* grad,
+                    int grad_dtype, int64_t n, double lr, int64_t step, const b2_adamw_cfg* cfg, void* weight_out,
+                    int weight_dtype, int round_bf16);
+/* lr_at_step (optim.cpp:17-24) and shard_slice (optim.cpp:43-50); host only */
+double b2_lr_at_step(int64_t step, const b2_adamw_cfg* cfg);
+int b2_shard_slice(int64_t numel, int group_size, int position, int64_t* begin, int64_t* end);
+/* number of this library's kernels launched by the last call on the handle */
+int b2_moe_last_launches(b2_moe* m);
+int b2_opt_last_launches(b2_opt* o);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B2MOE_H */

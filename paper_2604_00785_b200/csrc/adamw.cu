@@ -1,0 +1,216 @@
+// Fused optimizer-shard kernels: grad unscale (+ clip) -> AdamW -> bf16 recast.
+//
+// Reference: adamw_update (src/optim.cpp:88-107) and the per-slice steps of
+// ShardedOptimizer::step (optim.cpp:155 mean scale, 160-166 norm, 168-178 clip).
+// The arithmetic is the reference's, in fp64 with fp32-rounded moments, written
+// with explicit _rn intrinsics so nvcc cannot contract it into FMAs: given the same
+// inputs the master, moments and the bf16 weight are bitwise identical to the CPU.
+// HBM traffic per element: grad 2-4 B + master/m/v 12 B in + 12 B out + weight 2-4 B.
+#include "b2_common.cuh"
+#include "kernels.h"
+
+namespace b2 {
+
+__device__ __forceinline__ float load_grad(const void* g, int dtype, int64_t i) {
+    return dtype == F32 ? static_cast<const float*>(g)[i]
+                        : __bfloat162float(static_cast<const __nv_bfloat16*>(g)[i]);
+}
+
+// bf16 round-to-nearest-even of the master (common.hpp:116-131), NaN kept quiet
+__device__ __forceinline__ uint16_t bf16_bits_rne(float f) {
+    const uint32_t u = __float_as_uint(f);
+    if (isnan(f)) return (uint16_t)((u >> 16) | 0x0040u);
+    return (uint16_t)((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+}
+
+struct AdamWDev {
+    double lr, b1, b2, omb1, omb2, eps, lr_wd, bc1, bc2;
+};
+
+__device__ __forceinline__ void adamw_elem(float& master, float& m, float& v, float g, const AdamWDev& c,
+                                           float& wout_f) {
+    double w = (double)master;
+    const double gd = (double)g;
+    w = __dsub_rn(w, __dmul_rn(c.lr_wd, w));                                       // w -= lr*wd*w
+    const double mm = __dadd_rn(__dmul_rn(c.b1, (double)m), __dmul_rn(c.omb1, gd));  // b1*m + (1-b1)*g
+    const double vv = __dadd_rn(__dmul_rn(c.b2, (double)v), __dmul_rn(__dmul_rn(c.omb2, gd), gd));
+    m = (float)mm;
+    v = (float)vv;
+    const double num = __dmul_rn(c.lr, __ddiv_rn((double)m, c.bc1));
+    const double den = __dadd_rn(__dsqrt_rn(__ddiv_rn((double)v, c.bc2)), c.eps);
+    w = __dsub_rn(w, __ddiv_rn(num, den));
+    master = (float)w;
+    wout_f = master;
+}
+
+// grad_scale: the (float)(1/g) of optim.cpp:155; the clip scale is derived on the
+// device from the global norm (optim.cpp:168-171) so the step never waits on the host.
+__global__ void adamw_kernel(float* __restrict__ master, float* __restrict__ mom, float* __restrict__ vel,
+                             const void* __restrict__ grad, int grad_dtype, void* __restrict__ wout, int wdtype,
+                             int64_t n, AdamWDev c, float grad_scale, const double* __restrict__ norm_sq,
+                             double clip_norm, int clip_active, int round_bf16) {
+    double clip = 1.0;
+    if (norm_sq) {
+        const double norm = sqrt(*norm_sq);
+        if (clip_active && norm > clip_norm && norm > 0) clip = clip_norm / norm;
+    }
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        float g = load_grad(grad, grad_dtype, i);
+        if (grad_scale != 1.f) g = __fmul_rn(g, grad_scale);
+        if (clip != 1.0) g = (float)__dmul_rn((double)g, clip);
+        float ms = master[i], mv = mom[i], vv = vel[i], wf;
+        adamw_elem(ms, mv, vv, g, c, wf);
+        master[i] = ms;
+        mom[i] = mv;
+        vel[i] = vv;
+        if (wdtype == F32) {
+            static_cast<float*>(wout)[i] = round_bf16 ? __uint_as_float((uint32_t)bf16_bits_rne(wf) << 16) : wf;
+        } else {
+            static_cast<uint16_t*>(wout)[i] = bf16_bits_rne(wf);
+        }
+    }
+}
+
+// vectorised fast path: bf16 grads, bf16 weights, 4 elements per thread-iteration
+__global__ void adamw_bf16x4_kernel(float4* __restrict__ master, float4* __restrict__ mom, float4* __restrict__ vel,
+                                    const uint2* __restrict__ grad, uint2* __restrict__ wout, int64_t n4, AdamWDev c,
+                                    float grad_scale, const double* __restrict__ norm_sq, double clip_norm,
+                                    int clip_active) {
+    double clip = 1.0;
+    if (norm_sq) {
+        const double norm = sqrt(*norm_sq);
+        if (clip_active && norm > clip_norm && norm > 0) clip = clip_norm / norm;
+    }
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        const uint2 gb = __ldcs(grad + i);
+        float4 ms = __ldcs(master + i), mv = __ldcs(mom + i), vv = __ldcs(vel + i);
+        float g[4] = {__uint_as_float(gb.x << 16), __uint_as_float(gb.x & 0xFFFF0000u), __uint_as_float(gb.y << 16),
+                      __uint_as_float(gb.y & 0xFFFF0000u)};
+        float* pm = &ms.x;
+        float* pv1 = &mv.x;
+        float* pv2 = &vv.x;
+        uint16_t wb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float gq = g[q];
+            if (grad_scale != 1.f) gq = __fmul_rn(gq, grad_scale);
+            if (clip != 1.0) gq = (float)__dmul_rn((double)gq, clip);
+            float wf;
+            adamw_elem(pm[q], pv1[q], pv2[q], gq, c, wf);
+            wb[q] = bf16_bits_rne(wf);
+        }
+        __stcs(master + i, ms);
+        __stcs(mom + i, mv);
+        __stcs(vel + i, vv);
+        __stcs(wout + i, make_uint2((uint32_t)wb[0] | ((uint32_t)wb[1] << 16), (uint32_t)wb[2] | ((uint32_t)wb[3] << 16)));
+    }
+}
+
+// sum of squares of the scaled slice, fp64, fixed-order block reduction, then
+// accumulated into *acc in launch order (deterministic)
+__global__ void sumsq_partial_kernel(const void* __restrict__ g, int dtype, int64_t n, float scale,
+                                     double* __restrict__ partials) {
+    double s = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        float v = load_grad(g, dtype, i);
+        if (scale != 1.f) v = __fmul_rn(v, scale);
+        s += (double)v * (double)v;
+    }
+    __shared__ double red[256];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partials[blockIdx.x] = red[0];
+}
+
+__global__ void sumsq_final_kernel(const double* __restrict__ partials, int nparts, double* __restrict__ acc,
+                                   int init) {
+    if (threadIdx.x != 0) return;
+    double s = 0.0;
+    for (int i = 0; i < nparts; ++i) s += partials[i];
+    *acc = init ? s : *acc + s;
+}
+
+static int adamw_grid(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(148 * 8, ceil_div(n, 256))); }
+
+void launch_adamw_full(const AdamWKernelArgs& a, const double* norm_sq, double clip_norm, int clip_active,
+                       cudaStream_t st) {
+    if (a.n <= 0) return;
+    AdamWDev c;
+    c.lr = a.lr;
+    c.b1 = a.beta1;
+    c.b2 = a.beta2;
+    c.omb1 = 1.0 - a.beta1;
+    c.omb2 = 1.0 - a.beta2;
+    c.eps = a.eps;
+    c.lr_wd = a.lr * a.weight_decay;
+    c.bc1 = a.bc1;
+    c.bc2 = a.bc2;
+    const float gs = (float)a.grad_scale;
+    const bool vec = a.grad_dtype == BF16 && a.weight_dtype == BF16 && a.round_bf16 && a.n % 4 == 0 &&
+                     ((uintptr_t)a.master % 16 == 0) && ((uintptr_t)a.m % 16 == 0) && ((uintptr_t)a.v % 16 == 0) &&
+                     ((uintptr_t)a.grad % 8 == 0) && ((uintptr_t)a.weight_out % 8 == 0);
+    if (vec) {
+        adamw_bf16x4_kernel<<<adamw_grid(a.n / 4), 256, 0, st>>>((float4*)a.master, (float4*)a.m, (float4*)a.v,
+                                                                 (const uint2*)a.grad, (uint2*)a.weight_out, a.n / 4,
+                                                                 c, gs, norm_sq, clip_norm, clip_active);
+    } else {
+        adamw_kernel<<<adamw_grid(a.n), 256, 0, st>>>(a.master, a.m, a.v, a.grad, a.grad_dtype, a.weight_out,
+                                                      a.weight_dtype, a.n, c, gs, norm_sq, clip_norm, clip_active,
+                                                      a.round_bf16);
+    }
+    B2_LAUNCH_CHECK();
+}
+
+void launch_adamw(const AdamWKernelArgs& a, cudaStream_t st) { launch_adamw_full(a, nullptr, 0.0, 0, st); }
+
+void launch_sumsq_acc(const void* g, int dtype, int64_t n, float scale, double* partials, int nparts, double* acc,
+                      bool init, cudaStream_t st) {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nparts, ceil_div(std::max<int64_t>(n, 1), 256)));
+    sumsq_partial_kernel<<<grid, 256, 0, st>>>(g, dtype, n, scale, partials);
+    B2_LAUNCH_CHECK();
+    sumsq_final_kernel<<<1, 32, 0, st>>>(partials, grid, acc, init ? 1 : 0);
+    B2_LAUNCH_CHECK();
+}
+
+void launch_sumsq(const void* g, int dtype, int64_t n, double scale, double* partials, int nparts, cudaStream_t st) {
+    launch_sumsq_acc(g, dtype, n, (float)scale, partials, nparts, partials + nparts, true, st);
+}
+
+__global__ void scale_to_f32_kernel(const void* __restrict__ src, int dtype, int64_t n, float scale,
+                                    float* __restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = __fmul_rn(load_grad(src, dtype, i), scale);
+}
+
+void launch_scale_to_f32(const void* src, int dtype, int64_t n, double scale, float* dst, cudaStream_t st) {
+    if (n <= 0) return;
+    scale_to_f32_kernel<<<adamw_grid(n), 256, 0, st>>>(src, dtype, n, (float)scale, dst);
+    B2_LAUNCH_CHECK();
+}
+
+__global__ void scale_inplace_kernel(void* __restrict__ buf, int dtype, int64_t n, float scale) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (dtype == F32) {
+            float* p = static_cast<float*>(buf);
+            p[i] = __fmul_rn(p[i], scale);
+        } else {
+            __nv_bfloat16* p = static_cast<__nv_bfloat16*>(buf);
+            p[i] = __float2bfloat16_rn(__fmul_rn(__bfloat162float(p[i]), scale));
+        }
+    }
+}
+
+void launch_scale_inplace(void* buf, int dtype, int64_t n, float scale, cudaStream_t st) {
+    if (n <= 0) return;
+    scale_inplace_kernel<<<adamw_grid(n), 256, 0, st>>>(buf, dtype, n, scale);
+    B2_LAUNCH_CHECK();
+}
+
+}  // namespace b2

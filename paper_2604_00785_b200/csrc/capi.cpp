@@ -1,0 +1,515 @@
+// extern "C" entry points of include/b2moe.h over the C++ host classes.
+#include "../../include/b2moe.h"
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "comm.h"
+#include "kernels.h"
+#include "moe_layer.h"
+#include "optim.h"
+
+using namespace b2;
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return B2_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return B2_ERR_CONTRACT;
+    }
+}
+
+MoeConfig to_cfg(const b2_moe_cfg* c) {
+    check(c != nullptr, "moe: null config");
+    MoeConfig m;
+    m.n_experts = c->n_experts;
+    m.top_k = c->top_k;
+    m.hidden = c->hidden;
+    m.intermediate = c->intermediate;
+    m.ep = c->ep;
+    m.token_block = c->token_block;
+    m.normalize_topk = c->normalize_topk != 0;
+    return m;
+}
+
+AdamWConfig to_acfg(const b2_adamw_cfg* a) {
+    check(a != nullptr, "adamw: null config");
+    AdamWConfig c;
+    c.beta1 = a->beta1;
+    c.beta2 = a->beta2;
+    c.eps = a->eps;
+    c.weight_decay = a->weight_decay;
+    c.peak_lr = a->peak_lr;
+    c.min_lr = a->min_lr;
+    c.warmup_steps = a->warmup_steps;
+    c.total_steps = a->total_steps;
+    c.clip_norm = a->clip_norm;
+    c.clip_after_warmup_only = a->clip_after_warmup_only != 0;
+    c.round_weights_bf16 = a->round_weights_bf16 != 0;
+    return c;
+}
+
+void require_device() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) throw CudaError("no CUDA device: the B200 path has no CPU fallback");
+}
+}  // namespace
+
+struct b2_ctx {
+    Context c;
+    std::unique_ptr<Comm> comm;
+    bool own_stream = false;
+    cudaStream_t copy_stream = nullptr;
+};
+struct b2_moe {
+    b2_ctx* ctx;
+    std::unique_ptr<MoeLayer> layer;
+    void* dev_io = nullptr;  // staging for the host-buffer entry point
+    size_t dev_io_bytes = 0;
+    float* auxg = nullptr;
+};
+struct b2_opt {
+    b2_ctx* ctx;
+    std::unique_ptr<ShardedOptimizer> opt;
+};
+
+extern "C" {
+
+const char* b2_last_error(void) { return g_last_error.c_str(); }
+const char* b2_version(void) { return "b2moe 0.1 (sm_100a tcgen05 grouped GEMM, fused EPSO AdamW)"; }
+
+int b2_device_ok(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return 0;
+    return sm100_available() ? 1 : 0;
+}
+
+int b2_nccl_unique_id(uint8_t out[128]) {
+    return guard([&] {
+        ncclUniqueId id;
+        B2_NCCL(ncclGetUniqueId(&id));
+        std::memcpy(out, &id, 128);
+    });
+}
+
+int b2_ctx_create(int device, void* stream, int rank, int dp, int ep, int tp, int pp, const uint8_t* nccl_id,
+                  b2_ctx** out) {
+    return guard([&] {
+        require_device();
+        check(dp >= 1 && ep >= 1 && tp >= 1 && pp >= 1, "topology: axes must be >= 1");
+        const int world = dp * ep * tp * pp;
+        check(rank >= 0 && rank < world, "ctx: rank out of range");
+        auto c = std::make_unique<b2_ctx>();
+        Context& x = c->c;
+        x.device = device;
+        B2_CUDA(cudaSetDevice(device));
+        if (stream) {
+            x.stream = (cudaStream_t)stream;
+        } else {
+            B2_CUDA(cudaStreamCreateWithFlags(&x.stream, cudaStreamNonBlocking));
+            c->own_stream = true;
+        }
+        B2_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        B2_CUDA(cudaDeviceGetAttribute(&x.num_sms, cudaDevAttrMultiProcessorCount, device));
+        x.rank = rank;
+        x.world = world;
+        x.dp = dp;
+        x.ep = ep;
+        x.tp = tp;
+        x.pp = pp;
+        int r = rank;  // coord_of (comm.hpp:49-59)
+        x.coord_tp = r % tp;
+        r /= tp;
+        x.coord_ep = r % ep;
+        r /= ep;
+        x.coord_dp = r % dp;
+        r /= dp;
+        x.coord_pp = r;
+        if (world > 1) {
+            check(nccl_id != nullptr, "ctx: world > 1 needs an NCCL unique id");
+            c->comm.reset(comm_create(nccl_id, rank, dp, ep, tp, pp, x.coord_dp, x.coord_ep, x.coord_tp, x.coord_pp,
+                                      device));
+            x.comm = c->comm.get();
+        }
+        *out = c.release();
+    });
+}
+
+int b2_ctx_destroy(b2_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        cudaStreamSynchronize(ctx->c.stream);
+        ctx->comm.reset();
+        if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+        if (ctx->own_stream) cudaStreamDestroy(ctx->c.stream);
+        delete ctx;
+    });
+}
+
+int b2_ctx_sync(b2_ctx* ctx) { return guard([&] { B2_CUDA(cudaStreamSynchronize(ctx->c.stream)); }); }
+
+int b2_moe_create(b2_ctx* ctx, const b2_moe_cfg* cfg, int dtype, int64_t max_tokens, b2_moe** out) {
+    return guard([&] {
+        check(ctx != nullptr, "moe: null context");
+        auto m = std::make_unique<b2_moe>();
+        m->ctx = ctx;
+        if (dtype == BF16) check(sm100_available(), "bf16 expert path needs an sm_100 (B200) device");
+        m->layer = std::make_unique<MoeLayer>(ctx->c, to_cfg(cfg), dtype, max_tokens);
+        *out = m.release();
+    });
+}
+
+int b2_moe_destroy(b2_moe* m) {
+    return guard([&] {
+        if (!m) return;
+        cudaStreamSynchronize(m->ctx->c.stream);
+        if (m->dev_io) cudaFree(m->dev_io);
+        if (m->auxg) cudaFree(m->auxg);
+        delete m;
+    });
+}
+
+int b2_moe_forward(b2_moe* m, const void* x, const void* router, const void* gate, const void* up, const void* down,
+                   int64_t s_tokens, int fur, void* out) {
+    return guard([&] { m->layer->forward(x, router, gate, up, down, s_tokens, fur != 0, out); });
+}
+
+int b2_moe_backward(b2_moe* m, const void* router, const void* gate, const void* up, const void* down,
+                    const void* dout, const float* aux_probs_grad, void* dx, void* drouter, void* dgate, void* dup,
+                    void* ddown) {
+    return guard([&] { m->layer->backward(router, gate, up, down, dout, aux_probs_grad, dx, drouter, dgate, dup, ddown); });
+}
+
+int b2_moe_aux_probs_grad(b2_moe* m, double coeff, float* out) {
+    return guard([&] { m->layer->aux_probs_grad(coeff, out); });
+}
+
+int b2_moe_aux_loss(b2_moe* m, double* out) { return guard([&] { *out = m->layer->aux_loss(); }); }
+
+int b2_moe_routing(b2_moe* m, float* probs_host, float* weights_host, int64_t* indices_host) {
+    return guard([&] { m->layer->routing(probs_host, weights_host, indices_host); });
+}
+
+static void copy_artifacts(const MoeLayer::HostArtifacts& a, int64_t* sizes, int64_t* token_counts,
+                           int64_t* partial_token_counts, int64_t* partial_cum, int64_t* cum_token_counts,
+                           int64_t* expert_counts, int64_t* cum_expert_counts, int64_t* input_indices,
+                           int64_t* output_indices, int64_t* selected_k, int64_t* counter) {
+    sizes[0] = a.t_total;
+    sizes[1] = a.th;
+    sizes[2] = a.rt;
+    sizes[3] = a.padded_rows;
+    auto cp = [](int64_t* dst, const std::vector<int64_t>& v) {
+        if (dst && !v.empty()) std::memcpy(dst, v.data(), 8 * v.size());
+    };
+    cp(token_counts, a.token_counts);
+    cp(partial_token_counts, a.partial_token_counts);
+    cp(partial_cum, a.partial_cum);
+    cp(cum_token_counts, a.cum_token_counts);
+    cp(expert_counts, a.expert_counts);
+    cp(cum_expert_counts, a.cum_expert_counts);
+    cp(input_indices, a.input_indices);
+    cp(output_indices, a.output_indices);
+    cp(selected_k, a.selected_k);
+    cp(counter, a.counter);
+}
+
+int b2_moe_artifacts(b2_moe* m, int64_t* sizes_host, int64_t* token_counts, int64_t* partial_token_counts,
+                     int64_t* partial_cum, int64_t* cum_token_counts, int64_t* expert_counts,
+                     int64_t* cum_expert_counts, int64_t* input_indices, int64_t* output_indices,
+                     int64_t* selected_k, int64_t* counter) {
+    return guard([&] {
+        copy_artifacts(m->layer->artifacts(), sizes_host, token_counts, partial_token_counts, partial_cum,
+                       cum_token_counts, expert_counts, cum_expert_counts, input_indices, output_indices, selected_k,
+                       counter);
+    });
+}
+
+int b2_moe_fwd_bwd_host(b2_moe* m, const void* x_host, const void* dout_host, const void* router, const void* gate,
+                        const void* up, const void* down, double aux_coeff, void* out_host, void* dx_host,
+                        void* drouter, void* dgate, void* dup, void* ddown, int64_t s_tokens) {
+    return guard([&] {
+        MoeLayer& L = *m->layer;
+        const MoeConfig& c = L.cfg();
+        Context& cx = m->ctx->c;
+        const size_t es = dtype_size(L.dtype());
+        const size_t tok_bytes = (size_t)s_tokens * (size_t)c.hidden * es;
+        if (m->dev_io_bytes < 4 * tok_bytes) {
+            if (m->dev_io) B2_CUDA(cudaFree(m->dev_io));
+            B2_CUDA(cudaMalloc(&m->dev_io, std::max<size_t>(4 * tok_bytes, 256)));
+            m->dev_io_bytes = 4 * tok_bytes;
+            if (m->auxg) B2_CUDA(cudaFree(m->auxg));
+            B2_CUDA(cudaMalloc((void**)&m->auxg, sizeof(float) * std::max<int64_t>(1, L.cfg().n_experts * s_tokens)));
+        }
+        char* base = (char*)m->dev_io;
+        void *dx_in = base, *ddout = base + tok_bytes, *dout_d = base + 2 * tok_bytes, *ddx = base + 3 * tok_bytes;
+        cudaStream_t st = cx.stream, cs = m->ctx->copy_stream;
+        cudaEvent_t ev_x, ev_dout, ev_fwd, ev_out;
+        B2_CUDA(cudaEventCreateWithFlags(&ev_x, cudaEventDisableTiming));
+        B2_CUDA(cudaEventCreateWithFlags(&ev_dout, cudaEventDisableTiming));
+        B2_CUDA(cudaEventCreateWithFlags(&ev_fwd, cudaEventDisableTiming));
+        B2_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+        // x first (forward needs it), dout behind it on the copy stream (overlaps the forward)
+        B2_CUDA(cudaMemcpyAsync(dx_in, x_host, tok_bytes, cudaMemcpyHostToDevice, cs));
+        B2_CUDA(cudaEventRecord(ev_x, cs));
+        B2_CUDA(cudaMemcpyAsync(dout_d, dout_host, tok_bytes, cudaMemcpyHostToDevice, cs));
+        B2_CUDA(cudaEventRecord(ev_dout, cs));
+        B2_CUDA(cudaStreamWaitEvent(st, ev_x, 0));
+        L.forward(dx_in, router, gate, up, down, s_tokens, false, ddout);
+        B2_CUDA(cudaEventRecord(ev_fwd, st));
+        // the layer output streams back while the backward runs
+        B2_CUDA(cudaStreamWaitEvent(cs, ev_fwd, 0));
+        B2_CUDA(cudaMemcpyAsync(out_host, ddout, tok_bytes, cudaMemcpyDeviceToHost, cs));
+        B2_CUDA(cudaEventRecord(ev_out, cs));
+        const float* auxg = nullptr;
+        if (aux_coeff != 0.0) {
+            L.aux_probs_grad(aux_coeff, m->auxg);
+            auxg = m->auxg;
+        }
+        B2_CUDA(cudaStreamWaitEvent(st, ev_dout, 0));
+        L.backward(router, gate, up, down, dout_d, auxg, ddx, drouter, dgate, dup, ddown);
+        B2_CUDA(cudaMemcpyAsync(dx_host, ddx, tok_bytes, cudaMemcpyDeviceToHost, st));
+        B2_CUDA(cudaStreamWaitEvent(st, ev_out, 0));
+        B2_CUDA(cudaStreamSynchronize(st));
+        cudaEventDestroy(ev_x);
+        cudaEventDestroy(ev_dout);
+        cudaEventDestroy(ev_fwd);
+        cudaEventDestroy(ev_out);
+    });
+}
+
+int b2_route(b2_ctx* ctx, const b2_moe_cfg* cfg, int dtype, const void* x, const void* router, int64_t s_tokens,
+             float* logits, float* probs, float* weights, int32_t* indices) {
+    return guard([&] {
+        MoeConfig c = to_cfg(cfg);
+        c.validate();
+        cudaStream_t st = ctx->c.stream;
+        const int S = (int)s_tokens, H = (int)c.hidden, N = (int)c.n_experts, K = (int)c.top_k;
+        if (dtype == F32) launch_router_logits<float>((const float*)x, (const float*)router, logits, S, H, N, st);
+        else launch_router_logits<__nv_bfloat16>((const __nv_bfloat16*)x, (const __nv_bfloat16*)router, logits, S, H, N, st);
+        launch_softmax_topk(logits, probs, weights, indices, S, N, K, c.normalize_topk, st);
+    });
+}
+
+int b2_softmax_topk(b2_ctx* ctx, const float* logits, int64_t rows, int64_t n, int64_t k, int normalize, float* probs,
+                    float* weights, int32_t* indices) {
+    return guard([&] {
+        check(k >= 1 && k <= n, "topk: k out of range for width");
+        launch_softmax_topk(logits, probs, weights, indices, (int)rows, (int)n, (int)k, normalize != 0, ctx->c.stream);
+    });
+}
+
+int b2_routing_artifacts(b2_ctx* ctx, const b2_moe_cfg* cfg, const int32_t* indices, int64_t t_total, int ep_rank,
+                         int64_t* sizes_host, int64_t* token_counts, int64_t* partial_token_counts,
+                         int64_t* partial_cum, int64_t* cum_token_counts, int64_t* expert_counts,
+                         int64_t* cum_expert_counts, int64_t* input_indices, int64_t* output_indices,
+                         int64_t* selected_k, int64_t* counter) {
+    return guard([&] {
+        MoeConfig c = to_cfg(cfg);
+        c.validate();
+        check(ep_rank >= 0 && ep_rank < c.ep, "count_tokens: ep_rank out of range");
+        cudaStream_t st = ctx->c.stream;
+        const int64_t nr = c.experts_per_rank(), K = c.top_k;
+        const int64_t th = ceil_div(t_total, c.token_block);
+        const int64_t pmax = round_up(t_total * K + nr * (kRowAlign - 1), kRowAlign);
+        const int64_t nch = ceil_div(std::max<int64_t>(t_total, 1), 64);
+        Arena ar;
+        ar.reserve(4 * (size_t)(2 * nch * nr + 2 * t_total + 2 * nr * th + 3 * nr + 4 * t_total * K + pmax + 64) +
+                   32 * 256);
+        RoutingIndexArgs a{};
+        a.gidx = indices;
+        a.T = (int)t_total;
+        a.K = (int)K;
+        a.N = (int)c.n_experts;
+        a.n_start = ep_rank * (int)nr;
+        a.nr = (int)nr;
+        a.tbs = (int)c.token_block;
+        a.th = (int)th;
+        a.whist = ar.take<int32_t>(nch * nr);
+        a.wbase = ar.take<int32_t>(nch * nr);
+        a.expert_counts = ar.take<int32_t>(t_total);
+        a.cum_expert_counts = ar.take<int32_t>(t_total + 1);
+        a.partial_counts = ar.take<int32_t>(nr * th);
+        a.partial_cum = ar.take<int32_t>(nr * th + 1);
+        a.token_counts = ar.take<int32_t>(nr);
+        a.cum_token_counts = ar.take<int32_t>(nr + 1);
+        a.pad_start = ar.take<int32_t>(nr + 1);
+        a.input_indices = ar.take<int32_t>(t_total * K);
+        a.output_indices = ar.take<int32_t>(t_total * K);
+        a.selected_k = ar.take<int32_t>(t_total * K);
+        a.slot_prow = ar.take<int32_t>(t_total * K);
+        a.prow_src = ar.take<int32_t>(pmax);
+        a.err = ar.take<int32_t>(1);
+        B2_CUDA(cudaMemsetAsync(a.err, 0, 4, st));
+        launch_routing_index(a, st);
+        int32_t err = 0;
+        B2_CUDA(cudaMemcpyAsync(&err, a.err, 4, cudaMemcpyDeviceToHost, st));
+        B2_CUDA(cudaStreamSynchronize(st));
+        check(err == 0, "count_tokens: expert id out of range [0," + std::to_string(c.n_experts) + ")");
+        auto d2h = [&](const int32_t* d, int64_t n) {
+            std::vector<int32_t> t((size_t)std::max<int64_t>(n, 0));
+            if (n > 0) B2_CUDA(cudaMemcpy(t.data(), d, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+            return std::vector<int64_t>(t.begin(), t.end());
+        };
+        MoeLayer::HostArtifacts h;
+        h.t_total = t_total;
+        h.th = th;
+        h.cum_token_counts = d2h(a.cum_token_counts, nr + 1);
+        h.rt = h.cum_token_counts[(size_t)nr];
+        h.pad_start = d2h(a.pad_start, nr + 1);
+        h.padded_rows = h.pad_start[(size_t)nr];
+        h.token_counts = d2h(a.token_counts, nr);
+        h.partial_token_counts = d2h(a.partial_counts, nr * th);
+        h.partial_cum = d2h(a.partial_cum, nr * th + 1);
+        h.expert_counts = d2h(a.expert_counts, t_total);
+        h.cum_expert_counts = d2h(a.cum_expert_counts, t_total + 1);
+        h.input_indices = d2h(a.input_indices, h.rt);
+        h.output_indices = d2h(a.output_indices, h.rt);
+        h.selected_k = d2h(a.selected_k, h.rt);
+        h.counter.resize((size_t)(nr * th));
+        for (int64_t i = 0; i < nr * th; ++i) h.counter[(size_t)i] = h.partial_cum[(size_t)i + 1];
+        copy_artifacts(h, sizes_host, token_counts, partial_token_counts, partial_cum, cum_token_counts, expert_counts,
+                       cum_expert_counts, input_indices, output_indices, selected_k, counter);
+    });
+}
+
+int b2_opt_create(b2_ctx* ctx, const b2_adamw_cfg* cfg, const b2_param* params, int nparams, int mode,
+                  int weight_dtype, int grad_dtype, b2_opt** out) {
+    return guard([&] {
+        check(ctx != nullptr, "optimizer: null context");
+        if (mode < 0 || mode > 2) throw ConfigError("unknown optimizer sharding mode (expected ddp, so, or epso)");
+        std::vector<ParamSlot> slots((size_t)nparams);
+        for (int i = 0; i < nparams; ++i) {
+            slots[(size_t)i].weight = params[i].weight;
+            slots[(size_t)i].grad = params[i].grad;
+            slots[(size_t)i].numel = params[i].numel;
+            slots[(size_t)i].expert = params[i].cls == 1;
+            slots[(size_t)i].tp_sharded = params[i].tp_sharded != 0;
+        }
+        auto o = std::make_unique<b2_opt>();
+        o->ctx = ctx;
+        o->opt = std::make_unique<ShardedOptimizer>(ctx->c, to_acfg(cfg), std::move(slots), (ShardMode)mode,
+                                                    weight_dtype, grad_dtype);
+        *out = o.release();
+    });
+}
+
+int b2_opt_destroy(b2_opt* o) {
+    return guard([&] {
+        if (!o) return;
+        cudaStreamSynchronize(o->ctx->c.stream);
+        delete o;
+    });
+}
+
+int b2_opt_step(b2_opt* o, b2_step_stats* stats) {
+    return guard([&] {
+        StepStats s = o->opt->step(stats != nullptr);
+        if (stats) {
+            stats->step = s.step;
+            stats->lr = s.lr;
+            stats->grad_norm = s.grad_norm;
+            stats->clip_scale = s.clip_scale;
+        }
+    });
+}
+
+int64_t b2_opt_state_bytes(b2_opt* o) { return o ? o->opt->state_bytes() : -1; }
+
+int b2_opt_owned(b2_opt* o, int p, int64_t* begin, int64_t* end) {
+    return guard([&] { o->opt->owned(p, begin, end); });
+}
+
+int b2_opt_get_state(b2_opt* o, int p, float* master, float* exp_avg, float* exp_avg_sq) {
+    return guard([&] { o->opt->get_state(p, master, exp_avg, exp_avg_sq); });
+}
+
+int b2_opt_set_step_count(b2_opt* o, int64_t n) {
+    return guard([&] { o->opt->set_step_count(n); });
+}
+
+int b2_adamw_update(b2_ctx* ctx, float* master, float* exp_avg, float* exp_avg_sq, const void* grad, int grad_dtype,
+                    int64_t n, double lr, int64_t step, const b2_adamw_cfg* cfg, void* weight_out, int weight_dtype,
+                    int round_bf16) {
+    return guard([&] {
+        AdamWConfig c = to_acfg(cfg);
+        AdamWKernelArgs a{};
+        a.master = master;
+        a.m = exp_avg;
+        a.v = exp_avg_sq;
+        a.grad = grad;
+        a.weight_out = weight_out;
+        a.n = n;
+        a.grad_dtype = grad_dtype;
+        a.weight_dtype = weight_dtype;
+        a.lr = lr;
+        a.beta1 = c.beta1;
+        a.beta2 = c.beta2;
+        a.eps = c.eps;
+        a.weight_decay = c.weight_decay;
+        a.bc1 = 1.0 - std::pow(c.beta1, (double)(step + 1));
+        a.bc2 = 1.0 - std::pow(c.beta2, (double)(step + 1));
+        a.grad_scale = 1.0;
+        a.round_bf16 = round_bf16;
+        launch_adamw(a, ctx->c.stream);
+    });
+}
+
+double b2_lr_at_step(int64_t step, const b2_adamw_cfg* cfg) {
+    double r = -1.0;
+    guard([&] { r = lr_at_step(step, to_acfg(cfg)); });
+    return r;
+}
+
+int b2_shard_slice(int64_t numel, int group_size, int position, int64_t* begin, int64_t* end) {
+    return guard([&] { shard_slice(numel, group_size, position, begin, end); });
+}
+
+int b2_moe_last_launches(b2_moe* m) { return m ? m->layer->last_launches() : 0; }
+int b2_opt_last_launches(b2_opt* o) { return o ? o->opt->last_launches() : 0; }
+
+}  // extern "C"
+
+#include "../../include/b2moe_testing.h"
+
+extern "C" int b2x_grouped_gemm(b2_ctx* ctx, int kind, int hidden, int intermediate, int nr, const int32_t* pad_start,
+                                int64_t pmax, const void* x, const void* wg, const void* wu, const void* wd,
+                                const void* g, const void* u, const void* h, const void* dy, const void* dgu,
+                                void* out0, void* out1, void* out2, float scale) {
+    return guard([&] {
+        check(kind >= 0 && kind <= 5, "grouped gemm: unknown kind");
+        check(sm100_available(), "tcgen05 grouped GEMM needs an sm_100 (B200) device");
+        Sm100GemmArgs a{};
+        a.kind = (GemmKind)kind;
+        a.H = hidden;
+        a.I = intermediate;
+        a.nr = nr;
+        a.pmax = pmax;
+        a.pad_start = pad_start;
+        a.x = x;
+        a.wg = wg;
+        a.wu = wu;
+        a.wd = wd;
+        a.g = g;
+        a.u = u;
+        a.h = h;
+        a.dy = dy;
+        a.dgu = dgu;
+        a.out0 = out0;
+        a.out1 = out1;
+        a.out2 = out2;
+        a.scale = scale;
+        a.num_sms = ctx->c.num_sms;
+        launch_sm100_gemm(a, ctx->c.stream);
+    });
+}

@@ -1,0 +1,148 @@
+// Kernel launchers of the B200 MoE expert path (all asynchronous on `st`).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace b2 {
+
+// ---- router (route.cu) ----
+template <typename T>
+void launch_router_logits(const T* x, const T* w, float* logits, int S, int H, int N, cudaStream_t st);
+void launch_softmax_topk(const float* logits, float* probs, float* topw, int32_t* topi, int S, int N, int K,
+                         bool normalize, cudaStream_t st);
+void launch_fur_route(float* w, int32_t* idx, int S, int N, int K, cudaStream_t st);
+void launch_aux_stats(const float* probs, int S, int N, const int32_t* gidx, int64_t n_gidx, float* partial,
+                      float* mean_probs, int32_t* sel, cudaStream_t st);
+void launch_router_dlogits(const float* probs, const float* wgrad, const int32_t* topi, const float* topw,
+                           const float* aux_grad, float* dlogits, int S, int N, int K, bool normalize, bool fur,
+                           cudaStream_t st);
+void launch_aux_probs_grad(const int32_t* sel, float* out, int S, int N, double coeff, double total,
+                           cudaStream_t st);
+template <typename T>
+void launch_router_dw(const T* x, const float* dlogits, T* dw, int S, int H, int N, cudaStream_t st);
+
+// ---- counting / index generation (index.cu) ----
+struct RoutingIndexArgs {
+    const int32_t* gidx;  // [T, K] gathered expert ids
+    int T, K, N, n_start, nr, tbs, th;
+    int32_t* whist;              // [ceil(T/64), nr]
+    int32_t* wbase;              // [ceil(T/64), nr]
+    int32_t* expert_counts;      // [T]
+    int32_t* cum_expert_counts;  // [T+1]
+    int32_t* partial_counts;     // [nr*th]
+    int32_t* partial_cum;        // [nr*th+1]
+    int32_t* token_counts;       // [nr]
+    int32_t* cum_token_counts;   // [nr+1]
+    int32_t* pad_start;          // [nr+1]
+    int32_t* input_indices;      // [T*K] compact row -> token
+    int32_t* output_indices;     // [T*K] token-major slot -> compact row
+    int32_t* selected_k;         // [T*K]
+    int32_t* slot_prow;          // [T*K] token-major slot -> padded row
+    int32_t* prow_src;           // [pmax] padded row -> token (-1 pad)
+    int32_t* err;                // expert id out of range flag
+};
+void launch_routing_index(const RoutingIndexArgs& a, cudaStream_t st);
+
+// ---- permute / combine / element-wise (permute.cu) ----
+template <typename T>
+void launch_gather_rows(const T* x, const int32_t* prow_src, const int32_t* p_total, T* out, int H, int64_t pmax,
+                        cudaStream_t st);
+template <typename T>
+void launch_zero_pad_rows(T* buf, const int32_t* prow_src, const int32_t* p_total, int W, int64_t pmax,
+                          cudaStream_t st);
+template <typename T>
+void launch_combine(const T* y, const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec,
+                    const float* gw, T* out, int T_tok, int H, int K, cudaStream_t st);
+template <typename T>
+void launch_out_reduction_bwd(const T* dout, const T* y, const int32_t* slot_prow, const int32_t* selected_k,
+                              const int32_t* cec, const float* gw, T* dy, float* wgrad, int T_tok, int H, int K,
+                              cudaStream_t st);
+template <typename T>
+void launch_dx_finalize(const T* src, bool from_slots, const int32_t* slot_prow, const int32_t* cec, const float* dl,
+                        const T* wr, T* dx, int S, int H, int N, cudaStream_t st);
+template <typename T>
+void launch_swiglu_fwd(const T* g, const T* u, T* h, const int32_t* p_total, int I, int64_t pmax, cudaStream_t st);
+template <typename T>
+void launch_swiglu_bwd(const T* g, const T* u, const T* dh, T* dgu, const int32_t* p_total, int I, int64_t pmax,
+                       cudaStream_t st);
+
+// ---- SIMT grouped GEMM (simt_gemm.cu) ----
+struct SimtGemmArgs {
+    const void* A;
+    const void* B;
+    void* D;
+    int64_t lda_m, lda_k, a_gs;
+    int64_t ldb_k, ldb_n, b_gs;
+    int64_t ldd_m, ldd_n, d_gs;
+    const int32_t* group_start;  // [groups+1]
+    int groups;
+    int by_k;
+    int64_t M_lim;  // by_k: M; by_m: row capacity
+    int N, K;       // K used by by_m
+    float scale;
+    int accumulate;
+};
+template <typename T>
+void launch_simt_grouped_gemm(const SimtGemmArgs& a, int64_t m_extent, cudaStream_t st);
+
+// ---- tcgen05 grouped GEMM (gemm_sm100.cu) ----
+enum class GemmKind : int {
+    FwdGateUp = 0,   // [G|U] = X · [Wg|Wu], epilogue: G, U, H = silu(G)·U
+    FwdDown = 1,     // Y = H · Wd
+    BwdDownDgrad = 2,// dH = dY · Wdᵀ, epilogue: SwiGLU backward -> dGU = [dG | dU]
+    BwdDx = 3,       // dX = [dG|dU] · [Wg|Wu]ᵀ   (K = 2I)
+    WgradDown = 4,   // dWd[e] = Hᵀ · dY  over the rows of e
+    WgradGateUp = 5, // [dWg|dWu][e] = Xᵀ · [dG|dU]
+};
+struct Sm100GemmArgs {
+    GemmKind kind;
+    int H, I, nr;              // layer dims, local experts
+    int64_t pmax;              // padded row capacity
+    const int32_t* pad_start;  // [nr+1] device
+    // operands (bf16), meaning depends on kind
+    const void* x;      // mlp_in [P, H]
+    const void* wg;     // [nr, H, I]
+    const void* wu;     // [nr, H, I]
+    const void* wd;     // [nr, I, H]
+    const void* g;      // [P, I]
+    const void* u;      // [P, I]
+    const void* h;      // [P, I]
+    const void* dy;     // [P, H]
+    const void* dgu;    // [P, 2I]
+    void* out0;         // kind-specific outputs
+    void* out1;
+    void* out2;
+    float scale;        // wgrad: 1/EP
+    int num_sms;
+};
+void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st);
+bool sm100_available();
+
+// ---- optimizer (adamw.cu) ----
+struct AdamWKernelArgs {
+    float* master;
+    float* m;
+    float* v;
+    const void* grad;   // owned slice, grad_dtype
+    void* weight_out;   // owned slice of the weight, weight_dtype
+    int64_t n;
+    int grad_dtype, weight_dtype;
+    double lr, beta1, beta2, eps, weight_decay, bc1, bc2;
+    double grad_scale;  // 1/g (the reduce-scatter mean) applied as (float)(g * (float)scale)
+    double clip;        // clip scale (1.0: off)
+    int round_bf16;
+};
+void launch_adamw(const AdamWKernelArgs& a, cudaStream_t st);
+// norm_sq: device fp64 global sum of squares; the clip scale is derived on the device
+void launch_adamw_full(const AdamWKernelArgs& a, const double* norm_sq, double clip_norm, int clip_active,
+                       cudaStream_t st);
+// *acc (=|+=) sum of squares of (float)(g * scale); partials holds >= nparts doubles
+void launch_sumsq_acc(const void* g, int dtype, int64_t n, float scale, double* partials, int nparts, double* acc,
+                      bool init, cudaStream_t st);
+void launch_scale_inplace(void* buf, int dtype, int64_t n, float scale, cudaStream_t st);
+// sum of squares of an fp32/bf16 slice (after the 1/g scale), fp64 partials
+void launch_sumsq(const void* g, int dtype, int64_t n, double scale, double* partials, int nparts, cudaStream_t st);
+void launch_scale_to_f32(const void* src, int dtype, int64_t n, double scale, float* dst, cudaStream_t st);
+
+}  // namespace b2

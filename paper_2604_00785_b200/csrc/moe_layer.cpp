@@ -1,0 +1,476 @@
+// Host orchestration of the FastSparseMoE layer on one B200 (Algorithm 1,
+// include/optimus/moe.hpp:344-466), everything enqueued on the rank's stream with
+// no host synchronisation inside forward/backward: data-dependent sizes (RT, the
+// padded row count) stay on the device and the kernels read them from there.
+//
+// Stage map (reference line -> kernel):
+//   route 357              router_logits + softmax_topk (+ fur_route 360-364)
+//   count/indices 370-371  routing_index (count, scan, stable scatter, pad fill)
+//   expert_forward 374     gather_rows; bf16: tcgen05 FwdGateUp (SwiGLU epilogue) + FwdDown
+//                          fp32: SIMT gate, up, swiglu_fwd, down
+//   combine 377            combine (token-major weighted K-sum)
+//   stats 381-386          aux_stats
+//   backward 402-454       out_reduction_bwd, dgrad/wgrad GEMMs, dx_finalize, router dW
+#include "moe_layer.h"
+
+#include <algorithm>
+#include <cstring>
+
+#include "kernels.h"
+
+namespace b2 {
+
+void MoeConfig::validate() const {
+    check(n_experts >= 1 && top_k >= 1 && hidden >= 1 && intermediate >= 1 && ep >= 1,
+          "moe: config fields must be positive");
+    check(top_k <= n_experts, "moe: top_k cannot exceed n_experts");
+    check(n_experts % ep == 0, "moe: n_experts " + std::to_string(n_experts) + " must divide evenly over ep " +
+                                   std::to_string(ep));
+    check(token_block >= 1, "moe: token_block must be positive");
+}
+
+Arena::~Arena() {
+    if (base_) cudaFree(base_);
+}
+
+void Arena::reserve(size_t bytes) {
+    check(base_ == nullptr, "arena: already reserved");
+    cap_ = bytes;
+    B2_CUDA(cudaMalloc(&base_, std::max<size_t>(cap_, 256)));
+    off_ = 0;
+}
+
+void* Arena::take_bytes(size_t bytes) {
+    const size_t a = (off_ + 255) & ~size_t(255);
+    check(a + bytes <= cap_, "arena: workspace exhausted");
+    off_ = a + bytes;
+    return base_ + a;
+}
+
+MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_tokens)
+    : ctx_(ctx), cfg_(cfg), dtype_(dtype) {
+    cfg_.validate();
+    check(dtype == F32 || dtype == BF16, "moe: dtype must be f32 or bf16");
+    check(cfg_.ep == ctx_.ep, "fast_moe: cfg.ep must match the EP group size");
+    check(max_tokens >= 0, "moe: negative token capacity");
+    const int64_t N = cfg_.n_experts, K = cfg_.top_k, H = cfg_.hidden, I = cfg_.intermediate;
+    const int64_t nr = cfg_.experts_per_rank();
+    smax_ = max_tokens;
+    tmax_ = smax_ * cfg_.ep;  // gathered tokens (reference allgather semantics)
+    pmax_ = round_up(tmax_ * K + nr * (kRowAlign - 1), kRowAlign);
+    thmax_ = ceil_div(std::max<int64_t>(tmax_, 1), cfg_.token_block);
+    const int64_t nch = ceil_div(std::max<int64_t>(tmax_, 1), 64);
+    const size_t es = dtype_size(dtype);
+    size_t bytes = 0;
+    auto acc = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
+    // fp32
+    for (int64_t n : {smax_ * N, smax_ * N, smax_ * K, tmax_ * K, (ceil_div(smax_, 128) + 1) * N, N, tmax_ * K,
+                      smax_ * N})
+        acc(4 * (size_t)std::max<int64_t>(n, 1));
+    // int32
+    for (int64_t n : {smax_ * K, tmax_ * K, N, nch * nr, nch * nr, tmax_, tmax_ + 1, nr * thmax_, nr * thmax_ + 1, nr,
+                      nr + 1, nr + 1, tmax_ * K, tmax_ * K, tmax_ * K, tmax_ * K, pmax_, (int64_t)1})
+        acc(4 * (size_t)std::max<int64_t>(n, 1));
+    // dtype, padded rows
+    for (int64_t n : {pmax_ * H, pmax_ * I, pmax_ * I, pmax_ * I, pmax_ * H, pmax_ * H, pmax_ * I, pmax_ * 2 * I,
+                      pmax_ * H})
+        acc(es * (size_t)std::max<int64_t>(n, 1));
+    B2_CUDA(cudaSetDevice(ctx_.device));
+    arena_.reserve(bytes);
+    logits_ = arena_.take<float>(smax_ * N);
+    probs_ = arena_.take<float>(smax_ * N);
+    topw_ = arena_.take<float>(smax_ * K);
+    fw_ = arena_.take<float>(tmax_ * K);
+    colsum_ = arena_.take<float>((ceil_div(smax_, 128) + 1) * N);
+    mean_probs_ = arena_.take<float>(N);
+    wgrad_ = arena_.take<float>(tmax_ * K);
+    dlogits_ = arena_.take<float>(smax_ * N);
+    topi_ = arena_.take<int32_t>(smax_ * K);
+    fi_ = arena_.take<int32_t>(tmax_ * K);
+    sel_ = arena_.take<int32_t>(N);
+    whist_ = arena_.take<int32_t>(nch * nr);
+    wbase_ = arena_.take<int32_t>(nch * nr);
+    expert_counts_ = arena_.take<int32_t>(tmax_);
+    cec_ = arena_.take<int32_t>(tmax_ + 1);
+    partial_counts_ = arena_.take<int32_t>(nr * thmax_);
+    partial_cum_ = arena_.take<int32_t>(nr * thmax_ + 1);
+    token_counts_ = arena_.take<int32_t>(nr);
+    ctc_ = arena_.take<int32_t>(nr + 1);
+    pad_start_ = arena_.take<int32_t>(nr + 1);
+    input_indices_ = arena_.take<int32_t>(tmax_ * K);
+    output_indices_ = arena_.take<int32_t>(tmax_ * K);
+    selected_k_ = arena_.take<int32_t>(tmax_ * K);
+    slot_prow_ = arena_.take<int32_t>(tmax_ * K);
+    prow_src_ = arena_.take<int32_t>(pmax_);
+    err_ = arena_.take<int32_t>(1);
+    mlp_in_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
+    g_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
+    u_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
+    h_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
+    y_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
+    dy_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
+    dh_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
+    dgu_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * 2 * I, 1));
+    dxp_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
+    B2_CUDA(cudaMemsetAsync(err_, 0, 4, ctx_.stream));
+    B2_CUDA(cudaMemsetAsync(pad_start_, 0, 4 * (nr + 1), ctx_.stream));
+}
+
+MoeLayer::~MoeLayer() = default;
+
+void MoeLayer::forward(const void* x, const void* router, const void* gate, const void* up, const void* down,
+                       int64_t s, bool fur, void* out) {
+    check(s >= 0 && s <= smax_, "fast_moe: token count exceeds the layer's capacity");
+    check(ctx_.ep == 1, "fast_moe: EP > 1 runs through the expert-parallel dispatch (not in this build)");
+    B2_CUDA(cudaSetDevice(ctx_.device));
+    s_ = s;
+    t_ = s * cfg_.ep;
+    th_ = ceil_div(std::max<int64_t>(t_, 0), cfg_.token_block);
+    fur_ = fur;
+    x_ = x;
+    launches_ = 0;
+    if (dtype_ == F32)
+        forward_t<float>((const float*)x, (const float*)router, (const float*)gate, (const float*)up,
+                         (const float*)down, fur, (float*)out);
+    else
+        forward_t<__nv_bfloat16>((const __nv_bfloat16*)x, (const __nv_bfloat16*)router, (const __nv_bfloat16*)gate,
+                                 (const __nv_bfloat16*)up, (const __nv_bfloat16*)down, fur, (__nv_bfloat16*)out);
+    have_fwd_ = true;
+}
+
+template <typename T>
+void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up, const T* down, bool fur, T* out) {
+    cudaStream_t st = ctx_.stream;
+    const int S = (int)s_, Tt = (int)t_, N = (int)cfg_.n_experts, K = (int)cfg_.top_k, H = (int)cfg_.hidden,
+              I = (int)cfg_.intermediate, nr = (int)cfg_.experts_per_rank();
+    // stage 1: route locally (moe.hpp:357-364)
+    launch_router_logits<T>(x, router, logits_, S, H, N, st);
+    launch_softmax_topk(logits_, probs_, topw_, topi_, S, N, K, cfg_.normalize_topk, st);
+    launches_ += 2;
+    if (fur) {
+        launch_fur_route(fw_, fi_, S, N, K, st);
+        launches_ += 1;
+        gw_ = fw_;
+        gi_ = fi_;
+    } else {
+        gw_ = topw_;
+        gi_ = topi_;
+    }
+    // balancing statistics (381-386)
+    launch_aux_stats(probs_, S, N, gi_, (int64_t)Tt * K, colsum_, mean_probs_, sel_, st);
+    launches_ += 3;
+    // stages 2+3 (370-371)
+    RoutingIndexArgs ra{};
+    ra.gidx = gi_;
+    ra.T = Tt;
+    ra.K = K;
+    ra.N = N;
+    ra.n_start = ctx_.coord_ep * nr;
+    ra.nr = nr;
+    ra.tbs = (int)cfg_.token_block;
+    ra.th = (int)th_;
+    ra.whist = whist_;
+    ra.wbase = wbase_;
+    ra.expert_counts = expert_counts_;
+    ra.cum_expert_counts = cec_;
+    ra.partial_counts = partial_counts_;
+    ra.partial_cum = partial_cum_;
+    ra.token_counts = token_counts_;
+    ra.cum_token_counts = ctc_;
+    ra.pad_start = pad_start_;
+    ra.input_indices = input_indices_;
+    ra.output_indices = output_indices_;
+    ra.selected_k = selected_k_;
+    ra.slot_prow = slot_prow_;
+    ra.prow_src = prow_src_;
+    ra.err = err_;
+    launch_routing_index(ra, st);
+    launches_ += 4;
+    const int32_t* p_total = pad_start_ + nr;
+    // stage 4: expert MLP over the padded expert-sorted rows (225-244)
+    launch_gather_rows<T>(x, prow_src_, p_total, (T*)mlp_in_, H, pmax_, st);
+    launches_ += 1;
+    if (dtype_ == BF16) {
+        Sm100GemmArgs ga{};
+        ga.H = H;
+        ga.I = I;
+        ga.nr = nr;
+        ga.pmax = pmax_;
+        ga.pad_start = pad_start_;
+        ga.num_sms = ctx_.num_sms;
+        ga.kind = GemmKind::FwdGateUp;
+        ga.x = mlp_in_;
+        ga.wg = gate;
+        ga.wu = up;
+        ga.out0 = g_;
+        ga.out1 = u_;
+        ga.out2 = h_;
+        launch_sm100_gemm(ga, st);
+        ga.kind = GemmKind::FwdDown;
+        ga.h = h_;
+        ga.wd = down;
+        ga.out0 = y_;
+        launch_sm100_gemm(ga, st);
+        launches_ += 2;
+    } else {
+        SimtGemmArgs a{};
+        a.group_start = pad_start_;
+        a.groups = nr;
+        a.by_k = 0;
+        a.M_lim = pmax_;
+        a.scale = 1.f;
+        // G = X . Wg, U = X . Wu   (A [P,H] K-major; B [H,I] per expert)
+        a.A = mlp_in_;
+        a.lda_m = H;
+        a.lda_k = 1;
+        a.ldb_k = I;
+        a.ldb_n = 1;
+        a.b_gs = (int64_t)H * I;
+        a.ldd_m = I;
+        a.ldd_n = 1;
+        a.N = I;
+        a.K = H;
+        a.B = gate;
+        a.D = g_;
+        launch_simt_grouped_gemm<T>(a, pmax_, st);
+        a.B = up;
+        a.D = u_;
+        launch_simt_grouped_gemm<T>(a, pmax_, st);
+        launch_swiglu_fwd<T>((const T*)g_, (const T*)u_, (T*)h_, p_total, I, pmax_, st);
+        // Y = H . Wd
+        a.A = h_;
+        a.lda_m = I;
+        a.ldb_k = H;
+        a.b_gs = (int64_t)I * H;
+        a.ldd_m = H;
+        a.N = H;
+        a.K = I;
+        a.B = down;
+        a.D = y_;
+        launch_simt_grouped_gemm<T>(a, pmax_, st);
+        launches_ += 4;
+    }
+    // stage 5: weighted combine (377); EP = 1 so the reducescatter (378) is the identity
+    launch_combine<T>((const T*)y_, slot_prow_, selected_k_, cec_, gw_, out, Tt, H, K, st);
+    launches_ += 1;
+}
+
+void MoeLayer::backward(const void* router, const void* gate, const void* up, const void* down, const void* dout,
+                        const float* aux_probs_grad, void* dx, void* drouter, void* dgate, void* dup, void* ddown) {
+    check(have_fwd_, "fast_moe_backward: no forward state");
+    B2_CUDA(cudaSetDevice(ctx_.device));
+    launches_ = 0;
+    if (dtype_ == F32)
+        backward_t<float>((const float*)router, (const float*)gate, (const float*)up, (const float*)down,
+                          (const float*)dout, aux_probs_grad, (float*)dx, (float*)drouter, (float*)dgate,
+                          (float*)dup, (float*)ddown);
+    else
+        backward_t<__nv_bfloat16>((const __nv_bfloat16*)router, (const __nv_bfloat16*)gate,
+                                  (const __nv_bfloat16*)up, (const __nv_bfloat16*)down, (const __nv_bfloat16*)dout,
+                                  aux_probs_grad, (__nv_bfloat16*)dx, (__nv_bfloat16*)drouter,
+                                  (__nv_bfloat16*)dgate, (__nv_bfloat16*)dup, (__nv_bfloat16*)ddown);
+}
+
+template <typename T>
+void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* down, const T* dout,
+                          const float* aux_probs_grad, T* dx, T* drouter, T* dgate, T* dup, T* ddown) {
+    cudaStream_t st = ctx_.stream;
+    const int S = (int)s_, Tt = (int)t_, N = (int)cfg_.n_experts, K = (int)cfg_.top_k, H = (int)cfg_.hidden,
+              I = (int)cfg_.intermediate, nr = (int)cfg_.experts_per_rank();
+    const int32_t* p_total = pad_start_ + nr;
+    const float inv_ep = (float)(1.0 / (double)cfg_.ep);
+    // output_reduction_backward (402-403); EP = 1 so dout is already the allgather (400)
+    launch_out_reduction_bwd<T>(dout, (const T*)y_, slot_prow_, selected_k_, cec_, gw_, (T*)dy_, wgrad_, Tt, H, K, st);
+    launch_zero_pad_rows<T>((T*)dy_, prow_src_, p_total, H, pmax_, st);
+    launches_ += 2;
+    if (dtype_ == BF16) {
+        Sm100GemmArgs ga{};
+        ga.H = H;
+        ga.I = I;
+        ga.nr = nr;
+        ga.pmax = pmax_;
+        ga.pad_start = pad_start_;
+        ga.num_sms = ctx_.num_sms;
+        ga.x = mlp_in_;
+        ga.wg = gate;
+        ga.wu = up;
+        ga.wd = down;
+        ga.g = g_;
+        ga.u = u_;
+        ga.h = h_;
+        ga.dy = dy_;
+        ga.dgu = dgu_;
+        ga.scale = inv_ep;
+        ga.kind = GemmKind::BwdDownDgrad;  // 406 + silu_glu_backward 409
+        ga.out0 = dgu_;
+        launch_sm100_gemm(ga, st);
+        ga.kind = GemmKind::WgradDown;  // 407
+        ga.out0 = ddown;
+        launch_sm100_gemm(ga, st);
+        ga.kind = GemmKind::WgradGateUp;  // 410-413
+        ga.out0 = dgate;
+        ga.out1 = dup;
+        launch_sm100_gemm(ga, st);
+        ga.kind = GemmKind::BwdDx;  // 414-415
+        ga.out0 = dxp_;
+        launch_sm100_gemm(ga, st);
+        launches_ += 4;
+    } else {
+        SimtGemmArgs a{};
+        a.group_start = pad_start_;
+        a.groups = nr;
+        a.scale = 1.f;
+        // dH = dY . Wd^T (grouped_mm_nt): A [P,H]; B(k=h, n=i) = Wd[e][i][h]
+        a.by_k = 0;
+        a.M_lim = pmax_;
+        a.A = dy_;
+        a.lda_m = H;
+        a.lda_k = 1;
+        a.B = down;
+        a.ldb_k = 1;
+        a.ldb_n = H;
+        a.b_gs = (int64_t)I * H;
+        a.D = dh_;
+        a.ldd_m = I;
+        a.ldd_n = 1;
+        a.N = I;
+        a.K = H;
+        launch_simt_grouped_gemm<T>(a, pmax_, st);
+        launch_swiglu_bwd<T>((const T*)g_, (const T*)u_, (const T*)dh_, (T*)dgu_, p_total, I, pmax_, st);
+        // dWd[e] = H^T . dY over the rows of e, scaled 1/EP (407, 458-461)
+        SimtGemmArgs w{};
+        w.group_start = pad_start_;
+        w.groups = nr;
+        w.by_k = 1;
+        w.scale = inv_ep;
+        w.A = h_;
+        w.lda_m = 1;
+        w.lda_k = I;
+        w.B = dy_;
+        w.ldb_k = H;
+        w.ldb_n = 1;
+        w.D = ddown;
+        w.ldd_m = H;
+        w.ldd_n = 1;
+        w.d_gs = (int64_t)I * H;
+        w.M_lim = I;
+        w.N = H;
+        launch_simt_grouped_gemm<T>(w, I, st);
+        // dWg[e] = X^T . dG, dWu[e] = X^T . dU (410-413)
+        w.A = mlp_in_;
+        w.lda_k = H;
+        w.B = dgu_;
+        w.ldb_k = 2 * I;
+        w.D = dgate;
+        w.ldd_m = I;
+        w.d_gs = (int64_t)H * I;
+        w.M_lim = H;
+        w.N = I;
+        launch_simt_grouped_gemm<T>(w, H, st);
+        w.B = (const T*)dgu_ + I;
+        w.D = dup;
+        launch_simt_grouped_gemm<T>(w, H, st);
+        // dX_perm = dG . Wg^T + dU . Wu^T (414-415)
+        a.A = dgu_;
+        a.lda_m = 2 * I;
+        a.B = gate;
+        a.ldb_k = 1;
+        a.ldb_n = I;
+        a.b_gs = (int64_t)H * I;
+        a.D = dxp_;
+        a.ldd_m = H;
+        a.N = H;
+        a.K = I;
+        launch_simt_grouped_gemm<T>(a, pmax_, st);
+        a.A = (const T*)dgu_ + I;
+        a.B = up;
+        a.accumulate = 1;
+        launch_simt_grouped_gemm<T>(a, pmax_, st);
+        launches_ += 7;
+    }
+    // router path (431-454): EP = 1, so weights_grad_local == the full weights grad
+    launch_router_dlogits(probs_, wgrad_, topi_, topw_, aux_probs_grad, dlogits_, S, N, K, cfg_.normalize_topk, fur_,
+                          st);
+    launch_router_dw<T>((const T*)x_, dlogits_, drouter, S, H, N, st);
+    // scatter-add to tokens (418-423) + matmul_nt(dlogits, router) (454)
+    launch_dx_finalize<T>((const T*)dxp_, true, slot_prow_, cec_, dlogits_, router, dx, S, H, N, st);
+    launches_ += 3;
+}
+
+void MoeLayer::aux_probs_grad(double coeff, float* out) {
+    check(have_fwd_, "moe_aux_probs_grad: no forward state");
+    const double total = (double)t_ * (double)cfg_.top_k;
+    launch_aux_probs_grad(sel_, out, (int)s_, (int)cfg_.n_experts, coeff, total, ctx_.stream);
+}
+
+double MoeLayer::aux_loss() {
+    check(have_fwd_, "moe_aux_loss: no forward state");
+    const int N = (int)cfg_.n_experts;
+    std::vector<float> mp(N);
+    std::vector<int32_t> sel(N);
+    B2_CUDA(cudaMemcpyAsync(mp.data(), mean_probs_, 4 * N, cudaMemcpyDeviceToHost, ctx_.stream));
+    B2_CUDA(cudaMemcpyAsync(sel.data(), sel_, 4 * N, cudaMemcpyDeviceToHost, ctx_.stream));
+    B2_CUDA(cudaStreamSynchronize(ctx_.stream));
+    const double total = (double)t_ * (double)cfg_.top_k;
+    double acc = 0;
+    for (int e = 0; e < N; ++e) acc += ((double)sel[e] / total) * (double)mp[e];
+    return (double)N * acc;
+}
+
+static std::vector<int64_t> d2h_i64(const int32_t* d, int64_t n, cudaStream_t st) {
+    std::vector<int32_t> tmp((size_t)std::max<int64_t>(n, 0));
+    if (n > 0) B2_CUDA(cudaMemcpyAsync(tmp.data(), d, 4 * (size_t)n, cudaMemcpyDeviceToHost, st));
+    B2_CUDA(cudaStreamSynchronize(st));
+    return std::vector<int64_t>(tmp.begin(), tmp.end());
+}
+
+MoeLayer::HostArtifacts MoeLayer::artifacts() {
+    check(have_fwd_, "artifacts: no forward state");
+    cudaStream_t st = ctx_.stream;
+    const int64_t nr = cfg_.experts_per_rank();
+    HostArtifacts a;
+    a.t_total = t_;
+    a.th = th_;
+    a.cum_token_counts = d2h_i64(ctc_, nr + 1, st);
+    a.rt = a.cum_token_counts[(size_t)nr];
+    a.pad_start = d2h_i64(pad_start_, nr + 1, st);
+    a.padded_rows = a.pad_start[(size_t)nr];
+    a.token_counts = d2h_i64(token_counts_, nr, st);
+    a.partial_token_counts = d2h_i64(partial_counts_, nr * th_, st);
+    a.partial_cum = d2h_i64(partial_cum_, nr * th_ + 1, st);
+    a.expert_counts = d2h_i64(expert_counts_, t_, st);
+    a.cum_expert_counts = d2h_i64(cec_, t_ + 1, st);
+    a.input_indices = d2h_i64(input_indices_, a.rt, st);
+    a.output_indices = d2h_i64(output_indices_, a.rt, st);
+    a.selected_k = d2h_i64(selected_k_, a.rt, st);
+    // final write cursors of generate_indices (moe.hpp:176-188): partial_cum[ln*TH + tid + 1]
+    a.counter.resize((size_t)(nr * th_));
+    for (int64_t i = 0; i < nr * th_; ++i) a.counter[(size_t)i] = a.partial_cum[(size_t)i + 1];
+    return a;
+}
+
+void MoeLayer::routing(float* probs, float* weights, int64_t* indices) {
+    check(have_fwd_, "routing: no forward state");
+    cudaStream_t st = ctx_.stream;
+    const int64_t N = cfg_.n_experts, K = cfg_.top_k;
+    if (probs) B2_CUDA(cudaMemcpyAsync(probs, probs_, 4 * (size_t)(s_ * N), cudaMemcpyDeviceToHost, st));
+    if (weights) B2_CUDA(cudaMemcpyAsync(weights, topw_, 4 * (size_t)(s_ * K), cudaMemcpyDeviceToHost, st));
+    if (indices) {
+        std::vector<int64_t> v = d2h_i64(topi_, s_ * K, st);
+        std::memcpy(indices, v.data(), 8 * v.size());
+    }
+    B2_CUDA(cudaStreamSynchronize(st));
+}
+
+void MoeLayer::mean_probs_sel(float* mean_probs, int64_t* sel_counts) {
+    cudaStream_t st = ctx_.stream;
+    const int64_t N = cfg_.n_experts;
+    if (mean_probs) B2_CUDA(cudaMemcpyAsync(mean_probs, mean_probs_, 4 * (size_t)N, cudaMemcpyDeviceToHost, st));
+    if (sel_counts) {
+        std::vector<int64_t> v = d2h_i64(sel_, N, st);
+        std::memcpy(sel_counts, v.data(), 8 * v.size());
+    }
+    B2_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace b2

@@ -1,0 +1,120 @@
+// C++ host side of the B200 FastSparseMoE layer: the reference operator API
+// (fast_moe_forward / fast_moe_backward / moe_aux_probs_grad / moe_aux_loss over a
+// FastMoeState, include/optimus/moe.hpp:302-466) on device pointers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <memory>
+#include <vector>
+
+#include "b2_common.cuh"
+
+namespace b2 {
+
+struct MoeConfig {  // moe.hpp:13-31
+    int64_t n_experts = 8, top_k = 2, hidden = 64, intermediate = 128;
+    int ep = 1;
+    int64_t token_block = 8;
+    bool normalize_topk = false;
+    int64_t experts_per_rank() const { return n_experts / ep; }
+    void validate() const;
+};
+
+struct Comm;  // ep collectives (comm.cpp); null for ep == 1
+
+// One CUDA device + stream per rank (the reference's RankCtx, comm.hpp:205-231).
+struct Context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    int rank = 0, world = 1;
+    int dp = 1, ep = 1, tp = 1, pp = 1;
+    int coord_dp = 0, coord_ep = 0, coord_tp = 0, coord_pp = 0;
+    Comm* comm = nullptr;
+};
+
+// Bump allocator over one device allocation (workspace lives as long as the layer).
+class Arena {
+  public:
+    Arena() = default;
+    ~Arena();
+    Arena(const Arena&) = delete;
+    Arena& operator=(const Arena&) = delete;
+    void reserve(size_t bytes);
+    template <typename T>
+    T* take(int64_t n) {
+        return static_cast<T*>(take_bytes((size_t)std::max<int64_t>(n, 1) * sizeof(T)));
+    }
+    void* take_bytes(size_t bytes);
+    size_t used() const { return off_; }
+
+  private:
+    char* base_ = nullptr;
+    size_t cap_ = 0, off_ = 0;
+};
+
+// FastMoeState (moe.hpp:302-316) plus the device workspace of one MoE layer on one rank.
+class MoeLayer {
+  public:
+    MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_tokens);
+    ~MoeLayer();
+
+    // fast_moe_forward (moe.hpp:344-390). All pointers are device pointers of `dtype`.
+    void forward(const void* x, const void* router, const void* gate, const void* up, const void* down, int64_t s,
+                 bool fur, void* out);
+    // fast_moe_backward (moe.hpp:392-466). aux_probs_grad: [S, N] fp32 device or null.
+    void backward(const void* router, const void* gate, const void* up, const void* down, const void* dout,
+                  const float* aux_probs_grad, void* dx, void* drouter, void* dgate, void* dup, void* ddown);
+    // moe_aux_probs_grad (moe.hpp:331-342) into a [S, N] fp32 device buffer
+    void aux_probs_grad(double coeff, float* out);
+    // moe_aux_loss (moe.hpp:320-328); synchronises the stream
+    double aux_loss();
+
+    // host copies of the state for parity checks (synchronise the stream)
+    struct HostArtifacts {
+        int64_t t_total = 0, th = 0, rt = 0, padded_rows = 0;
+        std::vector<int64_t> token_counts, partial_token_counts, partial_cum, cum_token_counts, expert_counts,
+            cum_expert_counts, input_indices, output_indices, selected_k, counter, pad_start;
+    };
+    HostArtifacts artifacts();
+    void routing(float* probs, float* weights, int64_t* indices);  // local rows, host buffers
+    void mean_probs_sel(float* mean_probs, int64_t* sel_counts);
+
+    const MoeConfig& cfg() const { return cfg_; }
+    int dtype() const { return dtype_; }
+    int64_t pmax() const { return pmax_; }
+    int64_t tokens() const { return s_; }
+    size_t workspace_bytes() const { return arena_.used(); }
+    // number of kernels of this library launched by the last forward / backward
+    int last_launches() const { return launches_; }
+
+  private:
+    template <typename T>
+    void forward_t(const T* x, const T* router, const T* gate, const T* up, const T* down, bool fur, T* out);
+    template <typename T>
+    void backward_t(const T* router, const T* gate, const T* up, const T* down, const T* dout,
+                    const float* aux_probs_grad, T* dx, T* drouter, T* dgate, T* dup, T* ddown);
+
+    Context& ctx_;
+    MoeConfig cfg_;
+    int dtype_;
+    int64_t smax_, tmax_, pmax_, thmax_;
+    int64_t s_ = 0, t_ = 0, th_ = 0;
+    bool fur_ = false, have_fwd_ = false;
+    const void* x_ = nullptr;  // the caller's input, kept for the router weight-gradient
+    int launches_ = 0;
+    Arena arena_;
+    // fp32
+    float *logits_, *probs_, *topw_, *fw_, *colsum_, *mean_probs_, *wgrad_, *dlogits_;
+    // int32
+    int32_t *topi_, *fi_, *sel_, *whist_, *wbase_, *expert_counts_, *cec_, *partial_counts_, *partial_cum_,
+        *token_counts_, *ctc_, *pad_start_, *input_indices_, *output_indices_, *selected_k_, *slot_prow_,
+        *prow_src_, *err_;
+    const float* gw_ = nullptr;    // dispatch weights (learned or FUR)
+    const int32_t* gi_ = nullptr;  // dispatch indices
+    // dtype buffers (padded row space)
+    void *mlp_in_, *g_, *u_, *h_, *y_, *dy_, *dh_, *dgu_, *dxp_;
+};
+
+}  // namespace b2

@@ -1,0 +1,76 @@
+// EP-aware sharded AdamW on B200: ShardedOptimizer (include/optimus/optim.hpp:98-121,
+// src/optim.cpp:109-194) over device-resident weights/grads with NCCL collectives.
+#pragma once
+#include <stdint.h>
+
+#include <vector>
+
+#include "comm.h"
+#include "moe_layer.h"
+
+namespace b2 {
+
+struct AdamWConfig {  // optim.hpp:11-25
+    double beta1 = 0.9, beta2 = 0.99, eps = 1e-8, weight_decay = 0.1, peak_lr = 4e-4, min_lr = 4e-5;
+    int64_t warmup_steps = 2500, total_steps = 100000;
+    double clip_norm = 1.0;
+    bool clip_after_warmup_only = true, round_weights_bf16 = true;
+    void validate() const;
+};
+
+double lr_at_step(int64_t step, const AdamWConfig& cfg);
+void shard_slice(int64_t numel, int group_size, int position, int64_t* begin, int64_t* end);
+
+enum class ShardMode { ddp = 0, so = 1, epso = 2 };
+
+struct ParamSlot {
+    void* weight = nullptr;
+    const void* grad = nullptr;
+    int64_t numel = 0;
+    bool expert = false;
+    bool tp_sharded = false;
+};
+
+struct StepStats {
+    int64_t step = 0;
+    double lr = 0, grad_norm = 0, clip_scale = 1.0;
+};
+
+class ShardedOptimizer {
+  public:
+    ShardedOptimizer(Context& ctx, const AdamWConfig& cfg, std::vector<ParamSlot> params, ShardMode mode,
+                     int weight_dtype, int grad_dtype);
+    ~ShardedOptimizer();
+    // want_stats: copy the norm back (synchronises); otherwise fully asynchronous
+    StepStats step(bool want_stats);
+    int64_t state_bytes() const;
+    void owned(int p, int64_t* b, int64_t* e) const;
+    void get_state(int p, float* master, float* m, float* v);
+    void set_step_count(int64_t n) { step_count_ = n; }
+    int last_launches() const { return launches_; }
+
+  private:
+    struct Entry {
+        int64_t own_b = 0, own_e = 0;
+        bool over_dp_ep = false;
+        bool counts = true;
+        float *master = nullptr, *m = nullptr, *v = nullptr;
+        void* scratch = nullptr;       // synced owned slice (grad dtype), when the group has > 1 member
+        void* scratch_full = nullptr;  // SO/DDP pre-reduction buffer
+    };
+    const Group* group_of(const Entry& e) const;
+    Context& ctx_;
+    AdamWConfig cfg_;
+    std::vector<ParamSlot> params_;
+    ShardMode mode_;
+    int wdt_, gdt_;
+    std::vector<Entry> plan_;
+    Arena arena_;
+    double* norm_sq_ = nullptr;  // device
+    double* partials_ = nullptr;
+    int nparts_ = 1184;
+    int64_t step_count_ = 0;
+    int launches_ = 0;
+};
+
+}  // namespace b2

@@ -1,0 +1,381 @@
+// Router: logits = x · Wr, fp64-mirrored softmax, top-k, aux statistics, and the
+// router backward (softmax backward, dWr, dlogits · Wrᵀ).
+//
+// Reference: route (include/optimus/moe.hpp:58-80) over matmul (kernels.hpp:16-49),
+// softmax (kernels.hpp:194-214), topk (kernels.hpp:235-258), fur_route (moe.hpp:84-99),
+// balancing statistics (moe.hpp:381-386), router backward (moe.hpp:431-454).
+//
+// Parity: logits are accumulated exactly like the reference (fp32, p-outer order,
+// separate multiply and add, no FMA contraction), the softmax max/exp/sum/divide
+// follow kernels.hpp:201-212 in fp64 with the sequential sum order, and top-k uses
+// the same strict '>' (ties to the lower expert index). Given identical scores the
+// selections are bit-exact.
+#include "b2_common.cuh"
+#include "kernels.h"
+
+namespace b2 {
+
+// ---- logits: 64 tokens x 64 experts per CTA, 16 outputs per thread -----------------
+
+constexpr int kRtTok = 64, kRtExp = 64, kRtP = 32;
+
+template <typename T>
+__global__ void __launch_bounds__(256) router_logits_kernel(const T* __restrict__ x,
+                                                            const T* __restrict__ w,
+                                                            float* __restrict__ logits, int S,
+                                                            int H, int N) {
+    __shared__ float xs[kRtP][kRtTok + 1];
+    __shared__ float ws[kRtP][kRtExp];
+    const int t0 = blockIdx.x * kRtTok, e0 = blockIdx.y * kRtExp;
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // 16 expert-quads x 16 token-quads
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    for (int p0 = 0; p0 < H; p0 += kRtP) {
+        for (int i = threadIdx.x; i < kRtTok * kRtP; i += 256) {
+            const int tt = i / kRtP, pp = i % kRtP;
+            const int t = t0 + tt, p = p0 + pp;
+            xs[pp][tt] = (t < S && p < H) ? Elem<T>::load(x + (int64_t)t * H + p) : 0.f;
+        }
+        for (int i = threadIdx.x; i < kRtP * kRtExp; i += 256) {
+            const int pp = i / kRtExp, ee = i % kRtExp;
+            const int p = p0 + pp, e = e0 + ee;
+            ws[pp][ee] = (p < H && e < N) ? Elem<T>::load(w + (int64_t)p * N + e) : 0.f;
+        }
+        __syncthreads();
+        const int pend = min(kRtP, H - p0);
+        for (int pp = 0; pp < pend; ++pp) {
+            float a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = xs[pp][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = ws[pp][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(a[i], b[j]));
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int t = t0 + ty * 4 + i;
+        if (t >= S) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int e = e0 + tx * 4 + j;
+            if (e < N) logits[(int64_t)t * N + e] = acc[i][j];
+        }
+    }
+}
+
+// ---- softmax + top-k: one warp per token -------------------------------------------
+
+constexpr int kMaxExpertsPerLane = 8;  // N <= 256
+
+__global__ void softmax_topk_kernel(const float* __restrict__ logits, float* __restrict__ probs,
+                                    float* __restrict__ topw, int32_t* __restrict__ topi, int S,
+                                    int N, int K, int normalize) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+    if (warp >= S) return;
+    const float* lp = logits + (int64_t)warp * N;
+    float v[kMaxExpertsPerLane];
+    double e[kMaxExpertsPerLane];
+    float mx = lp[0];
+#pragma unroll
+    for (int i = 0; i < kMaxExpertsPerLane; ++i) {
+        const int j = lane + 32 * i;
+        v[i] = j < N ? lp[j] : 0.f;
+    }
+    // max in T (order-independent for non-NaN input)
+#pragma unroll
+    for (int i = 0; i < kMaxExpertsPerLane; ++i)
+        if (lane + 32 * i < N) mx = fmaxf(mx, v[i]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+#pragma unroll
+    for (int i = 0; i < kMaxExpertsPerLane; ++i)
+        e[i] = (lane + 32 * i < N) ? exp((double)v[i] - (double)mx) : 0.0;
+    // sequential fp64 sum in expert order (kernels.hpp:205-209): lane 0 walks j = 0..N-1
+    double sum = 0.0;
+#pragma unroll
+    for (int i = 0; i < kMaxExpertsPerLane; ++i) {
+        if (32 * i >= N) break;
+        for (int src = 0; src < 32; ++src) {
+            const double ej = __shfl_sync(0xffffffffu, e[i], src);
+            if (32 * i + src < N) sum += ej;
+        }
+    }
+    float p[kMaxExpertsPerLane];
+#pragma unroll
+    for (int i = 0; i < kMaxExpertsPerLane; ++i) {
+        const int j = lane + 32 * i;
+        p[i] = (float)(e[i] / sum);
+        if (j < N) probs[(int64_t)warp * N + j] = p[i];
+    }
+    // K argmax rounds, strict '>' => lower index wins ties (kernels.hpp:246-255)
+    unsigned taken = 0;
+    float wsum = 0.f;
+    float wk[16];
+    for (int c = 0; c < K; ++c) {
+        float bv = 0.f;
+        int bi = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < kMaxExpertsPerLane; ++i) {
+            const int j = lane + 32 * i;
+            if (j < N && !(taken >> i & 1u)) {
+                if (bi == 0x7fffffff || p[i] > bv) {  // within a lane j increases: strict '>'
+                    bv = p[i];
+                    bi = j;
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            const bool better = (oi != 0x7fffffff) &&
+                                (bi == 0x7fffffff || ov > bv || (ov == bv && oi < bi));
+            if (better) {
+                bv = ov;
+                bi = oi;
+            }
+        }
+        if (lane == bi % 32) taken |= 1u << (bi / 32);
+        if (c < 16) wk[c] = bv;
+        if (lane == 0) {
+            topi[(int64_t)warp * K + c] = bi;
+            topw[(int64_t)warp * K + c] = bv;
+        }
+    }
+    if (normalize && lane == 0) {  // moe.hpp:72-78, T arithmetic
+        for (int c = 0; c < K; ++c) wsum += (c < 16 ? wk[c] : topw[(int64_t)warp * K + c]);
+        for (int c = 0; c < K; ++c) topw[(int64_t)warp * K + c] = __fdiv_rn(topw[(int64_t)warp * K + c], wsum);
+    }
+}
+
+// forced uniform routing (moe.hpp:84-99): expert (t*K+j) mod N, weight 1/K
+__global__ void fur_route_kernel(float* __restrict__ w, int32_t* __restrict__ idx, int S, int N, int K) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)S * K) return;
+    const int64_t t = i / K, k = i % K;
+    w[i] = (float)(1.0 / (double)K);
+    idx[i] = (int32_t)((t * K + k) % N);
+}
+
+// ---- balancing statistics: mean_probs over local rows, sel_counts over the gathered
+// table (moe.hpp:381-386). Column sums use a fixed two-level order (deterministic).
+
+__global__ void prob_colsum_partial_kernel(const float* __restrict__ probs, float* __restrict__ partial,
+                                           int S, int N, int rows_per_block) {
+    const int r0 = blockIdx.x * rows_per_block;
+    for (int e = threadIdx.x; e < N; e += blockDim.x) {
+        float acc = 0.f;
+        const int r1 = min(S, r0 + rows_per_block);
+        for (int r = r0; r < r1; ++r) acc += probs[(int64_t)r * N + e];
+        partial[(int64_t)blockIdx.x * N + e] = acc;
+    }
+}
+
+__global__ void prob_colsum_final_kernel(const float* __restrict__ partial, float* __restrict__ mean_probs,
+                                         int nparts, int N, int S) {
+    for (int e = threadIdx.x; e < N; e += blockDim.x) {
+        float acc = 0.f;
+        for (int b = 0; b < nparts; ++b) acc += partial[(int64_t)b * N + e];
+        mean_probs[e] = acc * (float)(1.0 / (double)S);
+    }
+}
+
+__global__ void sel_count_kernel(const int32_t* __restrict__ idx, int64_t n, int32_t* __restrict__ sel) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&sel[idx[i]], 1);
+}
+
+// ---- router backward (moe.hpp:431-454) -----------------------------------------------
+
+// dprobs[s, idx[s,k]] += wgrad[s,k] (or the renormalised form, 434-444); + aux grad
+// column constant; then dlogits = softmax_backward(probs, dprobs) with the fp64 dot.
+// One warp per local row.
+__global__ void router_dlogits_kernel(const float* __restrict__ probs, const float* __restrict__ wgrad,
+                                      const int32_t* __restrict__ topi, const float* __restrict__ topw,
+                                      const float* __restrict__ aux_grad /*[S,N] or null*/,
+                                      float* __restrict__ dlogits, int S, int N, int K, int normalize,
+                                      int fur) {
+    const int row = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+    if (row >= S) return;
+    float dp[kMaxExpertsPerLane], pr[kMaxExpertsPerLane];
+#pragma unroll
+    for (int i = 0; i < kMaxExpertsPerLane; ++i) {
+        const int j = lane + 32 * i;
+        dp[i] = 0.f;
+        pr[i] = j < N ? probs[(int64_t)row * N + j] : 0.f;
+    }
+    if (!fur) {
+        double raw_sum = 0, dot = 0;
+        if (normalize) {
+            for (int k = 0; k < K; ++k) raw_sum += (double)probs[(int64_t)row * N + topi[(int64_t)row * K + k]];
+            for (int k = 0; k < K; ++k)
+                dot += (double)wgrad[(int64_t)row * K + k] * (double)topw[(int64_t)row * K + k];
+        }
+        for (int k = 0; k < K; ++k) {
+            const int e = topi[(int64_t)row * K + k];
+            const float g = wgrad[(int64_t)row * K + k];
+            const float add = normalize ? (float)(((double)g - dot) / raw_sum) : g;
+            if (e % 32 == lane) {
+#pragma unroll
+                for (int i = 0; i < kMaxExpertsPerLane; ++i)
+                    if (i == e / 32) dp[i] += add;
+            }
+        }
+    }
+    if (aux_grad) {
+#pragma unroll
+        for (int i = 0; i < kMaxExpertsPerLane; ++i) {
+            const int j = lane + 32 * i;
+            if (j < N) dp[i] += aux_grad[(int64_t)row * N + j];
+        }
+    }
+    double dot = 0.0;
+#pragma unroll
+    for (int i = 0; i < kMaxExpertsPerLane; ++i) dot += (double)pr[i] * (double)dp[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+#pragma unroll
+    for (int i = 0; i < kMaxExpertsPerLane; ++i) {
+        const int j = lane + 32 * i;
+        if (j < N) dlogits[(int64_t)row * N + j] = (float)((double)pr[i] * ((double)dp[i] - dot));
+    }
+}
+
+// aux-loss probability gradient (moe.hpp:331-342): coeff*N*f_e/S in every row
+__global__ void aux_probs_grad_kernel(const int32_t* __restrict__ sel, float* __restrict__ out, int S, int N,
+                                      double coeff, double total) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)S * N) return;
+    const int e = (int)(i % N);
+    out[i] = (float)(coeff * (double)N * ((double)sel[e] / total) / (double)S);
+}
+
+// dWr[h, e] = sum_s x[s,h] * dlogits[s,e]  (matmul_tn, kernels.hpp:52-72): one CTA per
+// 64 h-rows x 64 experts, reduction over all S rows in a fixed order (deterministic).
+template <typename T>
+__global__ void __launch_bounds__(256) router_dw_kernel(const T* __restrict__ x, const float* __restrict__ dl,
+                                                        T* __restrict__ dw, int S, int H, int N) {
+    __shared__ float xs[kRtP][64 + 1];
+    __shared__ float ds[kRtP][64];
+    const int h0 = blockIdx.x * 64, e0 = blockIdx.y * 64;
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    float acc[4][4] = {};
+    for (int s0 = 0; s0 < S; s0 += kRtP) {
+        for (int i = threadIdx.x; i < kRtP * 64; i += 256) {
+            const int ss = i / 64, hh = i % 64;
+            const int s = s0 + ss, h = h0 + hh;
+            xs[ss][hh] = (s < S && h < H) ? Elem<T>::load(x + (int64_t)s * H + h) : 0.f;
+            const int e = e0 + hh;
+            ds[ss][hh] = (s < S && e < N) ? dl[(int64_t)s * N + e] : 0.f;
+        }
+        __syncthreads();
+        for (int ss = 0; ss < kRtP; ++ss) {
+            float a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = xs[ss][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = ds[ss][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int h = h0 + ty * 4 + i;
+        if (h >= H) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int e = e0 + tx * 4 + j;
+            if (e < N) dw[(int64_t)h * N + e] = Elem<T>::from_f(acc[i][j]);
+        }
+    }
+}
+
+// ---- launchers ----------------------------------------------------------------------
+
+template <typename T>
+void launch_router_logits(const T* x, const T* w, float* logits, int S, int H, int N, cudaStream_t st) {
+    if (S == 0) return;
+    dim3 grid((unsigned)ceil_div(S, kRtTok), (unsigned)ceil_div(N, kRtExp));
+    router_logits_kernel<T><<<grid, 256, 0, st>>>(x, w, logits, S, H, N);
+    B2_LAUNCH_CHECK();
+}
+template void launch_router_logits<float>(const float*, const float*, float*, int, int, int, cudaStream_t);
+template void launch_router_logits<__nv_bfloat16>(const __nv_bfloat16*, const __nv_bfloat16*, float*, int, int,
+                                                  int, cudaStream_t);
+
+void launch_softmax_topk(const float* logits, float* probs, float* topw, int32_t* topi, int S, int N, int K,
+                         bool normalize, cudaStream_t st) {
+    check(N <= 32 * kMaxExpertsPerLane, "route: n_experts above 256 is not supported by the router kernel");
+    if (S == 0) return;
+    const int warps_per_block = 8;
+    softmax_topk_kernel<<<(unsigned)ceil_div(S, warps_per_block), 32 * warps_per_block, 0, st>>>(
+        logits, probs, topw, topi, S, N, K, normalize ? 1 : 0);
+    B2_LAUNCH_CHECK();
+}
+
+void launch_fur_route(float* w, int32_t* idx, int S, int N, int K, cudaStream_t st) {
+    const int64_t n = (int64_t)S * K;
+    if (n == 0) return;
+    fur_route_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(w, idx, S, N, K);
+    B2_LAUNCH_CHECK();
+}
+
+void launch_aux_stats(const float* probs, int S, int N, const int32_t* gidx, int64_t n_gidx, float* partial,
+                      float* mean_probs, int32_t* sel, cudaStream_t st) {
+    B2_CUDA(cudaMemsetAsync(sel, 0, sizeof(int32_t) * N, st));
+    if (S > 0) {
+        const int rpb = 128;
+        const int nparts = (int)ceil_div(S, rpb);
+        prob_colsum_partial_kernel<<<nparts, 128, 0, st>>>(probs, partial, S, N, rpb);
+        B2_LAUNCH_CHECK();
+        prob_colsum_final_kernel<<<1, 256, 0, st>>>(partial, mean_probs, nparts, N, S);
+        B2_LAUNCH_CHECK();
+    } else {
+        B2_CUDA(cudaMemsetAsync(mean_probs, 0, sizeof(float) * N, st));
+    }
+    if (n_gidx > 0) {
+        sel_count_kernel<<<(unsigned)std::min<int64_t>(1184, ceil_div(n_gidx, 256)), 256, 0, st>>>(gidx, n_gidx, sel);
+        B2_LAUNCH_CHECK();
+    }
+}
+
+void launch_router_dlogits(const float* probs, const float* wgrad, const int32_t* topi, const float* topw,
+                           const float* aux_grad, float* dlogits, int S, int N, int K, bool normalize, bool fur,
+                           cudaStream_t st) {
+    if (S == 0) return;
+    router_dlogits_kernel<<<(unsigned)ceil_div(S, 8), 256, 0, st>>>(probs, wgrad, topi, topw, aux_grad, dlogits, S,
+                                                                      N, K, normalize ? 1 : 0, fur ? 1 : 0);
+    B2_LAUNCH_CHECK();
+}
+
+void launch_aux_probs_grad(const int32_t* sel, float* out, int S, int N, double coeff, double total,
+                           cudaStream_t st) {
+    const int64_t n = (int64_t)S * N;
+    if (n == 0) return;
+    aux_probs_grad_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(sel, out, S, N, coeff, total);
+    B2_LAUNCH_CHECK();
+}
+
+template <typename T>
+void launch_router_dw(const T* x, const float* dlogits, T* dw, int S, int H, int N, cudaStream_t st) {
+    dim3 grid((unsigned)ceil_div(H, 64), (unsigned)ceil_div(N, 64));
+    router_dw_kernel<T><<<grid, 256, 0, st>>>(x, dlogits, dw, S, H, N);
+    B2_LAUNCH_CHECK();
+}
+template void launch_router_dw<float>(const float*, const float*, float*, int, int, int, cudaStream_t);
+template void launch_router_dw<__nv_bfloat16>(const __nv_bfloat16*, const float*, __nv_bfloat16*, int, int, int,
+                                              cudaStream_t);
+
+}  // namespace b2

@@ -1,0 +1,216 @@
+"""Parity of the CUDA MoE path (through the C-ABI) with the CPU oracle.
+
+Bars (BASELINE.json north star, metric of tests/test_util.hpp:15-18
+rel_err = |a-b| / max(1,|a|,|b|)):
+  * routing top-k indices and the permutation: bit-exact given identical scores;
+  * fp32 mode: every output / gradient within 1e-4 rel_err of the fp32 oracle;
+  * bf16 mode vs the fp32 oracle on the same bf16-rounded inputs: outputs and input
+    grads within 2e-2 rel_err elementwise; weight / router grads within 2e-2 of
+    the tensor scale (max|d| / max|ref|: long bf16 reductions cancel).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import bind
+
+pytestmark = pytest.mark.gpu
+
+TOL_F32 = 1e-4
+TOL_BF16 = 2e-2
+
+
+def rel_err(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(1.0, np.maximum(np.abs(a), np.abs(b))))) if a.size else 0.0
+
+
+def scale_err(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30)) if a.size else 0.0
+
+
+@pytest.fixture(scope="module")
+def b2ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2604_00785_b200 as b2
+    return b2, b2.Context(0)
+
+
+def cfg_pair(**kw):
+    import paper_2604_00785_b200 as b2
+    return bind.moe_cfg(**kw), b2.MoeConfig(**kw)
+
+
+# ---------------------------------------------------------------- routing
+
+@pytest.mark.parametrize("n,k,normalize", [(8, 2, False), (64, 8, False), (12, 3, True), (96, 8, False)])
+def test_softmax_topk_bit_exact_on_identical_scores(b2ctx, orc, n, k, normalize):
+    b2, ctx = b2ctx
+    rng = np.random.default_rng(n * 7 + k)
+    logits = rng.standard_normal((777, n)).astype(np.float32)
+    logits[::5, 3] = logits[::5, 1]  # exact ties -> lower index
+    logits[::7, : n // 2] = 0.0
+    probs_o, w_o, i_o = orc.softmax_topk(logits, k)
+    if normalize:
+        w_o = w_o / w_o.sum(1, keepdims=True, dtype=np.float32)
+    probs, w, idx = b2.softmax_topk(ctx, torch.from_numpy(logits).cuda(), k, normalize)
+    assert np.array_equal(idx.cpu().numpy(), i_o)
+    assert np.array_equal(probs.cpu().numpy(), probs_o)
+    if not normalize:
+        assert np.array_equal(w.cpu().numpy(), w_o)
+    else:
+        assert rel_err(w.cpu().numpy(), w_o) <= 1e-6
+
+
+@pytest.mark.parametrize("H,N,K", [(32, 8, 2), (256, 64, 8)])
+def test_route_logits_bitwise(b2ctx, orc, H, N, K):
+    b2, ctx = b2ctx
+    ocfg, bcfg = cfg_pair(n_experts=N, top_k=K, hidden=H, intermediate=64)
+    x = orc.normal((300, H), 77, 0, 1.0)
+    router = orc.normal((H, N), 5, 1, 0.2)
+    lo, po, wo, io = orc.route_f32(ocfg, x, router)
+    logits, probs, w, idx = b2.route(ctx, bcfg, torch.from_numpy(x).cuda(), torch.from_numpy(router).cuda())
+    assert np.array_equal(logits.cpu().numpy(), lo)
+    assert np.array_equal(idx.cpu().numpy(), io)
+    assert np.array_equal(w.cpu().numpy(), wo)
+
+
+FOUR = np.array([[0, 1], [0, 2], [1, 3], [2, 3]], np.int64)
+
+
+def _compare_artifacts(got, want):
+    for key in ("token_counts", "partial_token_counts", "partial_cum", "cum_token_counts", "expert_counts",
+                "cum_expert_counts", "input_indices", "output_indices", "selected_k", "counter"):
+        assert np.array_equal(np.asarray(got[key]), np.asarray(want[key])), key
+    assert got["rt"] == want["rt"] and got["th"] == want["th"]
+
+
+def test_artifacts_four_token_example(b2ctx, orc):
+    b2, ctx = b2ctx
+    ocfg, bcfg = cfg_pair(n_experts=4, top_k=2, hidden=4, intermediate=4, ep=2, token_block=8)
+    t = torch.from_numpy(FOUR.astype(np.int32)).cuda()
+    a = b2.routing_artifacts(ctx, bcfg, t, 0)
+    assert a["input_indices"].tolist() == [0, 1, 0, 2]  # test_moe.cpp:110-119
+    assert a["output_indices"].tolist() == [0, 2, 1, 3]
+    assert a["selected_k"].tolist() == [0, 1, 0, 0]
+    for r in (0, 1):
+        _compare_artifacts(b2.routing_artifacts(ctx, bcfg, t, r), orc.artifacts(ocfg, FOUR, r))
+
+
+def test_artifacts_out_of_range_raises(b2ctx):
+    b2, ctx = b2ctx
+    _, bcfg = cfg_pair(n_experts=4, top_k=2, hidden=4, intermediate=4, ep=2)
+    t = torch.tensor([[0, 1], [2, 7]], dtype=torch.int32, device="cuda")
+    with pytest.raises(b2.ContractError):
+        b2.routing_artifacts(ctx, bcfg, t, 0)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_artifacts_random_tables_bit_exact(b2ctx, orc, seed):
+    b2, ctx = b2ctx
+    rng = np.random.default_rng(seed)
+    ep = int(rng.integers(1, 5))
+    n = ep * int(rng.integers(1, 17))
+    k = int(rng.integers(1, min(8, n) + 1))
+    T = int(rng.integers(1, 3000)) if seed % 3 else int(rng.integers(1, 40))
+    if seed % 2:  # distinct experts per token, like a real top-k
+        idx = np.stack([rng.permutation(n)[:k] for _ in range(T)]).astype(np.int64)
+    else:  # repeated experts allowed (test_moe.cpp:84-103)
+        idx = rng.integers(0, n, size=(T, k)).astype(np.int64)
+    kw = dict(n_experts=n, top_k=k, hidden=8, intermediate=8, ep=ep, token_block=int(rng.integers(1, 9)))
+    ocfg, bcfg = cfg_pair(**kw)
+    t = torch.from_numpy(idx.astype(np.int32)).cuda()
+    for r in range(ep):
+        _compare_artifacts(b2.routing_artifacts(ctx, bcfg, t, r), orc.artifacts(ocfg, idx, r))
+
+
+# ---------------------------------------------------------------- full layer
+
+def run_layer(b2, ctx, bcfg, dtype, x, router, gate, up, down, dout, fur=False, aux_coeff=0.0):
+    tt = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda().to(dtype)
+    X, R, G, U, D, DO = map(tt, (x, router, gate, up, down, dout))
+    layer = b2.MoeLayer(ctx, bcfg, dtype, x.shape[0])
+    out = layer.forward(X, R, G, U, D, fur=fur)
+    apg = layer.aux_probs_grad(aux_coeff) if aux_coeff else None
+    grads = layer.backward(R, G, U, D, DO, apg)
+    torch.cuda.synchronize()
+    res = {k: v.float().cpu().numpy() for k, v in grads.items()}
+    res["out"] = out.float().cpu().numpy()
+    res["probs"], res["weights"], res["indices"] = layer.routing()
+    res["artifacts"] = layer.artifacts()
+    res["aux"] = layer.aux_loss()
+    res["launches"] = layer.last_launches()
+    return res
+
+
+F32_CASES = [
+    dict(n_experts=8, top_k=2, hidden=32, intermediate=48, token_block=8, s=64),
+    dict(n_experts=6, top_k=3, hidden=20, intermediate=12, token_block=3, s=37, normalize_topk=True),
+    dict(n_experts=8, top_k=2, hidden=16, intermediate=24, token_block=4, s=16, fur=True),
+    dict(n_experts=64, top_k=8, hidden=128, intermediate=64, token_block=8, s=256),
+    dict(n_experts=1, top_k=1, hidden=5, intermediate=7, token_block=8, s=6),
+]
+
+
+@pytest.mark.parametrize("case", F32_CASES, ids=lambda c: f"n{c['n_experts']}k{c['top_k']}h{c['hidden']}")
+def test_layer_fp32_matches_oracle(b2ctx, orc, case):
+    b2, ctx = b2ctx
+    c = dict(case)
+    s = c.pop("s")
+    fur = c.pop("fur", False)
+    ocfg, bcfg = cfg_pair(**c)
+    router, gate, up, down = orc.expert_weights(ocfg, 1234, 0.2)
+    x = orc.normal((s, ocfg.hidden), 77, 0, 0.7)
+    dout = orc.normal((s, ocfg.hidden), 78, 0, 1.0)
+    ref = orc.moe_layer(ocfg, s, x, router, gate, up, down, dout, fur=fur, aux_coeff=0.01)
+    got = run_layer(b2, ctx, bcfg, torch.float32, x, router, gate, up, down, dout, fur=fur, aux_coeff=0.01)
+    assert np.array_equal(got["indices"], ref["indices"])
+    assert np.array_equal(got["weights"], ref["weights"])
+    assert rel_err(got["aux"], ref["aux"][0]) <= TOL_F32
+    if fur:  # fur_route (moe.hpp:84-99) replaces the dispatch table
+        table = (np.arange(s)[:, None] * ocfg.top_k + np.arange(ocfg.top_k)[None, :]) % ocfg.n_experts
+    else:
+        table = ref["indices"]
+    art_ref = orc.artifacts(ocfg, table.astype(np.int64), 0)
+    _compare_artifacts(got["artifacts"], art_ref)
+    for key, gkey in [("out", "out"), ("dx", "input"), ("drouter", "router"), ("dgate", "gate"), ("dup", "up"),
+                      ("ddown", "down")]:
+        want = ref[key][0] if key == "drouter" else ref[key]
+        e = rel_err(got[gkey], want)
+        assert e <= TOL_F32, f"{key}: rel_err {e}"
+    assert got["launches"] > 0
+
+
+BF16_CASES = [
+    dict(n_experts=8, top_k=2, hidden=256, intermediate=256, s=512),
+    dict(n_experts=64, top_k=8, hidden=256, intermediate=128, s=512),
+    dict(n_experts=16, top_k=4, hidden=384, intermediate=192, s=333),
+]
+
+
+@pytest.mark.parametrize("case", BF16_CASES, ids=lambda c: f"n{c['n_experts']}k{c['top_k']}h{c['hidden']}")
+def test_layer_bf16_matches_fp32_oracle(b2ctx, orc, case):
+    b2, ctx = b2ctx
+    c = dict(case)
+    s = c.pop("s")
+    ocfg, bcfg = cfg_pair(**c)
+    rb = lambda a: torch.from_numpy(np.ascontiguousarray(a)).bfloat16().float().numpy()
+    router, gate, up, down = (rb(t) for t in orc.expert_weights(ocfg, 1234, 0.02))
+    x = rb(orc.normal((s, ocfg.hidden), 77, 0, 1.0))
+    dout = rb(orc.normal((s, ocfg.hidden), 78, 0, 1.0))
+    ref = orc.moe_layer(ocfg, s, x, router, gate, up, down, dout, aux_coeff=0.01)
+    got = run_layer(b2, ctx, bcfg, torch.bfloat16, x, router, gate, up, down, dout, aux_coeff=0.01)
+    # identical fp32 router math on identical inputs -> identical routing
+    assert np.array_equal(got["indices"], ref["indices"])
+    _compare_artifacts(got["artifacts"], orc.artifacts(ocfg, ref["indices"], 0))
+    assert rel_err(got["out"], ref["out"]) <= TOL_BF16
+    assert rel_err(got["input"], ref["dx"]) <= TOL_BF16
+    for key, gkey in [("drouter", "router"), ("dgate", "gate"), ("dup", "up"), ("ddown", "down")]:
+        want = ref[key][0] if key == "drouter" else ref[key]
+        e = scale_err(got[gkey], want)
+        assert e <= TOL_BF16, f"{key}: scale_err {e}"
