@@ -80,7 +80,9 @@ int b2_device_ok(void);
 /* ---- rank context: replaces optimus::RankCtx (comm.hpp:205-231) --------------------
  * rank layout rank = ((pp*DP + dp)*EP + ep)*TP + tp (comm.hpp:45-59). For world > 1,
  * nccl_id is the 128-byte ncclUniqueId from b2_nccl_unique_id() on rank 0, shared
- * by the caller; the DP, EP and DPxEP communicators are split from it. */
+ * by the caller; the DP, EP and DPxEP communicators are split from it. `stream` is
+ * the cudaStream_t every call of this context is ordered on (NULL: the legacy
+ * default stream). */
 int b2_nccl_unique_id(uint8_t out[128]);
 int b2_ctx_create(int device, void* stream, int rank, int dp, int ep, int tp, int pp, const uint8_t* nccl_id,
                   b2_ctx** out);

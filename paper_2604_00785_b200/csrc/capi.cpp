@@ -114,12 +114,9 @@ int b2_ctx_create(int device, void* stream, int rank, int dp, int ep, int tp, in
         Context& x = c->c;
         x.device = device;
         B2_CUDA(cudaSetDevice(device));
-        if (stream) {
-            x.stream = (cudaStream_t)stream;
-        } else {
-            B2_CUDA(cudaStreamCreateWithFlags(&x.stream, cudaStreamNonBlocking));
-            c->own_stream = true;
-        }
+        // the caller's stream; NULL is the legacy default stream, so work stays ordered
+        // with a framework (e.g. torch) that launches on it
+        x.stream = (cudaStream_t)stream;
         B2_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         B2_CUDA(cudaDeviceGetAttribute(&x.num_sms, cudaDevAttrMultiProcessorCount, device));
         x.rank = rank;
