@@ -161,6 +161,13 @@ int b2_adamw_update(b2_ctx* ctx, float* master, float* exp_avg, float* exp_avg_s
 /* lr_at_step (optim.cpp:17-24) and shard_slice (optim.cpp:43-50); host only */
 double b2_lr_at_step(int64_t step, const b2_adamw_cfg* cfg);
 int b2_shard_slice(int64_t numel, int group_size, int position, int64_t* begin, int64_t* end);
+/* per-stage CUDA-event timing of the layer (route, index, gather, the six GEMMs,
+ * combine, output-reduction backward, router backward): enable, run, then read
+ * B2_MOE_NUM_STAGES floats in ms (synchronises). */
+#define B2_MOE_NUM_STAGES 12
+int b2_moe_set_profiling(b2_moe* m, int on);
+int b2_moe_stage_times(b2_moe* m, float* ms_host);
+const char* b2_moe_stage_name(int stage);
 /* number of this library's kernels launched by the last call on the handle */
 int b2_moe_last_launches(b2_moe* m);
 int b2_opt_last_launches(b2_opt* o);

@@ -101,6 +101,9 @@ SIGNATURES = {
     "b2_adamw_update": (C.c_int, [P, P, P, P, P, C.c_int, I64, C.c_double, I64, P, P, C.c_int, C.c_int]),
     "b2_lr_at_step": (C.c_double, [I64, P]),
     "b2_shard_slice": (C.c_int, [I64, C.c_int, C.c_int, P, P]),
+    "b2_moe_set_profiling": (C.c_int, [P, C.c_int]),
+    "b2_moe_stage_times": (C.c_int, [P, P]),
+    "b2_moe_stage_name": (C.c_char_p, [C.c_int]),
     "b2_moe_last_launches": (C.c_int, [P]),
     "b2_opt_last_launches": (C.c_int, [P]),
 }
@@ -308,6 +311,24 @@ class MoeLayer:
 
     def last_launches(self) -> int:
         return lib().b2_moe_last_launches(self.h)
+
+    NUM_STAGES = 12
+
+    def set_profiling(self, on: bool = True):
+        _check(lib().b2_moe_set_profiling(self.h, int(on)))
+
+    def stage_times(self) -> dict:
+        import numpy as np
+        ms = np.zeros(self.NUM_STAGES, np.float32)
+        _check(lib().b2_moe_stage_times(self.h, ms.ctypes.data_as(P)))
+        return {lib().b2_moe_stage_name(i).decode(): float(ms[i]) for i in range(self.NUM_STAGES)}
+
+    def fwd_bwd_host(self, x_host, dout_host, router, gate, up, down, out_host, dx_host, grads, aux_coeff=0.0):
+        """forward+backward with pinned HOST x/dout in and out/dx back (b2_moe_fwd_bwd_host)."""
+        _check(lib().b2_moe_fwd_bwd_host(self.h, _ptr(x_host), _ptr(dout_host), _ptr(router), _ptr(gate), _ptr(up),
+                                         _ptr(down), aux_coeff, _ptr(out_host), _ptr(dx_host), _ptr(grads["router"]),
+                                         _ptr(grads["gate"]), _ptr(grads["up"]), _ptr(grads["down"]),
+                                         x_host.shape[0]))
 
     def close(self):
         if self.h:

@@ -116,7 +116,51 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     B2_CUDA(cudaMemsetAsync(pad_start_, 0, 4 * (nr + 1), ctx_.stream));
 }
 
-MoeLayer::~MoeLayer() = default;
+MoeLayer::~MoeLayer() {
+    for (auto& st : prof_ev_)
+        for (cudaEvent_t e : st) cudaEventDestroy(e);
+}
+
+const char* MoeLayer::stage_name(int s) {
+    static const char* names[kNumStages] = {"route",           "index",          "gather",       "gemm_fwd_gate_up",
+                                            "gemm_fwd_down",   "combine",        "out_red_bwd",  "gemm_bwd_dgrad",
+                                            "gemm_wgrad_down", "gemm_wgrad_gate_up", "gemm_bwd_dx", "router_bwd"};
+    return (s >= 0 && s < kNumStages) ? names[s] : "?";
+}
+
+// profiling: every forward+backward while enabled records one event pair per stage
+// (up to kMaxProfSteps); stage_times() returns the mean over the recorded steps.
+constexpr int kMaxProfSteps = 256;
+
+void MoeLayer::set_profiling(bool on) {
+    profiling_ = on;
+    prof_step_ = -1;
+}
+
+void MoeLayer::mark(int stage, bool end) {
+    if (!profiling_ || prof_step_ < 0 || prof_step_ >= kMaxProfSteps) return;
+    while ((int)prof_ev_.size() <= prof_step_) {
+        std::vector<cudaEvent_t> v(2 * kNumStages);
+        for (cudaEvent_t& e : v) B2_CUDA(cudaEventCreate(&e));
+        prof_ev_.push_back(std::move(v));
+    }
+    B2_CUDA(cudaEventRecord(prof_ev_[(size_t)prof_step_][(size_t)(2 * stage + (end ? 1 : 0))], ctx_.stream));
+}
+
+void MoeLayer::stage_times(float* ms) {
+    check(profiling_ && prof_step_ >= 0, "stage_times: no profiled step recorded");
+    B2_CUDA(cudaStreamSynchronize(ctx_.stream));
+    const int n = std::min(prof_step_ + 1, kMaxProfSteps);
+    for (int s = 0; s < kNumStages; ++s) {
+        double acc = 0;
+        for (int i = 0; i < n; ++i) {
+            float t = 0.f;
+            B2_CUDA(cudaEventElapsedTime(&t, prof_ev_[(size_t)i][(size_t)(2 * s)], prof_ev_[(size_t)i][(size_t)(2 * s + 1)]));
+            acc += t;
+        }
+        ms[s] = (float)(acc / n);
+    }
+}
 
 void MoeLayer::forward(const void* x, const void* router, const void* gate, const void* up, const void* down,
                        int64_t s, bool fur, void* out) {
@@ -129,6 +173,7 @@ void MoeLayer::forward(const void* x, const void* router, const void* gate, cons
     fur_ = fur;
     x_ = x;
     launches_ = 0;
+    if (profiling_) ++prof_step_;
     if (dtype_ == F32)
         forward_t<float>((const float*)x, (const float*)router, (const float*)gate, (const float*)up,
                          (const float*)down, fur, (float*)out);
@@ -144,6 +189,7 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     const int S = (int)s_, Tt = (int)t_, N = (int)cfg_.n_experts, K = (int)cfg_.top_k, H = (int)cfg_.hidden,
               I = (int)cfg_.intermediate, nr = (int)cfg_.experts_per_rank();
     // stage 1: route locally (moe.hpp:357-364)
+    mark(kRoute, false);
     launch_router_logits<T>(x, router, logits_, S, H, N, st);
     launch_softmax_topk(logits_, probs_, topw_, topi_, S, N, K, cfg_.normalize_topk, st);
     launches_ += 2;
@@ -159,6 +205,8 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     // balancing statistics (381-386)
     launch_aux_stats(probs_, S, N, gi_, (int64_t)Tt * K, colsum_, mean_probs_, sel_, st);
     launches_ += 3;
+    mark(kRoute, true);
+    mark(kIndex, false);
     // stages 2+3 (370-371)
     RoutingIndexArgs ra{};
     ra.gidx = gi_;
@@ -186,10 +234,13 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     ra.err = err_;
     launch_routing_index(ra, st);
     launches_ += 4;
+    mark(kIndex, true);
     const int32_t* p_total = pad_start_ + nr;
     // stage 4: expert MLP over the padded expert-sorted rows (225-244)
+    mark(kGather, false);
     launch_gather_rows<T>(x, prow_src_, p_total, (T*)mlp_in_, H, pmax_, st);
     launches_ += 1;
+    mark(kGather, true);
     if (dtype_ == BF16) {
         Sm100GemmArgs ga{};
         ga.H = H;
@@ -205,12 +256,16 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
         ga.out0 = g_;
         ga.out1 = u_;
         ga.out2 = h_;
+        mark(kGemmGateUp, false);
         launch_sm100_gemm(ga, st);
+        mark(kGemmGateUp, true);
         ga.kind = GemmKind::FwdDown;
         ga.h = h_;
         ga.wd = down;
         ga.out0 = y_;
+        mark(kGemmDown, false);
         launch_sm100_gemm(ga, st);
+        mark(kGemmDown, true);
         launches_ += 2;
     } else {
         SimtGemmArgs a{};
@@ -232,11 +287,14 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
         a.K = H;
         a.B = gate;
         a.D = g_;
+        mark(kGemmGateUp, false);
         launch_simt_grouped_gemm<T>(a, pmax_, st);
         a.B = up;
         a.D = u_;
         launch_simt_grouped_gemm<T>(a, pmax_, st);
         launch_swiglu_fwd<T>((const T*)g_, (const T*)u_, (T*)h_, p_total, I, pmax_, st);
+        mark(kGemmGateUp, true);
+        mark(kGemmDown, false);
         // Y = H . Wd
         a.A = h_;
         a.lda_m = I;
@@ -248,11 +306,14 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
         a.B = down;
         a.D = y_;
         launch_simt_grouped_gemm<T>(a, pmax_, st);
+        mark(kGemmDown, true);
         launches_ += 4;
     }
     // stage 5: weighted combine (377); EP = 1 so the reducescatter (378) is the identity
+    mark(kCombine, false);
     launch_combine<T>((const T*)y_, slot_prow_, selected_k_, cec_, gw_, out, Tt, H, K, st);
     launches_ += 1;
+    mark(kCombine, true);
 }
 
 void MoeLayer::backward(const void* router, const void* gate, const void* up, const void* down, const void* dout,
@@ -280,9 +341,11 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
     const int32_t* p_total = pad_start_ + nr;
     const float inv_ep = (float)(1.0 / (double)cfg_.ep);
     // output_reduction_backward (402-403); EP = 1 so dout is already the allgather (400)
+    mark(kOutRedBwd, false);
     launch_out_reduction_bwd<T>(dout, (const T*)y_, slot_prow_, selected_k_, cec_, gw_, (T*)dy_, wgrad_, Tt, H, K, st);
     launch_zero_pad_rows<T>((T*)dy_, prow_src_, p_total, H, pmax_, st);
     launches_ += 2;
+    mark(kOutRedBwd, true);
     if (dtype_ == BF16) {
         Sm100GemmArgs ga{};
         ga.H = H;
@@ -303,17 +366,25 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         ga.scale = inv_ep;
         ga.kind = GemmKind::BwdDownDgrad;  // 406 + silu_glu_backward 409
         ga.out0 = dgu_;
+        mark(kGemmDgrad, false);
         launch_sm100_gemm(ga, st);
+        mark(kGemmDgrad, true);
         ga.kind = GemmKind::WgradDown;  // 407
         ga.out0 = ddown;
+        mark(kGemmWgradDown, false);
         launch_sm100_gemm(ga, st);
+        mark(kGemmWgradDown, true);
         ga.kind = GemmKind::WgradGateUp;  // 410-413
         ga.out0 = dgate;
         ga.out1 = dup;
+        mark(kGemmWgradGateUp, false);
         launch_sm100_gemm(ga, st);
+        mark(kGemmWgradGateUp, true);
         ga.kind = GemmKind::BwdDx;  // 414-415
         ga.out0 = dxp_;
+        mark(kGemmDx, false);
         launch_sm100_gemm(ga, st);
+        mark(kGemmDx, true);
         launches_ += 4;
     } else {
         SimtGemmArgs a{};
@@ -335,6 +406,7 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         a.ldd_n = 1;
         a.N = I;
         a.K = H;
+        mark(kGemmDgrad, false);
         launch_simt_grouped_gemm<T>(a, pmax_, st);
         launch_swiglu_bwd<T>((const T*)g_, (const T*)u_, (const T*)dh_, (T*)dgu_, p_total, I, pmax_, st);
         // dWd[e] = H^T . dY over the rows of e, scaled 1/EP (407, 458-461)
@@ -355,7 +427,11 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         w.d_gs = (int64_t)I * H;
         w.M_lim = I;
         w.N = H;
+        mark(kGemmDgrad, true);
+        mark(kGemmWgradDown, false);
         launch_simt_grouped_gemm<T>(w, I, st);
+        mark(kGemmWgradDown, true);
+        mark(kGemmWgradGateUp, false);
         // dWg[e] = X^T . dG, dWu[e] = X^T . dU (410-413)
         w.A = mlp_in_;
         w.lda_k = H;
@@ -370,6 +446,8 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         w.B = (const T*)dgu_ + I;
         w.D = dup;
         launch_simt_grouped_gemm<T>(w, H, st);
+        mark(kGemmWgradGateUp, true);
+        mark(kGemmDx, false);
         // dX_perm = dG . Wg^T + dU . Wu^T (414-415)
         a.A = dgu_;
         a.lda_m = 2 * I;
@@ -386,15 +464,18 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         a.B = up;
         a.accumulate = 1;
         launch_simt_grouped_gemm<T>(a, pmax_, st);
+        mark(kGemmDx, true);
         launches_ += 7;
     }
     // router path (431-454): EP = 1, so weights_grad_local == the full weights grad
+    mark(kRouterBwd, false);
     launch_router_dlogits(probs_, wgrad_, topi_, topw_, aux_probs_grad, dlogits_, S, N, K, cfg_.normalize_topk, fur_,
                           st);
     launch_router_dw<T>((const T*)x_, dlogits_, drouter, S, H, N, st);
     // scatter-add to tokens (418-423) + matmul_nt(dlogits, router) (454)
     launch_dx_finalize<T>((const T*)dxp_, true, slot_prow_, cec_, dlogits_, router, dx, S, H, N, st);
     launches_ += 3;
+    mark(kRouterBwd, true);
 }
 
 void MoeLayer::aux_probs_grad(double coeff, float* out) {

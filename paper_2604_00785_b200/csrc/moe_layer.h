@@ -89,6 +89,15 @@ class MoeLayer {
     // number of kernels of this library launched by the last forward / backward
     int last_launches() const { return launches_; }
 
+    // per-stage CUDA-event timing of the last forward+backward (profiling mode)
+    enum Stage {
+        kRoute, kIndex, kGather, kGemmGateUp, kGemmDown, kCombine, kOutRedBwd, kGemmDgrad, kGemmWgradDown,
+        kGemmWgradGateUp, kGemmDx, kRouterBwd, kNumStages
+    };
+    static const char* stage_name(int s);
+    void set_profiling(bool on);
+    void stage_times(float* ms);  // synchronises
+
   private:
     template <typename T>
     void forward_t(const T* x, const T* router, const T* gate, const T* up, const T* down, bool fur, T* out);
@@ -96,8 +105,13 @@ class MoeLayer {
     void backward_t(const T* router, const T* gate, const T* up, const T* down, const T* dout,
                     const float* aux_probs_grad, T* dx, T* drouter, T* dgate, T* dup, T* ddown);
 
+    void mark(int stage, bool end);
+
     Context& ctx_;
     MoeConfig cfg_;
+    bool profiling_ = false;
+    int prof_step_ = -1;  // index of the profiled forward+backward being recorded
+    std::vector<std::vector<cudaEvent_t>> prof_ev_;  // [step][stage*2 + end]
     int dtype_;
     int64_t smax_, tmax_, pmax_, thmax_;
     int64_t s_ = 0, t_ = 0, th_ = 0;
