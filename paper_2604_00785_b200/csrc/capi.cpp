@@ -330,14 +330,12 @@ int b2_routing_artifacts(b2_ctx* ctx, const b2_moe_cfg* cfg, const int32_t* indi
         a.N = (int)c.n_experts;
         a.n_start = ep_rank * (int)nr;
         a.nr = (int)nr;
-        a.tbs = (int)c.token_block;
-        a.th = (int)th;
         a.whist = ar.take<int32_t>(nch * nr);
         a.wbase = ar.take<int32_t>(nch * nr);
         a.expert_counts = ar.take<int32_t>(t_total);
         a.cum_expert_counts = ar.take<int32_t>(t_total + 1);
-        a.partial_counts = ar.take<int32_t>(nr * th);
-        a.partial_cum = ar.take<int32_t>(nr * th + 1);
+        int32_t* partial_counts = ar.take<int32_t>(nr * th);
+        int32_t* partial_cum_d = ar.take<int32_t>(nr * th + 1);
         a.token_counts = ar.take<int32_t>(nr);
         a.cum_token_counts = ar.take<int32_t>(nr + 1);
         a.pad_start = ar.take<int32_t>(nr + 1);
@@ -349,6 +347,8 @@ int b2_routing_artifacts(b2_ctx* ctx, const b2_moe_cfg* cfg, const int32_t* indi
         a.err = ar.take<int32_t>(1);
         B2_CUDA(cudaMemsetAsync(a.err, 0, 4, st));
         launch_routing_index(a, st);
+        launch_partial_counts(indices, (int)t_total, (int)K, a.n_start, (int)nr, (int)c.token_block, (int)th,
+                              partial_counts, partial_cum_d, st);
         int32_t err = 0;
         B2_CUDA(cudaMemcpyAsync(&err, a.err, 4, cudaMemcpyDeviceToHost, st));
         B2_CUDA(cudaStreamSynchronize(st));
@@ -366,8 +366,8 @@ int b2_routing_artifacts(b2_ctx* ctx, const b2_moe_cfg* cfg, const int32_t* indi
         h.pad_start = d2h(a.pad_start, nr + 1);
         h.padded_rows = h.pad_start[(size_t)nr];
         h.token_counts = d2h(a.token_counts, nr);
-        h.partial_token_counts = d2h(a.partial_counts, nr * th);
-        h.partial_cum = d2h(a.partial_cum, nr * th + 1);
+        h.partial_token_counts = d2h(partial_counts, nr * th);
+        h.partial_cum = d2h(partial_cum_d, nr * th + 1);
         h.expert_counts = d2h(a.expert_counts, t_total);
         h.cum_expert_counts = d2h(a.cum_expert_counts, t_total + 1);
         h.input_indices = d2h(a.input_indices, h.rt);

@@ -7,12 +7,13 @@
 // (kernels.hpp:262-295) fused into the epilogues and the 1/EP expert-grad scaling
 // (moe.hpp:458-461) folded into the weight-gradient store.
 //
-// One persistent kernel per GEMM kind; per CTA (one per SM, 256 threads):
+// One persistent kernel per GEMM kind; per CTA (one per SM, 384 threads):
 //   warp 0      TMA producer (one elected lane): A/B tiles -> 4-stage smem ring
 //   warp 1      MMA issuer (one lane): tcgen05.mma.cta_group::1.kind::f16,
 //               128 x 256 x 16 per instruction, fp32 accumulators in TMEM
 //   warp 2      TMEM allocator (512 columns = two 128x256 fp32 accumulators)
-//   warps 4-7   epilogue: tcgen05.ld -> registers -> fused math -> global
+//   warps 4-11  epilogue: tcgen05.ld -> registers -> fused math -> global; warp w
+//               reads TMEM lanes 32*(w%4).. and half of the tile's columns
 // Two accumulators let the epilogue of tile i overlap the MMAs of tile i+1.
 //
 // Rows of every expert group are padded to 128 in the permuted buffers, so an
@@ -43,7 +44,8 @@ constexpr int B_BYTES = BN * BK * 2;           // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 48 KB
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int TMEM_COLS = 512;
-constexpr int NUM_THREADS = 256;
+constexpr int NUM_EPI_WARPS = 8;  // two warps per TMEM lane quadrant, each half the columns
+constexpr int NUM_THREADS = 128 + 32 * NUM_EPI_WARPS;
 
 struct Params {
     CUtensorMap mapA;
@@ -269,19 +271,19 @@ __device__ __forceinline__ void load_stage(const Params& p, const TileInfo& ti, 
     }
 }
 
-__device__ __forceinline__ float silu_f(float x) { return x / (1.f + __expf(-x)); }
+__device__ __forceinline__ float silu_f(float x) { return __fdividef(x, 1.f + __expf(-x)); }
 
 // epilogue for one 32-column chunk of one row (thread = row)
 template <GemmKind KIND>
 __device__ __forceinline__ void epilogue_tile(const Params& p, const TileInfo& ti, uint32_t tacc, int row_in_tile,
-                                              bool zero) {
+                                              bool zero, int half) {
     uint32_t r[32], r2[32];
     float v[32];
     if constexpr (KIND == GemmKind::FwdGateUp) {
         const int64_t row = ti.m0 + row_in_tile;
         const int nbase = ti.n0 / 2;
 #pragma unroll 1
-        for (int c = 0; c < BN / 2; c += 32) {
+        for (int c = half * (BN / 4); c < (half + 1) * (BN / 4); c += 32) {
             tmem_ld32(tacc + c, r);
             tmem_ld32(tacc + BN / 2 + c, r2);
             tmem_wait_ld();
@@ -312,7 +314,7 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const TileInfo& t
     } else if constexpr (KIND == GemmKind::FwdDown || KIND == GemmKind::BwdDx) {
         const int64_t row = ti.m0 + row_in_tile;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
             tmem_ld32(tacc + c, r);
             tmem_wait_ld();
             const int col = ti.n0 + c;
@@ -323,26 +325,36 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const TileInfo& t
             store_row32(p.out0 + row * p.H + col, v, valid);
         }
     } else if constexpr (KIND == GemmKind::BwdDownDgrad) {
-        // SwiGLU backward (kernels.hpp:277-295): dup = silu(g)*d, dgate = u*d*silu'(g)
+        // SwiGLU backward (kernels.hpp:277-295): dup = silu(g)*d, dgate = u*d*silu'(g).
+        // The G/U loads of a chunk are issued before its TMEM load so they overlap.
         const int64_t row = ti.m0 + row_in_tile;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-            tmem_ld32(tacc + c, r);
-            tmem_wait_ld();
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
             const int col = ti.n0 + c;
             const int valid = p.I - col;
-            if (valid <= 0) continue;
-            float dgv[32], duv[32];
+            uint4 g4[4], u4[4];
             const __nv_bfloat16* gp = p.g + row * p.I + col;
             const __nv_bfloat16* up = p.u + row * p.I + col;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                uint4 g4 = make_uint4(0, 0, 0, 0), u4 = make_uint4(0, 0, 0, 0);
-                if (valid >= 32) {
-                    g4 = *reinterpret_cast<const uint4*>(gp + 8 * q);
-                    u4 = *reinterpret_cast<const uint4*>(up + 8 * q);
+                g4[q] = make_uint4(0, 0, 0, 0);
+                u4[q] = make_uint4(0, 0, 0, 0);
+            }
+            if (valid >= 32) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    g4[q] = __ldg(reinterpret_cast<const uint4*>(gp) + q);
+                    u4[q] = __ldg(reinterpret_cast<const uint4*>(up) + q);
                 }
-                const uint32_t gw[4] = {g4.x, g4.y, g4.z, g4.w}, uw[4] = {u4.x, u4.y, u4.z, u4.w};
+            }
+            tmem_ld32(tacc + c, r);
+            tmem_wait_ld();
+            if (valid <= 0) continue;
+            float dgv[32], duv[32];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t gw[4] = {g4[q].x, g4[q].y, g4[q].z, g4[q].w};
+                const uint32_t uw[4] = {u4[q].x, u4[q].y, u4[q].z, u4[q].w};
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
 #pragma unroll
@@ -355,7 +367,7 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const TileInfo& t
                             uu = j < valid ? __bfloat162float(up[j]) : 0.f;
                         }
                         const float d = __uint_as_float(r[j]);
-                        const float sg = 1.f / (1.f + __expf(-x));
+                        const float sg = __fdividef(1.f, 1.f + __expf(-x));
                         duv[j] = x * sg * d;
                         dgv[j] = uu * d * (sg * (1.f + x * (1.f - sg)));
                     }
@@ -370,7 +382,7 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const TileInfo& t
         const int Mtot = (KIND == GemmKind::WgradDown) ? p.I : p.H;
         const bool row_ok = m < Mtot;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
             if (!zero) {
                 tmem_ld32(tacc + c, r);
                 tmem_wait_ld();
@@ -422,7 +434,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull_bar(a), 1);
-            mbar_init(tempty_bar(a), 4);
+            mbar_init(tempty_bar(a), NUM_EPI_WARPS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -496,7 +508,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
             }
         }
     } else if (warp >= 4) {
-        const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31
+        const int quad = warp % 4;        // TMEM lanes 32*quad .. 32*quad+31 (hardware rule: warp id % 4)
+        const int half = (warp - 4) / 4;  // column half of the tile
         int it = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
             const TileInfo ti = tile_info<KIND>(p, ps, t);
@@ -504,8 +517,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
             const uint32_t acc_phase = (it >> 1) & 1;
             mbar_wait(tfull_bar(acc), acc_phase);
             tc_fence_after();
-            const uint32_t tacc = tmem_base + ((uint32_t)(32 * ew) << 16) + acc * BN;
-            epilogue_tile<KIND>(p, ti, tacc, 32 * ew + lane, ti.kb == 0);
+            const uint32_t tacc = tmem_base + ((uint32_t)(32 * quad) << 16) + acc * BN;
+            epilogue_tile<KIND>(p, ti, tacc, 32 * quad + lane, ti.kb == 0, half);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty_bar(acc));

@@ -6,30 +6,33 @@
 // selections by expert, in (token, k) order within an expert, independent of the
 // token-block size (test_moe.cpp:130-207). Here:
 //   1. one warp per 64-token chunk builds a shared-memory histogram of its local
-//      selections (counts are order-free, so smem atomics are deterministic);
-//   2. one CTA scans the histograms in (expert-major, chunk-minor) order, giving
-//      each (expert, chunk) its first row; it also scans per-token counts
-//      (cum_expert_counts), the TBS-blocked diagnostics (partial_cum) and the
-//      128-row padded group starts used by the GEMMs;
+//      selections (counts are order-free, so smem atomics are deterministic) and the
+//      per-token local counts;
+//   2. one CTA scans: each warp walks one expert's chunk histogram (contiguous,
+//      expert-major) giving every (expert, chunk) its first row inside the expert;
+//      a warp scan over the expert totals gives cum_token_counts and the 128-row
+//      padded group starts the GEMMs use; a tiled block scan gives cum_expert_counts;
 //   3. each warp re-walks its chunk in (t, k) order in 32-entry batches and ranks
 //      equal experts with __match_any_sync plus a per-expert carry, so the row of
 //      every selection equals the reference's counter(ln, tid)++.
+// The TBS-blocked diagnostics (partial_token_counts / partial_cum / counter,
+// moe.hpp:148-158) do not feed any later stage; they are produced only when the
+// artifacts are exported (launch_partial_counts).
 #include "b2_common.cuh"
 #include "kernels.h"
 
 namespace b2 {
 
-constexpr int kChunk = 64;           // tokens per warp chunk
+constexpr int kChunk = 64;  // tokens per warp chunk
 constexpr int kWarpsPerCta = 4;
 
 __device__ __forceinline__ int local_of(int e, int n_start, int nr) {
     return (e >= n_start && e < n_start + nr) ? e - n_start : -1;
 }
 
-// 1. histograms + per-token local counts + TBS-blocked counts
-__global__ void count_kernel(const int32_t* __restrict__ gidx, int T, int K, int N, int n_start, int nr, int tbs,
-                             int th, int32_t* __restrict__ whist /*[nchunks][nr]*/,
-                             int32_t* __restrict__ expert_counts, int32_t* __restrict__ partial_counts,
+// 1. histograms (whist [nr][nchunks]) + per-token local counts
+__global__ void count_kernel(const int32_t* __restrict__ gidx, int T, int K, int N, int n_start, int nr,
+                             int nchunks, int32_t* __restrict__ whist, int32_t* __restrict__ expert_counts,
                              int32_t* __restrict__ err) {
     extern __shared__ int32_t sh[];  // [kWarpsPerCta][nr]
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -42,17 +45,13 @@ __global__ void count_kernel(const int32_t* __restrict__ gidx, int T, int K, int
         const int t1 = min(T, t0 + kChunk);
         const int nent = (t1 - t0) * K;
         for (int f = lane; f < nent; f += 32) {
-            const int t = t0 + f / K;
             const int e = gidx[(int64_t)t0 * K + f];
             if (e < 0 || e >= N) {
                 atomicExch(err, 1);
                 continue;
             }
             const int ln = local_of(e, n_start, nr);
-            if (ln >= 0) {
-                atomicAdd(&hist[ln], 1);
-                atomicAdd(&partial_counts[(int64_t)ln * th + t / tbs], 1);
-            }
+            if (ln >= 0) atomicAdd(&hist[ln], 1);
         }
         for (int t = t0 + lane; t < t1; t += 32) {
             int c = 0;
@@ -61,101 +60,113 @@ __global__ void count_kernel(const int32_t* __restrict__ gidx, int T, int K, int
         }
     }
     __syncwarp();
-    const int nchunks = (int)ceil_div(T, kChunk);
     if (chunk < nchunks)
-        for (int i = lane; i < nr; i += 32) whist[(int64_t)chunk * nr + i] = hist[i];
+        for (int i = lane; i < nr; i += 32) whist[(int64_t)i * nchunks + chunk] = hist[i];
 }
 
-// block-wide exclusive scan of n ints read through `get(i)`, results through `put(i, v)`;
-// returns the total. Each thread owns one contiguous segment (fixed order).
+__device__ __forceinline__ int warp_incl_scan(int x, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    return x;
+}
+
+// tiled exclusive block scan (coalesced), fixed order; returns the total
 template <class Get, class Put>
-__device__ int64_t block_exclusive_scan(int64_t n, Get get, Put put, int64_t* sh_partials) {
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int64_t seg = ceil_div(n, nt);
-    const int64_t b = min(n, (int64_t)tid * seg), e = min(n, b + seg);
-    int64_t s = 0;
-    for (int64_t i = b; i < e; ++i) s += get(i);
-    sh_partials[tid] = s;
-    __syncthreads();
-    if (tid == 0) {
-        int64_t acc = 0;
-        for (int i = 0; i < nt; ++i) {
-            const int64_t v = sh_partials[i];
-            sh_partials[i] = acc;
-            acc += v;
+__device__ int64_t block_scan(int64_t n, Get get, Put put, int* wsum) {
+    const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nw = blockDim.x / 32;
+    int64_t carry = 0;
+    for (int64_t base = 0; base < n; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const int v = i < n ? get(i) : 0;
+        const int x = warp_incl_scan(v, lane);
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            const int s = lane < nw ? wsum[lane] : 0;
+            const int si = warp_incl_scan(s, lane);
+            if (lane < nw) wsum[lane] = si;
         }
-        sh_partials[nt] = acc;
+        __syncthreads();
+        const int64_t excl = carry + (warp > 0 ? wsum[warp - 1] : 0) + x - v;
+        if (i < n) put(i, excl);
+        carry += wsum[nw - 1];
+        __syncthreads();
     }
-    __syncthreads();
-    int64_t acc = sh_partials[tid];
-    for (int64_t i = b; i < e; ++i) {
-        const int64_t v = get(i);
-        put(i, acc);
-        acc += v;
-    }
-    const int64_t total = sh_partials[nt];
-    __syncthreads();
-    return total;
+    return carry;
 }
 
-// 2. all scans, one CTA of 1024 threads
+// 2. scans, one CTA of 1024 threads
 __global__ void __launch_bounds__(1024) scan_kernel(const int32_t* __restrict__ whist, int nchunks, int nr,
                                                     const int32_t* __restrict__ expert_counts, int T,
-                                                    const int32_t* __restrict__ partial_counts, int th,
-                                                    int32_t* __restrict__ wbase /*[nchunks][nr]*/,
+                                                    int32_t* __restrict__ wbase /*[nr][nchunks]*/,
                                                     int32_t* __restrict__ token_counts,
                                                     int32_t* __restrict__ cum_token_counts,
                                                     int32_t* __restrict__ pad_start,
-                                                    int32_t* __restrict__ cum_expert_counts,
-                                                    int32_t* __restrict__ partial_cum) {
-    __shared__ int64_t part[1025];
-    // (expert-major, chunk-minor) scan of the chunk histograms
-    const int64_t n1 = (int64_t)nr * nchunks;
-    const int64_t rt = block_exclusive_scan(
-        n1, [&](int64_t i) { return (int64_t)whist[(i % nchunks) * nr + i / nchunks]; },
-        [&](int64_t i, int64_t v) { wbase[(i % nchunks) * nr + i / nchunks] = (int32_t)v; }, part);
-    // expert totals, group boundaries and padded starts (thread 0: nr is small)
-    if (threadIdx.x == 0) {
-        // cum_token_counts[ln] = partial_cum[ln * TH] in the reference (moe.hpp:156-158):
-        // here the scan value at (ln, chunk 0)
-        int64_t pacc = 0;
-        for (int ln = 0; ln < nr; ++ln) {
-            const int64_t b = nchunks ? wbase[ln] : 0;
-            const int64_t e = (ln + 1 < nr) ? (nchunks ? wbase[ln + 1] : 0) : rt;
-            token_counts[ln] = (int32_t)(e - b);
-            cum_token_counts[ln] = (int32_t)b;
-            pad_start[ln] = (int32_t)pacc;
-            pacc += round_up(e - b, kRowAlign);
+                                                    int32_t* __restrict__ cum_expert_counts) {
+    extern __shared__ int32_t tot[];  // [nr]
+    __shared__ int wsum[32];
+    const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nw = blockDim.x / 32;
+    // (a) within-expert chunk offsets (expert-major, chunk-minor == the reference's
+    //     partial_cum order restricted to whole chunks)
+    for (int ln = warp; ln < nr; ln += nw) {
+        int carry = 0;
+        const int32_t* hrow = whist + (int64_t)ln * nchunks;
+        int32_t* brow = wbase + (int64_t)ln * nchunks;
+        for (int c0 = 0; c0 < nchunks; c0 += 32) {
+            const int c = c0 + lane;
+            const int v = c < nchunks ? hrow[c] : 0;
+            const int x = warp_incl_scan(v, lane);
+            if (c < nchunks) brow[c] = carry + x - v;
+            carry += __shfl_sync(0xffffffffu, x, 31);
         }
-        cum_token_counts[nr] = (int32_t)rt;
-        pad_start[nr] = (int32_t)pacc;
+        if (lane == 0) tot[ln] = carry;
     }
     __syncthreads();
-    const int64_t tot_e = block_exclusive_scan(
-        T, [&](int64_t i) { return (int64_t)expert_counts[i]; },
-        [&](int64_t i, int64_t v) { cum_expert_counts[i] = (int32_t)v; }, part);
-    if (threadIdx.x == 0) cum_expert_counts[T] = (int32_t)tot_e;
-    const int64_t n3 = (int64_t)nr * th;
-    const int64_t tot_p = block_exclusive_scan(
-        n3, [&](int64_t i) { return (int64_t)partial_counts[i]; },
-        [&](int64_t i, int64_t v) { partial_cum[i] = (int32_t)v; }, part);
-    if (threadIdx.x == 0) partial_cum[n3] = (int32_t)tot_p;
+    // (b) expert boundaries and padded starts (warp 0)
+    if (warp == 0) {
+        int carry = 0, pcarry = 0;
+        for (int l0 = 0; l0 < nr; l0 += 32) {
+            const int ln = l0 + lane;
+            const int v = ln < nr ? tot[ln] : 0;
+            const int pv = (int)round_up(v, kRowAlign);
+            const int x = warp_incl_scan(v, lane), px = warp_incl_scan(pv, lane);
+            if (ln < nr) {
+                token_counts[ln] = v;
+                cum_token_counts[ln] = carry + x - v;
+                pad_start[ln] = pcarry + px - pv;
+            }
+            carry += __shfl_sync(0xffffffffu, x, 31);
+            pcarry += __shfl_sync(0xffffffffu, px, 31);
+        }
+        if (lane == 0) {
+            cum_token_counts[nr] = carry;
+            pad_start[nr] = pcarry;
+        }
+    }
+    // (c) cum_expert_counts: exclusive scan of the per-token local counts
+    const int64_t te = block_scan(
+        T, [&](int64_t i) { return expert_counts[i]; }, [&](int64_t i, int64_t v) { cum_expert_counts[i] = (int32_t)v; },
+        wsum);
+    if (threadIdx.x == 0) cum_expert_counts[T] = (int32_t)te;
 }
 
 // 3. stable scatter
-__global__ void scatter_kernel(const int32_t* __restrict__ gidx, int T, int K, int n_start, int nr,
+__global__ void scatter_kernel(const int32_t* __restrict__ gidx, int T, int K, int n_start, int nr, int nchunks,
                                const int32_t* __restrict__ wbase, const int32_t* __restrict__ cum_token_counts,
                                const int32_t* __restrict__ pad_start, const int32_t* __restrict__ cum_expert_counts,
                                int32_t* __restrict__ input_indices, int32_t* __restrict__ output_indices,
                                int32_t* __restrict__ selected_k, int32_t* __restrict__ slot_prow,
                                int32_t* __restrict__ prow_src) {
-    extern __shared__ int32_t sh[];  // carry [kWarpsPerCta][nr]
+    extern __shared__ int32_t sh[];  // carry [kWarpsPerCta][nr] (row offset inside the expert)
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int chunk = blockIdx.x * kWarpsPerCta + w;
     const int t0 = chunk * kChunk;
     if (t0 >= T) return;
     int32_t* carry = sh + w * nr;
-    for (int i = lane; i < nr; i += 32) carry[i] = wbase[(int64_t)chunk * nr + i];
+    for (int i = lane; i < nr; i += 32) carry[i] = wbase[(int64_t)i * nchunks + chunk];
     __syncwarp();
     const int t1 = min(T, t0 + kChunk);
     const int nent = (t1 - t0) * K;
@@ -167,8 +178,8 @@ __global__ void scatter_kernel(const int32_t* __restrict__ gidx, int T, int K, i
         const int e = valid ? gidx[(int64_t)t * K + k] : -1;
         const int ln = valid ? local_of(e, n_start, nr) : -1;
         const unsigned peers = __match_any_sync(0xffffffffu, ln);
-        int row = 0;
-        if (ln >= 0) row = carry[ln] + __popc(peers & lt);
+        int off = 0;
+        if (ln >= 0) off = carry[ln] + __popc(peers & lt);
         __syncwarp();
         if (ln >= 0 && (peers & lt) == 0) carry[ln] += __popc(peers);  // group leader
         __syncwarp();
@@ -176,7 +187,8 @@ __global__ void scatter_kernel(const int32_t* __restrict__ gidx, int T, int K, i
             int before = 0;  // local selections of token t with k' < k
             for (int kk = 0; kk < k; ++kk) before += local_of(gidx[(int64_t)t * K + kk], n_start, nr) >= 0;
             const int pos = cum_expert_counts[t] + before;
-            const int prow = pad_start[ln] + (row - cum_token_counts[ln]);
+            const int row = cum_token_counts[ln] + off;
+            const int prow = pad_start[ln] + off;
             input_indices[row] = t;
             output_indices[pos] = row;
             selected_k[pos] = k;
@@ -198,24 +210,55 @@ void launch_routing_index(const RoutingIndexArgs& a, cudaStream_t st) {
     const int nchunks = (int)ceil_div(a.T, kChunk);
     const int nblk = (int)ceil_div(std::max(nchunks, 1), kWarpsPerCta);
     const size_t smem = sizeof(int32_t) * kWarpsPerCta * a.nr;
-    B2_CUDA(cudaMemsetAsync(a.partial_counts, 0, sizeof(int32_t) * (size_t)a.nr * a.th, st));
     if (a.T > 0) {
-        count_kernel<<<nblk, 32 * kWarpsPerCta, smem, st>>>(a.gidx, a.T, a.K, a.N, a.n_start, a.nr, a.tbs, a.th,
-                                                            a.whist, a.expert_counts, a.partial_counts, a.err);
+        count_kernel<<<nblk, 32 * kWarpsPerCta, smem, st>>>(a.gidx, a.T, a.K, a.N, a.n_start, a.nr, nchunks, a.whist,
+                                                            a.expert_counts, a.err);
         B2_LAUNCH_CHECK();
     }
-    scan_kernel<<<1, 1024, 0, st>>>(a.whist, nchunks, a.nr, a.expert_counts, a.T, a.partial_counts, a.th, a.wbase,
-                                    a.token_counts, a.cum_token_counts, a.pad_start, a.cum_expert_counts,
-                                    a.partial_cum);
+    scan_kernel<<<1, 1024, sizeof(int32_t) * a.nr, st>>>(a.whist, nchunks, a.nr, a.expert_counts, a.T, a.wbase,
+                                                         a.token_counts, a.cum_token_counts, a.pad_start,
+                                                         a.cum_expert_counts);
     B2_LAUNCH_CHECK();
     if (a.T > 0) {
-        scatter_kernel<<<nblk, 32 * kWarpsPerCta, smem, st>>>(a.gidx, a.T, a.K, a.n_start, a.nr, a.wbase,
+        scatter_kernel<<<nblk, 32 * kWarpsPerCta, smem, st>>>(a.gidx, a.T, a.K, a.n_start, a.nr, nchunks, a.wbase,
                                                               a.cum_token_counts, a.pad_start, a.cum_expert_counts,
                                                               a.input_indices, a.output_indices, a.selected_k,
                                                               a.slot_prow, a.prow_src);
         B2_LAUNCH_CHECK();
     }
     pad_fill_kernel<<<a.nr, 128, 0, st>>>(a.token_counts, a.pad_start, a.nr, a.prow_src);
+    B2_LAUNCH_CHECK();
+}
+
+// ---- TBS-blocked diagnostics (export only) ----------------------------------------------
+
+__global__ void partial_count_kernel(const int32_t* __restrict__ gidx, int64_t n, int K, int n_start, int nr, int th,
+                                     int tbs, int32_t* __restrict__ partial) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int ln = local_of(gidx[i], n_start, nr);
+        if (ln >= 0) atomicAdd(&partial[(int64_t)ln * th + (i / K) / tbs], 1);
+    }
+}
+
+__global__ void __launch_bounds__(1024) partial_scan_kernel(const int32_t* __restrict__ partial, int64_t n,
+                                                            int32_t* __restrict__ partial_cum) {
+    __shared__ int wsum[32];
+    const int64_t tot = block_scan(
+        n, [&](int64_t i) { return partial[i]; }, [&](int64_t i, int64_t v) { partial_cum[i] = (int32_t)v; }, wsum);
+    if (threadIdx.x == 0) partial_cum[n] = (int32_t)tot;
+}
+
+void launch_partial_counts(const int32_t* gidx, int T, int K, int n_start, int nr, int tbs, int th, int32_t* partial,
+                           int32_t* partial_cum, cudaStream_t st) {
+    const int64_t np = (int64_t)nr * th;
+    B2_CUDA(cudaMemsetAsync(partial, 0, sizeof(int32_t) * (size_t)std::max<int64_t>(np, 1), st));
+    const int64_t n = (int64_t)T * K;
+    if (n > 0) {
+        partial_count_kernel<<<(unsigned)std::min<int64_t>(1184, ceil_div(n, 256)), 256, 0, st>>>(gidx, n, K, n_start,
+                                                                                                  nr, th, tbs, partial);
+        B2_LAUNCH_CHECK();
+    }
+    partial_scan_kernel<<<1, 1024, 0, st>>>(partial, np, partial_cum);
     B2_LAUNCH_CHECK();
 }
 

@@ -19,19 +19,20 @@ void launch_router_dlogits(const float* probs, const float* wgrad, const int32_t
                            cudaStream_t st);
 void launch_aux_probs_grad(const int32_t* sel, float* out, int S, int N, double coeff, double total,
                            cudaStream_t st);
+// dWr = x^T dlogits with a deterministic split over S; part holds max_splits*H*N floats
+constexpr int kRouterDwMaxSplits = 32;
 template <typename T>
-void launch_router_dw(const T* x, const float* dlogits, T* dw, int S, int H, int N, cudaStream_t st);
+void launch_router_dw(const T* x, const float* dlogits, T* dw, float* part, int max_splits, int S, int H, int N,
+                      cudaStream_t st);
 
 // ---- counting / index generation (index.cu) ----
 struct RoutingIndexArgs {
     const int32_t* gidx;  // [T, K] gathered expert ids
-    int T, K, N, n_start, nr, tbs, th;
-    int32_t* whist;              // [ceil(T/64), nr]
-    int32_t* wbase;              // [ceil(T/64), nr]
+    int T, K, N, n_start, nr;
+    int32_t* whist;              // [nr, ceil(T/64)]
+    int32_t* wbase;              // [nr, ceil(T/64)]
     int32_t* expert_counts;      // [T]
     int32_t* cum_expert_counts;  // [T+1]
-    int32_t* partial_counts;     // [nr*th]
-    int32_t* partial_cum;        // [nr*th+1]
     int32_t* token_counts;       // [nr]
     int32_t* cum_token_counts;   // [nr+1]
     int32_t* pad_start;          // [nr+1]
@@ -43,6 +44,9 @@ struct RoutingIndexArgs {
     int32_t* err;                // expert id out of range flag
 };
 void launch_routing_index(const RoutingIndexArgs& a, cudaStream_t st);
+// TBS-blocked diagnostics partial_token_counts [nr*th] / partial_cum [nr*th+1] (moe.hpp:148-158)
+void launch_partial_counts(const int32_t* gidx, int T, int K, int n_start, int nr, int tbs, int th, int32_t* partial,
+                           int32_t* partial_cum, cudaStream_t st);
 
 // ---- permute / combine / element-wise (permute.cu) ----
 template <typename T>

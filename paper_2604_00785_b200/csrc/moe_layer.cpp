@@ -65,7 +65,7 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     auto acc = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
     // fp32
     for (int64_t n : {smax_ * N, smax_ * N, smax_ * K, tmax_ * K, (ceil_div(smax_, 128) + 1) * N, N, tmax_ * K,
-                      smax_ * N})
+                      smax_ * N, (int64_t)kRouterDwMaxSplits * H * N})
         acc(4 * (size_t)std::max<int64_t>(n, 1));
     // int32
     for (int64_t n : {smax_ * K, tmax_ * K, N, nch * nr, nch * nr, tmax_, tmax_ + 1, nr * thmax_, nr * thmax_ + 1, nr,
@@ -85,6 +85,7 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     mean_probs_ = arena_.take<float>(N);
     wgrad_ = arena_.take<float>(tmax_ * K);
     dlogits_ = arena_.take<float>(smax_ * N);
+    dw_part_ = arena_.take<float>((int64_t)kRouterDwMaxSplits * H * N);
     topi_ = arena_.take<int32_t>(smax_ * K);
     fi_ = arena_.take<int32_t>(tmax_ * K);
     sel_ = arena_.take<int32_t>(N);
@@ -215,14 +216,10 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     ra.N = N;
     ra.n_start = ctx_.coord_ep * nr;
     ra.nr = nr;
-    ra.tbs = (int)cfg_.token_block;
-    ra.th = (int)th_;
     ra.whist = whist_;
     ra.wbase = wbase_;
     ra.expert_counts = expert_counts_;
     ra.cum_expert_counts = cec_;
-    ra.partial_counts = partial_counts_;
-    ra.partial_cum = partial_cum_;
     ra.token_counts = token_counts_;
     ra.cum_token_counts = ctc_;
     ra.pad_start = pad_start_;
@@ -471,7 +468,8 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
     mark(kRouterBwd, false);
     launch_router_dlogits(probs_, wgrad_, topi_, topw_, aux_probs_grad, dlogits_, S, N, K, cfg_.normalize_topk, fur_,
                           st);
-    launch_router_dw<T>((const T*)x_, dlogits_, drouter, S, H, N, st);
+    launch_router_dw<T>((const T*)x_, dlogits_, drouter, dw_part_, kRouterDwMaxSplits, S, H, N, st);
+    launches_ += 1;
     // scatter-add to tokens (418-423) + matmul_nt(dlogits, router) (454)
     launch_dx_finalize<T>((const T*)dxp_, true, slot_prow_, cec_, dlogits_, router, dx, S, H, N, st);
     launches_ += 3;
@@ -509,6 +507,8 @@ MoeLayer::HostArtifacts MoeLayer::artifacts() {
     check(have_fwd_, "artifacts: no forward state");
     cudaStream_t st = ctx_.stream;
     const int64_t nr = cfg_.experts_per_rank();
+    launch_partial_counts(gi_, (int)t_, (int)cfg_.top_k, ctx_.coord_ep * (int)nr, (int)nr, (int)cfg_.token_block,
+                          (int)th_, partial_counts_, partial_cum_, st);
     HostArtifacts a;
     a.t_total = t_;
     a.th = th_;

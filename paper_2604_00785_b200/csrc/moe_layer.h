@@ -120,7 +120,7 @@ class MoeLayer {
     int launches_ = 0;
     Arena arena_;
     // fp32
-    float *logits_, *probs_, *topw_, *fw_, *colsum_, *mean_probs_, *wgrad_, *dlogits_;
+    float *logits_, *probs_, *topw_, *fw_, *colsum_, *mean_probs_, *wgrad_, *dlogits_, *dw_part_;
     // int32
     int32_t *topi_, *fi_, *sel_, *whist_, *wbase_, *expert_counts_, *cec_, *partial_counts_, *partial_cum_,
         *token_counts_, *ctc_, *pad_start_, *input_indices_, *output_indices_, *selected_k_, *slot_prow_,

@@ -21,6 +21,52 @@ __device__ __forceinline__ bool vec_ok(int H) {
     return ((int64_t)H * (int64_t)sizeof(T)) % 16 == 0;
 }
 
+// 16-byte vectors of T as fp32 lanes
+template <typename T>
+struct V16 {
+    static constexpr int n = 16 / sizeof(T);
+    __device__ __forceinline__ static void load(const T* p, float* f) {
+        const int4 v = __ldg(reinterpret_cast<const int4*>(p));
+        if constexpr (sizeof(T) == 4) {
+            f[0] = __int_as_float(v.x); f[1] = __int_as_float(v.y); f[2] = __int_as_float(v.z); f[3] = __int_as_float(v.w);
+        } else {
+            const uint32_t w[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                f[2 * q] = __uint_as_float(w[q] << 16);
+                f[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+            }
+        }
+    }
+    __device__ __forceinline__ static void unpack(const int4 v, float* f) {
+        if constexpr (sizeof(T) == 4) {
+            f[0] = __int_as_float(v.x); f[1] = __int_as_float(v.y); f[2] = __int_as_float(v.z); f[3] = __int_as_float(v.w);
+        } else {
+            const uint32_t w[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                f[2 * q] = __uint_as_float(w[q] << 16);
+                f[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+            }
+        }
+    }
+    __device__ __forceinline__ static void store(T* p, const float* f) {
+        int4 v;
+        if constexpr (sizeof(T) == 4) {
+            v = make_int4(__float_as_int(f[0]), __float_as_int(f[1]), __float_as_int(f[2]), __float_as_int(f[3]));
+        } else {
+            uint32_t w[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                __nv_bfloat162 b = __floats2bfloat162_rn(f[2 * q], f[2 * q + 1]);
+                w[q] = *reinterpret_cast<uint32_t*>(&b);
+            }
+            v = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
+        }
+        *reinterpret_cast<int4*>(p) = v;
+    }
+};
+
 // mlp_in[prow] = x[prow_src[prow]] (zero row when prow_src < 0); rows < *p_total
 template <typename T>
 __global__ void gather_rows_kernel(const T* __restrict__ x, const int32_t* __restrict__ prow_src,
@@ -68,6 +114,22 @@ __global__ void combine_kernel(const T* __restrict__ y, const int32_t* __restric
     const int t = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
     if (t >= T_tok) return;
     const int j0 = cum_expert_counts[t], j1 = cum_expert_counts[t + 1];
+    if (vec_ok<T>(H)) {
+        constexpr int V = V16<T>::n;
+        for (int c0 = lane * V; c0 < H; c0 += 32 * V) {
+            float acc[V], v[V];
+#pragma unroll
+            for (int q = 0; q < V; ++q) acc[q] = 0.f;
+            for (int j = j0; j < j1; ++j) {
+                const float wv = gw[(int64_t)t * K + selected_k[j]];
+                V16<T>::load(y + (int64_t)slot_prow[j] * H + c0, v);
+#pragma unroll
+                for (int q = 0; q < V; ++q) acc[q] = __fadd_rn(acc[q], __fmul_rn(wv, v[q]));
+            }
+            V16<T>::store(out + (int64_t)t * H + c0, acc);
+        }
+        return;
+    }
     for (int c0 = lane * 4; c0 < H; c0 += 128) {
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         for (int j = j0; j < j1; ++j) {
@@ -97,6 +159,64 @@ __global__ void out_reduction_bwd_kernel(const T* __restrict__ dout, const T* __
     for (int k = lane; k < K; k += 32) wgrad[(int64_t)t * K + k] = 0.f;
     __syncwarp();
     const T* gp = dout + (int64_t)t * H;
+    if (vec_ok<T>(H) && H <= 32 * V16<T>::n * 8) {
+        // dout row cached in registers (<= 8 vectors per lane); the slots of a token are
+        // processed together so their row loads are in flight at the same time
+        constexpr int V = V16<T>::n;
+        constexpr int MAXJ = 4;
+        int4 graw[8];
+        const int nv = H / V;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (lane + 32 * i < nv) graw[i] = __ldg(reinterpret_cast<const int4*>(gp + (lane + 32 * i) * V));
+        for (int jb = j0; jb < j1; jb += MAXJ) {
+            const int nj = min(MAXJ, j1 - jb);
+            int64_t rows[MAXJ];
+            float wv[MAXJ];
+            double dot[MAXJ];
+#pragma unroll
+            for (int q = 0; q < MAXJ; ++q) {
+                rows[q] = q < nj ? slot_prow[jb + q] : 0;
+                wv[q] = q < nj ? gw[(int64_t)t * K + selected_k[jb + q]] : 0.f;
+                dot[q] = 0.0;
+            }
+#pragma unroll 1
+            for (int i = 0; i < 8; ++i) {
+                const int vi = lane + 32 * i;
+                if (vi >= nv) break;
+                int4 yr[MAXJ];
+#pragma unroll
+                for (int q = 0; q < MAXJ; ++q)
+                    if (q < nj) yr[q] = __ldg(reinterpret_cast<const int4*>(y + rows[q] * H + vi * V));
+                float g[V];
+                int4 gsel = graw[0];
+#pragma unroll
+                for (int z = 1; z < 8; ++z)
+                    if (z == i) gsel = graw[z];
+                V16<T>::unpack(gsel, g);
+#pragma unroll
+                for (int q = 0; q < MAXJ; ++q) {
+                    if (q >= nj) break;
+                    float yv[V], o[V];
+                    V16<T>::unpack(yr[q], yv);
+#pragma unroll
+                    for (int z = 0; z < V; ++z) {
+                        o[z] = __fmul_rn(wv[q], g[z]);
+                        dot[q] += (double)g[z] * (double)yv[z];
+                    }
+                    V16<T>::store(dy + rows[q] * H + vi * V, o);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < MAXJ; ++q) {
+                double d = dot[q];
+#pragma unroll
+                for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+                if (lane == 0 && q < nj) wgrad[(int64_t)t * K + selected_k[jb + q]] = (float)d;
+            }
+        }
+        return;
+    }
     for (int j = j0; j < j1; ++j) {
         const int k = selected_k[j];
         const int64_t r = slot_prow[j];
@@ -114,64 +234,91 @@ __global__ void out_reduction_bwd_kernel(const T* __restrict__ dout, const T* __
 }
 
 // dx[t, h] = (sum over t's slots of dxp[slot_prow, h]) [or base[t, h]] + sum_e dl[t, e] * Wr[h, e]
-// 64 tokens x 64 h per CTA; the router term is a small SIMT GEMM (matmul_nt order).
+// CTA tile: 64 tokens x 64 h. Phase 1 computes the router term (matmul_nt order over e)
+// with 8 x 4 register tiles from transposed shared-memory operands; phase 2 re-maps
+// the threads onto 16-byte column vectors for the slot sum and the store.
 constexpr int kDxT = 64, kDxH = 64, kDxE = 32;
 template <typename T, bool FROM_SLOTS>
-__global__ void __launch_bounds__(256) dx_finalize_kernel(const T* __restrict__ src, const int32_t* __restrict__ slot_prow,
+__global__ void __launch_bounds__(128) dx_finalize_kernel(const T* __restrict__ src, const int32_t* __restrict__ slot_prow,
                                                           const int32_t* __restrict__ cum_expert_counts,
                                                           const float* __restrict__ dl, const T* __restrict__ wr,
                                                           T* __restrict__ dx, int S, int H, int N) {
-    __shared__ float ds[kDxE][kDxT + 1];
-    __shared__ float ws[kDxE][kDxH + 1];
+    __shared__ __align__(16) float sm[kDxT * (kDxH + 4)];  // phase 1: ds[e][t], ws[e][h]; phase 2: rt[t][h]
+    float (*ds)[kDxT] = reinterpret_cast<float (*)[kDxT]>(sm);
+    float (*ws)[kDxH] = reinterpret_cast<float (*)[kDxH]>(sm + kDxE * kDxT);
     const int t0 = blockIdx.x * kDxT, h0 = blockIdx.y * kDxH;
-    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-    float acc[4][4];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // 16 h-quads x 8 token-octets
+    float acc[8][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
     for (int e0 = 0; e0 < N; e0 += kDxE) {
-        for (int i = threadIdx.x; i < kDxE * kDxT; i += 256) {
-            const int ee = i % kDxE, tt = i / kDxE;
-            const int e = e0 + ee, t = t0 + tt, h = h0 + tt;
-            ds[ee][tt] = (e < N && t < S) ? dl[(int64_t)t * N + e] : 0.f;
-            ws[ee][tt] = (e < N && h < H) ? Elem<T>::load(wr + (int64_t)h * N + e) : 0.f;
+        for (int i = threadIdx.x; i < kDxE * kDxT; i += 128) {
+            const int ee = i % kDxE, rr = i / kDxE;  // consecutive threads: consecutive e (coalesced)
+            const int e = e0 + ee, t = t0 + rr, h = h0 + rr;
+            ds[ee][rr] = (e < N && t < S) ? dl[(int64_t)t * N + e] : 0.f;
+            ws[ee][rr] = (e < N && h < H) ? Elem<T>::load(wr + (int64_t)h * N + e) : 0.f;
         }
         __syncthreads();
         const int eend = min(kDxE, N - e0);
         for (int ee = 0; ee < eend; ++ee) {
-            float a[4], b[4];
+            const float4 a0 = *reinterpret_cast<const float4*>(&ds[ee][ty * 8]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&ds[ee][ty * 8 + 4]);
+            const float4 b4 = *reinterpret_cast<const float4*>(&ws[ee][tx * 4]);
+            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float b[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = ds[ee][ty * 4 + i];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = ws[ee][tx * 4 + j];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < 8; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(a[i], b[j]));
         }
         __syncthreads();
     }
+    float (*rt)[kDxH + 4] = reinterpret_cast<float (*)[kDxH + 4]>(sm);  // 64 x 68 floats fits in sm
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int t = t0 + ty * 4 + i;
-        if (t >= S) continue;
-        int j0 = 0, j1 = 0;
-        if (FROM_SLOTS) {
-            j0 = cum_expert_counts[t];
-            j1 = cum_expert_counts[t + 1];
+    for (int i = 0; i < 8; ++i)
+        *reinterpret_cast<float4*>(&rt[ty * 8 + i][tx * 4]) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    __syncthreads();
+    constexpr int V = 16 / sizeof(T);
+    const bool vec = (H % V) == 0 && (h0 + kDxH <= H);
+    if (vec) {
+        constexpr int VPT = kDxH / V;  // vectors per token row
+        for (int q = threadIdx.x; q < kDxT * VPT; q += 128) {
+            const int tt = q / VPT, vv = q % VPT;
+            const int t = t0 + tt;
+            if (t >= S) continue;
+            const int h = h0 + vv * V;
+            float base[V], v[V];
+#pragma unroll
+            for (int z = 0; z < V; ++z) base[z] = 0.f;
+            if (FROM_SLOTS) {
+                const int j0 = cum_expert_counts[t], j1 = cum_expert_counts[t + 1];
+                for (int j = j0; j < j1; ++j) {
+                    V16<T>::load(src + (int64_t)slot_prow[j] * H + h, v);
+#pragma unroll
+                    for (int z = 0; z < V; ++z) base[z] = __fadd_rn(base[z], v[z]);
+                }
+            } else {
+                V16<T>::load(src + (int64_t)t * H + h, base);
+            }
+#pragma unroll
+            for (int z = 0; z < V; ++z) base[z] = __fadd_rn(base[z], rt[tt][vv * V + z]);
+            V16<T>::store(dx + (int64_t)t * H + h, base);
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int h = h0 + tx * 4 + j;
-            if (h >= H) continue;
+    } else {
+        for (int q = threadIdx.x; q < kDxT * kDxH; q += 128) {
+            const int tt = q / kDxH, hh = q % kDxH;
+            const int t = t0 + tt, h = h0 + hh;
+            if (t >= S || h >= H) continue;
             float base = 0.f;
             if (FROM_SLOTS) {
-                for (int s = j0; s < j1; ++s) base = __fadd_rn(base, Elem<T>::to_f(src[(int64_t)slot_prow[s] * H + h]));
+                const int j0 = cum_expert_counts[t], j1 = cum_expert_counts[t + 1];
+                for (int j = j0; j < j1; ++j) base = __fadd_rn(base, Elem<T>::to_f(src[(int64_t)slot_prow[j] * H + h]));
             } else {
                 base = Elem<T>::to_f(src[(int64_t)t * H + h]);
             }
-            dx[(int64_t)t * H + h] = Elem<T>::from_f(__fadd_rn(base, acc[i][j]));
+            dx[(int64_t)t * H + h] = Elem<T>::from_f(__fadd_rn(base, rt[tt][hh]));
         }
     }
 }
@@ -255,9 +402,9 @@ void launch_dx_finalize(const T* src, bool from_slots, const int32_t* slot_prow,
     if (S <= 0) return;
     dim3 grid((unsigned)ceil_div(S, kDxT), (unsigned)ceil_div(H, kDxH));
     if (from_slots)
-        dx_finalize_kernel<T, true><<<grid, 256, 0, st>>>(src, slot_prow, cec, dl, wr, dx, S, H, N);
+        dx_finalize_kernel<T, true><<<grid, 128, 0, st>>>(src, slot_prow, cec, dl, wr, dx, S, H, N);
     else
-        dx_finalize_kernel<T, false><<<grid, 256, 0, st>>>(src, slot_prow, cec, dl, wr, dx, S, H, N);
+        dx_finalize_kernel<T, false><<<grid, 128, 0, st>>>(src, slot_prow, cec, dl, wr, dx, S, H, N);
     B2_LAUNCH_CHECK();
 }
 

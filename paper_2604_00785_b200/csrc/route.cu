@@ -15,31 +15,64 @@
 
 namespace b2 {
 
-// ---- logits: 64 tokens x 64 experts per CTA, 16 outputs per thread -----------------
+// ---- logits: 64 tokens x 64 experts per CTA, 128 threads, 8 x 4 outputs per thread ------
+// x tiles are loaded with 16-byte vectors and stored transposed (xs[p][token]) so the
+// inner loop reads operands with 128-bit shared loads. For bf16 inputs every product
+// is exact in fp32, so an FMA rounds exactly like the reference's multiply-then-add;
+// fp32 inputs use a separate multiply and add.
 
-constexpr int kRtTok = 64, kRtExp = 64, kRtP = 32;
+constexpr int kRtTok = 64, kRtExp = 64, kRtP = 32, kRtXs = kRtTok + 4;
 
 template <typename T>
-__global__ void __launch_bounds__(256) router_logits_kernel(const T* __restrict__ x,
-                                                            const T* __restrict__ w,
-                                                            float* __restrict__ logits, int S,
-                                                            int H, int N) {
-    __shared__ float xs[kRtP][kRtTok + 1];
-    __shared__ float ws[kRtP][kRtExp];
+__global__ void __launch_bounds__(128) router_logits_kernel(const T* __restrict__ x, const T* __restrict__ w,
+                                                            float* __restrict__ logits, int S, int H, int N) {
+    __shared__ __align__(16) float xs[kRtP][kRtXs];
+    __shared__ __align__(16) float ws[kRtP][kRtExp];
     const int t0 = blockIdx.x * kRtTok, e0 = blockIdx.y * kRtExp;
-    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // 16 expert-quads x 16 token-quads
-    float acc[4][4];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // 16 expert-quads x 8 token-octets
+    constexpr int VX = 16 / sizeof(T);
+    const bool vec = (H % VX) == 0;
+    float acc[8][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
     for (int p0 = 0; p0 < H; p0 += kRtP) {
-        for (int i = threadIdx.x; i < kRtTok * kRtP; i += 256) {
-            const int tt = i / kRtP, pp = i % kRtP;
-            const int t = t0 + tt, p = p0 + pp;
-            xs[pp][tt] = (t < S && p < H) ? Elem<T>::load(x + (int64_t)t * H + p) : 0.f;
+        if (vec) {
+            for (int v = threadIdx.x; v < kRtTok * kRtP / VX; v += 128) {
+                const int tt = v / (kRtP / VX), pp = (v % (kRtP / VX)) * VX;
+                const int t = t0 + tt, p = p0 + pp;
+                float f[VX];
+                if (t < S && p < H) {
+                    const int4 raw = __ldg(reinterpret_cast<const int4*>(x + (int64_t)t * H + p));
+                    if constexpr (sizeof(T) == 2) {
+                        const uint32_t wv[4] = {(uint32_t)raw.x, (uint32_t)raw.y, (uint32_t)raw.z, (uint32_t)raw.w};
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            f[2 * q] = __uint_as_float(wv[q] << 16);
+                            f[2 * q + 1] = __uint_as_float(wv[q] & 0xFFFF0000u);
+                        }
+                    } else {
+                        f[0] = __int_as_float(raw.x);
+                        f[1] = __int_as_float(raw.y);
+                        f[2] = __int_as_float(raw.z);
+                        f[3] = __int_as_float(raw.w);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < VX; ++q) f[q] = 0.f;
+                }
+#pragma unroll
+                for (int q = 0; q < VX; ++q) xs[pp + q][tt] = f[q];
+            }
+        } else {
+            for (int i = threadIdx.x; i < kRtTok * kRtP; i += 128) {
+                const int tt = i / kRtP, pp = i % kRtP;
+                const int t = t0 + tt, p = p0 + pp;
+                xs[pp][tt] = (t < S && p < H) ? Elem<T>::load(x + (int64_t)t * H + p) : 0.f;
+            }
         }
-        for (int i = threadIdx.x; i < kRtP * kRtExp; i += 256) {
+        for (int i = threadIdx.x; i < kRtP * kRtExp; i += 128) {
             const int pp = i / kRtExp, ee = i % kRtExp;
             const int p = p0 + pp, e = e0 + ee;
             ws[pp][ee] = (p < H && e < N) ? Elem<T>::load(w + (int64_t)p * N + e) : 0.f;
@@ -47,26 +80,34 @@ __global__ void __launch_bounds__(256) router_logits_kernel(const T* __restrict_
         __syncthreads();
         const int pend = min(kRtP, H - p0);
         for (int pp = 0; pp < pend; ++pp) {
-            float a[4], b[4];
+            const float4 a0 = *reinterpret_cast<const float4*>(&xs[pp][ty * 8]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&xs[pp][ty * 8 + 4]);
+            const float4 b4 = *reinterpret_cast<const float4*>(&ws[pp][tx * 4]);
+            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float b[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = xs[pp][ty * 4 + i];
+            for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = ws[pp][tx * 4 + j];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(a[i], b[j]));
+                for (int j = 0; j < 4; ++j) {
+                    if constexpr (sizeof(T) == 2) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+                    else acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(a[i], b[j]));
+                }
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int t = t0 + ty * 4 + i;
+    for (int i = 0; i < 8; ++i) {
+        const int t = t0 + ty * 8 + i;
         if (t >= S) continue;
+        if (e0 + tx * 4 + 3 < N && (N % 4) == 0) {
+            *reinterpret_cast<float4*>(logits + (int64_t)t * N + e0 + tx * 4) =
+                make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int e = e0 + tx * 4 + j;
-            if (e < N) logits[(int64_t)t * N + e] = acc[i][j];
+            for (int j = 0; j < 4; ++j) {
+                const int e = e0 + tx * 4 + j;
+                if (e < N) logits[(int64_t)t * N + e] = acc[i][j];
+            }
         }
     }
 }
@@ -188,9 +229,15 @@ __global__ void prob_colsum_final_kernel(const float* __restrict__ partial, floa
     }
 }
 
-__global__ void sel_count_kernel(const int32_t* __restrict__ idx, int64_t n, int32_t* __restrict__ sel) {
+__global__ void sel_count_kernel(const int32_t* __restrict__ idx, int64_t n, int32_t* __restrict__ sel, int N) {
+    extern __shared__ int32_t hist[];
+    for (int e = threadIdx.x; e < N; e += blockDim.x) hist[e] = 0;
+    __syncthreads();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(&sel[idx[i]], 1);
+        atomicAdd(&hist[idx[i]], 1);
+    __syncthreads();
+    for (int e = threadIdx.x; e < N; e += blockDim.x)
+        if (hist[e]) atomicAdd(&sel[e], hist[e]);
 }
 
 // ---- router backward (moe.hpp:431-454) -----------------------------------------------
@@ -258,48 +305,64 @@ __global__ void aux_probs_grad_kernel(const int32_t* __restrict__ sel, float* __
     out[i] = (float)(coeff * (double)N * ((double)sel[e] / total) / (double)S);
 }
 
-// dWr[h, e] = sum_s x[s,h] * dlogits[s,e]  (matmul_tn, kernels.hpp:52-72): one CTA per
-// 64 h-rows x 64 experts, reduction over all S rows in a fixed order (deterministic).
+// dWr[h, e] = sum_s x[s,h] * dlogits[s,e]  (matmul_tn, kernels.hpp:52-72): CTA tile of
+// 64 h-rows x 64 experts over one slice of the S rows; the slices' partials are then
+// summed in slice order by router_dw_reduce_kernel (deterministic split-S).
 template <typename T>
-__global__ void __launch_bounds__(256) router_dw_kernel(const T* __restrict__ x, const float* __restrict__ dl,
-                                                        T* __restrict__ dw, int S, int H, int N) {
-    __shared__ float xs[kRtP][64 + 1];
-    __shared__ float ds[kRtP][64];
-    const int h0 = blockIdx.x * 64, e0 = blockIdx.y * 64;
-    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-    float acc[4][4] = {};
-    for (int s0 = 0; s0 < S; s0 += kRtP) {
-        for (int i = threadIdx.x; i < kRtP * 64; i += 256) {
+__global__ void __launch_bounds__(128) router_dw_partial_kernel(const T* __restrict__ x, const float* __restrict__ dl,
+                                                                float* __restrict__ part, int S, int H, int N,
+                                                                int rows_per_split) {
+    __shared__ __align__(16) float xs[kRtP][64];
+    __shared__ __align__(16) float ds[kRtP][64];
+    const int h0 = blockIdx.x * 64, e0 = blockIdx.y * 64, split = blockIdx.z;
+    const int sb = split * rows_per_split, se = min(S, sb + rows_per_split);
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // 16 expert-quads x 8 h-octets
+    float acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    for (int s0 = sb; s0 < se; s0 += kRtP) {
+        for (int i = threadIdx.x; i < kRtP * 64; i += 128) {
             const int ss = i / 64, hh = i % 64;
-            const int s = s0 + ss, h = h0 + hh;
-            xs[ss][hh] = (s < S && h < H) ? Elem<T>::load(x + (int64_t)s * H + h) : 0.f;
-            const int e = e0 + hh;
-            ds[ss][hh] = (s < S && e < N) ? dl[(int64_t)s * N + e] : 0.f;
+            const int s = s0 + ss, h = h0 + hh, e = e0 + hh;
+            xs[ss][hh] = (s < se && h < H) ? Elem<T>::load(x + (int64_t)s * H + h) : 0.f;
+            ds[ss][hh] = (s < se && e < N) ? dl[(int64_t)s * N + e] : 0.f;
         }
         __syncthreads();
+#pragma unroll 4
         for (int ss = 0; ss < kRtP; ++ss) {
-            float a[4], b[4];
+            const float4 a0 = *reinterpret_cast<const float4*>(&xs[ss][ty * 8]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&xs[ss][ty * 8 + 4]);
+            const float4 b4 = *reinterpret_cast<const float4*>(&ds[ss][tx * 4]);
+            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float b[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = xs[ss][ty * 4 + i];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = ds[ss][tx * 4 + j];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < 8; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int h = h0 + ty * 4 + i;
+    for (int i = 0; i < 8; ++i) {
+        const int h = h0 + ty * 8 + i;
         if (h >= H) continue;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int e = e0 + tx * 4 + j;
-            if (e < N) dw[(int64_t)h * N + e] = Elem<T>::from_f(acc[i][j]);
+            if (e < N) part[((int64_t)split * H + h) * N + e] = acc[i][j];
         }
     }
+}
+
+template <typename T>
+__global__ void router_dw_reduce_kernel(const float* __restrict__ part, T* __restrict__ dw, int nsplit, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float acc = 0.f;
+    for (int sp = 0; sp < nsplit; ++sp) acc += part[(int64_t)sp * n + i];
+    dw[i] = Elem<T>::from_f(acc);
 }
 
 // ---- launchers ----------------------------------------------------------------------
@@ -308,7 +371,7 @@ template <typename T>
 void launch_router_logits(const T* x, const T* w, float* logits, int S, int H, int N, cudaStream_t st) {
     if (S == 0) return;
     dim3 grid((unsigned)ceil_div(S, kRtTok), (unsigned)ceil_div(N, kRtExp));
-    router_logits_kernel<T><<<grid, 256, 0, st>>>(x, w, logits, S, H, N);
+    router_logits_kernel<T><<<grid, 128, 0, st>>>(x, w, logits, S, H, N);
     B2_LAUNCH_CHECK();
 }
 template void launch_router_logits<float>(const float*, const float*, float*, int, int, int, cudaStream_t);
@@ -346,7 +409,8 @@ void launch_aux_stats(const float* probs, int S, int N, const int32_t* gidx, int
         B2_CUDA(cudaMemsetAsync(mean_probs, 0, sizeof(float) * N, st));
     }
     if (n_gidx > 0) {
-        sel_count_kernel<<<(unsigned)std::min<int64_t>(1184, ceil_div(n_gidx, 256)), 256, 0, st>>>(gidx, n_gidx, sel);
+        sel_count_kernel<<<(unsigned)std::min<int64_t>(148, ceil_div(n_gidx, 256)), 256, sizeof(int32_t) * N, st>>>(
+            gidx, n_gidx, sel, N);
         B2_LAUNCH_CHECK();
     }
 }
@@ -369,13 +433,21 @@ void launch_aux_probs_grad(const int32_t* sel, float* out, int S, int N, double 
 }
 
 template <typename T>
-void launch_router_dw(const T* x, const float* dlogits, T* dw, int S, int H, int N, cudaStream_t st) {
-    dim3 grid((unsigned)ceil_div(H, 64), (unsigned)ceil_div(N, 64));
-    router_dw_kernel<T><<<grid, 256, 0, st>>>(x, dlogits, dw, S, H, N);
+void launch_router_dw(const T* x, const float* dlogits, T* dw, float* part, int max_splits, int S, int H, int N,
+                      cudaStream_t st) {
+    const int tiles = (int)(ceil_div(H, 64) * ceil_div(N, 64));
+    int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(max_splits, ceil_div(4 * 148, tiles)));
+    const int rows = (int)round_up(ceil_div(std::max(S, 1), nsplit), kRtP);
+    nsplit = (int)ceil_div(std::max(S, 1), rows);
+    dim3 grid((unsigned)ceil_div(H, 64), (unsigned)ceil_div(N, 64), (unsigned)nsplit);
+    router_dw_partial_kernel<T><<<grid, 128, 0, st>>>(x, dlogits, part, S, H, N, rows);
+    B2_LAUNCH_CHECK();
+    const int64_t n = (int64_t)H * N;
+    router_dw_reduce_kernel<T><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(part, dw, nsplit, n);
     B2_LAUNCH_CHECK();
 }
-template void launch_router_dw<float>(const float*, const float*, float*, int, int, int, cudaStream_t);
-template void launch_router_dw<__nv_bfloat16>(const __nv_bfloat16*, const float*, __nv_bfloat16*, int, int, int,
-                                              cudaStream_t);
+template void launch_router_dw<float>(const float*, const float*, float*, float*, int, int, int, int, cudaStream_t);
+template void launch_router_dw<__nv_bfloat16>(const __nv_bfloat16*, const float*, __nv_bfloat16*, float*, int, int,
+                                              int, int, cudaStream_t);
 
 }  // namespace b2
