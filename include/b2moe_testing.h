@@ -11,9 +11,10 @@ extern "C" {
 #endif
 /* One tcgen05 grouped GEMM of the expert MLP (kind: 0 FwdGateUp, 1 FwdDown,
  * 2 BwdDownDgrad, 3 BwdDx, 4 WgradDown, 5 WgradGateUp), bf16 operands in the
- * padded expert-row layout; pad_start [nr+1] int32 device (multiples of 128). */
+ * padded expert-row layout; pad_start [nr+1] int32 device (multiples of 256),
+ * counts [nr] int32 device rows per expert. */
 int b2x_grouped_gemm(b2_ctx* ctx, int kind, int hidden, int intermediate, int nr, const int32_t* pad_start,
-                     int64_t pmax, const void* x, const void* wg, const void* wu, const void* wd, const void* g,
+                     const int32_t* counts, int64_t pmax, const void* x, const void* wg, const void* wu, const void* wd, const void* g,
                      const void* u, const void* h, const void* dy, const void* dgu, void* out0, void* out1,
                      void* out2, float scale);
 #ifdef __cplusplus

@@ -68,8 +68,8 @@ __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + 
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 // rows of each expert group are padded to this multiple inside the permuted
-// buffers, so GEMM M-tiles (forward/dgrad) and K-blocks (wgrad) never straddle
-// two experts; pad rows are zero and contribute nothing.
-constexpr int kRowAlign = 128;
+// buffers, so the 256-row GEMM tiles of a CTA pair (forward/dgrad) and the wgrad
+// K-blocks never straddle two experts; pad rows are zero and contribute nothing.
+constexpr int kRowAlign = 256;
 
 }  // namespace b2

@@ -484,7 +484,7 @@ int b2_opt_last_launches(b2_opt* o) { return o ? o->opt->last_launches() : 0; }
 #include "../../include/b2moe_testing.h"
 
 extern "C" int b2x_grouped_gemm(b2_ctx* ctx, int kind, int hidden, int intermediate, int nr, const int32_t* pad_start,
-                                int64_t pmax, const void* x, const void* wg, const void* wu, const void* wd,
+                                const int32_t* counts, int64_t pmax, const void* x, const void* wg, const void* wu, const void* wd,
                                 const void* g, const void* u, const void* h, const void* dy, const void* dgu,
                                 void* out0, void* out1, void* out2, float scale) {
     return guard([&] {
@@ -497,6 +497,7 @@ extern "C" int b2x_grouped_gemm(b2_ctx* ctx, int kind, int hidden, int intermedi
         a.nr = nr;
         a.pmax = pmax;
         a.pad_start = pad_start;
+        a.counts = counts;
         a.x = x;
         a.wg = wg;
         a.wu = wu;

@@ -38,11 +38,21 @@
 namespace b2 {
 namespace sm100 {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2;           // 16 KB
-constexpr int B_BYTES = BN * BK * 2;           // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 48 KB
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int BM = 128, BN = 256, BK = 64;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB: the A rows one CTA holds per stage
+// CG = CTAs per MMA (cta_group). CG = 1: 128 x 256 tile per CTA, 4 stages of 48 KB.
+// CG = 2: 256 x 256 tile per CTA pair (tcgen05.mma.cta_group::2); each CTA holds its
+// 128 A rows and HALF of the B columns, so a stage is 32 KB and 6 stages fit.
+template <int CG>
+struct Cfg {
+    static constexpr int B_COLS = BN / CG;                  // B columns held per CTA
+    static constexpr int B_BYTES = B_COLS * BK * 2;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGES = CG == 1 ? 4 : 6;
+    static constexpr int TILE_M = BM * CG;
+};
+constexpr int SMEM_BYTES = 6 * (A_BYTES + 128 * BK * 2) + 1024 /*align*/ + 512 /*barriers*/;
+static_assert(SMEM_BYTES >= 4 * (A_BYTES + 256 * BK * 2) + 1024 + 512, "smem sized for both CTA groupings");
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_EPI_WARPS = 8;  // two warps per TMEM lane quadrant, each half the columns
 constexpr int NUM_THREADS = 128 + 32 * NUM_EPI_WARPS;
@@ -52,6 +62,7 @@ struct Params {
     CUtensorMap mapB0;
     CUtensorMap mapB1;
     const int32_t* pad_start;  // [nr+1]
+    const int32_t* counts;     // [nr] rows per expert (wgrad K extent)
     int nr, H, I;
     int m_tiles_fixed;  // by_k kinds: tiles along M
     int n_tiles;
@@ -62,6 +73,16 @@ struct Params {
     __nv_bfloat16* out1;
     __nv_bfloat16* out2;
     float scale;
+    uint32_t idesc;       // instruction descriptor (runtime N for the router kinds)
+    int umma_n;           // accumulator columns in use
+    int b_chunks;         // 64-column B boxes per stage (MN-major B)
+    uint32_t stage_tx;    // bytes a stage's TMA loads deliver
+    int S, N;             // router kinds: tokens, experts
+    int rows_per_split;   // RouterDw
+    const int32_t* cec;
+    const int32_t* slot_prow;
+    const __nv_bfloat16* src;
+    float* part;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -96,6 +117,31 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         "l"((uint64_t)map), "r"(bar), "r"(c0), "r"(c1)
         : "memory");
 }
+// 2-CTA (cta_group::2) load: the bytes complete_tx on the LEADER CTA's barrier
+__device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"((uint64_t)map), "r"(leader_bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// shared::cluster address of the same smem offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)map) : "memory");
 }
@@ -111,10 +157,10 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
     return d;
 }
 
-// kind::f16 instruction descriptor: bf16 x bf16 -> fp32, M = 128, N = 256
-__host__ __device__ constexpr uint32_t umma_idesc(bool a_mn, bool b_mn) {
+// kind::f16 instruction descriptor: bf16 x bf16 -> fp32, M = 128, N = n (16..256, %16)
+__host__ __device__ constexpr uint32_t umma_idesc(bool a_mn, bool b_mn, int n = BN, int m = BM) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
-           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+           ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
 __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -126,8 +172,24 @@ __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
         : "memory");
 }
+__device__ __forceinline__ void umma_f16_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+// arrive on the same barrier offset in both CTAs of the pair once the MMAs retire
+__device__ __forceinline__ void umma_commit_cg2(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+        "h"((uint16_t)0x3)
+        : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -195,6 +257,14 @@ template <>
 struct Traits<GemmKind::WgradGateUp> {
     static constexpr bool by_k = true, a_mn = true, b_mn = true;
 };
+template <>
+struct Traits<GemmKind::RouterDx> {
+    static constexpr bool by_k = false, a_mn = false, b_mn = false;
+};
+template <>
+struct Traits<GemmKind::RouterDw> {
+    static constexpr bool by_k = true, a_mn = true, b_mn = true;
+};
 
 struct TileInfo {
     int e;       // expert
@@ -203,27 +273,46 @@ struct TileInfo {
     int krow0;   // by_k: first padded row of the expert
 };
 
-template <GemmKind KIND>
+template <GemmKind KIND, int CG>
 __device__ __forceinline__ int total_tiles(const Params& p, const int32_t* ps) {
+    if (KIND == GemmKind::RouterDx) return (int)ceil_div(p.S, BM) * p.n_tiles;
     if (Traits<KIND>::by_k) return p.nr * p.m_tiles_fixed * p.n_tiles;
-    return (ps[p.nr] / BM) * p.n_tiles;
+    return (ps[p.nr] / Cfg<CG>::TILE_M) * p.n_tiles;
 }
 
-template <GemmKind KIND>
+template <GemmKind KIND, int CG>
 __device__ __forceinline__ TileInfo tile_info(const Params& p, const int32_t* ps, int t) {
+    constexpr int TM = Cfg<CG>::TILE_M;
     TileInfo ti;
+    if (KIND == GemmKind::RouterDx) {
+        ti.m0 = (t / p.n_tiles) * BM;
+        ti.n0 = (t % p.n_tiles) * BN;
+        ti.e = 0;
+        ti.krow0 = 0;
+        ti.kb = p.num_kb_fixed;
+        return ti;
+    }
+    if (KIND == GemmKind::RouterDw) {  // "experts" are the S splits; n_tiles == 1
+        ti.e = t / p.m_tiles_fixed;
+        ti.m0 = (t % p.m_tiles_fixed) * BM;
+        ti.n0 = 0;
+        ti.krow0 = ti.e * p.rows_per_split;
+        const int rows = min(p.S, ti.krow0 + p.rows_per_split) - ti.krow0;
+        ti.kb = rows > 0 ? (rows + BK - 1) / BK : 0;
+        return ti;
+    }
     if (Traits<KIND>::by_k) {
         const int per_e = p.m_tiles_fixed * p.n_tiles;
         ti.e = t / per_e;
         const int r = t % per_e;
-        ti.m0 = (r / p.n_tiles) * BM;
+        ti.m0 = (r / p.n_tiles) * TM;
         ti.n0 = (r % p.n_tiles) * BN;
         ti.krow0 = ps[ti.e];
-        ti.kb = (ps[ti.e + 1] - ps[ti.e]) / BK;
+        ti.kb = (p.counts[ti.e] + BK - 1) / BK;  // pad rows past the count are zero: skip them
     } else {
         const int mt = t / p.n_tiles;
         ti.n0 = (t % p.n_tiles) * BN;
-        ti.m0 = mt * BM;
+        ti.m0 = mt * TM;
         int lo = 0, hi = p.nr - 1;  // last expert whose padded start <= m0
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
@@ -237,37 +326,58 @@ __device__ __forceinline__ TileInfo tile_info(const Params& p, const int32_t* ps
     return ti;
 }
 
-// producer: one stage of A and B for (tile, kb)
-template <GemmKind KIND>
-__device__ __forceinline__ void load_stage(const Params& p, const TileInfo& ti, int kb, uint32_t sA, uint32_t sB,
-                                           uint32_t bar) {
+// producer: one stage of A and B for (tile, kb). `m_own` is the first A row this CTA
+// holds (the pair's tile base + 128 * rank); with CG = 2 each CTA loads B columns
+// [128 * rank, 128 * rank + 128) of the tile and signals the leader's barrier.
+template <GemmKind KIND, int CG>
+__device__ __forceinline__ void load_stage(const Params& p, const TileInfo& ti, int kb, int m_own, uint32_t rank,
+                                           uint32_t sA, uint32_t sB, uint32_t bar) {
     const int k0 = kb * BK;
+    auto ld = [&](uint32_t dst, const CUtensorMap* map, int c0, int c1) {
+        if constexpr (CG == 1) tma_load_2d(dst, map, bar, c0, c1);
+        else tma_load_2d_cg2(dst, map, bar, c0, c1);
+    };
+    constexpr int BC = Cfg<CG>::B_COLS;
+    const int nb = ti.n0 + BC * (int)rank;  // this CTA's first B column of the tile
     if constexpr (KIND == GemmKind::FwdGateUp) {
-        tma_load_2d(sA, &p.mapA, bar, k0, ti.m0);
+        ld(sA, &p.mapA, k0, m_own);
         const int row = ti.e * p.H + k0;
         const int n0 = ti.n0 / 2;  // 128 gate columns + 128 up columns per tile
-        tma_load_2d(sB + 0 * 8192, &p.mapB0, bar, n0, row);
-        tma_load_2d(sB + 1 * 8192, &p.mapB0, bar, n0 + 64, row);
-        tma_load_2d(sB + 2 * 8192, &p.mapB1, bar, n0, row);
-        tma_load_2d(sB + 3 * 8192, &p.mapB1, bar, n0 + 64, row);
+        if (CG == 1 || rank == 0) {
+            ld(sB + 0 * 8192, &p.mapB0, n0, row);
+            ld(sB + 1 * 8192, &p.mapB0, n0 + 64, row);
+        }
+        if (CG == 1 || rank == 1) {
+            const uint32_t o = CG == 1 ? 2 * 8192 : 0;
+            ld(sB + o, &p.mapB1, n0, row);
+            ld(sB + o + 8192, &p.mapB1, n0 + 64, row);
+        }
     } else if constexpr (KIND == GemmKind::FwdDown) {
-        tma_load_2d(sA, &p.mapA, bar, k0, ti.m0);
+        ld(sA, &p.mapA, k0, m_own);
         const int row = ti.e * p.I + k0;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tma_load_2d(sB + c * 8192, &p.mapB0, bar, ti.n0 + 64 * c, row);
+        for (int c = 0; c < BC / 64; ++c) ld(sB + c * 8192, &p.mapB0, nb + 64 * c, row);
     } else if constexpr (KIND == GemmKind::BwdDownDgrad) {
-        tma_load_2d(sA, &p.mapA, bar, k0, ti.m0);
-        tma_load_2d(sB, &p.mapB0, bar, k0, ti.e * p.I + ti.n0);
+        ld(sA, &p.mapA, k0, m_own);
+        ld(sB, &p.mapB0, k0, ti.e * p.I + nb);
     } else if constexpr (KIND == GemmKind::BwdDx) {
-        tma_load_2d(sA, &p.mapA, bar, k0, ti.m0);
-        if (k0 < p.I) tma_load_2d(sB, &p.mapB0, bar, k0, ti.e * p.H + ti.n0);
-        else tma_load_2d(sB, &p.mapB1, bar, k0 - p.I, ti.e * p.H + ti.n0);
+        ld(sA, &p.mapA, k0, m_own);
+        if (k0 < p.I) ld(sB, &p.mapB0, k0, ti.e * p.H + nb);
+        else ld(sB, &p.mapB1, k0 - p.I, ti.e * p.H + nb);
+    } else if constexpr (KIND == GemmKind::RouterDx) {
+        ld(sA, &p.mapA, k0, ti.m0);
+        ld(sB, &p.mapB0, k0, ti.n0);
+    } else if constexpr (KIND == GemmKind::RouterDw) {
+        const int row = ti.krow0 + k0;
+        ld(sA + 0, &p.mapA, ti.m0, row);
+        ld(sA + 8192, &p.mapA, ti.m0 + 64, row);
+        for (int c = 0; c < p.b_chunks; ++c) ld(sB + c * 8192, &p.mapB0, 64 * c, row);
     } else {  // wgrad: K runs over the expert's rows; both operands MN-major
         const int row = ti.krow0 + k0;
-        tma_load_2d(sA + 0, &p.mapA, bar, ti.m0, row);
-        tma_load_2d(sA + 8192, &p.mapA, bar, ti.m0 + 64, row);
+        ld(sA + 0, &p.mapA, m_own, row);
+        ld(sA + 8192, &p.mapA, m_own + 64, row);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tma_load_2d(sB + c * 8192, &p.mapB0, bar, ti.n0 + 64 * c, row);
+        for (int c = 0; c < BC / 64; ++c) ld(sB + c * 8192, &p.mapB0, nb + 64 * c, row);
     }
 }
 
@@ -376,6 +486,85 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const TileInfo& t
             store_row32(p.out0 + row * 2 * p.I + col, dgv, valid);
             store_row32(p.out0 + row * 2 * p.I + p.I + col, duv, valid);
         }
+    } else if constexpr (KIND == GemmKind::RouterDx) {
+        // dx[t] = (sum of t's expert rows of dXperm, slot order | base[t]) + router term
+        // (moe.hpp:418-427 scatter-add + 454 matmul_nt); rows beyond S only drain TMEM
+        const int t = ti.m0 + row_in_tile;
+        const bool row_ok = t < p.S;
+        int j0 = 0, j1 = 0;
+        if (row_ok && p.cec) {
+            j0 = p.cec[t];
+            j1 = p.cec[t + 1];
+        }
+#pragma unroll 1
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+            tmem_ld32(tacc + c, r);
+            tmem_wait_ld();
+            const int col = ti.n0 + c;
+            const int valid = p.H - col;
+            if (!row_ok || valid <= 0) continue;
+            float base[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) base[j] = 0.f;
+            if (p.cec) {
+                for (int j = j0; j < j1; ++j) {
+                    const __nv_bfloat16* sp = p.src + (int64_t)p.slot_prow[j] * p.H + col;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(sp) + q);
+                        const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            base[8 * q + 2 * h] += bf16_lo(w[h]);
+                            base[8 * q + 2 * h + 1] += bf16_hi(w[h]);
+                        }
+                    }
+                }
+            } else {
+                const __nv_bfloat16* sp = p.src + (int64_t)t * p.H + col;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(sp) + q);
+                    const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        base[8 * q + 2 * h] = bf16_lo(w[h]);
+                        base[8 * q + 2 * h + 1] = bf16_hi(w[h]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = base[j] + __uint_as_float(r[j]);
+            store_row32(p.out0 + (int64_t)t * p.H + col, v, valid);
+        }
+    } else if constexpr (KIND == GemmKind::RouterDw) {
+        // fp32 partial of dWr for this S split; half 0 covers all umma_n columns
+        if (half != 0) return;
+        const int h = ti.m0 + row_in_tile;
+        const bool row_ok = h < p.H;
+#pragma unroll 1
+        for (int c = 0; c < p.umma_n; c += 32) {
+            if (!zero) {
+                tmem_ld32(tacc + c, r);
+                tmem_wait_ld();
+            }
+            if (!row_ok) continue;
+            float* dst = p.part + ((int64_t)ti.e * p.H + h) * p.N + c;
+            const int valid = min(32, p.N - c);
+            if (valid <= 0) continue;
+            if (valid == 32 && (p.N % 4) == 0) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    reinterpret_cast<float4*>(dst)[q] =
+                        zero ? make_float4(0.f, 0.f, 0.f, 0.f)
+                             : make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                           __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (j < valid) dst[j] = zero ? 0.f : __uint_as_float(r[j]);
+            }
+        }
     } else {  // weight gradients: out[e][m][n] * scale
         // tcgen05.ld is warp-collective: every lane loads, only in-range rows store
         const int m = ti.m0 + row_in_tile;
@@ -409,21 +598,25 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const TileInfo& t
     }
 }
 
-template <GemmKind KIND>
+template <GemmKind KIND, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __grid_constant__ Params p) {
+    using C = Cfg<CG>;
+    constexpr int STAGES = C::STAGES;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* gbase = smem_raw + (base - raw);
-    const uint32_t bar0 = base + STAGES * STAGE_BYTES;
+    const uint32_t bar0 = base + STAGES * C::STAGE_BYTES;
     // barrier layout: full[S], empty[S], tfull[2], tempty[2], then the TMEM address slot
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
     auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
     auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + a); };
     auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + 2 + a); };
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + STAGES * STAGE_BYTES + 8 * (2 * STAGES + 4));
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + STAGES * C::STAGE_BYTES + 8 * (2 * STAGES + 4));
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+    const bool leader = rank == 0;
     if (warp == 0 && lane == 0) {
         prefetch_map(&p.mapA);
         prefetch_map(&p.mapB0);
@@ -434,37 +627,49 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull_bar(a), 1);
-            mbar_init(tempty_bar(a), NUM_EPI_WARPS);
+            mbar_init(tempty_bar(a), NUM_EPI_WARPS * CG);  // the leader's counts both CTAs' epilogues
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if constexpr (CG == 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before any remote arrive
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     const int32_t* ps = p.pad_start;
-    const int ntiles = total_tiles<KIND>(p, ps);
-    constexpr uint32_t idesc = umma_idesc(Traits<KIND>::a_mn, Traits<KIND>::b_mn);
+    const int ntiles = total_tiles<KIND, CG>(p, ps);
+    const uint32_t idesc = p.idesc;
+    const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;  // tile scheduler over CTA pairs
 
     if (warp == 0) {
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                const TileInfo ti = tile_info<KIND>(p, ps, t);
+            for (int t = unit; t < ntiles; t += nunits) {
+                const TileInfo ti = tile_info<KIND, CG>(p, ps, t);
+                const int m_own = ti.m0 + BM * (int)rank;
                 for (int kb = 0; kb < ti.kb; ++kb) {
                     mbar_wait(empty_bar(stage), phase ^ 1u);
-                    const uint32_t sA = base + stage * STAGE_BYTES, sB = sA + A_BYTES;
-                    mbar_expect_tx(full_bar(stage), STAGE_BYTES);
-                    load_stage<KIND>(p, ti, kb, sA, sB, full_bar(stage));
+                    const uint32_t sA = base + stage * C::STAGE_BYTES, sB = sA + A_BYTES;
+                    uint32_t fb = full_bar(stage);
+                    if constexpr (CG == 2) fb = map_to_rank(fb, 0);
+                    if (leader) mbar_expect_tx(full_bar(stage), p.stage_tx);
+                    load_stage<KIND, CG>(p, ti, kb, m_own, rank, sA, sB, fb);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1u;
@@ -473,12 +678,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (lane == 0 && leader) {
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-                const TileInfo ti = tile_info<KIND>(p, ps, t);
+            for (int t = unit; t < ntiles; t += nunits, ++it) {
+                const TileInfo ti = tile_info<KIND, CG>(p, ps, t);
                 const int acc = it & 1;
                 const uint32_t acc_phase = (it >> 1) & 1;
                 mbar_wait(tempty_bar(acc), acc_phase ^ 1u);
@@ -487,7 +692,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                 for (int kb = 0; kb < ti.kb; ++kb) {
                     mbar_wait(full_bar(stage), phase);
                     tc_fence_after();
-                    const uint32_t sA = base + stage * STAGE_BYTES, sB = sA + A_BYTES;
+                    const uint32_t sA = base + stage * C::STAGE_BYTES, sB = sA + A_BYTES;
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k) {
                         uint64_t ad, bd;
@@ -495,24 +700,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                         else ad = umma_desc(sA + k * 32, 16, 1024);
                         if (Traits<KIND>::b_mn) bd = umma_desc(sB + k * 2048, 8192, 1024);
                         else bd = umma_desc(sB + k * 32, 16, 1024);
-                        umma_f16(tacc, ad, bd, idesc, (kb | k) ? 1u : 0u);
+                        if constexpr (CG == 1) umma_f16(tacc, ad, bd, idesc, (kb | k) ? 1u : 0u);
+                        else umma_f16_cg2(tacc, ad, bd, idesc, (kb | k) ? 1u : 0u);
                     }
-                    umma_commit(empty_bar(stage));
+                    if constexpr (CG == 1) umma_commit(empty_bar(stage));
+                    else umma_commit_cg2(empty_bar(stage));
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1u;
                     }
                 }
-                if (ti.kb > 0) umma_commit(tfull_bar(acc));
-                else mbar_arrive(tfull_bar(acc));
+                if (ti.kb > 0) {
+                    if constexpr (CG == 1) umma_commit(tfull_bar(acc));
+                    else umma_commit_cg2(tfull_bar(acc));
+                } else {  // empty K range: nothing to wait for, the epilogues store zeros
+                    mbar_arrive(tfull_bar(acc));
+                    if constexpr (CG == 2) mbar_arrive_cluster(map_to_rank(tfull_bar(acc), 1));
+                }
             }
         }
     } else if (warp >= 4) {
         const int quad = warp % 4;        // TMEM lanes 32*quad .. 32*quad+31 (hardware rule: warp id % 4)
         const int half = (warp - 4) / 4;  // column half of the tile
+        const uint32_t tempty0 = CG == 2 ? map_to_rank(tempty_bar(0), 0) : tempty_bar(0);
         int it = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-            const TileInfo ti = tile_info<KIND>(p, ps, t);
+        for (int t = unit; t < ntiles; t += nunits, ++it) {
+            TileInfo ti = tile_info<KIND, CG>(p, ps, t);
+            ti.m0 += BM * (int)rank;  // this CTA's 128 rows of the pair's tile
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             mbar_wait(tfull_bar(acc), acc_phase);
@@ -521,15 +735,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
             epilogue_tile<KIND>(p, ti, tacc, 32 * quad + lane, ti.kb == 0, half);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(tempty_bar(acc));
+            if (lane == 0) {
+                if constexpr (CG == 1) mbar_arrive(tempty_bar(acc));
+                else mbar_arrive_cluster(tempty0 + 8u * acc);
+            }
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();
+    else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
-                     : "memory");
+        if constexpr (CG == 1)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                         : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                         : "memory");
     }
 }
 
@@ -563,18 +785,37 @@ static CUtensorMap make_map(const void* ptr, int64_t cols, int64_t rows, int bc,
     return m;
 }
 
-template <GemmKind KIND>
+template <GemmKind KIND, int CG>
 static void launch_kind(const Params& p, int grid, cudaStream_t st) {
     static std::once_flag once;
     std::call_once(once, [] {
-        B2_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        B2_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<KIND, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      SMEM_BYTES));
     });
-    grouped_gemm_kernel<KIND><<<grid, NUM_THREADS, SMEM_BYTES, st>>>(p);
-    B2_LAUNCH_CHECK();
+    grid = std::max(CG, grid / CG * CG);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    B2_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<KIND, CG>, p));
 }
 
 }  // namespace sm100
+
+int router_dw_splits(int64_t S, int64_t H, int num_sms) {
+    const int64_t mt = ceil_div(H, sm100::BM);
+    const int64_t want = std::max<int64_t>(1, (num_sms > 0 ? num_sms : 148) / mt);
+    const int64_t max_by_rows = std::max<int64_t>(1, ceil_div(std::max<int64_t>(S, 1), 256));
+    return (int)std::min<int64_t>(std::min<int64_t>(want, max_by_rows), kRouterDwMaxSplits);
+}
 
 bool sm100_available() {
     int dev = 0, major = 0, minor = 0;
@@ -603,6 +844,32 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
     p.out2 = (__nv_bfloat16*)a.out2;
     const int64_t P = a.pmax, H = a.H, I = a.I, nr = a.nr;
     int grid = a.num_sms > 0 ? a.num_sms : 148;
+    p.umma_n = BN;
+    p.b_chunks = 4;
+    p.S = a.S;
+    p.N = a.N;
+    p.counts = a.counts;
+    // the six expert GEMMs run as 256 x 256 tiles on CTA pairs (cta_group::2)
+    constexpr int G = 2;
+    using C2 = Cfg<G>;
+    p.stage_tx = G * C2::STAGE_BYTES;
+    switch (a.kind) {
+        case GemmKind::FwdGateUp:
+        case GemmKind::FwdDown:
+            p.idesc = umma_idesc(false, true, BN, BM * G);
+            break;
+        case GemmKind::BwdDownDgrad:
+        case GemmKind::BwdDx:
+            p.idesc = umma_idesc(false, false, BN, BM * G);
+            break;
+        case GemmKind::RouterDx:
+            p.idesc = umma_idesc(false, false);
+            p.stage_tx = Cfg<1>::STAGE_BYTES;
+            break;
+        default:
+            p.idesc = umma_idesc(true, true, BN, BM * G);
+            break;
+    }
     switch (a.kind) {
         case GemmKind::FwdGateUp:
             p.mapA = make_map(a.x, H, P, 64, BM);
@@ -610,8 +877,7 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.mapB1 = make_map(a.wu, I, nr * H, 64, 64);
             p.n_tiles = (int)ceil_div(I, BN / 2);
             p.num_kb_fixed = (int)ceil_div(H, BK);
-            p.mapB1 = p.mapB1;
-            launch_kind<GemmKind::FwdGateUp>(p, grid, st);
+            launch_kind<GemmKind::FwdGateUp, G>(p, grid, st);
             break;
         case GemmKind::FwdDown:
             p.mapA = make_map(a.h, I, P, 64, BM);
@@ -619,42 +885,80 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.mapB1 = p.mapB0;
             p.n_tiles = (int)ceil_div(H, BN);
             p.num_kb_fixed = (int)ceil_div(I, BK);
-            launch_kind<GemmKind::FwdDown>(p, grid, st);
+            launch_kind<GemmKind::FwdDown, G>(p, grid, st);
             break;
         case GemmKind::BwdDownDgrad:
             p.mapA = make_map(a.dy, H, P, 64, BM);
-            p.mapB0 = make_map(a.wd, H, nr * I, 64, BN);
+            p.mapB0 = make_map(a.wd, H, nr * I, 64, C2::B_COLS);
             p.mapB1 = p.mapB0;
             p.n_tiles = (int)ceil_div(I, BN);
             p.num_kb_fixed = (int)ceil_div(H, BK);
-            launch_kind<GemmKind::BwdDownDgrad>(p, grid, st);
+            launch_kind<GemmKind::BwdDownDgrad, G>(p, grid, st);
             break;
         case GemmKind::BwdDx:
             p.mapA = make_map(a.dgu, 2 * I, P, 64, BM);
-            p.mapB0 = make_map(a.wg, I, nr * H, 64, BN);
-            p.mapB1 = make_map(a.wu, I, nr * H, 64, BN);
+            p.mapB0 = make_map(a.wg, I, nr * H, 64, C2::B_COLS);
+            p.mapB1 = make_map(a.wu, I, nr * H, 64, C2::B_COLS);
             p.n_tiles = (int)ceil_div(H, BN);
             p.num_kb_fixed = (int)ceil_div(2 * I, BK);
-            launch_kind<GemmKind::BwdDx>(p, grid, st);
+            launch_kind<GemmKind::BwdDx, G>(p, grid, st);
             break;
         case GemmKind::WgradDown:
+            check(a.counts != nullptr, "wgrad: expert row counts required");
             p.mapA = make_map(a.h, I, P, 64, 64);
             p.mapB0 = make_map(a.dy, H, P, 64, 64);
             p.mapB1 = p.mapB0;
-            p.m_tiles_fixed = (int)ceil_div(I, BM);
+            p.m_tiles_fixed = (int)ceil_div(I, BM * G);
             p.n_tiles = (int)ceil_div(H, BN);
-            grid = (int)std::min<int64_t>(grid, nr * p.m_tiles_fixed * p.n_tiles);
-            launch_kind<GemmKind::WgradDown>(p, grid, st);
+            grid = (int)std::min<int64_t>(grid, G * nr * p.m_tiles_fixed * p.n_tiles);
+            launch_kind<GemmKind::WgradDown, G>(p, grid, st);
             break;
         case GemmKind::WgradGateUp:
+            check(a.counts != nullptr, "wgrad: expert row counts required");
             p.mapA = make_map(a.x, H, P, 64, 64);
             p.mapB0 = make_map(a.dgu, 2 * I, P, 64, 64);
             p.mapB1 = p.mapB0;
-            p.m_tiles_fixed = (int)ceil_div(H, BM);
+            p.m_tiles_fixed = (int)ceil_div(H, BM * G);
             p.n_tiles = (int)ceil_div(2 * I, BN);
-            grid = (int)std::min<int64_t>(grid, nr * p.m_tiles_fixed * p.n_tiles);
-            launch_kind<GemmKind::WgradGateUp>(p, grid, st);
+            grid = (int)std::min<int64_t>(grid, G * nr * p.m_tiles_fixed * p.n_tiles);
+            launch_kind<GemmKind::WgradGateUp, G>(p, grid, st);
             break;
+        case GemmKind::RouterDx: {
+            check(a.N % 8 == 0 && a.N <= 256, "router dx GEMM: n_experts must be a multiple of 8, <= 256");
+            const int64_t S = a.S;
+            if (S <= 0) return;
+            p.mapA = make_map(a.dl, a.N, S, 64, BM);
+            p.mapB0 = make_map(a.wr, a.N, H, 64, BN);
+            p.mapB1 = p.mapB0;
+            p.n_tiles = (int)ceil_div(H, BN);
+            p.num_kb_fixed = (int)ceil_div(a.N, BK);
+            p.cec = a.cec;
+            p.slot_prow = a.slot_prow;
+            p.src = (const __nv_bfloat16*)a.src;
+            grid = (int)std::min<int64_t>(grid, ceil_div(S, BM) * p.n_tiles);
+            launch_kind<GemmKind::RouterDx, 1>(p, grid, st);
+            break;
+        }
+        case GemmKind::RouterDw: {
+            check(a.N % 8 == 0 && a.N <= 256, "router dW GEMM: n_experts must be a multiple of 8, <= 256");
+            const int64_t S = a.S;
+            p.umma_n = (int)round_up(a.N, 16);
+            p.idesc = umma_idesc(true, true, p.umma_n);
+            p.b_chunks = (int)ceil_div(a.N, 64);
+            p.stage_tx = A_BYTES + 8192u * p.b_chunks;
+            p.mapA = make_map(a.x, H, std::max<int64_t>(S, 1), 64, 64);
+            p.mapB0 = make_map(a.dl, a.N, std::max<int64_t>(S, 1), 64, 64);
+            p.mapB1 = p.mapB0;
+            p.m_tiles_fixed = (int)ceil_div(H, BM);
+            p.n_tiles = 1;
+            const int nsplit = router_dw_splits(S, H, a.num_sms);
+            p.rows_per_split = (int)round_up(ceil_div(std::max<int64_t>(S, 1), nsplit), BK);
+            p.nr = nsplit;  // tiles = nsplit * m_tiles
+            p.part = a.part;
+            grid = (int)std::min<int64_t>(grid, (int64_t)nsplit * p.m_tiles_fixed);
+            launch_kind<GemmKind::RouterDw, 1>(p, grid, st);
+            break;
+        }
     }
 }
 

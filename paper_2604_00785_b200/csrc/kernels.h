@@ -14,16 +14,18 @@ void launch_softmax_topk(const float* logits, float* probs, float* topw, int32_t
 void launch_fur_route(float* w, int32_t* idx, int S, int N, int K, cudaStream_t st);
 void launch_aux_stats(const float* probs, int S, int N, const int32_t* gidx, int64_t n_gidx, float* partial,
                       float* mean_probs, int32_t* sel, cudaStream_t st);
+// dl_bf16 (optional): a bf16 copy of dlogits for the tensor-core router GEMMs
 void launch_router_dlogits(const float* probs, const float* wgrad, const int32_t* topi, const float* topw,
-                           const float* aux_grad, float* dlogits, int S, int N, int K, bool normalize, bool fur,
-                           cudaStream_t st);
+                           const float* aux_grad, float* dlogits, void* dl_bf16, int S, int N, int K, bool normalize,
+                           bool fur, cudaStream_t st);
 void launch_aux_probs_grad(const int32_t* sel, float* out, int S, int N, double coeff, double total,
                            cudaStream_t st);
 // dWr = x^T dlogits with a deterministic split over S; part holds max_splits*H*N floats
-constexpr int kRouterDwMaxSplits = 32;
 template <typename T>
 void launch_router_dw(const T* x, const float* dlogits, T* dw, float* part, int max_splits, int S, int H, int N,
                       cudaStream_t st);
+
+constexpr int kRouterDwMaxSplits = 32;
 
 // ---- counting / index generation (index.cu) ----
 struct RoutingIndexArgs {
@@ -98,12 +100,15 @@ enum class GemmKind : int {
     BwdDx = 3,       // dX = [dG|dU] · [Wg|Wu]ᵀ   (K = 2I)
     WgradDown = 4,   // dWd[e] = Hᵀ · dY  over the rows of e
     WgradGateUp = 5, // [dWg|dWu][e] = Xᵀ · [dG|dU]
+    RouterDx = 6,    // dx = (Σ_slots dXperm | base) + dlogits · Wrᵀ   (M = S, K = N experts)
+    RouterDw = 7,    // dWr partials [split][H][N] = x[rows of split]ᵀ · dlogits (split-K over S)
 };
 struct Sm100GemmArgs {
     GemmKind kind;
     int H, I, nr;              // layer dims, local experts
     int64_t pmax;              // padded row capacity
     const int32_t* pad_start;  // [nr+1] device
+    const int32_t* counts;     // [nr] device rows per expert (wgrad kinds)
     // operands (bf16), meaning depends on kind
     const void* x;      // mlp_in [P, H]
     const void* wg;     // [nr, H, I]
@@ -119,8 +124,21 @@ struct Sm100GemmArgs {
     void* out2;
     float scale;        // wgrad: 1/EP
     int num_sms;
+    // router kinds
+    int S, N;                    // local tokens, experts
+    const void* wr;              // router weight [H, N] bf16
+    const void* dl;              // dlogits [S, N] bf16
+    const int32_t* cec;          // RouterDx: cum_expert_counts [S+1] (null: add `base` rows instead)
+    const int32_t* slot_prow;    // RouterDx: slot -> padded row of dXperm
+    const void* src;             // RouterDx: dXperm [P, H] (slots) or base [S, H]
+    float* part;                 // RouterDw: fp32 partials [nsplit][H][N]
+    int nsplit_out;              // RouterDw: number of S splits used (set by the launcher)
 };
 void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st);
+// number of S splits the RouterDw kind uses (its partial buffer holds splits*H*N floats)
+int router_dw_splits(int64_t S, int64_t H, int num_sms);
+// sums RouterDw partials in split order into dW (T = bf16)
+void launch_router_dw_reduce_bf16(const float* part, void* dw, int nsplit, int64_t n, cudaStream_t st);
 bool sm100_available();
 
 // ---- optimizer (adamw.cu) ----

@@ -75,6 +75,7 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     for (int64_t n : {pmax_ * H, pmax_ * I, pmax_ * I, pmax_ * I, pmax_ * H, pmax_ * H, pmax_ * I, pmax_ * 2 * I,
                       pmax_ * H})
         acc(es * (size_t)std::max<int64_t>(n, 1));
+    acc(2 * (size_t)std::max<int64_t>(smax_ * N, 1));
     B2_CUDA(cudaSetDevice(ctx_.device));
     arena_.reserve(bytes);
     logits_ = arena_.take<float>(smax_ * N);
@@ -113,6 +114,7 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     dh_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
     dgu_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * 2 * I, 1));
     dxp_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
+    dl_bf16_ = arena_.take_bytes(2 * (size_t)std::max<int64_t>(smax_ * N, 1));
     B2_CUDA(cudaMemsetAsync(err_, 0, 4, ctx_.stream));
     B2_CUDA(cudaMemsetAsync(pad_start_, 0, 4 * (nr + 1), ctx_.stream));
 }
@@ -245,6 +247,7 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
         ga.nr = nr;
         ga.pmax = pmax_;
         ga.pad_start = pad_start_;
+        ga.counts = token_counts_;
         ga.num_sms = ctx_.num_sms;
         ga.kind = GemmKind::FwdGateUp;
         ga.x = mlp_in_;
@@ -350,6 +353,7 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         ga.nr = nr;
         ga.pmax = pmax_;
         ga.pad_start = pad_start_;
+        ga.counts = token_counts_;
         ga.num_sms = ctx_.num_sms;
         ga.x = mlp_in_;
         ga.wg = gate;
@@ -466,13 +470,42 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
     }
     // router path (431-454): EP = 1, so weights_grad_local == the full weights grad
     mark(kRouterBwd, false);
-    launch_router_dlogits(probs_, wgrad_, topi_, topw_, aux_probs_grad, dlogits_, S, N, K, cfg_.normalize_topk, fur_,
-                          st);
-    launch_router_dw<T>((const T*)x_, dlogits_, drouter, dw_part_, kRouterDwMaxSplits, S, H, N, st);
-    launches_ += 1;
-    // scatter-add to tokens (418-423) + matmul_nt(dlogits, router) (454)
-    launch_dx_finalize<T>((const T*)dxp_, true, slot_prow_, cec_, dlogits_, router, dx, S, H, N, st);
-    launches_ += 3;
+    const bool tc_router = dtype_ == BF16 && N % 8 == 0 && N <= 256;
+    launch_router_dlogits(probs_, wgrad_, topi_, topw_, aux_probs_grad, dlogits_, tc_router ? dl_bf16_ : nullptr, S,
+                          N, K, cfg_.normalize_topk, fur_, st);
+    if (tc_router) {
+        // router dW and dx on the tensor cores (bf16 dlogits, fp32 accumulation)
+        Sm100GemmArgs ga{};
+        ga.H = H;
+        ga.I = I;
+        ga.nr = 1;
+        ga.pmax = pmax_;
+        ga.pad_start = pad_start_;
+        ga.num_sms = ctx_.num_sms;
+        ga.S = S;
+        ga.N = N;
+        ga.x = x_;
+        ga.dl = dl_bf16_;
+        ga.wr = router;
+        ga.part = dw_part_;
+        ga.kind = GemmKind::RouterDw;
+        launch_sm100_gemm(ga, st);
+        launch_router_dw_reduce_bf16(dw_part_, drouter, router_dw_splits(S, H, ctx_.num_sms), (int64_t)H * N, st);
+        // scatter-add to tokens (418-423), then + matmul_nt(dlogits, router) (454) as a GEMM whose
+        // epilogue adds the scattered rows
+        launch_combine<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, dx, S, H, K, st);
+        ga.kind = GemmKind::RouterDx;
+        ga.cec = nullptr;
+        ga.src = dx;
+        ga.out0 = dx;
+        launch_sm100_gemm(ga, st);
+        launches_ += 5;
+    } else {
+        launch_router_dw<T>((const T*)x_, dlogits_, drouter, dw_part_, kRouterDwMaxSplits, S, H, N, st);
+        // scatter-add to tokens (418-423) + matmul_nt(dlogits, router) (454)
+        launch_dx_finalize<T>((const T*)dxp_, true, slot_prow_, cec_, dlogits_, router, dx, S, H, N, st);
+        launches_ += 4;
+    }
     mark(kRouterBwd, true);
 }
 

@@ -129,6 +129,7 @@ class MoeLayer {
     const int32_t* gi_ = nullptr;  // dispatch indices
     // dtype buffers (padded row space)
     void *mlp_in_, *g_, *u_, *h_, *y_, *dy_, *dh_, *dgu_, *dxp_;
+    void* dl_bf16_ = nullptr;  // bf16 dlogits for the tensor-core router GEMMs
 };
 
 }  // namespace b2

@@ -121,10 +121,15 @@ __global__ void combine_kernel(const T* __restrict__ y, const int32_t* __restric
 #pragma unroll
             for (int q = 0; q < V; ++q) acc[q] = 0.f;
             for (int j = j0; j < j1; ++j) {
-                const float wv = gw[(int64_t)t * K + selected_k[j]];
                 V16<T>::load(y + (int64_t)slot_prow[j] * H + c0, v);
+                if (gw) {
+                    const float wv = gw[(int64_t)t * K + selected_k[j]];
 #pragma unroll
-                for (int q = 0; q < V; ++q) acc[q] = __fadd_rn(acc[q], __fmul_rn(wv, v[q]));
+                    for (int q = 0; q < V; ++q) acc[q] = __fadd_rn(acc[q], __fmul_rn(wv, v[q]));
+                } else {  // unweighted: the scatter-add of dX rows to their token (moe.hpp:418-423)
+#pragma unroll
+                    for (int q = 0; q < V; ++q) acc[q] = __fadd_rn(acc[q], v[q]);
+                }
             }
             V16<T>::store(out + (int64_t)t * H + c0, acc);
         }
@@ -133,7 +138,7 @@ __global__ void combine_kernel(const T* __restrict__ y, const int32_t* __restric
     for (int c0 = lane * 4; c0 < H; c0 += 128) {
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         for (int j = j0; j < j1; ++j) {
-            const float wv = gw[(int64_t)t * K + selected_k[j]];
+            const float wv = gw ? gw[(int64_t)t * K + selected_k[j]] : 1.f;
             const T* yr = y + (int64_t)slot_prow[j] * H;
 #pragma unroll
             for (int q = 0; q < 4; ++q)

@@ -26,87 +26,121 @@ constexpr int kRtTok = 64, kRtExp = 64, kRtP = 32, kRtXs = kRtTok + 4;
 template <typename T>
 __global__ void __launch_bounds__(128) router_logits_kernel(const T* __restrict__ x, const T* __restrict__ w,
                                                             float* __restrict__ logits, int S, int H, int N) {
-    __shared__ __align__(16) float xs[kRtP][kRtXs];
-    __shared__ __align__(16) float ws[kRtP][kRtExp];
+    __shared__ __align__(16) float xs[2][kRtP][kRtXs];
+    __shared__ __align__(16) float ws[2][kRtP][kRtExp];
     const int t0 = blockIdx.x * kRtTok, e0 = blockIdx.y * kRtExp;
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // 16 expert-quads x 8 token-octets
     constexpr int VX = 16 / sizeof(T);
+    constexpr int XV = kRtTok * kRtP / VX / 128;  // x vectors per thread per chunk
     const bool vec = (H % VX) == 0;
-    float acc[8][4];
+    float2 acc[8][2];  // packed pairs of experts: f32x2 FMA (sm_100), per-lane IEEE rounding
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-    for (int p0 = 0; p0 < H; p0 += kRtP) {
+        for (int j = 0; j < 2; ++j) acc[i][j] = make_float2(0.f, 0.f);
+    int4 xr[XV];
+    float wr[kRtP * kRtExp / 128];
+    // chunk loads into registers (issued one chunk ahead of the math)
+    auto load = [&](int p0) {
         if (vec) {
-            for (int v = threadIdx.x; v < kRtTok * kRtP / VX; v += 128) {
+#pragma unroll
+            for (int q = 0; q < XV; ++q) {
+                const int v = threadIdx.x + 128 * q;
                 const int tt = v / (kRtP / VX), pp = (v % (kRtP / VX)) * VX;
                 const int t = t0 + tt, p = p0 + pp;
-                float f[VX];
-                if (t < S && p < H) {
-                    const int4 raw = __ldg(reinterpret_cast<const int4*>(x + (int64_t)t * H + p));
-                    if constexpr (sizeof(T) == 2) {
-                        const uint32_t wv[4] = {(uint32_t)raw.x, (uint32_t)raw.y, (uint32_t)raw.z, (uint32_t)raw.w};
+                xr[q] = (t < S && p < H) ? __ldg(reinterpret_cast<const int4*>(x + (int64_t)t * H + p))
+                                         : make_int4(0, 0, 0, 0);
+            }
+        }
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            f[2 * q] = __uint_as_float(wv[q] << 16);
-                            f[2 * q + 1] = __uint_as_float(wv[q] & 0xFFFF0000u);
-                        }
-                    } else {
-                        f[0] = __int_as_float(raw.x);
-                        f[1] = __int_as_float(raw.y);
-                        f[2] = __int_as_float(raw.z);
-                        f[3] = __int_as_float(raw.w);
+        for (int q = 0; q < kRtP * kRtExp / 128; ++q) {
+            const int i = threadIdx.x + 128 * q;
+            const int pp = i / kRtExp, ee = i % kRtExp;
+            const int p = p0 + pp, e = e0 + ee;
+            wr[q] = (p < H && e < N) ? Elem<T>::load(w + (int64_t)p * N + e) : 0.f;
+        }
+    };
+    auto stash = [&](int buf, int p0) {
+        if (vec) {
+#pragma unroll
+            for (int q = 0; q < XV; ++q) {
+                const int v = threadIdx.x + 128 * q;
+                const int tt = v / (kRtP / VX), pp = (v % (kRtP / VX)) * VX;
+                float f[VX];
+                if constexpr (sizeof(T) == 2) {
+                    const uint32_t wv[4] = {(uint32_t)xr[q].x, (uint32_t)xr[q].y, (uint32_t)xr[q].z, (uint32_t)xr[q].w};
+#pragma unroll
+                    for (int z = 0; z < 4; ++z) {
+                        f[2 * z] = __uint_as_float(wv[z] << 16);
+                        f[2 * z + 1] = __uint_as_float(wv[z] & 0xFFFF0000u);
                     }
                 } else {
-#pragma unroll
-                    for (int q = 0; q < VX; ++q) f[q] = 0.f;
+                    f[0] = __int_as_float(xr[q].x);
+                    f[1] = __int_as_float(xr[q].y);
+                    f[2] = __int_as_float(xr[q].z);
+                    f[3] = __int_as_float(xr[q].w);
                 }
 #pragma unroll
-                for (int q = 0; q < VX; ++q) xs[pp + q][tt] = f[q];
+                for (int z = 0; z < VX; ++z) xs[buf][pp + z][tt] = f[z];
             }
         } else {
             for (int i = threadIdx.x; i < kRtTok * kRtP; i += 128) {
                 const int tt = i / kRtP, pp = i % kRtP;
                 const int t = t0 + tt, p = p0 + pp;
-                xs[pp][tt] = (t < S && p < H) ? Elem<T>::load(x + (int64_t)t * H + p) : 0.f;
+                xs[buf][pp][tt] = (t < S && p < H) ? Elem<T>::load(x + (int64_t)t * H + p) : 0.f;
             }
         }
-        for (int i = threadIdx.x; i < kRtP * kRtExp; i += 128) {
-            const int pp = i / kRtExp, ee = i % kRtExp;
-            const int p = p0 + pp, e = e0 + ee;
-            ws[pp][ee] = (p < H && e < N) ? Elem<T>::load(w + (int64_t)p * N + e) : 0.f;
+#pragma unroll
+        for (int q = 0; q < kRtP * kRtExp / 128; ++q) {
+            const int i = threadIdx.x + 128 * q;
+            ws[buf][i / kRtExp][i % kRtExp] = wr[q];
         }
-        __syncthreads();
+    };
+    load(0);
+    stash(0, 0);
+    __syncthreads();
+    int buf = 0;
+    for (int p0 = 0; p0 < H; p0 += kRtP) {
+        const bool more = p0 + kRtP < H;
+        if (more) load(p0 + kRtP);
         const int pend = min(kRtP, H - p0);
+#pragma unroll 8
         for (int pp = 0; pp < pend; ++pp) {
-            const float4 a0 = *reinterpret_cast<const float4*>(&xs[pp][ty * 8]);
-            const float4 a1 = *reinterpret_cast<const float4*>(&xs[pp][ty * 8 + 4]);
-            const float4 b4 = *reinterpret_cast<const float4*>(&ws[pp][tx * 4]);
+            const float4 a0 = *reinterpret_cast<const float4*>(&xs[buf][pp][ty * 8]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&xs[buf][pp][ty * 8 + 4]);
+            const float4 b4 = *reinterpret_cast<const float4*>(&ws[buf][pp][tx * 4]);
             const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float b[4] = {b4.x, b4.y, b4.z, b4.w};
+            const float2 b[2] = {make_float2(b4.x, b4.y), make_float2(b4.z, b4.w)};
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < 8; ++i) {
+                const float2 a2 = make_float2(a[i], a[i]);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    if constexpr (sizeof(T) == 2) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-                    else acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(a[i], b[j]));
+                for (int j = 0; j < 2; ++j) {
+                    if constexpr (sizeof(T) == 2) {
+                        acc[i][j] = __ffma2_rn(a2, b[j], acc[i][j]);
+                    } else {  // scalar _rn intrinsics are never contracted into an FMA
+                        acc[i][j].x = __fadd_rn(acc[i][j].x, __fmul_rn(a2.x, b[j].x));
+                        acc[i][j].y = __fadd_rn(acc[i][j].y, __fmul_rn(a2.y, b[j].y));
+                    }
                 }
+            }
         }
+        if (more) stash(buf ^ 1, p0 + kRtP);
         __syncthreads();
+        buf ^= 1;
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const int t = t0 + ty * 8 + i;
         if (t >= S) continue;
+        const float o[4] = {acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y};
         if (e0 + tx * 4 + 3 < N && (N % 4) == 0) {
-            *reinterpret_cast<float4*>(logits + (int64_t)t * N + e0 + tx * 4) =
-                make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+            *reinterpret_cast<float4*>(logits + (int64_t)t * N + e0 + tx * 4) = make_float4(o[0], o[1], o[2], o[3]);
         } else {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int e = e0 + tx * 4 + j;
-                if (e < N) logits[(int64_t)t * N + e] = acc[i][j];
+                if (e < N) logits[(int64_t)t * N + e] = o[j];
             }
         }
     }
@@ -248,8 +282,8 @@ __global__ void sel_count_kernel(const int32_t* __restrict__ idx, int64_t n, int
 __global__ void router_dlogits_kernel(const float* __restrict__ probs, const float* __restrict__ wgrad,
                                       const int32_t* __restrict__ topi, const float* __restrict__ topw,
                                       const float* __restrict__ aux_grad /*[S,N] or null*/,
-                                      float* __restrict__ dlogits, int S, int N, int K, int normalize,
-                                      int fur) {
+                                      float* __restrict__ dlogits, __nv_bfloat16* __restrict__ dl_bf16, int S,
+                                      int N, int K, int normalize, int fur) {
     const int row = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
     if (row >= S) return;
     float dp[kMaxExpertsPerLane], pr[kMaxExpertsPerLane];
@@ -292,7 +326,11 @@ __global__ void router_dlogits_kernel(const float* __restrict__ probs, const flo
 #pragma unroll
     for (int i = 0; i < kMaxExpertsPerLane; ++i) {
         const int j = lane + 32 * i;
-        if (j < N) dlogits[(int64_t)row * N + j] = (float)((double)pr[i] * ((double)dp[i] - dot));
+        if (j < N) {
+            const float v = (float)((double)pr[i] * ((double)dp[i] - dot));
+            dlogits[(int64_t)row * N + j] = v;
+            if (dl_bf16) dl_bf16[(int64_t)row * N + j] = __float2bfloat16_rn(v);
+        }
     }
 }
 
@@ -416,11 +454,12 @@ void launch_aux_stats(const float* probs, int S, int N, const int32_t* gidx, int
 }
 
 void launch_router_dlogits(const float* probs, const float* wgrad, const int32_t* topi, const float* topw,
-                           const float* aux_grad, float* dlogits, int S, int N, int K, bool normalize, bool fur,
-                           cudaStream_t st) {
+                           const float* aux_grad, float* dlogits, void* dl_bf16, int S, int N, int K, bool normalize,
+                           bool fur, cudaStream_t st) {
     if (S == 0) return;
-    router_dlogits_kernel<<<(unsigned)ceil_div(S, 8), 256, 0, st>>>(probs, wgrad, topi, topw, aux_grad, dlogits, S,
-                                                                      N, K, normalize ? 1 : 0, fur ? 1 : 0);
+    router_dlogits_kernel<<<(unsigned)ceil_div(S, 8), 256, 0, st>>>(probs, wgrad, topi, topw, aux_grad, dlogits,
+                                                                      (__nv_bfloat16*)dl_bf16, S, N, K,
+                                                                      normalize ? 1 : 0, fur ? 1 : 0);
     B2_LAUNCH_CHECK();
 }
 
@@ -446,6 +485,12 @@ void launch_router_dw(const T* x, const float* dlogits, T* dw, float* part, int 
     router_dw_reduce_kernel<T><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(part, dw, nsplit, n);
     B2_LAUNCH_CHECK();
 }
+void launch_router_dw_reduce_bf16(const float* part, void* dw, int nsplit, int64_t n, cudaStream_t st) {
+    if (n <= 0) return;
+    router_dw_reduce_kernel<__nv_bfloat16><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(part, (__nv_bfloat16*)dw, nsplit, n);
+    B2_LAUNCH_CHECK();
+}
+
 template void launch_router_dw<float>(const float*, const float*, float*, float*, int, int, int, int, cudaStream_t);
 template void launch_router_dw<__nv_bfloat16>(const __nv_bfloat16*, const float*, __nv_bfloat16*, float*, int, int,
                                               int, int, cudaStream_t);

@@ -21,7 +21,8 @@ def _lib():
     lb = b2.lib()
     fn = lb.b2x_grouped_gemm
     fn.restype = C.c_int
-    fn.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64] + [C.c_void_p] * 12 + [C.c_float]
+    fn.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int64] + \
+        [C.c_void_p] * 12 + [C.c_float]
     return b2, fn
 
 
@@ -41,15 +42,16 @@ def setup():
     b2, fn = _lib()
     ctx = b2.Context(0)
     torch.manual_seed(0)
-    counts = [200, 0, 77, 128]
+    counts = [200, 0, 77, 300, 256]
     nr = len(counts)
     H, I = 320, 192
     starts = [0]
     for c in counts:
-        starts.append(starts[-1] + (c + 127) // 128 * 128)
-    pmax = starts[-1] + 128
+        starts.append(starts[-1] + (c + 255) // 256 * 256)
+    pmax = starts[-1] + 256
     dev = "cuda"
     ps = torch.tensor(starts, dtype=torch.int32, device=dev)
+    cnt = torch.tensor(counts, dtype=torch.int32, device=dev)
     valid = torch.zeros(pmax, dtype=torch.bool, device=dev)
     for e, c in enumerate(counts):
         valid[starts[e]:starts[e] + c] = True
@@ -59,7 +61,8 @@ def setup():
         t[~valid] = 0
         return t.bfloat16()
 
-    d = dict(b2=b2, fn=fn, ctx=ctx, counts=counts, nr=nr, H=H, I=I, starts=starts, pmax=pmax, ps=ps, valid=valid)
+    d = dict(b2=b2, fn=fn, ctx=ctx, counts=counts, nr=nr, H=H, I=I, starts=starts, pmax=pmax, ps=ps, cnt=cnt,
+             valid=valid)
     d["x"] = rows((pmax, H))
     d["wg"] = (torch.randn(nr, H, I, device=dev) * 0.05).bfloat16()
     d["wu"] = (torch.randn(nr, H, I, device=dev) * 0.05).bfloat16()
@@ -73,7 +76,7 @@ def setup():
 
 
 def run(d, kind, out0, out1=None, out2=None, scale=1.0):
-    rc = d["fn"](d["ctx"].h, kind, d["H"], d["I"], d["nr"], _p(d["ps"]), d["pmax"], _p(d["x"]), _p(d["wg"]),
+    rc = d["fn"](d["ctx"].h, kind, d["H"], d["I"], d["nr"], _p(d["ps"]), _p(d["cnt"]), d["pmax"], _p(d["x"]), _p(d["wg"]),
                  _p(d["wu"]), _p(d["wd"]), _p(d["g"]), _p(d["u"]), _p(d["h"]), _p(d["dy"]), _p(d["dgu"]), _p(out0),
                  _p(out1), _p(out2), scale)
     assert rc == 0, d["b2"].lib().b2_last_error().decode()
