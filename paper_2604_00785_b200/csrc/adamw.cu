@@ -72,39 +72,66 @@ __global__ void adamw_kernel(float* __restrict__ master, float* __restrict__ mom
     }
 }
 
-// vectorised fast path: bf16 grads, bf16 weights, 4 elements per thread-iteration
-__global__ void adamw_bf16x4_kernel(float4* __restrict__ master, float4* __restrict__ mom, float4* __restrict__ vel,
-                                    const uint2* __restrict__ grad, uint2* __restrict__ wout, int64_t n4, AdamWDev c,
-                                    float grad_scale, const double* __restrict__ norm_sq, double clip_norm,
-                                    int clip_active) {
+// vectorised fast path: bf16 grads, bf16 weights; each thread-iteration handles two
+// groups of 4 elements with all 8 loads issued before the fp64 math (more bytes in flight)
+__device__ __forceinline__ void adamw_group4(float4& ms, float4& mv, float4& vv, uint2 gb, const AdamWDev& c,
+                                             float grad_scale, double clip, uint2& wout) {
+    float g[4] = {__uint_as_float(gb.x << 16), __uint_as_float(gb.x & 0xFFFF0000u), __uint_as_float(gb.y << 16),
+                  __uint_as_float(gb.y & 0xFFFF0000u)};
+    float* pm = &ms.x;
+    float* pv1 = &mv.x;
+    float* pv2 = &vv.x;
+    uint16_t wb[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        float gq = g[q];
+        if (grad_scale != 1.f) gq = __fmul_rn(gq, grad_scale);
+        if (clip != 1.0) gq = (float)__dmul_rn((double)gq, clip);
+        float wf;
+        adamw_elem(pm[q], pv1[q], pv2[q], gq, c, wf);
+        wb[q] = bf16_bits_rne(wf);
+    }
+    wout = make_uint2((uint32_t)wb[0] | ((uint32_t)wb[1] << 16), (uint32_t)wb[2] | ((uint32_t)wb[3] << 16));
+}
+
+__global__ void __launch_bounds__(256) adamw_bf16x4_kernel(float4* __restrict__ master, float4* __restrict__ mom,
+                                                           float4* __restrict__ vel, const uint2* __restrict__ grad,
+                                                           uint2* __restrict__ wout, int64_t n4, AdamWDev c,
+                                                           float grad_scale, const double* __restrict__ norm_sq,
+                                                           double clip_norm, int clip_active) {
     double clip = 1.0;
     if (norm_sq) {
         const double norm = sqrt(*norm_sq);
         if (clip_active && norm > clip_norm && norm > 0) clip = clip_norm / norm;
     }
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
-        const uint2 gb = __ldcs(grad + i);
-        float4 ms = __ldcs(master + i), mv = __ldcs(mom + i), vv = __ldcs(vel + i);
-        float g[4] = {__uint_as_float(gb.x << 16), __uint_as_float(gb.x & 0xFFFF0000u), __uint_as_float(gb.y << 16),
-                      __uint_as_float(gb.y & 0xFFFF0000u)};
-        float* pm = &ms.x;
-        float* pv1 = &mv.x;
-        float* pv2 = &vv.x;
-        uint16_t wb[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            float gq = g[q];
-            if (grad_scale != 1.f) gq = __fmul_rn(gq, grad_scale);
-            if (clip != 1.0) gq = (float)__dmul_rn((double)gq, clip);
-            float wf;
-            adamw_elem(pm[q], pv1[q], pv2[q], gq, c, wf);
-            wb[q] = bf16_bits_rne(wf);
-        }
-        __stcs(master + i, ms);
-        __stcs(mom + i, mv);
-        __stcs(vel + i, vv);
-        __stcs(wout + i, make_uint2((uint32_t)wb[0] | ((uint32_t)wb[1] << 16), (uint32_t)wb[2] | ((uint32_t)wb[3] << 16)));
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + stride < n4; i += 2 * stride) {
+        const int64_t j = i + stride;
+        const uint2 g0 = __ldcs(grad + i), g1 = __ldcs(grad + j);
+        float4 m0 = __ldcs(master + i), a0 = __ldcs(mom + i), v0 = __ldcs(vel + i);
+        float4 m1 = __ldcs(master + j), a1 = __ldcs(mom + j), v1 = __ldcs(vel + j);
+        uint2 w0, w1;
+        adamw_group4(m0, a0, v0, g0, c, grad_scale, clip, w0);
+        adamw_group4(m1, a1, v1, g1, c, grad_scale, clip, w1);
+        __stcs(master + i, m0);
+        __stcs(mom + i, a0);
+        __stcs(vel + i, v0);
+        __stcs(wout + i, w0);
+        __stcs(master + j, m1);
+        __stcs(mom + j, a1);
+        __stcs(vel + j, v1);
+        __stcs(wout + j, w1);
+    }
+    if (i < n4) {
+        const uint2 g0 = __ldcs(grad + i);
+        float4 m0 = __ldcs(master + i), a0 = __ldcs(mom + i), v0 = __ldcs(vel + i);
+        uint2 w0;
+        adamw_group4(m0, a0, v0, g0, c, grad_scale, clip, w0);
+        __stcs(master + i, m0);
+        __stcs(mom + i, a0);
+        __stcs(vel + i, v0);
+        __stcs(wout + i, w0);
     }
 }
 

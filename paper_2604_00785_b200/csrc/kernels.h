@@ -73,6 +73,18 @@ template <typename T>
 void launch_swiglu_bwd(const T* g, const T* u, const T* dh, T* dgu, const int32_t* p_total, int I, int64_t pmax,
                        cudaStream_t st);
 
+// ---- expert-parallel dispatch / combine (ep_dispatch.cu) ----
+void launch_dest_plan(const int32_t* gi, int S, int K, int E, int NR, int32_t* send_pos, int32_t* send_cnt,
+                      int32_t* send_off, cudaStream_t st);
+template <typename T>
+void launch_pack_rows(const T* x, const int32_t* send_pos, const int32_t* send_off, int S, int E, int H, T* send_x,
+                      const int32_t* gi, const float* gw, int K, int32_t* meta, cudaStream_t st);
+void launch_unpack_meta(const int32_t* meta, int64_t n, int K, int32_t* gi, float* gw, int32_t* src_t,
+                        cudaStream_t st);
+template <typename T>
+void launch_return_sum(const T* ret, const int32_t* send_pos, const int32_t* send_off, int S, int E, int W, T* out,
+                       cudaStream_t st);
+
 // ---- SIMT grouped GEMM (simt_gemm.cu) ----
 struct SimtGemmArgs {
     const void* A;

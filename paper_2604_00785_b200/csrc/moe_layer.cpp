@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstring>
 
+#include "comm.h"
 #include "kernels.h"
 
 namespace b2 {
@@ -57,7 +58,7 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     const int64_t nr = cfg_.experts_per_rank();
     smax_ = max_tokens;
     tmax_ = smax_ * cfg_.ep;  // gathered tokens (reference allgather semantics)
-    pmax_ = round_up(tmax_ * K + nr * (kRowAlign - 1), kRowAlign);
+    pmax_ = round_up(tmax_ * std::min<int64_t>(K, nr) + nr * (kRowAlign - 1), kRowAlign);
     thmax_ = ceil_div(std::max<int64_t>(tmax_, 1), cfg_.token_block);
     const int64_t nch = ceil_div(std::max<int64_t>(tmax_, 1), 64);
     const size_t es = dtype_size(dtype);
@@ -76,6 +77,16 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
                       pmax_ * H})
         acc(es * (size_t)std::max<int64_t>(n, 1));
     acc(2 * (size_t)std::max<int64_t>(smax_ * N, 1));
+    const int E = cfg_.ep;
+    const int64_t MW = 1 + 2 * K;
+    if (E > 1) {
+        for (int64_t n : {(int64_t)E * smax_, (int64_t)E, (int64_t)E, (int64_t)E, tmax_ * MW, tmax_ * MW, tmax_ * K,
+                          tmax_})
+            acc(4 * (size_t)std::max<int64_t>(n, 1));
+        for (int64_t n : {tmax_ * K, tmax_ * K, smax_ * K}) acc(4 * (size_t)std::max<int64_t>(n, 1));
+        for (int64_t n : {tmax_ * H, tmax_ * H, tmax_ * H, tmax_ * H, smax_ * H})
+            acc(es * (size_t)std::max<int64_t>(n, 1));
+    }
     B2_CUDA(cudaSetDevice(ctx_.device));
     arena_.reserve(bytes);
     logits_ = arena_.take<float>(smax_ * N);
@@ -115,6 +126,25 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     dgu_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * 2 * I, 1));
     dxp_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
     dl_bf16_ = arena_.take_bytes(2 * (size_t)std::max<int64_t>(smax_ * N, 1));
+    if (E > 1) {
+        check(ctx_.comm != nullptr && ctx_.comm->ep.size == E, "fast_moe: EP > 1 needs the EP communicator");
+        send_pos_ = arena_.take<int32_t>((int64_t)E * smax_);
+        send_cnt_d_ = arena_.take<int32_t>(E);
+        send_off_d_ = arena_.take<int32_t>(E);
+        recv_cnt_d_ = arena_.take<int32_t>(E);
+        meta_send_ = arena_.take<int32_t>(tmax_ * MW);
+        meta_recv_ = arena_.take<int32_t>(tmax_ * MW);
+        gi_recv_ = arena_.take<int32_t>(tmax_ * K);
+        src_t_ = arena_.take<int32_t>(tmax_);
+        gw_recv_ = arena_.take<float>(tmax_ * K);
+        wret_ = arena_.take<float>(tmax_ * K);
+        wgrad_local_ = arena_.take<float>(smax_ * K);
+        send_x_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(tmax_ * H, 1));
+        recv_x_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(tmax_ * H, 1));
+        comb_recv_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(tmax_ * H, 1));
+        ret_x_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(tmax_ * H, 1));
+        dx_exp_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(smax_ * H, 1));
+    }
     B2_CUDA(cudaMemsetAsync(err_, 0, 4, ctx_.stream));
     B2_CUDA(cudaMemsetAsync(pad_start_, 0, 4 * (nr + 1), ctx_.stream));
 }
@@ -165,10 +195,52 @@ void MoeLayer::stage_times(float* ms) {
     }
 }
 
+// rows travel forward (source -> expert owner, counts scnt/rcnt) or back (owner -> source)
+void MoeLayer::ep_exchange(const void* send, void* recv, size_t row_bytes, bool forward) {
+    const Group& g = ctx_.comm->ep;
+    if (forward) all_to_all_v(g, send, scnt_.data(), soff_.data(), recv, rcnt_.data(), roff_.data(), row_bytes, ctx_.stream);
+    else all_to_all_v(g, send, rcnt_.data(), roff_.data(), recv, scnt_.data(), soff_.data(), row_bytes, ctx_.stream);
+}
+
+// dispatch (replaces the allgathers of moe.hpp:365-367): plan, count exchange (one small
+// host sync: NCCL needs the row counts), pack, all-to-all of rows + routing metadata
+template <typename T>
+void MoeLayer::ep_dispatch(const T* x, const int32_t* gi_local, const float* gw_local) {
+    cudaStream_t st = ctx_.stream;
+    const int E = cfg_.ep, S = (int)s_, K = (int)cfg_.top_k, H = (int)cfg_.hidden, nr = (int)cfg_.experts_per_rank();
+    launch_dest_plan(gi_local, S, K, E, nr, send_pos_, send_cnt_d_, send_off_d_, st);
+    std::vector<int64_t> one(E, 1), idx(E);
+    for (int r = 0; r < E; ++r) idx[r] = r;
+    all_to_all_v(ctx_.comm->ep, send_cnt_d_, one.data(), idx.data(), recv_cnt_d_, one.data(), idx.data(), 4, st);
+    std::vector<int32_t> sc(E), so(E), rc(E);
+    B2_CUDA(cudaMemcpyAsync(sc.data(), send_cnt_d_, 4 * E, cudaMemcpyDeviceToHost, st));
+    B2_CUDA(cudaMemcpyAsync(so.data(), send_off_d_, 4 * E, cudaMemcpyDeviceToHost, st));
+    B2_CUDA(cudaMemcpyAsync(rc.data(), recv_cnt_d_, 4 * E, cudaMemcpyDeviceToHost, st));
+    B2_CUDA(cudaStreamSynchronize(st));
+    scnt_.assign(E, 0);
+    soff_.assign(E, 0);
+    rcnt_.assign(E, 0);
+    roff_.assign(E, 0);
+    int64_t acc = 0;
+    for (int r = 0; r < E; ++r) {
+        scnt_[r] = sc[r];
+        soff_[r] = so[r];
+        rcnt_[r] = rc[r];
+        roff_[r] = acc;
+        acc += rc[r];
+    }
+    t_recv_ = acc;
+    check(t_recv_ <= tmax_, "ep dispatch: received more tokens than the layer's capacity");
+    launch_pack_rows<T>(x, send_pos_, send_off_d_, S, E, H, (T*)send_x_, gi_local, gw_local, K, meta_send_, st);
+    ep_exchange(send_x_, recv_x_, sizeof(T) * (size_t)H, true);
+    ep_exchange(meta_send_, meta_recv_, 4 * (size_t)(1 + 2 * K), true);
+    launch_unpack_meta(meta_recv_, t_recv_, K, gi_recv_, gw_recv_, src_t_, st);
+    launches_ += 3;
+}
+
 void MoeLayer::forward(const void* x, const void* router, const void* gate, const void* up, const void* down,
                        int64_t s, bool fur, void* out) {
     check(s >= 0 && s <= smax_, "fast_moe: token count exceeds the layer's capacity");
-    check(ctx_.ep == 1, "fast_moe: EP > 1 runs through the expert-parallel dispatch (not in this build)");
     B2_CUDA(cudaSetDevice(ctx_.device));
     s_ = s;
     t_ = s * cfg_.ep;
@@ -189,8 +261,10 @@ void MoeLayer::forward(const void* x, const void* router, const void* gate, cons
 template <typename T>
 void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up, const T* down, bool fur, T* out) {
     cudaStream_t st = ctx_.stream;
-    const int S = (int)s_, Tt = (int)t_, N = (int)cfg_.n_experts, K = (int)cfg_.top_k, H = (int)cfg_.hidden,
+    const int E = cfg_.ep;
+    const int S = (int)s_, N = (int)cfg_.n_experts, K = (int)cfg_.top_k, H = (int)cfg_.hidden,
               I = (int)cfg_.intermediate, nr = (int)cfg_.experts_per_rank();
+    int Tt = S;  // rows of the (gathered) table this rank processes
     // stage 1: route locally (moe.hpp:357-364)
     mark(kRoute, false);
     launch_router_logits<T>(x, router, logits_, S, H, N, st);
@@ -205,9 +279,21 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
         gw_ = topw_;
         gi_ = topi_;
     }
-    // balancing statistics (381-386)
-    launch_aux_stats(probs_, S, N, gi_, (int64_t)Tt * K, colsum_, mean_probs_, sel_, st);
+    // balancing statistics (381-386): sel_counts are over the gathered table of every
+    // EP rank, i.e. the sum of the ranks' local counts
+    launch_aux_stats(probs_, S, N, gi_, (int64_t)S * K, colsum_, mean_probs_, sel_, st);
     launches_ += 3;
+    const T* xsrc = x;
+    if (E > 1) {
+        all_reduce_sum(ctx_.comm->ep, sel_, sel_, N, ncclInt32, st);
+        ep_dispatch<T>(x, gi_, gw_);
+        gi_ = gi_recv_;
+        gw_ = gw_recv_;
+        xsrc = (const T*)recv_x_;
+        Tt = (int)t_recv_;
+    } else {
+        t_recv_ = S;
+    }
     mark(kRoute, true);
     mark(kIndex, false);
     // stages 2+3 (370-371)
@@ -237,7 +323,7 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     const int32_t* p_total = pad_start_ + nr;
     // stage 4: expert MLP over the padded expert-sorted rows (225-244)
     mark(kGather, false);
-    launch_gather_rows<T>(x, prow_src_, p_total, (T*)mlp_in_, H, pmax_, st);
+    launch_gather_rows<T>(xsrc, prow_src_, p_total, (T*)mlp_in_, H, pmax_, st);
     launches_ += 1;
     mark(kGather, true);
     if (dtype_ == BF16) {
@@ -311,8 +397,16 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     }
     // stage 5: weighted combine (377); EP = 1 so the reducescatter (378) is the identity
     mark(kCombine, false);
-    launch_combine<T>((const T*)y_, slot_prow_, selected_k_, cec_, gw_, out, Tt, H, K, st);
-    launches_ += 1;
+    if (E > 1) {
+        // partial rows per received token, sent back and summed in rank order (reducescatter, 378)
+        launch_combine<T>((const T*)y_, slot_prow_, selected_k_, cec_, gw_, (T*)comb_recv_, Tt, H, K, st);
+        ep_exchange(comb_recv_, ret_x_, sizeof(T) * (size_t)H, false);
+        launch_return_sum<T>((const T*)ret_x_, send_pos_, send_off_d_, S, E, H, out, st);
+        launches_ += 2;
+    } else {
+        launch_combine<T>((const T*)y_, slot_prow_, selected_k_, cec_, gw_, out, Tt, H, K, st);
+        launches_ += 1;
+    }
     mark(kCombine, true);
 }
 
@@ -336,13 +430,23 @@ template <typename T>
 void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* down, const T* dout,
                           const float* aux_probs_grad, T* dx, T* drouter, T* dgate, T* dup, T* ddown) {
     cudaStream_t st = ctx_.stream;
-    const int S = (int)s_, Tt = (int)t_, N = (int)cfg_.n_experts, K = (int)cfg_.top_k, H = (int)cfg_.hidden,
+    const int E = cfg_.ep;
+    const int S = (int)s_, Tt = (int)t_recv_, N = (int)cfg_.n_experts, K = (int)cfg_.top_k, H = (int)cfg_.hidden,
               I = (int)cfg_.intermediate, nr = (int)cfg_.experts_per_rank();
     const int32_t* p_total = pad_start_ + nr;
     const float inv_ep = (float)(1.0 / (double)cfg_.ep);
-    // output_reduction_backward (402-403); EP = 1 so dout is already the allgather (400)
+    // output_reduction_backward (402-403). The allgather of dout (400) becomes a dispatch of
+    // dout rows to the same ranks the tokens went to.
     mark(kOutRedBwd, false);
-    launch_out_reduction_bwd<T>(dout, (const T*)y_, slot_prow_, selected_k_, cec_, gw_, (T*)dy_, wgrad_, Tt, H, K, st);
+    const T* dout_rows = dout;
+    if (E > 1) {
+        launch_pack_rows<T>(dout, send_pos_, send_off_d_, S, E, H, (T*)send_x_, nullptr, nullptr, K, nullptr, st);
+        ep_exchange(send_x_, recv_x_, sizeof(T) * (size_t)H, true);
+        dout_rows = (const T*)recv_x_;
+        launches_ += 1;
+    }
+    launch_out_reduction_bwd<T>(dout_rows, (const T*)y_, slot_prow_, selected_k_, cec_, gw_, (T*)dy_, wgrad_, Tt, H, K,
+                                st);
     launch_zero_pad_rows<T>((T*)dy_, prow_src_, p_total, H, pmax_, st);
     launches_ += 2;
     mark(kOutRedBwd, true);
@@ -468,11 +572,25 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         mark(kGemmDx, true);
         launches_ += 7;
     }
-    // router path (431-454): EP = 1, so weights_grad_local == the full weights grad
+    // router path (431-454)
     mark(kRouterBwd, false);
+    const float* wgrad_local = wgrad_;
+    const T* dx_rows = nullptr;  // EP > 1: the token's summed expert-gradient rows
+    if (E > 1) {
+        // the two reducescatters of moe.hpp:427-428: per-token partial dX rows and the
+        // weight grads go back to the source, which sums them in rank order
+        launch_combine<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, (T*)comb_recv_, Tt, H, K, st);
+        ep_exchange(comb_recv_, ret_x_, sizeof(T) * (size_t)H, false);
+        launch_return_sum<T>((const T*)ret_x_, send_pos_, send_off_d_, S, E, H, (T*)dx_exp_, st);
+        ep_exchange(wgrad_, wret_, sizeof(float) * (size_t)K, false);
+        launch_return_sum<float>(wret_, send_pos_, send_off_d_, S, E, K, wgrad_local_, st);
+        wgrad_local = wgrad_local_;
+        dx_rows = (const T*)dx_exp_;
+        launches_ += 3;
+    }
     const bool tc_router = dtype_ == BF16 && N % 8 == 0 && N <= 256;
-    launch_router_dlogits(probs_, wgrad_, topi_, topw_, aux_probs_grad, dlogits_, tc_router ? dl_bf16_ : nullptr, S,
-                          N, K, cfg_.normalize_topk, fur_, st);
+    launch_router_dlogits(probs_, wgrad_local, topi_, topw_, aux_probs_grad, dlogits_, tc_router ? dl_bf16_ : nullptr,
+                          S, N, K, cfg_.normalize_topk, fur_, st);
     if (tc_router) {
         // router dW and dx on the tensor cores (bf16 dlogits, fp32 accumulation)
         Sm100GemmArgs ga{};
@@ -493,17 +611,23 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         launch_router_dw_reduce_bf16(dw_part_, drouter, router_dw_splits(S, H, ctx_.num_sms), (int64_t)H * N, st);
         // scatter-add to tokens (418-423), then + matmul_nt(dlogits, router) (454) as a GEMM whose
         // epilogue adds the scattered rows
-        launch_combine<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, dx, S, H, K, st);
+        if (!dx_rows) {
+            launch_combine<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, dx, S, H, K, st);
+            dx_rows = dx;
+        }
         ga.kind = GemmKind::RouterDx;
         ga.cec = nullptr;
-        ga.src = dx;
+        ga.src = dx_rows;
         ga.out0 = dx;
         launch_sm100_gemm(ga, st);
         launches_ += 5;
     } else {
         launch_router_dw<T>((const T*)x_, dlogits_, drouter, dw_part_, kRouterDwMaxSplits, S, H, N, st);
         // scatter-add to tokens (418-423) + matmul_nt(dlogits, router) (454)
-        launch_dx_finalize<T>((const T*)dxp_, true, slot_prow_, cec_, dlogits_, router, dx, S, H, N, st);
+        if (dx_rows)
+            launch_dx_finalize<T>(dx_rows, false, slot_prow_, cec_, dlogits_, router, dx, S, H, N, st);
+        else
+            launch_dx_finalize<T>((const T*)dxp_, true, slot_prow_, cec_, dlogits_, router, dx, S, H, N, st);
         launches_ += 4;
     }
     mark(kRouterBwd, true);
@@ -539,9 +663,8 @@ static std::vector<int64_t> d2h_i64(const int32_t* d, int64_t n, cudaStream_t st
 MoeLayer::HostArtifacts MoeLayer::artifacts() {
     check(have_fwd_, "artifacts: no forward state");
     cudaStream_t st = ctx_.stream;
-    const int64_t nr = cfg_.experts_per_rank();
-    launch_partial_counts(gi_, (int)t_, (int)cfg_.top_k, ctx_.coord_ep * (int)nr, (int)nr, (int)cfg_.token_block,
-                          (int)th_, partial_counts_, partial_cum_, st);
+    const int64_t nr = cfg_.experts_per_rank(), K = cfg_.top_k, tbs = cfg_.token_block;
+    const int E = cfg_.ep;
     HostArtifacts a;
     a.t_total = t_;
     a.th = th_;
@@ -550,13 +673,40 @@ MoeLayer::HostArtifacts MoeLayer::artifacts() {
     a.pad_start = d2h_i64(pad_start_, nr + 1, st);
     a.padded_rows = a.pad_start[(size_t)nr];
     a.token_counts = d2h_i64(token_counts_, nr, st);
-    a.partial_token_counts = d2h_i64(partial_counts_, nr * th_, st);
-    a.partial_cum = d2h_i64(partial_cum_, nr * th_ + 1, st);
-    a.expert_counts = d2h_i64(expert_counts_, t_, st);
-    a.cum_expert_counts = d2h_i64(cec_, t_ + 1, st);
     a.input_indices = d2h_i64(input_indices_, a.rt, st);
     a.output_indices = d2h_i64(output_indices_, a.rt, st);
     a.selected_k = d2h_i64(selected_k_, a.rt, st);
+    if (E == 1) {
+        launch_partial_counts(gi_, (int)t_, (int)K, 0, (int)nr, (int)tbs, (int)th_, partial_counts_, partial_cum_, st);
+        a.partial_token_counts = d2h_i64(partial_counts_, nr * th_, st);
+        a.partial_cum = d2h_i64(partial_cum_, nr * th_ + 1, st);
+        a.expert_counts = d2h_i64(expert_counts_, t_, st);
+        a.cum_expert_counts = d2h_i64(cec_, t_ + 1, st);
+    } else {
+        // The rank holds only the tokens routed to it, in the gathered order; re-index them
+        // to the reference's gathered token id src_rank * S + t (moe.hpp:365-371).
+        const int64_t tr = t_recv_;
+        std::vector<int64_t> src_t = d2h_i64(src_t_, tr, st), gi = d2h_i64(gi_recv_, tr * K, st);
+        std::vector<int64_t> ec = d2h_i64(expert_counts_, tr, st);
+        std::vector<int64_t> gid((size_t)tr);
+        for (int r = 0; r < E; ++r)
+            for (int64_t i = roff_[(size_t)r]; i < roff_[(size_t)r] + rcnt_[(size_t)r]; ++i)
+                gid[(size_t)i] = (int64_t)r * s_ + src_t[(size_t)i];
+        for (auto& v : a.input_indices) v = gid[(size_t)v];
+        a.expert_counts.assign((size_t)t_, 0);
+        for (int64_t i = 0; i < tr; ++i) a.expert_counts[(size_t)gid[(size_t)i]] = ec[(size_t)i];
+        a.cum_expert_counts.assign((size_t)t_ + 1, 0);
+        for (int64_t t = 0; t < t_; ++t) a.cum_expert_counts[(size_t)t + 1] = a.cum_expert_counts[(size_t)t] + a.expert_counts[(size_t)t];
+        const int64_t n_start = (int64_t)ctx_.coord_ep * nr;
+        a.partial_token_counts.assign((size_t)(nr * th_), 0);
+        for (int64_t i = 0; i < tr; ++i)
+            for (int64_t k = 0; k < K; ++k) {
+                const int64_t e = gi[(size_t)(i * K + k)];
+                if (e >= n_start && e < n_start + nr) a.partial_token_counts[(size_t)((e - n_start) * th_ + gid[(size_t)i] / tbs)]++;
+            }
+        a.partial_cum.assign((size_t)(nr * th_ + 1), 0);
+        for (int64_t i = 0; i < nr * th_; ++i) a.partial_cum[(size_t)i + 1] = a.partial_cum[(size_t)i] + a.partial_token_counts[(size_t)i];
+    }
     // final write cursors of generate_indices (moe.hpp:176-188): partial_cum[ln*TH + tid + 1]
     a.counter.resize((size_t)(nr * th_));
     for (int64_t i = 0; i < nr * th_; ++i) a.counter[(size_t)i] = a.partial_cum[(size_t)i + 1];

@@ -130,6 +130,16 @@ class MoeLayer {
     // dtype buffers (padded row space)
     void *mlp_in_, *g_, *u_, *h_, *y_, *dy_, *dh_, *dgu_, *dxp_;
     void* dl_bf16_ = nullptr;  // bf16 dlogits for the tensor-core router GEMMs
+    // expert parallelism (ep > 1): dispatch plan, exchange buffers, returned rows
+    template <typename T>
+    void ep_dispatch(const T* x, const int32_t* gi_local, const float* gw_local);
+    void ep_exchange(const void* send, void* recv, size_t row_bytes, bool forward);
+    int64_t t_recv_ = 0;  // tokens received by this rank (rows of the gathered table it needs)
+    int32_t *send_pos_ = nullptr, *send_cnt_d_ = nullptr, *send_off_d_ = nullptr, *recv_cnt_d_ = nullptr;
+    int32_t *meta_send_ = nullptr, *meta_recv_ = nullptr, *gi_recv_ = nullptr, *src_t_ = nullptr;
+    float *gw_recv_ = nullptr, *wret_ = nullptr, *wgrad_local_ = nullptr;
+    void *send_x_ = nullptr, *recv_x_ = nullptr, *comb_recv_ = nullptr, *ret_x_ = nullptr, *dx_exp_ = nullptr;
+    std::vector<int64_t> scnt_, soff_, rcnt_, roff_;  // host copies of the exchange plan
 };
 
 }  // namespace b2
