@@ -166,10 +166,11 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def mula7b_param_set():
-    """Mula-7B-A1B ParamSlots (model.cpp:189-229, preset model.cpp:43-45) at EP=1:
-    (numel, expert?, tp_sharded?)."""
-    hid, layers, vocab, nexp, inter = 2048, 16, 50304, 64, 1024
+def mula7b_param_set(ep=1):
+    """Mula-7B-A1B ParamSlots of one rank (model.cpp:189-229, preset model.cpp:43-45):
+    (numel, expert?, tp_sharded?); the rank holds 64/ep experts per MoE layer."""
+    hid, layers, vocab, inter = 2048, 16, 50304, 1024
+    nexp = 64 // ep
     slots = [(vocab * hid, False, False)]
     for _ in range(layers):
         slots += [(hid, False, False)] + [(hid * hid, False, True)] * 4 + [(hid, False, False)]
@@ -179,10 +180,9 @@ def mula7b_param_set():
 
 
 def bench_adamw(torch, b2, ctx, dev, steps, warmup, world, rank, hbm_peak):
-    slots = mula7b_param_set()
-    total = sum(n for n, _, _ in slots)
-    assert total == 6_919_096_320, total
-    per_rank = [(n, e, t) for n, e, t in slots]
+    assert sum(n for n, _, _ in mula7b_param_set()) == 6_919_096_320
+    per_rank = mula7b_param_set(world)  # EPSO at DP=1, EP=world: strong scaling over the same 6.92B set
+    total = 6_919_096_320
     gen = torch.Generator(device=dev).manual_seed(11)
     weights = [(torch.randn(n, device=dev, generator=gen, dtype=torch.float32) * 0.02).bfloat16()
                for n, _, _ in per_rank]
@@ -209,11 +209,22 @@ def bench_adamw(torch, b2, ctx, dev, steps, warmup, world, rank, hbm_peak):
     gbs = byt / (ms * 1e-3) / 1e9
     del opt, weights, grads
     torch.cuda.empty_cache()
+    ms_t = torch.tensor([ms], device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
     return {"metric": "sharded AdamW step ms (EPSO, Mula-7B-A1B param set, bf16 grads/weights, fp32 state)",
+            "parallelism": f"dp1 x ep{world}", "scaling": "strong",
             "ms": ms, "params": total, "owned_params_per_rank": owned, "launches_per_step": launches,
             "grad_norm": st["grad_norm"],
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
                          "traffic": None, "algorithmic_bytes_per_step": byt}}
+
+
+def layer_rt(layer):
+    """rows routed to this rank's experts in the last step (sum of the expert group sizes)."""
+    return int(layer.artifacts()["rt"])
 
 
 def main():
@@ -244,11 +255,21 @@ def main():
         dist.init_process_group("nccl", init_method="env://", device_id=dev)
     hbm_peak, bf16_peak, bf16_sust, peak_kind = measured_peaks()
 
-    ctx = b2.Context(local, rank=0)  # each rank runs its own layer replica (EP dispatch: next round)
-    cfg = b2.MoeConfig(n_experts=N, top_k=K, hidden=H, intermediate=I, ep=1, token_block=8)
+    # N GPUs = expert parallelism over N ranks (config C): each rank owns N_experts/N experts
+    # and its own 16,384 tokens; tokens travel to their experts' ranks by all-to-all
+    ep = world
+    nccl_id = None
+    if world > 1:
+        ids = [b2.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        nccl_id = ids[0]
+    ctx = b2.Context(local, rank=rank, dp=1, ep=ep, nccl_id=nccl_id)
+    cfg = b2.MoeConfig(n_experts=N, top_k=K, hidden=H, intermediate=I, ep=ep, token_block=8)
+    NR = N // ep
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     mk = lambda shape, std: (torch.randn(shape, device=dev, generator=gen) * std).bfloat16()
-    router, gate, up, down = mk((H, N), 0.02), mk((N, H, I), 0.02), mk((N, H, I), 0.02), mk((N, I, H), 0.02)
+    router = (torch.randn((H, N), device=dev, generator=torch.Generator(device=dev).manual_seed(7)) * 0.02).bfloat16()
+    gate, up, down = mk((NR, H, I), 0.02), mk((NR, H, I), 0.02), mk((NR, I, H), 0.02)
     x, dout = mk((S, H), 1.0), mk((S, H), 1.0)
     layer = b2.MoeLayer(ctx, cfg, torch.bfloat16, S)
 
@@ -293,15 +314,13 @@ def main():
     layer.set_profiling(False)
     gemm_stages = [k for k in st if k.startswith("gemm")]
     gemm_ms = sum(st[k] for k in gemm_stages)
-    art = layer.artifacts()
-    rt = art["rt"]
+    rt = int(layer_rt(layer))
     gemm_flop = 18.0 * rt * H * I
     achieved = gemm_flop / (gemm_ms * 1e-3) / 1e12
     if args.profile and rank == 0:
         for k_, v in st.items():
             print(f"  {k_:>20s} {v:8.3f} ms", file=sys.stderr)
-        print(f"  gemm total {gemm_ms:.3f} ms  {achieved:.1f} TFLOP/s  step {ms:.3f} ms  rt {rt} padded "
-              f"{art['padded_rows']}", file=sys.stderr)
+        print(f"  gemm total {gemm_ms:.3f} ms  {achieved:.1f} TFLOP/s  step {ms:.3f} ms  rt {rt}", file=sys.stderr)
 
     # end to end through the host-buffer entry point (pinned host x/dout in, out/dx back)
     xh, douth = x.cpu().pin_memory(), dout.cpu().pin_memory()
@@ -348,7 +367,8 @@ def main():
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded randn tokens, random-init weights)",
-            "config": {"workload": WORKLOAD, "global_batch_tokens": world * S, "parallelism": f"{world}x ep1 replicas",
+            "config": {"workload": WORKLOAD, "global_batch_tokens": world * S,
+                       "parallelism": f"ep{world} (all-to-all dispatch/combine over NCCL)" if world > 1 else "ep1",
                        "l2": "working set (weights 0.8 GB + activations ~4 GB) >> 126 MB L2; no flush needed"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
                          "frac": achieved / bf16_peak, "traffic": None, "peak_kind": peak_kind,

@@ -1,0 +1,102 @@
+"""Multi-GPU worker for the sharded-optimizer parity tests (one process per GPU).
+
+Every rank steps b2.ShardedOptimizer (NCCL reduce-scatter / all-gather over the DP,
+EP and DP x EP communicators) on its own synthetic gradients; rank 0 compares every
+rank's final weights, fp32 masters, moments and step statistics with the oracle's
+ShardedOptimizer world (oracle/moe_oracle.c, pinned bitwise to optim.cpp:109-194).
+fp32 grads keep NCCL's sums of two members exact, so 2-member groups are bitwise.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+NUMEL = [33, 30, 7, 1029]
+CLS = [0, 1, 0, 1]
+
+
+def run(rank, world, port, dp, ep, mode, result_path):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_00785_b200 as b2
+    from oracle import bind
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(rank)
+    ids = [b2.Context.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(ids, src=0)
+    ctx = b2.Context(rank, rank=rank, dp=dp, ep=ep, nccl_id=ids[0])
+    orc = bind.get("orc")
+    total = sum(NUMEL)
+    steps = 6
+    rng = np.random.default_rng(1000 + dp * 10 + ep + mode)
+    w0 = np.zeros((world, total), np.float32)
+    for r in range(world):
+        e = r % ep
+        off = 0
+        for p, (n, c) in enumerate(zip(NUMEL, CLS)):
+            w0[r, off:off + n] = orc.normal((n,), 402 + p, 100 + e if c else 1, 0.05)
+            off += n
+    grads = (rng.standard_normal((steps, world, total)) * 0.5).astype(np.float32)
+    cfg = b2.AdamWConfig(warmup_steps=2, total_steps=100, peak_lr=1e-2, min_lr=1e-3)
+    dev = torch.device("cuda", rank)
+    W = torch.from_numpy(w0[rank].copy()).to(dev)
+    G = torch.zeros(total, dtype=torch.float32, device=dev)
+    params, off = [], 0
+    for n, c in zip(NUMEL, CLS):
+        params.append((W[off:off + n], G[off:off + n], c, 0))
+        off += n
+    opt = b2.ShardedOptimizer(ctx, cfg, params, mode)
+    stats = []
+    for s in range(steps):
+        G.copy_(torch.from_numpy(grads[s, rank]))
+        st = opt.step(stats=True)
+        stats.append([st["lr"], st["grad_norm"], st["clip_scale"]])
+    torch.cuda.synchronize()
+    mine = {"w": W.cpu().numpy().tolist(), "stats": stats, "sb": opt.state_bytes(),
+            "master": [opt.state(p)[0].tolist() for p in range(len(NUMEL))],
+            "m": [opt.state(p)[1].tolist() for p in range(len(NUMEL))],
+            "v": [opt.state(p)[2].tolist() for p in range(len(NUMEL))]}
+    gathered = [None] * world
+    dist.all_gather_object(gathered, mine)
+    if rank == 0:
+        ocfg = orc.adamw_cfg(warmup_steps=2, total_steps=100, peak_lr=1e-2, min_lr=1e-3)
+        ref = orc.sharded_steps(dp, ep, 1, mode, ocfg, NUMEL, CLS, [0] * len(NUMEL), w0, grads)
+        res = {"weights_equal": True, "state_equal": True, "stats_maxdiff": 0.0, "state_bytes_equal": True,
+               "weights_maxrel": 0.0}
+        for r in range(world):
+            g = gathered[r]
+            wg = np.asarray(g["w"], np.float32)
+            if not np.array_equal(wg, ref["weights"][r]):
+                res["weights_equal"] = False
+            d = np.abs(wg.astype(np.float64) - ref["weights"][r]) / np.maximum(1.0, np.abs(ref["weights"][r]))
+            res["weights_maxrel"] = max(res["weights_maxrel"], float(d.max()))
+            packed = [np.concatenate([np.asarray(g[k][p], np.float32) for p in range(len(NUMEL))]) for k in
+                      ("master", "m", "v")]
+            n_own = packed[0].size
+            for arr, key in zip(packed, ("master", "m", "v")):
+                if not np.array_equal(arr, ref[key][r][:n_own]):
+                    res["state_equal"] = False
+            res["stats_maxdiff"] = max(res["stats_maxdiff"],
+                                       float(np.max(np.abs(np.asarray(g["stats"]) - ref["stats"][:, r, :]))))
+            if g["sb"] != int(ref["state_bytes"][r]):
+                res["state_bytes_equal"] = False
+        with open(result_path, "w") as f:
+            json.dump(res, f)
+    dist.barrier()
+    opt.close()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    rank, world, port = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
+    dp, ep, mode = int(sys.argv[4]), int(sys.argv[5]), int(sys.argv[6])
+    run(rank, world, port, dp, ep, mode, sys.argv[7])
