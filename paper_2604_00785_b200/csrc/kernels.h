@@ -61,9 +61,9 @@ template <typename T>
 void launch_combine(const T* y, const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec,
                     const float* gw, T* out, int T_tok, int H, int K, cudaStream_t st);
 template <typename T>
-void launch_out_reduction_bwd(const T* dout, const T* y, const int32_t* slot_prow, const int32_t* selected_k,
-                              const int32_t* cec, const float* gw, T* dy, float* wgrad, int T_tok, int H, int K,
-                              cudaStream_t st);
+void launch_out_reduction_bwd(const T* dout, const T* const* peer_dout, int s_local, const T* y,
+                              const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec, const float* gw,
+                              T* dy, float* wgrad, int T_tok, int H, int K, cudaStream_t st);
 template <typename T>
 void launch_dx_finalize(const T* src, bool from_slots, const int32_t* slot_prow, const int32_t* cec, const float* dl,
                         const T* wr, T* dx, int S, int H, int N, cudaStream_t st);
@@ -73,17 +73,19 @@ template <typename T>
 void launch_swiglu_bwd(const T* g, const T* u, const T* dh, T* dgu, const int32_t* p_total, int I, int64_t pmax,
                        cudaStream_t st);
 
-// ---- expert-parallel dispatch / combine (ep_dispatch.cu) ----
-void launch_dest_plan(const int32_t* gi, int S, int K, int E, int NR, int32_t* send_pos, int32_t* send_cnt,
-                      int32_t* send_off, cudaStream_t st);
+// ---- expert-parallel dispatch / combine over NVLink peer memory (ep_dispatch.cu) ----
 template <typename T>
-void launch_pack_rows(const T* x, const int32_t* send_pos, const int32_t* send_off, int S, int E, int H, T* send_x,
-                      const int32_t* gi, const float* gw, int K, int32_t* meta, cudaStream_t st);
-void launch_unpack_meta(const int32_t* meta, int64_t n, int K, int32_t* gi, float* gw, int32_t* src_t,
-                        cudaStream_t st);
+void launch_ep_gather_pull(const T* const* peer_src, int S, int T_tot, int H, const int32_t* cec,
+                           const int32_t* slot_prow, T* out, cudaStream_t st);
 template <typename T>
-void launch_return_sum(const T* ret, const int32_t* send_pos, const int32_t* send_off, int S, int E, int W, T* out,
-                       cudaStream_t st);
+void launch_ep_combine_push(const T* y, const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec,
+                            const float* gw, int K, int S, int T_tot, int H, int me, T* const* peer_ret,
+                            cudaStream_t st);
+void launch_ep_wgrad_push(const float* wgrad, const int32_t* cec, int K, int S, int T_tot, int me,
+                          float* const* peer_wret, cudaStream_t st);
+template <typename T>
+void launch_ep_return_sum(const T* slab, const int32_t* gi_local, int S, int K, int E, int NR, int W, T* out,
+                          cudaStream_t st);
 
 // ---- SIMT grouped GEMM (simt_gemm.cu) ----
 struct SimtGemmArgs {

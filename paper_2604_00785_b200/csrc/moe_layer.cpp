@@ -78,14 +78,9 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
         acc(es * (size_t)std::max<int64_t>(n, 1));
     acc(2 * (size_t)std::max<int64_t>(smax_ * N, 1));
     const int E = cfg_.ep;
-    const int64_t MW = 1 + 2 * K;
     if (E > 1) {
-        for (int64_t n : {(int64_t)E * smax_, (int64_t)E, (int64_t)E, (int64_t)E, tmax_ * MW, tmax_ * MW, tmax_ * K,
-                          tmax_})
-            acc(4 * (size_t)std::max<int64_t>(n, 1));
-        for (int64_t n : {tmax_ * K, tmax_ * K, smax_ * K}) acc(4 * (size_t)std::max<int64_t>(n, 1));
-        for (int64_t n : {tmax_ * H, tmax_ * H, tmax_ * H, tmax_ * H, smax_ * H})
-            acc(es * (size_t)std::max<int64_t>(n, 1));
+        for (int64_t n : {tmax_ * K, tmax_ * K, smax_ * K, (int64_t)8}) acc(4 * (size_t)std::max<int64_t>(n, 1));
+        acc(es * (size_t)std::max<int64_t>(smax_ * H, 1));
     }
     B2_CUDA(cudaSetDevice(ctx_.device));
     arena_.reserve(bytes);
@@ -128,22 +123,12 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     dl_bf16_ = arena_.take_bytes(2 * (size_t)std::max<int64_t>(smax_ * N, 1));
     if (E > 1) {
         check(ctx_.comm != nullptr && ctx_.comm->ep.size == E, "fast_moe: EP > 1 needs the EP communicator");
-        send_pos_ = arena_.take<int32_t>((int64_t)E * smax_);
-        send_cnt_d_ = arena_.take<int32_t>(E);
-        send_off_d_ = arena_.take<int32_t>(E);
-        recv_cnt_d_ = arena_.take<int32_t>(E);
-        meta_send_ = arena_.take<int32_t>(tmax_ * MW);
-        meta_recv_ = arena_.take<int32_t>(tmax_ * MW);
-        gi_recv_ = arena_.take<int32_t>(tmax_ * K);
-        src_t_ = arena_.take<int32_t>(tmax_);
-        gw_recv_ = arena_.take<float>(tmax_ * K);
-        wret_ = arena_.take<float>(tmax_ * K);
+        gi_all_ = arena_.take<int32_t>(tmax_ * K);
+        gw_all_ = arena_.take<float>(tmax_ * K);
         wgrad_local_ = arena_.take<float>(smax_ * K);
-        send_x_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(tmax_ * H, 1));
-        recv_x_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(tmax_ * H, 1));
-        comb_recv_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(tmax_ * H, 1));
-        ret_x_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(tmax_ * H, 1));
+        bar_ = arena_.take<int32_t>(8);
         dx_exp_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(smax_ * H, 1));
+        ep_setup();
     }
     B2_CUDA(cudaMemsetAsync(err_, 0, 4, ctx_.stream));
     B2_CUDA(cudaMemsetAsync(pad_start_, 0, 4 * (nr + 1), ctx_.stream));
@@ -152,7 +137,65 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
 MoeLayer::~MoeLayer() {
     for (auto& st : prof_ev_)
         for (cudaEvent_t e : st) cudaEventDestroy(e);
+    if (sym_) {
+        cudaStreamSynchronize(ctx_.stream);
+        for (int p = 0; p < (int)peer_base_.size(); ++p)
+            if (p != ctx_.coord_ep && peer_base_[(size_t)p]) cudaIpcCloseMemHandle(peer_base_[(size_t)p]);
+        cudaFree(sym_);
+        cudaFree(peer_tab_);
+    }
 }
+
+// symmetric buffer: [x_sh S*H | dout_sh S*H | ret_f E*S*H | ret_b E*S*H] (dtype) + wret [E*S*K] f32,
+// identical offsets on every rank; IPC handles are exchanged with an NCCL all-gather
+void MoeLayer::ep_setup() {
+    const int E = cfg_.ep, me = ctx_.coord_ep;
+    const size_t es = dtype_size(dtype_);
+    const size_t H = (size_t)cfg_.hidden, S = (size_t)std::max<int64_t>(smax_, 1), K = (size_t)cfg_.top_k;
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t o_x = 0, o_d = o_x + al(es * S * H), o_rf = o_d + al(es * S * H), o_rb = o_rf + al(es * E * S * H),
+                 o_w = o_rb + al(es * E * S * H), total = o_w + al(4 * E * S * K);
+    B2_CUDA(cudaMalloc(&sym_, total));
+    cudaIpcMemHandle_t h;
+    B2_CUDA(cudaIpcGetMemHandle(&h, sym_));
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+    char* dh = nullptr;
+    B2_CUDA(cudaMalloc(&dh, 64 * (size_t)E));
+    B2_CUDA(cudaMemcpyAsync(dh + 64 * me, &h, 64, cudaMemcpyHostToDevice, ctx_.stream));
+    B2_NCCL(ncclAllGather(dh + 64 * me, dh, 64, ncclUint8, ctx_.comm->ep.comm, ctx_.stream));
+    std::vector<cudaIpcMemHandle_t> hs((size_t)E);
+    B2_CUDA(cudaMemcpyAsync(hs.data(), dh, 64 * (size_t)E, cudaMemcpyDeviceToHost, ctx_.stream));
+    B2_CUDA(cudaStreamSynchronize(ctx_.stream));
+    B2_CUDA(cudaFree(dh));
+    peer_base_.assign((size_t)E, nullptr);
+    for (int p = 0; p < E; ++p) {
+        if (p == me) {
+            peer_base_[(size_t)p] = sym_;
+        } else {
+            void* ptr = nullptr;
+            B2_CUDA(cudaIpcOpenMemHandle(&ptr, hs[(size_t)p], cudaIpcMemLazyEnablePeerAccess));
+            peer_base_[(size_t)p] = (char*)ptr;
+        }
+    }
+    std::vector<void*> tab((size_t)5 * E);
+    for (int p = 0; p < E; ++p) {
+        tab[(size_t)(0 * E + p)] = peer_base_[(size_t)p] + o_x;
+        tab[(size_t)(1 * E + p)] = peer_base_[(size_t)p] + o_d;
+        tab[(size_t)(2 * E + p)] = peer_base_[(size_t)p] + o_rf;
+        tab[(size_t)(3 * E + p)] = peer_base_[(size_t)p] + o_rb;
+        tab[(size_t)(4 * E + p)] = peer_base_[(size_t)p] + o_w;
+    }
+    B2_CUDA(cudaMalloc(&peer_tab_, sizeof(void*) * tab.size()));
+    B2_CUDA(cudaMemcpy(peer_tab_, tab.data(), sizeof(void*) * tab.size(), cudaMemcpyHostToDevice));
+    x_sh_ = sym_ + o_x;
+    dout_sh_ = sym_ + o_d;
+    ret_f_ = sym_ + o_rf;
+    ret_b_ = sym_ + o_rb;
+    wret_ = (float*)(sym_ + o_w);
+}
+
+// every rank's preceding stream work (and its peer stores) is complete once this returns
+void MoeLayer::ep_barrier() { all_reduce_sum(ctx_.comm->ep, bar_, bar_, 1, ncclInt32, ctx_.stream); }
 
 const char* MoeLayer::stage_name(int s) {
     static const char* names[kNumStages] = {"route",           "index",          "gather",       "gemm_fwd_gate_up",
@@ -193,49 +236,6 @@ void MoeLayer::stage_times(float* ms) {
         }
         ms[s] = (float)(acc / n);
     }
-}
-
-// rows travel forward (source -> expert owner, counts scnt/rcnt) or back (owner -> source)
-void MoeLayer::ep_exchange(const void* send, void* recv, size_t row_bytes, bool forward) {
-    const Group& g = ctx_.comm->ep;
-    if (forward) all_to_all_v(g, send, scnt_.data(), soff_.data(), recv, rcnt_.data(), roff_.data(), row_bytes, ctx_.stream);
-    else all_to_all_v(g, send, rcnt_.data(), roff_.data(), recv, scnt_.data(), soff_.data(), row_bytes, ctx_.stream);
-}
-
-// dispatch (replaces the allgathers of moe.hpp:365-367): plan, count exchange (one small
-// host sync: NCCL needs the row counts), pack, all-to-all of rows + routing metadata
-template <typename T>
-void MoeLayer::ep_dispatch(const T* x, const int32_t* gi_local, const float* gw_local) {
-    cudaStream_t st = ctx_.stream;
-    const int E = cfg_.ep, S = (int)s_, K = (int)cfg_.top_k, H = (int)cfg_.hidden, nr = (int)cfg_.experts_per_rank();
-    launch_dest_plan(gi_local, S, K, E, nr, send_pos_, send_cnt_d_, send_off_d_, st);
-    std::vector<int64_t> one(E, 1), idx(E);
-    for (int r = 0; r < E; ++r) idx[r] = r;
-    all_to_all_v(ctx_.comm->ep, send_cnt_d_, one.data(), idx.data(), recv_cnt_d_, one.data(), idx.data(), 4, st);
-    std::vector<int32_t> sc(E), so(E), rc(E);
-    B2_CUDA(cudaMemcpyAsync(sc.data(), send_cnt_d_, 4 * E, cudaMemcpyDeviceToHost, st));
-    B2_CUDA(cudaMemcpyAsync(so.data(), send_off_d_, 4 * E, cudaMemcpyDeviceToHost, st));
-    B2_CUDA(cudaMemcpyAsync(rc.data(), recv_cnt_d_, 4 * E, cudaMemcpyDeviceToHost, st));
-    B2_CUDA(cudaStreamSynchronize(st));
-    scnt_.assign(E, 0);
-    soff_.assign(E, 0);
-    rcnt_.assign(E, 0);
-    roff_.assign(E, 0);
-    int64_t acc = 0;
-    for (int r = 0; r < E; ++r) {
-        scnt_[r] = sc[r];
-        soff_[r] = so[r];
-        rcnt_[r] = rc[r];
-        roff_[r] = acc;
-        acc += rc[r];
-    }
-    t_recv_ = acc;
-    check(t_recv_ <= tmax_, "ep dispatch: received more tokens than the layer's capacity");
-    launch_pack_rows<T>(x, send_pos_, send_off_d_, S, E, H, (T*)send_x_, gi_local, gw_local, K, meta_send_, st);
-    ep_exchange(send_x_, recv_x_, sizeof(T) * (size_t)H, true);
-    ep_exchange(meta_send_, meta_recv_, 4 * (size_t)(1 + 2 * K), true);
-    launch_unpack_meta(meta_recv_, t_recv_, K, gi_recv_, gw_recv_, src_t_, st);
-    launches_ += 3;
 }
 
 void MoeLayer::forward(const void* x, const void* router, const void* gate, const void* up, const void* down,
@@ -279,21 +279,23 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
         gw_ = topw_;
         gi_ = topi_;
     }
-    // balancing statistics (381-386): sel_counts are over the gathered table of every
-    // EP rank, i.e. the sum of the ranks' local counts
-    launch_aux_stats(probs_, S, N, gi_, (int64_t)S * K, colsum_, mean_probs_, sel_, st);
-    launches_ += 3;
-    const T* xsrc = x;
+    gi_local_ = gi_;
     if (E > 1) {
-        all_reduce_sum(ctx_.comm->ep, sel_, sel_, N, ncclInt32, st);
-        ep_dispatch<T>(x, gi_, gw_);
-        gi_ = gi_recv_;
-        gw_ = gw_recv_;
-        xsrc = (const T*)recv_x_;
-        Tt = (int)t_recv_;
-    } else {
-        t_recv_ = S;
+        // the allgathers of weights and indices (moe.hpp:366-367): the reference's gathered
+        // routing table; token rows stay where they are until an expert owner pulls them
+        B2_CUDA(cudaMemcpyAsync(x_sh_, x, sizeof(T) * (size_t)S * H, cudaMemcpyDeviceToDevice, st));
+        B2_NCCL(ncclGroupStart());
+        B2_NCCL(ncclAllGather(gi_, gi_all_, (size_t)S * K, ncclInt32, ctx_.comm->ep.comm, st));
+        B2_NCCL(ncclAllGather(gw_, gw_all_, (size_t)S * K, ncclFloat32, ctx_.comm->ep.comm, st));
+        B2_NCCL(ncclGroupEnd());
+        gi_ = gi_all_;
+        gw_ = gw_all_;
+        Tt = E * S;
     }
+    // balancing statistics (381-386): mean_probs over the local rows, sel_counts over the
+    // gathered table
+    launch_aux_stats(probs_, S, N, gi_, (int64_t)Tt * K, colsum_, mean_probs_, sel_, st);
+    launches_ += 3;
     mark(kRoute, true);
     mark(kIndex, false);
     // stages 2+3 (370-371)
@@ -323,8 +325,14 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     const int32_t* p_total = pad_start_ + nr;
     // stage 4: expert MLP over the padded expert-sorted rows (225-244)
     mark(kGather, false);
-    launch_gather_rows<T>(xsrc, prow_src_, p_total, (T*)mlp_in_, H, pmax_, st);
-    launches_ += 1;
+    if (E > 1) {
+        launch_ep_gather_pull<T>((const T* const*)peer_tab_, S, Tt, H, cec_, slot_prow_, (T*)mlp_in_, st);
+        launch_zero_pad_rows<T>((T*)mlp_in_, prow_src_, p_total, H, pmax_, st);
+        launches_ += 2;
+    } else {
+        launch_gather_rows<T>(x, prow_src_, p_total, (T*)mlp_in_, H, pmax_, st);
+        launches_ += 1;
+    }
     mark(kGather, true);
     if (dtype_ == BF16) {
         Sm100GemmArgs ga{};
@@ -398,10 +406,12 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     // stage 5: weighted combine (377); EP = 1 so the reducescatter (378) is the identity
     mark(kCombine, false);
     if (E > 1) {
-        // partial rows per received token, sent back and summed in rank order (reducescatter, 378)
-        launch_combine<T>((const T*)y_, slot_prow_, selected_k_, cec_, gw_, (T*)comb_recv_, Tt, H, K, st);
-        ep_exchange(comb_recv_, ret_x_, sizeof(T) * (size_t)H, false);
-        launch_return_sum<T>((const T*)ret_x_, send_pos_, send_off_d_, S, E, H, out, st);
+        // weighted partial rows stored into the source ranks' slabs, then summed there in
+        // rank order (the reducescatter of moe.hpp:378)
+        launch_ep_combine_push<T>((const T*)y_, slot_prow_, selected_k_, cec_, gw_, K, S, Tt, H, ctx_.coord_ep,
+                                  (T* const*)peer_tab_ + 2 * E, st);
+        ep_barrier();
+        launch_ep_return_sum<T>((const T*)ret_f_, gi_local_, S, K, E, nr, H, out, st);
         launches_ += 2;
     } else {
         launch_combine<T>((const T*)y_, slot_prow_, selected_k_, cec_, gw_, out, Tt, H, K, st);
@@ -431,22 +441,21 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
                           const float* aux_probs_grad, T* dx, T* drouter, T* dgate, T* dup, T* ddown) {
     cudaStream_t st = ctx_.stream;
     const int E = cfg_.ep;
-    const int S = (int)s_, Tt = (int)t_recv_, N = (int)cfg_.n_experts, K = (int)cfg_.top_k, H = (int)cfg_.hidden,
+    const int S = (int)s_, Tt = (int)t_, N = (int)cfg_.n_experts, K = (int)cfg_.top_k, H = (int)cfg_.hidden,
               I = (int)cfg_.intermediate, nr = (int)cfg_.experts_per_rank();
     const int32_t* p_total = pad_start_ + nr;
     const float inv_ep = (float)(1.0 / (double)cfg_.ep);
     // output_reduction_backward (402-403). The allgather of dout (400) becomes a dispatch of
     // dout rows to the same ranks the tokens went to.
     mark(kOutRedBwd, false);
-    const T* dout_rows = dout;
-    if (E > 1) {
-        launch_pack_rows<T>(dout, send_pos_, send_off_d_, S, E, H, (T*)send_x_, nullptr, nullptr, K, nullptr, st);
-        ep_exchange(send_x_, recv_x_, sizeof(T) * (size_t)H, true);
-        dout_rows = (const T*)recv_x_;
-        launches_ += 1;
+    const T* const* peer_dout = nullptr;
+    if (E > 1) {  // owners pull dout rows straight from the source rank
+        B2_CUDA(cudaMemcpyAsync(dout_sh_, dout, sizeof(T) * (size_t)S * H, cudaMemcpyDeviceToDevice, st));
+        ep_barrier();
+        peer_dout = (const T* const*)peer_tab_ + E;
     }
-    launch_out_reduction_bwd<T>(dout_rows, (const T*)y_, slot_prow_, selected_k_, cec_, gw_, (T*)dy_, wgrad_, Tt, H, K,
-                                st);
+    launch_out_reduction_bwd<T>(dout, peer_dout, S, (const T*)y_, slot_prow_, selected_k_, cec_, gw_, (T*)dy_, wgrad_,
+                                Tt, H, K, st);
     launch_zero_pad_rows<T>((T*)dy_, prow_src_, p_total, H, pmax_, st);
     launches_ += 2;
     mark(kOutRedBwd, true);
@@ -579,14 +588,15 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
     if (E > 1) {
         // the two reducescatters of moe.hpp:427-428: per-token partial dX rows and the
         // weight grads go back to the source, which sums them in rank order
-        launch_combine<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, (T*)comb_recv_, Tt, H, K, st);
-        ep_exchange(comb_recv_, ret_x_, sizeof(T) * (size_t)H, false);
-        launch_return_sum<T>((const T*)ret_x_, send_pos_, send_off_d_, S, E, H, (T*)dx_exp_, st);
-        ep_exchange(wgrad_, wret_, sizeof(float) * (size_t)K, false);
-        launch_return_sum<float>(wret_, send_pos_, send_off_d_, S, E, K, wgrad_local_, st);
+        launch_ep_combine_push<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, K, S, Tt, H, ctx_.coord_ep,
+                                  (T* const*)peer_tab_ + 3 * E, st);
+        launch_ep_wgrad_push(wgrad_, cec_, K, S, Tt, ctx_.coord_ep, (float* const*)peer_tab_ + 4 * E, st);
+        ep_barrier();
+        launch_ep_return_sum<T>((const T*)ret_b_, gi_local_, S, K, E, nr, H, (T*)dx_exp_, st);
+        launch_ep_return_sum<float>(wret_, gi_local_, S, K, E, nr, K, wgrad_local_, st);
         wgrad_local = wgrad_local_;
         dx_rows = (const T*)dx_exp_;
-        launches_ += 3;
+        launches_ += 4;
     }
     const bool tc_router = dtype_ == BF16 && N % 8 == 0 && N <= 256;
     launch_router_dlogits(probs_, wgrad_local, topi_, topw_, aux_probs_grad, dlogits_, tc_router ? dl_bf16_ : nullptr,
@@ -664,7 +674,6 @@ MoeLayer::HostArtifacts MoeLayer::artifacts() {
     check(have_fwd_, "artifacts: no forward state");
     cudaStream_t st = ctx_.stream;
     const int64_t nr = cfg_.experts_per_rank(), K = cfg_.top_k, tbs = cfg_.token_block;
-    const int E = cfg_.ep;
     HostArtifacts a;
     a.t_total = t_;
     a.th = th_;
@@ -676,37 +685,12 @@ MoeLayer::HostArtifacts MoeLayer::artifacts() {
     a.input_indices = d2h_i64(input_indices_, a.rt, st);
     a.output_indices = d2h_i64(output_indices_, a.rt, st);
     a.selected_k = d2h_i64(selected_k_, a.rt, st);
-    if (E == 1) {
-        launch_partial_counts(gi_, (int)t_, (int)K, 0, (int)nr, (int)tbs, (int)th_, partial_counts_, partial_cum_, st);
-        a.partial_token_counts = d2h_i64(partial_counts_, nr * th_, st);
-        a.partial_cum = d2h_i64(partial_cum_, nr * th_ + 1, st);
-        a.expert_counts = d2h_i64(expert_counts_, t_, st);
-        a.cum_expert_counts = d2h_i64(cec_, t_ + 1, st);
-    } else {
-        // The rank holds only the tokens routed to it, in the gathered order; re-index them
-        // to the reference's gathered token id src_rank * S + t (moe.hpp:365-371).
-        const int64_t tr = t_recv_;
-        std::vector<int64_t> src_t = d2h_i64(src_t_, tr, st), gi = d2h_i64(gi_recv_, tr * K, st);
-        std::vector<int64_t> ec = d2h_i64(expert_counts_, tr, st);
-        std::vector<int64_t> gid((size_t)tr);
-        for (int r = 0; r < E; ++r)
-            for (int64_t i = roff_[(size_t)r]; i < roff_[(size_t)r] + rcnt_[(size_t)r]; ++i)
-                gid[(size_t)i] = (int64_t)r * s_ + src_t[(size_t)i];
-        for (auto& v : a.input_indices) v = gid[(size_t)v];
-        a.expert_counts.assign((size_t)t_, 0);
-        for (int64_t i = 0; i < tr; ++i) a.expert_counts[(size_t)gid[(size_t)i]] = ec[(size_t)i];
-        a.cum_expert_counts.assign((size_t)t_ + 1, 0);
-        for (int64_t t = 0; t < t_; ++t) a.cum_expert_counts[(size_t)t + 1] = a.cum_expert_counts[(size_t)t] + a.expert_counts[(size_t)t];
-        const int64_t n_start = (int64_t)ctx_.coord_ep * nr;
-        a.partial_token_counts.assign((size_t)(nr * th_), 0);
-        for (int64_t i = 0; i < tr; ++i)
-            for (int64_t k = 0; k < K; ++k) {
-                const int64_t e = gi[(size_t)(i * K + k)];
-                if (e >= n_start && e < n_start + nr) a.partial_token_counts[(size_t)((e - n_start) * th_ + gid[(size_t)i] / tbs)]++;
-            }
-        a.partial_cum.assign((size_t)(nr * th_ + 1), 0);
-        for (int64_t i = 0; i < nr * th_; ++i) a.partial_cum[(size_t)i + 1] = a.partial_cum[(size_t)i] + a.partial_token_counts[(size_t)i];
-    }
+    launch_partial_counts(gi_, (int)t_, (int)K, ctx_.coord_ep * (int)nr, (int)nr, (int)tbs, (int)th_, partial_counts_,
+                          partial_cum_, st);
+    a.partial_token_counts = d2h_i64(partial_counts_, nr * th_, st);
+    a.partial_cum = d2h_i64(partial_cum_, nr * th_ + 1, st);
+    a.expert_counts = d2h_i64(expert_counts_, t_, st);
+    a.cum_expert_counts = d2h_i64(cec_, t_ + 1, st);
     // final write cursors of generate_indices (moe.hpp:176-188): partial_cum[ln*TH + tid + 1]
     a.counter.resize((size_t)(nr * th_));
     for (int64_t i = 0; i < nr * th_; ++i) a.counter[(size_t)i] = a.partial_cum[(size_t)i + 1];

@@ -130,16 +130,22 @@ class MoeLayer {
     // dtype buffers (padded row space)
     void *mlp_in_, *g_, *u_, *h_, *y_, *dy_, *dh_, *dgu_, *dxp_;
     void* dl_bf16_ = nullptr;  // bf16 dlogits for the tensor-core router GEMMs
-    // expert parallelism (ep > 1): dispatch plan, exchange buffers, returned rows
-    template <typename T>
-    void ep_dispatch(const T* x, const int32_t* gi_local, const float* gw_local);
-    void ep_exchange(const void* send, void* recv, size_t row_bytes, bool forward);
-    int64_t t_recv_ = 0;  // tokens received by this rank (rows of the gathered table it needs)
-    int32_t *send_pos_ = nullptr, *send_cnt_d_ = nullptr, *send_off_d_ = nullptr, *recv_cnt_d_ = nullptr;
-    int32_t *meta_send_ = nullptr, *meta_recv_ = nullptr, *gi_recv_ = nullptr, *src_t_ = nullptr;
-    float *gw_recv_ = nullptr, *wret_ = nullptr, *wgrad_local_ = nullptr;
-    void *send_x_ = nullptr, *recv_x_ = nullptr, *comb_recv_ = nullptr, *ret_x_ = nullptr, *dx_exp_ = nullptr;
-    std::vector<int64_t> scnt_, soff_, rcnt_, roff_;  // host copies of the exchange plan
+    // expert parallelism (ep > 1) over NVLink peer memory: a symmetric CUDA-IPC buffer per
+    // rank holds x / dout (pulled by the expert owners) and the return slabs the owners
+    // store into; only the [S,K] routing table goes through an NCCL all-gather
+    void ep_setup();
+    void ep_barrier();
+    const int32_t* gi_local_ = nullptr;  // this rank's dispatch table [S,K] (learned or FUR)
+    char* sym_ = nullptr;
+    std::vector<char*> peer_base_;
+    void** peer_tab_ = nullptr;  // device: tables of E pointers: x, dout, ret_f, ret_b, wret
+    void *x_sh_ = nullptr, *dout_sh_ = nullptr, *ret_f_ = nullptr, *ret_b_ = nullptr;
+    float* wret_ = nullptr;
+    int32_t* gi_all_ = nullptr;
+    float* gw_all_ = nullptr;
+    int32_t* bar_ = nullptr;
+    float* wgrad_local_ = nullptr;
+    void* dx_exp_ = nullptr;
 };
 
 }  // namespace b2

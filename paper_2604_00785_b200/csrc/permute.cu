@@ -153,8 +153,11 @@ __global__ void combine_kernel(const T* __restrict__ y, const int32_t* __restric
 // output_reduction_backward (moe.hpp:271-298): for each local slot of token t,
 // dy[prow] = w * dout[t]; wgrad[t, k] = <dout[t], y[prow]> accumulated in fp64.
 // Non-local (t, k) entries of wgrad are written as 0.
+// dout rows come from `dout` ([T,H]) or, for expert parallelism, straight from the
+// source rank's buffer over NVLink: peer_dout[t / s_local] + (t % s_local) * H.
 template <typename T>
-__global__ void out_reduction_bwd_kernel(const T* __restrict__ dout, const T* __restrict__ y,
+__global__ void out_reduction_bwd_kernel(const T* __restrict__ dout, const T* const* __restrict__ peer_dout,
+                                         int s_local, const T* __restrict__ y,
                                          const int32_t* __restrict__ slot_prow, const int32_t* __restrict__ selected_k,
                                          const int32_t* __restrict__ cum_expert_counts, const float* __restrict__ gw,
                                          T* __restrict__ dy, float* __restrict__ wgrad, int T_tok, int H, int K) {
@@ -163,7 +166,8 @@ __global__ void out_reduction_bwd_kernel(const T* __restrict__ dout, const T* __
     const int j0 = cum_expert_counts[t], j1 = cum_expert_counts[t + 1];
     for (int k = lane; k < K; k += 32) wgrad[(int64_t)t * K + k] = 0.f;
     __syncwarp();
-    const T* gp = dout + (int64_t)t * H;
+    if (j0 == j1) return;
+    const T* gp = peer_dout ? peer_dout[t / s_local] + (int64_t)(t % s_local) * H : dout + (int64_t)t * H;
     if (vec_ok<T>(H) && H <= 32 * V16<T>::n * 8) {
         // dout row cached in registers (<= 8 vectors per lane); the slots of a token are
         // processed together so their row loads are in flight at the same time
@@ -392,12 +396,13 @@ void launch_combine(const T* y, const int32_t* slot_prow, const int32_t* selecte
 }
 
 template <typename T>
-void launch_out_reduction_bwd(const T* dout, const T* y, const int32_t* slot_prow, const int32_t* selected_k,
-                              const int32_t* cec, const float* gw, T* dy, float* wgrad, int T_tok, int H, int K,
-                              cudaStream_t st) {
+void launch_out_reduction_bwd(const T* dout, const T* const* peer_dout, int s_local, const T* y,
+                              const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec, const float* gw,
+                              T* dy, float* wgrad, int T_tok, int H, int K, cudaStream_t st) {
     if (T_tok <= 0) return;
-    out_reduction_bwd_kernel<T><<<(unsigned)ceil_div(T_tok, 8), 256, 0, st>>>(dout, y, slot_prow, selected_k, cec, gw,
-                                                                               dy, wgrad, T_tok, H, K);
+    out_reduction_bwd_kernel<T><<<(unsigned)ceil_div(T_tok, 8), 256, 0, st>>>(dout, peer_dout, s_local, y, slot_prow,
+                                                                               selected_k, cec, gw, dy, wgrad, T_tok,
+                                                                               H, K);
     B2_LAUNCH_CHECK();
 }
 
@@ -433,8 +438,9 @@ void launch_swiglu_bwd(const T* g, const T* u, const T* dh, T* dgu, const int32_
     template void launch_zero_pad_rows<T>(T*, const int32_t*, const int32_t*, int, int64_t, cudaStream_t);        \
     template void launch_combine<T>(const T*, const int32_t*, const int32_t*, const int32_t*, const float*, T*, int, \
                                     int, int, cudaStream_t);                                                       \
-    template void launch_out_reduction_bwd<T>(const T*, const T*, const int32_t*, const int32_t*, const int32_t*,   \
-                                              const float*, T*, float*, int, int, int, cudaStream_t);              \
+    template void launch_out_reduction_bwd<T>(const T*, const T* const*, int, const T*, const int32_t*,           \
+                                              const int32_t*, const int32_t*, const float*, T*, float*, int, int,  \
+                                              int, cudaStream_t);                                                  \
     template void launch_dx_finalize<T>(const T*, bool, const int32_t*, const int32_t*, const float*, const T*, T*, \
                                         int, int, int, cudaStream_t);                                              \
     template void launch_swiglu_fwd<T>(const T*, const T*, T*, const int32_t*, int, int64_t, cudaStream_t);        \
