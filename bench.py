@@ -91,6 +91,20 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def ncu_traffic():
+    """DRAM bytes (read + write) per step of the six expert-GEMM launches, from the committed
+    `ncu --set full` capture (tools/ncu_summary.py -> profiles/*_ncu_traffic.json)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_traffic.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
+        d = json.load(f)
+    tot = sum(v["dram_bytes"] for k, v in d["kernels"].items()
+              if "grouped_gemm_kernel" in k and k.split("<")[1][0] in "012345")
+    return tot, os.path.relpath(files[-1], ROOT)
+
+
 def cpu_info():
     model = "unknown"
     try:
@@ -222,6 +236,73 @@ def bench_adamw(torch, b2, ctx, dev, steps, warmup, world, rank, hbm_peak):
                          "traffic": None, "algorithmic_bytes_per_step": byt}}
 
 
+def zipf_tokens(torch, dev, S, Hd, N, s, seed):
+    """Config E routing: logits[t,e] = log z_e + Gumbel(t,e), z_e ∝ (e+1)^-s,
+    identity expert permutation (the hottest experts on rank 0). Realised through the
+    layer's own router: x[:, :N] carries the logits and Wr = [I_N; 0]."""
+    g = torch.Generator(device=dev).manual_seed(seed)
+    z = (torch.arange(N, device=dev, dtype=torch.float64) + 1.0) ** -s
+    z = z / z.sum()
+    u = torch.rand((S, N), device=dev, generator=g, dtype=torch.float64).clamp_(1e-12, 1.0)
+    x = torch.randn((S, Hd), device=dev, generator=g)
+    x[:, :N] = (torch.log(z)[None, :] - torch.log(-torch.log(u))).float()
+    router = torch.zeros((Hd, N), device=dev)
+    router[torch.arange(N), torch.arange(N)] = 1.0
+    return x.bfloat16(), router.bfloat16()
+
+
+def bench_zipf(torch, b2, ctx, dev, stream, world, rank, zipf_s, steps, warmup):
+    """Mula-20B-A2B-shaped layer (H 2048, 96 experts top-8, ffn 1024; model.cpp:46-48) under
+    Zipf-skewed routing, EP = world (config E): the load-imbalance stress line."""
+    import torch.distributed as dist
+    Nz = 96
+    cfg = b2.MoeConfig(n_experts=Nz, top_k=K, hidden=H, intermediate=I, ep=world, token_block=8)
+    NR = Nz // world
+    x, router = zipf_tokens(torch, dev, S, H, Nz, zipf_s, 4242 + rank)
+    gen = torch.Generator(device=dev).manual_seed(99 + rank)
+    mk = lambda shape, std: (torch.randn(shape, device=dev, generator=gen) * std).bfloat16()
+    gate, up, down, dout = mk((NR, H, I), 0.02), mk((NR, H, I), 0.02), mk((NR, I, H), 0.02), mk((S, H), 1.0)
+    layer = b2.MoeLayer(ctx, cfg, torch.bfloat16, S)
+    layer.set_graph(True)
+    out, apg = torch.empty_like(x), torch.empty((S, Nz), dtype=torch.float32, device=dev)
+    grads = dict(input=torch.empty_like(x), router=torch.empty_like(router), gate=torch.empty_like(gate),
+                 up=torch.empty_like(up), down=torch.empty_like(down))
+
+    def step():
+        layer.forward(x, router, gate, up, down, out=out)
+        layer.aux_probs_grad(0.01, out=apg)
+        layer.backward(router, gate, up, down, dout, apg, grads=grads)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / steps], device=dev)
+    rows = torch.tensor([float(layer_rt(layer))], device=dev)
+    rows_max, rows_sum = rows.clone(), rows.clone()
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        dist.all_reduce(rows_max, op=dist.ReduceOp.MAX)
+        dist.all_reduce(rows_sum, op=dist.ReduceOp.SUM)
+    counts = layer.artifacts()["token_counts"]
+    del layer
+    torch.cuda.empty_cache()
+    ms = float(ms.item())
+    return {"metric": METRIC + " (Zipf-skewed routing)", "value": world * S / (ms * 1e-3), "unit": "tokens/s",
+            "ms_per_step": ms, "zipf_s": zipf_s, "experts": Nz, "ep": world,
+            "workload": f"Mula-20B-A2B layer shape: hidden 2048, 96 experts top-8, ffn 1024, {S} tokens/GPU, bf16, "
+                        f"Zipf s={zipf_s}, identity expert permutation",
+            "rows_per_rank_max_over_mean": float(rows_max.item()) / (float(rows_sum.item()) / world),
+            "rank0_rows_per_expert_max_over_mean": float(max(counts)) / max(1e-9, sum(counts) / len(counts))}
+
+
 def layer_rt(layer):
     """rows routed to this rank's experts in the last step (sum of the expert group sizes)."""
     return int(layer.artifacts()["rt"])
@@ -236,6 +317,9 @@ def main():
     ap.add_argument("--profile", action="store_true", help="print per-stage times to stderr")
     ap.add_argument("--no-adamw", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA-graph replay")
+    ap.add_argument("--zipf", type=float, default=1.2,
+                    help="Zipf exponent of the config-E load-imbalance line (96 experts); 0 disables it")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
 
@@ -251,6 +335,10 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # one non-default stream per rank for everything (the layer captures its forward and
+    # backward into CUDA graphs on it; the legacy default stream cannot be captured)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
     if world > 1:
         dist.init_process_group("nccl", init_method="env://", device_id=dev)
     hbm_peak, bf16_peak, bf16_sust, peak_kind = measured_peaks()
@@ -263,7 +351,7 @@ def main():
         ids = [b2.Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(ids, src=0)
         nccl_id = ids[0]
-    ctx = b2.Context(local, rank=rank, dp=1, ep=ep, nccl_id=nccl_id)
+    ctx = b2.Context(local, rank=rank, dp=1, ep=ep, nccl_id=nccl_id, stream=stream)
     cfg = b2.MoeConfig(n_experts=N, top_k=K, hidden=H, intermediate=I, ep=ep, token_block=8)
     NR = N // ep
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -272,13 +360,18 @@ def main():
     gate, up, down = mk((NR, H, I), 0.02), mk((NR, H, I), 0.02), mk((NR, I, H), 0.02)
     x, dout = mk((S, H), 1.0), mk((S, H), 1.0)
     layer = b2.MoeLayer(ctx, cfg, torch.bfloat16, S)
+    layer.set_graph(not args.no_graph)
+    out = torch.empty_like(x)
+    apg = torch.empty((S, N), dtype=torch.float32, device=dev)
+    grads = dict(input=torch.empty_like(x), router=torch.empty_like(router), gate=torch.empty_like(gate),
+                 up=torch.empty_like(up), down=torch.empty_like(down))
 
     def step():
-        out = layer.forward(x, router, gate, up, down)
+        layer.forward(x, router, gate, up, down, out=out)
         nf = layer.last_launches()
-        apg = layer.aux_probs_grad(0.01)
-        g = layer.backward(router, gate, up, down, dout, apg)
-        return nf + 1 + layer.last_launches(), out, g
+        layer.aux_probs_grad(0.01, out=apg)
+        layer.backward(router, gate, up, down, dout, apg, grads=grads)
+        return nf + 1 + layer.last_launches(), out, grads
 
     for _ in range(args.warmup):
         step()
@@ -290,11 +383,11 @@ def main():
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
     torch.cuda.synchronize()
-    t0.record()
+    t0.record(stream)
     for _ in range(args.steps):
         n, _, _ = step()
         launches += n
-    t1.record()
+    t1.record(stream)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / args.steps
     if world > 1:
@@ -325,18 +418,16 @@ def main():
     # end to end through the host-buffer entry point (pinned host x/dout in, out/dx back)
     xh, douth = x.cpu().pin_memory(), dout.cpu().pin_memory()
     outh, dxh = torch.empty_like(xh).pin_memory(), torch.empty_like(xh).pin_memory()
-    grads = {"router": torch.empty_like(router), "gate": torch.empty_like(gate), "up": torch.empty_like(up),
-             "down": torch.empty_like(down)}
     for _ in range(2):
         layer.fwd_bwd_host(xh, douth, router, gate, up, down, outh, dxh, grads, 0.01)
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    e0.record()
+    e0.record(stream)
     for _ in range(args.steps):
         layer.fwd_bwd_host(xh, douth, router, gate, up, down, outh, dxh, grads, 0.01)
-    e1.record()
+    e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
     if world > 1:
@@ -346,6 +437,9 @@ def main():
 
     del layer
     torch.cuda.empty_cache()
+    zipf = None
+    if args.zipf > 0:
+        zipf = bench_zipf(torch, b2, ctx, dev, stream, world, rank, args.zipf, max(2, args.steps // 2), 2)
     adamw = None
     if not args.no_adamw:
         adamw = bench_adamw(torch, b2, ctx, dev, 5, 2, world, rank, hbm_peak)
@@ -362,6 +456,7 @@ def main():
         except Exception as e:  # reported, never fatal for the GPU number
             cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
+    traffic, traffic_src = ncu_traffic()
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -371,7 +466,9 @@ def main():
                        "parallelism": f"ep{world} (all-to-all dispatch/combine over NCCL)" if world > 1 else "ep1",
                        "l2": "working set (weights 0.8 GB + activations ~4 GB) >> 126 MB L2; no flush needed"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
-                         "frac": achieved / bf16_peak, "traffic": None, "peak_kind": peak_kind,
+                         "frac": achieved / bf16_peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "traffic_unit": "DRAM bytes per step (6 expert-GEMM launches, ncu --set full)",
+                         "peak_kind": peak_kind,
                          "kernel": "tcgen05 grouped GEMMs (6 kinds, 9 expert GEMMs)",
                          "flop_per_step": gemm_flop, "gemm_ms_per_step": gemm_ms,
                          "frac_of_sustained": achieved / bf16_sust if bf16_sust else None},
@@ -383,6 +480,7 @@ def main():
             "gpu_launches": launches,
             "clocks": clk,
             "adamw": adamw,
+            "zipf": zipf,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -66,6 +66,10 @@ typedef struct {
 typedef struct {
     int64_t step;
     double lr, grad_norm, clip_scale;
+    /* B200 addition: a synced gradient held NaN/Inf (the soft-failure scan of
+     * reliability.cpp:706-723 fused into the norm pass); the update was skipped on the
+     * device and every weight / state is unchanged */
+    int32_t nonfinite;
 } b2_step_stats;
 
 typedef struct b2_ctx b2_ctx;
@@ -154,6 +158,10 @@ int b2_opt_owned(b2_opt* o, int p, int64_t* begin, int64_t* end);
 /* host copies of the fp32 master / exp_avg / exp_avg_sq of param p's owned slice */
 int b2_opt_get_state(b2_opt* o, int p, float* master, float* exp_avg, float* exp_avg_sq);
 int b2_opt_set_step_count(b2_opt* o, int64_t n);
+/* detect_soft_failure (reliability.cpp:706-723, called at train.cpp:193): NaN/Inf in
+ * `loss` or in this rank's LOCAL gradients -> max over WORLD of (node + 1); *sick =
+ * the highest sick node, or -1. Collective over WORLD; synchronises. */
+int b2_opt_detect_soft_failure(b2_opt* o, double loss, int node, int* sick);
 /* adamw_update (optim.cpp:88-107) on device slices */
 int b2_adamw_update(b2_ctx* ctx, float* master, float* exp_avg, float* exp_avg_sq, const void* grad,
                     int grad_dtype, int64_t n, double lr, int64_t step, const b2_adamw_cfg* cfg, void* weight_out,
@@ -168,6 +176,11 @@ int b2_shard_slice(int64_t numel, int group_size, int position, int64_t* begin, 
 int b2_moe_set_profiling(b2_moe* m, int on);
 int b2_moe_stage_times(b2_moe* m, float* ms_host);
 const char* b2_moe_stage_name(int stage);
+/* CUDA-graph mode for b2_moe_forward / b2_moe_backward (B200-side addition; the
+ * reference has no equivalent): a call whose pointer arguments and token count repeat
+ * the previous call's is captured once and then replayed as a single graph launch.
+ * Needs a non-default stream on the context; profiling runs eagerly. */
+int b2_moe_set_graph(b2_moe* m, int on);
 /* number of this library's kernels launched by the last call on the handle */
 int b2_moe_last_launches(b2_moe* m);
 int b2_opt_last_launches(b2_opt* o);

@@ -67,7 +67,8 @@ class CParam(C.Structure):
 
 
 class CStepStats(C.Structure):
-    _fields_ = [("step", C.c_int64), ("lr", C.c_double), ("grad_norm", C.c_double), ("clip_scale", C.c_double)]
+    _fields_ = [("step", C.c_int64), ("lr", C.c_double), ("grad_norm", C.c_double), ("clip_scale", C.c_double),
+                ("nonfinite", C.c_int32)]
 
 
 # every entry point of include/b2moe.h with its ctypes signature
@@ -94,6 +95,7 @@ SIGNATURES = {
     "b2_opt_create": (C.c_int, [P, P, P, C.c_int, C.c_int, C.c_int, C.c_int, P]),
     "b2_opt_destroy": (C.c_int, [P]),
     "b2_opt_step": (C.c_int, [P, P]),
+    "b2_opt_detect_soft_failure": (C.c_int, [P, C.c_double, C.c_int, P]),
     "b2_opt_state_bytes": (C.c_int64, [P]),
     "b2_opt_owned": (C.c_int, [P, C.c_int, P, P]),
     "b2_opt_get_state": (C.c_int, [P, C.c_int, P, P, P]),
@@ -102,6 +104,7 @@ SIGNATURES = {
     "b2_lr_at_step": (C.c_double, [I64, P]),
     "b2_shard_slice": (C.c_int, [I64, C.c_int, C.c_int, P, P]),
     "b2_moe_set_profiling": (C.c_int, [P, C.c_int]),
+    "b2_moe_set_graph": (C.c_int, [P, C.c_int]),
     "b2_moe_stage_times": (C.c_int, [P, P]),
     "b2_moe_stage_name": (C.c_char_p, [C.c_int]),
     "b2_moe_last_launches": (C.c_int, [P]),
@@ -275,21 +278,27 @@ class MoeLayer:
                                     x.shape[0], int(fur), _ptr(out)))
         return out
 
-    def backward(self, router, gate, up, down, dout, aux_probs_grad=None, x=None):
+    def backward(self, router, gate, up, down, dout, aux_probs_grad=None, x=None, grads=None):
+        """Returns dict(input, router, gate, up, down); `grads` (same keys) supplies the outputs."""
         torch = _torch()
-        dx = torch.empty_like(dout)
-        drouter = torch.empty_like(router)
-        dgate, dup, ddown = torch.empty_like(gate), torch.empty_like(up), torch.empty_like(down)
+        if grads is None:
+            grads = dict(input=torch.empty_like(dout), router=torch.empty_like(router), gate=torch.empty_like(gate),
+                         up=torch.empty_like(up), down=torch.empty_like(down))
         _check(lib().b2_moe_backward(self.h, _ptr(router), _ptr(gate), _ptr(up), _ptr(down), _ptr(dout),
-                                     _ptr(aux_probs_grad), _ptr(dx), _ptr(drouter), _ptr(dgate), _ptr(dup),
-                                     _ptr(ddown)))
-        return dict(input=dx, router=drouter, gate=dgate, up=dup, down=ddown)
+                                     _ptr(aux_probs_grad), _ptr(grads["input"]), _ptr(grads["router"]),
+                                     _ptr(grads["gate"]), _ptr(grads["up"]), _ptr(grads["down"])))
+        return grads
 
-    def aux_probs_grad(self, coeff: float):
+    def aux_probs_grad(self, coeff: float, out=None):
         torch = _torch()
-        out = torch.empty((self.s, self.cfg.n_experts), dtype=torch.float32, device=f"cuda:{self.ctx.device}")
+        if out is None:
+            out = torch.empty((self.s, self.cfg.n_experts), dtype=torch.float32, device=f"cuda:{self.ctx.device}")
         _check(lib().b2_moe_aux_probs_grad(self.h, coeff, _ptr(out)))
         return out
+
+    def set_graph(self, on: bool = True):
+        """CUDA-graph replay of repeated forward/backward calls (needs a non-default stream)."""
+        _check(lib().b2_moe_set_graph(self.h, int(on)))
 
     def aux_loss(self) -> float:
         v = C.c_double()
@@ -420,7 +429,14 @@ class ShardedOptimizer:
     def step(self, stats: bool = True):
         s = CStepStats()
         _check(lib().b2_opt_step(self.h, C.byref(s) if stats else None))
-        return dict(step=s.step, lr=s.lr, grad_norm=s.grad_norm, clip_scale=s.clip_scale) if stats else None
+        return dict(step=s.step, lr=s.lr, grad_norm=s.grad_norm, clip_scale=s.clip_scale,
+                    nonfinite=bool(s.nonfinite)) if stats else None
+
+    def detect_soft_failure(self, loss: float, node: int = 0) -> int:
+        """detect_soft_failure (reliability.cpp:706-723): highest sick node over WORLD, or -1."""
+        out = C.c_int()
+        _check(lib().b2_opt_detect_soft_failure(self.h, float(loss), int(node), C.byref(out)))
+        return out.value
 
     def state_bytes(self) -> int:
         return lib().b2_opt_state_bytes(self.h)

@@ -240,4 +240,197 @@ void launch_scale_inplace(void* buf, int dtype, int64_t n, float scale, cudaStre
     B2_LAUNCH_CHECK();
 }
 
+// ---------------------------------------------------------------- multi-tensor step
+
+__device__ __forceinline__ void flag_nonfinite(bool bad, int32_t* flag) {
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x % 32) == 0) atomicExch(flag, 1);
+}
+
+__device__ __forceinline__ double block_sum_fixed(double s, double* red) {
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    return red[0];
+}
+
+__global__ void __launch_bounds__(256) sumsq_chunks_kernel(const OptSeg* __restrict__ segs,
+                                                           const OptChunk* __restrict__ chunks,
+                                                           const int32_t* __restrict__ ids, int grad_dtype,
+                                                           double* __restrict__ partials, int32_t* nonfinite) {
+    __shared__ double red[256];
+    const int cid = ids[blockIdx.x];
+    const OptChunk ch = chunks[cid];
+    const OptSeg sg = segs[ch.seg];
+    const float scale = sg.scale;
+    double s = 0.0;
+    bool bad = false;
+    if (grad_dtype == BF16 && (ch.begin % 8) == 0 &&
+        (((uintptr_t)sg.grad + 2 * ch.begin) & 15) == 0) {
+        const uint4* g8 = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(sg.grad) + ch.begin);
+        const int64_t n8 = ch.len / 8;
+        for (int64_t i = threadIdx.x; i < n8; i += blockDim.x) {
+            const uint4 r = __ldcs(g8 + i);
+            const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                float a = __uint_as_float(w[q] << 16), b = __uint_as_float(w[q] & 0xFFFF0000u);
+                if (scale != 1.f) {
+                    a = __fmul_rn(a, scale);
+                    b = __fmul_rn(b, scale);
+                }
+                bad |= !isfinite(a) || !isfinite(b);
+                s += (double)a * (double)a;
+                s += (double)b * (double)b;
+            }
+        }
+        for (int64_t i = 8 * n8 + threadIdx.x; i < ch.len; i += blockDim.x) {
+            float v = load_grad(sg.grad, grad_dtype, ch.begin + i);
+            if (scale != 1.f) v = __fmul_rn(v, scale);
+            bad |= !isfinite(v);
+            s += (double)v * (double)v;
+        }
+    } else {
+        for (int64_t i = threadIdx.x; i < ch.len; i += blockDim.x) {
+            float v = load_grad(sg.grad, grad_dtype, ch.begin + i);
+            if (scale != 1.f) v = __fmul_rn(v, scale);
+            bad |= !isfinite(v);
+            s += (double)v * (double)v;
+        }
+    }
+    flag_nonfinite(bad, nonfinite);
+    const double tot = block_sum_fixed(s, red);
+    if (threadIdx.x == 0) partials[cid] = tot;
+}
+
+__global__ void __launch_bounds__(1024) norm_final_kernel(const double* __restrict__ partials, int n,
+                                                          double* __restrict__ out) {
+    __shared__ double red[1024];
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    double s = 0.0;
+    const int b = threadIdx.x * per, e = min(n, b + per);
+    for (int i = b; i < e; ++i) s += partials[i];
+    const double tot = block_sum_fixed(s, red);
+    if (threadIdx.x == 0) *out = tot;
+}
+
+__global__ void __launch_bounds__(256) adamw_chunks_kernel(const OptSeg* __restrict__ segs,
+                                                           const OptChunk* __restrict__ chunks,
+                                                           const int32_t* __restrict__ ids, int nids, AdamWDev c,
+                                                           OptStepArgs a, const double* __restrict__ norm_sq,
+                                                           const int32_t* __restrict__ nonfinite) {
+    if (nonfinite && *nonfinite) return;
+    double clip = 1.0;
+    if (norm_sq) {
+        const double norm = sqrt(*norm_sq);
+        if (a.clip_active && norm > a.clip_norm && norm > 0) clip = a.clip_norm / norm;
+    }
+    for (int q = blockIdx.x; q < nids; q += gridDim.x) {
+        const OptChunk ch = chunks[ids[q]];
+        const OptSeg sg = segs[ch.seg];
+        if (sg.vec) {
+            float4* ms = reinterpret_cast<float4*>(sg.master + ch.begin);
+            float4* mo = reinterpret_cast<float4*>(sg.m + ch.begin);
+            float4* ve = reinterpret_cast<float4*>(sg.v + ch.begin);
+            const uint2* gr = reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(sg.grad) + ch.begin);
+            uint2* wo = reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(sg.wout) + ch.begin);
+            const int64_t n4 = ch.len / 4;
+            int64_t i = threadIdx.x;
+            for (; i + (int64_t)blockDim.x < n4; i += 2 * (int64_t)blockDim.x) {
+                const int64_t j = i + blockDim.x;
+                const uint2 g0 = __ldcs(gr + i), g1 = __ldcs(gr + j);
+                float4 m0 = __ldcs(ms + i), a0 = __ldcs(mo + i), v0 = __ldcs(ve + i);
+                float4 m1 = __ldcs(ms + j), a1 = __ldcs(mo + j), v1 = __ldcs(ve + j);
+                uint2 w0, w1;
+                adamw_group4(m0, a0, v0, g0, c, sg.scale, clip, w0);
+                adamw_group4(m1, a1, v1, g1, c, sg.scale, clip, w1);
+                __stcs(ms + i, m0);
+                __stcs(mo + i, a0);
+                __stcs(ve + i, v0);
+                __stcs(wo + i, w0);
+                __stcs(ms + j, m1);
+                __stcs(mo + j, a1);
+                __stcs(ve + j, v1);
+                __stcs(wo + j, w1);
+            }
+            if (i < n4) {
+                const uint2 g0 = __ldcs(gr + i);
+                float4 m0 = __ldcs(ms + i), a0 = __ldcs(mo + i), v0 = __ldcs(ve + i);
+                uint2 w0;
+                adamw_group4(m0, a0, v0, g0, c, sg.scale, clip, w0);
+                __stcs(ms + i, m0);
+                __stcs(mo + i, a0);
+                __stcs(ve + i, v0);
+                __stcs(wo + i, w0);
+            }
+        } else {
+            for (int64_t i = threadIdx.x; i < ch.len; i += blockDim.x) {
+                const int64_t e = ch.begin + i;
+                float g = load_grad(sg.grad, a.grad_dtype, e);
+                if (sg.scale != 1.f) g = __fmul_rn(g, sg.scale);
+                if (clip != 1.0) g = (float)__dmul_rn((double)g, clip);
+                float ms = sg.master[e], mv = sg.m[e], vv = sg.v[e], wf;
+                adamw_elem(ms, mv, vv, g, c, wf);
+                sg.master[e] = ms;
+                sg.m[e] = mv;
+                sg.v[e] = vv;
+                if (a.weight_dtype == F32) {
+                    static_cast<float*>(sg.wout)[e] =
+                        a.round_bf16 ? __uint_as_float((uint32_t)bf16_bits_rne(wf) << 16) : wf;
+                } else {
+                    static_cast<uint16_t*>(sg.wout)[e] = bf16_bits_rne(wf);
+                }
+            }
+        }
+    }
+}
+
+__global__ void nonfinite_scan_kernel(const void* __restrict__ g, int dtype, int64_t n, int32_t* flag) {
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(load_grad(g, dtype, i));
+    flag_nonfinite(bad, flag);
+}
+
+void launch_sumsq_chunks(const OptSeg* segs, const OptChunk* chunks, const int32_t* ids, int nids, int grad_dtype,
+                         double* partials, int32_t* nonfinite, cudaStream_t st) {
+    if (nids <= 0) return;
+    sumsq_chunks_kernel<<<nids, 256, 0, st>>>(segs, chunks, ids, grad_dtype, partials, nonfinite);
+    B2_LAUNCH_CHECK();
+}
+
+void launch_norm_final(const double* partials, int n, double* norm_sq, cudaStream_t st) {
+    norm_final_kernel<<<1, 1024, 0, st>>>(partials, n, norm_sq);
+    B2_LAUNCH_CHECK();
+}
+
+void launch_adamw_chunks(const OptSeg* segs, const OptChunk* chunks, const int32_t* ids, int nids,
+                         const OptStepArgs& a, const double* norm_sq, const int32_t* nonfinite, cudaStream_t st) {
+    if (nids <= 0) return;
+    AdamWDev c;
+    c.lr = a.lr;
+    c.b1 = a.beta1;
+    c.b2 = a.beta2;
+    c.omb1 = 1.0 - a.beta1;
+    c.omb2 = 1.0 - a.beta2;
+    c.eps = a.eps;
+    c.lr_wd = a.lr * a.weight_decay;
+    c.bc1 = a.bc1;
+    c.bc2 = a.bc2;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = std::min(nids, sms * 8);
+    adamw_chunks_kernel<<<grid, 256, 0, st>>>(segs, chunks, ids, nids, c, a, norm_sq, nonfinite);
+    B2_LAUNCH_CHECK();
+}
+
+void launch_nonfinite_scan(const void* g, int dtype, int64_t n, int32_t* flag, cudaStream_t st) {
+    if (n <= 0) return;
+    nonfinite_scan_kernel<<<adamw_grid(n), 256, 0, st>>>(g, dtype, n, flag);
+    B2_LAUNCH_CHECK();
+}
+
 }  // namespace b2

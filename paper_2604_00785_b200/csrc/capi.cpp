@@ -417,8 +417,13 @@ int b2_opt_step(b2_opt* o, b2_step_stats* stats) {
             stats->lr = s.lr;
             stats->grad_norm = s.grad_norm;
             stats->clip_scale = s.clip_scale;
+            stats->nonfinite = s.nonfinite;
         }
     });
+}
+
+int b2_opt_detect_soft_failure(b2_opt* o, double loss, int node, int* sick) {
+    return guard([&] { *sick = o->opt->detect_soft_failure(loss, node); });
 }
 
 int64_t b2_opt_state_bytes(b2_opt* o) { return o ? o->opt->state_bytes() : -1; }
@@ -473,6 +478,7 @@ int b2_shard_slice(int64_t numel, int group_size, int position, int64_t* begin, 
 }
 
 int b2_moe_set_profiling(b2_moe* m, int on) { return guard([&] { m->layer->set_profiling(on != 0); }); }
+int b2_moe_set_graph(b2_moe* m, int on) { return guard([&] { m->layer->set_graph(on != 0); }); }
 int b2_moe_stage_times(b2_moe* m, float* ms_host) { return guard([&] { m->layer->stage_times(ms_host); }); }
 const char* b2_moe_stage_name(int stage) { return MoeLayer::stage_name(stage); }
 

@@ -51,16 +51,26 @@ struct Cfg {
     static constexpr int STAGES = CG == 1 ? 4 : 6;
     static constexpr int TILE_M = BM * CG;
 };
-constexpr int SMEM_BYTES = 6 * (A_BYTES + 128 * BK * 2) + 1024 /*align*/ + 512 /*barriers*/;
-static_assert(SMEM_BYTES >= 4 * (A_BYTES + 256 * BK * 2) + 1024 + 512, "smem sized for both CTA groupings");
+constexpr int SMEM_BYTES = 6 * (A_BYTES + 128 * BK * 2) + 1024 /*align*/ + 1024 /*barriers*/;
+static_assert(SMEM_BYTES >= 4 * (A_BYTES + 256 * BK * 2) + 1024 + 1024, "smem sized for both CTA groupings");
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_EPI_WARPS = 8;  // two warps per TMEM lane quadrant, each half the columns
 constexpr int NUM_THREADS = 128 + 32 * NUM_EPI_WARPS;
+// dgrad epilogue (BwdDownDgrad): each epilogue warp stages the G and U operands of its
+// next 32-row x 32-column chunk by TMA (SWIZZLE_64B boxes) while it works on the current one
+constexpr int EPI_GU_BYTES = 2 * 32 * 32 * 2;  // g box + u box
+template <GemmKind K>
+constexpr int smem_bytes() {
+    return SMEM_BYTES + (K == GemmKind::BwdDownDgrad ? NUM_EPI_WARPS * EPI_GU_BYTES : 0);
+}
+static_assert(SMEM_BYTES + NUM_EPI_WARPS * EPI_GU_BYTES <= 232448, "dgrad kernel exceeds 227 KB of shared memory");
 
 struct Params {
     CUtensorMap mapA;
     CUtensorMap mapB0;
     CUtensorMap mapB1;
+    CUtensorMap mapG;  // BwdDownDgrad epilogue operands (32 x 32 boxes, SWIZZLE_64B)
+    CUtensorMap mapU;
     const int32_t* pad_start;  // [nr+1]
     const int32_t* counts;     // [nr] rows per expert (wgrad K extent)
     int nr, H, I;
@@ -98,8 +108,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// bounded spin: a barrier that never completes (a protocol bug) traps after ~20 s instead
+// of hanging the GPU; `tag` identifies the waiter in the message
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int tag = 0) {
     uint32_t done = 0;
+    uint32_t spins = 0;
+    uint64_t t0 = 0;
     do {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
@@ -108,6 +127,16 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
             : "=r"(done)
             : "r"(bar), "r"(parity)
             : "memory");
+        if (!done && (++spins & 0xFFFFu) == 0) {
+            const uint64_t now = global_ns();
+            if (t0 == 0) {
+                t0 = now;
+            } else if (now - t0 > 20000000000ull) {
+                printf("b2 gemm: mbarrier wait stuck (tag %d, block %d, thread %d, parity %u)\n", tag,
+                       (int)blockIdx.x, (int)threadIdx.x, parity);
+                __trap();
+            }
+        }
     } while (!done);
 }
 
@@ -435,57 +464,7 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const TileInfo& t
             store_row32(p.out0 + row * p.H + col, v, valid);
         }
     } else if constexpr (KIND == GemmKind::BwdDownDgrad) {
-        // SwiGLU backward (kernels.hpp:277-295): dup = silu(g)*d, dgate = u*d*silu'(g).
-        // The G/U loads of a chunk are issued before its TMEM load so they overlap.
-        const int64_t row = ti.m0 + row_in_tile;
-#pragma unroll 1
-        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
-            const int col = ti.n0 + c;
-            const int valid = p.I - col;
-            uint4 g4[4], u4[4];
-            const __nv_bfloat16* gp = p.g + row * p.I + col;
-            const __nv_bfloat16* up = p.u + row * p.I + col;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                g4[q] = make_uint4(0, 0, 0, 0);
-                u4[q] = make_uint4(0, 0, 0, 0);
-            }
-            if (valid >= 32) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    g4[q] = __ldg(reinterpret_cast<const uint4*>(gp) + q);
-                    u4[q] = __ldg(reinterpret_cast<const uint4*>(up) + q);
-                }
-            }
-            tmem_ld32(tacc + c, r);
-            tmem_wait_ld();
-            if (valid <= 0) continue;
-            float dgv[32], duv[32];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t gw[4] = {g4[q].x, g4[q].y, g4[q].z, g4[q].w};
-                const uint32_t uw[4] = {u4[q].x, u4[q].y, u4[q].z, u4[q].w};
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-#pragma unroll
-                    for (int s = 0; s < 2; ++s) {
-                        const int j = 8 * q + 2 * h + s;
-                        float x = s ? bf16_hi(gw[h]) : bf16_lo(gw[h]);
-                        float uu = s ? bf16_hi(uw[h]) : bf16_lo(uw[h]);
-                        if (valid < 32) {
-                            x = j < valid ? __bfloat162float(gp[j]) : 0.f;
-                            uu = j < valid ? __bfloat162float(up[j]) : 0.f;
-                        }
-                        const float d = __uint_as_float(r[j]);
-                        const float sg = __fdividef(1.f, 1.f + __expf(-x));
-                        duv[j] = x * sg * d;
-                        dgv[j] = uu * d * (sg * (1.f + x * (1.f - sg)));
-                    }
-                }
-            }
-            store_row32(p.out0 + row * 2 * p.I + col, dgv, valid);
-            store_row32(p.out0 + row * 2 * p.I + p.I + col, duv, valid);
-        }
+        // the SwiGLU-backward epilogue lives in the kernel body (TMA-staged G/U operands)
     } else if constexpr (KIND == GemmKind::RouterDx) {
         // dx[t] = (sum of t's expert rows of dXperm, slot order | base[t]) + router term
         // (moe.hpp:418-427 scatter-add + 454 matmul_nt); rows beyond S only drain TMEM
@@ -613,6 +592,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
     auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + a); };
     auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + 2 + a); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + STAGES * C::STAGE_BYTES + 8 * (2 * STAGES + 4));
+    auto epi_bar = [&](int w) { return bar0 + 256u + 8u * w; };     // BwdDownDgrad staging barriers
+    const uint32_t epi_base = bar0 + 1024u;                          // 1 KB aligned (bar0 is)
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
@@ -628,6 +609,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull_bar(a), 1);
             mbar_init(tempty_bar(a), NUM_EPI_WARPS * CG);  // the leader's counts both CTAs' epilogues
+        }
+        if constexpr (KIND == GemmKind::BwdDownDgrad) {
+            prefetch_map(&p.mapG);
+            prefetch_map(&p.mapU);
+            for (int w = 0; w < NUM_EPI_WARPS; ++w) mbar_init(epi_bar(w), 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -664,7 +650,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                 const TileInfo ti = tile_info<KIND, CG>(p, ps, t);
                 const int m_own = ti.m0 + BM * (int)rank;
                 for (int kb = 0; kb < ti.kb; ++kb) {
-                    mbar_wait(empty_bar(stage), phase ^ 1u);
+                    mbar_wait(empty_bar(stage), phase ^ 1u, 0);
                     const uint32_t sA = base + stage * C::STAGE_BYTES, sB = sA + A_BYTES;
                     uint32_t fb = full_bar(stage);
                     if constexpr (CG == 2) fb = map_to_rank(fb, 0);
@@ -686,11 +672,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                 const TileInfo ti = tile_info<KIND, CG>(p, ps, t);
                 const int acc = it & 1;
                 const uint32_t acc_phase = (it >> 1) & 1;
-                mbar_wait(tempty_bar(acc), acc_phase ^ 1u);
+                mbar_wait(tempty_bar(acc), acc_phase ^ 1u, 2);
                 tc_fence_after();
                 const uint32_t tacc = tmem_base + acc * BN;
                 for (int kb = 0; kb < ti.kb; ++kb) {
-                    mbar_wait(full_bar(stage), phase);
+                    mbar_wait(full_bar(stage), phase, 1);
                     tc_fence_after();
                     const uint32_t sA = base + stage * C::STAGE_BYTES, sB = sA + A_BYTES;
 #pragma unroll
@@ -723,16 +709,88 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
         const int quad = warp % 4;        // TMEM lanes 32*quad .. 32*quad+31 (hardware rule: warp id % 4)
         const int half = (warp - 4) / 4;  // column half of the tile
         const uint32_t tempty0 = CG == 2 ? map_to_rank(tempty_bar(0), 0) : tempty_bar(0);
+        // BwdDownDgrad: per-warp G/U staging buffer + mbarrier, one chunk ahead
+        const int ew = warp - 4;
+        const uint32_t gu_s = epi_base + (uint32_t)(ew * EPI_GU_BYTES);
+        const uint32_t gu_bar = epi_bar(ew);
+        uint32_t gu_phase = 0;
+        auto gu_issue = [&](const TileInfo& tn, int c) {
+            if (lane == 0 && tn.n0 + c < p.I) {
+                mbar_expect_tx(gu_bar, EPI_GU_BYTES);
+                tma_load_2d(gu_s, &p.mapG, gu_bar, tn.n0 + c, tn.m0 + 32 * quad);
+                tma_load_2d(gu_s + EPI_GU_BYTES / 2, &p.mapU, gu_bar, tn.n0 + c, tn.m0 + 32 * quad);
+            }
+        };
+        if constexpr (KIND == GemmKind::BwdDownDgrad) {
+            if (unit < ntiles) {
+                TileInfo t0i = tile_info<KIND, CG>(p, ps, unit);
+                t0i.m0 += BM * (int)rank;
+                gu_issue(t0i, half * (BN / 2));
+            }
+        }
         int it = 0;
         for (int t = unit; t < ntiles; t += nunits, ++it) {
             TileInfo ti = tile_info<KIND, CG>(p, ps, t);
             ti.m0 += BM * (int)rank;  // this CTA's 128 rows of the pair's tile
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
-            mbar_wait(tfull_bar(acc), acc_phase);
+            mbar_wait(tfull_bar(acc), acc_phase, 3);
             tc_fence_after();
             const uint32_t tacc = tmem_base + ((uint32_t)(32 * quad) << 16) + acc * BN;
-            epilogue_tile<KIND>(p, ti, tacc, 32 * quad + lane, ti.kb == 0, half);
+            if constexpr (KIND == GemmKind::BwdDownDgrad) {
+                const int64_t row = ti.m0 + 32 * quad + lane;
+                const uint8_t* gs = gbase + (gu_s - base);
+                const uint8_t* us = gs + EPI_GU_BYTES / 2;
+                const int sw = (lane >> 1) & 3;
+#pragma unroll 1
+                for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+                    const int col = ti.n0 + c;
+                    const bool live = col < p.I;  // I % 64 == 0: a chunk is all in or all out
+                    float gv[32], uv[32];
+                    if (live) {
+                        mbar_wait(gu_bar, gu_phase, 100 + ew);
+                        gu_phase ^= 1u;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint4 g4 = *reinterpret_cast<const uint4*>(gs + lane * 64 + ((q ^ sw) << 4));
+                            const uint4 u4 = *reinterpret_cast<const uint4*>(us + lane * 64 + ((q ^ sw) << 4));
+                            const uint32_t gw[4] = {g4.x, g4.y, g4.z, g4.w}, uw[4] = {u4.x, u4.y, u4.z, u4.w};
+#pragma unroll
+                            for (int h = 0; h < 4; ++h) {
+                                gv[8 * q + 2 * h] = bf16_lo(gw[h]);
+                                gv[8 * q + 2 * h + 1] = bf16_hi(gw[h]);
+                                uv[8 * q + 2 * h] = bf16_lo(uw[h]);
+                                uv[8 * q + 2 * h + 1] = bf16_hi(uw[h]);
+                            }
+                        }
+                        __syncwarp();
+                    }
+                    // the staging buffer is free again: fetch the next chunk (or the next tile's first)
+                    if (c + 32 < (half + 1) * (BN / 2)) {
+                        gu_issue(ti, c + 32);
+                    } else if (t + nunits < ntiles) {
+                        TileInfo tn = tile_info<KIND, CG>(p, ps, t + nunits);
+                        tn.m0 += BM * (int)rank;
+                        gu_issue(tn, half * (BN / 2));
+                    }
+                    uint32_t r[32];
+                    tmem_ld32(tacc + c, r);
+                    tmem_wait_ld();
+                    if (!live) continue;
+                    float dgv[32], duv[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float x = gv[j], uu = uv[j], d = __uint_as_float(r[j]);
+                        const float sg = __fdividef(1.f, 1.f + __expf(-x));
+                        duv[j] = x * sg * d;
+                        dgv[j] = uu * d * (sg * (1.f + x * (1.f - sg)));
+                    }
+                    store_row32(p.out0 + row * 2 * p.I + col, dgv, 32);
+                    store_row32(p.out0 + row * 2 * p.I + p.I + col, duv, 32);
+                }
+            } else {
+                epilogue_tile<KIND>(p, ti, tacc, 32 * quad + lane, ti.kb == 0, half);
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -772,14 +830,15 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // 2-D bf16 tensor [rows][cols] (cols contiguous), box {bc, br}, 128B swizzle
-static CUtensorMap make_map(const void* ptr, int64_t cols, int64_t rows, int bc, int br) {
+static CUtensorMap make_map(const void* ptr, int64_t cols, int64_t rows, int bc, int br,
+                            CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     CUtensorMap m;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)std::max<int64_t>(rows, 1)};
     cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
     cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)br};
     cuuint32_t es[2] = {1, 1};
     CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
     return m;
@@ -788,15 +847,16 @@ static CUtensorMap make_map(const void* ptr, int64_t cols, int64_t rows, int bc,
 template <GemmKind KIND, int CG>
 static void launch_kind(const Params& p, int grid, cudaStream_t st) {
     static std::once_flag once;
+    constexpr int smem = smem_bytes<KIND>();
     std::call_once(once, [] {
         B2_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<KIND, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     SMEM_BYTES));
+                                     smem));
     });
     grid = std::max(CG, grid / CG * CG);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(NUM_THREADS);
-    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -891,6 +951,8 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.mapA = make_map(a.dy, H, P, 64, BM);
             p.mapB0 = make_map(a.wd, H, nr * I, 64, C2::B_COLS);
             p.mapB1 = p.mapB0;
+            p.mapG = make_map(a.g, I, P, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+            p.mapU = make_map(a.u, I, P, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
             p.n_tiles = (int)ceil_div(I, BN);
             p.num_kb_fixed = (int)ceil_div(H, BK);
             launch_kind<GemmKind::BwdDownDgrad, G>(p, grid, st);

@@ -181,4 +181,39 @@ void launch_scale_inplace(void* buf, int dtype, int64_t n, float scale, cudaStre
 void launch_sumsq(const void* g, int dtype, int64_t n, double scale, double* partials, int nparts, cudaStream_t st);
 void launch_scale_to_f32(const void* src, int dtype, int64_t n, double scale, float* dst, cudaStream_t st);
 
+// ---- multi-tensor optimizer step (adamw.cu): every owned slice of every parameter is cut
+// into chunks of <= kOptChunk elements; one launch covers a list of chunk ids.
+constexpr int64_t kOptChunk = 1 << 16;
+struct OptSeg {
+    const void* grad;  // synced owned grad slice (grad dtype)
+    void* wout;        // owned slice of the weight (weight dtype)
+    float* master;
+    float* m;
+    float* v;
+    int64_t n;
+    float scale;  // (float)(1/g), optim.cpp:155
+    int vec;      // bf16 grad + bf16 weight, 16/8-byte aligned, n % 4 == 0: the x4 fast path
+};
+struct OptChunk {
+    int64_t begin, len;
+    int32_t seg, pad;
+};
+struct OptStepArgs {
+    double lr, beta1, beta2, eps, weight_decay, bc1, bc2;
+    double clip_norm;
+    int clip_active, grad_dtype, weight_dtype, round_bf16;
+};
+// partials[ids[b]] = sum over chunk ids[b] of (float)(g*scale)^2 in fp64; non-finite grads
+// set *nonfinite (the soft-failure scan of reliability.cpp:706-723, fused into this pass)
+void launch_sumsq_chunks(const OptSeg* segs, const OptChunk* chunks, const int32_t* ids, int nids, int grad_dtype,
+                         double* partials, int32_t* nonfinite, cudaStream_t st);
+// *norm_sq = fixed-order sum of partials[0, n)
+void launch_norm_final(const double* partials, int n, double* norm_sq, cudaStream_t st);
+// fused unscale + clip (from *norm_sq) + AdamW + bf16 recast over the listed chunks; a set
+// *nonfinite leaves every state untouched
+void launch_adamw_chunks(const OptSeg* segs, const OptChunk* chunks, const int32_t* ids, int nids,
+                         const OptStepArgs& a, const double* norm_sq, const int32_t* nonfinite, cudaStream_t st);
+// any non-finite element in the n-element buffer -> *flag = 1
+void launch_nonfinite_scan(const void* g, int dtype, int64_t n, int32_t* flag, cudaStream_t st);
+
 }  // namespace b2

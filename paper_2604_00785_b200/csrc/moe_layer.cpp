@@ -135,6 +135,8 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
 }
 
 MoeLayer::~MoeLayer() {
+    gfwd_.reset();
+    gbwd_.reset();
     for (auto& st : prof_ev_)
         for (cudaEvent_t e : st) cudaEventDestroy(e);
     if (sym_) {
@@ -238,6 +240,71 @@ void MoeLayer::stage_times(float* ms) {
     }
 }
 
+void MoeLayer::GraphCache::reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    exec = nullptr;
+    seen = false;
+    key.clear();
+}
+
+void MoeLayer::set_graph(bool on) {
+    B2_CUDA(cudaStreamSynchronize(ctx_.stream));
+    graph_ = on;
+    gfwd_.reset();
+    gbwd_.reset();
+}
+
+template <typename F>
+void MoeLayer::run_graphed(GraphCache& gc, std::vector<const void*> key, F&& body) {
+    cudaStream_t st = ctx_.stream;
+    if (!graph_ || profiling_ || st == nullptr) {  // the legacy default stream cannot be captured
+        body();
+        return;
+    }
+    if (gc.exec && key == gc.key) {
+        B2_CUDA(cudaGraphLaunch(gc.exec, st));
+        launches_ = gc.launches;
+        return;
+    }
+    if (!gc.seen || key != gc.key) {
+        gc.reset();
+        gc.key = std::move(key);
+        gc.seen = true;
+        body();
+        return;
+    }
+    cudaGraph_t g = nullptr;
+    B2_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+        body();
+    } catch (...) {
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        gc.reset();
+        throw;
+    }
+    B2_CUDA(cudaStreamEndCapture(st, &g));
+    const cudaError_t e = cudaGraphInstantiate(&gc.exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+        gc.reset();
+        B2_CUDA(e);
+    }
+    gc.launches = launches_;
+    B2_CUDA(cudaGraphLaunch(gc.exec, st));
+}
+
+// dispatch weights/indices of this forward (learned top-k or FUR; the gathered table at EP > 1)
+void MoeLayer::set_dispatch_tables() {
+    gw_ = fur_ ? (const float*)fw_ : (const float*)topw_;
+    gi_ = fur_ ? (const int32_t*)fi_ : (const int32_t*)topi_;
+    gi_local_ = gi_;
+    if (cfg_.ep > 1) {
+        gi_ = gi_all_;
+        gw_ = gw_all_;
+    }
+}
+
 void MoeLayer::forward(const void* x, const void* router, const void* gate, const void* up, const void* down,
                        int64_t s, bool fur, void* out) {
     check(s >= 0 && s <= smax_, "fast_moe: token count exceeds the layer's capacity");
@@ -247,14 +314,18 @@ void MoeLayer::forward(const void* x, const void* router, const void* gate, cons
     th_ = ceil_div(std::max<int64_t>(t_, 0), cfg_.token_block);
     fur_ = fur;
     x_ = x;
+    set_dispatch_tables();
     launches_ = 0;
     if (profiling_) ++prof_step_;
-    if (dtype_ == F32)
-        forward_t<float>((const float*)x, (const float*)router, (const float*)gate, (const float*)up,
-                         (const float*)down, fur, (float*)out);
-    else
-        forward_t<__nv_bfloat16>((const __nv_bfloat16*)x, (const __nv_bfloat16*)router, (const __nv_bfloat16*)gate,
-                                 (const __nv_bfloat16*)up, (const __nv_bfloat16*)down, fur, (__nv_bfloat16*)out);
+    run_graphed(gfwd_, {x, router, gate, up, down, out, (const void*)(intptr_t)s, (const void*)(intptr_t)fur}, [&] {
+        if (dtype_ == F32)
+            forward_t<float>((const float*)x, (const float*)router, (const float*)gate, (const float*)up,
+                             (const float*)down, fur, (float*)out);
+        else
+            forward_t<__nv_bfloat16>((const __nv_bfloat16*)x, (const __nv_bfloat16*)router,
+                                     (const __nv_bfloat16*)gate, (const __nv_bfloat16*)up,
+                                     (const __nv_bfloat16*)down, fur, (__nv_bfloat16*)out);
+    });
     have_fwd_ = true;
 }
 
@@ -273,23 +344,16 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     if (fur) {
         launch_fur_route(fw_, fi_, S, N, K, st);
         launches_ += 1;
-        gw_ = fw_;
-        gi_ = fi_;
-    } else {
-        gw_ = topw_;
-        gi_ = topi_;
     }
-    gi_local_ = gi_;
     if (E > 1) {
         // the allgathers of weights and indices (moe.hpp:366-367): the reference's gathered
         // routing table; token rows stay where they are until an expert owner pulls them
         B2_CUDA(cudaMemcpyAsync(x_sh_, x, sizeof(T) * (size_t)S * H, cudaMemcpyDeviceToDevice, st));
         B2_NCCL(ncclGroupStart());
-        B2_NCCL(ncclAllGather(gi_, gi_all_, (size_t)S * K, ncclInt32, ctx_.comm->ep.comm, st));
-        B2_NCCL(ncclAllGather(gw_, gw_all_, (size_t)S * K, ncclFloat32, ctx_.comm->ep.comm, st));
+        B2_NCCL(ncclAllGather(gi_local_, gi_all_, (size_t)S * K, ncclInt32, ctx_.comm->ep.comm, st));
+        B2_NCCL(ncclAllGather(fur ? (const float*)fw_ : (const float*)topw_, gw_all_, (size_t)S * K, ncclFloat32,
+                              ctx_.comm->ep.comm, st));
         B2_NCCL(ncclGroupEnd());
-        gi_ = gi_all_;
-        gw_ = gw_all_;
         Tt = E * S;
     }
     // balancing statistics (381-386): mean_probs over the local rows, sel_counts over the
@@ -425,15 +489,21 @@ void MoeLayer::backward(const void* router, const void* gate, const void* up, co
     check(have_fwd_, "fast_moe_backward: no forward state");
     B2_CUDA(cudaSetDevice(ctx_.device));
     launches_ = 0;
-    if (dtype_ == F32)
-        backward_t<float>((const float*)router, (const float*)gate, (const float*)up, (const float*)down,
-                          (const float*)dout, aux_probs_grad, (float*)dx, (float*)drouter, (float*)dgate,
-                          (float*)dup, (float*)ddown);
-    else
-        backward_t<__nv_bfloat16>((const __nv_bfloat16*)router, (const __nv_bfloat16*)gate,
-                                  (const __nv_bfloat16*)up, (const __nv_bfloat16*)down, (const __nv_bfloat16*)dout,
-                                  aux_probs_grad, (__nv_bfloat16*)dx, (__nv_bfloat16*)drouter,
-                                  (__nv_bfloat16*)dgate, (__nv_bfloat16*)dup, (__nv_bfloat16*)ddown);
+    run_graphed(gbwd_,
+                {router, gate, up, down, dout, aux_probs_grad, dx, drouter, dgate, dup, ddown, x_,
+                 (const void*)(intptr_t)s_, (const void*)(intptr_t)fur_},
+                [&] {
+                    if (dtype_ == F32)
+                        backward_t<float>((const float*)router, (const float*)gate, (const float*)up,
+                                          (const float*)down, (const float*)dout, aux_probs_grad, (float*)dx,
+                                          (float*)drouter, (float*)dgate, (float*)dup, (float*)ddown);
+                    else
+                        backward_t<__nv_bfloat16>(
+                            (const __nv_bfloat16*)router, (const __nv_bfloat16*)gate, (const __nv_bfloat16*)up,
+                            (const __nv_bfloat16*)down, (const __nv_bfloat16*)dout, aux_probs_grad,
+                            (__nv_bfloat16*)dx, (__nv_bfloat16*)drouter, (__nv_bfloat16*)dgate,
+                            (__nv_bfloat16*)dup, (__nv_bfloat16*)ddown);
+                });
 }
 
 template <typename T>

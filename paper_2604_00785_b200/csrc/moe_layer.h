@@ -98,6 +98,12 @@ class MoeLayer {
     void set_profiling(bool on);
     void stage_times(float* ms);  // synchronises
 
+    // CUDA-graph mode: a forward (backward) whose arguments repeat the previous call's is
+    // captured once on the rank's stream and replayed as one graph launch afterwards.
+    // Every data-dependent size lives on the device, so a replay is exact. Profiling
+    // runs eagerly.
+    void set_graph(bool on);
+
   private:
     template <typename T>
     void forward_t(const T* x, const T* router, const T* gate, const T* up, const T* down, bool fur, T* out);
@@ -106,6 +112,20 @@ class MoeLayer {
                     const float* aux_probs_grad, T* dx, T* drouter, T* dgate, T* dup, T* ddown);
 
     void mark(int stage, bool end);
+    void set_dispatch_tables();
+
+    struct GraphCache {
+        std::vector<const void*> key;
+        int launches = 0;
+        bool seen = false;
+        cudaGraphExec_t exec = nullptr;
+        void reset();
+    };
+    // eager the first time `key` is seen, captured the second time, replayed after that
+    template <typename F>
+    void run_graphed(GraphCache& gc, std::vector<const void*> key, F&& body);
+    bool graph_ = false;
+    GraphCache gfwd_, gbwd_;
 
     Context& ctx_;
     MoeConfig cfg_;

@@ -62,7 +62,9 @@ ShardedOptimizer::ShardedOptimizer(Context& ctx, const AdamWConfig& cfg, std::ve
     B2_CUDA(cudaSetDevice(ctx_.device));
     const size_t ge = dtype_size(gdt_);
     plan_.resize(params_.size());
-    size_t bytes = 2 * 8 * (size_t)(nparts_ + 2) + 4096;
+    pre_.assign(params_.size(), 0);
+    size_t bytes = 4096;
+    int64_t nchunks = 0;
     for (size_t i = 0; i < params_.size(); ++i) {
         const ParamSlot& p = params_[i];
         check(p.weight && p.grad && p.numel >= 0, "shard plan: parameter needs matching weight/grad");
@@ -83,10 +85,28 @@ ShardedOptimizer::ShardedOptimizer(Context& ctx, const AdamWConfig& cfg, std::ve
         const int gsize = mode_ == ShardMode::ddp ? ctx_.dp : (e.over_dp_ep ? ctx_.dp * ctx_.ep : ctx_.dp);
         if (gsize > 1) bytes += (size_t)(mode_ == ShardMode::ddp ? p.numel : n) * ge + 512;
         if (pre_ep || mode_ == ShardMode::ddp) bytes += (size_t)p.numel * ge + 512;
+        pre_[i] = pre_ep || gsize > 1;
+        nchunks += ceil_div(n, kOptChunk);
     }
+    check(nchunks < (int64_t)1 << 31, "optimizer: too many chunks");
+    n_chunks_ = (int)nchunks;
+    bytes += 8 * (size_t)(n_chunks_ + 2) + sizeof(OptSeg) * params_.size() + sizeof(OptChunk) * (size_t)n_chunks_ +
+             4 * 4 * (size_t)n_chunks_ + 16 * 256;
     arena_.reserve(bytes);
     norm_sq_ = arena_.take<double>(1);
-    partials_ = arena_.take<double>(nparts_ + 1);
+    partials_ = arena_.take<double>(n_chunks_ + 1);
+    nonfinite_ = arena_.take<int32_t>(2);
+    sick_ = nonfinite_ + 1;
+    segs_ = arena_.take<OptSeg>((int64_t)params_.size());
+    chunks_ = arena_.take<OptChunk>(n_chunks_);
+    ids_local_norm_ = arena_.take<int32_t>(n_chunks_);
+    ids_pre_norm_ = arena_.take<int32_t>(n_chunks_);
+    ids_local_ = arena_.take<int32_t>(n_chunks_);
+    ids_pre_ = arena_.take<int32_t>(n_chunks_);
+    std::vector<OptSeg> segs(params_.size());
+    std::vector<OptChunk> chunks;
+    std::vector<int32_t> loc_norm, pre_norm, loc, pre;
+    chunks.reserve((size_t)n_chunks_);
     for (size_t i = 0; i < params_.size(); ++i) {
         const ParamSlot& p = params_[i];
         Entry& e = plan_[i];
@@ -109,112 +129,189 @@ ShardedOptimizer::ShardedOptimizer(Context& ctx, const AdamWConfig& cfg, std::ve
         const int gsize = mode_ == ShardMode::ddp ? ctx_.dp : (e.over_dp_ep ? ctx_.dp * ctx_.ep : ctx_.dp);
         if (gsize > 1 && mode_ != ShardMode::ddp) e.scratch = arena_.take_bytes((size_t)n * ge);
         if (pre_ep || mode_ == ShardMode::ddp) e.scratch_full = arena_.take_bytes((size_t)p.numel * ge);
+        // where the synced owned slice lives (fixed for the optimizer's lifetime)
+        const void* synced;
+        if (mode_ == ShardMode::ddp) synced = (ctx_.dp > 1 || pre_ep) ? e.scratch_full : p.grad;
+        else if (gsize > 1) synced = e.scratch;
+        else synced = (const char*)(pre_ep ? e.scratch_full : p.grad) + (size_t)e.own_b * ge;
+        OptSeg& sg = segs[i];
+        sg.grad = synced;
+        sg.wout = (char*)p.weight + (size_t)e.own_b * dtype_size(wdt_);
+        sg.master = e.master;
+        sg.m = e.m;
+        sg.v = e.v;
+        sg.n = n;
+        sg.scale = (float)(1.0 / (double)gsize);
+        sg.vec = gdt_ == BF16 && wdt_ == BF16 && cfg_.round_weights_bf16 && n % 4 == 0 &&
+                 ((uintptr_t)sg.grad % 8) == 0 && ((uintptr_t)sg.wout % 8) == 0 && ((uintptr_t)e.master % 16) == 0 &&
+                 ((uintptr_t)e.m % 16) == 0 && ((uintptr_t)e.v % 16) == 0;
+        for (int64_t b = 0; b < n; b += kOptChunk) {
+            const int32_t id = (int32_t)chunks.size();
+            chunks.push_back(OptChunk{b, std::min<int64_t>(kOptChunk, n - b), (int32_t)i, 0});
+            (pre_[i] ? pre : loc).push_back(id);
+            if (e.counts) (pre_[i] ? pre_norm : loc_norm).push_back(id);
+        }
     }
+    n_local_norm_ = (int)loc_norm.size();
+    n_pre_norm_ = (int)pre_norm.size();
+    n_local_ = (int)loc.size();
+    n_pre_ = (int)pre.size();
+    auto up = [&](void* dst, const void* src, size_t b) {
+        if (b) B2_CUDA(cudaMemcpyAsync(dst, src, b, cudaMemcpyHostToDevice, ctx_.stream));
+    };
+    up(segs_, segs.data(), sizeof(OptSeg) * segs.size());
+    up(chunks_, chunks.data(), sizeof(OptChunk) * chunks.size());
+    up(ids_local_norm_, loc_norm.data(), 4 * loc_norm.size());
+    up(ids_pre_norm_, pre_norm.data(), 4 * pre_norm.size());
+    up(ids_local_, loc.data(), 4 * loc.size());
+    up(ids_pre_, pre.data(), 4 * pre.size());
+    // partials of chunks that do not count toward the norm stay zero
+    B2_CUDA(cudaMemsetAsync(partials_, 0, 8 * (size_t)(n_chunks_ + 1), ctx_.stream));
+    B2_CUDA(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking));
+    for (cudaEvent_t* ev : {&ev_start_, &ev_synced_, &ev_pre_done_, &ev_ag_})
+        B2_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     B2_CUDA(cudaStreamSynchronize(ctx_.stream));
 }
 
-ShardedOptimizer::~ShardedOptimizer() = default;
+ShardedOptimizer::~ShardedOptimizer() {
+    if (ctx_.stream) cudaStreamSynchronize(ctx_.stream);
+    if (comm_stream_) {
+        cudaStreamSynchronize(comm_stream_);
+        cudaStreamDestroy(comm_stream_);
+    }
+    for (cudaEvent_t ev : {ev_start_, ev_synced_, ev_pre_done_, ev_ag_})
+        if (ev) cudaEventDestroy(ev);
+}
 
 const Group* ShardedOptimizer::group_of(const Entry& e) const {
     if (!ctx_.comm) return nullptr;
     return e.over_dp_ep ? &ctx_.comm->dp_ep : &ctx_.comm->dp;
 }
 
+// Stream schedule of one step (two streams, four events):
+//   comm   : [EP all-reduce / reduce-scatter of every synced param] ......... [all-gather of them]
+//   compute: sumsq(local) -> wait synced -> sumsq(synced) -> norm -> AdamW(synced) -> AdamW(local) -> wait AG
+// The expert slices (no collective at DP = 1) keep the HBM busy while NVLink moves the
+// non-expert ones; the all-gather of the non-expert slices overlaps the expert update.
 StepStats ShardedOptimizer::step(bool want_stats) {
     B2_CUDA(cudaSetDevice(ctx_.device));
-    cudaStream_t st = ctx_.stream;
+    cudaStream_t st = ctx_.stream, cs = comm_stream_;
     launches_ = 0;
     StepStats stats;
     stats.step = step_count_;
     stats.lr = lr_at_step(step_count_, cfg_);
-    const size_t ge = dtype_size(gdt_);
-    // 1. gradient sync -> synced owned slice + its mean scale (optim.cpp:136-158)
-    std::vector<const void*> synced(params_.size());
-    std::vector<float> scale(params_.size(), 1.f);
+    B2_CUDA(cudaMemsetAsync(nonfinite_, 0, 4, st));
+    const bool any_pre = n_pre_ > 0;
+    if (any_pre) {
+        B2_CUDA(cudaEventRecord(ev_start_, st));
+        B2_CUDA(cudaStreamWaitEvent(cs, ev_start_, 0));
+    }
+    // 1. gradient sync of the params that need it (optim.cpp:136-158), on the comm stream
     for (size_t i = 0; i < params_.size(); ++i) {
+        if (!pre_[i]) continue;
         const ParamSlot& p = params_[i];
         Entry& e = plan_[i];
         const void* src = p.grad;
         if (!p.expert && mode_ != ShardMode::epso && ctx_.ep > 1) {
             // allreduce_mean over EP (optim.cpp:142-143)
-            all_reduce_sum(ctx_.comm->ep, p.grad, e.scratch_full, p.numel, nccl_dtype(gdt_), st);
-            launch_scale_inplace(e.scratch_full, gdt_, p.numel, (float)(1.0 / (double)ctx_.ep), st);
+            all_reduce_sum(ctx_.comm->ep, p.grad, e.scratch_full, p.numel, nccl_dtype(gdt_), cs);
+            launch_scale_inplace(e.scratch_full, gdt_, p.numel, (float)(1.0 / (double)ctx_.ep), cs);
             ++launches_;
             src = e.scratch_full;
         }
         if (mode_ == ShardMode::ddp) {
-            if (ctx_.dp > 1) {
-                all_reduce_sum(ctx_.comm->dp, src, e.scratch_full, p.numel, nccl_dtype(gdt_), st);
-                src = e.scratch_full;
-            }
-            synced[i] = src;
-            scale[i] = (float)(1.0 / (double)ctx_.dp);
+            if (ctx_.dp > 1) all_reduce_sum(ctx_.comm->dp, src, e.scratch_full, p.numel, nccl_dtype(gdt_), cs);
         } else {
-            const Group* g = group_of(e);
             const int gsize = e.over_dp_ep ? ctx_.dp * ctx_.ep : ctx_.dp;
-            if (gsize > 1) {
-                reduce_scatter_v(*g, src, e.scratch, p.numel, gdt_, st);
-                synced[i] = e.scratch;
-            } else {
-                synced[i] = (const char*)src + (size_t)e.own_b * ge;
-            }
-            scale[i] = (float)(1.0 / (double)gsize);
+            if (gsize > 1) reduce_scatter_v(*group_of(e), src, e.scratch, p.numel, gdt_, cs);
         }
     }
-    // 2. global grad norm over counted slices, all-reduced over WORLD (optim.cpp:160-166)
-    bool first = true;
-    for (size_t i = 0; i < params_.size(); ++i) {
-        const Entry& e = plan_[i];
-        if (!e.counts) continue;
-        launch_sumsq_acc(synced[i], gdt_, e.own_e - e.own_b, scale[i], partials_, nparts_, norm_sq_, first, st);
-        launches_ += 2;
-        first = false;
+    if (any_pre) B2_CUDA(cudaEventRecord(ev_synced_, cs));
+    // 2. global grad norm over counted slices (optim.cpp:160-166): local slices while the
+    // collectives run, then the synced ones; fp64 all-reduce over WORLD. The same pass
+    // flags NaN/Inf (the soft-failure scan).
+    launch_sumsq_chunks(segs_, chunks_, ids_local_norm_, n_local_norm_, gdt_, partials_, nonfinite_, st);
+    if (any_pre) B2_CUDA(cudaStreamWaitEvent(st, ev_synced_, 0));
+    launch_sumsq_chunks(segs_, chunks_, ids_pre_norm_, n_pre_norm_, gdt_, partials_, nonfinite_, st);
+    launch_norm_final(partials_, n_chunks_, norm_sq_, st);
+    launches_ += (n_local_norm_ > 0) + (n_pre_norm_ > 0) + 1;
+    if (ctx_.world > 1) {
+        all_reduce_sum(ctx_.comm->world, norm_sq_, norm_sq_, 1, ncclFloat64, st);
+        ncclRedOp_t mx = ncclMax;
+        B2_NCCL(ncclAllReduce(nonfinite_, nonfinite_, 1, ncclInt32, mx, ctx_.comm->world.comm, st));
     }
-    if (first) B2_CUDA(cudaMemsetAsync(norm_sq_, 0, 8, st));
-    if (ctx_.world > 1) all_reduce_sum(ctx_.comm->world, norm_sq_, norm_sq_, 1, ncclFloat64, st);
     const bool clip_active = !cfg_.clip_after_warmup_only || step_count_ >= cfg_.warmup_steps;
-    // 3. fused unscale + clip + AdamW + bf16 recast on the owned slices (optim.cpp:174-184)
-    const double bc1 = 1.0 - std::pow(cfg_.beta1, (double)(step_count_ + 1));
-    const double bc2 = 1.0 - std::pow(cfg_.beta2, (double)(step_count_ + 1));
-    for (size_t i = 0; i < params_.size(); ++i) {
-        const ParamSlot& p = params_[i];
-        Entry& e = plan_[i];
-        AdamWKernelArgs a{};
-        a.master = e.master;
-        a.m = e.m;
-        a.v = e.v;
-        a.grad = synced[i];
-        a.weight_out = (char*)p.weight + (size_t)e.own_b * dtype_size(wdt_);
-        a.n = e.own_e - e.own_b;
-        a.grad_dtype = gdt_;
-        a.weight_dtype = wdt_;
-        a.lr = stats.lr;
-        a.beta1 = cfg_.beta1;
-        a.beta2 = cfg_.beta2;
-        a.eps = cfg_.eps;
-        a.weight_decay = cfg_.weight_decay;
-        a.bc1 = bc1;
-        a.bc2 = bc2;
-        a.grad_scale = scale[i];
-        a.round_bf16 = cfg_.round_weights_bf16 ? 1 : 0;
-        launch_adamw_full(a, norm_sq_, cfg_.clip_norm, clip_active ? 1 : 0, st);
-        ++launches_;
-        // 4. re-share (optim.cpp:185-190)
-        if (mode_ != ShardMode::ddp) {
+    // 3. fused unscale + clip + AdamW + bf16 recast (optim.cpp:174-184): synced params first
+    OptStepArgs a{};
+    a.lr = stats.lr;
+    a.beta1 = cfg_.beta1;
+    a.beta2 = cfg_.beta2;
+    a.eps = cfg_.eps;
+    a.weight_decay = cfg_.weight_decay;
+    a.bc1 = 1.0 - std::pow(cfg_.beta1, (double)(step_count_ + 1));
+    a.bc2 = 1.0 - std::pow(cfg_.beta2, (double)(step_count_ + 1));
+    a.clip_norm = cfg_.clip_norm;
+    a.clip_active = clip_active ? 1 : 0;
+    a.grad_dtype = gdt_;
+    a.weight_dtype = wdt_;
+    a.round_bf16 = cfg_.round_weights_bf16 ? 1 : 0;
+    launch_adamw_chunks(segs_, chunks_, ids_pre_, n_pre_, a, norm_sq_, nonfinite_, st);
+    launches_ += n_pre_ > 0;
+    // 4. re-share the updated slices (optim.cpp:185-190) on the comm stream, overlapping
+    // the update of the local (expert) slices
+    bool any_ag = false;
+    if (mode_ != ShardMode::ddp && any_pre) {
+        B2_CUDA(cudaEventRecord(ev_pre_done_, st));
+        B2_CUDA(cudaStreamWaitEvent(cs, ev_pre_done_, 0));
+        for (size_t i = 0; i < params_.size(); ++i) {
+            const Entry& e = plan_[i];
             const int gsize = e.over_dp_ep ? ctx_.dp * ctx_.ep : ctx_.dp;
-            if (gsize > 1) all_gather_v(*group_of(e), p.weight, p.numel, wdt_, st);
+            if (!pre_[i] || gsize <= 1) continue;
+            all_gather_v(*group_of(e), params_[i].weight, params_[i].numel, wdt_, cs);
+            any_ag = true;
         }
+        B2_CUDA(cudaEventRecord(ev_ag_, cs));
     }
+    launch_adamw_chunks(segs_, chunks_, ids_local_, n_local_, a, norm_sq_, nonfinite_, st);
+    launches_ += n_local_ > 0;
+    if (any_ag || (mode_ != ShardMode::ddp && any_pre)) B2_CUDA(cudaStreamWaitEvent(st, ev_ag_, 0));
     if (want_stats) {
         double sq = 0;
+        int32_t bad = 0;
         B2_CUDA(cudaMemcpyAsync(&sq, norm_sq_, 8, cudaMemcpyDeviceToHost, st));
+        B2_CUDA(cudaMemcpyAsync(&bad, nonfinite_, 4, cudaMemcpyDeviceToHost, st));
         B2_CUDA(cudaStreamSynchronize(st));
         stats.grad_norm = std::sqrt(sq);
+        stats.nonfinite = bad;
         if (clip_active && stats.grad_norm > cfg_.clip_norm && stats.grad_norm > 0)
             stats.clip_scale = cfg_.clip_norm / stats.grad_norm;
     }
     step_count_++;
     return stats;
+}
+
+int ShardedOptimizer::detect_soft_failure(double loss, int node) {
+    B2_CUDA(cudaSetDevice(ctx_.device));
+    cudaStream_t st = ctx_.stream;
+    B2_CUDA(cudaMemsetAsync(sick_, 0, 4, st));
+    if (std::isfinite(loss)) {
+        for (const ParamSlot& p : params_) launch_nonfinite_scan(p.grad, gdt_, p.numel, sick_, st);
+    } else {
+        const int32_t one = 1;
+        B2_CUDA(cudaMemcpyAsync(sick_, &one, 4, cudaMemcpyHostToDevice, st));
+    }
+    int32_t flag = 0;
+    B2_CUDA(cudaMemcpyAsync(&flag, sick_, 4, cudaMemcpyDeviceToHost, st));
+    B2_CUDA(cudaStreamSynchronize(st));
+    // flag = bad ? node + 1 : 0, max over WORLD (reliability.cpp:719-722)
+    int32_t v = flag ? node + 1 : 0;
+    if (ctx_.world > 1) {
+        B2_CUDA(cudaMemcpyAsync(sick_, &v, 4, cudaMemcpyHostToDevice, st));
+        B2_NCCL(ncclAllReduce(sick_, sick_, 1, ncclInt32, ncclMax, ctx_.comm->world.comm, st));
+        B2_CUDA(cudaMemcpyAsync(&v, sick_, 4, cudaMemcpyDeviceToHost, st));
+        B2_CUDA(cudaStreamSynchronize(st));
+    }
+    return v - 1;
 }
 
 int64_t ShardedOptimizer::state_bytes() const {

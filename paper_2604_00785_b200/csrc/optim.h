@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "comm.h"
+#include "kernels.h"
 #include "moe_layer.h"
 
 namespace b2 {
@@ -34,6 +35,7 @@ struct ParamSlot {
 struct StepStats {
     int64_t step = 0;
     double lr = 0, grad_norm = 0, clip_scale = 1.0;
+    int nonfinite = 0;  // a synced grad held NaN/Inf: the update was skipped on the device
 };
 
 class ShardedOptimizer {
@@ -48,6 +50,10 @@ class ShardedOptimizer {
     void get_state(int p, float* master, float* m, float* v);
     void set_step_count(int64_t n) { step_count_ = n; }
     int last_launches() const { return launches_; }
+    // detect_soft_failure (reliability.cpp:706-723): scans this rank's LOCAL grads (and
+    // the loss) for NaN/Inf and max-all-reduces (node + 1) over WORLD; returns the
+    // highest sick node or -1. Synchronises.
+    int detect_soft_failure(double loss, int node);
 
   private:
     struct Entry {
@@ -67,8 +73,17 @@ class ShardedOptimizer {
     std::vector<Entry> plan_;
     Arena arena_;
     double* norm_sq_ = nullptr;  // device
-    double* partials_ = nullptr;
-    int nparts_ = 1184;
+    double* partials_ = nullptr;  // one fp64 partial per chunk, param-major (fixed reduction order)
+    int32_t* nonfinite_ = nullptr;
+    int32_t* sick_ = nullptr;
+    // multi-tensor tables: segments (one per param), chunks, and chunk-id lists per phase
+    OptSeg* segs_ = nullptr;
+    OptChunk* chunks_ = nullptr;
+    int32_t *ids_local_norm_ = nullptr, *ids_pre_norm_ = nullptr, *ids_local_ = nullptr, *ids_pre_ = nullptr;
+    int n_chunks_ = 0, n_local_norm_ = 0, n_pre_norm_ = 0, n_local_ = 0, n_pre_ = 0;
+    std::vector<char> pre_;  // param needs a collective before its update
+    cudaStream_t comm_stream_ = nullptr;
+    cudaEvent_t ev_start_ = nullptr, ev_synced_ = nullptr, ev_pre_done_ = nullptr, ev_ag_ = nullptr;
     int64_t step_count_ = 0;
     int launches_ = 0;
 };

@@ -115,20 +115,53 @@ __global__ void combine_kernel(const T* __restrict__ y, const int32_t* __restric
     if (t >= T_tok) return;
     const int j0 = cum_expert_counts[t], j1 = cum_expert_counts[t + 1];
     if (vec_ok<T>(H)) {
-        constexpr int V = V16<T>::n;
+        // the slot rows of a column block are loaded together (up to 8 in flight per lane),
+        // then summed in slot order
+        constexpr int V = V16<T>::n, MAXJ = 8;
+        int64_t rows[MAXJ];
+        float wv[MAXJ];
+        const int nj0 = min(MAXJ, j1 - j0);
+#pragma unroll
+        for (int q = 0; q < MAXJ; ++q) {
+            rows[q] = q < nj0 ? slot_prow[j0 + q] : 0;
+            wv[q] = (q < nj0 && gw) ? gw[(int64_t)t * K + selected_k[j0 + q]] : 1.f;
+        }
         for (int c0 = lane * V; c0 < H; c0 += 32 * V) {
-            float acc[V], v[V];
+            float acc[V];
 #pragma unroll
-            for (int q = 0; q < V; ++q) acc[q] = 0.f;
-            for (int j = j0; j < j1; ++j) {
-                V16<T>::load(y + (int64_t)slot_prow[j] * H + c0, v);
-                if (gw) {
-                    const float wv = gw[(int64_t)t * K + selected_k[j]];
+            for (int z = 0; z < V; ++z) acc[z] = 0.f;
+            for (int jb = j0; jb < j1; jb += MAXJ) {
+                const int nj = min(MAXJ, j1 - jb);
+                if (jb != j0) {  // more than 8 local slots (K > 8): reload the slot table
 #pragma unroll
-                    for (int q = 0; q < V; ++q) acc[q] = __fadd_rn(acc[q], __fmul_rn(wv, v[q]));
-                } else {  // unweighted: the scatter-add of dX rows to their token (moe.hpp:418-423)
+                    for (int q = 0; q < MAXJ; ++q) {
+                        rows[q] = q < nj ? slot_prow[jb + q] : 0;
+                        wv[q] = (q < nj && gw) ? gw[(int64_t)t * K + selected_k[jb + q]] : 1.f;
+                    }
+                }
+                int4 raw[MAXJ];
 #pragma unroll
-                    for (int q = 0; q < V; ++q) acc[q] = __fadd_rn(acc[q], v[q]);
+                for (int q = 0; q < MAXJ; ++q)
+                    if (q < nj) raw[q] = __ldg(reinterpret_cast<const int4*>(y + rows[q] * H + c0));
+#pragma unroll
+                for (int q = 0; q < MAXJ; ++q) {
+                    if (q >= nj) break;
+                    float v[V];
+                    V16<T>::unpack(raw[q], v);
+                    if (gw) {
+#pragma unroll
+                        for (int z = 0; z < V; ++z) acc[z] = __fadd_rn(acc[z], __fmul_rn(wv[q], v[z]));
+                    } else {  // unweighted: the scatter-add of dX rows to their token (moe.hpp:418-423)
+#pragma unroll
+                        for (int z = 0; z < V; ++z) acc[z] = __fadd_rn(acc[z], v[z]);
+                    }
+                }
+            }
+            if (j1 - j0 > MAXJ) {  // restore the first block's table for the next column block
+#pragma unroll
+                for (int q = 0; q < MAXJ; ++q) {
+                    rows[q] = q < nj0 ? slot_prow[j0 + q] : 0;
+                    wv[q] = (q < nj0 && gw) ? gw[(int64_t)t * K + selected_k[j0 + q]] : 1.f;
                 }
             }
             V16<T>::store(out + (int64_t)t * H + c0, acc);

@@ -80,6 +80,22 @@ def test_route_logits_bitwise(b2ctx, orc, H, N, K):
     assert np.array_equal(w.cpu().numpy(), wo)
 
 
+@pytest.mark.parametrize("S,H,N,K", [(300, 2048, 64, 8), (129, 256, 96, 8), (64, 64, 8, 2), (77, 96, 24, 3),
+                                     (1000, 160, 200, 4)])
+def test_route_logits_bf16_bitwise(b2ctx, orc, S, H, N, K):
+    """bf16 inputs take the cp.async/f32x2 logits kernel (H % 32 == 0, N % 8 == 0):
+    bit-identical to the reference's fp32 multiply-then-add on the same rounded values."""
+    b2, ctx = b2ctx
+    ocfg, bcfg = cfg_pair(n_experts=N, top_k=K, hidden=H, intermediate=64)
+    rb = lambda a: torch.from_numpy(np.ascontiguousarray(a)).bfloat16()
+    x, router = rb(orc.normal((S, H), 77, 0, 1.0)), rb(orc.normal((H, N), 5, 1, 0.2))
+    lo, po, wo, io = orc.route_f32(ocfg, x.float().numpy(), router.float().numpy())
+    logits, probs, w, idx = b2.route(ctx, bcfg, x.cuda(), router.cuda())
+    assert np.array_equal(logits.cpu().numpy(), lo)
+    assert np.array_equal(idx.cpu().numpy(), io)
+    assert np.array_equal(w.cpu().numpy(), wo)
+
+
 FOUR = np.array([[0, 1], [0, 2], [1, 3], [2, 3]], np.int64)
 
 
@@ -214,3 +230,95 @@ def test_layer_bf16_matches_fp32_oracle(b2ctx, orc, case):
         want = ref[key][0] if key == "drouter" else ref[key]
         e = scale_err(got[gkey], want)
         assert e <= TOL_BF16, f"{key}: scale_err {e}"
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_graph_replay_matches_eager(b2ctx, dtype):
+    """CUDA-graph mode: the captured forward/backward replays bit-identically to the
+    eager path, including after the inputs behind the same pointers change (every
+    data-dependent size is read on the device)."""
+    b2, _ = b2ctx
+    dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    stream = torch.cuda.Stream()
+    ctx = b2.Context(0, stream=stream)
+    cfg = b2.MoeConfig(n_experts=16, top_k=4, hidden=256, intermediate=128)
+    S = 300
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    mk = lambda shape, std: (torch.randn(shape, device="cuda", generator=gen) * std).to(dt)
+    router, gate, up, down = mk((256, 16), 0.05), mk((16, 256, 128), 0.05), mk((16, 256, 128), 0.05), \
+        mk((16, 128, 256), 0.05)
+    xs = [mk((S, 256), 1.0) for _ in range(3)]
+    douts = [mk((S, 256), 1.0) for _ in range(3)]
+
+    def run(layer, x_buf, d_buf, out, apg, grads, i):
+        with torch.cuda.stream(stream):
+            x_buf.copy_(xs[i])
+            d_buf.copy_(douts[i])
+            layer.forward(x_buf, router, gate, up, down, out=out)
+            layer.aux_probs_grad(0.01, out=apg)
+            layer.backward(router, gate, up, down, d_buf, apg, grads=grads)
+        stream.synchronize()
+        return [out.clone()] + [grads[k].clone() for k in ("input", "router", "gate", "up", "down")]
+
+    def bufs():
+        with torch.cuda.stream(stream):
+            out = torch.empty((S, 256), dtype=dt, device="cuda")
+            grads = dict(input=torch.empty((S, 256), dtype=dt, device="cuda"), router=torch.empty_like(router),
+                         gate=torch.empty_like(gate), up=torch.empty_like(up), down=torch.empty_like(down))
+            apg = torch.empty((S, 16), dtype=torch.float32, device="cuda")
+            return torch.empty_like(xs[0]), torch.empty_like(douts[0]), out, apg, grads
+
+    eager = b2.MoeLayer(ctx, cfg, dt, S)
+    want = [run(eager, *bufs(), i) for i in range(3)]
+    graphed = b2.MoeLayer(ctx, cfg, dt, S)
+    graphed.set_graph(True)
+    b = bufs()
+    got = [run(graphed, *b, i) for i in (0, 1, 2, 0, 1)]  # eager, capture, replay x3
+    for g, i in zip(got, (0, 1, 2, 0, 1)):
+        for a, w in zip(g, want[i]):
+            assert torch.equal(a, w)
+    assert graphed.last_launches() > 0
+
+
+def zipf_inputs(S, H, N, s, seed=4242):
+    """Config-E style skewed routing: logits[t,e] = log z_e + Gumbel(t,e) with
+    z_e ∝ (e+1)^-s (identity permutation: the hottest experts first). Realised through the
+    layer's own router: x[t, :N] holds the logits, Wr = [I_N; 0], so x·Wr reproduces them."""
+    rng = np.random.default_rng(seed)
+    z = (np.arange(N) + 1.0) ** -s
+    z /= z.sum()
+    gumbel = -np.log(-np.log(rng.uniform(1e-12, 1.0, (S, N))))
+    x = rng.standard_normal((S, H)).astype(np.float32)
+    x[:, :N] = (np.log(z)[None, :] + gumbel).astype(np.float32)
+    router = np.zeros((H, N), np.float32)
+    router[np.arange(N), np.arange(N)] = 1.0
+    return x, router
+
+
+@pytest.mark.parametrize("s,K", [(1.2, 4), (3.0, 1)])
+def test_layer_bf16_zipf_skewed_routing(b2ctx, orc, s, K):
+    """Load-imbalance stress: hot experts get many 256-row tiles, cold ones few or none
+    (empty groups in every GEMM kind, zero weight-gradients)."""
+    b2, ctx = b2ctx
+    S, H, N, I = 512, 256, 16, 128
+    ocfg, bcfg = cfg_pair(n_experts=N, top_k=K, hidden=H, intermediate=I)
+    rb = lambda a: torch.from_numpy(np.ascontiguousarray(a)).bfloat16().float().numpy()
+    x, router = zipf_inputs(S, H, N, s)
+    x, router = rb(x), rb(router)
+    _, gate, up, down = (rb(t) for t in orc.expert_weights(ocfg, 1234, 0.02))
+    dout = rb(orc.normal((S, H), 78, 0, 1.0))
+    ref = orc.moe_layer(ocfg, S, x, router, gate, up, down, dout, aux_coeff=0.01)
+    counts = np.bincount(ref["indices"].ravel(), minlength=N)
+    assert counts.max() >= 3 * counts.mean() and (s < 2 or counts.min() == 0), counts
+    got = run_layer(b2, ctx, bcfg, torch.bfloat16, x, router, gate, up, down, dout, aux_coeff=0.01)
+    assert np.array_equal(got["indices"], ref["indices"])
+    _compare_artifacts(got["artifacts"], orc.artifacts(ocfg, ref["indices"], 0))
+    assert rel_err(got["out"], ref["out"]) <= TOL_BF16
+    assert rel_err(got["input"], ref["dx"]) <= TOL_BF16
+    for key, gkey in [("drouter", "router"), ("dgate", "gate"), ("dup", "up"), ("ddown", "down")]:
+        want = ref[key][0] if key == "drouter" else ref[key]
+        e = scale_err(got[gkey], want)
+        assert e <= TOL_BF16, f"{key}: scale_err {e}"
+    # experts that received no rows have exactly zero weight gradients
+    for e in np.where(counts == 0)[0]:
+        assert not got["gate"][e].any() and not got["up"][e].any() and not got["down"][e].any()

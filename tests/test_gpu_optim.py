@@ -1,0 +1,100 @@
+"""Single-GPU parity of the multi-tensor ShardedOptimizer step (optim.cpp:130-194) with the
+oracle's ShardedOptimizer (oracle/moe_oracle.c, pinned bitwise to the reference), and the
+soft-failure paths (reliability.cpp:706-723).
+
+Bars: bf16 / fp32 grads, weights, fp32 masters and moments bitwise equal to the oracle
+after several steps (warmup, clipping active); grad-norm statistics within 1e-12 relative
+(the fp64 sum is reduced in a different, fixed order)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+# ragged sizes: a slice that is not a multiple of 4, one spanning several 64K chunks
+NUMEL = [33, 130_001, 7, 4096, 70_000]
+CLS = [0, 1, 0, 1, 1]
+
+
+@pytest.fixture(scope="module")
+def b2ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2604_00785_b200 as b2
+    return b2, b2.Context(0)
+
+
+def make(orc, dtype, steps, seed=3):
+    total = sum(NUMEL)
+    w0 = np.concatenate([orc.normal((n,), 402 + p, 1, 0.05) for p, n in enumerate(NUMEL)])
+    rng = np.random.default_rng(seed)
+    grads = (rng.standard_normal((steps, total)) * 0.02).astype(np.float32)
+    if dtype == torch.bfloat16:  # the oracle sees the same bf16-rounded values
+        w0 = torch.from_numpy(w0).bfloat16().float().numpy()
+        grads = torch.from_numpy(grads).bfloat16().float().numpy()
+    return w0, grads
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32], ids=["bf16", "f32"])
+@pytest.mark.parametrize("mode", [0, 1, 2], ids=["ddp", "so", "epso"])
+def test_step_matches_oracle(b2ctx, orc, dtype, mode):
+    b2, ctx = b2ctx
+    steps = 5
+    w0, grads = make(orc, dtype, steps)
+    W = torch.from_numpy(w0).cuda().to(dtype)
+    G = torch.zeros(W.numel(), dtype=dtype, device="cuda")
+    params, off = [], 0
+    for n, c in zip(NUMEL, CLS):
+        params.append((W[off:off + n], G[off:off + n], c, 0))
+        off += n
+    cfg = b2.AdamWConfig(warmup_steps=2, total_steps=50, peak_lr=1e-2, min_lr=1e-3, clip_norm=1.0)
+    opt = b2.ShardedOptimizer(ctx, cfg, params, mode)
+    got = []
+    for s in range(steps):
+        G.copy_(torch.from_numpy(grads[s]).to(dtype))
+        got.append(opt.step(stats=True))
+    torch.cuda.synchronize()
+    ocfg = orc.adamw_cfg(warmup_steps=2, total_steps=50, peak_lr=1e-2, min_lr=1e-3, clip_norm=1.0)
+    ref = orc.sharded_steps(1, 1, 1, mode, ocfg, NUMEL, CLS, [0] * len(NUMEL), w0[None], grads[:, None, :])
+    want_w = ref["weights"][0]
+    if dtype == torch.bfloat16:
+        assert np.array_equal(W.float().cpu().numpy(), want_w)
+    else:
+        assert np.array_equal(W.cpu().numpy(), want_w)
+    ms = np.concatenate([opt.state(p)[0] for p in range(len(NUMEL))])
+    m = np.concatenate([opt.state(p)[1] for p in range(len(NUMEL))])
+    v = np.concatenate([opt.state(p)[2] for p in range(len(NUMEL))])
+    assert np.array_equal(ms, ref["master"][0]) and np.array_equal(m, ref["m"][0]) and np.array_equal(v, ref["v"][0])
+    for s, st in enumerate(got):
+        lr, norm, clip = ref["stats"][s, 0]
+        assert st["lr"] == lr and abs(st["grad_norm"] - norm) <= 1e-12 * norm and not st["nonfinite"]
+        assert abs(st["clip_scale"] - clip) <= 1e-12
+    assert any(st["clip_scale"] < 1.0 for st in got)  # clipping was exercised
+    assert opt.state_bytes() == 12 * sum(NUMEL)
+    assert opt.last_launches() > 0
+
+
+def test_nonfinite_grad_skips_update_and_is_detected(b2ctx, orc):
+    b2, ctx = b2ctx
+    w0, grads = make(orc, torch.bfloat16, 2)
+    W = torch.from_numpy(w0).cuda().bfloat16()
+    G = torch.from_numpy(grads[0]).cuda().bfloat16()
+    params, off = [], 0
+    for n, c in zip(NUMEL, CLS):
+        params.append((W[off:off + n], G[off:off + n], c, 0))
+        off += n
+    opt = b2.ShardedOptimizer(ctx, b2.AdamWConfig(warmup_steps=0), params, b2.EPSO)
+    assert opt.detect_soft_failure(1.25, node=0) == -1
+    assert opt.detect_soft_failure(float("nan"), node=0) == 0  # a non-finite loss is a failure too
+    G[130_500] = float("inf")
+    assert opt.detect_soft_failure(1.25, node=3) == 3
+    before = W.clone()
+    st = opt.step(stats=True)
+    torch.cuda.synchronize()
+    assert st["nonfinite"]
+    assert torch.equal(W, before)  # the fused scan skipped the update on the device
+    assert not np.any(opt.state(1)[1])  # moments untouched (still zero)
+    G.copy_(torch.from_numpy(grads[1]).cuda().bfloat16())
+    st = opt.step(stats=True)
+    assert not st["nonfinite"] and not torch.equal(W, before)
