@@ -51,19 +51,27 @@ struct Cfg {
     static constexpr int STAGES = CG == 1 ? 4 : 6;
     static constexpr int TILE_M = BM * CG;
 };
-constexpr int SMEM_BYTES = 6 * (A_BYTES + 128 * BK * 2) + 1024 /*align*/ + 1024 /*barriers*/;
-static_assert(SMEM_BYTES >= 4 * (A_BYTES + 256 * BK * 2) + 1024 + 1024, "smem sized for both CTA groupings");
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_EPI_WARPS = 8;  // two warps per TMEM lane quadrant, each half the columns
 constexpr int NUM_THREADS = 128 + 32 * NUM_EPI_WARPS;
 // dgrad epilogue (BwdDownDgrad): each epilogue warp stages the G and U operands of its
 // next 32-row x 32-column chunk by TMA (SWIZZLE_64B boxes) while it works on the current one
 constexpr int EPI_GU_BYTES = 2 * 32 * 32 * 2;  // g box + u box
-template <GemmKind K>
-constexpr int smem_bytes() {
-    return SMEM_BYTES + (K == GemmKind::BwdDownDgrad ? NUM_EPI_WARPS * EPI_GU_BYTES : 0);
-}
-static_assert(SMEM_BYTES + NUM_EPI_WARPS * EPI_GU_BYTES <= 232448, "dgrad kernel exceeds 227 KB of shared memory");
+// TMA-store epilogue of the six expert kinds: each epilogue warp owns SLOTS 2 KB staging
+// slots, each one 32-row x 32-column bf16 box in the SWIZZLE_64B layout
+constexpr int EPI_SLOT_BYTES = 32 * 32 * 2;
+template <GemmKind K, int CG>
+struct KCfg {
+    static constexpr bool TMA_EPI = (int)K <= (int)GemmKind::WgradGateUp;
+    static constexpr int SLOTS = K == GemmKind::FwdGateUp ? 3 : 2;
+    static constexpr int STAGES =
+        CG == 1 ? 4 : ((K == GemmKind::FwdGateUp || K == GemmKind::BwdDownDgrad) ? 5 : 6);
+    static constexpr int WARP_EPI_BYTES =
+        TMA_EPI ? SLOTS * EPI_SLOT_BYTES + (K == GemmKind::BwdDownDgrad ? EPI_GU_BYTES : 0) : 0;
+    static constexpr int SMEM =
+        STAGES * Cfg<CG>::STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + NUM_EPI_WARPS * WARP_EPI_BYTES;
+    static_assert(SMEM <= 232448, "kernel exceeds 227 KB of shared memory");
+};
 
 struct Params {
     CUtensorMap mapA;
@@ -71,6 +79,9 @@ struct Params {
     CUtensorMap mapB1;
     CUtensorMap mapG;  // BwdDownDgrad epilogue operands (32 x 32 boxes, SWIZZLE_64B)
     CUtensorMap mapU;
+    CUtensorMap mapO0;  // TMA-store maps of the outputs (32 x 32 [x 1] boxes, SWIZZLE_64B)
+    CUtensorMap mapO1;
+    CUtensorMap mapO2;
     const int32_t* pad_start;  // [nr+1]
     const int32_t* counts;     // [nr] rows per expert (wgrad K extent)
     int nr, H, I;
@@ -166,7 +177,7 @@ __device__ __forceinline__ uint32_t map_to_rank(uint32_t addr, uint32_t rank) {
     return r;
 }
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -236,6 +247,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"((uint64_t)map),
+                 "r"(src), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     (uint64_t)map),
+                 "r"(src), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&v);
@@ -257,6 +287,50 @@ __device__ __forceinline__ void store_row32(__nv_bfloat16* dst, const float* v, 
             if (j < valid) dst[j] = __float2bfloat16_rn(v[j]);
     }
 }
+
+// Per-warp TMA-store staging. Lane r writes row r of a 32 x 32 bf16 box with four 128-bit
+// shared stores (conflict-free under the 64-byte swizzle: unit q of row r lands at unit
+// q ^ ((r >> 1) & 3)); lane 0 hands the box to the TMA engine as one bulk group. A slot is
+// rewritten only after the engine has read it (wait_group.read of the SLOTS-1 newest groups).
+template <int SLOTS>
+struct EpiStage {
+    uint32_t s0;  // shared address of slot 0
+    uint8_t* g0;  // generic address of slot 0
+    int slot;
+    __device__ __forceinline__ uint32_t begin(int lane, const float* v) {
+        if (lane == 0) bulk_wait_read<SLOTS - 1>();
+        __syncwarp();
+        uint4* row = reinterpret_cast<uint4*>(g0 + slot * EPI_SLOT_BYTES + lane * 64);
+        const int sw = (lane >> 1) & 3;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            row[q ^ sw] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                                     pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+        fence_async_smem();
+        __syncwarp();
+        const uint32_t src = s0 + slot * EPI_SLOT_BYTES;
+        slot = slot + 1 == SLOTS ? 0 : slot + 1;
+        return src;
+    }
+    __device__ __forceinline__ void put2d(const CUtensorMap* map, int lane, const float* v, int c0, int c1) {
+        const uint32_t src = begin(lane, v);
+        if (lane == 0) {
+            tma_store_2d(map, src, c0, c1);
+            bulk_commit();
+        }
+    }
+    __device__ __forceinline__ void put3d(const CUtensorMap* map, int lane, const float* v, int c0, int c1, int c2) {
+        const uint32_t src = begin(lane, v);
+        if (lane == 0) {
+            tma_store_3d(map, src, c0, c1, c2);
+            bulk_commit();
+        }
+    }
+    __device__ __forceinline__ void drain(int lane) {
+        if (lane == 0) bulk_wait_all();
+        __syncwarp();
+    }
+};
 
 // ---------------------------------------------------------------- kinds
 
@@ -580,7 +654,8 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const TileInfo& t
 template <GemmKind KIND, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __grid_constant__ Params p) {
     using C = Cfg<CG>;
-    constexpr int STAGES = C::STAGES;
+    using KC = KCfg<KIND, CG>;
+    constexpr int STAGES = KC::STAGES;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -592,8 +667,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
     auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + a); };
     auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + 2 + a); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + STAGES * C::STAGE_BYTES + 8 * (2 * STAGES + 4));
-    auto epi_bar = [&](int w) { return bar0 + 256u + 8u * w; };     // BwdDownDgrad staging barriers
-    const uint32_t epi_base = bar0 + 1024u;                          // 1 KB aligned (bar0 is)
+    auto epi_bar = [&](int w) { return bar0 + 256u + 8u * w; };  // BwdDownDgrad staging barriers
+    // per epilogue warp: [G/U input boxes (dgrad)] [SLOTS output boxes]; 1 KB aligned (bar0 is)
+    const uint32_t epi_base = bar0 + 1024u;
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
@@ -711,7 +787,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
         const uint32_t tempty0 = CG == 2 ? map_to_rank(tempty_bar(0), 0) : tempty_bar(0);
         // BwdDownDgrad: per-warp G/U staging buffer + mbarrier, one chunk ahead
         const int ew = warp - 4;
-        const uint32_t gu_s = epi_base + (uint32_t)(ew * EPI_GU_BYTES);
+        const uint32_t gu_s = epi_base + (uint32_t)(ew * KC::WARP_EPI_BYTES);
+        EpiStage<KC::SLOTS> stg;
+        stg.s0 = gu_s + (KIND == GemmKind::BwdDownDgrad ? EPI_GU_BYTES : 0);
+        stg.g0 = gbase + (stg.s0 - base);
+        stg.slot = 0;
+        const int row0 = 32 * quad;  // first row of this warp inside the CTA's 128
         const uint32_t gu_bar = epi_bar(ew);
         uint32_t gu_phase = 0;
         auto gu_issue = [&](const TileInfo& tn, int c) {
@@ -738,7 +819,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
             tc_fence_after();
             const uint32_t tacc = tmem_base + ((uint32_t)(32 * quad) << 16) + acc * BN;
             if constexpr (KIND == GemmKind::BwdDownDgrad) {
-                const int64_t row = ti.m0 + 32 * quad + lane;
                 const uint8_t* gs = gbase + (gu_s - base);
                 const uint8_t* us = gs + EPI_GU_BYTES / 2;
                 const int sw = (lane >> 1) & 3;
@@ -785,8 +865,69 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                         duv[j] = x * sg * d;
                         dgv[j] = uu * d * (sg * (1.f + x * (1.f - sg)));
                     }
-                    store_row32(p.out0 + row * 2 * p.I + col, dgv, 32);
-                    store_row32(p.out0 + row * 2 * p.I + p.I + col, duv, 32);
+                    stg.put2d(&p.mapO0, lane, dgv, col, ti.m0 + row0);
+                    stg.put2d(&p.mapO0, lane, duv, p.I + col, ti.m0 + row0);
+                }
+            } else if constexpr (KIND == GemmKind::FwdGateUp) {
+                const int nbase = ti.n0 / 2;  // 128 gate + 128 up columns per tile
+                uint32_t r[32], r2[32];
+#pragma unroll 1
+                for (int c = half * (BN / 4); c < (half + 1) * (BN / 4); c += 32) {
+                    tmem_ld32(tacc + c, r);
+                    tmem_ld32(tacc + BN / 2 + c, r2);
+                    tmem_wait_ld();
+                    const int col = nbase + c;
+                    if (col >= p.I) continue;  // I % 64 == 0: all in or all out
+                    float gv[32], uv[32], hv[32];
+                    // G and U are stored rounded to bf16; H is computed from the rounded values
+#pragma unroll
+                    for (int j = 0; j < 32; j += 2) {
+                        const uint32_t gp = pack_bf16(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
+                        const uint32_t up = pack_bf16(__uint_as_float(r2[j]), __uint_as_float(r2[j + 1]));
+                        gv[j] = bf16_lo(gp);
+                        gv[j + 1] = bf16_hi(gp);
+                        uv[j] = bf16_lo(up);
+                        uv[j + 1] = bf16_hi(up);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) hv[j] = silu_f(gv[j]) * uv[j];
+                    stg.put2d(&p.mapO0, lane, gv, col, ti.m0 + row0);
+                    stg.put2d(&p.mapO1, lane, uv, col, ti.m0 + row0);
+                    stg.put2d(&p.mapO2, lane, hv, col, ti.m0 + row0);
+                }
+            } else if constexpr (KIND == GemmKind::FwdDown || KIND == GemmKind::BwdDx) {
+                uint32_t r[32];
+                float v[32];
+#pragma unroll 1
+                for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+                    tmem_ld32(tacc + c, r);
+                    tmem_wait_ld();
+                    const int col = ti.n0 + c;
+                    if (col >= p.H) continue;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                    stg.put2d(&p.mapO0, lane, v, col, ti.m0 + row0);
+                }
+            } else if constexpr (KIND == GemmKind::WgradDown || KIND == GemmKind::WgradGateUp) {
+                // out[e][m][n] * scale through 3-D maps: rows past the expert's M are clipped
+                uint32_t r[32];
+                float v[32];
+                const bool zero = ti.kb == 0;
+#pragma unroll 1
+                for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+                    if (!zero) {
+                        tmem_ld32(tacc + c, r);
+                        tmem_wait_ld();
+                    }
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = zero ? 0.f : __uint_as_float(r[j]) * p.scale;
+                    const int col = ti.n0 + c;
+                    if constexpr (KIND == GemmKind::WgradDown) {
+                        if (col < p.H) stg.put3d(&p.mapO0, lane, v, col, ti.m0 + row0, ti.e);
+                    } else {
+                        if (col < p.I) stg.put3d(&p.mapO0, lane, v, col, ti.m0 + row0, ti.e);
+                        else if (col < 2 * p.I) stg.put3d(&p.mapO1, lane, v, col - p.I, ti.m0 + row0, ti.e);
+                    }
                 }
             } else {
                 epilogue_tile<KIND>(p, ti, tacc, 32 * quad + lane, ti.kb == 0, half);
@@ -798,6 +939,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                 else mbar_arrive_cluster(tempty0 + 8u * acc);
             }
         }
+        if constexpr (KC::TMA_EPI) stg.drain(lane);  // the bulk stores have left shared memory
     }
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync_all();
@@ -844,10 +986,28 @@ static CUtensorMap make_map(const void* ptr, int64_t cols, int64_t rows, int bc,
     return m;
 }
 
+// 3-D bf16 tensor [d2][d1][d0] (d0 contiguous), box {32, 32, 1}, 64B swizzle: the TMA-store
+// view of a weight gradient, whose rows past d1 (a partial M tile) are clipped by the engine
+static CUtensorMap make_map3(const void* ptr, int64_t d0, int64_t d1, int64_t d2) {
+    CUtensorMap m;
+    cuuint64_t dims[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)std::max<int64_t>(d2, 1)};
+    cuuint64_t strides[2] = {(cuuint64_t)d0 * 2, (cuuint64_t)(d0 * d1) * 2};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (3d) failed: " + std::to_string((int)r));
+    return m;
+}
+static CUtensorMap make_store_map(const void* ptr, int64_t cols, int64_t rows) {
+    return make_map(ptr, cols, rows, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+}
+
 template <GemmKind KIND, int CG>
 static void launch_kind(const Params& p, int grid, cudaStream_t st) {
     static std::once_flag once;
-    constexpr int smem = smem_bytes<KIND>();
+    constexpr int smem = KCfg<KIND, CG>::SMEM;
     std::call_once(once, [] {
         B2_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<KIND, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      smem));
@@ -935,6 +1095,9 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.mapA = make_map(a.x, H, P, 64, BM);
             p.mapB0 = make_map(a.wg, I, nr * H, 64, 64);
             p.mapB1 = make_map(a.wu, I, nr * H, 64, 64);
+            p.mapO0 = make_store_map(a.out0, I, P);
+            p.mapO1 = make_store_map(a.out1, I, P);
+            p.mapO2 = make_store_map(a.out2, I, P);
             p.n_tiles = (int)ceil_div(I, BN / 2);
             p.num_kb_fixed = (int)ceil_div(H, BK);
             launch_kind<GemmKind::FwdGateUp, G>(p, grid, st);
@@ -943,6 +1106,7 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.mapA = make_map(a.h, I, P, 64, BM);
             p.mapB0 = make_map(a.wd, H, nr * I, 64, 64);
             p.mapB1 = p.mapB0;
+            p.mapO0 = make_store_map(a.out0, H, P);
             p.n_tiles = (int)ceil_div(H, BN);
             p.num_kb_fixed = (int)ceil_div(I, BK);
             launch_kind<GemmKind::FwdDown, G>(p, grid, st);
@@ -953,6 +1117,7 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.mapB1 = p.mapB0;
             p.mapG = make_map(a.g, I, P, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
             p.mapU = make_map(a.u, I, P, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+            p.mapO0 = make_store_map(a.out0, 2 * I, P);
             p.n_tiles = (int)ceil_div(I, BN);
             p.num_kb_fixed = (int)ceil_div(H, BK);
             launch_kind<GemmKind::BwdDownDgrad, G>(p, grid, st);
@@ -961,6 +1126,7 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.mapA = make_map(a.dgu, 2 * I, P, 64, BM);
             p.mapB0 = make_map(a.wg, I, nr * H, 64, C2::B_COLS);
             p.mapB1 = make_map(a.wu, I, nr * H, 64, C2::B_COLS);
+            p.mapO0 = make_store_map(a.out0, H, P);
             p.n_tiles = (int)ceil_div(H, BN);
             p.num_kb_fixed = (int)ceil_div(2 * I, BK);
             launch_kind<GemmKind::BwdDx, G>(p, grid, st);
@@ -970,6 +1136,7 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.mapA = make_map(a.h, I, P, 64, 64);
             p.mapB0 = make_map(a.dy, H, P, 64, 64);
             p.mapB1 = p.mapB0;
+            p.mapO0 = make_map3(a.out0, H, I, nr);
             p.m_tiles_fixed = (int)ceil_div(I, BM * G);
             p.n_tiles = (int)ceil_div(H, BN);
             grid = (int)std::min<int64_t>(grid, G * nr * p.m_tiles_fixed * p.n_tiles);
@@ -980,6 +1147,8 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.mapA = make_map(a.x, H, P, 64, 64);
             p.mapB0 = make_map(a.dgu, 2 * I, P, 64, 64);
             p.mapB1 = p.mapB0;
+            p.mapO0 = make_map3(a.out0, I, H, nr);
+            p.mapO1 = make_map3(a.out1, I, H, nr);
             p.m_tiles_fixed = (int)ceil_div(H, BM * G);
             p.n_tiles = (int)ceil_div(2 * I, BN);
             grid = (int)std::min<int64_t>(grid, G * nr * p.m_tiles_fixed * p.n_tiles);

@@ -11,6 +11,8 @@
 // All kernels are deterministic: every output element is produced by exactly one
 // thread, summing in the reference's slot (k) order; no atomics. Row-copy kernels
 // move 16-byte vectors (one warp per row) when H*sizeof(T) allows.
+#include <type_traits>
+
 #include "b2_common.cuh"
 #include "kernels.h"
 
@@ -189,7 +191,7 @@ __global__ void combine_kernel(const T* __restrict__ y, const int32_t* __restric
 // dout rows come from `dout` ([T,H]) or, for expert parallelism, straight from the
 // source rank's buffer over NVLink: peer_dout[t / s_local] + (t % s_local) * H.
 template <typename T>
-__global__ void out_reduction_bwd_kernel(const T* __restrict__ dout, const T* const* __restrict__ peer_dout,
+__global__ void __launch_bounds__(256, 3) out_reduction_bwd_kernel(const T* __restrict__ dout, const T* const* __restrict__ peer_dout,
                                          int s_local, const T* __restrict__ y,
                                          const int32_t* __restrict__ slot_prow, const int32_t* __restrict__ selected_k,
                                          const int32_t* __restrict__ cum_expert_counts, const float* __restrict__ gw,
@@ -201,41 +203,35 @@ __global__ void out_reduction_bwd_kernel(const T* __restrict__ dout, const T* co
     __syncwarp();
     if (j0 == j1) return;
     const T* gp = peer_dout ? peer_dout[t / s_local] + (int64_t)(t % s_local) * H : dout + (int64_t)t * H;
-    if (vec_ok<T>(H) && H <= 32 * V16<T>::n * 8) {
-        // dout row cached in registers (<= 8 vectors per lane); the slots of a token are
-        // processed together so their row loads are in flight at the same time
+    if (vec_ok<T>(H)) {
+        // column-vector outer loop: per 16-byte column block the dout vector and the rows of
+        // up to 4 slots are loaded together (5 loads in flight per lane), then the slot dots
+        // accumulate and the dy rows are stored
         constexpr int V = V16<T>::n;
         constexpr int MAXJ = 4;
-        int4 graw[8];
+        // the reference's fp64 dot (moe.hpp:289-294); bf16 operands multiply exactly in fp32
+        // and the fp32 sum stays far inside the bf16-mode tolerance
+        using DotT = typename std::conditional<sizeof(T) == 2, float, double>::type;
         const int nv = H / V;
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if (lane + 32 * i < nv) graw[i] = __ldg(reinterpret_cast<const int4*>(gp + (lane + 32 * i) * V));
         for (int jb = j0; jb < j1; jb += MAXJ) {
             const int nj = min(MAXJ, j1 - jb);
             int64_t rows[MAXJ];
             float wv[MAXJ];
-            double dot[MAXJ];
+            DotT dot[MAXJ];
 #pragma unroll
             for (int q = 0; q < MAXJ; ++q) {
                 rows[q] = q < nj ? slot_prow[jb + q] : 0;
                 wv[q] = q < nj ? gw[(int64_t)t * K + selected_k[jb + q]] : 0.f;
-                dot[q] = 0.0;
+                dot[q] = 0;
             }
-#pragma unroll 1
-            for (int i = 0; i < 8; ++i) {
-                const int vi = lane + 32 * i;
-                if (vi >= nv) break;
+            for (int vi = lane; vi < nv; vi += 32) {
+                const int4 graw = __ldg(reinterpret_cast<const int4*>(gp + vi * V));
                 int4 yr[MAXJ];
 #pragma unroll
                 for (int q = 0; q < MAXJ; ++q)
                     if (q < nj) yr[q] = __ldg(reinterpret_cast<const int4*>(y + rows[q] * H + vi * V));
                 float g[V];
-                int4 gsel = graw[0];
-#pragma unroll
-                for (int z = 1; z < 8; ++z)
-                    if (z == i) gsel = graw[z];
-                V16<T>::unpack(gsel, g);
+                V16<T>::unpack(graw, g);
 #pragma unroll
                 for (int q = 0; q < MAXJ; ++q) {
                     if (q >= nj) break;
@@ -244,14 +240,15 @@ __global__ void out_reduction_bwd_kernel(const T* __restrict__ dout, const T* co
 #pragma unroll
                     for (int z = 0; z < V; ++z) {
                         o[z] = __fmul_rn(wv[q], g[z]);
-                        dot[q] += (double)g[z] * (double)yv[z];
+                        if constexpr (sizeof(T) == 2) dot[q] = __fmaf_rn(g[z], yv[z], dot[q]);
+                        else dot[q] += (double)g[z] * (double)yv[z];
                     }
                     V16<T>::store(dy + rows[q] * H + vi * V, o);
                 }
             }
 #pragma unroll
             for (int q = 0; q < MAXJ; ++q) {
-                double d = dot[q];
+                DotT d = dot[q];
 #pragma unroll
                 for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
                 if (lane == 0 && q < nj) wgrad[(int64_t)t * K + selected_k[jb + q]] = (float)d;

@@ -82,8 +82,9 @@ def run_opt(dp, ep, mode):
 def test_sharded_optimizer_matches_oracle(dp, ep, mode):
     r = run_opt(dp, ep, mode)
     if dp * ep <= 2:  # two-member groups sum exactly: weights, masters and moments are bitwise equal
-        assert r["weights_equal"] and r["state_equal"]
+        assert r["weights_equal"] and r["state_equal"], r
     else:  # NCCL's summation order over 4 members may differ from the reference's member order
-        assert r["weights_maxrel"] <= 1e-6
-    assert r["state_bytes_equal"]
-    assert r["stats_maxdiff"] <= 1e-9
+        assert r["weights_maxrel"] <= 1e-6, r
+    assert r["state_bytes_equal"], r
+    # grad norm / clip: exact sums at 2 members; NCCL's 4-member fp32 order moves the last bits
+    assert r["stats_maxdiff"] <= (1e-9 if dp * ep <= 2 else 1e-7), r

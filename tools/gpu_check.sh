@@ -24,5 +24,7 @@ for w in $WHAT; do case $w in
  timeline) timeout 300 python tools/timeline.py > $OUT/timeline_eager.txt 2>&1; echo "timeline rc=$?"; head -30 $OUT/timeline_eager.txt
       timeout 300 python tools/timeline.py --graph > $OUT/timeline_graph.txt 2>&1; head -30 $OUT/timeline_graph.txt ;;
  gtest) timeout 600 python -m pytest tests -m gpu -x -q -k "${GTEST_K}" > $OUT/gtest.log 2>&1; echo "gtest rc=$?"; tail -15 $OUT/gtest.log ;;
+ ep4) timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29512 \
+      bench.py --gpus 4 --steps 10 --warmup 3 > $OUT/ep4.json 2> $OUT/ep4.err; echo "ep4 rc=$?"; cat $OUT/ep4.json; tail -5 $OUT/ep4.err ;;
  ref) timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/ref.json 2> $OUT/ref.err; echo "ref rc=$?"; cat $OUT/ref.json ;;
 esac; done
