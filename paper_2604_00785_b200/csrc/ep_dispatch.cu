@@ -33,10 +33,25 @@ __global__ void ep_gather_pull_kernel(const T* const* __restrict__ peer_src, int
         if (j0 == j1) continue;
         const T* src = peer_src[gid / S] + (int64_t)(gid % S) * H;
         if (((int64_t)H * sizeof(T)) % 16 == 0) {
+            // up to 8 x 16 B of the remote row in flight per lane (a 4 KB row per warp), then
+            // the local copies: NVLink latency is hidden by bytes in flight, not by occupancy
+            constexpr int B = 8;
             const int nv = (int)((int64_t)H * sizeof(T) / 16);
-            for (int v = lane; v < nv; v += 32) {
-                const int4 val = reinterpret_cast<const int4*>(src)[v];
-                for (int j = j0; j < j1; ++j) reinterpret_cast<int4*>(out + (int64_t)slot_prow[j] * H)[v] = val;
+            for (int v0 = 0; v0 < nv; v0 += 32 * B) {
+                int4 val[B];
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    const int v = v0 + lane + 32 * b;
+                    if (v < nv) val[b] = reinterpret_cast<const int4*>(src)[v];
+                }
+                for (int j = j0; j < j1; ++j) {
+                    int4* dst = reinterpret_cast<int4*>(out + (int64_t)slot_prow[j] * H);
+#pragma unroll
+                    for (int b = 0; b < B; ++b) {
+                        const int v = v0 + lane + 32 * b;
+                        if (v < nv) dst[v] = val[b];
+                    }
+                }
             }
         } else {
             for (int c = lane; c < H; c += 32) {
@@ -86,29 +101,41 @@ __global__ void ep_combine_push_vec_kernel(const T* __restrict__ y, const int32_
         const int j0 = cec[gid], j1 = cec[gid + 1];
         if (j0 == j1) continue;
         T* dst = peer_ret[gid / S] + ((int64_t)me * S + gid % S) * H;
+        // all local slot rows of a column block are loaded together (<= 8 in flight)
+        constexpr int MAXJ = 8;
         for (int v = lane; v < nv; v += 32) {
             float acc[V];
 #pragma unroll
             for (int q = 0; q < V; ++q) acc[q] = 0.f;
-            for (int j = j0; j < j1; ++j) {
-                const int4 raw = __ldg(reinterpret_cast<const int4*>(y + (int64_t)slot_prow[j] * H) + v);
-                float f[V];
-                if constexpr (sizeof(T) == 4) {
-                    f[0] = __int_as_float(raw.x);
-                    f[1] = __int_as_float(raw.y);
-                    f[2] = __int_as_float(raw.z);
-                    f[3] = __int_as_float(raw.w);
-                } else {
-                    const uint32_t w[4] = {(uint32_t)raw.x, (uint32_t)raw.y, (uint32_t)raw.z, (uint32_t)raw.w};
+            for (int jb = j0; jb < j1; jb += MAXJ) {
+                const int nj = min(MAXJ, j1 - jb);
+                int4 raw[MAXJ];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        f[2 * q] = __uint_as_float(w[q] << 16);
-                        f[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+                for (int q = 0; q < MAXJ; ++q)
+                    if (q < nj) raw[q] = __ldg(reinterpret_cast<const int4*>(y + (int64_t)slot_prow[jb + q] * H) + v);
+#pragma unroll
+                for (int q = 0; q < MAXJ; ++q) {
+                    if (q >= nj) break;
+                    float f[V];
+                    if constexpr (sizeof(T) == 4) {
+                        f[0] = __int_as_float(raw[q].x);
+                        f[1] = __int_as_float(raw[q].y);
+                        f[2] = __int_as_float(raw[q].z);
+                        f[3] = __int_as_float(raw[q].w);
+                    } else {
+                        const uint32_t w[4] = {(uint32_t)raw[q].x, (uint32_t)raw[q].y, (uint32_t)raw[q].z,
+                                               (uint32_t)raw[q].w};
+#pragma unroll
+                        for (int z = 0; z < 4; ++z) {
+                            f[2 * z] = __uint_as_float(w[z] << 16);
+                            f[2 * z + 1] = __uint_as_float(w[z] & 0xFFFF0000u);
+                        }
                     }
-                }
-                const float wv = gw ? gw[(int64_t)gid * K + selected_k[j]] : 1.f;
+                    const float wv = gw ? gw[(int64_t)gid * K + selected_k[jb + q]] : 1.f;
 #pragma unroll
-                for (int q = 0; q < V; ++q) acc[q] = gw ? __fadd_rn(acc[q], __fmul_rn(wv, f[q])) : __fadd_rn(acc[q], f[q]);
+                    for (int z = 0; z < V; ++z)
+                        acc[z] = gw ? __fadd_rn(acc[z], __fmul_rn(wv, f[z])) : __fadd_rn(acc[z], f[z]);
+                }
             }
             int4 o;
             if constexpr (sizeof(T) == 4) {
@@ -117,9 +144,9 @@ __global__ void ep_combine_push_vec_kernel(const T* __restrict__ y, const int32_
             } else {
                 uint32_t w[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    __nv_bfloat162 b = __floats2bfloat162_rn(acc[2 * q], acc[2 * q + 1]);
-                    w[q] = *reinterpret_cast<uint32_t*>(&b);
+                for (int z = 0; z < 4; ++z) {
+                    __nv_bfloat162 b = __floats2bfloat162_rn(acc[2 * z], acc[2 * z + 1]);
+                    w[z] = *reinterpret_cast<uint32_t*>(&b);
                 }
                 o = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
             }
@@ -153,29 +180,38 @@ __global__ void ep_return_sum_kernel(const T* __restrict__ slab, const int32_t* 
     const bool vec = ((int64_t)W * sizeof(T)) % 16 == 0;
     if (vec) {
         constexpr int V = 16 / sizeof(T);
+        constexpr int MAXR = 8;  // slabs of up to 8 ranks in flight per lane
         for (int v = lane; v < W / V; v += 32) {
             float acc[V];
             bool any = false;
-            for (int r = 0; r < E; ++r) {
-                if (!(mask >> r & 1u)) continue;
-                const int4 raw = __ldcv(reinterpret_cast<const int4*>(slab + ((int64_t)r * S + t) * W) + v);
-                float f[V];
-                if constexpr (sizeof(T) == 4) {
-                    f[0] = __int_as_float(raw.x);
-                    f[1] = __int_as_float(raw.y);
-                    f[2] = __int_as_float(raw.z);
-                    f[3] = __int_as_float(raw.w);
-                } else {
-                    const uint32_t w[4] = {(uint32_t)raw.x, (uint32_t)raw.y, (uint32_t)raw.z, (uint32_t)raw.w};
+            for (int r0 = 0; r0 < E; r0 += MAXR) {
+                int4 raw[MAXR];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        f[2 * q] = __uint_as_float(w[q] << 16);
-                        f[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+                for (int q = 0; q < MAXR; ++q)
+                    if (r0 + q < E && (mask >> (r0 + q) & 1u))
+                        raw[q] = __ldcv(reinterpret_cast<const int4*>(slab + ((int64_t)(r0 + q) * S + t) * W) + v);
+#pragma unroll
+                for (int q = 0; q < MAXR; ++q) {
+                    if (!(r0 + q < E && (mask >> (r0 + q) & 1u))) continue;
+                    float f[V];
+                    if constexpr (sizeof(T) == 4) {
+                        f[0] = __int_as_float(raw[q].x);
+                        f[1] = __int_as_float(raw[q].y);
+                        f[2] = __int_as_float(raw[q].z);
+                        f[3] = __int_as_float(raw[q].w);
+                    } else {
+                        const uint32_t w[4] = {(uint32_t)raw[q].x, (uint32_t)raw[q].y, (uint32_t)raw[q].z,
+                                               (uint32_t)raw[q].w};
+#pragma unroll
+                        for (int z = 0; z < 4; ++z) {
+                            f[2 * z] = __uint_as_float(w[z] << 16);
+                            f[2 * z + 1] = __uint_as_float(w[z] & 0xFFFF0000u);
+                        }
                     }
-                }
 #pragma unroll
-                for (int q = 0; q < V; ++q) acc[q] = any ? __fadd_rn(acc[q], f[q]) : f[q];
-                any = true;
+                    for (int z = 0; z < V; ++z) acc[z] = any ? __fadd_rn(acc[z], f[z]) : f[z];
+                    any = true;
+                }
             }
             if (!any)
                 for (int q = 0; q < V; ++q) acc[q] = 0.f;

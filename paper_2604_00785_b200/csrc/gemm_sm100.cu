@@ -104,6 +104,8 @@ struct Params {
     const int32_t* slot_prow;
     const __nv_bfloat16* src;
     float* part;
+    const int32_t* gather_rows;  // FwdGateUp / WgradGateUp: padded row -> token (gather4 mode)
+    int gather_oob;              // the zero-filled row index used for pad rows (-1 entries)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -156,6 +158,30 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
         "l"((uint64_t)map), "r"(bar), "r"(c0), "r"(c1)
         : "memory");
+}
+// 4 arbitrary rows x one box of columns (TMA tile::gather4); the map's box is {cols, 1}
+template <int CG>
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, uint32_t bar, int col, int4 rows) {
+    if constexpr (CG == 1)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+            "%4, %5, %6, %7}], [%2];" ::"r"(dst),
+            "l"((uint64_t)map), "r"(bar), "r"(col), "r"(rows.x), "r"(rows.y), "r"(rows.z), "r"(rows.w)
+            : "memory");
+    else
+        asm volatile(
+            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+            "l"((uint64_t)map), "r"(bar), "r"(col), "r"(rows.x), "r"(rows.y), "r"(rows.z), "r"(rows.w)
+            : "memory");
+}
+__device__ __forceinline__ int4 gather_ids(const int32_t* rows, int64_t at, int oob) {
+    int4 r = __ldg(reinterpret_cast<const int4*>(rows + at));
+    r.x = r.x < 0 ? oob : r.x;
+    r.y = r.y < 0 ? oob : r.y;
+    r.z = r.z < 0 ? oob : r.z;
+    r.w = r.w < 0 ? oob : r.w;
+    return r;
 }
 // 2-CTA (cta_group::2) load: the bytes complete_tx on the LEADER CTA's barrier
 __device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
@@ -443,7 +469,7 @@ __device__ __forceinline__ void load_stage(const Params& p, const TileInfo& ti, 
     constexpr int BC = Cfg<CG>::B_COLS;
     const int nb = ti.n0 + BC * (int)rank;  // this CTA's first B column of the tile
     if constexpr (KIND == GemmKind::FwdGateUp) {
-        ld(sA, &p.mapA, k0, m_own);
+        if (!p.gather_rows) ld(sA, &p.mapA, k0, m_own);
         const int row = ti.e * p.H + k0;
         const int n0 = ti.n0 / 2;  // 128 gate columns + 128 up columns per tile
         if (CG == 1 || rank == 0) {
@@ -477,8 +503,10 @@ __device__ __forceinline__ void load_stage(const Params& p, const TileInfo& ti, 
         for (int c = 0; c < p.b_chunks; ++c) ld(sB + c * 8192, &p.mapB0, 64 * c, row);
     } else {  // wgrad: K runs over the expert's rows; both operands MN-major
         const int row = ti.krow0 + k0;
-        ld(sA + 0, &p.mapA, m_own, row);
-        ld(sA + 8192, &p.mapA, m_own + 64, row);
+        if (KIND != GemmKind::WgradGateUp || !p.gather_rows) {
+            ld(sA + 0, &p.mapA, m_own, row);
+            ld(sA + 8192, &p.mapA, m_own + 64, row);
+        }
 #pragma unroll
         for (int c = 0; c < BC / 64; ++c) ld(sB + c * 8192, &p.mapB0, nb + 64 * c, row);
     }
@@ -719,7 +747,43 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
     const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;  // tile scheduler over CTA pairs
 
     if (warp == 0) {
-        if (lane == 0) {
+        constexpr bool kGatherKind = KIND == GemmKind::FwdGateUp || KIND == GemmKind::WgradGateUp;
+        if (kGatherKind && p.gather_rows != nullptr) {
+            // X gathered from the token rows with tile::gather4: every lane of the producer warp
+            // issues the 4-row pieces of the A tile (32 per stage), lane 0 the barrier and B
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = unit; t < ntiles; t += nunits) {
+                const TileInfo ti = tile_info<KIND, CG>(p, ps, t);
+                const int m_own = ti.m0 + BM * (int)rank;
+                int4 rows_fwd = make_int4(0, 0, 0, 0);
+                if constexpr (KIND == GemmKind::FwdGateUp)  // A = X [rows m_own.., K], rows fixed per tile
+                    rows_fwd = gather_ids(p.gather_rows, (int64_t)m_own + 4 * lane, p.gather_oob);
+                for (int kb = 0; kb < ti.kb; ++kb) {
+                    mbar_wait(empty_bar(stage), phase ^ 1u, 0);
+                    const uint32_t sA = base + stage * C::STAGE_BYTES, sB = sA + A_BYTES;
+                    uint32_t fb = full_bar(stage);
+                    if constexpr (CG == 2) fb = map_to_rank(fb, 0);
+                    if (lane == 0) {
+                        if (leader) mbar_expect_tx(full_bar(stage), p.stage_tx);
+                        load_stage<KIND, CG>(p, ti, kb, m_own, rank, sA, sB, fb);  // B only in gather mode
+                    }
+                    const int k0 = kb * BK;
+                    if constexpr (KIND == GemmKind::FwdGateUp) {
+                        tma_gather4<CG>(sA + 512u * lane, &p.mapA, fb, k0, rows_fwd);
+                    } else {  // WgradGateUp: A = X^T, K runs over the expert's rows; 2 boxes of 64 columns
+                        const int i = lane % 16, b = lane / 16;
+                        const int4 r = gather_ids(p.gather_rows, (int64_t)ti.krow0 + k0 + 4 * i, p.gather_oob);
+                        tma_gather4<CG>(sA + 8192u * b + 512u * i, &p.mapA, fb, m_own + 64 * b, r);
+                    }
+                    __syncwarp();
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
+        } else if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
             for (int t = unit; t < ntiles; t += nunits) {
@@ -1062,6 +1126,9 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
     p.out0 = (__nv_bfloat16*)a.out0;
     p.out1 = (__nv_bfloat16*)a.out1;
     p.out2 = (__nv_bfloat16*)a.out2;
+    p.gather_rows = a.gather_rows;
+    p.gather_oob = a.gather_tokens;
+    if (a.gather_rows) check(a.gather_tokens >= 0 && a.pmax % 4 == 0, "gather4 operand: bad token count / row capacity");
     const int64_t P = a.pmax, H = a.H, I = a.I, nr = a.nr;
     int grid = a.num_sms > 0 ? a.num_sms : 148;
     p.umma_n = BN;
@@ -1092,7 +1159,7 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
     }
     switch (a.kind) {
         case GemmKind::FwdGateUp:
-            p.mapA = make_map(a.x, H, P, 64, BM);
+            p.mapA = a.gather_rows ? make_map(a.x, H, a.gather_tokens, 64, 1) : make_map(a.x, H, P, 64, BM);
             p.mapB0 = make_map(a.wg, I, nr * H, 64, 64);
             p.mapB1 = make_map(a.wu, I, nr * H, 64, 64);
             p.mapO0 = make_store_map(a.out0, I, P);
@@ -1144,7 +1211,7 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             break;
         case GemmKind::WgradGateUp:
             check(a.counts != nullptr, "wgrad: expert row counts required");
-            p.mapA = make_map(a.x, H, P, 64, 64);
+            p.mapA = a.gather_rows ? make_map(a.x, H, a.gather_tokens, 64, 1) : make_map(a.x, H, P, 64, 64);
             p.mapB0 = make_map(a.dgu, 2 * I, P, 64, 64);
             p.mapB1 = p.mapB0;
             p.mapO0 = make_map3(a.out0, I, H, nr);

@@ -147,6 +147,11 @@ struct Sm100GemmArgs {
     const void* src;             // RouterDx: dXperm [P, H] (slots) or base [S, H]
     float* part;                 // RouterDw: fp32 partials [nsplit][H][N]
     int nsplit_out;              // RouterDw: number of S splits used (set by the launcher)
+    // FwdGateUp / WgradGateUp: gather the X operand straight from the token rows `x` [S,H]
+    // with TMA tile::gather4 (padded row -> token via gather_rows, -1 = zero row) instead
+    // of reading a materialised mlp_in; null: `x` is mlp_in [P,H]
+    const int32_t* gather_rows;
+    int gather_tokens;           // S: rows of `x` (row S is the zero-filled out-of-bounds row)
 };
 void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st);
 // number of S splits the RouterDw kind uses (its partial buffer holds splits*H*N floats)

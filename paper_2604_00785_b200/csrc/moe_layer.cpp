@@ -295,6 +295,10 @@ void MoeLayer::run_graphed(GraphCache& gc, std::vector<const void*> key, F&& bod
 }
 
 // dispatch weights/indices of this forward (learned top-k or FUR; the gathered table at EP > 1)
+bool MoeLayer::gather_in_gemm() const {
+    return dtype_ == BF16 && cfg_.ep == 1 && !gather_copy_ && ((uintptr_t)x_ & 15) == 0 && s_ > 0;
+}
+
 void MoeLayer::set_dispatch_tables() {
     gw_ = fur_ ? (const float*)fw_ : (const float*)topw_;
     gi_ = fur_ ? (const int32_t*)fi_ : (const int32_t*)topi_;
@@ -388,12 +392,15 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     mark(kIndex, true);
     const int32_t* p_total = pad_start_ + nr;
     // stage 4: expert MLP over the padded expert-sorted rows (225-244)
+    // bf16 at EP = 1: the expert GEMMs gather their X operand straight from x (TMA
+    // tile::gather4 by prow_src), so no mlp_in copy is materialised
+    const bool tma_gather = gather_in_gemm();
     mark(kGather, false);
     if (E > 1) {
         launch_ep_gather_pull<T>((const T* const*)peer_tab_, S, Tt, H, cec_, slot_prow_, (T*)mlp_in_, st);
         launch_zero_pad_rows<T>((T*)mlp_in_, prow_src_, p_total, H, pmax_, st);
         launches_ += 2;
-    } else {
+    } else if (!tma_gather) {
         launch_gather_rows<T>(x, prow_src_, p_total, (T*)mlp_in_, H, pmax_, st);
         launches_ += 1;
     }
@@ -408,7 +415,9 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
         ga.counts = token_counts_;
         ga.num_sms = ctx_.num_sms;
         ga.kind = GemmKind::FwdGateUp;
-        ga.x = mlp_in_;
+        ga.x = tma_gather ? (const void*)x : mlp_in_;
+        ga.gather_rows = tma_gather ? prow_src_ : nullptr;
+        ga.gather_tokens = S;
         ga.wg = gate;
         ga.wu = up;
         ga.out0 = g_;
@@ -418,6 +427,7 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
         launch_sm100_gemm(ga, st);
         mark(kGemmGateUp, true);
         ga.kind = GemmKind::FwdDown;
+        ga.gather_rows = nullptr;
         ga.h = h_;
         ga.wd = down;
         ga.out0 = y_;
@@ -559,12 +569,19 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         launch_sm100_gemm(ga, st);
         mark(kGemmWgradDown, true);
         ga.kind = GemmKind::WgradGateUp;  // 410-413
+        if (gather_in_gemm()) {  // X^T gathered from the caller's x (kept alive since forward)
+            ga.x = x_;
+            ga.gather_rows = prow_src_;
+            ga.gather_tokens = S;
+        }
         ga.out0 = dgate;
         ga.out1 = dup;
         mark(kGemmWgradGateUp, false);
         launch_sm100_gemm(ga, st);
         mark(kGemmWgradGateUp, true);
         ga.kind = GemmKind::BwdDx;  // 414-415
+        ga.gather_rows = nullptr;
+        ga.x = mlp_in_;
         ga.out0 = dxp_;
         mark(kGemmDx, false);
         launch_sm100_gemm(ga, st);

@@ -103,6 +103,8 @@ class MoeLayer {
     // Every data-dependent size lives on the device, so a replay is exact. Profiling
     // runs eagerly.
     void set_graph(bool on);
+    // force the materialised-mlp_in path instead of the TMA gather4 operand loads
+    void set_gather_copy(bool on) { gather_copy_ = on; }
 
   private:
     template <typename T>
@@ -113,6 +115,8 @@ class MoeLayer {
 
     void mark(int stage, bool end);
     void set_dispatch_tables();
+    bool gather_in_gemm() const;  // bf16, EP = 1: GEMMs gather X rows by TMA (no mlp_in pass)
+    bool gather_copy_ = false;    // force the materialised mlp_in path (A/B testing)
 
     struct GraphCache {
         std::vector<const void*> key;
