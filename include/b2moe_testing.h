@@ -17,9 +17,9 @@ int b2x_grouped_gemm(b2_ctx* ctx, int kind, int hidden, int intermediate, int nr
                      const int32_t* counts, int64_t pmax, const void* x, const void* wg, const void* wu, const void* wd, const void* g,
                      const void* u, const void* h, const void* dy, const void* dgu, void* out0, void* out1,
                      void* out2, float scale);
-/* Force (1) or release (0) the materialised mlp_in path of the bf16 layer instead of the
- * GEMMs' TMA tile::gather4 operand loads (A/B checks: both must agree bitwise). */
-int b2x_moe_set_gather_copy(b2_moe* m, int on);
+/* Opt the bf16 layer into (1) / out of (0) the GEMMs' TMA tile::gather4 X-operand loads
+ * instead of the materialised mlp_in rows (A/B checks: both must agree bitwise). */
+int b2x_moe_set_tma_gather(b2_moe* m, int on);
 #ifdef __cplusplus
 }
 #endif

@@ -489,8 +489,8 @@ int b2_opt_last_launches(b2_opt* o) { return o ? o->opt->last_launches() : 0; }
 
 #include "../../include/b2moe_testing.h"
 
-extern "C" int b2x_moe_set_gather_copy(b2_moe* m, int on) {
-    return guard([&] { m->layer->set_gather_copy(on != 0); });
+extern "C" int b2x_moe_set_tma_gather(b2_moe* m, int on) {
+    return guard([&] { m->layer->set_tma_gather(on != 0); });
 }
 
 extern "C" int b2x_grouped_gemm(b2_ctx* ctx, int kind, int hidden, int intermediate, int nr, const int32_t* pad_start,

@@ -15,7 +15,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--graph", action="store_true")
     ap.add_argument("--tokens", type=int, default=16384)
-    ap.add_argument("--gather-copy", action="store_true", help="materialised mlp_in instead of TMA gather4")
+    ap.add_argument("--tma-gather", action="store_true", help="TMA gather4 X operand instead of mlp_in rows")
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -34,10 +34,10 @@ def main():
     layer = b2.MoeLayer(ctx, cfg, torch.bfloat16, S)
     if args.graph:
         layer.set_graph(True)
-    if args.gather_copy:
+    if args.tma_gather:
         import ctypes
-        b2.lib().b2x_moe_set_gather_copy.argtypes = [ctypes.c_void_p, ctypes.c_int]
-        b2.lib().b2x_moe_set_gather_copy(layer.h, 1)
+        b2.lib().b2x_moe_set_tma_gather.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        b2.lib().b2x_moe_set_tma_gather(layer.h, 1)
     out = torch.empty_like(x)
     grads = dict(input=torch.empty_like(x), router=torch.empty_like(router), gate=torch.empty_like(gate),
                  up=torch.empty_like(up), down=torch.empty_like(down))
