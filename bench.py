@@ -7,8 +7,8 @@ package's CUDA kernels, inputs and weights resident in HBM. The same JSON line
 also carries:
   * roofline   - the tcgen05 grouped GEMMs (9 expert GEMMs, 18*RT*H*I FLOP per step)
                  against the measured bf16 peak (MEASURED_PEAKS.json)
-  * e2e        - the same metric through b2_moe_fwd_bwd_host with pinned host x/dout
-                 in and out/dx back every step
+  * e2e        - the same metric through b2_moe_fwd_bwd_host(_async) with pinned host
+                 x/dout in and out/dx back every step (two-slot copy/compute pipeline)
   * adamw      - the EP-aware sharded AdamW step on the Mula-7B-A1B parameter set
                  (6,919,096,320 params), HBM roofline
   * cpu_baseline - the reference (oracle/_ref, compiled in place) on host cores
@@ -415,18 +415,21 @@ def main():
             print(f"  {k_:>20s} {v:8.3f} ms", file=sys.stderr)
         print(f"  gemm total {gemm_ms:.3f} ms  {achieved:.1f} TFLOP/s  step {ms:.3f} ms  rt {rt}", file=sys.stderr)
 
-    # end to end through the host-buffer entry point (pinned host x/dout in, out/dx back)
+    # end to end through the host-buffer entry point (pinned host x/dout in, out/dx back): the
+    # pipelined call overlaps step i+1's host->device copies and step i's read-back with compute
     xh, douth = x.cpu().pin_memory(), dout.cpu().pin_memory()
     outh, dxh = torch.empty_like(xh).pin_memory(), torch.empty_like(xh).pin_memory()
-    for _ in range(2):
-        layer.fwd_bwd_host(xh, douth, router, gate, up, down, outh, dxh, grads, 0.01)
+    for _ in range(3):
+        layer.fwd_bwd_host(xh, douth, router, gate, up, down, outh, dxh, grads, 0.01, wait=False)
+    layer.host_wait()
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record(stream)
     for _ in range(args.steps):
-        layer.fwd_bwd_host(xh, douth, router, gate, up, down, outh, dxh, grads, 0.01)
+        layer.fwd_bwd_host(xh, douth, router, gate, up, down, outh, dxh, grads, 0.01, wait=False)
+    layer.host_wait()  # every step's results are back in host memory
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)

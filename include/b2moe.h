@@ -121,11 +121,20 @@ int b2_moe_artifacts(b2_moe* m, int64_t* sizes_host, int64_t* token_counts, int6
                      int64_t* selected_k, int64_t* counter);
 /* MoE layer forward+backward with HOST input/output buffers (the reference's
  * Tensor-in/Tensor-out façade): x_host/dout_host -> out_host/dx_host, weights and
- * their grads device-resident. Copies run on a side stream overlapped with compute.
+ * their grads device-resident. Copies run on side streams overlapped with compute.
  * Synchronises. */
 int b2_moe_fwd_bwd_host(b2_moe* m, const void* x_host, const void* dout_host, const void* router,
                         const void* gate, const void* up, const void* down, double aux_coeff, void* out_host,
                         void* dx_host, void* drouter, void* dgate, void* dup, void* ddown, int64_t s_tokens);
+/* Pipelined variant (B200-side addition): enqueues the same work and returns; two
+ * device staging slots let step i+1's host->device copies and step i's device->host
+ * results overlap the compute of the neighbouring steps. out_host/dx_host are valid
+ * after b2_moe_host_wait (or a later synchronous call). Host buffers must stay alive
+ * until then. */
+int b2_moe_fwd_bwd_host_async(b2_moe* m, const void* x_host, const void* dout_host, const void* router,
+                              const void* gate, const void* up, const void* down, double aux_coeff, void* out_host,
+                              void* dx_host, void* drouter, void* dgate, void* dup, void* ddown, int64_t s_tokens);
+int b2_moe_host_wait(b2_moe* m);
 
 /* ---- standalone routing stages (for identical-score parity checks) ---- */
 /* route (moe.hpp:58-80): logits/probs [S,N] f32, weights [S,K] f32, indices [S,K] int32, all device */

@@ -89,6 +89,8 @@ SIGNATURES = {
     "b2_moe_routing": (C.c_int, [P, P, P, P]),
     "b2_moe_artifacts": (C.c_int, [P] + [P] * 11),
     "b2_moe_fwd_bwd_host": (C.c_int, [P, P, P, P, P, P, P, C.c_double, P, P, P, P, P, P, I64]),
+    "b2_moe_fwd_bwd_host_async": (C.c_int, [P, P, P, P, P, P, P, C.c_double, P, P, P, P, P, P, I64]),
+    "b2_moe_host_wait": (C.c_int, [P]),
     "b2_route": (C.c_int, [P, P, C.c_int, P, P, I64, P, P, P, P]),
     "b2_softmax_topk": (C.c_int, [P, P, I64, I64, I64, C.c_int, P, P, P]),
     "b2_routing_artifacts": (C.c_int, [P, P, P, I64, C.c_int] + [P] * 11),
@@ -332,12 +334,18 @@ class MoeLayer:
         _check(lib().b2_moe_stage_times(self.h, ms.ctypes.data_as(P)))
         return {lib().b2_moe_stage_name(i).decode(): float(ms[i]) for i in range(self.NUM_STAGES)}
 
-    def fwd_bwd_host(self, x_host, dout_host, router, gate, up, down, out_host, dx_host, grads, aux_coeff=0.0):
-        """forward+backward with pinned HOST x/dout in and out/dx back (b2_moe_fwd_bwd_host)."""
-        _check(lib().b2_moe_fwd_bwd_host(self.h, _ptr(x_host), _ptr(dout_host), _ptr(router), _ptr(gate), _ptr(up),
-                                         _ptr(down), aux_coeff, _ptr(out_host), _ptr(dx_host), _ptr(grads["router"]),
-                                         _ptr(grads["gate"]), _ptr(grads["up"]), _ptr(grads["down"]),
-                                         x_host.shape[0]))
+    def fwd_bwd_host(self, x_host, dout_host, router, gate, up, down, out_host, dx_host, grads, aux_coeff=0.0,
+                     wait=True):
+        """forward+backward with pinned HOST x/dout in and out/dx back (b2_moe_fwd_bwd_host).
+        wait=False enqueues on the two-slot copy/compute pipeline and returns
+        (b2_moe_fwd_bwd_host_async); results are valid after host_wait()."""
+        fn = lib().b2_moe_fwd_bwd_host if wait else lib().b2_moe_fwd_bwd_host_async
+        _check(fn(self.h, _ptr(x_host), _ptr(dout_host), _ptr(router), _ptr(gate), _ptr(up), _ptr(down), aux_coeff,
+                  _ptr(out_host), _ptr(dx_host), _ptr(grads["router"]), _ptr(grads["gate"]), _ptr(grads["up"]),
+                  _ptr(grads["down"]), x_host.shape[0]))
+
+    def host_wait(self):
+        _check(lib().b2_moe_host_wait(self.h))
 
     def close(self):
         if self.h:

@@ -72,12 +72,21 @@ struct b2_ctx {
     bool own_stream = false;
     cudaStream_t copy_stream = nullptr;
 };
+// host-buffer entry point: two staging slots {x, dout, out, dx, aux grad} so step i+1's
+// host->device copies run while step i computes and step i's results stream back
+struct HostIo {
+    char* dev = nullptr;
+    size_t slot_bytes = 0;
+    int64_t cap_tokens = -1;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_in[2] = {}, ev_fwd[2] = {}, ev_bwd[2] = {}, ev_out[2] = {};
+    bool used[2] = {false, false};
+    int next = 0;
+};
 struct b2_moe {
     b2_ctx* ctx;
     std::unique_ptr<MoeLayer> layer;
-    void* dev_io = nullptr;  // staging for the host-buffer entry point
-    size_t dev_io_bytes = 0;
-    float* auxg = nullptr;
+    HostIo io;
 };
 struct b2_opt {
     b2_ctx* ctx;
@@ -171,8 +180,15 @@ int b2_moe_destroy(b2_moe* m) {
     return guard([&] {
         if (!m) return;
         cudaStreamSynchronize(m->ctx->c.stream);
-        if (m->dev_io) cudaFree(m->dev_io);
-        if (m->auxg) cudaFree(m->auxg);
+        HostIo& io = m->io;
+        if (io.h2d) cudaStreamSynchronize(io.h2d);
+        if (io.d2h) cudaStreamSynchronize(io.d2h);
+        if (io.dev) cudaFree(io.dev);
+        for (int b = 0; b < 2; ++b)
+            for (cudaEvent_t e : {io.ev_in[b], io.ev_fwd[b], io.ev_bwd[b], io.ev_out[b]})
+                if (e) cudaEventDestroy(e);
+        if (io.h2d) cudaStreamDestroy(io.h2d);
+        if (io.d2h) cudaStreamDestroy(io.d2h);
         delete m;
     });
 }
@@ -232,56 +248,95 @@ int b2_moe_artifacts(b2_moe* m, int64_t* sizes_host, int64_t* token_counts, int6
     });
 }
 
+// Enqueues one forward+backward over host buffers on a two-slot pipeline:
+//   h2d stream : [wait: slot's previous backward] x, dout -> slot          (ev_in)
+//   compute    : [wait ev_in, slot's previous out/dx read-back] forward (ev_fwd), aux grad,
+//                backward (ev_bwd)
+//   d2h stream : [wait ev_fwd] out -> host, [wait ev_bwd] dx -> host       (ev_out)
+static void fwd_bwd_host_enqueue(b2_moe* m, const void* x_host, const void* dout_host, const void* router,
+                                 const void* gate, const void* up, const void* down, double aux_coeff,
+                                 void* out_host, void* dx_host, void* drouter, void* dgate, void* dup, void* ddown,
+                                 int64_t s_tokens) {
+    MoeLayer& L = *m->layer;
+    const MoeConfig& c = L.cfg();
+    Context& cx = m->ctx->c;
+    HostIo& io = m->io;
+    B2_CUDA(cudaSetDevice(cx.device));
+    const size_t es = dtype_size(L.dtype());
+    const size_t tok_bytes = (size_t)s_tokens * (size_t)c.hidden * es;
+    const size_t aux_bytes = sizeof(float) * (size_t)std::max<int64_t>(1, c.n_experts * s_tokens);
+    if (io.cap_tokens < s_tokens) {  // (re)size the staging slots: drain the pipeline first
+        for (cudaStream_t q : {cx.stream, io.h2d, io.d2h})
+            if (q) B2_CUDA(cudaStreamSynchronize(q));
+        if (io.dev) B2_CUDA(cudaFree(io.dev));
+        io.slot_bytes = ((4 * tok_bytes + aux_bytes + 255) & ~size_t(255));
+        B2_CUDA(cudaMalloc((void**)&io.dev, 2 * std::max<size_t>(io.slot_bytes, 256)));
+        io.cap_tokens = s_tokens;
+        io.used[0] = io.used[1] = false;
+        if (!io.h2d) {
+            B2_CUDA(cudaStreamCreateWithFlags(&io.h2d, cudaStreamNonBlocking));
+            B2_CUDA(cudaStreamCreateWithFlags(&io.d2h, cudaStreamNonBlocking));
+            for (int b = 0; b < 2; ++b)
+                for (cudaEvent_t* e : {&io.ev_in[b], &io.ev_fwd[b], &io.ev_bwd[b], &io.ev_out[b]})
+                    B2_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        }
+    }
+    const int b = io.next;
+    io.next ^= 1;
+    char* base = io.dev + (size_t)b * io.slot_bytes;
+    void *xd = base, *outd = base + tok_bytes, *doutd = base + 2 * tok_bytes, *dxd = base + 3 * tok_bytes;
+    float* auxg = (float*)(base + 4 * tok_bytes);
+    cudaStream_t st = cx.stream;
+    // inputs: the slot's previous step must be done reading x / dout
+    if (io.used[b]) B2_CUDA(cudaStreamWaitEvent(io.h2d, io.ev_bwd[b], 0));
+    B2_CUDA(cudaMemcpyAsync(xd, x_host, tok_bytes, cudaMemcpyHostToDevice, io.h2d));
+    B2_CUDA(cudaMemcpyAsync(doutd, dout_host, tok_bytes, cudaMemcpyHostToDevice, io.h2d));
+    B2_CUDA(cudaEventRecord(io.ev_in[b], io.h2d));
+    B2_CUDA(cudaStreamWaitEvent(st, io.ev_in[b], 0));
+    if (io.used[b]) B2_CUDA(cudaStreamWaitEvent(st, io.ev_out[b], 0));  // out/dx of the slot read back
+    L.forward(xd, router, gate, up, down, s_tokens, false, outd);
+    B2_CUDA(cudaEventRecord(io.ev_fwd[b], st));
+    const float* ag = nullptr;
+    if (aux_coeff != 0.0) {
+        L.aux_probs_grad(aux_coeff, auxg);
+        ag = auxg;
+    }
+    L.backward(router, gate, up, down, doutd, ag, dxd, drouter, dgate, dup, ddown);
+    B2_CUDA(cudaEventRecord(io.ev_bwd[b], st));
+    // results stream back while the next step computes
+    B2_CUDA(cudaStreamWaitEvent(io.d2h, io.ev_fwd[b], 0));
+    B2_CUDA(cudaMemcpyAsync(out_host, outd, tok_bytes, cudaMemcpyDeviceToHost, io.d2h));
+    B2_CUDA(cudaStreamWaitEvent(io.d2h, io.ev_bwd[b], 0));
+    B2_CUDA(cudaMemcpyAsync(dx_host, dxd, tok_bytes, cudaMemcpyDeviceToHost, io.d2h));
+    B2_CUDA(cudaEventRecord(io.ev_out[b], io.d2h));
+    io.used[b] = true;
+}
+
 int b2_moe_fwd_bwd_host(b2_moe* m, const void* x_host, const void* dout_host, const void* router, const void* gate,
                         const void* up, const void* down, double aux_coeff, void* out_host, void* dx_host,
                         void* drouter, void* dgate, void* dup, void* ddown, int64_t s_tokens) {
     return guard([&] {
-        MoeLayer& L = *m->layer;
-        const MoeConfig& c = L.cfg();
-        Context& cx = m->ctx->c;
-        const size_t es = dtype_size(L.dtype());
-        const size_t tok_bytes = (size_t)s_tokens * (size_t)c.hidden * es;
-        if (m->dev_io_bytes < 4 * tok_bytes) {
-            if (m->dev_io) B2_CUDA(cudaFree(m->dev_io));
-            B2_CUDA(cudaMalloc(&m->dev_io, std::max<size_t>(4 * tok_bytes, 256)));
-            m->dev_io_bytes = 4 * tok_bytes;
-            if (m->auxg) B2_CUDA(cudaFree(m->auxg));
-            B2_CUDA(cudaMalloc((void**)&m->auxg, sizeof(float) * std::max<int64_t>(1, L.cfg().n_experts * s_tokens)));
-        }
-        char* base = (char*)m->dev_io;
-        void *dx_in = base, *ddout = base + tok_bytes, *dout_d = base + 2 * tok_bytes, *ddx = base + 3 * tok_bytes;
-        cudaStream_t st = cx.stream, cs = m->ctx->copy_stream;
-        cudaEvent_t ev_x, ev_dout, ev_fwd, ev_out;
-        B2_CUDA(cudaEventCreateWithFlags(&ev_x, cudaEventDisableTiming));
-        B2_CUDA(cudaEventCreateWithFlags(&ev_dout, cudaEventDisableTiming));
-        B2_CUDA(cudaEventCreateWithFlags(&ev_fwd, cudaEventDisableTiming));
-        B2_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
-        // x first (forward needs it), dout behind it on the copy stream (overlaps the forward)
-        B2_CUDA(cudaMemcpyAsync(dx_in, x_host, tok_bytes, cudaMemcpyHostToDevice, cs));
-        B2_CUDA(cudaEventRecord(ev_x, cs));
-        B2_CUDA(cudaMemcpyAsync(dout_d, dout_host, tok_bytes, cudaMemcpyHostToDevice, cs));
-        B2_CUDA(cudaEventRecord(ev_dout, cs));
-        B2_CUDA(cudaStreamWaitEvent(st, ev_x, 0));
-        L.forward(dx_in, router, gate, up, down, s_tokens, false, ddout);
-        B2_CUDA(cudaEventRecord(ev_fwd, st));
-        // the layer output streams back while the backward runs
-        B2_CUDA(cudaStreamWaitEvent(cs, ev_fwd, 0));
-        B2_CUDA(cudaMemcpyAsync(out_host, ddout, tok_bytes, cudaMemcpyDeviceToHost, cs));
-        B2_CUDA(cudaEventRecord(ev_out, cs));
-        const float* auxg = nullptr;
-        if (aux_coeff != 0.0) {
-            L.aux_probs_grad(aux_coeff, m->auxg);
-            auxg = m->auxg;
-        }
-        B2_CUDA(cudaStreamWaitEvent(st, ev_dout, 0));
-        L.backward(router, gate, up, down, dout_d, auxg, ddx, drouter, dgate, dup, ddown);
-        B2_CUDA(cudaMemcpyAsync(dx_host, ddx, tok_bytes, cudaMemcpyDeviceToHost, st));
-        B2_CUDA(cudaStreamWaitEvent(st, ev_out, 0));
-        B2_CUDA(cudaStreamSynchronize(st));
-        cudaEventDestroy(ev_x);
-        cudaEventDestroy(ev_dout);
-        cudaEventDestroy(ev_fwd);
-        cudaEventDestroy(ev_out);
+        fwd_bwd_host_enqueue(m, x_host, dout_host, router, gate, up, down, aux_coeff, out_host, dx_host, drouter,
+                             dgate, dup, ddown, s_tokens);
+        B2_CUDA(cudaStreamSynchronize(m->io.d2h));
+        B2_CUDA(cudaStreamSynchronize(m->ctx->c.stream));
+    });
+}
+
+int b2_moe_fwd_bwd_host_async(b2_moe* m, const void* x_host, const void* dout_host, const void* router,
+                              const void* gate, const void* up, const void* down, double aux_coeff, void* out_host,
+                              void* dx_host, void* drouter, void* dgate, void* dup, void* ddown, int64_t s_tokens) {
+    return guard([&] {
+        fwd_bwd_host_enqueue(m, x_host, dout_host, router, gate, up, down, aux_coeff, out_host, dx_host, drouter,
+                             dgate, dup, ddown, s_tokens);
+    });
+}
+
+int b2_moe_host_wait(b2_moe* m) {
+    return guard([&] {
+        if (m->io.d2h) B2_CUDA(cudaStreamSynchronize(m->io.d2h));
+        if (m->io.h2d) B2_CUDA(cudaStreamSynchronize(m->io.h2d));
+        B2_CUDA(cudaStreamSynchronize(m->ctx->c.stream));
     });
 }
 

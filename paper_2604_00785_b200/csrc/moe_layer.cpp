@@ -135,8 +135,10 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
 }
 
 MoeLayer::~MoeLayer() {
-    gfwd_.reset();
-    gbwd_.reset();
+    for (int i = 0; i < kGraphSlots; ++i) {
+        gfwd_[i].reset();
+        gbwd_[i].reset();
+    }
     for (auto& st : prof_ev_)
         for (cudaEvent_t e : st) cudaEventDestroy(e);
     if (sym_) {
@@ -250,26 +252,34 @@ void MoeLayer::GraphCache::reset() {
 void MoeLayer::set_graph(bool on) {
     B2_CUDA(cudaStreamSynchronize(ctx_.stream));
     graph_ = on;
-    gfwd_.reset();
-    gbwd_.reset();
+    for (int i = 0; i < kGraphSlots; ++i) {
+        gfwd_[i].reset();
+        gbwd_[i].reset();
+    }
 }
 
 template <typename F>
-void MoeLayer::run_graphed(GraphCache& gc, std::vector<const void*> key, F&& body) {
+void MoeLayer::run_graphed(GraphCache (&gcs)[kGraphSlots], std::vector<const void*> key, F&& body) {
     cudaStream_t st = ctx_.stream;
     if (!graph_ || profiling_ || st == nullptr) {  // the legacy default stream cannot be captured
         body();
         return;
     }
-    if (gc.exec && key == gc.key) {
-        B2_CUDA(cudaGraphLaunch(gc.exec, st));
-        launches_ = gc.launches;
+    int& lru = graph_lru_[&gcs[0] == &gfwd_[0] ? 0 : 1];
+    GraphCache* gc = nullptr;
+    for (auto& c : gcs)
+        if (c.seen && c.key == key) gc = &c;
+    if (gc && gc->exec) {
+        B2_CUDA(cudaGraphLaunch(gc->exec, st));
+        launches_ = gc->launches;
         return;
     }
-    if (!gc.seen || key != gc.key) {
-        gc.reset();
-        gc.key = std::move(key);
-        gc.seen = true;
+    if (!gc) {  // first sight of this key: run eagerly, remember it (evicting round-robin)
+        gc = &gcs[lru];
+        lru = (lru + 1) % kGraphSlots;
+        gc->reset();
+        gc->key = std::move(key);
+        gc->seen = true;
         body();
         return;
     }
@@ -280,18 +290,18 @@ void MoeLayer::run_graphed(GraphCache& gc, std::vector<const void*> key, F&& bod
     } catch (...) {
         cudaStreamEndCapture(st, &g);
         if (g) cudaGraphDestroy(g);
-        gc.reset();
+        gc->reset();
         throw;
     }
     B2_CUDA(cudaStreamEndCapture(st, &g));
-    const cudaError_t e = cudaGraphInstantiate(&gc.exec, g, 0);
+    const cudaError_t e = cudaGraphInstantiate(&gc->exec, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) {
-        gc.reset();
+        gc->reset();
         B2_CUDA(e);
     }
-    gc.launches = launches_;
-    B2_CUDA(cudaGraphLaunch(gc.exec, st));
+    gc->launches = launches_;
+    B2_CUDA(cudaGraphLaunch(gc->exec, st));
 }
 
 // dispatch weights/indices of this forward (learned top-k or FUR; the gathered table at EP > 1)

@@ -125,11 +125,15 @@ class MoeLayer {
         cudaGraphExec_t exec = nullptr;
         void reset();
     };
-    // eager the first time `key` is seen, captured the second time, replayed after that
+    // eager the first time `key` is seen, captured the second time, replayed after that;
+    // two entries per direction so double-buffered callers (the pipelined host-buffer
+    // entry point alternates two staging slots) replay both
+    static constexpr int kGraphSlots = 2;
     template <typename F>
-    void run_graphed(GraphCache& gc, std::vector<const void*> key, F&& body);
+    void run_graphed(GraphCache (&gcs)[kGraphSlots], std::vector<const void*> key, F&& body);
     bool graph_ = false;
-    GraphCache gfwd_, gbwd_;
+    GraphCache gfwd_[kGraphSlots], gbwd_[kGraphSlots];
+    int graph_lru_[2] = {0, 0};  // next slot to evict, per direction
 
     Context& ctx_;
     MoeConfig cfg_;

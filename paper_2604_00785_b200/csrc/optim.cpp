@@ -206,25 +206,44 @@ StepStats ShardedOptimizer::step(bool want_stats) {
         B2_CUDA(cudaEventRecord(ev_start_, st));
         B2_CUDA(cudaStreamWaitEvent(cs, ev_start_, 0));
     }
-    // 1. gradient sync of the params that need it (optim.cpp:136-158), on the comm stream
-    for (size_t i = 0; i < params_.size(); ++i) {
-        if (!pre_[i]) continue;
-        const ParamSlot& p = params_[i];
-        Entry& e = plan_[i];
-        const void* src = p.grad;
-        if (!p.expert && mode_ != ShardMode::epso && ctx_.ep > 1) {
-            // allreduce_mean over EP (optim.cpp:142-143)
-            all_reduce_sum(ctx_.comm->ep, p.grad, e.scratch_full, p.numel, nccl_dtype(gdt_), cs);
-            launch_scale_inplace(e.scratch_full, gdt_, p.numel, (float)(1.0 / (double)ctx_.ep), cs);
-            ++launches_;
-            src = e.scratch_full;
+    // 1. gradient sync of the params that need it (optim.cpp:136-158), on the comm stream.
+    // Each phase is one NCCL group, so the ~100 per-parameter collectives of a model go
+    // out as a few aggregated launches instead of one launch (and one latency) each.
+    auto pre_ep_of = [&](size_t i) { return !params_[i].expert && mode_ != ShardMode::epso && ctx_.ep > 1; };
+    {
+        // allreduce_mean over EP of the non-expert grads (SO / DDP with EP > 1, optim.cpp:142-143)
+        bool grp = false;
+        for (size_t i = 0; i < params_.size(); ++i) {
+            if (!pre_[i] || !pre_ep_of(i)) continue;
+            if (!grp) B2_NCCL(ncclGroupStart());
+            grp = true;
+            all_reduce_sum(ctx_.comm->ep, params_[i].grad, plan_[i].scratch_full, params_[i].numel, nccl_dtype(gdt_),
+                           cs);
         }
-        if (mode_ == ShardMode::ddp) {
-            if (ctx_.dp > 1) all_reduce_sum(ctx_.comm->dp, src, e.scratch_full, p.numel, nccl_dtype(gdt_), cs);
-        } else {
-            const int gsize = e.over_dp_ep ? ctx_.dp * ctx_.ep : ctx_.dp;
-            if (gsize > 1) reduce_scatter_v(*group_of(e), src, e.scratch, p.numel, gdt_, cs);
+        if (grp) {
+            B2_NCCL(ncclGroupEnd());
+            for (size_t i = 0; i < params_.size(); ++i) {
+                if (!pre_[i] || !pre_ep_of(i)) continue;
+                launch_scale_inplace(plan_[i].scratch_full, gdt_, params_[i].numel, (float)(1.0 / (double)ctx_.ep), cs);
+                ++launches_;
+            }
         }
+    }
+    {
+        bool grp = false;
+        for (size_t i = 0; i < params_.size(); ++i) {
+            if (!pre_[i]) continue;
+            const ParamSlot& p = params_[i];
+            Entry& e = plan_[i];
+            const void* src = pre_ep_of(i) ? e.scratch_full : p.grad;
+            const int gsize = mode_ == ShardMode::ddp ? ctx_.dp : (e.over_dp_ep ? ctx_.dp * ctx_.ep : ctx_.dp);
+            if (gsize <= 1) continue;
+            if (!grp) B2_NCCL(ncclGroupStart());
+            grp = true;
+            if (mode_ == ShardMode::ddp) all_reduce_sum(ctx_.comm->dp, src, e.scratch_full, p.numel, nccl_dtype(gdt_), cs);
+            else reduce_scatter_v(*group_of(e), src, e.scratch, p.numel, gdt_, cs);
+        }
+        if (grp) B2_NCCL(ncclGroupEnd());
     }
     if (any_pre) B2_CUDA(cudaEventRecord(ev_synced_, cs));
     // 2. global grad norm over counted slices (optim.cpp:160-166): local slices while the
@@ -267,9 +286,11 @@ StepStats ShardedOptimizer::step(bool want_stats) {
             const Entry& e = plan_[i];
             const int gsize = e.over_dp_ep ? ctx_.dp * ctx_.ep : ctx_.dp;
             if (!pre_[i] || gsize <= 1) continue;
+            if (!any_ag) B2_NCCL(ncclGroupStart());
             all_gather_v(*group_of(e), params_[i].weight, params_[i].numel, wdt_, cs);
             any_ag = true;
         }
+        if (any_ag) B2_NCCL(ncclGroupEnd());
         B2_CUDA(cudaEventRecord(ev_ag_, cs));
     }
     launch_adamw_chunks(segs_, chunks_, ids_local_, n_local_, a, norm_sq_, nonfinite_, st);

@@ -305,85 +305,84 @@ __global__ void __launch_bounds__(128) router_logits_bf16_kernel(const __nv_bflo
 
 constexpr int kMaxExpertsPerLane = 8;  // N <= 256
 
-__global__ void softmax_topk_kernel(const float* __restrict__ logits, float* __restrict__ probs,
-                                    float* __restrict__ topw, int32_t* __restrict__ topi, int S,
-                                    int N, int K, int normalize) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+// NPL = experts per lane (N <= 32 * NPL), a compile-time bound so the per-lane arrays
+// stay in registers. The fp64 exponentials go to shared memory and one lane adds them in
+// expert order (kernels.hpp:205-209); each top-k round is two warp reductions
+// (redux.sync): the max probability's bit pattern (probs are >= 0, so their IEEE bits
+// order like unsigned integers), then the lowest expert index holding it — strict '>'
+// with ties to the lower index (kernels.hpp:246-255).
+template <int NPL>
+__global__ void __launch_bounds__(256) softmax_topk_kernel(const float* __restrict__ logits, float* __restrict__ probs,
+                                                           float* __restrict__ topw, int32_t* __restrict__ topi, int S,
+                                                           int N, int K, int normalize) {
+    __shared__ double es[8][32 * NPL];
+    const int wib = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int warp = blockIdx.x * 8 + wib;
     if (warp >= S) return;
     const float* lp = logits + (int64_t)warp * N;
-    float v[kMaxExpertsPerLane];
-    double e[kMaxExpertsPerLane];
+    float v[NPL];
     float mx = lp[0];
 #pragma unroll
-    for (int i = 0; i < kMaxExpertsPerLane; ++i) {
+    for (int i = 0; i < NPL; ++i) {
         const int j = lane + 32 * i;
         v[i] = j < N ? lp[j] : 0.f;
+        if (j < N) mx = fmaxf(mx, v[i]);
     }
     // max in T (order-independent for non-NaN input)
 #pragma unroll
-    for (int i = 0; i < kMaxExpertsPerLane; ++i)
-        if (lane + 32 * i < N) mx = fmaxf(mx, v[i]);
-#pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    double e[NPL];
 #pragma unroll
-    for (int i = 0; i < kMaxExpertsPerLane; ++i)
-        e[i] = (lane + 32 * i < N) ? exp((double)v[i] - (double)mx) : 0.0;
-    // sequential fp64 sum in expert order (kernels.hpp:205-209): lane 0 walks j = 0..N-1
-    double sum = 0.0;
-#pragma unroll
-    for (int i = 0; i < kMaxExpertsPerLane; ++i) {
-        if (32 * i >= N) break;
-        for (int src = 0; src < 32; ++src) {
-            const double ej = __shfl_sync(0xffffffffu, e[i], src);
-            if (32 * i + src < N) sum += ej;
-        }
+    for (int i = 0; i < NPL; ++i) {
+        const int j = lane + 32 * i;
+        e[i] = j < N ? exp((double)v[i] - (double)mx) : 0.0;
+        if (j < N) es[wib][j] = e[i];
     }
-    float p[kMaxExpertsPerLane];
+    __syncwarp();
+    double sum = 0.0;
+    if (lane == 0) {
+        const double* row = es[wib];
+#pragma unroll 8
+        for (int j = 0; j < N; ++j) sum += row[j];
+    }
+    sum = __shfl_sync(0xffffffffu, sum, 0);
+    float p[NPL];
 #pragma unroll
-    for (int i = 0; i < kMaxExpertsPerLane; ++i) {
+    for (int i = 0; i < NPL; ++i) {
         const int j = lane + 32 * i;
         p[i] = (float)(e[i] / sum);
         if (j < N) probs[(int64_t)warp * N + j] = p[i];
     }
-    // K argmax rounds, strict '>' => lower index wins ties (kernels.hpp:246-255)
     unsigned taken = 0;
     float wsum = 0.f;
-    float wk[16];
     for (int c = 0; c < K; ++c) {
-        float bv = 0.f;
+        // this lane's best untaken candidate (within a lane j increases: strict '>')
+        uint32_t bb = 0;
         int bi = 0x7fffffff;
 #pragma unroll
-        for (int i = 0; i < kMaxExpertsPerLane; ++i) {
+        for (int i = 0; i < NPL; ++i) {
             const int j = lane + 32 * i;
             if (j < N && !(taken >> i & 1u)) {
-                if (bi == 0x7fffffff || p[i] > bv) {  // within a lane j increases: strict '>'
-                    bv = p[i];
+                const uint32_t pb = __float_as_uint(p[i]);
+                if (bi == 0x7fffffff || pb > bb) {
+                    bb = pb;
                     bi = j;
                 }
             }
         }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            const bool better = (oi != 0x7fffffff) &&
-                                (bi == 0x7fffffff || ov > bv || (ov == bv && oi < bi));
-            if (better) {
-                bv = ov;
-                bi = oi;
-            }
-        }
-        if (lane == bi % 32) taken |= 1u << (bi / 32);
-        if (c < 16) wk[c] = bv;
+        const uint32_t best = __reduce_max_sync(0xffffffffu, bi == 0x7fffffff ? 0u : bb);
+        const uint32_t cand = (bi != 0x7fffffff && bb == best) ? (uint32_t)bi : 0xffffffffu;
+        const int win = (int)__reduce_min_sync(0xffffffffu, cand);
+        if (lane == win % 32) taken |= 1u << (win / 32);
+        const float bv = __uint_as_float(best);
+        wsum += bv;  // K-order sum in T for the renormalisation (moe.hpp:72-78)
         if (lane == 0) {
-            topi[(int64_t)warp * K + c] = bi;
+            topi[(int64_t)warp * K + c] = win;
             topw[(int64_t)warp * K + c] = bv;
         }
     }
-    if (normalize && lane == 0) {  // moe.hpp:72-78, T arithmetic
-        for (int c = 0; c < K; ++c) wsum += (c < 16 ? wk[c] : topw[(int64_t)warp * K + c]);
+    if (normalize && lane == 0)
         for (int c = 0; c < K; ++c) topw[(int64_t)warp * K + c] = __fdiv_rn(topw[(int64_t)warp * K + c], wsum);
-    }
 }
 
 // forced uniform routing (moe.hpp:84-99): expert (t*K+j) mod N, weight 1/K
@@ -589,9 +588,11 @@ void launch_softmax_topk(const float* logits, float* probs, float* topw, int32_t
                          bool normalize, cudaStream_t st) {
     check(N <= 32 * kMaxExpertsPerLane, "route: n_experts above 256 is not supported by the router kernel");
     if (S == 0) return;
-    const int warps_per_block = 8;
-    softmax_topk_kernel<<<(unsigned)ceil_div(S, warps_per_block), 32 * warps_per_block, 0, st>>>(
-        logits, probs, topw, topi, S, N, K, normalize ? 1 : 0);
+    const unsigned grid = (unsigned)ceil_div(S, 8);  // 8 warps (tokens) per block
+    const int nm = normalize ? 1 : 0;
+    if (N <= 64) softmax_topk_kernel<2><<<grid, 256, 0, st>>>(logits, probs, topw, topi, S, N, K, nm);
+    else if (N <= 128) softmax_topk_kernel<4><<<grid, 256, 0, st>>>(logits, probs, topw, topi, S, N, K, nm);
+    else softmax_topk_kernel<8><<<grid, 256, 0, st>>>(logits, probs, topw, topi, S, N, K, nm);
     B2_LAUNCH_CHECK();
 }
 

@@ -348,3 +348,36 @@ def test_tma_gather_matches_materialised_rows(b2ctx):
         res.append([out] + [g[k] for k in ("input", "router", "gate", "up", "down")])
     for a, b in zip(*res):
         assert torch.equal(a, b)
+
+
+def test_host_pipeline_matches_synchronous(b2ctx):
+    """b2_moe_fwd_bwd_host_async (two staging slots, copies overlapped with compute) gives
+    every step exactly the results of the synchronous host-buffer call."""
+    b2, _ = b2ctx
+    stream = torch.cuda.Stream()
+    ctx = b2.Context(0, stream=stream)
+    cfg = b2.MoeConfig(n_experts=16, top_k=4, hidden=256, intermediate=128)
+    S = 256
+    gen = torch.Generator(device="cuda").manual_seed(21)
+    mk = lambda shape, std: (torch.randn(shape, device="cuda", generator=gen) * std).bfloat16()
+    router, gate, up, down = mk((256, 16), 0.05), mk((16, 256, 128), 0.05), mk((16, 256, 128), 0.05), \
+        mk((16, 128, 256), 0.05)
+    xs = [mk((S, 256), 1.0).cpu().pin_memory() for _ in range(4)]
+    ds = [mk((S, 256), 1.0).cpu().pin_memory() for _ in range(4)]
+    grads = lambda: dict(router=torch.empty_like(router), gate=torch.empty_like(gate), up=torch.empty_like(up),
+                         down=torch.empty_like(down))
+    ref_layer, pipe_layer = b2.MoeLayer(ctx, cfg, torch.bfloat16, S), b2.MoeLayer(ctx, cfg, torch.bfloat16, S)
+    pipe_layer.set_graph(True)
+    want, outs = [], []
+    for i in range(4):
+        o, d, g = torch.empty_like(xs[i]).pin_memory(), torch.empty_like(xs[i]).pin_memory(), grads()
+        ref_layer.fwd_bwd_host(xs[i], ds[i], router, gate, up, down, o, d, g, 0.01)
+        want.append((o, d))
+    g = grads()
+    for i in range(4):
+        o, d = torch.empty_like(xs[i]).pin_memory(), torch.empty_like(xs[i]).pin_memory()
+        pipe_layer.fwd_bwd_host(xs[i], ds[i], router, gate, up, down, o, d, g, 0.01, wait=False)
+        outs.append((o, d))
+    pipe_layer.host_wait()
+    for (o, d), (wo, wd) in zip(outs, want):
+        assert torch.equal(o, wo) and torch.equal(d, wd)
