@@ -409,6 +409,13 @@ def main():
     gemm_ms = sum(st[k] for k in gemm_stages)
     rt = int(layer_rt(layer))
     gemm_flop = 18.0 * rt * H * I
+    # expert-parallel load balance: routed rows on this rank vs the mean over ranks
+    rows_t = torch.tensor([float(rt)], device=dev)
+    rows_max, rows_sum = rows_t.clone(), rows_t.clone()
+    if world > 1:
+        dist.all_reduce(rows_max, op=dist.ReduceOp.MAX)
+        dist.all_reduce(rows_sum, op=dist.ReduceOp.SUM)
+    ep_balance = float(rows_max.item()) / (float(rows_sum.item()) / world)
     achieved = gemm_flop / (gemm_ms * 1e-3) / 1e12
     if args.profile and rank == 0:
         for k_, v in st.items():
@@ -476,6 +483,7 @@ def main():
                          "flop_per_step": gemm_flop, "gemm_ms_per_step": gemm_ms,
                          "frac_of_sustained": achieved / bf16_sust if bf16_sust else None},
             "stage_ms": {k: round(v, 4) for k, v in st.items()},
+            "ep_rows_max_over_mean": ep_balance,
             "model_flop_per_token": FLOP_PER_TOKEN,
             "model_tflops": value * FLOP_PER_TOKEN / 1e12 / world,
             "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": 2 * tok_bytes,

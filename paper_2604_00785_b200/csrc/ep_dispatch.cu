@@ -10,12 +10,14 @@
 //   gather   the expert owner PULLS each gathered token that has a local expert once
 //            from the source rank's x over NVLink (CUDA IPC mapping) and writes it to
 //            every padded row of that token (dedup per destination);
-//   combine  the owner computes the token's weighted partial row and STORES it straight
-//            into the source rank's return slab [owner][t] (peer memory);
-//   return   after a barrier the source sums the slabs of the ranks its token routed
-//            to, in rank order (the reducescatter's member order, comm.hpp:391-394).
-// The backward pulls dout rows the same way and pushes dX partial rows and the top-k
-// weight gradients back. No host synchronisation, no staging copies.
+//   combine  the owner combines the token's local slots (weighted, slot order) into its OWN
+//            slab row [gid]; after a barrier the source PULLS the rows of the ranks its
+//            token routed to and sums them in rank order (the reducescatter's member order,
+//            comm.hpp:391-394) — remote loads with many bytes in flight, fused with the sum.
+// The backward pulls dout rows the same way; dX partial rows and the top-k weight
+// gradients go back through the owners' slabs and the same pull-sum. No host
+// synchronisation, no staging copies. (The push-based kernels below are kept for the
+// stress tests of the peer-store path.)
 #include "b2_common.cuh"
 #include "kernels.h"
 
@@ -92,7 +94,7 @@ template <typename T>
 __global__ void ep_combine_push_vec_kernel(const T* __restrict__ y, const int32_t* __restrict__ slot_prow,
                                            const int32_t* __restrict__ selected_k, const int32_t* __restrict__ cec,
                                            const float* __restrict__ gw, int K, int S, int T_tot, int H, int me,
-                                           T* const* __restrict__ peer_ret) {
+                                           T* const* __restrict__ peer_ret, T* __restrict__ local_out) {
     constexpr int V = 16 / sizeof(T);
     const int lane = threadIdx.x % 32;
     const int nw = gridDim.x * blockDim.x / 32;
@@ -100,7 +102,7 @@ __global__ void ep_combine_push_vec_kernel(const T* __restrict__ y, const int32_
     for (int gid = (blockIdx.x * blockDim.x + threadIdx.x) / 32; gid < T_tot; gid += nw) {
         const int j0 = cec[gid], j1 = cec[gid + 1];
         if (j0 == j1) continue;
-        T* dst = peer_ret[gid / S] + ((int64_t)me * S + gid % S) * H;
+        T* dst = local_out ? local_out + (int64_t)gid * H : peer_ret[gid / S] + ((int64_t)me * S + gid % S) * H;
         // all local slot rows of a column block are loaded together (<= 8 in flight)
         constexpr int MAXJ = 8;
         for (int v = lane; v < nv; v += 32) {
@@ -153,7 +155,7 @@ __global__ void ep_combine_push_vec_kernel(const T* __restrict__ y, const int32_
             reinterpret_cast<int4*>(dst)[v] = o;
         }
     }
-    __threadfence_system();
+    if (!local_out) __threadfence_system();
 }
 
 // the owner's top-k weight-gradient rows of the gathered tokens it serves, pushed to
@@ -245,6 +247,84 @@ __global__ void ep_return_sum_kernel(const T* __restrict__ slab, const int32_t* 
     }
 }
 
+// out[t] = sum over the ranks r (in order) that token t routes to of owner r's partial row
+// [me * S + t], read over NVLink from r's own slab (written there before the barrier):
+// the reducescatter of moe.hpp:378 / 427-428 in member order, as remote loads with up to
+// 8 owners' 16-byte vectors in flight per lane
+template <typename T>
+__global__ void ep_pull_sum_kernel(const T* const* __restrict__ peer_slab, const int32_t* __restrict__ gi_local,
+                                   int S, int K, int E, int NR, int W, int me, T* __restrict__ out) {
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+    if (t >= S) return;
+    unsigned mask = 0;
+    for (int k = 0; k < K; ++k) mask |= 1u << (gi_local[(int64_t)t * K + k] / NR);
+    const int64_t row = (int64_t)me * S + t;
+    if (((int64_t)W * sizeof(T)) % 16 == 0) {
+        constexpr int V = 16 / sizeof(T), MAXR = 8;
+        for (int v = lane; v < W / V; v += 32) {
+            float acc[V];
+            bool any = false;
+            for (int r0 = 0; r0 < E; r0 += MAXR) {
+                int4 raw[MAXR];
+#pragma unroll
+                for (int q = 0; q < MAXR; ++q)
+                    if (r0 + q < E && (mask >> (r0 + q) & 1u))
+                        raw[q] = __ldcv(reinterpret_cast<const int4*>(peer_slab[r0 + q] + row * W) + v);
+#pragma unroll
+                for (int q = 0; q < MAXR; ++q) {
+                    if (!(r0 + q < E && (mask >> (r0 + q) & 1u))) continue;
+                    float f[V];
+                    if constexpr (sizeof(T) == 4) {
+                        f[0] = __int_as_float(raw[q].x);
+                        f[1] = __int_as_float(raw[q].y);
+                        f[2] = __int_as_float(raw[q].z);
+                        f[3] = __int_as_float(raw[q].w);
+                    } else {
+                        const uint32_t w[4] = {(uint32_t)raw[q].x, (uint32_t)raw[q].y, (uint32_t)raw[q].z,
+                                               (uint32_t)raw[q].w};
+#pragma unroll
+                        for (int z = 0; z < 4; ++z) {
+                            f[2 * z] = __uint_as_float(w[z] << 16);
+                            f[2 * z + 1] = __uint_as_float(w[z] & 0xFFFF0000u);
+                        }
+                    }
+#pragma unroll
+                    for (int z = 0; z < V; ++z) acc[z] = any ? __fadd_rn(acc[z], f[z]) : f[z];
+                    any = true;
+                }
+            }
+            if (!any)
+                for (int z = 0; z < V; ++z) acc[z] = 0.f;
+            int4 o;
+            if constexpr (sizeof(T) == 4) {
+                o = make_int4(__float_as_int(acc[0]), __float_as_int(acc[1]), __float_as_int(acc[2]),
+                              __float_as_int(acc[3]));
+            } else {
+                uint32_t w[4];
+#pragma unroll
+                for (int z = 0; z < 4; ++z) {
+                    __nv_bfloat162 b = __floats2bfloat162_rn(acc[2 * z], acc[2 * z + 1]);
+                    w[z] = *reinterpret_cast<uint32_t*>(&b);
+                }
+                o = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
+            }
+            reinterpret_cast<int4*>(out + (int64_t)t * W)[v] = o;
+        }
+    } else {
+        for (int c = lane; c < W; c += 32) {
+            float acc = 0.f;
+            bool any = false;
+            for (int r = 0; r < E; ++r) {
+                if (!(mask >> r & 1u)) continue;
+                const float v = Elem<T>::to_f(__ldcv(peer_slab[r] + row * W + c));
+                acc = any ? __fadd_rn(acc, v) : v;
+                any = true;
+            }
+            out[(int64_t)t * W + c] = Elem<T>::from_f(acc);
+        }
+    }
+}
+
 static unsigned ep_grid(int64_t warps) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(148 * 16, ceil_div(warps, 8))); }
 
 template <typename T>
@@ -262,10 +342,28 @@ void launch_ep_combine_push(const T* y, const int32_t* slot_prow, const int32_t*
     if (T_tot <= 0) return;
     if (((int64_t)H * sizeof(T)) % 16 == 0)
         ep_combine_push_vec_kernel<T><<<ep_grid(T_tot), 256, 0, st>>>(y, slot_prow, selected_k, cec, gw, K, S, T_tot,
-                                                                      H, me, peer_ret);
+                                                                      H, me, peer_ret, nullptr);
     else
         ep_combine_push_kernel<T><<<ep_grid(T_tot), 256, 0, st>>>(y, slot_prow, selected_k, cec, gw, K, S, T_tot, H,
                                                                   me, peer_ret);
+    B2_LAUNCH_CHECK();
+}
+
+template <typename T>
+void launch_ep_combine_local(const T* y, const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec,
+                             const float* gw, int K, int S, int T_tot, int H, T* own_slab, cudaStream_t st) {
+    if (T_tot <= 0) return;
+    check(((int64_t)H * sizeof(T)) % 16 == 0, "ep combine: rows must be 16-byte multiples");
+    ep_combine_push_vec_kernel<T><<<ep_grid(T_tot), 256, 0, st>>>(y, slot_prow, selected_k, cec, gw, K, S, T_tot, H,
+                                                                  0, nullptr, own_slab);
+    B2_LAUNCH_CHECK();
+}
+
+template <typename T>
+void launch_ep_pull_sum(const T* const* peer_slab, const int32_t* gi_local, int S, int K, int E, int NR, int W, int me,
+                        T* out, cudaStream_t st) {
+    if (S <= 0) return;
+    ep_pull_sum_kernel<T><<<(unsigned)ceil_div(S, 8), 256, 0, st>>>(peer_slab, gi_local, S, K, E, NR, W, me, out);
     B2_LAUNCH_CHECK();
 }
 
@@ -291,7 +389,11 @@ void launch_ep_return_sum(const T* slab, const int32_t* gi_local, int S, int K, 
                                            cudaStream_t);                                                         \
     template void launch_ep_combine_push<T>(const T*, const int32_t*, const int32_t*, const int32_t*, const float*, \
                                             int, int, int, int, int, T* const*, cudaStream_t);                   \
-    template void launch_ep_return_sum<T>(const T*, const int32_t*, int, int, int, int, int, T*, cudaStream_t);
+    template void launch_ep_return_sum<T>(const T*, const int32_t*, int, int, int, int, int, T*, cudaStream_t); \
+    template void launch_ep_combine_local<T>(const T*, const int32_t*, const int32_t*, const int32_t*, const float*, \
+                                             int, int, int, int, T*, cudaStream_t);                              \
+    template void launch_ep_pull_sum<T>(const T* const*, const int32_t*, int, int, int, int, int, int, T*,        \
+                                        cudaStream_t);
 B2_EP_INST(float)
 B2_EP_INST(__nv_bfloat16)
 #undef B2_EP_INST

@@ -81,6 +81,15 @@ template <typename T>
 void launch_ep_combine_push(const T* y, const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec,
                             const float* gw, int K, int S, int T_tot, int H, int me, T* const* peer_ret,
                             cudaStream_t st);
+// owner side of the pull-based combine: the token's (weighted) partial row into the owner's
+// OWN slab row [gid]; sources pull them after a barrier (launch_ep_pull_sum)
+template <typename T>
+void launch_ep_combine_local(const T* y, const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec,
+                             const float* gw, int K, int S, int T_tot, int H, T* own_slab, cudaStream_t st);
+// out[t] = sum over t's owner ranks (in rank order) of peer_slab[r][(me*S + t)*W ..]
+template <typename T>
+void launch_ep_pull_sum(const T* const* peer_slab, const int32_t* gi_local, int S, int K, int E, int NR, int W, int me,
+                        T* out, cudaStream_t st);
 void launch_ep_wgrad_push(const float* wgrad, const int32_t* cec, int K, int S, int T_tot, int me,
                           float* const* peer_wret, cudaStream_t st);
 template <typename T>

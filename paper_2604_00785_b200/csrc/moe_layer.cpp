@@ -494,10 +494,11 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     if (E > 1) {
         // weighted partial rows stored into the source ranks' slabs, then summed there in
         // rank order (the reducescatter of moe.hpp:378)
-        launch_ep_combine_push<T>((const T*)y_, slot_prow_, selected_k_, cec_, gw_, K, S, Tt, H, ctx_.coord_ep,
-                                  (T* const*)peer_tab_ + 2 * E, st);
+        // each owner combines its slots into its OWN slab row [gid]; after the barrier the
+        // source pulls its rows from the owners and sums them in rank order
+        launch_ep_combine_local<T>((const T*)y_, slot_prow_, selected_k_, cec_, gw_, K, S, Tt, H, (T*)ret_f_, st);
         ep_barrier();
-        launch_ep_return_sum<T>((const T*)ret_f_, gi_local_, S, K, E, nr, H, out, st);
+        launch_ep_pull_sum<T>((const T* const*)peer_tab_ + 2 * E, gi_local_, S, K, E, nr, H, ctx_.coord_ep, out, st);
         launches_ += 2;
     } else {
         launch_combine<T>((const T*)y_, slot_prow_, selected_k_, cec_, gw_, out, Tt, H, K, st);
@@ -546,8 +547,10 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         ep_barrier();
         peer_dout = (const T* const*)peer_tab_ + E;
     }
-    launch_out_reduction_bwd<T>(dout, peer_dout, S, (const T*)y_, slot_prow_, selected_k_, cec_, gw_, (T*)dy_, wgrad_,
-                                Tt, H, K, st);
+    // EP > 1: the top-k weight gradients go straight into this rank's symmetric slab, where
+    // the sources pull them from
+    launch_out_reduction_bwd<T>(dout, peer_dout, S, (const T*)y_, slot_prow_, selected_k_, cec_, gw_, (T*)dy_,
+                                E > 1 ? wret_ : wgrad_, Tt, H, K, st);
     launch_zero_pad_rows<T>((T*)dy_, prow_src_, p_total, H, pmax_, st);
     launches_ += 2;
     mark(kOutRedBwd, true);
@@ -685,17 +688,18 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
     const float* wgrad_local = wgrad_;
     const T* dx_rows = nullptr;  // EP > 1: the token's summed expert-gradient rows
     if (E > 1) {
-        // the two reducescatters of moe.hpp:427-428: per-token partial dX rows and the
-        // weight grads go back to the source, which sums them in rank order
-        launch_ep_combine_push<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, K, S, Tt, H, ctx_.coord_ep,
-                                  (T* const*)peer_tab_ + 3 * E, st);
-        launch_ep_wgrad_push(wgrad_, cec_, K, S, Tt, ctx_.coord_ep, (float* const*)peer_tab_ + 4 * E, st);
+        // the two reducescatters of moe.hpp:427-428: owners combine dX partials into their own slab (the top-k weight gradients already
+        // sit in their own wret, written by the output-reduction backward); after the barrier
+        // each source pulls and sums its rows in rank order
+        launch_ep_combine_local<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, K, S, Tt, H, (T*)ret_b_, st);
         ep_barrier();
-        launch_ep_return_sum<T>((const T*)ret_b_, gi_local_, S, K, E, nr, H, (T*)dx_exp_, st);
-        launch_ep_return_sum<float>(wret_, gi_local_, S, K, E, nr, K, wgrad_local_, st);
+        launch_ep_pull_sum<T>((const T* const*)peer_tab_ + 3 * E, gi_local_, S, K, E, nr, H, ctx_.coord_ep,
+                              (T*)dx_exp_, st);
+        launch_ep_pull_sum<float>((const float* const*)peer_tab_ + 4 * E, gi_local_, S, K, E, nr, K, ctx_.coord_ep,
+                                  wgrad_local_, st);
         wgrad_local = wgrad_local_;
         dx_rows = (const T*)dx_exp_;
-        launches_ += 4;
+        launches_ += 3;
     }
     const bool tc_router = dtype_ == BF16 && N % 8 == 0 && N <= 256;
     launch_router_dlogits(probs_, wgrad_local, topi_, topw_, aux_probs_grad, dlogits_, tc_router ? dl_bf16_ : nullptr,

@@ -23,6 +23,8 @@ for w in $WHAT; do case $w in
       bench.py --gpus 2 --steps 10 --warmup 3 > $OUT/ep2.json 2> $OUT/ep2.err; echo "ep2 rc=$?"; cat $OUT/ep2.json; tail -5 $OUT/ep2.err ;;
  timeline) timeout 300 python tools/timeline.py > $OUT/timeline_eager.txt 2>&1; echo "timeline rc=$?"; head -30 $OUT/timeline_eager.txt
       timeout 300 python tools/timeline.py --graph > $OUT/timeline_graph.txt 2>&1; head -30 $OUT/timeline_graph.txt ;;
+ tl2) timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29513 tools/timeline.py --graph 2>&1 | grep -v "Warn\|warn\|\*\*\*\|OMP" | head -45 ;;
+ tl4) timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29514 tools/timeline.py --graph 2>&1 | grep -v "Warn\|warn\|\*\*\*\|OMP" | head -45 ;;
  ab) for opt in "--graph" "--graph --tma-gather"; do echo "== timeline $opt"; timeout 300 python tools/timeline.py $opt 2>&1 | grep -v Warn | head -24; done ;;
  gtest) timeout 600 python -m pytest tests -m gpu -x -q -k "${GTEST_K}" > $OUT/gtest.log 2>&1; echo "gtest rc=$?"; tail -15 $OUT/gtest.log ;;
  ep4) timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29512 \

@@ -22,14 +22,25 @@ def main():
 
     import paper_2604_00785_b200 as b2
     H, N, K, I, S = 2048, 64, 8, 1024, args.tokens
-    dev = torch.device("cuda", 0)
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    dev = torch.device("cuda", rank)
+    torch.cuda.set_device(dev)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    ctx = b2.Context(0, stream=stream)
-    cfg = b2.MoeConfig(n_experts=N, top_k=K, hidden=H, intermediate=I)
-    gen = torch.Generator(device=dev).manual_seed(1234)
+    nccl_id = None
+    if world > 1:  # EP = world over NVLink peer memory (launch with torchrun)
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        ids = [b2.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        nccl_id = ids[0]
+    ctx = b2.Context(rank, rank=rank, ep=world, nccl_id=nccl_id, stream=stream)
+    cfg = b2.MoeConfig(n_experts=N, top_k=K, hidden=H, intermediate=I, ep=world)
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     mk = lambda shape, std: (torch.randn(shape, device=dev, generator=gen) * std).bfloat16()
-    router, gate, up, down = mk((H, N), 0.02), mk((N, H, I), 0.02), mk((N, H, I), 0.02), mk((N, I, H), 0.02)
+    NR = N // world
+    router = (torch.randn((H, N), device=dev, generator=torch.Generator(device=dev).manual_seed(7)) * 0.02).bfloat16()
+    gate, up, down = mk((NR, H, I), 0.02), mk((NR, H, I), 0.02), mk((NR, I, H), 0.02)
     x, dout = mk((S, H), 1.0), mk((S, H), 1.0)
     layer = b2.MoeLayer(ctx, cfg, torch.bfloat16, S)
     if args.graph:
@@ -57,11 +68,14 @@ def main():
         step()
     e1.record(stream)
     torch.cuda.synchronize()
-    print(f"event-timed step: {e0.elapsed_time(e1) / 10:.3f} ms")
+    if rank == 0:
+        print(f"event-timed step: {e0.elapsed_time(e1) / 10:.3f} ms (EP={world})")
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(args.steps):
             step()
         torch.cuda.synchronize()
+    if rank != 0:
+        return
     ev = [e for e in prof.events() if e.device_type.name == "CUDA" and e.time_range.elapsed_us() > 0]
     ev.sort(key=lambda e: e.time_range.start)
     agg = collections.defaultdict(list)
