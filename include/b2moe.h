@@ -97,6 +97,16 @@ int b2_ctx_sync(b2_ctx* ctx);
  * (moe.hpp:344-466) and the state they share (FastMoeState, moe.hpp:302-316).
  * max_tokens is the per-rank S capacity; the state owns its workspace. */
 int b2_moe_create(b2_ctx* ctx, const b2_moe_cfg* cfg, int dtype, int64_t max_tokens, b2_moe** out);
+/* moe_block_forward's `ckpt` (blocks.cpp:339-377) and a workspace shared across layers:
+ * share_workspace (or NULL) lends its activation workspace to the new layer (it must be
+ * at least as large); with checkpoint != 0 the layer holds only its input pointer and the
+ * balancing statistics between forward and backward, and b2_moe_backward replays the
+ * forward (EP collectives included) first — gradients are bitwise those of the
+ * non-checkpointed layer (test_model.cpp:680-720). The caller keeps x alive until backward. */
+int b2_moe_create_ex(b2_ctx* ctx, const b2_moe_cfg* cfg, int dtype, int64_t max_tokens, const b2_moe* share_workspace,
+                     int checkpoint, b2_moe** out);
+/* bytes held between forward and backward (MoeRec::held, blocks.cpp:343-350) */
+int64_t b2_moe_held_bytes(b2_moe* m);
 int b2_moe_destroy(b2_moe* m);
 /* fast_moe_forward (moe.hpp:344-390): out [S,H] */
 int b2_moe_forward(b2_moe* m, const void* x, const void* router, const void* gate, const void* up,

@@ -107,6 +107,8 @@ SIGNATURES = {
     "b2_shard_slice": (C.c_int, [I64, C.c_int, C.c_int, P, P]),
     "b2_moe_set_profiling": (C.c_int, [P, C.c_int]),
     "b2_moe_set_graph": (C.c_int, [P, C.c_int]),
+    "b2_moe_create_ex": (C.c_int, [P, P, C.c_int, I64, P, C.c_int, P]),
+    "b2_moe_held_bytes": (I64, [P]),
     "b2_moe_stage_times": (C.c_int, [P, P]),
     "b2_moe_stage_name": (C.c_char_p, [C.c_int]),
     "b2_moe_last_launches": (C.c_int, [P]),
@@ -260,16 +262,26 @@ class Context:
 class MoeLayer:
     """FastSparseMoE layer on one rank (FastMoeState + fast_moe_forward/backward)."""
 
-    def __init__(self, ctx: Context, cfg: MoeConfig, dtype, max_tokens: int):
+    def __init__(self, ctx: Context, cfg: MoeConfig, dtype, max_tokens: int, share_workspace=None,
+                 checkpoint: bool = False):
+        """share_workspace: another MoeLayer whose activation workspace this one reuses;
+        checkpoint: hold only x between forward and backward and replay the forward in
+        backward (moe_block_forward's ckpt, blocks.cpp:339-377)."""
         torch = _torch()
         self.ctx, self.cfg = ctx, cfg
         self.dtype = dtype
         self.dt = F32 if dtype == torch.float32 else BF16
         h = C.c_void_p()
         c = cfg.c()
-        _check(lib().b2_moe_create(ctx.h, C.byref(c), self.dt, max_tokens, C.byref(h)))
+        _check(lib().b2_moe_create_ex(ctx.h, C.byref(c), self.dt, max_tokens,
+                                      share_workspace.h if share_workspace is not None else None, int(checkpoint),
+                                      C.byref(h)))
         self.h = h
+        self._share = share_workspace  # keeps the lender alive
         self.s = 0
+
+    def held_bytes(self) -> int:
+        return lib().b2_moe_held_bytes(self.h)
 
     def forward(self, x, router, gate, up, down, fur: bool = False, out=None):
         torch = _torch()

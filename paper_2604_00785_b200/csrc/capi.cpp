@@ -165,16 +165,25 @@ int b2_ctx_destroy(b2_ctx* ctx) {
 
 int b2_ctx_sync(b2_ctx* ctx) { return guard([&] { B2_CUDA(cudaStreamSynchronize(ctx->c.stream)); }); }
 
-int b2_moe_create(b2_ctx* ctx, const b2_moe_cfg* cfg, int dtype, int64_t max_tokens, b2_moe** out) {
+int b2_moe_create_ex(b2_ctx* ctx, const b2_moe_cfg* cfg, int dtype, int64_t max_tokens, const b2_moe* share_workspace,
+                     int checkpoint, b2_moe** out) {
     return guard([&] {
         check(ctx != nullptr, "moe: null context");
         auto m = std::make_unique<b2_moe>();
         m->ctx = ctx;
         if (dtype == BF16) check(sm100_available(), "bf16 expert path needs an sm_100 (B200) device");
-        m->layer = std::make_unique<MoeLayer>(ctx->c, to_cfg(cfg), dtype, max_tokens);
+        m->layer = std::make_unique<MoeLayer>(ctx->c, to_cfg(cfg), dtype, max_tokens,
+                                              share_workspace ? share_workspace->layer.get() : nullptr,
+                                              checkpoint != 0);
         *out = m.release();
     });
 }
+
+int b2_moe_create(b2_ctx* ctx, const b2_moe_cfg* cfg, int dtype, int64_t max_tokens, b2_moe** out) {
+    return b2_moe_create_ex(ctx, cfg, dtype, max_tokens, nullptr, 0, out);
+}
+
+int64_t b2_moe_held_bytes(b2_moe* m) { return m ? (int64_t)m->layer->held_bytes() : -1; }
 
 int b2_moe_destroy(b2_moe* m) {
     return guard([&] {

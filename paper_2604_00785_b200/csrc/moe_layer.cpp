@@ -31,7 +31,19 @@ void MoeConfig::validate() const {
 }
 
 Arena::~Arena() {
-    if (base_) cudaFree(base_);
+    if (base_ && owned_) cudaFree(base_);
+}
+
+void Arena::adopt(char* base, size_t cap) {
+    check(base_ == nullptr, "arena: already reserved");
+    base_ = base;
+    cap_ = cap;
+    off_ = 0;
+    owned_ = false;
+}
+
+Workspace::~Workspace() {
+    if (base) cudaFree(base);
 }
 
 void Arena::reserve(size_t bytes) {
@@ -48,8 +60,9 @@ void* Arena::take_bytes(size_t bytes) {
     return base_ + a;
 }
 
-MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_tokens)
-    : ctx_(ctx), cfg_(cfg), dtype_(dtype) {
+MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_tokens, const MoeLayer* share_ws,
+                   bool checkpoint)
+    : ctx_(ctx), cfg_(cfg), dtype_(dtype), checkpoint_(checkpoint) {
     cfg_.validate();
     check(dtype == F32 || dtype == BF16, "moe: dtype must be f32 or bf16");
     check(cfg_.ep == ctx_.ep, "fast_moe: cfg.ep must match the EP group size");
@@ -64,70 +77,83 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     const size_t es = dtype_size(dtype);
     size_t bytes = 0;
     auto acc = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
-    // fp32
-    for (int64_t n : {smax_ * N, smax_ * N, smax_ * K, tmax_ * K, (ceil_div(smax_, 128) + 1) * N, N, tmax_ * K,
+    // workspace: fp32
+    for (int64_t n : {smax_ * N, smax_ * N, smax_ * K, tmax_ * K, (ceil_div(smax_, 128) + 1) * N, tmax_ * K,
                       smax_ * N, (int64_t)kRouterDwMaxSplits * H * N})
         acc(4 * (size_t)std::max<int64_t>(n, 1));
-    // int32
-    for (int64_t n : {smax_ * K, tmax_ * K, N, nch * nr, nch * nr, tmax_, tmax_ + 1, nr * thmax_, nr * thmax_ + 1, nr,
-                      nr + 1, nr + 1, tmax_ * K, tmax_ * K, tmax_ * K, tmax_ * K, pmax_, (int64_t)1})
+    // workspace: int32
+    for (int64_t n : {smax_ * K, tmax_ * K, nch * nr, nch * nr, tmax_, tmax_ + 1, nr * thmax_, nr * thmax_ + 1, nr,
+                      nr + 1, nr + 1, tmax_ * K, tmax_ * K, tmax_ * K, tmax_ * K, pmax_})
         acc(4 * (size_t)std::max<int64_t>(n, 1));
-    // dtype, padded rows
+    // workspace: dtype, padded rows (+ the replay output)
     for (int64_t n : {pmax_ * H, pmax_ * I, pmax_ * I, pmax_ * I, pmax_ * H, pmax_ * H, pmax_ * I, pmax_ * 2 * I,
-                      pmax_ * H})
+                      pmax_ * H, smax_ * H})
         acc(es * (size_t)std::max<int64_t>(n, 1));
     acc(2 * (size_t)std::max<int64_t>(smax_ * N, 1));
     const int E = cfg_.ep;
     if (E > 1) {
-        for (int64_t n : {tmax_ * K, tmax_ * K, smax_ * K, (int64_t)8}) acc(4 * (size_t)std::max<int64_t>(n, 1));
+        for (int64_t n : {tmax_ * K, tmax_ * K, smax_ * K}) acc(4 * (size_t)std::max<int64_t>(n, 1));
         acc(es * (size_t)std::max<int64_t>(smax_ * H, 1));
     }
     B2_CUDA(cudaSetDevice(ctx_.device));
-    arena_.reserve(bytes);
-    logits_ = arena_.take<float>(smax_ * N);
-    probs_ = arena_.take<float>(smax_ * N);
-    topw_ = arena_.take<float>(smax_ * K);
-    fw_ = arena_.take<float>(tmax_ * K);
-    colsum_ = arena_.take<float>((ceil_div(smax_, 128) + 1) * N);
+    if (share_ws) {
+        check(share_ws->ws_ && share_ws->ws_->cap >= bytes && share_ws->ctx_.device == ctx_.device,
+              "moe: the shared workspace is too small for this layer (or on another device)");
+        ws_ = share_ws->ws_;
+    } else {
+        ws_ = std::make_shared<Workspace>();
+        B2_CUDA(cudaMalloc((void**)&ws_->base, std::max<size_t>(bytes, 256)));
+        ws_->cap = bytes;
+    }
+    ws_arena_.adopt(ws_->base, ws_->cap);
+    // persistent per-layer state
+    arena_.reserve(4 * 256 + 4 * (size_t)N * 2 + 64);
     mean_probs_ = arena_.take<float>(N);
-    wgrad_ = arena_.take<float>(tmax_ * K);
-    dlogits_ = arena_.take<float>(smax_ * N);
-    dw_part_ = arena_.take<float>((int64_t)kRouterDwMaxSplits * H * N);
-    topi_ = arena_.take<int32_t>(smax_ * K);
-    fi_ = arena_.take<int32_t>(tmax_ * K);
     sel_ = arena_.take<int32_t>(N);
-    whist_ = arena_.take<int32_t>(nch * nr);
-    wbase_ = arena_.take<int32_t>(nch * nr);
-    expert_counts_ = arena_.take<int32_t>(tmax_);
-    cec_ = arena_.take<int32_t>(tmax_ + 1);
-    partial_counts_ = arena_.take<int32_t>(nr * thmax_);
-    partial_cum_ = arena_.take<int32_t>(nr * thmax_ + 1);
-    token_counts_ = arena_.take<int32_t>(nr);
-    ctc_ = arena_.take<int32_t>(nr + 1);
-    pad_start_ = arena_.take<int32_t>(nr + 1);
-    input_indices_ = arena_.take<int32_t>(tmax_ * K);
-    output_indices_ = arena_.take<int32_t>(tmax_ * K);
-    selected_k_ = arena_.take<int32_t>(tmax_ * K);
-    slot_prow_ = arena_.take<int32_t>(tmax_ * K);
-    prow_src_ = arena_.take<int32_t>(pmax_);
     err_ = arena_.take<int32_t>(1);
-    mlp_in_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
-    g_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
-    u_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
-    h_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
-    y_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
-    dy_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
-    dh_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
-    dgu_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * 2 * I, 1));
-    dxp_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
-    dl_bf16_ = arena_.take_bytes(2 * (size_t)std::max<int64_t>(smax_ * N, 1));
+    bar_ = arena_.take<int32_t>(8);
+    Arena& w = ws_arena_;
+    logits_ = w.take<float>(smax_ * N);
+    probs_ = w.take<float>(smax_ * N);
+    topw_ = w.take<float>(smax_ * K);
+    fw_ = w.take<float>(tmax_ * K);
+    colsum_ = w.take<float>((ceil_div(smax_, 128) + 1) * N);
+    wgrad_ = w.take<float>(tmax_ * K);
+    dlogits_ = w.take<float>(smax_ * N);
+    dw_part_ = w.take<float>((int64_t)kRouterDwMaxSplits * H * N);
+    topi_ = w.take<int32_t>(smax_ * K);
+    fi_ = w.take<int32_t>(tmax_ * K);
+    whist_ = w.take<int32_t>(nch * nr);
+    wbase_ = w.take<int32_t>(nch * nr);
+    expert_counts_ = w.take<int32_t>(tmax_);
+    cec_ = w.take<int32_t>(tmax_ + 1);
+    partial_counts_ = w.take<int32_t>(nr * thmax_);
+    partial_cum_ = w.take<int32_t>(nr * thmax_ + 1);
+    token_counts_ = w.take<int32_t>(nr);
+    ctc_ = w.take<int32_t>(nr + 1);
+    pad_start_ = w.take<int32_t>(nr + 1);
+    input_indices_ = w.take<int32_t>(tmax_ * K);
+    output_indices_ = w.take<int32_t>(tmax_ * K);
+    selected_k_ = w.take<int32_t>(tmax_ * K);
+    slot_prow_ = w.take<int32_t>(tmax_ * K);
+    prow_src_ = w.take<int32_t>(pmax_);
+    mlp_in_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
+    g_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
+    u_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
+    h_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
+    y_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
+    dy_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
+    dh_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
+    dgu_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * 2 * I, 1));
+    dxp_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
+    dl_bf16_ = w.take_bytes(2 * (size_t)std::max<int64_t>(smax_ * N, 1));
+    replay_out_ = w.take_bytes(es * (size_t)std::max<int64_t>(smax_ * H, 1));
     if (E > 1) {
         check(ctx_.comm != nullptr && ctx_.comm->ep.size == E, "fast_moe: EP > 1 needs the EP communicator");
-        gi_all_ = arena_.take<int32_t>(tmax_ * K);
-        gw_all_ = arena_.take<float>(tmax_ * K);
-        wgrad_local_ = arena_.take<float>(smax_ * K);
-        bar_ = arena_.take<int32_t>(8);
-        dx_exp_ = arena_.take_bytes(es * (size_t)std::max<int64_t>(smax_ * H, 1));
+        gi_all_ = w.take<int32_t>(tmax_ * K);
+        gw_all_ = w.take<float>(tmax_ * K);
+        wgrad_local_ = w.take<float>(smax_ * K);
+        dx_exp_ = w.take_bytes(es * (size_t)std::max<int64_t>(smax_ * H, 1));
         ep_setup();
     }
     B2_CUDA(cudaMemsetAsync(err_, 0, 4, ctx_.stream));
@@ -516,6 +542,18 @@ void MoeLayer::backward(const void* router, const void* gate, const void* up, co
                 {router, gate, up, down, dout, aux_probs_grad, dx, drouter, dgate, dup, ddown, x_,
                  (const void*)(intptr_t)s_, (const void*)(intptr_t)fur_},
                 [&] {
+                    if (checkpoint_) {
+                        // moe_block_backward with ckpt (blocks.cpp:361-367): replay the forward,
+                        // its EP collectives included, from the held input; deterministic
+                        // kernels make the replayed state bitwise equal to the original
+                        if (dtype_ == F32)
+                            forward_t<float>((const float*)x_, (const float*)router, (const float*)gate,
+                                             (const float*)up, (const float*)down, fur_, (float*)replay_out_);
+                        else
+                            forward_t<__nv_bfloat16>((const __nv_bfloat16*)x_, (const __nv_bfloat16*)router,
+                                                     (const __nv_bfloat16*)gate, (const __nv_bfloat16*)up,
+                                                     (const __nv_bfloat16*)down, fur_, (__nv_bfloat16*)replay_out_);
+                    }
                     if (dtype_ == F32)
                         backward_t<float>((const float*)router, (const float*)gate, (const float*)up,
                                           (const float*)down, (const float*)dout, aux_probs_grad, (float*)dx,
@@ -744,6 +782,12 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         launches_ += 4;
     }
     mark(kRouterBwd, true);
+}
+
+size_t MoeLayer::held_bytes() const {
+    const size_t persistent = arena_.used();
+    return checkpoint_ ? persistent + (size_t)s_ * (size_t)cfg_.hidden * dtype_size(dtype_)  // + the input
+                       : persistent + ws_arena_.used();
 }
 
 void MoeLayer::aux_probs_grad(double coeff, float* out) {

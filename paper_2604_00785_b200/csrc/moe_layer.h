@@ -34,7 +34,8 @@ struct Context {
     Comm* comm = nullptr;
 };
 
-// Bump allocator over one device allocation (workspace lives as long as the layer).
+// Bump allocator over one device allocation (workspace lives as long as the layer), or
+// over borrowed memory (adopt: a workspace shared by several layers).
 class Arena {
   public:
     Arena() = default;
@@ -42,6 +43,7 @@ class Arena {
     Arena(const Arena&) = delete;
     Arena& operator=(const Arena&) = delete;
     void reserve(size_t bytes);
+    void adopt(char* base, size_t cap);  // not owned: the caller keeps it alive
     template <typename T>
     T* take(int64_t n) {
         return static_cast<T*>(take_bytes((size_t)std::max<int64_t>(n, 1) * sizeof(T)));
@@ -52,12 +54,26 @@ class Arena {
   private:
     char* base_ = nullptr;
     size_t cap_ = 0, off_ = 0;
+    bool owned_ = true;
+};
+
+// Device memory of the per-step activations of a layer; layers may share one (activation
+// checkpointing: each backward replays its forward into the shared workspace).
+struct Workspace {
+    char* base = nullptr;
+    size_t cap = 0;
+    ~Workspace();
 };
 
 // FastMoeState (moe.hpp:302-316) plus the device workspace of one MoE layer on one rank.
 class MoeLayer {
   public:
-    MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_tokens);
+    // share_ws: reuse that layer's activation workspace (it must be large enough);
+    // checkpoint: moe_block_forward's `ckpt` (blocks.cpp:339-377) — after forward only the
+    // input pointer and the balancing statistics are held, and backward replays the forward
+    // (its EP collectives included) before differentiating, bitwise like the reference.
+    MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_tokens, const MoeLayer* share_ws = nullptr,
+             bool checkpoint = false);
     ~MoeLayer();
 
     // fast_moe_forward (moe.hpp:344-390). All pointers are device pointers of `dtype`.
@@ -85,7 +101,11 @@ class MoeLayer {
     int dtype() const { return dtype_; }
     int64_t pmax() const { return pmax_; }
     int64_t tokens() const { return s_; }
-    size_t workspace_bytes() const { return arena_.used(); }
+    size_t workspace_bytes() const { return ws_arena_.used() + arena_.used(); }
+    // bytes this layer holds between forward and backward (the reference's MoeRec::held):
+    // the persistent state, plus the workspace unless the layer checkpoints
+    size_t held_bytes() const;
+    bool checkpointing() const { return checkpoint_; }
     // number of kernels of this library launched by the last forward / backward
     int last_launches() const { return launches_; }
 
@@ -146,7 +166,11 @@ class MoeLayer {
     bool fur_ = false, have_fwd_ = false;
     const void* x_ = nullptr;  // the caller's input, kept for the router weight-gradient
     int launches_ = 0;
-    Arena arena_;
+    Arena arena_;     // persistent per-layer state (balancing statistics, flags)
+    Arena ws_arena_;  // activations, routing artifacts, scratch: in ws_ (maybe shared)
+    std::shared_ptr<Workspace> ws_;
+    bool checkpoint_ = false;
+    void* replay_out_ = nullptr;  // forward output of the checkpoint replay (discarded)
     // fp32
     float *logits_, *probs_, *topw_, *fw_, *colsum_, *mean_probs_, *wgrad_, *dlogits_, *dw_part_;
     // int32

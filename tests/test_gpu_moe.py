@@ -381,3 +381,61 @@ def test_host_pipeline_matches_synchronous(b2ctx):
     pipe_layer.host_wait()
     for (o, d), (wo, wd) in zip(outs, want):
         assert torch.equal(o, wo) and torch.equal(d, wd)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_checkpoint_replay_bitwise_and_lighter(b2ctx, dtype):
+    """moe_block_forward/backward with ckpt (blocks.cpp:339-377; test_model.cpp:680-720):
+    the replayed backward gives bitwise the same output, aux loss and gradients, and the
+    layer holds fewer bytes between forward and backward."""
+    b2, ctx = b2ctx
+    dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    cfg = b2.MoeConfig(n_experts=8, top_k=2, hidden=256, intermediate=128)
+    S = 200
+    gen = torch.Generator(device="cuda").manual_seed(33)
+    mk = lambda shape, std: (torch.randn(shape, device="cuda", generator=gen) * std).to(dt)
+    x, dout = mk((S, 256), 0.5), mk((S, 256), 0.3)
+    router, gate, up, down = mk((256, 8), 0.1), mk((8, 256, 128), 0.1), mk((8, 256, 128), 0.1), mk((8, 128, 256), 0.1)
+    res, held = [], []
+    for ckpt in (False, True):
+        layer = b2.MoeLayer(ctx, cfg, dt, S, checkpoint=ckpt)
+        out = layer.forward(x, router, gate, up, down)
+        aux = layer.aux_loss()
+        held.append(layer.held_bytes())
+        g = layer.backward(router, gate, up, down, dout, layer.aux_probs_grad(0.01))
+        torch.cuda.synchronize()
+        res.append(([out] + [g[k] for k in ("input", "router", "gate", "up", "down")], aux))
+    (a, aux_a), (b, aux_b) = res
+    for u, v in zip(a, b):
+        assert torch.equal(u, v)
+    assert aux_a == aux_b
+    assert held[1] < held[0]
+
+
+def test_shared_workspace_layers_match_private(b2ctx):
+    """Two checkpointed layers on ONE activation workspace (forward 1, forward 2, backward 2,
+    backward 1 — the order a model runs them) give the results of two private layers."""
+    b2, ctx = b2ctx
+    cfg = b2.MoeConfig(n_experts=16, top_k=4, hidden=256, intermediate=128)
+    S = 300
+    gen = torch.Generator(device="cuda").manual_seed(34)
+    mk = lambda shape, std: (torch.randn(shape, device="cuda", generator=gen) * std).bfloat16()
+    ws = [dict(router=mk((256, 16), 0.05), gate=mk((16, 256, 128), 0.05), up=mk((16, 256, 128), 0.05),
+               down=mk((16, 128, 256), 0.05)) for _ in range(2)]
+    x1, d2 = mk((S, 256), 1.0), mk((S, 256), 1.0)
+
+    def run(l1, l2):
+        w1, w2 = ws
+        y1 = l1.forward(x1, w1["router"], w1["gate"], w1["up"], w1["down"])
+        y2 = l2.forward(y1, w2["router"], w2["gate"], w2["up"], w2["down"])
+        g2 = l2.backward(w2["router"], w2["gate"], w2["up"], w2["down"], d2)
+        g1 = l1.backward(w1["router"], w1["gate"], w1["up"], w1["down"], g2["input"])
+        torch.cuda.synchronize()
+        return [y1, y2] + [g[k] for g in (g1, g2) for k in ("input", "router", "gate", "up", "down")]
+
+    want = run(b2.MoeLayer(ctx, cfg, torch.bfloat16, S), b2.MoeLayer(ctx, cfg, torch.bfloat16, S))
+    a = b2.MoeLayer(ctx, cfg, torch.bfloat16, S, checkpoint=True)
+    b = b2.MoeLayer(ctx, cfg, torch.bfloat16, S, share_workspace=a, checkpoint=True)
+    got = run(a, b)
+    for u, v in zip(got, want):
+        assert torch.equal(u, v)
