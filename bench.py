@@ -118,7 +118,9 @@ def cpu_info():
 
 
 def ref_ep_threads():
-    n = min(8, os.cpu_count() or 1)
+    """the reference runs one thread per EP rank (comm.cpp:90-94): use as many host cores as
+    a power-of-two EP width dividing the 64 experts allows"""
+    n = min(64, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1))
     ep = 1
     while ep * 2 <= n:
         ep *= 2
