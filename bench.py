@@ -230,12 +230,21 @@ def bench_adamw(torch, b2, ctx, dev, steps, warmup, world, rank, hbm_peak):
         import torch.distributed as dist
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "r01_ncu_adamw_traffic.json")
+    if os.path.exists(tf):  # DRAM bytes per element of the capture (0.5 G elements), scaled to this step
+        with open(tf) as f:
+            k = json.load(f)["kernels"]
+        per_elem = sum(v["dram_bytes"] for v in k.values()) / 0.5e9
+        traffic = per_elem * owned
     return {"metric": "sharded AdamW step ms (EPSO, Mula-7B-A1B param set, bf16 grads/weights, fp32 state)",
             "parallelism": f"dp1 x ep{world}", "scaling": "strong",
             "ms": ms, "params": total, "owned_params_per_rank": owned, "launches_per_step": launches,
             "grad_norm": st["grad_norm"],
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
-                         "traffic": None, "algorithmic_bytes_per_step": byt}}
+                         "traffic": traffic, "traffic_source": "profiles/r01_ncu_adamw_traffic.json (sumsq + update, "
+                                                               "per element x owned elements)",
+                         "algorithmic_bytes_per_step": byt}}
 
 
 def zipf_tokens(torch, dev, S, Hd, N, s, seed):

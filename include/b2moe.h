@@ -176,6 +176,12 @@ int64_t b2_opt_state_bytes(b2_opt* o);
 int b2_opt_owned(b2_opt* o, int p, int64_t* begin, int64_t* end);
 /* host copies of the fp32 master / exp_avg / exp_avg_sq of param p's owned slice */
 int b2_opt_get_state(b2_opt* o, int p, float* master, float* exp_avg, float* exp_avg_sq);
+/* checkpoint assembly (reliability.cpp:411-440): the FULL fp32 master / exp_avg /
+ * exp_avg_sq of param p (numel floats each, host; NULL skips one), all-gathered over the
+ * param's owning group with the shard_slice bounds — collective on that group */
+int b2_opt_gather_state(b2_opt* o, int p, float* master, float* exp_avg, float* exp_avg_sq);
+/* restore (reliability.cpp:658-667): copy this rank's owned slice out of full host tensors */
+int b2_opt_load_state(b2_opt* o, int p, const float* master, const float* exp_avg, const float* exp_avg_sq);
 int b2_opt_set_step_count(b2_opt* o, int64_t n);
 /* detect_soft_failure (reliability.cpp:706-723, called at train.cpp:193): NaN/Inf in
  * `loss` or in this rank's LOCAL gradients -> max over WORLD of (node + 1); *sick =

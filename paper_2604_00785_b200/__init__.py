@@ -101,6 +101,8 @@ SIGNATURES = {
     "b2_opt_state_bytes": (C.c_int64, [P]),
     "b2_opt_owned": (C.c_int, [P, C.c_int, P, P]),
     "b2_opt_get_state": (C.c_int, [P, C.c_int, P, P, P]),
+    "b2_opt_gather_state": (C.c_int, [P, C.c_int, P, P, P]),
+    "b2_opt_load_state": (C.c_int, [P, C.c_int, P, P, P]),
     "b2_opt_set_step_count": (C.c_int, [P, I64]),
     "b2_adamw_update": (C.c_int, [P, P, P, P, P, C.c_int, I64, C.c_double, I64, P, P, C.c_int, C.c_int]),
     "b2_lr_at_step": (C.c_double, [I64, P]),
@@ -473,6 +475,19 @@ class ShardedOptimizer:
         ms, m, v = (np.zeros(n, np.float32) for _ in range(3))
         _check(lib().b2_opt_get_state(self.h, p, ms.ctypes.data_as(P), m.ctypes.data_as(P), v.ctypes.data_as(P)))
         return ms, m, v
+
+    def gather_state(self, p: int, numel: int):
+        """full (master, exp_avg, exp_avg_sq) of param p over its owning group (collective)."""
+        import numpy as np
+        ms, m, v = (np.zeros(numel, np.float32) for _ in range(3))
+        _check(lib().b2_opt_gather_state(self.h, p, ms.ctypes.data_as(P), m.ctypes.data_as(P), v.ctypes.data_as(P)))
+        return ms, m, v
+
+    def load_state(self, p: int, master, exp_avg, exp_avg_sq):
+        """restore this rank's owned slice of param p from full fp32 host arrays."""
+        import numpy as np
+        arrs = [np.ascontiguousarray(a, np.float32) for a in (master, exp_avg, exp_avg_sq)]
+        _check(lib().b2_opt_load_state(self.h, p, *[a.ctypes.data_as(P) for a in arrs]))
 
     def set_step_count(self, n: int):
         _check(lib().b2_opt_set_step_count(self.h, n))

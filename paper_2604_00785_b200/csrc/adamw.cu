@@ -6,6 +6,8 @@
 // with explicit _rn intrinsics so nvcc cannot contract it into FMAs: given the same
 // inputs the master, moments and the bf16 weight are bitwise identical to the CPU.
 // HBM traffic per element: grad 2-4 B + master/m/v 12 B in + 12 B out + weight 2-4 B.
+#include <cstdlib>
+
 #include "b2_common.cuh"
 #include "kernels.h"
 
@@ -316,7 +318,10 @@ __global__ void __launch_bounds__(1024) norm_final_kernel(const double* __restri
     if (threadIdx.x == 0) *out = tot;
 }
 
-__global__ void __launch_bounds__(256) adamw_chunks_kernel(const OptSeg* __restrict__ segs,
+// 256 threads x 4 blocks per SM: the fp64 divide / sqrt chains are long, so occupancy (not the
+// FP64 pipe, ~28 % busy at 3 blocks) is what keeps enough bytes in flight
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) adamw_chunks_kernel(const OptSeg* __restrict__ segs,
                                                            const OptChunk* __restrict__ chunks,
                                                            const int32_t* __restrict__ ids, int nids, AdamWDev c,
                                                            OptStepArgs a, const double* __restrict__ norm_sq,
@@ -337,25 +342,9 @@ __global__ void __launch_bounds__(256) adamw_chunks_kernel(const OptSeg* __restr
             const uint2* gr = reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(sg.grad) + ch.begin);
             uint2* wo = reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(sg.wout) + ch.begin);
             const int64_t n4 = ch.len / 4;
-            int64_t i = threadIdx.x;
-            for (; i + (int64_t)blockDim.x < n4; i += 2 * (int64_t)blockDim.x) {
-                const int64_t j = i + blockDim.x;
-                const uint2 g0 = __ldcs(gr + i), g1 = __ldcs(gr + j);
-                float4 m0 = __ldcs(ms + i), a0 = __ldcs(mo + i), v0 = __ldcs(ve + i);
-                float4 m1 = __ldcs(ms + j), a1 = __ldcs(mo + j), v1 = __ldcs(ve + j);
-                uint2 w0, w1;
-                adamw_group4(m0, a0, v0, g0, c, sg.scale, clip, w0);
-                adamw_group4(m1, a1, v1, g1, c, sg.scale, clip, w1);
-                __stcs(ms + i, m0);
-                __stcs(mo + i, a0);
-                __stcs(ve + i, v0);
-                __stcs(wo + i, w0);
-                __stcs(ms + j, m1);
-                __stcs(mo + j, a1);
-                __stcs(ve + j, v1);
-                __stcs(wo + j, w1);
-            }
-            if (i < n4) {
+            // one group of 4 per thread-iteration: occupancy (not per-thread ILP) hides the
+            // fp64 divide/sqrt latency without spilling
+            for (int64_t i = threadIdx.x; i < n4; i += blockDim.x) {
                 const uint2 g0 = __ldcs(gr + i);
                 float4 m0 = __ldcs(ms + i), a0 = __ldcs(mo + i), v0 = __ldcs(ve + i);
                 uint2 w0;
@@ -419,11 +408,20 @@ void launch_adamw_chunks(const OptSeg* segs, const OptChunk* chunks, const int32
     c.lr_wd = a.lr * a.weight_decay;
     c.bc1 = a.bc1;
     c.bc2 = a.bc2;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = std::min(nids, sms * 8);
-    adamw_chunks_kernel<<<grid, 256, 0, st>>>(segs, chunks, ids, nids, c, a, norm_sq, nonfinite);
+    static int minb = 0, grid_cap = 0;  // resident blocks on the whole GPU (persistent grid)
+    if (grid_cap == 0) {
+        const char* env = getenv("B2_ADAMW_MINB");  // A/B hook: 3 (no spills) or 4 (more warps)
+        minb = env && atoi(env) == 3 ? 3 : 4;
+        int dev = 0, sms = 148, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (minb == 3) B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adamw_chunks_kernel<3>, 256, 0));
+        else B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adamw_chunks_kernel<4>, 256, 0));
+        grid_cap = sms * std::max(1, per_sm);
+    }
+    const int grid = std::min(nids, grid_cap);
+    if (minb == 3) adamw_chunks_kernel<3><<<grid, 256, 0, st>>>(segs, chunks, ids, nids, c, a, norm_sq, nonfinite);
+    else adamw_chunks_kernel<4><<<grid, 256, 0, st>>>(segs, chunks, ids, nids, c, a, norm_sq, nonfinite);
     B2_LAUNCH_CHECK();
 }
 

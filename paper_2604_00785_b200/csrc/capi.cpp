@@ -496,6 +496,14 @@ int b2_opt_owned(b2_opt* o, int p, int64_t* begin, int64_t* end) {
     return guard([&] { o->opt->owned(p, begin, end); });
 }
 
+int b2_opt_gather_state(b2_opt* o, int p, float* master, float* exp_avg, float* exp_avg_sq) {
+    return guard([&] { o->opt->gather_state(p, master, exp_avg, exp_avg_sq); });
+}
+
+int b2_opt_load_state(b2_opt* o, int p, const float* master, const float* exp_avg, const float* exp_avg_sq) {
+    return guard([&] { o->opt->load_state(p, master, exp_avg, exp_avg_sq); });
+}
+
 int b2_opt_get_state(b2_opt* o, int p, float* master, float* exp_avg, float* exp_avg_sq) {
     return guard([&] { o->opt->get_state(p, master, exp_avg, exp_avg_sq); });
 }

@@ -358,4 +358,43 @@ void ShardedOptimizer::get_state(int p, float* master, float* m, float* v) {
     B2_CUDA(cudaStreamSynchronize(ctx_.stream));
 }
 
+void ShardedOptimizer::gather_state(int p, float* master, float* m, float* v) {
+    check(p >= 0 && p < (int)plan_.size(), "optimizer: parameter index out of range");
+    B2_CUDA(cudaSetDevice(ctx_.device));
+    const Entry& e = plan_[(size_t)p];
+    const int64_t numel = params_[(size_t)p].numel, n = e.own_e - e.own_b;
+    const int gsize = mode_ == ShardMode::ddp ? 1 : (e.over_dp_ep ? ctx_.dp * ctx_.ep : ctx_.dp);
+    if (gsize <= 1) {  // the owned slice is the whole tensor
+        get_state(p, master, m, v);
+        return;
+    }
+    // replicas hold disjoint shard_slice pieces: an in-place all-gather with the same bounds
+    // reproduces every value bitwise (the reference uses a zero-filled allreduce)
+    float* full = nullptr;
+    B2_CUDA(cudaMallocAsync((void**)&full, 4 * (size_t)std::max<int64_t>(numel, 1), ctx_.stream));
+    float* dst[3] = {master, m, v};
+    const float* src[3] = {e.master, e.m, e.v};
+    for (int q = 0; q < 3; ++q) {
+        if (!dst[q]) continue;
+        if (n > 0)
+            B2_CUDA(cudaMemcpyAsync(full + e.own_b, src[q], 4 * (size_t)n, cudaMemcpyDeviceToDevice, ctx_.stream));
+        all_gather_v(*group_of(e), full, numel, F32, ctx_.stream);
+        B2_CUDA(cudaMemcpyAsync(dst[q], full, 4 * (size_t)numel, cudaMemcpyDeviceToHost, ctx_.stream));
+    }
+    B2_CUDA(cudaFreeAsync(full, ctx_.stream));
+    B2_CUDA(cudaStreamSynchronize(ctx_.stream));
+}
+
+void ShardedOptimizer::load_state(int p, const float* master, const float* m, const float* v) {
+    check(p >= 0 && p < (int)plan_.size(), "optimizer: parameter index out of range");
+    B2_CUDA(cudaSetDevice(ctx_.device));
+    const Entry& e = plan_[(size_t)p];
+    const size_t n = (size_t)(e.own_e - e.own_b);
+    if (n == 0) return;
+    if (master) B2_CUDA(cudaMemcpyAsync(e.master, master + e.own_b, 4 * n, cudaMemcpyHostToDevice, ctx_.stream));
+    if (m) B2_CUDA(cudaMemcpyAsync(e.m, m + e.own_b, 4 * n, cudaMemcpyHostToDevice, ctx_.stream));
+    if (v) B2_CUDA(cudaMemcpyAsync(e.v, v + e.own_b, 4 * n, cudaMemcpyHostToDevice, ctx_.stream));
+    B2_CUDA(cudaStreamSynchronize(ctx_.stream));
+}
+
 }  // namespace b2

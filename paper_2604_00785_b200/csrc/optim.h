@@ -48,6 +48,11 @@ class ShardedOptimizer {
     int64_t state_bytes() const;
     void owned(int p, int64_t* b, int64_t* e) const;
     void get_state(int p, float* master, float* m, float* v);
+    // checkpoint assembly (reliability.cpp:411-440): the FULL master / exp_avg / exp_avg_sq of
+    // param p, gathered over its owning group (collective on that group; host buffers of numel)
+    void gather_state(int p, float* master, float* m, float* v);
+    // restore (reliability.cpp:658-667): this rank's owned slice from full host tensors
+    void load_state(int p, const float* master, const float* m, const float* v);
     void set_step_count(int64_t n) { step_count_ = n; }
     int last_launches() const { return launches_; }
     // detect_soft_failure (reliability.cpp:706-723): scans this rank's LOCAL grads (and

@@ -60,7 +60,11 @@ def run(rank, world, port, dp, ep, mode, result_path):
         st = opt.step(stats=True)
         stats.append([st["lr"], st["grad_norm"], st["clip_scale"]])
     torch.cuda.synchronize()
+    # checkpoint assembly: every member's full state must equal the members' owned slices
+    # stitched together (each rank checks its own view against the oracle's per-rank slices)
+    full = [opt.gather_state(p, n) for p, n in enumerate(NUMEL)]
     mine = {"w": W.cpu().numpy().tolist(), "stats": stats, "sb": opt.state_bytes(),
+            "full_master": [f[0].tolist() for f in full], "owned": [list(opt.owned(p)) for p in range(len(NUMEL))],
             "master": [opt.state(p)[0].tolist() for p in range(len(NUMEL))],
             "m": [opt.state(p)[1].tolist() for p in range(len(NUMEL))],
             "v": [opt.state(p)[2].tolist() for p in range(len(NUMEL))]}
@@ -88,6 +92,25 @@ def run(rank, world, port, dp, ep, mode, result_path):
                                        float(np.max(np.abs(np.asarray(g["stats"]) - ref["stats"][:, r, :]))))
             if g["sb"] != int(ref["state_bytes"][r]):
                 res["state_bytes_equal"] = False
+        # gathered full masters: rank r's full view of param p must hold, on every slice owned
+        # by a member q of r's owning group, exactly q's owned master
+        res["gather_ok"] = True
+        for p in range(len(NUMEL)):
+            for r in range(world):
+                got = np.asarray(gathered[r]["full_master"][p], np.float32)
+                for q in range(world):
+                    same_ep = (r % ep) == (q % ep)
+                    if mode == 0:
+                        members = q == r
+                    elif mode == 2 and CLS[p] == 0:
+                        members = True  # EPSO non-expert: the fused DP x EP group
+                    else:
+                        members = same_ep  # expert params, and SO: the EP-orthogonal DP group
+                    if not members:
+                        continue
+                    b_, e_ = gathered[q]["owned"][p]
+                    if not np.array_equal(got[b_:e_], np.asarray(gathered[q]["master"][p], np.float32)):
+                        res["gather_ok"] = False
         with open(result_path, "w") as f:
             json.dump(res, f)
     dist.barrier()

@@ -98,3 +98,41 @@ def test_nonfinite_grad_skips_update_and_is_detected(b2ctx, orc):
     G.copy_(torch.from_numpy(grads[1]).cuda().bfloat16())
     st = opt.step(stats=True)
     assert not st["nonfinite"] and not torch.equal(W, before)
+
+
+def test_state_checkpoint_restore_continues_bitwise(b2ctx, orc):
+    """gather_state / load_state (reliability.cpp:411-440, 658-667): a fresh optimizer
+    restored from the assembled state (+ the step count) continues exactly like the
+    original."""
+    b2, ctx = b2ctx
+    w0, grads = make(orc, torch.bfloat16, 6, seed=8)
+    cfg = b2.AdamWConfig(warmup_steps=2, total_steps=50, peak_lr=1e-2, min_lr=1e-3)
+
+    def build(w):
+        W = torch.from_numpy(w).cuda().bfloat16()
+        G = torch.zeros(W.numel(), dtype=torch.bfloat16, device="cuda")
+        params, off = [], 0
+        for n, c in zip(NUMEL, CLS):
+            params.append((W[off:off + n], G[off:off + n], c, 0))
+            off += n
+        return W, G, b2.ShardedOptimizer(ctx, cfg, params, b2.EPSO)
+
+    W, G, opt = build(w0)
+    for s in range(3):
+        G.copy_(torch.from_numpy(grads[s]).bfloat16())
+        opt.step(stats=False)
+    torch.cuda.synchronize()
+    saved = [opt.gather_state(p, n) for p, n in enumerate(NUMEL)]
+    W2, G2, opt2 = build(W.float().cpu().numpy())
+    for p, st in enumerate(saved):
+        opt2.load_state(p, *st)
+    opt2.set_step_count(3)
+    for s in range(3, 6):
+        for G_, o in ((G, opt), (G2, opt2)):
+            G_.copy_(torch.from_numpy(grads[s]).bfloat16())
+            o.step(stats=False)
+    torch.cuda.synchronize()
+    assert torch.equal(W, W2)
+    for p, n in enumerate(NUMEL):
+        for a, b in zip(opt.gather_state(p, n), opt2.gather_state(p, n)):
+            assert np.array_equal(a, b)
