@@ -91,6 +91,26 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def bind_numa_local(torch, gpu: int):
+    """Pin this rank's process to the CPUs closest to its GPU (NVML affinity, matched by PCI
+    bus id), so the pinned host buffers of the e2e leg are allocated on the GPU's own NUMA node."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        p = torch.cuda.get_device_properties(gpu)
+        bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, 16)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1}
+        cpus &= set(os.sched_getaffinity(0))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return len(cpus)
+    except Exception as e:  # reported, never fatal
+        return f"unbound: {type(e).__name__}"
+    return "unbound"
+
+
 def ncu_traffic():
     """DRAM bytes (read + write) per step of the six expert-GEMM launches, from the committed
     `ncu --set full` capture (tools/ncu_summary.py -> profiles/*_ncu_traffic.json)."""
@@ -346,6 +366,8 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    all_cpus = set(os.sched_getaffinity(0))
+    numa = bind_numa_local(torch, local)  # host buffers (pinned, first touch) on the GPU's own socket
     # one non-default stream per rank for everything (the layer captures its forward and
     # backward into CUDA graphs on it; the legacy default stream cannot be captured)
     stream = torch.cuda.Stream(device=dev)
@@ -466,6 +488,7 @@ def main():
         adamw = bench_adamw(torch, b2, ctx, dev, 5, 2, world, rank, hbm_peak)
 
     cpu = None
+    os.sched_setaffinity(0, all_cpus)  # the CPU reference leg may use every host core
     if rank == 0 and not args.no_cpu:
         try:
             ep = ref_ep_threads()
@@ -485,7 +508,8 @@ def main():
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded randn tokens, random-init weights)",
             "config": {"workload": WORKLOAD, "global_batch_tokens": world * S,
                        "parallelism": f"ep{world} (all-to-all dispatch/combine over NCCL)" if world > 1 else "ep1",
-                       "l2": "working set (weights 0.8 GB + activations ~4 GB) >> 126 MB L2; no flush needed"},
+                       "l2": "working set (weights 0.8 GB + activations ~4 GB) >> 126 MB L2; no flush needed",
+                       "host_cpus_bound": numa},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
                          "frac": achieved / bf16_peak, "traffic": traffic, "traffic_source": traffic_src,
                          "traffic_unit": "DRAM bytes per step (6 expert-GEMM launches, ncu --set full)",
