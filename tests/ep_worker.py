@@ -39,9 +39,13 @@ def run(rank, world, port, case, result_path):
     torch.cuda.set_device(rank)
     ids = [b2.Context.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(ids, src=0)
-    ctx = b2.Context(rank, rank=rank, dp=1, ep=world, nccl_id=ids[0])
-
     c = dict(case)
+    ckpt, graph = c.pop("ckpt", False), c.pop("graph", False)
+    stream = torch.cuda.Stream() if graph else None  # graph capture needs a non-default stream
+    if stream is not None:
+        torch.cuda.set_stream(stream)
+    ctx = b2.Context(rank, rank=rank, dp=1, ep=world, nccl_id=ids[0], stream=stream)
+
     s = c.pop("s")
     dtype = torch.float32 if c.pop("dtype") == "f32" else torch.bfloat16
     fur = c.pop("fur", False)
@@ -63,10 +67,17 @@ def run(rank, world, port, case, result_path):
     el = slice(rank * NR, (rank + 1) * NR)
     X, DO = tt(x[sl]), tt(dout[sl])
     R, G, U, D = tt(router), tt(gate[el]), tt(up[el]), tt(down[el])
-    layer = b2.MoeLayer(ctx, bcfg, dtype, s)
-    out = layer.forward(X, R, G, U, D, fur=fur)
-    apg = layer.aux_probs_grad(0.01)
-    g = layer.backward(R, G, U, D, DO, apg)
+    layer = b2.MoeLayer(ctx, bcfg, dtype, s, checkpoint=ckpt)
+    reps = 3 if graph else 1  # eager, capture, replay: the last one is checked
+    if graph:
+        layer.set_graph(True)
+    out, apg = torch.empty_like(X), torch.empty((s, N), dtype=torch.float32, device=dev)
+    g = dict(input=torch.empty_like(X), router=torch.empty_like(R), gate=torch.empty_like(G), up=torch.empty_like(U),
+             down=torch.empty_like(D))
+    for _ in range(reps):
+        layer.forward(X, R, G, U, D, fur=fur, out=out)
+        layer.aux_probs_grad(0.01, out=apg)
+        layer.backward(R, G, U, D, DO, apg, grads=g)
     torch.cuda.synchronize()
     mine = {
         "out": out.float().cpu(), "dx": g["input"].float().cpu(), "drouter": g["router"].float().cpu(),
