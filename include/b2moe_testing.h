@@ -20,6 +20,10 @@ int b2x_grouped_gemm(b2_ctx* ctx, int kind, int hidden, int intermediate, int nr
 /* Opt the bf16 layer into (1) / out of (0) the GEMMs' TMA tile::gather4 X-operand loads
  * instead of the materialised mlp_in rows (A/B checks: both must agree bitwise). */
 int b2x_moe_set_tma_gather(b2_moe* m, int on);
+/* EP > 1, bf16: opt into (1) the GEMM-fused combine (FwdDown / BwdDx epilogues storing each
+ * row into the source rank's slab over NVLink) instead of (0, default) the owner-local
+ * combine + coalesced NVLink pull. */
+int b2x_moe_set_fused_combine(b2_moe* m, int on);
 #ifdef __cplusplus
 }
 #endif

@@ -325,6 +325,68 @@ __global__ void ep_pull_sum_kernel(const T* const* __restrict__ peer_slab, const
     }
 }
 
+// source side of the GEMM-fused combine: out[t] = sum_k slab[k][t] in k order (every (t, k)
+// row was stored by the owner's epilogue over NVLink before the barrier)
+template <typename T>
+__global__ void kslab_sum_kernel(const T* __restrict__ slab, int S, int K, int W, T* __restrict__ out) {
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+    if (t >= S) return;
+    constexpr int V = 16 / sizeof(T), MAXK = 8;
+    for (int v = lane; v < W / V; v += 32) {
+        float acc[V];
+#pragma unroll
+        for (int z = 0; z < V; ++z) acc[z] = 0.f;
+        for (int k0 = 0; k0 < K; k0 += MAXK) {
+            int4 raw[MAXK];
+#pragma unroll
+            for (int q = 0; q < MAXK; ++q)
+                if (k0 + q < K) raw[q] = __ldcv(reinterpret_cast<const int4*>(slab + ((int64_t)(k0 + q) * S + t) * W) + v);
+#pragma unroll
+            for (int q = 0; q < MAXK; ++q) {
+                if (k0 + q >= K) break;
+                float f[V];
+                if constexpr (sizeof(T) == 4) {
+                    f[0] = __int_as_float(raw[q].x);
+                    f[1] = __int_as_float(raw[q].y);
+                    f[2] = __int_as_float(raw[q].z);
+                    f[3] = __int_as_float(raw[q].w);
+                } else {
+                    const uint32_t w[4] = {(uint32_t)raw[q].x, (uint32_t)raw[q].y, (uint32_t)raw[q].z,
+                                           (uint32_t)raw[q].w};
+#pragma unroll
+                    for (int z = 0; z < 4; ++z) {
+                        f[2 * z] = __uint_as_float(w[z] << 16);
+                        f[2 * z + 1] = __uint_as_float(w[z] & 0xFFFF0000u);
+                    }
+                }
+#pragma unroll
+                for (int z = 0; z < V; ++z) acc[z] = __fadd_rn(acc[z], f[z]);
+            }
+        }
+        int4 o;
+        if constexpr (sizeof(T) == 4) {
+            o = make_int4(__float_as_int(acc[0]), __float_as_int(acc[1]), __float_as_int(acc[2]), __float_as_int(acc[3]));
+        } else {
+            uint32_t w[4];
+#pragma unroll
+            for (int z = 0; z < 4; ++z) {
+                __nv_bfloat162 b = __floats2bfloat162_rn(acc[2 * z], acc[2 * z + 1]);
+                w[z] = *reinterpret_cast<uint32_t*>(&b);
+            }
+            o = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
+        }
+        reinterpret_cast<int4*>(out + (int64_t)t * W)[v] = o;
+    }
+}
+
+template <typename T>
+void launch_kslab_sum(const T* slab, int S, int K, int W, T* out, cudaStream_t st) {
+    if (S <= 0) return;
+    check(((int64_t)W * sizeof(T)) % 16 == 0, "kslab sum: rows must be 16-byte multiples");
+    kslab_sum_kernel<T><<<(unsigned)ceil_div(S, 8), 256, 0, st>>>(slab, S, K, W, out);
+    B2_LAUNCH_CHECK();
+}
+
 static unsigned ep_grid(int64_t warps) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(148 * 16, ceil_div(warps, 8))); }
 
 template <typename T>
@@ -393,7 +455,8 @@ void launch_ep_return_sum(const T* slab, const int32_t* gi_local, int S, int K, 
     template void launch_ep_combine_local<T>(const T*, const int32_t*, const int32_t*, const int32_t*, const float*, \
                                              int, int, int, int, T*, cudaStream_t);                              \
     template void launch_ep_pull_sum<T>(const T* const*, const int32_t*, int, int, int, int, int, int, T*,        \
-                                        cudaStream_t);
+                                        cudaStream_t);                                                            \
+    template void launch_kslab_sum<T>(const T*, int, int, int, T*, cudaStream_t);
 B2_EP_INST(float)
 B2_EP_INST(__nv_bfloat16)
 #undef B2_EP_INST

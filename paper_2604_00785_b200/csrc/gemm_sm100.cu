@@ -106,6 +106,11 @@ struct Params {
     const int32_t* slot_prow;
     const __nv_bfloat16* src;
     float* part;
+    void* const* peer_kslab;     // FwdDown / BwdDx, EP > 1: fused combine into the sources' slabs
+    const int32_t* prow_src;
+    const int32_t* prow_k;
+    const float* gw;
+    int ep_S, ep_K;
     const int32_t* gather_rows;  // FwdGateUp / WgradGateUp: padded row -> token (gather4 mode)
     int gather_oob;              // the zero-filled row index used for pad rows (-1 entries)
 };
@@ -966,6 +971,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
             } else if constexpr (KIND == GemmKind::FwdDown || KIND == GemmKind::BwdDx) {
                 uint32_t r[32];
                 float v[32];
+                // EP > 1: fused combine (output_reduction_forward / the dX scatter-add, then the
+                // reducescatter, moe.hpp:250-268, 378, 418-428): this row's contribution goes
+                // straight into its source rank's [K][S][H] slab over NVLink, tile by tile
+                __nv_bfloat16* kdst = nullptr;
+                float wv = 1.f;
+                if (p.peer_kslab) {
+                    const int64_t prow = ti.m0 + row0 + lane;
+                    const int gid = p.prow_src[prow];
+                    if (gid >= 0) {
+                        const int kk = p.prow_k[prow];
+                        if constexpr (KIND == GemmKind::FwdDown) wv = p.gw[(int64_t)gid * p.ep_K + kk];
+                        kdst = static_cast<__nv_bfloat16*>(p.peer_kslab[gid / p.ep_S]) +
+                               ((int64_t)kk * p.ep_S + gid % p.ep_S) * p.H;
+                    }
+                }
+                const bool keep_local = KIND == GemmKind::FwdDown || !p.peer_kslab;  // y feeds the backward
 #pragma unroll 1
                 for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
                     tmem_ld32(tacc + c, r);
@@ -974,8 +995,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                     if (col >= p.H) continue;
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                    stg.put2d(&p.mapO0, lane, v, col, ti.m0 + row0);
+                    if (keep_local) stg.put2d(&p.mapO0, lane, v, col, ti.m0 + row0);
+                    if (kdst) {
+                        if constexpr (KIND == GemmKind::FwdDown) {  // w * (the stored bf16 y), as the combine
+#pragma unroll
+                            for (int j = 0; j < 32; j += 2) {
+                                const uint32_t yb = pack_bf16(v[j], v[j + 1]);
+                                v[j] = __fmul_rn(wv, bf16_lo(yb));
+                                v[j + 1] = __fmul_rn(wv, bf16_hi(yb));
+                            }
+                        }
+                        store_row32(kdst + col, v, 32);
+                    }
                 }
+                if (p.peer_kslab) __threadfence_system();
             } else if constexpr (KIND == GemmKind::WgradDown || KIND == GemmKind::WgradGateUp) {
                 // out[e][m][n] * scale through 3-D maps: rows past the expert's M are clipped
                 uint32_t r[32];
@@ -1132,6 +1165,16 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
     p.out2 = (__nv_bfloat16*)a.out2;
     p.gather_rows = a.gather_rows;
     p.gather_oob = a.gather_tokens;
+    p.peer_kslab = a.peer_kslab;
+    p.prow_src = a.prow_src;
+    p.prow_k = a.prow_k;
+    p.gw = a.gw;
+    p.ep_S = a.ep_S;
+    p.ep_K = a.ep_K;
+    if (a.peer_kslab)
+        check((a.kind == GemmKind::FwdDown || a.kind == GemmKind::BwdDx) && a.prow_src && a.prow_k && a.ep_S > 0 &&
+                  (a.kind != GemmKind::FwdDown || a.gw),
+              "fused combine: FwdDown / BwdDx with the row tables");
     if (a.gather_rows) check(a.gather_tokens >= 0 && a.pmax % 4 == 0, "gather4 operand: bad token count / row capacity");
     const int64_t P = a.pmax, H = a.H, I = a.I, nr = a.nr;
     int grid = a.num_sms > 0 ? a.num_sms : 148;

@@ -43,6 +43,7 @@ struct RoutingIndexArgs {
     int32_t* selected_k;         // [T*K]
     int32_t* slot_prow;          // [T*K] token-major slot -> padded row
     int32_t* prow_src;           // [pmax] padded row -> token (-1 pad)
+    int32_t* prow_k;             // [pmax] padded row -> top-k slot k (nullptr: not needed)
     int32_t* err;                // expert id out of range flag
 };
 void launch_routing_index(const RoutingIndexArgs& a, cudaStream_t st);
@@ -90,6 +91,11 @@ void launch_ep_combine_local(const T* y, const int32_t* slot_prow, const int32_t
 template <typename T>
 void launch_ep_pull_sum(const T* const* peer_slab, const int32_t* gi_local, int S, int K, int E, int NR, int W, int me,
                         T* out, cudaStream_t st);
+// out[t] = sum over k (in k order) of slab[k][t] — the source side of the GEMM-fused
+// combine: every (t, k) row was stored into this rank's [K][S][W] slab by its owner's
+// FwdDown / BwdDx epilogue over NVLink
+template <typename T>
+void launch_kslab_sum(const T* slab, int S, int K, int W, T* out, cudaStream_t st);
 void launch_ep_wgrad_push(const float* wgrad, const int32_t* cec, int K, int S, int T_tot, int me,
                           float* const* peer_wret, cudaStream_t st);
 template <typename T>
@@ -161,6 +167,14 @@ struct Sm100GemmArgs {
     // of reading a materialised mlp_in; null: `x` is mlp_in [P,H]
     const int32_t* gather_rows;
     int gather_tokens;           // S: rows of `x` (row S is the zero-filled out-of-bounds row)
+    // FwdDown / BwdDx at EP > 1: the GEMM-fused combine. The epilogue also stores each padded
+    // row's result (FwdDown: w * y; BwdDx: dX) straight into the source rank's [K][S][H] slab
+    // over NVLink (peer_kslab: device table of EP pointers); the source sums over k
+    void* const* peer_kslab;
+    const int32_t* prow_src;     // padded row -> gathered token id (-1 pad)
+    const int32_t* prow_k;       // padded row -> top-k slot
+    const float* gw;             // [T, K] gathered routing weights (FwdDown)
+    int ep_S, ep_K;              // tokens per rank, top-k
 };
 void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st);
 // number of S splits the RouterDw kind uses (its partial buffer holds splits*H*N floats)

@@ -83,7 +83,7 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
         acc(4 * (size_t)std::max<int64_t>(n, 1));
     // workspace: int32
     for (int64_t n : {smax_ * K, tmax_ * K, nch * nr, nch * nr, tmax_, tmax_ + 1, nr * thmax_, nr * thmax_ + 1, nr,
-                      nr + 1, nr + 1, tmax_ * K, tmax_ * K, tmax_ * K, tmax_ * K, pmax_})
+                      nr + 1, nr + 1, tmax_ * K, tmax_ * K, tmax_ * K, tmax_ * K, pmax_, pmax_})
         acc(4 * (size_t)std::max<int64_t>(n, 1));
     // workspace: dtype, padded rows (+ the replay output)
     for (int64_t n : {pmax_ * H, pmax_ * I, pmax_ * I, pmax_ * I, pmax_ * H, pmax_ * H, pmax_ * I, pmax_ * 2 * I,
@@ -137,6 +137,7 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     selected_k_ = w.take<int32_t>(tmax_ * K);
     slot_prow_ = w.take<int32_t>(tmax_ * K);
     prow_src_ = w.take<int32_t>(pmax_);
+    prow_k_ = w.take<int32_t>(pmax_);
     mlp_in_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
     g_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
     u_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
@@ -176,15 +177,16 @@ MoeLayer::~MoeLayer() {
     }
 }
 
-// symmetric buffer: [x_sh S*H | dout_sh S*H | ret_f E*S*H | ret_b E*S*H] (dtype) + wret [E*S*K] f32,
-// identical offsets on every rank; IPC handles are exchanged with an NCCL all-gather
+// symmetric buffer: [x_sh S*H | dout_sh S*H | ret_f E*S*H | ret_b E*S*H] (dtype) + wret [E*S*K] f32
+// + kslab [K*S*H] (dtype, the GEMM-fused combine's landing slab), identical offsets on every
+// rank; IPC handles are exchanged with an NCCL all-gather
 void MoeLayer::ep_setup() {
     const int E = cfg_.ep, me = ctx_.coord_ep;
     const size_t es = dtype_size(dtype_);
     const size_t H = (size_t)cfg_.hidden, S = (size_t)std::max<int64_t>(smax_, 1), K = (size_t)cfg_.top_k;
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t o_x = 0, o_d = o_x + al(es * S * H), o_rf = o_d + al(es * S * H), o_rb = o_rf + al(es * E * S * H),
-                 o_w = o_rb + al(es * E * S * H), total = o_w + al(4 * E * S * K);
+                 o_w = o_rb + al(es * E * S * H), o_k = o_w + al(4 * E * S * K), total = o_k + al(es * K * S * H);
     B2_CUDA(cudaMalloc(&sym_, total));
     cudaIpcMemHandle_t h;
     B2_CUDA(cudaIpcGetMemHandle(&h, sym_));
@@ -207,13 +209,14 @@ void MoeLayer::ep_setup() {
             peer_base_[(size_t)p] = (char*)ptr;
         }
     }
-    std::vector<void*> tab((size_t)5 * E);
+    std::vector<void*> tab((size_t)6 * E);
     for (int p = 0; p < E; ++p) {
         tab[(size_t)(0 * E + p)] = peer_base_[(size_t)p] + o_x;
         tab[(size_t)(1 * E + p)] = peer_base_[(size_t)p] + o_d;
         tab[(size_t)(2 * E + p)] = peer_base_[(size_t)p] + o_rf;
         tab[(size_t)(3 * E + p)] = peer_base_[(size_t)p] + o_rb;
         tab[(size_t)(4 * E + p)] = peer_base_[(size_t)p] + o_w;
+        tab[(size_t)(5 * E + p)] = peer_base_[(size_t)p] + o_k;
     }
     B2_CUDA(cudaMalloc(&peer_tab_, sizeof(void*) * tab.size()));
     B2_CUDA(cudaMemcpy(peer_tab_, tab.data(), sizeof(void*) * tab.size(), cudaMemcpyHostToDevice));
@@ -222,6 +225,7 @@ void MoeLayer::ep_setup() {
     ret_f_ = sym_ + o_rf;
     ret_b_ = sym_ + o_rb;
     wret_ = (float*)(sym_ + o_w);
+    kslab_ = sym_ + o_k;
 }
 
 // every rank's preceding stream work (and its peer stores) is complete once this returns
@@ -331,6 +335,8 @@ void MoeLayer::run_graphed(GraphCache (&gcs)[kGraphSlots], std::vector<const voi
 }
 
 // dispatch weights/indices of this forward (learned top-k or FUR; the gathered table at EP > 1)
+bool MoeLayer::fused_combine() const { return dtype_ == BF16 && cfg_.ep > 1 && fused_combine_opt_; }
+
 bool MoeLayer::gather_in_gemm() const {
     return dtype_ == BF16 && cfg_.ep == 1 && tma_gather_ && ((uintptr_t)x_ & 15) == 0 && s_ > 0;
 }
@@ -422,6 +428,7 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     ra.selected_k = selected_k_;
     ra.slot_prow = slot_prow_;
     ra.prow_src = prow_src_;
+    ra.prow_k = fused_combine() ? prow_k_ : nullptr;
     ra.err = err_;
     launch_routing_index(ra, st);
     launches_ += 4;
@@ -466,6 +473,14 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
         mark(kGemmGateUp, true);
         ga.kind = GemmKind::FwdDown;
         ga.gather_rows = nullptr;
+        if (fused_combine()) {  // w * y rows go straight into the sources' slabs over NVLink
+            ga.peer_kslab = (void* const*)peer_tab_ + 5 * E;
+            ga.prow_src = prow_src_;
+            ga.prow_k = prow_k_;
+            ga.gw = gw_;
+            ga.ep_S = S;
+            ga.ep_K = K;
+        }
         ga.h = h_;
         ga.wd = down;
         ga.out0 = y_;
@@ -517,9 +532,12 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     }
     // stage 5: weighted combine (377); EP = 1 so the reducescatter (378) is the identity
     mark(kCombine, false);
-    if (E > 1) {
-        // weighted partial rows stored into the source ranks' slabs, then summed there in
-        // rank order (the reducescatter of moe.hpp:378)
+    if (E > 1 && fused_combine()) {
+        // the FwdDown epilogue already stored every (t, k) row w * y into the source's slab
+        ep_barrier();
+        launch_kslab_sum<T>((const T*)kslab_, S, K, H, out, st);
+        launches_ += 1;
+    } else if (E > 1) {
         // each owner combines its slots into its OWN slab row [gid]; after the barrier the
         // source pulls its rows from the owners and sums them in rank order
         launch_ep_combine_local<T>((const T*)y_, slot_prow_, selected_k_, cec_, gw_, K, S, Tt, H, (T*)ret_f_, st);
@@ -635,6 +653,14 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         ga.kind = GemmKind::BwdDx;  // 414-415
         ga.gather_rows = nullptr;
         ga.x = mlp_in_;
+        if (fused_combine()) {  // dX rows go straight into the sources' slabs over NVLink
+            ga.peer_kslab = (void* const*)peer_tab_ + 5 * E;
+            ga.prow_src = prow_src_;
+            ga.prow_k = prow_k_;
+            ga.gw = nullptr;
+            ga.ep_S = S;
+            ga.ep_K = K;
+        }
         ga.out0 = dxp_;
         mark(kGemmDx, false);
         launch_sm100_gemm(ga, st);
@@ -729,10 +755,16 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         // the two reducescatters of moe.hpp:427-428: owners combine dX partials into their own slab (the top-k weight gradients already
         // sit in their own wret, written by the output-reduction backward); after the barrier
         // each source pulls and sums its rows in rank order
-        launch_ep_combine_local<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, K, S, Tt, H, (T*)ret_b_, st);
-        ep_barrier();
-        launch_ep_pull_sum<T>((const T* const*)peer_tab_ + 3 * E, gi_local_, S, K, E, nr, H, ctx_.coord_ep,
-                              (T*)dx_exp_, st);
+        if (fused_combine()) {  // the BwdDx epilogue stored every (t, k) dX row into the slab
+            ep_barrier();
+            launch_kslab_sum<T>((const T*)kslab_, S, K, H, (T*)dx_exp_, st);
+        } else {
+            launch_ep_combine_local<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, K, S, Tt, H,
+                                       (T*)ret_b_, st);
+            ep_barrier();
+            launch_ep_pull_sum<T>((const T* const*)peer_tab_ + 3 * E, gi_local_, S, K, E, nr, H, ctx_.coord_ep,
+                                  (T*)dx_exp_, st);
+        }
         launch_ep_pull_sum<float>((const float* const*)peer_tab_ + 4 * E, gi_local_, S, K, E, nr, K, ctx_.coord_ep,
                                   wgrad_local_, st);
         wgrad_local = wgrad_local_;

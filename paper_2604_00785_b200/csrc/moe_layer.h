@@ -125,6 +125,11 @@ class MoeLayer {
     void set_graph(bool on);
     // opt into the TMA tile::gather4 X operand (no materialised mlp_in); off by default
     void set_tma_gather(bool on) { tma_gather_ = on; }
+    // EP > 1: opt into the GEMM-fused combine instead of the owner-local combine + NVLink pull
+    void set_fused_combine(bool on) {
+        fused_combine_opt_ = on;
+        set_graph(graph_);  // the captured sequences change
+    }
 
   private:
     template <typename T>
@@ -135,7 +140,13 @@ class MoeLayer {
 
     void mark(int stage, bool end);
     void set_dispatch_tables();
-    bool gather_in_gemm() const;  // bf16, EP = 1, opted in: GEMMs gather X rows by TMA gather4
+    bool gather_in_gemm() const;
+    // bf16, EP > 1, opt-in: the FwdDown / BwdDx epilogues store their rows straight into the
+    // source ranks' [K][S][H] slabs over NVLink (GEMM-fused combine). Correct, but measured
+    // slower (7.65 vs 5.32 ms per EP=2 step): each lane's 64-byte remote stores to scattered
+    // rows make the epilogue NVLink-bound; the owner-local combine + coalesced pull is default
+    bool fused_combine() const;
+    bool fused_combine_opt_ = false;  // bf16, EP = 1, opted in: GEMMs gather X rows by TMA gather4
     bool tma_gather_ = false;     // off by default: measured 1.9x slower GEMMs (32 TMA ops/stage)
 
     struct GraphCache {
@@ -176,7 +187,7 @@ class MoeLayer {
     // int32
     int32_t *topi_, *fi_, *sel_, *whist_, *wbase_, *expert_counts_, *cec_, *partial_counts_, *partial_cum_,
         *token_counts_, *ctc_, *pad_start_, *input_indices_, *output_indices_, *selected_k_, *slot_prow_,
-        *prow_src_, *err_;
+        *prow_src_, *prow_k_, *err_;
     const float* gw_ = nullptr;    // dispatch weights (learned or FUR)
     const int32_t* gi_ = nullptr;  // dispatch indices
     // dtype buffers (padded row space)
@@ -193,6 +204,7 @@ class MoeLayer {
     void** peer_tab_ = nullptr;  // device: tables of E pointers: x, dout, ret_f, ret_b, wret
     void *x_sh_ = nullptr, *dout_sh_ = nullptr, *ret_f_ = nullptr, *ret_b_ = nullptr;
     float* wret_ = nullptr;
+    void* kslab_ = nullptr;
     int32_t* gi_all_ = nullptr;
     float* gw_all_ = nullptr;
     int32_t* bar_ = nullptr;

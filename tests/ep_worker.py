@@ -40,7 +40,7 @@ def run(rank, world, port, case, result_path):
     ids = [b2.Context.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(ids, src=0)
     c = dict(case)
-    ckpt, graph = c.pop("ckpt", False), c.pop("graph", False)
+    ckpt, graph, fused = c.pop("ckpt", False), c.pop("graph", False), c.pop("fused", False)
     stream = torch.cuda.Stream() if graph else None  # graph capture needs a non-default stream
     if stream is not None:
         torch.cuda.set_stream(stream)
@@ -68,6 +68,10 @@ def run(rank, world, port, case, result_path):
     X, DO = tt(x[sl]), tt(dout[sl])
     R, G, U, D = tt(router), tt(gate[el]), tt(up[el]), tt(down[el])
     layer = b2.MoeLayer(ctx, bcfg, dtype, s, checkpoint=ckpt)
+    if fused:  # the opt-in GEMM-fused combine (epilogue stores into the sources' slabs)
+        import ctypes
+        b2.lib().b2x_moe_set_fused_combine.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        b2.lib().b2x_moe_set_fused_combine(layer.h, 1)
     reps = 3 if graph else 1  # eager, capture, replay: the last one is checked
     if graph:
         layer.set_graph(True)
