@@ -387,6 +387,66 @@ void launch_kslab_sum(const T* slab, int S, int K, int W, T* out, cudaStream_t s
     B2_LAUNCH_CHECK();
 }
 
+// NVLink flag barrier over the EP group: every rank bumps its slot in every peer's flag
+// array (system-scope release), then waits until all of its own slots reach the epoch it
+// expects (acquire). Epochs live on the device (graph-replay safe); every rank calls the
+// barriers in the same order, so the counts agree. Bounded spin: traps after ~20 s.
+__global__ void ep_flag_barrier_kernel(int* const* __restrict__ peer_flags, int* __restrict__ own_flags,
+                                       int* __restrict__ epoch, int E, int me) {
+    const int p = threadIdx.x;
+    __shared__ int target;
+    if (p == 0) target = *epoch + 1;
+    __syncthreads();
+    __threadfence_system();  // this rank's earlier stores (incl. peer memory) before the signal
+    if (p < E) atomicAdd_system(peer_flags[p] + me, 1);
+    if (p < E) {
+        uint64_t t0 = 0;
+        unsigned spins = 0;
+        while (atomicAdd_system(own_flags + p, 0) < target) {
+            if ((++spins & 0xFFFu) == 0) {
+                uint64_t now;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                if (t0 == 0) t0 = now;
+                else if (now - t0 > 20000000000ull) {
+                    printf("b2 ep barrier stuck: rank %d waits on %d (epoch %d)\n", me, p, target);
+                    __trap();
+                }
+            }
+        }
+    }
+    __syncthreads();
+    __threadfence_system();
+    if (p == 0) *epoch = target;
+}
+
+void launch_ep_flag_barrier(int* const* peer_flags, int* own_flags, int* epoch, int E, int me, cudaStream_t st) {
+    check(E <= 1024, "ep barrier: group too large");
+    ep_flag_barrier_kernel<<<1, std::max(32, (E + 31) / 32 * 32), 0, st>>>(peer_flags, own_flags, epoch, E, me);
+    B2_LAUNCH_CHECK();
+}
+
+// the routing tables of all EP ranks (the reference's allgathered indices_g / weights_g,
+// moe.hpp:366-367), pulled from the peers' symmetric buffers after a barrier
+__global__ void ep_table_pull_kernel(const int32_t* const* __restrict__ peer_ids,
+                                     const float* const* __restrict__ peer_w, int64_t n, int E,
+                                     int32_t* __restrict__ ids_all, float* __restrict__ w_all) {
+    const int64_t total = n * E;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i / n);
+        const int64_t j = i % n;
+        ids_all[i] = __ldcv(peer_ids[r] + j);
+        w_all[i] = __ldcv(peer_w[r] + j);
+    }
+}
+
+void launch_ep_table_pull(const int32_t* const* peer_ids, const float* const* peer_w, int64_t n, int E,
+                          int32_t* ids_all, float* w_all, cudaStream_t st) {
+    if (n <= 0) return;
+    ep_table_pull_kernel<<<(unsigned)std::min<int64_t>(1184, ceil_div(n * E, 256)), 256, 0, st>>>(peer_ids, peer_w, n, E,
+                                                                                                ids_all, w_all);
+    B2_LAUNCH_CHECK();
+}
+
 static unsigned ep_grid(int64_t warps) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(148 * 16, ceil_div(warps, 8))); }
 
 template <typename T>

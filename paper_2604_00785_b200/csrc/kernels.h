@@ -96,6 +96,11 @@ void launch_ep_pull_sum(const T* const* peer_slab, const int32_t* gi_local, int 
 // FwdDown / BwdDx epilogue over NVLink
 template <typename T>
 void launch_kslab_sum(const T* slab, int S, int K, int W, T* out, cudaStream_t st);
+// [E][n] routing tables gathered from the peers' symmetric buffers
+void launch_ep_table_pull(const int32_t* const* peer_ids, const float* const* peer_w, int64_t n, int E,
+                          int32_t* ids_all, float* w_all, cudaStream_t st);
+// all-ranks barrier over NVLink peer memory (flag counters in the symmetric buffer)
+void launch_ep_flag_barrier(int* const* peer_flags, int* own_flags, int* epoch, int E, int me, cudaStream_t st);
 void launch_ep_wgrad_push(const float* wgrad, const int32_t* cec, int K, int S, int T_tot, int me,
                           float* const* peer_wret, cudaStream_t st);
 template <typename T>

@@ -186,8 +186,13 @@ void MoeLayer::ep_setup() {
     const size_t H = (size_t)cfg_.hidden, S = (size_t)std::max<int64_t>(smax_, 1), K = (size_t)cfg_.top_k;
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t o_x = 0, o_d = o_x + al(es * S * H), o_rf = o_d + al(es * S * H), o_rb = o_rf + al(es * E * S * H),
-                 o_w = o_rb + al(es * E * S * H), o_k = o_w + al(4 * E * S * K), total = o_k + al(es * K * S * H);
+                 o_w = o_rb + al(es * E * S * H), o_k = o_w + al(4 * E * S * K), o_f = o_k + al(es * K * S * H),
+                 o_t = o_f + al(4 * (size_t)E), total = o_t + al(8 * S * K);
     B2_CUDA(cudaMalloc(&sym_, total));
+    // barrier flags start at zero before any peer can see this buffer: the memset precedes
+    // this rank's handle contribution on the same stream
+    B2_CUDA(cudaMemsetAsync(sym_ + o_f, 0, 4 * (size_t)E, ctx_.stream));
+    B2_CUDA(cudaMemsetAsync(bar_, 0, 4, ctx_.stream));
     cudaIpcMemHandle_t h;
     B2_CUDA(cudaIpcGetMemHandle(&h, sym_));
     static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
@@ -209,7 +214,7 @@ void MoeLayer::ep_setup() {
             peer_base_[(size_t)p] = (char*)ptr;
         }
     }
-    std::vector<void*> tab((size_t)6 * E);
+    std::vector<void*> tab((size_t)9 * E);
     for (int p = 0; p < E; ++p) {
         tab[(size_t)(0 * E + p)] = peer_base_[(size_t)p] + o_x;
         tab[(size_t)(1 * E + p)] = peer_base_[(size_t)p] + o_d;
@@ -217,6 +222,9 @@ void MoeLayer::ep_setup() {
         tab[(size_t)(3 * E + p)] = peer_base_[(size_t)p] + o_rb;
         tab[(size_t)(4 * E + p)] = peer_base_[(size_t)p] + o_w;
         tab[(size_t)(5 * E + p)] = peer_base_[(size_t)p] + o_k;
+        tab[(size_t)(6 * E + p)] = peer_base_[(size_t)p] + o_f;
+        tab[(size_t)(7 * E + p)] = peer_base_[(size_t)p] + o_t;                // routing ids [S,K]
+        tab[(size_t)(8 * E + p)] = peer_base_[(size_t)p] + o_t + 4 * S * K;    // routing weights [S,K]
     }
     B2_CUDA(cudaMalloc(&peer_tab_, sizeof(void*) * tab.size()));
     B2_CUDA(cudaMemcpy(peer_tab_, tab.data(), sizeof(void*) * tab.size(), cudaMemcpyHostToDevice));
@@ -226,10 +234,15 @@ void MoeLayer::ep_setup() {
     ret_b_ = sym_ + o_rb;
     wret_ = (float*)(sym_ + o_w);
     kslab_ = sym_ + o_k;
+    flags_ = (int*)(sym_ + o_f);
+    tab_ids_ = (int32_t*)(sym_ + o_t);
+    tab_w_ = (float*)(sym_ + o_t + 4 * S * K);
 }
 
 // every rank's preceding stream work (and its peer stores) is complete once this returns
-void MoeLayer::ep_barrier() { all_reduce_sum(ctx_.comm->ep, bar_, bar_, 1, ncclInt32, ctx_.stream); }
+void MoeLayer::ep_barrier() {
+    launch_ep_flag_barrier((int* const*)peer_tab_ + 6 * cfg_.ep, flags_, bar_, cfg_.ep, ctx_.coord_ep, ctx_.stream);
+}
 
 const char* MoeLayer::stage_name(int s) {
     static const char* names[kNumStages] = {"route",           "index",          "gather",       "gemm_fwd_gate_up",
@@ -393,13 +406,17 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     }
     if (E > 1) {
         // the allgathers of weights and indices (moe.hpp:366-367): the reference's gathered
-        // routing table; token rows stay where they are until an expert owner pulls them
+        // routing table; token rows stay where they are until an expert owner pulls them.
+        // Publish x and this rank's table in the symmetric buffer, barrier, then pull every
+        // rank's table (NVLink peer memory; no NCCL on the step's path)
         B2_CUDA(cudaMemcpyAsync(x_sh_, x, sizeof(T) * (size_t)S * H, cudaMemcpyDeviceToDevice, st));
-        B2_NCCL(ncclGroupStart());
-        B2_NCCL(ncclAllGather(gi_local_, gi_all_, (size_t)S * K, ncclInt32, ctx_.comm->ep.comm, st));
-        B2_NCCL(ncclAllGather(fur ? (const float*)fw_ : (const float*)topw_, gw_all_, (size_t)S * K, ncclFloat32,
-                              ctx_.comm->ep.comm, st));
-        B2_NCCL(ncclGroupEnd());
+        B2_CUDA(cudaMemcpyAsync(tab_ids_, gi_local_, 4 * (size_t)S * K, cudaMemcpyDeviceToDevice, st));
+        B2_CUDA(cudaMemcpyAsync(tab_w_, fur ? (const float*)fw_ : (const float*)topw_, 4 * (size_t)S * K,
+                                cudaMemcpyDeviceToDevice, st));
+        ep_barrier();
+        launch_ep_table_pull((const int32_t* const*)peer_tab_ + 7 * E, (const float* const*)peer_tab_ + 8 * E,
+                             (int64_t)S * K, E, gi_all_, gw_all_, st);
+        launches_ += 2;
         Tt = E * S;
     }
     // balancing statistics (381-386): mean_probs over the local rows, sel_counts over the

@@ -205,6 +205,9 @@ class MoeLayer {
     void *x_sh_ = nullptr, *dout_sh_ = nullptr, *ret_f_ = nullptr, *ret_b_ = nullptr;
     float* wret_ = nullptr;
     void* kslab_ = nullptr;
+    int* flags_ = nullptr;  // NVLink barrier counters (one per peer), in the symmetric buffer
+    int32_t* tab_ids_ = nullptr;  // this rank's published routing table [S,K] (symmetric buffer)
+    float* tab_w_ = nullptr;
     int32_t* gi_all_ = nullptr;
     float* gw_all_ = nullptr;
     int32_t* bar_ = nullptr;
