@@ -65,9 +65,10 @@ constexpr int EPI_SLOT_BYTES = 32 * 32 * 2;
 template <GemmKind K, int CG>
 struct KCfg {
     static constexpr bool TMA_EPI = (int)K <= (int)GemmKind::WgradGateUp;
-    static constexpr int SLOTS = K == GemmKind::FwdGateUp ? 3 : 2;
-    static constexpr int STAGES =
-        CG == 1 ? 4 : ((K == GemmKind::FwdGateUp || K == GemmKind::BwdDownDgrad) ? 5 : 6);
+    // two staging slots everywhere (FwdGateUp's three boxes per chunk rotate through them),
+    // so every kind but the dgrad (which also stages its G/U operands) keeps 6 stages
+    static constexpr int SLOTS = 2;
+    static constexpr int STAGES = CG == 1 ? 4 : (K == GemmKind::BwdDownDgrad ? 5 : 6);
     static constexpr int WARP_EPI_BYTES =
         TMA_EPI ? SLOTS * EPI_SLOT_BYTES + (K == GemmKind::BwdDownDgrad ? EPI_GU_BYTES : 0) : 0;
     static constexpr int SMEM =
