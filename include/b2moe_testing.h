@@ -24,6 +24,9 @@ int b2x_moe_set_tma_gather(b2_moe* m, int on);
  * row into the source rank's slab over NVLink) instead of (0, default) the owner-local
  * combine + coalesced NVLink pull. */
 int b2x_moe_set_fused_combine(b2_moe* m, int on);
+/* EP > 1, bf16: overlap (1, default) the backward's dX return with the weight-gradient
+ * GEMMs (side stream, reduced GEMM grid) or run it after them (0). */
+int b2x_moe_set_overlap_return(b2_moe* m, int on);
 #ifdef __cplusplus
 }
 #endif

@@ -1179,6 +1179,7 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
     if (a.gather_rows) check(a.gather_tokens >= 0 && a.pmax % 4 == 0, "gather4 operand: bad token count / row capacity");
     const int64_t P = a.pmax, H = a.H, I = a.I, nr = a.nr;
     int grid = a.num_sms > 0 ? a.num_sms : 148;
+    if (a.max_ctas > 0) grid = std::min(grid, std::max(2, a.max_ctas));
     p.umma_n = BN;
     p.b_chunks = 4;
     p.S = a.S;

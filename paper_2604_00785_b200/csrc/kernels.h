@@ -180,6 +180,7 @@ struct Sm100GemmArgs {
     const int32_t* prow_k;       // padded row -> top-k slot
     const float* gw;             // [T, K] gathered routing weights (FwdDown)
     int ep_S, ep_K;              // tokens per rank, top-k
+    int max_ctas;                // > 0: cap the persistent grid (SMs left to concurrent comm kernels)
 };
 void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st);
 // number of S splits the RouterDw kind uses (its partial buffer holds splits*H*N floats)

@@ -156,6 +156,9 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
         wgrad_local_ = w.take<float>(smax_ * K);
         dx_exp_ = w.take_bytes(es * (size_t)std::max<int64_t>(smax_ * H, 1));
         ep_setup();
+        B2_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+        B2_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+        B2_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     }
     B2_CUDA(cudaMemsetAsync(err_, 0, 4, ctx_.stream));
     B2_CUDA(cudaMemsetAsync(pad_start_, 0, 4 * (nr + 1), ctx_.stream));
@@ -168,6 +171,12 @@ MoeLayer::~MoeLayer() {
     }
     for (auto& st : prof_ev_)
         for (cudaEvent_t e : st) cudaEventDestroy(e);
+    if (side_) {
+        cudaStreamSynchronize(side_);
+        cudaStreamDestroy(side_);
+        cudaEventDestroy(ev_fork_);
+        cudaEventDestroy(ev_join_);
+    }
     if (sym_) {
         cudaStreamSynchronize(ctx_.stream);
         for (int p = 0; p < (int)peer_base_.size(); ++p)
@@ -240,8 +249,13 @@ void MoeLayer::ep_setup() {
 }
 
 // every rank's preceding stream work (and its peer stores) is complete once this returns
-void MoeLayer::ep_barrier() {
-    launch_ep_flag_barrier((int* const*)peer_tab_ + 6 * cfg_.ep, flags_, bar_, cfg_.ep, ctx_.coord_ep, ctx_.stream);
+void MoeLayer::ep_barrier(cudaStream_t st) {
+    launch_ep_flag_barrier((int* const*)peer_tab_ + 6 * cfg_.ep, flags_, bar_, cfg_.ep, ctx_.coord_ep,
+                           st ? st : ctx_.stream);
+}
+
+bool MoeLayer::overlap_return() const {
+    return dtype_ == BF16 && cfg_.ep > 1 && !fused_combine() && side_ != nullptr && overlap_opt_;
 }
 
 const char* MoeLayer::stage_name(int s) {
@@ -651,6 +665,27 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         mark(kGemmDgrad, false);
         launch_sm100_gemm(ga, st);
         mark(kGemmDgrad, true);
+        if (overlap_return()) {
+            // EP > 1: dX first, then its return to the source ranks (owner combine, barrier,
+            // NVLink pull-sums: the reducescatters of moe.hpp:427-428) runs on a side stream
+            // while the weight-gradient GEMMs run on the SMs left to them
+            ga.kind = GemmKind::BwdDx;  // 414-415
+            ga.out0 = dxp_;
+            mark(kGemmDx, false);
+            launch_sm100_gemm(ga, st);
+            mark(kGemmDx, true);
+            B2_CUDA(cudaEventRecord(ev_fork_, st));
+            B2_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+            launch_ep_combine_local<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, K, S, Tt, H,
+                                       (T*)ret_b_, side_);
+            ep_barrier(side_);
+            launch_ep_pull_sum<T>((const T* const*)peer_tab_ + 3 * E, gi_local_, S, K, E, nr, H, ctx_.coord_ep,
+                                  (T*)dx_exp_, side_);
+            launch_ep_pull_sum<float>((const float* const*)peer_tab_ + 4 * E, gi_local_, S, K, E, nr, K,
+                                      ctx_.coord_ep, wgrad_local_, side_);
+            B2_CUDA(cudaEventRecord(ev_join_, side_));
+            ga.max_ctas = ctx_.num_sms - kCommSMs;
+        }
         ga.kind = GemmKind::WgradDown;  // 407
         ga.out0 = ddown;
         mark(kGemmWgradDown, false);
@@ -667,22 +702,28 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         mark(kGemmWgradGateUp, false);
         launch_sm100_gemm(ga, st);
         mark(kGemmWgradGateUp, true);
-        ga.kind = GemmKind::BwdDx;  // 414-415
-        ga.gather_rows = nullptr;
-        ga.x = mlp_in_;
-        if (fused_combine()) {  // dX rows go straight into the sources' slabs over NVLink
-            ga.peer_kslab = (void* const*)peer_tab_ + 5 * E;
-            ga.prow_src = prow_src_;
-            ga.prow_k = prow_k_;
-            ga.gw = nullptr;
-            ga.ep_S = S;
-            ga.ep_K = K;
+        ga.max_ctas = 0;
+        if (overlap_return()) {
+            B2_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
+            launches_ += 4 + 4;
+        } else {
+            ga.kind = GemmKind::BwdDx;  // 414-415
+            ga.gather_rows = nullptr;
+            ga.x = mlp_in_;
+            if (fused_combine()) {  // dX rows go straight into the sources' slabs over NVLink
+                ga.peer_kslab = (void* const*)peer_tab_ + 5 * E;
+                ga.prow_src = prow_src_;
+                ga.prow_k = prow_k_;
+                ga.gw = nullptr;
+                ga.ep_S = S;
+                ga.ep_K = K;
+            }
+            ga.out0 = dxp_;
+            mark(kGemmDx, false);
+            launch_sm100_gemm(ga, st);
+            mark(kGemmDx, true);
+            launches_ += 4;
         }
-        ga.out0 = dxp_;
-        mark(kGemmDx, false);
-        launch_sm100_gemm(ga, st);
-        mark(kGemmDx, true);
-        launches_ += 4;
     } else {
         SimtGemmArgs a{};
         a.group_start = pad_start_;
@@ -768,7 +809,10 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
     mark(kRouterBwd, false);
     const float* wgrad_local = wgrad_;
     const T* dx_rows = nullptr;  // EP > 1: the token's summed expert-gradient rows
-    if (E > 1) {
+    if (E > 1 && overlap_return()) {  // already returned on the side stream
+        wgrad_local = wgrad_local_;
+        dx_rows = (const T*)dx_exp_;
+    } else if (E > 1) {
         // the two reducescatters of moe.hpp:427-428: owners combine dX partials into their own slab (the top-k weight gradients already
         // sit in their own wret, written by the output-reduction backward); after the barrier
         // each source pulls and sums its rows in rank order

@@ -126,6 +126,10 @@ class MoeLayer {
     // opt into the TMA tile::gather4 X operand (no materialised mlp_in); off by default
     void set_tma_gather(bool on) { tma_gather_ = on; }
     // EP > 1: opt into the GEMM-fused combine instead of the owner-local combine + NVLink pull
+    void set_overlap_return(bool on) {
+        overlap_opt_ = on;
+        set_graph(graph_);
+    }
     void set_fused_combine(bool on) {
         fused_combine_opt_ = on;
         set_graph(graph_);  // the captured sequences change
@@ -197,7 +201,14 @@ class MoeLayer {
     // rank holds x / dout (pulled by the expert owners) and the return slabs the owners
     // store into; only the [S,K] routing table goes through an NCCL all-gather
     void ep_setup();
-    void ep_barrier();
+    void ep_barrier(cudaStream_t st = nullptr);
+    // bf16, EP > 1: the backward returns dX / top-k weight gradients on a side stream while
+    // the weight-gradient GEMMs run on num_sms - kCommSMs SMs
+    bool overlap_return() const;
+    static constexpr int kCommSMs = 16;
+    bool overlap_opt_ = true;
+    cudaStream_t side_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     const int32_t* gi_local_ = nullptr;  // this rank's dispatch table [S,K] (learned or FUR)
     char* sym_ = nullptr;
     std::vector<char*> peer_base_;

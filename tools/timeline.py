@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--tokens", type=int, default=16384)
     ap.add_argument("--tma-gather", action="store_true", help="TMA gather4 X operand instead of mlp_in rows")
     ap.add_argument("--fused", action="store_true", help="EP: the GEMM-fused combine (opt-in)")
+    ap.add_argument("--no-overlap", action="store_true", help="EP: dX return after the wgrad GEMMs")
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -46,6 +47,10 @@ def main():
     layer = b2.MoeLayer(ctx, cfg, torch.bfloat16, S)
     if args.graph:
         layer.set_graph(True)
+    if args.no_overlap:
+        import ctypes
+        b2.lib().b2x_moe_set_overlap_return.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        b2.lib().b2x_moe_set_overlap_return(layer.h, 0)
     if args.fused:
         import ctypes
         b2.lib().b2x_moe_set_fused_combine.argtypes = [ctypes.c_void_p, ctypes.c_int]
