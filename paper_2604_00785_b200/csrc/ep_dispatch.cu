@@ -4,9 +4,9 @@
 // rank (allgather, moe.hpp:365-367), computes its experts on the gathered table and
 // returns the combined rows with a rank-ordered reducescatter (moe.hpp:378); the
 // backward mirrors both (moe.hpp:400, 427-428). Here only the routing TABLE is
-// all-gathered (NCCL, [S,K] ids + weights: the reference's indices_g / weights_g, so
-// counting and index generation see exactly the reference's gathered table). Token
-// rows never take a collective:
+// gathered ([S,K] ids + weights, pulled from every rank's symmetric buffer after an NVLink
+// flag barrier: the reference's indices_g / weights_g, so counting and index generation
+// see exactly the reference's gathered table). Token rows never take a collective:
 //   gather   the expert owner PULLS each gathered token that has a local expert once
 //            from the source rank's x over NVLink (CUDA IPC mapping) and writes it to
 //            every padded row of that token (dedup per destination);
@@ -16,8 +16,7 @@
 //            comm.hpp:391-394) — remote loads with many bytes in flight, fused with the sum.
 // The backward pulls dout rows the same way; dX partial rows and the top-k weight
 // gradients go back through the owners' slabs and the same pull-sum. No host
-// synchronisation, no staging copies. (The push-based kernels below are kept for the
-// stress tests of the peer-store path.)
+// synchronisation, no staging copies.
 #include "b2_common.cuh"
 #include "kernels.h"
 
@@ -64,34 +63,10 @@ __global__ void ep_gather_pull_kernel(const T* const* __restrict__ peer_src, int
     }
 }
 
-// warp per gathered token with local slots: (weighted) sum of its expert rows in slot
-// (k) order, stored into the source rank's slab row [me * S + t]
+// the owner's (weighted) sum of a gathered token's local slot rows, in slot (k) order, into
+// its own slab row [gid] (local_out) or — push variant — the source rank's slab [me * S + t]
 template <typename T>
-__global__ void ep_combine_push_kernel(const T* __restrict__ y, const int32_t* __restrict__ slot_prow,
-                                       const int32_t* __restrict__ selected_k, const int32_t* __restrict__ cec,
-                                       const float* __restrict__ gw /*[T,K] or null*/, int K, int S, int T_tot, int H,
-                                       int me, T* const* __restrict__ peer_ret) {
-    const int lane = threadIdx.x % 32;
-    const int nw = gridDim.x * blockDim.x / 32;
-    for (int gid = (blockIdx.x * blockDim.x + threadIdx.x) / 32; gid < T_tot; gid += nw) {
-        const int j0 = cec[gid], j1 = cec[gid + 1];
-        if (j0 == j1) continue;
-        T* dst = peer_ret[gid / S] + ((int64_t)me * S + gid % S) * H;
-        for (int c = lane; c < H; c += 32) {
-            float acc = 0.f;
-            for (int j = j0; j < j1; ++j) {
-                const float v = Elem<T>::to_f(y[(int64_t)slot_prow[j] * H + c]);
-                acc = gw ? __fadd_rn(acc, __fmul_rn(gw[(int64_t)gid * K + selected_k[j]], v)) : __fadd_rn(acc, v);
-            }
-            dst[c] = Elem<T>::from_f(acc);
-        }
-    }
-    __threadfence_system();
-}
-
-// vectorised (16-byte) variant
-template <typename T>
-__global__ void ep_combine_push_vec_kernel(const T* __restrict__ y, const int32_t* __restrict__ slot_prow,
+__global__ void ep_combine_slots_kernel(const T* __restrict__ y, const int32_t* __restrict__ slot_prow,
                                            const int32_t* __restrict__ selected_k, const int32_t* __restrict__ cec,
                                            const float* __restrict__ gw, int K, int S, int T_tot, int H, int me,
                                            T* const* __restrict__ peer_ret, T* __restrict__ local_out) {
@@ -156,95 +131,6 @@ __global__ void ep_combine_push_vec_kernel(const T* __restrict__ y, const int32_
         }
     }
     if (!local_out) __threadfence_system();
-}
-
-// the owner's top-k weight-gradient rows of the gathered tokens it serves, pushed to
-// the source rank's slab [me * S + t][K] (entries of non-local k are zero)
-__global__ void ep_wgrad_push_kernel(const float* __restrict__ wgrad, const int32_t* __restrict__ cec, int K, int S,
-                                     int T_tot, int me, float* const* __restrict__ peer_wret) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)T_tot * K;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int gid = (int)(i / K), k = (int)(i % K);
-        if (cec[gid] == cec[gid + 1]) continue;
-        peer_wret[gid / S][((int64_t)me * S + gid % S) * K + k] = wgrad[i];
-    }
-    __threadfence_system();
-}
-
-// out[t] = sum over the ranks r (in order) that token t routes to of slab[r][t]
-template <typename T>
-__global__ void ep_return_sum_kernel(const T* __restrict__ slab, const int32_t* __restrict__ gi_local, int S, int K,
-                                     int E, int NR, int W, T* __restrict__ out) {
-    const int t = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
-    if (t >= S) return;
-    unsigned mask = 0;
-    for (int k = 0; k < K; ++k) mask |= 1u << (gi_local[(int64_t)t * K + k] / NR);
-    const bool vec = ((int64_t)W * sizeof(T)) % 16 == 0;
-    if (vec) {
-        constexpr int V = 16 / sizeof(T);
-        constexpr int MAXR = 8;  // slabs of up to 8 ranks in flight per lane
-        for (int v = lane; v < W / V; v += 32) {
-            float acc[V];
-            bool any = false;
-            for (int r0 = 0; r0 < E; r0 += MAXR) {
-                int4 raw[MAXR];
-#pragma unroll
-                for (int q = 0; q < MAXR; ++q)
-                    if (r0 + q < E && (mask >> (r0 + q) & 1u))
-                        raw[q] = __ldcv(reinterpret_cast<const int4*>(slab + ((int64_t)(r0 + q) * S + t) * W) + v);
-#pragma unroll
-                for (int q = 0; q < MAXR; ++q) {
-                    if (!(r0 + q < E && (mask >> (r0 + q) & 1u))) continue;
-                    float f[V];
-                    if constexpr (sizeof(T) == 4) {
-                        f[0] = __int_as_float(raw[q].x);
-                        f[1] = __int_as_float(raw[q].y);
-                        f[2] = __int_as_float(raw[q].z);
-                        f[3] = __int_as_float(raw[q].w);
-                    } else {
-                        const uint32_t w[4] = {(uint32_t)raw[q].x, (uint32_t)raw[q].y, (uint32_t)raw[q].z,
-                                               (uint32_t)raw[q].w};
-#pragma unroll
-                        for (int z = 0; z < 4; ++z) {
-                            f[2 * z] = __uint_as_float(w[z] << 16);
-                            f[2 * z + 1] = __uint_as_float(w[z] & 0xFFFF0000u);
-                        }
-                    }
-#pragma unroll
-                    for (int z = 0; z < V; ++z) acc[z] = any ? __fadd_rn(acc[z], f[z]) : f[z];
-                    any = true;
-                }
-            }
-            if (!any)
-                for (int q = 0; q < V; ++q) acc[q] = 0.f;
-            int4 o;
-            if constexpr (sizeof(T) == 4) {
-                o = make_int4(__float_as_int(acc[0]), __float_as_int(acc[1]), __float_as_int(acc[2]),
-                              __float_as_int(acc[3]));
-            } else {
-                uint32_t w[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    __nv_bfloat162 b = __floats2bfloat162_rn(acc[2 * q], acc[2 * q + 1]);
-                    w[q] = *reinterpret_cast<uint32_t*>(&b);
-                }
-                o = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
-            }
-            reinterpret_cast<int4*>(out + (int64_t)t * W)[v] = o;
-        }
-    } else {
-        for (int c = lane; c < W; c += 32) {
-            float acc = 0.f;
-            bool any = false;
-            for (int r = 0; r < E; ++r) {
-                if (!(mask >> r & 1u)) continue;
-                const float v = Elem<T>::to_f(slab[((int64_t)r * S + t) * W + c]);
-                acc = any ? __fadd_rn(acc, v) : v;
-                any = true;
-            }
-            out[(int64_t)t * W + c] = Elem<T>::from_f(acc);
-        }
-    }
 }
 
 // out[t] = sum over the ranks r (in order) that token t routes to of owner r's partial row
@@ -458,25 +344,11 @@ void launch_ep_gather_pull(const T* const* peer_src, int S, int T_tot, int H, co
 }
 
 template <typename T>
-void launch_ep_combine_push(const T* y, const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec,
-                            const float* gw, int K, int S, int T_tot, int H, int me, T* const* peer_ret,
-                            cudaStream_t st) {
-    if (T_tot <= 0) return;
-    if (((int64_t)H * sizeof(T)) % 16 == 0)
-        ep_combine_push_vec_kernel<T><<<ep_grid(T_tot), 256, 0, st>>>(y, slot_prow, selected_k, cec, gw, K, S, T_tot,
-                                                                      H, me, peer_ret, nullptr);
-    else
-        ep_combine_push_kernel<T><<<ep_grid(T_tot), 256, 0, st>>>(y, slot_prow, selected_k, cec, gw, K, S, T_tot, H,
-                                                                  me, peer_ret);
-    B2_LAUNCH_CHECK();
-}
-
-template <typename T>
 void launch_ep_combine_local(const T* y, const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec,
                              const float* gw, int K, int S, int T_tot, int H, T* own_slab, cudaStream_t st) {
     if (T_tot <= 0) return;
     check(((int64_t)H * sizeof(T)) % 16 == 0, "ep combine: rows must be 16-byte multiples");
-    ep_combine_push_vec_kernel<T><<<ep_grid(T_tot), 256, 0, st>>>(y, slot_prow, selected_k, cec, gw, K, S, T_tot, H,
+    ep_combine_slots_kernel<T><<<ep_grid(T_tot), 256, 0, st>>>(y, slot_prow, selected_k, cec, gw, K, S, T_tot, H,
                                                                   0, nullptr, own_slab);
     B2_LAUNCH_CHECK();
 }
@@ -489,29 +361,9 @@ void launch_ep_pull_sum(const T* const* peer_slab, const int32_t* gi_local, int 
     B2_LAUNCH_CHECK();
 }
 
-void launch_ep_wgrad_push(const float* wgrad, const int32_t* cec, int K, int S, int T_tot, int me,
-                          float* const* peer_wret, cudaStream_t st) {
-    const int64_t n = (int64_t)T_tot * K;
-    if (n <= 0) return;
-    ep_wgrad_push_kernel<<<(unsigned)std::min<int64_t>(1184, ceil_div(n, 256)), 256, 0, st>>>(wgrad, cec, K, S, T_tot,
-                                                                                             me, peer_wret);
-    B2_LAUNCH_CHECK();
-}
-
-template <typename T>
-void launch_ep_return_sum(const T* slab, const int32_t* gi_local, int S, int K, int E, int NR, int W, T* out,
-                          cudaStream_t st) {
-    if (S <= 0) return;
-    ep_return_sum_kernel<T><<<(unsigned)ceil_div(S, 8), 256, 0, st>>>(slab, gi_local, S, K, E, NR, W, out);
-    B2_LAUNCH_CHECK();
-}
-
 #define B2_EP_INST(T)                                                                                             \
     template void launch_ep_gather_pull<T>(const T* const*, int, int, int, const int32_t*, const int32_t*, T*,    \
                                            cudaStream_t);                                                         \
-    template void launch_ep_combine_push<T>(const T*, const int32_t*, const int32_t*, const int32_t*, const float*, \
-                                            int, int, int, int, int, T* const*, cudaStream_t);                   \
-    template void launch_ep_return_sum<T>(const T*, const int32_t*, int, int, int, int, int, T*, cudaStream_t); \
     template void launch_ep_combine_local<T>(const T*, const int32_t*, const int32_t*, const int32_t*, const float*, \
                                              int, int, int, int, T*, cudaStream_t);                              \
     template void launch_ep_pull_sum<T>(const T* const*, const int32_t*, int, int, int, int, int, int, T*,        \

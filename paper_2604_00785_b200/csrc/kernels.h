@@ -78,10 +78,6 @@ void launch_swiglu_bwd(const T* g, const T* u, const T* dh, T* dgu, const int32_
 template <typename T>
 void launch_ep_gather_pull(const T* const* peer_src, int S, int T_tot, int H, const int32_t* cec,
                            const int32_t* slot_prow, T* out, cudaStream_t st);
-template <typename T>
-void launch_ep_combine_push(const T* y, const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec,
-                            const float* gw, int K, int S, int T_tot, int H, int me, T* const* peer_ret,
-                            cudaStream_t st);
 // owner side of the pull-based combine: the token's (weighted) partial row into the owner's
 // OWN slab row [gid]; sources pull them after a barrier (launch_ep_pull_sum)
 template <typename T>
@@ -101,12 +97,6 @@ void launch_ep_table_pull(const int32_t* const* peer_ids, const float* const* pe
                           int32_t* ids_all, float* w_all, cudaStream_t st);
 // all-ranks barrier over NVLink peer memory (flag counters in the symmetric buffer)
 void launch_ep_flag_barrier(int* const* peer_flags, int* own_flags, int* epoch, int E, int me, cudaStream_t st);
-void launch_ep_wgrad_push(const float* wgrad, const int32_t* cec, int K, int S, int T_tot, int me,
-                          float* const* peer_wret, cudaStream_t st);
-template <typename T>
-void launch_ep_return_sum(const T* slab, const int32_t* gi_local, int S, int K, int E, int NR, int W, T* out,
-                          cudaStream_t st);
-
 // ---- SIMT grouped GEMM (simt_gemm.cu) ----
 struct SimtGemmArgs {
     const void* A;
