@@ -439,3 +439,33 @@ def test_shared_workspace_layers_match_private(b2ctx):
     got = run(a, b)
     for u, v in zip(got, want):
         assert torch.equal(u, v)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("S,N,K", [(0, 8, 2), (1, 8, 2), (3, 1, 1), (65, 4, 4)])
+def test_layer_edge_shapes(b2ctx, orc, dtype, S, N, K):
+    """Empty and ragged inputs (S = 0, 1, odd), a single expert, top-k = all experts: the
+    layer runs, matches the oracle, and an empty batch yields empty outputs and zero
+    weight gradients."""
+    b2, ctx = b2ctx
+    dt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    H, I = 128, 64
+    ocfg, bcfg = cfg_pair(n_experts=N, top_k=K, hidden=H, intermediate=I)
+    rb = (lambda a: torch.from_numpy(np.ascontiguousarray(a)).bfloat16().float().numpy()) if dtype == "bf16" \
+        else (lambda a: a)
+    router, gate, up, down = (rb(t) for t in orc.expert_weights(ocfg, 1234, 0.05))
+    x = rb(orc.normal((S, H), 77, 0, 1.0)) if S else np.zeros((0, H), np.float32)
+    dout = rb(orc.normal((S, H), 78, 0, 1.0)) if S else np.zeros((0, H), np.float32)
+    got = run_layer(b2, ctx, bcfg, dt, x, router, gate, up, down, dout, aux_coeff=0.0)
+    if S == 0:
+        assert got["out"].shape == (0, H) and got["input"].shape == (0, H)
+        for k in ("gate", "up", "down", "router"):
+            assert not np.any(got[k])
+        return
+    ref = orc.moe_layer(ocfg, S, x, router, gate, up, down, dout, aux_coeff=0.0)
+    assert np.array_equal(got["indices"], ref["indices"])
+    tol = 1e-4 if dtype == "f32" else 2e-2
+    assert rel_err(got["out"], ref["out"]) <= tol
+    assert rel_err(got["input"], ref["dx"]) <= tol
+    for key, gkey in [("dgate", "gate"), ("dup", "up"), ("ddown", "down")]:
+        assert (rel_err if dtype == "f32" else scale_err)(got[gkey], ref[key]) <= tol, key
