@@ -27,6 +27,9 @@ int b2x_moe_set_fused_combine(b2_moe* m, int on);
 /* EP > 1, bf16: overlap (1, default) the backward's dX return with the weight-gradient
  * GEMMs (side stream, reduced GEMM grid) or run it after them (0). */
 int b2x_moe_set_overlap_return(b2_moe* m, int on);
+/* EP > 1: forward token exchange as a copy-engine all-gather overlapped with routing (1,
+ * opt-in) or as SM pulls of the needed rows after routing (0, default). */
+int b2x_moe_set_ce_dispatch(b2_moe* m, int on);
 #ifdef __cplusplus
 }
 #endif

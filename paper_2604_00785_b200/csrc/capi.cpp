@@ -561,6 +561,10 @@ int b2_opt_last_launches(b2_opt* o) { return o ? o->opt->last_launches() : 0; }
 
 #include "../../include/b2moe_testing.h"
 
+extern "C" int b2x_moe_set_ce_dispatch(b2_moe* m, int on) {
+    return guard([&] { m->layer->set_ce_dispatch(on != 0); });
+}
+
 extern "C" int b2x_moe_set_overlap_return(b2_moe* m, int on) {
     return guard([&] { m->layer->set_overlap_return(on != 0); });
 }

@@ -94,6 +94,7 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     if (E > 1) {
         for (int64_t n : {tmax_ * K, tmax_ * K, smax_ * K}) acc(4 * (size_t)std::max<int64_t>(n, 1));
         acc(es * (size_t)std::max<int64_t>(smax_ * H, 1));
+        acc(es * (size_t)std::max<int64_t>(tmax_ * H, 1));  // x_all (copy-engine dispatch)
     }
     B2_CUDA(cudaSetDevice(ctx_.device));
     if (share_ws) {
@@ -155,10 +156,12 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
         gw_all_ = w.take<float>(tmax_ * K);
         wgrad_local_ = w.take<float>(smax_ * K);
         dx_exp_ = w.take_bytes(es * (size_t)std::max<int64_t>(smax_ * H, 1));
+        x_all_ = w.take_bytes(es * (size_t)std::max<int64_t>(tmax_ * H, 1));
         ep_setup();
         B2_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
         B2_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
         B2_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+        B2_CUDA(cudaEventCreateWithFlags(&ev_xall_, cudaEventDisableTiming));
     }
     B2_CUDA(cudaMemsetAsync(err_, 0, 4, ctx_.stream));
     B2_CUDA(cudaMemsetAsync(pad_start_, 0, 4 * (nr + 1), ctx_.stream));
@@ -176,6 +179,7 @@ MoeLayer::~MoeLayer() {
         cudaStreamDestroy(side_);
         cudaEventDestroy(ev_fork_);
         cudaEventDestroy(ev_join_);
+        cudaEventDestroy(ev_xall_);
     }
     if (sym_) {
         cudaStreamSynchronize(ctx_.stream);
@@ -238,6 +242,7 @@ void MoeLayer::ep_setup() {
     B2_CUDA(cudaMalloc(&peer_tab_, sizeof(void*) * tab.size()));
     B2_CUDA(cudaMemcpy(peer_tab_, tab.data(), sizeof(void*) * tab.size(), cudaMemcpyHostToDevice));
     x_sh_ = sym_ + o_x;
+    x_sh_off_ = o_x;
     dout_sh_ = sym_ + o_d;
     ret_f_ = sym_ + o_rf;
     ret_b_ = sym_ + o_rb;
@@ -409,6 +414,20 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     const int S = (int)s_, N = (int)cfg_.n_experts, K = (int)cfg_.top_k, H = (int)cfg_.hidden,
               I = (int)cfg_.intermediate, nr = (int)cfg_.experts_per_rank();
     int Tt = S;  // rows of the (gathered) table this rank processes
+    const bool ce_dispatch = E > 1 && ce_dispatch_opt_;
+    if (ce_dispatch) {
+        // the token exchange of moe.hpp:365 as copy-engine all-gather: publish x, barrier, then
+        // a side stream copies every rank's x over NVLink into x_all while the SMs route
+        B2_CUDA(cudaMemcpyAsync(x_sh_, x, sizeof(T) * (size_t)S * H, cudaMemcpyDeviceToDevice, st));
+        ep_barrier();
+        B2_CUDA(cudaEventRecord(ev_fork_, st));
+        B2_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+        const size_t rb = sizeof(T) * (size_t)S * H;
+        for (int p = 0; p < E; ++p)
+            B2_CUDA(cudaMemcpyAsync((char*)x_all_ + (size_t)p * rb, peer_base_[(size_t)p] + x_sh_off_, rb,
+                                    cudaMemcpyDeviceToDevice, side_));
+        B2_CUDA(cudaEventRecord(ev_xall_, side_));
+    }
     // stage 1: route locally (moe.hpp:357-364)
     mark(kRoute, false);
     launch_router_logits<T>(x, router, logits_, S, H, N, st);
@@ -423,7 +442,8 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
         // routing table; token rows stay where they are until an expert owner pulls them.
         // Publish x and this rank's table in the symmetric buffer, barrier, then pull every
         // rank's table (NVLink peer memory; no NCCL on the step's path)
-        B2_CUDA(cudaMemcpyAsync(x_sh_, x, sizeof(T) * (size_t)S * H, cudaMemcpyDeviceToDevice, st));
+        if (!ce_dispatch)
+            B2_CUDA(cudaMemcpyAsync(x_sh_, x, sizeof(T) * (size_t)S * H, cudaMemcpyDeviceToDevice, st));
         B2_CUDA(cudaMemcpyAsync(tab_ids_, gi_local_, 4 * (size_t)S * K, cudaMemcpyDeviceToDevice, st));
         B2_CUDA(cudaMemcpyAsync(tab_w_, fur ? (const float*)fw_ : (const float*)topw_, 4 * (size_t)S * K,
                                 cudaMemcpyDeviceToDevice, st));
@@ -473,9 +493,15 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     const bool tma_gather = gather_in_gemm();
     mark(kGather, false);
     if (E > 1) {
-        launch_ep_gather_pull<T>((const T* const*)peer_tab_, S, Tt, H, cec_, slot_prow_, (T*)mlp_in_, st);
-        launch_zero_pad_rows<T>((T*)mlp_in_, prow_src_, p_total, H, pmax_, st);
-        launches_ += 2;
+        if (ce_dispatch) {  // every rank's rows are local now: a plain gather (pads zeroed)
+            B2_CUDA(cudaStreamWaitEvent(st, ev_xall_, 0));
+            launch_gather_rows<T>((const T*)x_all_, prow_src_, p_total, (T*)mlp_in_, H, pmax_, st);
+            launches_ += 1;
+        } else {
+            launch_ep_gather_pull<T>((const T* const*)peer_tab_, S, Tt, H, cec_, slot_prow_, (T*)mlp_in_, st);
+            launch_zero_pad_rows<T>((T*)mlp_in_, prow_src_, p_total, H, pmax_, st);
+            launches_ += 2;
+        }
     } else if (!tma_gather) {
         launch_gather_rows<T>(x, prow_src_, p_total, (T*)mlp_in_, H, pmax_, st);
         launches_ += 1;

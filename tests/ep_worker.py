@@ -41,6 +41,7 @@ def run(rank, world, port, case, result_path):
     dist.broadcast_object_list(ids, src=0)
     c = dict(case)
     ckpt, graph, fused = c.pop("ckpt", False), c.pop("graph", False), c.pop("fused", False)
+    ce = c.pop("ce", False)
     stream = torch.cuda.Stream() if graph else None  # graph capture needs a non-default stream
     if stream is not None:
         torch.cuda.set_stream(stream)
@@ -68,6 +69,10 @@ def run(rank, world, port, case, result_path):
     X, DO = tt(x[sl]), tt(dout[sl])
     R, G, U, D = tt(router), tt(gate[el]), tt(up[el]), tt(down[el])
     layer = b2.MoeLayer(ctx, bcfg, dtype, s, checkpoint=ckpt)
+    if ce:  # the opt-in copy-engine all-gather dispatch
+        import ctypes
+        b2.lib().b2x_moe_set_ce_dispatch.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        b2.lib().b2x_moe_set_ce_dispatch(layer.h, 1)
     if fused:  # the opt-in GEMM-fused combine (epilogue stores into the sources' slabs)
         import ctypes
         b2.lib().b2x_moe_set_fused_combine.argtypes = [ctypes.c_void_p, ctypes.c_int]

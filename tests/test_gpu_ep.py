@@ -50,12 +50,13 @@ CASES = [
     dict(n_experts=16, top_k=4, hidden=256, intermediate=128, token_block=8, s=300, dtype="bf16", ckpt=True,
          graph=True),
     dict(n_experts=64, top_k=8, hidden=256, intermediate=128, token_block=8, s=512, dtype="bf16", fused=True),
+    dict(n_experts=16, top_k=4, hidden=256, intermediate=128, token_block=8, s=300, dtype="bf16", ce=True),
 ]
 
 
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c['dtype']}-n{c['n_experts']}k{c['top_k']}"
-                         + ("-ckpt-graph" if c.get("ckpt") else "") + ("-fused" if c.get("fused") else ""))
+                         + ("-ckpt-graph" if c.get("ckpt") else "") + ("-fused" if c.get("fused") else "") + ("-ce" if c.get("ce") else ""))
 def test_ep_matches_oracle(world, case):
     if case["n_experts"] % world:
         pytest.skip("experts do not divide")

@@ -24,8 +24,8 @@ for w in $WHAT; do case $w in
  timeline) timeout 300 python tools/timeline.py > $OUT/timeline_eager.txt 2>&1; echo "timeline rc=$?"; head -30 $OUT/timeline_eager.txt
       timeout 300 python tools/timeline.py --graph > $OUT/timeline_graph.txt 2>&1; head -30 $OUT/timeline_graph.txt ;;
  tl2) timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29513 tools/timeline.py --graph 2>&1 | grep -v "Warn\|warn\|\*\*\*\|OMP" | head -45 ;;
- tl2n) timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29515 tools/timeline.py --graph --no-overlap 2>&1 | grep -v "Warn\|warn\|\*\*\*\|OMP" | head -20 ;;
- tl4n) timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29516 tools/timeline.py --graph --no-overlap 2>&1 | grep -v "Warn\|warn\|\*\*\*\|OMP" | head -20 ;;
+ tl2n) timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29515 tools/timeline.py --graph --ce-dispatch 2>&1 | grep -v "Warn\|warn\|\*\*\*\|OMP" | head -20 ;;
+ tl4n) timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29516 tools/timeline.py --graph --ce-dispatch 2>&1 | grep -v "Warn\|warn\|\*\*\*\|OMP" | head -20 ;;
  tl4) timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29514 tools/timeline.py --graph 2>&1 | grep -v "Warn\|warn\|\*\*\*\|OMP" | head -45 ;;
  adamw) timeout 300 python tools/adamw_probe.py --gelems 2 > $OUT/adamw.txt 2>&1; cat $OUT/adamw.txt
       timeout 600 ncu --set full --clock-control none -k regex:"adamw_chunks|sumsq_chunks" --launch-skip 2 -c 2 -o $OUT/adamw_full python tools/adamw_probe.py --gelems 0.5 --steps 1 > $OUT/ncu_adamw.log 2>&1; echo "adamw ncu rc=$?" ;;

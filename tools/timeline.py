@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--tma-gather", action="store_true", help="TMA gather4 X operand instead of mlp_in rows")
     ap.add_argument("--fused", action="store_true", help="EP: the GEMM-fused combine (opt-in)")
     ap.add_argument("--no-overlap", action="store_true", help="EP: dX return after the wgrad GEMMs")
+    ap.add_argument("--ce-dispatch", action="store_true", help="EP: copy-engine all-gather of x (opt-in)")
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -47,6 +48,10 @@ def main():
     layer = b2.MoeLayer(ctx, cfg, torch.bfloat16, S)
     if args.graph:
         layer.set_graph(True)
+    if args.ce_dispatch:
+        import ctypes
+        b2.lib().b2x_moe_set_ce_dispatch.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        b2.lib().b2x_moe_set_ce_dispatch(layer.h, 1)
     if args.no_overlap:
         import ctypes
         b2.lib().b2x_moe_set_overlap_return.argtypes = [ctypes.c_void_p, ctypes.c_int]
