@@ -262,6 +262,8 @@ __global__ void __launch_bounds__(256) sumsq_chunks_kernel(const OptSeg* __restr
                                                            const OptChunk* __restrict__ chunks,
                                                            const int32_t* __restrict__ ids, int grad_dtype,
                                                            double* __restrict__ partials, int32_t* nonfinite) {
+    pdl_wait();
+    pdl_launch();
     __shared__ double red[256];
     const int cid = ids[blockIdx.x];
     const OptChunk ch = chunks[cid];
@@ -309,6 +311,8 @@ __global__ void __launch_bounds__(256) sumsq_chunks_kernel(const OptSeg* __restr
 
 __global__ void __launch_bounds__(1024) norm_final_kernel(const double* __restrict__ partials, int n,
                                                           double* __restrict__ out) {
+    pdl_wait();
+    pdl_launch();
     __shared__ double red[1024];
     const int per = (n + blockDim.x - 1) / blockDim.x;
     double s = 0.0;
@@ -326,6 +330,8 @@ __global__ void __launch_bounds__(256, MINB) adamw_chunks_kernel(const OptSeg* _
                                                            const int32_t* __restrict__ ids, int nids, AdamWDev c,
                                                            OptStepArgs a, const double* __restrict__ norm_sq,
                                                            const int32_t* __restrict__ nonfinite) {
+    pdl_wait();
+    pdl_launch();
     if (nonfinite && *nonfinite) return;
     double clip = 1.0;
     if (norm_sq) {
@@ -386,12 +392,12 @@ __global__ void nonfinite_scan_kernel(const void* __restrict__ g, int dtype, int
 void launch_sumsq_chunks(const OptSeg* segs, const OptChunk* chunks, const int32_t* ids, int nids, int grad_dtype,
                          double* partials, int32_t* nonfinite, cudaStream_t st) {
     if (nids <= 0) return;
-    sumsq_chunks_kernel<<<nids, 256, 0, st>>>(segs, chunks, ids, grad_dtype, partials, nonfinite);
+    launch_k(sumsq_chunks_kernel, dim3(nids), dim3(256), 0, st, segs, chunks, ids, grad_dtype, partials, nonfinite);
     B2_LAUNCH_CHECK();
 }
 
 void launch_norm_final(const double* partials, int n, double* norm_sq, cudaStream_t st) {
-    norm_final_kernel<<<1, 1024, 0, st>>>(partials, n, norm_sq);
+    launch_k(norm_final_kernel, dim3(1), dim3(1024), 0, st, partials, n, norm_sq);
     B2_LAUNCH_CHECK();
 }
 
@@ -420,8 +426,8 @@ void launch_adamw_chunks(const OptSeg* segs, const OptChunk* chunks, const int32
         grid_cap = sms * std::max(1, per_sm);
     }
     const int grid = std::min(nids, grid_cap);
-    if (minb == 3) adamw_chunks_kernel<3><<<grid, 256, 0, st>>>(segs, chunks, ids, nids, c, a, norm_sq, nonfinite);
-    else adamw_chunks_kernel<4><<<grid, 256, 0, st>>>(segs, chunks, ids, nids, c, a, norm_sq, nonfinite);
+    if (minb == 3) launch_k(adamw_chunks_kernel<3>, dim3(grid), dim3(256), 0, st, segs, chunks, ids, nids, c, a, norm_sq, nonfinite);
+    else launch_k(adamw_chunks_kernel<4>, dim3(grid), dim3(256), 0, st, segs, chunks, ids, nids, c, a, norm_sq, nonfinite);
     B2_LAUNCH_CHECK();
 }
 

@@ -6,6 +6,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 namespace b2 {
 
@@ -40,6 +41,40 @@ inline void check(bool cond, const std::string& msg) {
 #define B2_LAUNCH_CHECK() B2_CUDA(cudaGetLastError())
 
 enum DType : int { F32 = 0, BF16 = 1 };
+
+// ---- programmatic dependent launch (PDL) --------------------------------------------
+// Every hot-path kernel starts with pdl_wait() (griddepcontrol.wait: the previous kernel on
+// the stream has completed and its memory is visible) followed by pdl_launch() (lets the
+// next kernel be scheduled now). Kernels launched through launch_k() carry the programmatic
+// stream-serialisation attribute, so the next kernel's launch and prologue overlap this
+// one's tail; inside CUDA graphs these become programmatic edges. Without the attribute
+// both instructions are no-ops.
+__device__ __forceinline__ void pdl_wait() {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 900
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_launch() {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 900
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+bool pdl_enabled();  // B2_PDL=0 turns the attribute off (A/B checks)
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    B2_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 inline size_t dtype_size(int dt) { return dt == F32 ? 4 : 2; }
 

@@ -2,6 +2,7 @@
 #include "../../include/b2moe.h"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -92,6 +93,16 @@ struct b2_opt {
     b2_ctx* ctx;
     std::unique_ptr<ShardedOptimizer> opt;
 };
+
+namespace b2 {
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("B2_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+}  // namespace b2
 
 extern "C" {
 

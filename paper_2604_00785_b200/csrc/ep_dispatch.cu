@@ -27,6 +27,8 @@ template <typename T>
 __global__ void ep_gather_pull_kernel(const T* const* __restrict__ peer_src, int S, int T_tot, int H,
                                       const int32_t* __restrict__ cec, const int32_t* __restrict__ slot_prow,
                                       T* __restrict__ out) {
+    pdl_wait();
+    pdl_launch();
     const int lane = threadIdx.x % 32;
     const int nw = gridDim.x * blockDim.x / 32;
     for (int gid = (blockIdx.x * blockDim.x + threadIdx.x) / 32; gid < T_tot; gid += nw) {
@@ -70,6 +72,8 @@ __global__ void ep_combine_slots_kernel(const T* __restrict__ y, const int32_t* 
                                            const int32_t* __restrict__ selected_k, const int32_t* __restrict__ cec,
                                            const float* __restrict__ gw, int K, int S, int T_tot, int H, int me,
                                            T* const* __restrict__ peer_ret, T* __restrict__ local_out) {
+    pdl_wait();
+    pdl_launch();
     constexpr int V = 16 / sizeof(T);
     const int lane = threadIdx.x % 32;
     const int nw = gridDim.x * blockDim.x / 32;
@@ -140,6 +144,8 @@ __global__ void ep_combine_slots_kernel(const T* __restrict__ y, const int32_t* 
 template <typename T>
 __global__ void ep_pull_sum_kernel(const T* const* __restrict__ peer_slab, const int32_t* __restrict__ gi_local,
                                    int S, int K, int E, int NR, int W, int me, T* __restrict__ out) {
+    pdl_wait();
+    pdl_launch();
     const int t = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
     if (t >= S) return;
     unsigned mask = 0;
@@ -215,6 +221,8 @@ __global__ void ep_pull_sum_kernel(const T* const* __restrict__ peer_slab, const
 // row was stored by the owner's epilogue over NVLink before the barrier)
 template <typename T>
 __global__ void kslab_sum_kernel(const T* __restrict__ slab, int S, int K, int W, T* __restrict__ out) {
+    pdl_wait();
+    pdl_launch();
     const int t = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
     if (t >= S) return;
     constexpr int V = 16 / sizeof(T), MAXK = 8;
@@ -269,7 +277,7 @@ template <typename T>
 void launch_kslab_sum(const T* slab, int S, int K, int W, T* out, cudaStream_t st) {
     if (S <= 0) return;
     check(((int64_t)W * sizeof(T)) % 16 == 0, "kslab sum: rows must be 16-byte multiples");
-    kslab_sum_kernel<T><<<(unsigned)ceil_div(S, 8), 256, 0, st>>>(slab, S, K, W, out);
+    launch_k(kslab_sum_kernel<T>, dim3((unsigned)ceil_div(S, 8)), dim3(256), 0, st, slab, S, K, W, out);
     B2_LAUNCH_CHECK();
 }
 
@@ -279,6 +287,8 @@ void launch_kslab_sum(const T* slab, int S, int K, int W, T* out, cudaStream_t s
 // barriers in the same order, so the counts agree. Bounded spin: traps after ~20 s.
 __global__ void ep_flag_barrier_kernel(int* const* __restrict__ peer_flags, int* __restrict__ own_flags,
                                        int* __restrict__ epoch, int E, int me) {
+    pdl_wait();
+    pdl_launch();
     const int p = threadIdx.x;
     __shared__ int target;
     if (p == 0) target = *epoch + 1;
@@ -307,7 +317,7 @@ __global__ void ep_flag_barrier_kernel(int* const* __restrict__ peer_flags, int*
 
 void launch_ep_flag_barrier(int* const* peer_flags, int* own_flags, int* epoch, int E, int me, cudaStream_t st) {
     check(E <= 1024, "ep barrier: group too large");
-    ep_flag_barrier_kernel<<<1, std::max(32, (E + 31) / 32 * 32), 0, st>>>(peer_flags, own_flags, epoch, E, me);
+    launch_k(ep_flag_barrier_kernel, dim3(1), dim3(std::max(32, (E + 31) / 32 * 32)), 0, st, peer_flags, own_flags, epoch, E, me);
     B2_LAUNCH_CHECK();
 }
 
@@ -316,6 +326,8 @@ void launch_ep_flag_barrier(int* const* peer_flags, int* own_flags, int* epoch, 
 __global__ void ep_table_pull_kernel(const int32_t* const* __restrict__ peer_ids,
                                      const float* const* __restrict__ peer_w, int64_t n, int E,
                                      int32_t* __restrict__ ids_all, float* __restrict__ w_all) {
+    pdl_wait();
+    pdl_launch();
     const int64_t total = n * E;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int r = (int)(i / n);
@@ -328,7 +340,7 @@ __global__ void ep_table_pull_kernel(const int32_t* const* __restrict__ peer_ids
 void launch_ep_table_pull(const int32_t* const* peer_ids, const float* const* peer_w, int64_t n, int E,
                           int32_t* ids_all, float* w_all, cudaStream_t st) {
     if (n <= 0) return;
-    ep_table_pull_kernel<<<(unsigned)std::min<int64_t>(1184, ceil_div(n * E, 256)), 256, 0, st>>>(peer_ids, peer_w, n, E,
+    launch_k(ep_table_pull_kernel, dim3((unsigned)std::min<int64_t>(1184, ceil_div(n * E, 256))), dim3(256), 0, st, peer_ids, peer_w, n, E,
                                                                                                 ids_all, w_all);
     B2_LAUNCH_CHECK();
 }
@@ -339,7 +351,7 @@ template <typename T>
 void launch_ep_gather_pull(const T* const* peer_src, int S, int T_tot, int H, const int32_t* cec,
                            const int32_t* slot_prow, T* out, cudaStream_t st) {
     if (T_tot <= 0) return;
-    ep_gather_pull_kernel<T><<<ep_grid(T_tot), 256, 0, st>>>(peer_src, S, T_tot, H, cec, slot_prow, out);
+    launch_k(ep_gather_pull_kernel<T>, dim3(ep_grid(T_tot)), dim3(256), 0, st, peer_src, S, T_tot, H, cec, slot_prow, out);
     B2_LAUNCH_CHECK();
 }
 
@@ -348,7 +360,7 @@ void launch_ep_combine_local(const T* y, const int32_t* slot_prow, const int32_t
                              const float* gw, int K, int S, int T_tot, int H, T* own_slab, cudaStream_t st) {
     if (T_tot <= 0) return;
     check(((int64_t)H * sizeof(T)) % 16 == 0, "ep combine: rows must be 16-byte multiples");
-    ep_combine_slots_kernel<T><<<ep_grid(T_tot), 256, 0, st>>>(y, slot_prow, selected_k, cec, gw, K, S, T_tot, H,
+    launch_k(ep_combine_slots_kernel<T>, dim3(ep_grid(T_tot)), dim3(256), 0, st, y, slot_prow, selected_k, cec, gw, K, S, T_tot, H,
                                                                   0, nullptr, own_slab);
     B2_LAUNCH_CHECK();
 }
@@ -357,7 +369,7 @@ template <typename T>
 void launch_ep_pull_sum(const T* const* peer_slab, const int32_t* gi_local, int S, int K, int E, int NR, int W, int me,
                         T* out, cudaStream_t st) {
     if (S <= 0) return;
-    ep_pull_sum_kernel<T><<<(unsigned)ceil_div(S, 8), 256, 0, st>>>(peer_slab, gi_local, S, K, E, NR, W, me, out);
+    launch_k(ep_pull_sum_kernel<T>, dim3((unsigned)ceil_div(S, 8)), dim3(256), 0, st, peer_slab, gi_local, S, K, E, NR, W, me, out);
     B2_LAUNCH_CHECK();
 }
 

@@ -707,6 +707,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
     // per epilogue warp: [G/U input boxes (dgrad)] [SLOTS output boxes]; 1 KB aligned (bar0 is)
     const uint32_t epi_base = bar0 + 1024u;
 
+    pdl_launch();  // the next kernel may be scheduled (it waits for this grid's completion)
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
     const bool leader = rank == 0;
@@ -748,6 +749,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // PDL: the set-up above overlapped the previous kernel's tail; no global memory was
+    // touched yet. From here on the previous kernel's results are needed.
+    pdl_wait();
 
     const int32_t* ps = p.pad_start;
     const int ntiles = total_tiles<KIND, CG>(p, ps);
@@ -1120,13 +1124,15 @@ static void launch_kind(const Params& p, int grid, cudaStream_t st) {
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     B2_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<KIND, CG>, p));
 }
 

@@ -34,6 +34,8 @@ __device__ __forceinline__ int local_of(int e, int n_start, int nr) {
 __global__ void count_kernel(const int32_t* __restrict__ gidx, int T, int K, int N, int n_start, int nr,
                              int nchunks, int32_t* __restrict__ whist, int32_t* __restrict__ expert_counts,
                              int32_t* __restrict__ err) {
+    pdl_wait();
+    pdl_launch();
     extern __shared__ int32_t sh[];  // [kWarpsPerCta][nr]
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int chunk = blockIdx.x * kWarpsPerCta + w;
@@ -106,6 +108,8 @@ __global__ void __launch_bounds__(1024) scan_kernel(const int32_t* __restrict__ 
                                                     int32_t* __restrict__ cum_token_counts,
                                                     int32_t* __restrict__ pad_start,
                                                     int32_t* __restrict__ cum_expert_counts) {
+    pdl_wait();
+    pdl_launch();
     extern __shared__ int32_t tot[];  // [nr]
     __shared__ int wsum[32];
     const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nw = blockDim.x / 32;
@@ -160,6 +164,8 @@ __global__ void scatter_kernel(const int32_t* __restrict__ gidx, int T, int K, i
                                int32_t* __restrict__ input_indices, int32_t* __restrict__ output_indices,
                                int32_t* __restrict__ selected_k, int32_t* __restrict__ slot_prow,
                                int32_t* __restrict__ prow_src, int32_t* __restrict__ prow_k) {
+    pdl_wait();
+    pdl_launch();
     extern __shared__ int32_t sh[];  // carry [kWarpsPerCta][nr] (row offset inside the expert)
     const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int chunk = blockIdx.x * kWarpsPerCta + w;
@@ -202,6 +208,8 @@ __global__ void scatter_kernel(const int32_t* __restrict__ gidx, int T, int K, i
 // pad rows of each expert group read as zero tokens
 __global__ void pad_fill_kernel(const int32_t* __restrict__ token_counts, const int32_t* __restrict__ pad_start,
                                 int nr, int32_t* __restrict__ prow_src) {
+    pdl_wait();
+    pdl_launch();
     const int ln = blockIdx.x;
     const int b = pad_start[ln] + token_counts[ln], e = pad_start[ln + 1];
     for (int r = b + threadIdx.x; r < e; r += blockDim.x) prow_src[r] = -1;
@@ -212,22 +220,22 @@ void launch_routing_index(const RoutingIndexArgs& a, cudaStream_t st) {
     const int nblk = (int)ceil_div(std::max(nchunks, 1), kWarpsPerCta);
     const size_t smem = sizeof(int32_t) * kWarpsPerCta * a.nr;
     if (a.T > 0) {
-        count_kernel<<<nblk, 32 * kWarpsPerCta, smem, st>>>(a.gidx, a.T, a.K, a.N, a.n_start, a.nr, nchunks, a.whist,
+        launch_k(count_kernel, dim3(nblk), dim3(32 * kWarpsPerCta), smem, st, a.gidx, a.T, a.K, a.N, a.n_start, a.nr, nchunks, a.whist,
                                                             a.expert_counts, a.err);
         B2_LAUNCH_CHECK();
     }
-    scan_kernel<<<1, 1024, sizeof(int32_t) * a.nr, st>>>(a.whist, nchunks, a.nr, a.expert_counts, a.T, a.wbase,
+    launch_k(scan_kernel, dim3(1), dim3(1024), sizeof(int32_t) * a.nr, st, a.whist, nchunks, a.nr, a.expert_counts, a.T, a.wbase,
                                                          a.token_counts, a.cum_token_counts, a.pad_start,
                                                          a.cum_expert_counts);
     B2_LAUNCH_CHECK();
     if (a.T > 0) {
-        scatter_kernel<<<nblk, 32 * kWarpsPerCta, smem, st>>>(a.gidx, a.T, a.K, a.n_start, a.nr, nchunks, a.wbase,
+        launch_k(scatter_kernel, dim3(nblk), dim3(32 * kWarpsPerCta), smem, st, a.gidx, a.T, a.K, a.n_start, a.nr, nchunks, a.wbase,
                                                               a.cum_token_counts, a.pad_start, a.cum_expert_counts,
                                                               a.input_indices, a.output_indices, a.selected_k,
                                                               a.slot_prow, a.prow_src, a.prow_k);
         B2_LAUNCH_CHECK();
     }
-    pad_fill_kernel<<<a.nr, 128, 0, st>>>(a.token_counts, a.pad_start, a.nr, a.prow_src);
+    launch_k(pad_fill_kernel, dim3(a.nr), dim3(128), 0, st, a.token_counts, a.pad_start, a.nr, a.prow_src);
     B2_LAUNCH_CHECK();
 }
 

@@ -73,6 +73,8 @@ struct V16 {
 template <typename T>
 __global__ void gather_rows_kernel(const T* __restrict__ x, const int32_t* __restrict__ prow_src,
                                    const int32_t* __restrict__ p_total, T* __restrict__ out, int H, int64_t pmax) {
+    pdl_wait();
+    pdl_launch();
     const int64_t P = min((int64_t)*p_total, pmax);
     const int lane = threadIdx.x % 32;
     const int64_t warps = (int64_t)gridDim.x * blockDim.x / 32;
@@ -98,6 +100,8 @@ __global__ void gather_rows_kernel(const T* __restrict__ x, const int32_t* __res
 template <typename T>
 __global__ void zero_pad_rows_kernel(T* __restrict__ buf, const int32_t* __restrict__ prow_src,
                                      const int32_t* __restrict__ p_total, int W, int64_t pmax) {
+    pdl_wait();
+    pdl_launch();
     const int64_t P = min((int64_t)*p_total, pmax);
     const int lane = threadIdx.x % 32;
     const int64_t warps = (int64_t)gridDim.x * blockDim.x / 32;
@@ -113,6 +117,8 @@ template <typename T>
 __global__ void combine_kernel(const T* __restrict__ y, const int32_t* __restrict__ slot_prow,
                                const int32_t* __restrict__ selected_k, const int32_t* __restrict__ cum_expert_counts,
                                const float* __restrict__ gw, T* __restrict__ out, int T_tok, int H, int K) {
+    pdl_wait();
+    pdl_launch();
     const int t = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
     if (t >= T_tok) return;
     const int j0 = cum_expert_counts[t], j1 = cum_expert_counts[t + 1];
@@ -196,6 +202,8 @@ __global__ void __launch_bounds__(256, 3) out_reduction_bwd_kernel(const T* __re
                                          const int32_t* __restrict__ slot_prow, const int32_t* __restrict__ selected_k,
                                          const int32_t* __restrict__ cum_expert_counts, const float* __restrict__ gw,
                                          T* __restrict__ dy, float* __restrict__ wgrad, int T_tok, int H, int K) {
+    pdl_wait();
+    pdl_launch();
     const int t = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
     if (t >= T_tok) return;
     const int j0 = cum_expert_counts[t], j1 = cum_expert_counts[t + 1];
@@ -405,7 +413,7 @@ template <typename T>
 void launch_gather_rows(const T* x, const int32_t* prow_src, const int32_t* p_total, T* out, int H, int64_t pmax,
                         cudaStream_t st) {
     if (pmax <= 0) return;
-    gather_rows_kernel<T><<<grid_for_rows(pmax), 256, 0, st>>>(x, prow_src, p_total, out, H, pmax);
+    launch_k(gather_rows_kernel<T>, dim3(grid_for_rows(pmax)), dim3(256), 0, st, x, prow_src, p_total, out, H, pmax);
     B2_LAUNCH_CHECK();
 }
 
@@ -413,7 +421,7 @@ template <typename T>
 void launch_zero_pad_rows(T* buf, const int32_t* prow_src, const int32_t* p_total, int W, int64_t pmax,
                           cudaStream_t st) {
     if (pmax <= 0) return;
-    zero_pad_rows_kernel<T><<<grid_for_rows(pmax), 256, 0, st>>>(buf, prow_src, p_total, W, pmax);
+    launch_k(zero_pad_rows_kernel<T>, dim3(grid_for_rows(pmax)), dim3(256), 0, st, buf, prow_src, p_total, W, pmax);
     B2_LAUNCH_CHECK();
 }
 
@@ -421,7 +429,7 @@ template <typename T>
 void launch_combine(const T* y, const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec,
                     const float* gw, T* out, int T_tok, int H, int K, cudaStream_t st) {
     if (T_tok <= 0) return;
-    combine_kernel<T><<<(unsigned)ceil_div(T_tok, 8), 256, 0, st>>>(y, slot_prow, selected_k, cec, gw, out, T_tok, H, K);
+    launch_k(combine_kernel<T>, dim3((unsigned)ceil_div(T_tok, 8)), dim3(256), 0, st, y, slot_prow, selected_k, cec, gw, out, T_tok, H, K);
     B2_LAUNCH_CHECK();
 }
 
@@ -430,7 +438,7 @@ void launch_out_reduction_bwd(const T* dout, const T* const* peer_dout, int s_lo
                               const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec, const float* gw,
                               T* dy, float* wgrad, int T_tok, int H, int K, cudaStream_t st) {
     if (T_tok <= 0) return;
-    out_reduction_bwd_kernel<T><<<(unsigned)ceil_div(T_tok, 8), 256, 0, st>>>(dout, peer_dout, s_local, y, slot_prow,
+    launch_k(out_reduction_bwd_kernel<T>, dim3((unsigned)ceil_div(T_tok, 8)), dim3(256), 0, st, dout, peer_dout, s_local, y, slot_prow,
                                                                                selected_k, cec, gw, dy, wgrad, T_tok,
                                                                                H, K);
     B2_LAUNCH_CHECK();

@@ -26,6 +26,8 @@ constexpr int kRtTok = 64, kRtExp = 64, kRtP = 32, kRtXs = kRtTok + 4;
 template <typename T>
 __global__ void __launch_bounds__(128) router_logits_kernel(const T* __restrict__ x, const T* __restrict__ w,
                                                             float* __restrict__ logits, int S, int H, int N) {
+    pdl_wait();
+    pdl_launch();
     __shared__ __align__(16) float xs[2][kRtP][kRtXs];
     __shared__ __align__(16) float ws[2][kRtP][kRtExp];
     const int t0 = blockIdx.x * kRtTok, e0 = blockIdx.y * kRtExp;
@@ -176,6 +178,8 @@ __device__ __forceinline__ void cp_async_wait() {
 __global__ void __launch_bounds__(128) router_logits_bf16_kernel(const __nv_bfloat16* __restrict__ x,
                                                                  const __nv_bfloat16* __restrict__ w,
                                                                  float* __restrict__ logits, int S, int H, int N) {
+    pdl_wait();
+    pdl_launch();
     extern __shared__ __align__(128) uint8_t l2_smem[];
     LogitsSmem& sm = *reinterpret_cast<LogitsSmem*>(l2_smem);
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
@@ -315,6 +319,8 @@ template <int NPL>
 __global__ void __launch_bounds__(256) softmax_topk_kernel(const float* __restrict__ logits, float* __restrict__ probs,
                                                            float* __restrict__ topw, int32_t* __restrict__ topi, int S,
                                                            int N, int K, int normalize) {
+    pdl_wait();
+    pdl_launch();
     __shared__ double es[8][32 * NPL];
     const int wib = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int warp = blockIdx.x * 8 + wib;
@@ -387,6 +393,8 @@ __global__ void __launch_bounds__(256) softmax_topk_kernel(const float* __restri
 
 // forced uniform routing (moe.hpp:84-99): expert (t*K+j) mod N, weight 1/K
 __global__ void fur_route_kernel(float* __restrict__ w, int32_t* __restrict__ idx, int S, int N, int K) {
+    pdl_wait();
+    pdl_launch();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (int64_t)S * K) return;
     const int64_t t = i / K, k = i % K;
@@ -399,6 +407,8 @@ __global__ void fur_route_kernel(float* __restrict__ w, int32_t* __restrict__ id
 
 __global__ void prob_colsum_partial_kernel(const float* __restrict__ probs, float* __restrict__ partial,
                                            int S, int N, int rows_per_block) {
+    pdl_wait();
+    pdl_launch();
     const int r0 = blockIdx.x * rows_per_block;
     for (int e = threadIdx.x; e < N; e += blockDim.x) {
         float acc = 0.f;
@@ -410,6 +420,8 @@ __global__ void prob_colsum_partial_kernel(const float* __restrict__ probs, floa
 
 __global__ void prob_colsum_final_kernel(const float* __restrict__ partial, float* __restrict__ mean_probs,
                                          int nparts, int N, int S) {
+    pdl_wait();
+    pdl_launch();
     for (int e = threadIdx.x; e < N; e += blockDim.x) {
         float acc = 0.f;
         for (int b = 0; b < nparts; ++b) acc += partial[(int64_t)b * N + e];
@@ -418,6 +430,8 @@ __global__ void prob_colsum_final_kernel(const float* __restrict__ partial, floa
 }
 
 __global__ void sel_count_kernel(const int32_t* __restrict__ idx, int64_t n, int32_t* __restrict__ sel, int N) {
+    pdl_wait();
+    pdl_launch();
     extern __shared__ int32_t hist[];
     for (int e = threadIdx.x; e < N; e += blockDim.x) hist[e] = 0;
     __syncthreads();
@@ -438,6 +452,8 @@ __global__ void router_dlogits_kernel(const float* __restrict__ probs, const flo
                                       const float* __restrict__ aux_grad /*[S,N] or null*/,
                                       float* __restrict__ dlogits, __nv_bfloat16* __restrict__ dl_bf16, int S,
                                       int N, int K, int normalize, int fur) {
+    pdl_wait();
+    pdl_launch();
     const int row = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
     if (row >= S) return;
     float dp[kMaxExpertsPerLane], pr[kMaxExpertsPerLane];
@@ -491,6 +507,8 @@ __global__ void router_dlogits_kernel(const float* __restrict__ probs, const flo
 // aux-loss probability gradient (moe.hpp:331-342): coeff*N*f_e/S in every row
 __global__ void aux_probs_grad_kernel(const int32_t* __restrict__ sel, float* __restrict__ out, int S, int N,
                                       double coeff, double total) {
+    pdl_wait();
+    pdl_launch();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (int64_t)S * N) return;
     const int e = (int)(i % N);
@@ -550,6 +568,8 @@ __global__ void __launch_bounds__(128) router_dw_partial_kernel(const T* __restr
 
 template <typename T>
 __global__ void router_dw_reduce_kernel(const float* __restrict__ part, T* __restrict__ dw, int nsplit, int64_t n) {
+    pdl_wait();
+    pdl_launch();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float acc = 0.f;
@@ -571,13 +591,13 @@ void launch_router_logits(const T* x, const T* w, float* logits, int S, int H, i
                 attr = true;
             }
             dim3 grid((unsigned)ceil_div(S, kL2Tok), (unsigned)ceil_div(N, kL2Exp));
-            router_logits_bf16_kernel<<<grid, 128, sizeof(LogitsSmem), st>>>(x, w, logits, S, H, N);
+            launch_k(router_logits_bf16_kernel, dim3(grid), dim3(128), sizeof(LogitsSmem), st, x, w, logits, S, H, N);
             B2_LAUNCH_CHECK();
             return;
         }
     }
     dim3 grid((unsigned)ceil_div(S, kRtTok), (unsigned)ceil_div(N, kRtExp));
-    router_logits_kernel<T><<<grid, 128, 0, st>>>(x, w, logits, S, H, N);
+    launch_k(router_logits_kernel<T>, dim3(grid), dim3(128), 0, st, x, w, logits, S, H, N);
     B2_LAUNCH_CHECK();
 }
 template void launch_router_logits<float>(const float*, const float*, float*, int, int, int, cudaStream_t);
@@ -590,16 +610,16 @@ void launch_softmax_topk(const float* logits, float* probs, float* topw, int32_t
     if (S == 0) return;
     const unsigned grid = (unsigned)ceil_div(S, 8);  // 8 warps (tokens) per block
     const int nm = normalize ? 1 : 0;
-    if (N <= 64) softmax_topk_kernel<2><<<grid, 256, 0, st>>>(logits, probs, topw, topi, S, N, K, nm);
-    else if (N <= 128) softmax_topk_kernel<4><<<grid, 256, 0, st>>>(logits, probs, topw, topi, S, N, K, nm);
-    else softmax_topk_kernel<8><<<grid, 256, 0, st>>>(logits, probs, topw, topi, S, N, K, nm);
+    if (N <= 64) launch_k(softmax_topk_kernel<2>, dim3(grid), dim3(256), 0, st, logits, probs, topw, topi, S, N, K, nm);
+    else if (N <= 128) launch_k(softmax_topk_kernel<4>, dim3(grid), dim3(256), 0, st, logits, probs, topw, topi, S, N, K, nm);
+    else launch_k(softmax_topk_kernel<8>, dim3(grid), dim3(256), 0, st, logits, probs, topw, topi, S, N, K, nm);
     B2_LAUNCH_CHECK();
 }
 
 void launch_fur_route(float* w, int32_t* idx, int S, int N, int K, cudaStream_t st) {
     const int64_t n = (int64_t)S * K;
     if (n == 0) return;
-    fur_route_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(w, idx, S, N, K);
+    launch_k(fur_route_kernel, dim3((unsigned)ceil_div(n, 256)), dim3(256), 0, st, w, idx, S, N, K);
     B2_LAUNCH_CHECK();
 }
 
@@ -609,15 +629,15 @@ void launch_aux_stats(const float* probs, int S, int N, const int32_t* gidx, int
     if (S > 0) {
         const int rpb = 128;
         const int nparts = (int)ceil_div(S, rpb);
-        prob_colsum_partial_kernel<<<nparts, 128, 0, st>>>(probs, partial, S, N, rpb);
+        launch_k(prob_colsum_partial_kernel, dim3(nparts), dim3(128), 0, st, probs, partial, S, N, rpb);
         B2_LAUNCH_CHECK();
-        prob_colsum_final_kernel<<<1, 256, 0, st>>>(partial, mean_probs, nparts, N, S);
+        launch_k(prob_colsum_final_kernel, dim3(1), dim3(256), 0, st, partial, mean_probs, nparts, N, S);
         B2_LAUNCH_CHECK();
     } else {
         B2_CUDA(cudaMemsetAsync(mean_probs, 0, sizeof(float) * N, st));
     }
     if (n_gidx > 0) {
-        sel_count_kernel<<<(unsigned)std::min<int64_t>(148, ceil_div(n_gidx, 256)), 256, sizeof(int32_t) * N, st>>>(
+        launch_k(sel_count_kernel, dim3((unsigned)std::min<int64_t>(148, ceil_div(n_gidx, 256))), dim3(256), sizeof(int32_t) * N, st, 
             gidx, n_gidx, sel, N);
         B2_LAUNCH_CHECK();
     }
@@ -627,7 +647,7 @@ void launch_router_dlogits(const float* probs, const float* wgrad, const int32_t
                            const float* aux_grad, float* dlogits, void* dl_bf16, int S, int N, int K, bool normalize,
                            bool fur, cudaStream_t st) {
     if (S == 0) return;
-    router_dlogits_kernel<<<(unsigned)ceil_div(S, 8), 256, 0, st>>>(probs, wgrad, topi, topw, aux_grad, dlogits,
+    launch_k(router_dlogits_kernel, dim3((unsigned)ceil_div(S, 8)), dim3(256), 0, st, probs, wgrad, topi, topw, aux_grad, dlogits,
                                                                       (__nv_bfloat16*)dl_bf16, S, N, K,
                                                                       normalize ? 1 : 0, fur ? 1 : 0);
     B2_LAUNCH_CHECK();
@@ -637,7 +657,7 @@ void launch_aux_probs_grad(const int32_t* sel, float* out, int S, int N, double 
                            cudaStream_t st) {
     const int64_t n = (int64_t)S * N;
     if (n == 0) return;
-    aux_probs_grad_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(sel, out, S, N, coeff, total);
+    launch_k(aux_probs_grad_kernel, dim3((unsigned)ceil_div(n, 256)), dim3(256), 0, st, sel, out, S, N, coeff, total);
     B2_LAUNCH_CHECK();
 }
 
@@ -652,12 +672,12 @@ void launch_router_dw(const T* x, const float* dlogits, T* dw, float* part, int 
     router_dw_partial_kernel<T><<<grid, 128, 0, st>>>(x, dlogits, part, S, H, N, rows);
     B2_LAUNCH_CHECK();
     const int64_t n = (int64_t)H * N;
-    router_dw_reduce_kernel<T><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(part, dw, nsplit, n);
+    launch_k(router_dw_reduce_kernel<T>, dim3((unsigned)ceil_div(n, 256)), dim3(256), 0, st, part, dw, nsplit, n);
     B2_LAUNCH_CHECK();
 }
 void launch_router_dw_reduce_bf16(const float* part, void* dw, int nsplit, int64_t n, cudaStream_t st) {
     if (n <= 0) return;
-    router_dw_reduce_kernel<__nv_bfloat16><<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(part, (__nv_bfloat16*)dw, nsplit, n);
+    launch_k(router_dw_reduce_kernel<__nv_bfloat16>, dim3((unsigned)ceil_div(n, 256)), dim3(256), 0, st, part, (__nv_bfloat16*)dw, nsplit, n);
     B2_LAUNCH_CHECK();
 }
 

@@ -29,6 +29,7 @@ for w in $WHAT; do case $w in
  tl4) timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29514 tools/timeline.py --graph 2>&1 | grep -v "Warn\|warn\|\*\*\*\|OMP" | head -45 ;;
  adamw) timeout 300 python tools/adamw_probe.py --gelems 2 > $OUT/adamw.txt 2>&1; cat $OUT/adamw.txt
       timeout 600 ncu --set full --clock-control none -k regex:"adamw_chunks|sumsq_chunks" --launch-skip 2 -c 2 -o $OUT/adamw_full python tools/adamw_probe.py --gelems 0.5 --steps 1 > $OUT/ncu_adamw.log 2>&1; echo "adamw ncu rc=$?" ;;
+ pdl) for i in 1 2; do for v in 1 0; do echo "== B2_PDL=$v"; B2_PDL=$v timeout 300 python tools/timeline.py --graph 2>&1 | grep -E "event-timed|span"; done; done ;;
  ab) for opt in "--graph" "--graph --tma-gather"; do echo "== timeline $opt"; timeout 300 python tools/timeline.py $opt 2>&1 | grep -v Warn | head -24; done ;;
  gtest) timeout 600 python -m pytest tests -m gpu -x -q -k "${GTEST_K}" > $OUT/gtest.log 2>&1; echo "gtest rc=$?"; tail -15 $OUT/gtest.log ;;
  ep4) timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29512 \
