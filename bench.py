@@ -215,9 +215,12 @@ def mula7b_param_set(ep=1):
     return slots
 
 
-def bench_adamw(torch, b2, ctx, dev, steps, warmup, world, rank, hbm_peak):
+def bench_adamw(torch, b2, ctx, dev, steps, warmup, world, rank, hbm_peak, dp=1):
+    """EPSO step on the Mula-7B-A1B set. dp=1: DP=1 x EP=world (the EP axis, strong scaling);
+    dp=world: DP=world x EP=1 (the DP axis: every rank holds all experts, expert grads are
+    reduce-scattered too — NVLink-bound by construction)."""
     assert sum(n for n, _, _ in mula7b_param_set()) == 6_919_096_320
-    per_rank = mula7b_param_set(world)  # EPSO at DP=1, EP=world: strong scaling over the same 6.92B set
+    per_rank = mula7b_param_set(world // dp)
     total = 6_919_096_320
     gen = torch.Generator(device=dev).manual_seed(11)
     weights = [(torch.randn(n, device=dev, generator=gen, dtype=torch.float32) * 0.02).bfloat16()
@@ -257,8 +260,16 @@ def bench_adamw(torch, b2, ctx, dev, steps, warmup, world, rank, hbm_peak):
             k = json.load(f)["kernels"]
         per_elem = sum(v["dram_bytes"] for v in k.values()) / 0.5e9
         traffic = per_elem * owned
+    # NVLink bytes per rank (bf16 reduce-scatter + all-gather) and the roofline time
+    # HBM term + NVLink term at ~85 % of 900 GB/s per direction
+    ep = world // dp
+    exp_el = sum(n for n, e, _ in per_rank if e)
+    ne_el = sum(n for n, e, _ in per_rank if not e)
+    nvl = 2 * 2 * exp_el * (dp - 1) / dp + 2 * 2 * ne_el * (world - 1) / world
+    t_roof = byt / (hbm_peak * 1e9) * 1e3 + nvl / 765e9 * 1e3
     return {"metric": "sharded AdamW step ms (EPSO, Mula-7B-A1B param set, bf16 grads/weights, fp32 state)",
-            "parallelism": f"dp1 x ep{world}", "scaling": "strong",
+            "parallelism": f"dp{dp} x ep{ep}", "scaling": "strong",
+            "nvlink_bytes_per_rank": nvl, "t_roofline_ms": t_roof, "roofline_over_measured": t_roof / ms,
             "ms": ms, "params": total, "owned_params_per_rank": owned, "launches_per_step": launches,
             "grad_norm": st["grad_norm"],
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
@@ -483,9 +494,15 @@ def main():
     zipf = None
     if args.zipf > 0:
         zipf = bench_zipf(torch, b2, ctx, dev, stream, world, rank, args.zipf, max(2, args.steps // 2), 2)
-    adamw = None
+    adamw = adamw_dp = None
     if not args.no_adamw:
         adamw = bench_adamw(torch, b2, ctx, dev, 5, 2, world, rank, hbm_peak)
+        if world > 1:  # the DP axis of config D on its own communicators
+            ids = [b2.Context.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(ids, src=0)
+            ctx_dp = b2.Context(local, rank=rank, dp=world, ep=1, nccl_id=ids[0], stream=stream)
+            adamw_dp = bench_adamw(torch, b2, ctx_dp, dev, 3, 1, world, rank, hbm_peak, dp=world)
+            ctx_dp.close()
 
     cpu = None
     os.sched_setaffinity(0, all_cpus)  # the CPU reference leg may use every host core
@@ -526,6 +543,7 @@ def main():
             "gpu_launches": launches,
             "clocks": clk,
             "adamw": adamw,
+            "adamw_dp_axis": adamw_dp,
             "zipf": zipf,
             "cpu_baseline": cpu,
         }
