@@ -30,6 +30,7 @@ extern "C" {
 #define B2_ERR_CONFIG 2
 #define B2_ERR_CUDA 3
 #define B2_ERR_NCCL 4
+#define B2_ERR_IO 5 /* optimus::IoError: record files (reliability.cpp:272-280) */
 
 #define B2_F32 0
 #define B2_BF16 1
@@ -187,6 +188,53 @@ int b2_opt_set_step_count(b2_opt* o, int64_t n);
  * `loss` or in this rank's LOCAL gradients -> max over WORLD of (node + 1); *sick =
  * the highest sick node, or -1. Collective over WORLD; synchronises. */
 int b2_opt_detect_soft_failure(b2_opt* o, double loss, int node, int* sick);
+
+/* ---- sharded checkpoint record files ----
+ * Format of the reference's record file (reliability.hpp:33-70, reliability.cpp:23-31):
+ * "OPTT", u32 version 1, u32 count, per record {u32 name length, name, u32 dtype, u32 ndim,
+ * u64 dims, little-endian payload}, u32 crc32 (zlib) of everything before it. Payloads
+ * come from / go to DEVICE memory; their crc32 is computed on the GPU. */
+#define B2_REC_F32 0  /* RecDtype::f32 */
+#define B2_REC_BF16 1 /* RecDtype::bf16 */
+typedef struct b2_rec_writer b2_rec_writer;
+typedef struct b2_rec_file b2_rec_file;
+/* zlib crc32(crc_in, bytes) of n DEVICE bytes (crc_in 0 starts a new checksum); synchronises */
+int b2_crc32(b2_ctx* ctx, const void* dev, int64_t n, uint32_t crc_in, uint32_t* crc_out);
+/* RecordFileWriter (reliability.hpp:47-71, reliability.cpp:222-270) */
+int b2_rec_writer_open(b2_ctx* ctx, const char* path, b2_rec_writer** out);
+/* add_f32 / add_bf16: prod(dims) elements of src_dtype (B2_F32 / B2_BF16) at DEVICE
+ * pointer src; a B2_F32 source of a B2_REC_BF16 record rounds to nearest even
+ * (common.hpp:116-122). Streams the payload to the file; synchronises. */
+int b2_rec_writer_add(b2_rec_writer* w, const char* name, int rec_dtype, const int64_t* dims, int ndim,
+                      const void* src, int src_dtype);
+/* writes the header count and the crc footer, fsyncs; frees w (also on error) */
+int b2_rec_writer_finish(b2_rec_writer* w, int64_t* bytes, uint32_t* crc);
+/* read_record_file (reliability.cpp:272-320): validates magic, version, crc and every
+ * record bound (B2_ERR_IO with the reference's message otherwise) */
+int b2_rec_file_open(b2_ctx* ctx, const char* path, b2_rec_file** out);
+int b2_rec_file_count(b2_rec_file* f, int* count);
+/* record i: name (NUL-terminated, truncated to name_cap), dtype, dims (up to 8) */
+int b2_rec_file_info(b2_rec_file* f, int i, char* name, int name_cap, int* rec_dtype, int64_t* dims, int* ndim);
+int b2_rec_file_find(b2_rec_file* f, const char* name, int* index); /* -1 when absent */
+/* elements [begin, end) of record i into DEVICE memory of dst_dtype (bf16 -> f32 widens) */
+int b2_rec_file_read(b2_rec_file* f, int i, int64_t begin, int64_t end, void* dst, int dst_dtype);
+int b2_rec_file_close(b2_rec_file* f);
+/* write_state_dir's shard file (reliability.cpp:402-460): assembles the FULL master/m/v
+ * of every parameter over its owning group (collective on those groups) and, on the rank
+ * that is its model shard's scattered_writer (reliability.cpp:322-328), writes
+ * <dir>/shard-<m>.bin with records <name>.w16 [, .master, .m, .v, .g16] for every
+ * parameter the shard stores (expert, or ep coordinate 0). names[p]: record prefix;
+ * dims: the shapes concatenated, ndims[p] entries each (dims NULL -> {numel}).
+ * full = 0: weights only. *bytes / *crc = 0 on non-writers; *model_shard = m. */
+int b2_opt_write_shard(b2_opt* o, const char* dir, const char* const* names, const int64_t* dims,
+                       const int* ndims, int full, int64_t* bytes, uint32_t* crc, int* model_shard);
+/* restore_full's per-parameter loop (reliability.cpp:623-675): weights (and with full:
+ * this rank's owned master/m/v slice and the grads) from the shard files in dir; every
+ * rank reads its own files, no collective. The step count comes from the manifest
+ * (b2_opt_set_step_count). */
+int b2_opt_restore_shard(b2_opt* o, const char* dir, const char* const* names, const int64_t* dims,
+                         const int* ndims, int full);
+
 /* adamw_update (optim.cpp:88-107) on device slices */
 int b2_adamw_update(b2_ctx* ctx, float* master, float* exp_avg, float* exp_avg_sq, const void* grad,
                     int grad_dtype, int64_t n, double lr, int64_t step, const b2_adamw_cfg* cfg, void* weight_out,

@@ -254,6 +254,51 @@ class Oracle:
         return dict(weights=w_out, master=master, m=m, v=v, owned=owned, stats=stats, state_bytes=sb)
 
 
+    # ---- record files (reliability.hpp:33-70, reliability.cpp:222-320) ----
+    def record_file_write(self, path, records):
+        """records: [(name, rec_dtype 0|1, dims, f32 array)] -> (bytes, crc) of the file at path."""
+        names = b"".join(n.encode() + b"\0" for n, _, _, _ in records)
+        dts = np.array([d for _, d, _, _ in records], np.int32)
+        nds = np.array([len(s) for _, _, s, _ in records], np.int32)
+        dims = np.array([x for _, _, s, _ in records for x in s] or [0], np.int64)
+        data = np.concatenate([np.asarray(a, np.float32).ravel() for *_, a in records] or
+                              [np.zeros(1, np.float32)])
+        n = len(records)
+        if self.which == "orc":
+            f = self._f("record_file_bytes")
+            f.restype = I64
+            args = (n, names, _p(dts), _p(nds), _p(dims), _p(data))
+            size = f(*args, None)
+            if size < 0:
+                self._check(1)
+            out = np.zeros(size, np.uint8)
+            f(*args, _p(out))
+            with open(path, "wb") as fh:
+                fh.write(out.tobytes())
+            return int(size), int.from_bytes(out[-4:].tobytes(), "little")
+        b, c = I64(), C.c_uint32()
+        self._check(self._f("record_file_write")(path.encode(), n, names, _p(dts), _p(nds), _p(dims), _p(data),
+                                                 C.byref(b), C.byref(c)))
+        return b.value, c.value
+
+    def record_file_read(self, path):
+        """read_record_file -> (count, all records widened to f32 and concatenated);
+        raises RuntimeError with the reference's message on an invalid file."""
+        cnt, tot = I64(), I64()
+        if self.which == "orc":
+            raw = np.fromfile(path, np.uint8)
+            f = self._f("record_file_parse")
+            self._check(f(_p(raw), I64(raw.size), C.byref(cnt), C.byref(tot), None, I64(0)))
+            out = np.zeros(max(tot.value, 1), np.float32)
+            self._check(f(_p(raw), I64(raw.size), C.byref(cnt), C.byref(tot), _p(out), I64(out.size)))
+        else:
+            f = self._f("record_file_read")
+            self._check(f(path.encode(), C.byref(cnt), C.byref(tot), None, I64(0)))
+            out = np.zeros(max(tot.value, 1), np.float32)
+            self._check(f(path.encode(), C.byref(cnt), C.byref(tot), _p(out), I64(out.size)))
+        return cnt.value, out[:tot.value]
+
+
 _CACHE: dict = {}
 
 

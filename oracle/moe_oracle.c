@@ -553,3 +553,121 @@ int orc_sharded_steps(int DP, int EP, int TP, int mode, const orc_adamw_cfg* c, 
     free(upd);
     return 0;
 }
+
+/* ---- record files (reliability.hpp:33-70, reliability.cpp:23-320) -------------------------
+ * Layout: "OPTT", u32 version 1, u32 count, per record {u32 name length, name, u32 dtype
+ * (0 f32, 1 bf16), u32 ndim, u64 dims, payload LE}, then u32 zlib crc32 of all of it.
+ * Records are given as NUL-separated names plus f32 data, all records concatenated;
+ * bf16 records round with orc_f32_to_bf16_bits (RecordFileWriter::add_bf16, 238-253). */
+
+uint32_t orc_crc32(uint32_t crc, const uint8_t* p, int64_t n) { /* zlib crc32, bitwise */
+    uint32_t r = ~crc;
+    for (int64_t i = 0; i < n; ++i) {
+        r ^= p[i];
+        for (int b = 0; b < 8; ++b) r = (r & 1u) ? (r >> 1) ^ 0xEDB88320u : r >> 1;
+    }
+    return ~r;
+}
+
+static void put_le(uint8_t* out, int64_t* at, uint64_t v, int bytes) {
+    for (int i = 0; i < bytes; ++i) {
+        if (out) out[*at] = (uint8_t)((v >> (8 * i)) & 0xff);
+        ++*at;
+    }
+}
+static uint64_t get_le(const uint8_t* b, int bytes) {
+    uint64_t v = 0;
+    for (int i = 0; i < bytes; ++i) v |= (uint64_t)b[i] << (8 * i);
+    return v;
+}
+
+/* serialise into out (NULL: size query); returns the file size, or -1 on a bad record */
+int64_t orc_record_file_bytes(int n_rec, const char* names, const int32_t* dtypes, const int32_t* ndims,
+                              const int64_t* dims, const float* data, uint8_t* out) {
+    int64_t at = 0, di = 0, de = 0;
+    const char magic[4] = {'O', 'P', 'T', 'T'};
+    for (int i = 0; i < 4; ++i) put_le(out, &at, (uint8_t)magic[i], 1);
+    put_le(out, &at, 1, 4);
+    put_le(out, &at, (uint64_t)n_rec, 4);
+    for (int r = 0; r < n_rec; ++r) {
+        const size_t len = strlen(names);
+        put_le(out, &at, len, 4);
+        for (size_t c = 0; c < len; ++c) put_le(out, &at, (uint8_t)names[c], 1);
+        names += len + 1;
+        if (dtypes[r] < 0 || dtypes[r] > 1 || ndims[r] < 0 || ndims[r] > 8) {
+            strcpy(g_err, "record: bad dtype or rank");
+            return -1;
+        }
+        put_le(out, &at, (uint64_t)dtypes[r], 4);
+        put_le(out, &at, (uint64_t)ndims[r], 4);
+        int64_t n = 1;
+        for (int d = 0; d < ndims[r]; ++d) {
+            if (dims[di] < 0) {
+                strcpy(g_err, "record: negative dimension");
+                return -1;
+            }
+            n *= dims[di];
+            put_le(out, &at, (uint64_t)dims[di++], 8);
+        }
+        for (int64_t e = 0; e < n; ++e, ++de) {
+            if (dtypes[r] == 0) {
+                uint32_t u;
+                memcpy(&u, &data[de], 4);
+                put_le(out, &at, u, 4);
+            } else {
+                put_le(out, &at, orc_f32_to_bf16_bits(data[de]), 2);
+            }
+        }
+    }
+    const int64_t body = at;
+    put_le(out, &at, out ? orc_crc32(0, out, body) : 0, 4);
+    return at;
+}
+
+/* read_record_file: 0 and the record count / total elements (data_out: the records
+ * widened to f32 and concatenated, cap elements) or 1 with the reference's message */
+int orc_record_file_parse(const uint8_t* b, int64_t size, int64_t* count, int64_t* total, float* data_out,
+                          int64_t cap) {
+#define BAD(msg)                \
+    do {                        \
+        strcpy(g_err, msg);     \
+        return 1;               \
+    } while (0)
+    if (size < 16) BAD("truncated header");
+    if (memcmp(b, "OPTT", 4) != 0) BAD("bad magic");
+    if (get_le(b + 4, 4) != 1) BAD("unsupported version");
+    if (orc_crc32(0, b, size - 4) != (uint32_t)get_le(b + size - 4, 4)) BAD("checksum mismatch");
+    const uint32_t cnt = (uint32_t)get_le(b + 8, 4);
+    const int64_t end = size - 4;
+    int64_t off = 12, tot = 0;
+    for (uint32_t r = 0; r < cnt; ++r) {
+        if (end - off < 4) BAD("truncated record");
+        const uint32_t name_len = (uint32_t)get_le(b + off, 4);
+        off += 4;
+        if (name_len > 4096) BAD("oversized record name");
+        if (end - off < name_len) BAD("truncated record");
+        off += name_len;
+        if (end - off < 8) BAD("truncated record");
+        const uint32_t dt = (uint32_t)get_le(b + off, 4), nd = (uint32_t)get_le(b + off + 4, 4);
+        off += 8;
+        if (dt > 1) BAD("unknown dtype");
+        if (nd > 8) BAD("too many dimensions");
+        if (end - off < (int64_t)nd * 8) BAD("truncated record");
+        int64_t n = 1;
+        for (uint32_t d = 0; d < nd; ++d, off += 8) n *= (int64_t)get_le(b + off, 8);
+        const int64_t payload = n * (dt == 0 ? 4 : 2);
+        if (end - off < payload) BAD("truncated record");
+        for (int64_t e = 0; e < n && data_out; ++e) {
+            if (tot + e >= cap) break;
+            uint32_t u = dt == 0 ? (uint32_t)get_le(b + off + 4 * e, 4) : (uint32_t)get_le(b + off + 2 * e, 2) << 16;
+            memcpy(&data_out[tot + e], &u, 4);
+        }
+        off += payload;
+        tot += n;
+    }
+    if (off != end) BAD("trailing bytes after last record");
+#undef BAD
+    *count = cnt;
+    *total = tot;
+    return 0;
+}

@@ -452,3 +452,50 @@ int ref_bench_optim(int dp, int ep, int mode, int64_t n_expert, int64_t n_non_ex
 }
 
 }  // extern "C"
+
+// ---- record files: RecordFileWriter / read_record_file (src/reliability.cpp:222-320) ----
+#include "optimus/reliability.hpp"
+
+extern "C" {
+// names NUL-separated; data: every record's f32 values concatenated (add_f32 / add_bf16)
+int ref_record_file_write(const char* path, int n_rec, const char* names, const int32_t* dtypes,
+                          const int32_t* ndims, const int64_t* dims, const float* data, int64_t* bytes,
+                          uint32_t* crc) {
+    return guard([&] {
+        RecordFileWriter w(path);
+        int64_t di = 0, de = 0;
+        for (int r = 0; r < n_rec; ++r) {
+            const std::string name(names);
+            names += name.size() + 1;
+            std::vector<int64_t> d(dims + di, dims + di + ndims[r]);
+            di += ndims[r];
+            int64_t n = 1;
+            for (int64_t x : d) n *= x;
+            if (dtypes[r] == 0)
+                w.add_f32(name, d, data + de, n);
+            else
+                w.add_bf16(name, d, data + de, n);
+            de += n;
+        }
+        const RecordFileWriter::Written done = w.finish();
+        *bytes = done.bytes;
+        *crc = done.crc;
+    });
+}
+
+// read_record_file: count, total elements, and (data_out) every record as_f32, concatenated
+int ref_record_file_read(const char* path, int64_t* count, int64_t* total, float* data_out, int64_t cap) {
+    return guard([&] {
+        std::vector<TensorRecord> recs = read_record_file(path);
+        int64_t tot = 0;
+        for (const TensorRecord& r : recs) {
+            std::vector<float> f = r.as_f32();
+            for (size_t e = 0; e < f.size() && data_out; ++e)
+                if (tot + (int64_t)e < cap) data_out[tot + (int64_t)e] = f[e];
+            tot += (int64_t)f.size();
+        }
+        *count = (int64_t)recs.size();
+        *total = tot;
+    });
+}
+}  // extern "C"

@@ -34,7 +34,7 @@ I64 = C.c_int64
 
 
 class B2Error(RuntimeError):
-    """Status != 0 from the C-ABI: 1 contract, 2 config, 3 cuda, 4 nccl."""
+    """Status != 0 from the C-ABI: 1 contract, 2 config, 3 cuda, 4 nccl, 5 io."""
 
     def __init__(self, code: int, msg: str):
         super().__init__(f"[b2 status {code}] {msg}")
@@ -47,6 +47,10 @@ class ContractError(B2Error):
 
 class ConfigError(B2Error):
     pass
+
+
+class IoError(B2Error):
+    """optimus::IoError (common.hpp:14-36): unreadable / invalid record files."""
 
 
 class CMoeCfg(C.Structure):
@@ -115,6 +119,18 @@ SIGNATURES = {
     "b2_moe_stage_name": (C.c_char_p, [C.c_int]),
     "b2_moe_last_launches": (C.c_int, [P]),
     "b2_opt_last_launches": (C.c_int, [P]),
+    "b2_crc32": (C.c_int, [P, P, I64, C.c_uint32, P]),
+    "b2_rec_writer_open": (C.c_int, [P, C.c_char_p, P]),
+    "b2_rec_writer_add": (C.c_int, [P, C.c_char_p, C.c_int, P, C.c_int, P, C.c_int]),
+    "b2_rec_writer_finish": (C.c_int, [P, P, P]),
+    "b2_rec_file_open": (C.c_int, [P, C.c_char_p, P]),
+    "b2_rec_file_count": (C.c_int, [P, P]),
+    "b2_rec_file_info": (C.c_int, [P, C.c_int, P, C.c_int, P, P, P]),
+    "b2_rec_file_find": (C.c_int, [P, C.c_char_p, P]),
+    "b2_rec_file_read": (C.c_int, [P, C.c_int, I64, I64, P, C.c_int]),
+    "b2_rec_file_close": (C.c_int, [P]),
+    "b2_opt_write_shard": (C.c_int, [P, C.c_char_p, P, P, P, C.c_int, P, P, P]),
+    "b2_opt_restore_shard": (C.c_int, [P, C.c_char_p, P, P, P, C.c_int]),
 }
 
 _LIB = None
@@ -138,7 +154,7 @@ def lib():
 def _check(rc: int):
     if rc != 0:
         msg = lib().b2_last_error().decode()
-        cls = ContractError if rc == 1 else ConfigError if rc == 2 else B2Error
+        cls = {1: ContractError, 2: ConfigError, 5: IoError}.get(rc, B2Error)
         raise cls(rc, msg)
 
 
@@ -492,12 +508,114 @@ class ShardedOptimizer:
     def set_step_count(self, n: int):
         _check(lib().b2_opt_set_step_count(self.h, n))
 
+    @staticmethod
+    def _shard_args(names, shapes):
+        arr = (C.c_char_p * len(names))(*[n.encode() for n in names])
+        if shapes is None:
+            return arr, None, None
+        nd = (C.c_int * len(shapes))(*[len(s) for s in shapes])
+        flat = [int(d) for s in shapes for d in s]
+        dims = (C.c_int64 * max(len(flat), 1))(*flat)
+        return arr, dims, nd
+
+    def write_shard(self, directory: str, names, shapes=None, full: bool = True):
+        """write_state_dir's shard file (reliability.cpp:402-460); collective. Returns
+        (bytes, crc, model_shard); bytes = crc = 0 on ranks that are not the shard's writer."""
+        arr, dims, nd = self._shard_args(names, shapes)
+        b, c, m = C.c_int64(), C.c_uint32(), C.c_int()
+        _check(lib().b2_opt_write_shard(self.h, directory.encode(), arr, dims, nd, int(full), C.byref(b),
+                                        C.byref(c), C.byref(m)))
+        return b.value, c.value, m.value
+
+    def restore_shard(self, directory: str, names, shapes=None, full: bool = True):
+        """restore_full's per-parameter loop (reliability.cpp:623-675): weights, owned
+        master/m/v slices and grads from the shard files; no collective."""
+        arr, dims, nd = self._shard_args(names, shapes)
+        _check(lib().b2_opt_restore_shard(self.h, directory.encode(), arr, dims, nd, int(full)))
+
     def last_launches(self) -> int:
         return lib().b2_opt_last_launches(self.h)
 
     def close(self):
         if self.h:
             _check(lib().b2_opt_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+REC_F32, REC_BF16 = 0, 1
+
+
+def crc32(ctx: Context, t, crc: int = 0) -> int:
+    """zlib.crc32 of a device tensor's bytes, computed on the GPU (synchronises)."""
+    out = C.c_uint32()
+    _check(lib().b2_crc32(ctx.h, _ptr(t), t.numel() * t.element_size(), crc, C.byref(out)))
+    return out.value
+
+
+class RecordWriter:
+    """RecordFileWriter (reliability.hpp:47-71) over device tensors."""
+
+    def __init__(self, ctx: Context, path: str):
+        h = C.c_void_p()
+        _check(lib().b2_rec_writer_open(ctx.h, path.encode(), C.byref(h)))
+        self.h = h
+
+    def add(self, name: str, t, rec_dtype: int, dims=None):
+        dims = list(t.shape) if dims is None else list(dims)
+        d = (C.c_int64 * max(len(dims), 1))(*dims)
+        _check(lib().b2_rec_writer_add(self.h, name.encode(), rec_dtype, d, len(dims), _ptr(t), _dt_code(t)))
+
+    def add_f32(self, name, t, dims=None):
+        self.add(name, t, REC_F32, dims)
+
+    def add_bf16(self, name, t, dims=None):
+        self.add(name, t, REC_BF16, dims)
+
+    def finish(self):
+        b, c = C.c_int64(), C.c_uint32()
+        h, self.h = self.h, None
+        _check(lib().b2_rec_writer_finish(h, C.byref(b), C.byref(c)))
+        return b.value, c.value
+
+
+class RecordFile:
+    """read_record_file (reliability.cpp:272-320): validated on open; records read into device tensors."""
+
+    def __init__(self, ctx: Context, path: str):
+        h = C.c_void_p()
+        _check(lib().b2_rec_file_open(ctx.h, path.encode(), C.byref(h)))
+        self.h, self.ctx = h, ctx
+        n = C.c_int()
+        _check(lib().b2_rec_file_count(self.h, C.byref(n)))
+        self.records = []
+        for i in range(n.value):
+            name = C.create_string_buffer(4097)
+            dt, nd = C.c_int(), C.c_int()
+            dims = (C.c_int64 * 8)()
+            _check(lib().b2_rec_file_info(self.h, i, name, 4097, C.byref(dt), dims, C.byref(nd)))
+            self.records.append((name.value.decode(), dt.value, tuple(dims[:nd.value])))
+
+    def find(self, name: str) -> int:
+        i = C.c_int()
+        _check(lib().b2_rec_file_find(self.h, name.encode(), C.byref(i)))
+        return i.value
+
+    def read(self, i: int, out, begin: int = 0, end=None):
+        """elements [begin, end) of record i into the device tensor out (f32 or bf16)."""
+        if end is None:
+            end = begin + out.numel()
+        _check(lib().b2_rec_file_read(self.h, i, begin, end, _ptr(out), _dt_code(out)))
+        return out
+
+    def close(self):
+        if self.h:
+            _check(lib().b2_rec_file_close(self.h))
             self.h = None
 
     def __del__(self):

@@ -7,6 +7,7 @@
 #include <memory>
 #include <string>
 
+#include "ckpt_state.h"
 #include "comm.h"
 #include "kernels.h"
 #include "moe_layer.h"
@@ -513,6 +514,128 @@ int b2_opt_gather_state(b2_opt* o, int p, float* master, float* exp_avg, float* 
 
 int b2_opt_load_state(b2_opt* o, int p, const float* master, const float* exp_avg, const float* exp_avg_sq) {
     return guard([&] { o->opt->load_state(p, master, exp_avg, exp_avg_sq); });
+}
+
+int b2_crc32(b2_ctx* ctx, const void* dev, int64_t n, uint32_t crc_in, uint32_t* crc_out) {
+    return guard([&] {
+        check(ctx && crc_out, "crc32: null argument");
+        B2_CUDA(cudaSetDevice(ctx->c.device));
+        *crc_out = crc32_device(dev, n, crc_in, ctx->c.stream);
+    });
+}
+
+int b2_rec_writer_open(b2_ctx* ctx, const char* path, b2_rec_writer** out) {
+    return guard([&] {
+        check(ctx && path && out, "record writer: null argument");
+        require_device();
+        *out = reinterpret_cast<b2_rec_writer*>(new RecordWriter(ctx->c.device, ctx->c.stream, path));
+    });
+}
+
+int b2_rec_writer_add(b2_rec_writer* w, const char* name, int rec_dtype, const int64_t* dims, int ndim,
+                      const void* src, int src_dtype) {
+    return guard([&] {
+        check(w && name && (ndim == 0 || dims) && ndim >= 0, "record writer: null argument");
+        check(rec_dtype == B2_REC_F32 || rec_dtype == B2_REC_BF16, "record writer: unknown record dtype");
+        reinterpret_cast<RecordWriter*>(w)->add(name, (RecDtype)rec_dtype, std::vector<int64_t>(dims, dims + ndim),
+                                                src, src_dtype);
+    });
+}
+
+int b2_rec_writer_finish(b2_rec_writer* w, int64_t* bytes, uint32_t* crc) {
+    std::unique_ptr<RecordWriter> owned(reinterpret_cast<RecordWriter*>(w));
+    return guard([&] {
+        check(w != nullptr, "record writer: null handle");
+        const RecordWriter::Written d = owned->finish();
+        if (bytes) *bytes = d.bytes;
+        if (crc) *crc = d.crc;
+    });
+}
+
+int b2_rec_file_open(b2_ctx* ctx, const char* path, b2_rec_file** out) {
+    return guard([&] {
+        check(ctx && path && out, "record file: null argument");
+        require_device();
+        *out = reinterpret_cast<b2_rec_file*>(new RecordFile(ctx->c.device, ctx->c.stream, path));
+    });
+}
+
+int b2_rec_file_count(b2_rec_file* f, int* count) {
+    return guard([&] { *count = (int)reinterpret_cast<RecordFile*>(f)->records().size(); });
+}
+
+int b2_rec_file_info(b2_rec_file* f, int i, char* name, int name_cap, int* rec_dtype, int64_t* dims, int* ndim) {
+    return guard([&] {
+        const auto& recs = reinterpret_cast<RecordFile*>(f)->records();
+        check(i >= 0 && i < (int)recs.size(), "record file: record index out of range");
+        const RecordInfo& r = recs[(size_t)i];
+        if (name && name_cap > 0) {
+            const size_t k = std::min(r.name.size(), (size_t)name_cap - 1);
+            std::memcpy(name, r.name.data(), k);
+            name[k] = 0;
+        }
+        if (rec_dtype) *rec_dtype = (int)r.dtype;
+        if (dims)
+            for (size_t d = 0; d < r.dims.size(); ++d) dims[d] = r.dims[d];
+        if (ndim) *ndim = (int)r.dims.size();
+    });
+}
+
+int b2_rec_file_find(b2_rec_file* f, const char* name, int* index) {
+    return guard([&] { *index = reinterpret_cast<RecordFile*>(f)->find(name); });
+}
+
+int b2_rec_file_read(b2_rec_file* f, int i, int64_t begin, int64_t end, void* dst, int dst_dtype) {
+    return guard([&] { reinterpret_cast<RecordFile*>(f)->read(i, begin, end, dst, dst_dtype); });
+}
+
+int b2_rec_file_close(b2_rec_file* f) {
+    return guard([&] { delete reinterpret_cast<RecordFile*>(f); });
+}
+
+namespace {
+void shard_args(b2_opt* o, const char* const* names, const int64_t* dims, const int* ndims,
+                std::vector<std::string>* nm, std::vector<std::vector<int64_t>>* dv) {
+    check(o && names, "checkpoint: null argument");
+    const int np = o->opt->num_params();
+    size_t at = 0;
+    for (int p = 0; p < np; ++p) {
+        check(names[p] != nullptr, "checkpoint: null parameter name");
+        nm->push_back(names[p]);
+        std::vector<int64_t> d;
+        if (dims && ndims) {
+            check(ndims[p] >= 0 && ndims[p] <= 8, "checkpoint: at most 8 dimensions");
+            d.assign(dims + at, dims + at + ndims[p]);
+            at += (size_t)ndims[p];
+        }
+        dv->push_back(std::move(d));
+    }
+}
+}  // namespace
+
+int b2_opt_write_shard(b2_opt* o, const char* dir, const char* const* names, const int64_t* dims,
+                       const int* ndims, int full, int64_t* bytes, uint32_t* crc, int* model_shard) {
+    return guard([&] {
+        check(dir != nullptr, "checkpoint: null directory");
+        std::vector<std::string> nm;
+        std::vector<std::vector<int64_t>> dv;
+        shard_args(o, names, dims, ndims, &nm, &dv);
+        const ShardWritten w = write_state_shard(*o->opt, dir, nm, dv, full != 0);
+        if (bytes) *bytes = w.bytes;
+        if (crc) *crc = w.crc;
+        if (model_shard) *model_shard = w.model_shard;
+    });
+}
+
+int b2_opt_restore_shard(b2_opt* o, const char* dir, const char* const* names, const int64_t* dims,
+                         const int* ndims, int full) {
+    return guard([&] {
+        check(dir != nullptr, "checkpoint: null directory");
+        std::vector<std::string> nm;
+        std::vector<std::vector<int64_t>> dv;
+        shard_args(o, names, dims, ndims, &nm, &dv);
+        restore_state_shard(*o->opt, dir, nm, dv, full != 0);
+    });
 }
 
 int b2_opt_get_state(b2_opt* o, int p, float* master, float* exp_avg, float* exp_avg_sq) {

@@ -385,6 +385,30 @@ void ShardedOptimizer::gather_state(int p, float* master, float* m, float* v) {
     B2_CUDA(cudaStreamSynchronize(ctx_.stream));
 }
 
+void ShardedOptimizer::gather_state_device(int p, float* master, float* m, float* v) {
+    check(p >= 0 && p < (int)plan_.size(), "optimizer: parameter index out of range");
+    B2_CUDA(cudaSetDevice(ctx_.device));
+    const Entry& e = plan_[(size_t)p];
+    const int64_t numel = params_[(size_t)p].numel, n = e.own_e - e.own_b;
+    const int gsize = mode_ == ShardMode::ddp ? 1 : (e.over_dp_ep ? ctx_.dp * ctx_.ep : ctx_.dp);
+    float* dst[3] = {master, m, v};
+    const float* src[3] = {e.master, e.m, e.v};
+    for (int q = 0; q < 3; ++q) {
+        if (!dst[q]) continue;
+        if (n > 0)
+            B2_CUDA(cudaMemcpyAsync(dst[q] + e.own_b, src[q], 4 * (size_t)n, cudaMemcpyDeviceToDevice, ctx_.stream));
+        if (gsize > 1) all_gather_v(*group_of(e), dst[q], numel, F32, ctx_.stream);
+    }
+}
+
+void ShardedOptimizer::state_slices(int p, float** master, float** m, float** v) const {
+    check(p >= 0 && p < (int)plan_.size(), "optimizer: parameter index out of range");
+    const Entry& e = plan_[(size_t)p];
+    *master = e.master;
+    *m = e.m;
+    *v = e.v;
+}
+
 void ShardedOptimizer::load_state(int p, const float* master, const float* m, const float* v) {
     check(p >= 0 && p < (int)plan_.size(), "optimizer: parameter index out of range");
     B2_CUDA(cudaSetDevice(ctx_.device));

@@ -53,6 +53,17 @@ class ShardedOptimizer {
     void gather_state(int p, float* master, float* m, float* v);
     // restore (reliability.cpp:658-667): this rank's owned slice from full host tensors
     void load_state(int p, const float* master, const float* m, const float* v);
+    // device variants for the record-file checkpoint (ckpt_state.cpp): full fp32 tensors
+    // gathered into device buffers of numel floats (NULL skips one) / the owned slices
+    void gather_state_device(int p, float* master, float* m, float* v);
+    void state_slices(int p, float** master, float** m, float** v) const;
+    int num_params() const { return (int)params_.size(); }
+    const ParamSlot& param(int p) const { return params_[(size_t)p]; }
+    bool over_dp_ep(int p) const { return plan_[(size_t)p].over_dp_ep; }
+    int weight_dtype() const { return wdt_; }
+    int grad_dtype() const { return gdt_; }
+    Context& context() { return ctx_; }
+    int64_t step_count() const { return step_count_; }
     void set_step_count(int64_t n) { step_count_ = n; }
     int last_launches() const { return launches_; }
     // detect_soft_failure (reliability.cpp:706-723): scans this rank's LOCAL grads (and

@@ -94,6 +94,13 @@ def main():
             r = ref.sharded_steps(dp, ep, 1, mode, acfg, numel, cls, tps, w0, grads)
             np.savez_compressed(os.path.join(HERE, f"sharded_dp{dp}_ep{ep}_m{mode}.npz"), numel=numel, cls=cls,
                                 w0=w0, grads=grads, **r)
+
+    # record files (RecordFileWriter, reliability.cpp:222-270): the reference's own test
+    # cases plus format edge cases, written by the reference itself
+    sys.path.insert(0, os.path.dirname(HERE))
+    import record_cases
+    for name, recs in record_cases.cases(ref).items():
+        ref.record_file_write(os.path.join(HERE, f"records_{name}.bin"), recs)
     print("ok")
 
 

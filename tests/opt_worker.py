@@ -68,6 +68,39 @@ def run(rank, world, port, dp, ep, mode, result_path):
             "master": [opt.state(p)[0].tolist() for p in range(len(NUMEL))],
             "m": [opt.state(p)[1].tolist() for p in range(len(NUMEL))],
             "v": [opt.state(p)[2].tolist() for p in range(len(NUMEL))]}
+    # record-file checkpoint round trip (reliability.cpp:402-460 / 623-675): write the shard
+    # files, restore into a fresh optimizer, then one more identical step on both
+    ck = os.path.join(os.path.dirname(result_path), "ckpt")
+    if rank == 0:
+        os.makedirs(ck, exist_ok=True)
+    dist.barrier()
+    names = [f"layer.p{p}" for p in range(len(NUMEL))]
+    nbytes, _, shard = opt.write_shard(ck, names)
+    torch.cuda.synchronize()
+    dist.barrier()
+    W2 = torch.zeros_like(W)
+    G2 = torch.zeros_like(G)
+    params2, off = [], 0
+    for n, c in zip(NUMEL, CLS):
+        params2.append((W2[off:off + n], G2[off:off + n], c, 0))
+        off += n
+    opt2 = b2.ShardedOptimizer(ctx, cfg, params2, mode)
+    opt2.restore_shard(ck, names)
+    opt2.set_step_count(steps)
+    torch.cuda.synchronize()
+    ck_ok = bool(torch.equal(W2, W)) and bool(torch.equal(G2, G.bfloat16().float()))
+    ck_ok = ck_ok and all(np.array_equal(a, b_) for p in range(len(NUMEL)) for a, b_ in zip(opt.state(p), opt2.state(p)))
+    G.copy_(G2)
+    opt.step(stats=False)
+    opt2.step(stats=False)
+    torch.cuda.synchronize()
+    ck_ok = ck_ok and bool(torch.equal(W2, W))
+    ck_ok = ck_ok and all(np.array_equal(a, b_) for p in range(len(NUMEL)) for a, b_ in zip(opt.state(p), opt2.state(p)))
+    if nbytes:  # the writer's file parses under the oracle's read_record_file
+        cnt, _ = orc.record_file_read(os.path.join(ck, f"shard-{shard}.bin"))
+        ck_ok = ck_ok and cnt > 0 and nbytes == os.path.getsize(os.path.join(ck, f"shard-{shard}.bin"))
+    mine["ckpt_ok"] = ck_ok
+    opt2.close()
     gathered = [None] * world
     dist.all_gather_object(gathered, mine)
     if rank == 0:
@@ -111,6 +144,7 @@ def run(rank, world, port, dp, ep, mode, result_path):
                     b_, e_ = gathered[q]["owned"][p]
                     if not np.array_equal(got[b_:e_], np.asarray(gathered[q]["master"][p], np.float32)):
                         res["gather_ok"] = False
+        res["ckpt_ok"] = all(g["ckpt_ok"] for g in gathered)
         with open(result_path, "w") as f:
             json.dump(res, f)
     dist.barrier()

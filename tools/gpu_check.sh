@@ -27,6 +27,8 @@ for w in $WHAT; do case $w in
  tl2n) timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29515 tools/timeline.py --graph --ce-dispatch 2>&1 | grep -v "Warn\|warn\|\*\*\*\|OMP" | head -20 ;;
  tl4n) timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29516 tools/timeline.py --graph --ce-dispatch 2>&1 | grep -v "Warn\|warn\|\*\*\*\|OMP" | head -20 ;;
  tl4) timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29514 tools/timeline.py --graph 2>&1 | grep -v "Warn\|warn\|\*\*\*\|OMP" | head -45 ;;
+ ckpt) timeout 600 python -m pytest tests/test_gpu_ckpt.py tests/test_records.py -x -q > $OUT/ckpt_tests.log 2>&1; echo "ckpt tests rc=$?"; tail -15 $OUT/ckpt_tests.log
+      timeout 300 python tools/ckpt_probe.py --dir /tmp > $OUT/ckpt_probe.json 2> $OUT/ckpt_probe.err; echo "probe rc=$?"; cat $OUT/ckpt_probe.json; tail -3 $OUT/ckpt_probe.err ;;
  adamw) timeout 300 python tools/adamw_probe.py --gelems 2 > $OUT/adamw.txt 2>&1; cat $OUT/adamw.txt
       timeout 600 ncu --set full --clock-control none -k regex:"adamw_chunks|sumsq_chunks" --launch-skip 2 -c 2 -o $OUT/adamw_full python tools/adamw_probe.py --gelems 0.5 --steps 1 > $OUT/ncu_adamw.log 2>&1; echo "adamw ncu rc=$?" ;;
  pdl) for i in 1 2; do for v in 1 0; do echo "== B2_PDL=$v"; B2_PDL=$v timeout 300 python tools/timeline.py --graph 2>&1 | grep -E "event-timed|span"; done; done ;;
