@@ -77,6 +77,18 @@ def run(rank, world, port, dp, ep, mode, result_path):
     names = [f"layer.p{p}" for p in range(len(NUMEL))]
     nbytes, _, shard = opt.write_shard(ck, names)
     torch.cuda.synchronize()
+    # the .g16 records hold the WRITER's grads (reliability.cpp:455): expert params come from
+    # this rank's model-shard file, non-expert params from the ep-0 shard (restore_full)
+    writers = [None] * world
+    dist.all_gather_object(writers, (shard, nbytes > 0, G.cpu().numpy()))
+    g_of = {sh: g for sh, w, g in writers if w}
+    g_exp = np.empty(total, np.float32)
+    off = 0
+    for n, c in zip(NUMEL, CLS):
+        src = g_of[shard] if c else g_of[min(g_of)]
+        g_exp[off:off + n] = src[off:off + n]
+        off += n
+    g_exp = torch.from_numpy(g_exp).to(dev).bfloat16().float()
     dist.barrier()
     W2 = torch.zeros_like(W)
     G2 = torch.zeros_like(G)
@@ -88,18 +100,19 @@ def run(rank, world, port, dp, ep, mode, result_path):
     opt2.restore_shard(ck, names)
     opt2.set_step_count(steps)
     torch.cuda.synchronize()
-    ck_ok = bool(torch.equal(W2, W)) and bool(torch.equal(G2, G.bfloat16().float()))
-    ck_ok = ck_ok and all(np.array_equal(a, b_) for p in range(len(NUMEL)) for a, b_ in zip(opt.state(p), opt2.state(p)))
+    same_state = lambda: all(np.array_equal(a, b_) for p in range(len(NUMEL)) for a, b_ in zip(opt.state(p), opt2.state(p)))
+    detail = {"w": bool(torch.equal(W2, W)), "g": bool(torch.equal(G2, g_exp)), "state": same_state()}
     G.copy_(G2)
     opt.step(stats=False)
     opt2.step(stats=False)
     torch.cuda.synchronize()
-    ck_ok = ck_ok and bool(torch.equal(W2, W))
-    ck_ok = ck_ok and all(np.array_equal(a, b_) for p in range(len(NUMEL)) for a, b_ in zip(opt.state(p), opt2.state(p)))
+    detail["w_after"] = bool(torch.equal(W2, W))
+    detail["state_after"] = same_state()
     if nbytes:  # the writer's file parses under the oracle's read_record_file
         cnt, _ = orc.record_file_read(os.path.join(ck, f"shard-{shard}.bin"))
-        ck_ok = ck_ok and cnt > 0 and nbytes == os.path.getsize(os.path.join(ck, f"shard-{shard}.bin"))
-    mine["ckpt_ok"] = ck_ok
+        detail["file"] = cnt > 0 and nbytes == os.path.getsize(os.path.join(ck, f"shard-{shard}.bin"))
+    mine["ckpt_ok"] = all(detail.values())
+    mine["ckpt_detail"] = detail
     opt2.close()
     gathered = [None] * world
     dist.all_gather_object(gathered, mine)
@@ -145,6 +158,7 @@ def run(rank, world, port, dp, ep, mode, result_path):
                     if not np.array_equal(got[b_:e_], np.asarray(gathered[q]["master"][p], np.float32)):
                         res["gather_ok"] = False
         res["ckpt_ok"] = all(g["ckpt_ok"] for g in gathered)
+        res["ckpt_detail"] = [g["ckpt_detail"] for g in gathered]
         with open(result_path, "w") as f:
             json.dump(res, f)
     dist.barrier()

@@ -94,6 +94,6 @@ def test_sharded_optimizer_matches_oracle(dp, ep, mode):
         assert r["weights_maxrel"] <= 1e-6, r
     assert r["state_bytes_equal"], r
     assert r.get("gather_ok", True), r
-    assert r.get("ckpt_ok", True), r  # shard files written, restored, stepped bitwise
+    assert r.get("ckpt_ok", True), r.get("ckpt_detail")  # shard files written, restored, stepped bitwise
     # grad norm / clip: exact sums at 2 members; NCCL's 4-member fp32 order moves the last bits
     assert r["stats_maxdiff"] <= (1e-9 if dp * ep <= 2 else 1e-7), r
