@@ -407,7 +407,10 @@ __global__ void __launch_bounds__(256, MINB) adamw_chunks_kernel(const OptSeg* _
 // writes master/m/v/weight back with bulk stores and frees the slot once they have read it.
 // Up to five tiles (135 KB per SM) are in flight while the math runs. The divide / sqrt
 // chains are latency-bound (their slow-path branches serialise a thread's elements), so the
-// block runs the full 32 warps and no thread ever waits on a global load. Persistent: one block per
+// block runs the full 32 warps and no thread ever waits on a global load.
+// Measured (tools/adamw_probe.py, 2 G elements, B200): 4.85 TB/s vs 5.25 TB/s for the
+// register kernel below (whose 32 warps x 4 elements keep more fp64 chains in flight than one
+// block's per-tile barrier allows), so this one stays opt-in (B2_ADAMW_IMPL=stream). Persistent: one block per
 // SM walks the chunk list. Chunks whose pointers are not 16-byte aligned (or not the bf16 x4
 // layout) and the <8-element tail of a chunk go through the per-element path from global.
 constexpr int kStCompute = 992;
@@ -436,6 +439,23 @@ __device__ __forceinline__ void st_wait(uint32_t bar, uint32_t parity) {
             : "r"(bar), "r"(parity)
             : "memory");
     } while (!done);
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ float2 lds_f2(uint32_t a) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_f2(uint32_t a, float2 v) {
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
 }
 
 __device__ __forceinline__ bool st_fast(const OptSeg& sg, const OptChunk& ch) {
@@ -474,7 +494,6 @@ __global__ void __launch_bounds__(kStThreads, 1) adamw_stream_kernel(const OptSe
     extern __shared__ __align__(128) uint8_t st_raw[];
     const uint32_t raw = st_smem_u32(st_raw);
     const uint32_t base = (raw + 127u) & ~127u;
-    uint8_t* gbase = st_raw + (base - raw);
     const uint32_t bar0 = base + kStStages * kStStageBytes;  // full[S], empty[S]
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
     auto empty_bar = [&](int s) { return bar0 + 8u * (kStStages + s); };
@@ -540,14 +559,13 @@ __global__ void __launch_bounds__(kStThreads, 1) adamw_stream_kernel(const OptSe
             const int tl = (int)(main - t0 < kStTE ? main - t0 : kStTE);
             st_wait(full_bar(stage), phase);
             const uint32_t sb = base + stage * kStStageBytes;
-            uint8_t* gs = gbase + (sb - base);
             if (2 * tid < tl) {
-                uint32_t* g2 = reinterpret_cast<uint32_t*>(gs + OG) + tid;
-                float2* pm = reinterpret_cast<float2*>(gs + OM) + tid;
-                float2* pa = reinterpret_cast<float2*>(gs + OA) + tid;
-                float2* pv = reinterpret_cast<float2*>(gs + OV) + tid;
-                const uint32_t gb = *g2;
-                float2 m0 = *pm, a0 = *pa, v0 = *pv;
+                // explicit shared-window accesses (a generic pointer here compiles to LD.E with
+                // a long-scoreboard wait per element pair, measured 40 % of the kernel's stalls)
+                const uint32_t ag = sb + OG + 4u * tid, am = sb + OM + 8u * tid, aa = sb + OA + 8u * tid,
+                               av = sb + OV + 8u * tid;
+                const uint32_t gb = lds_u32(ag);
+                float2 m0 = lds_f2(am), a0 = lds_f2(aa), v0 = lds_f2(av);
                 const float g[2] = {__uint_as_float(gb << 16), __uint_as_float(gb & 0xFFFF0000u)};
                 float* fm = &m0.x;
                 float* fa = &a0.x;
@@ -562,10 +580,10 @@ __global__ void __launch_bounds__(kStThreads, 1) adamw_stream_kernel(const OptSe
                     adamw_elem(fm[q], fa[q], fv[q], gq, c, wf);
                     wb[q] = bf16_bits_rne(wf);
                 }
-                *pm = m0;
-                *pa = a0;
-                *pv = v0;
-                *g2 = wb[0] | (wb[1] << 16);
+                sts_f2(am, m0);
+                sts_f2(aa, a0);
+                sts_f2(av, v0);
+                sts_u32(ag, wb[0] | (wb[1] << 16));
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("bar.sync 1, %0;" ::"n"(kStCompute) : "memory");
@@ -625,10 +643,10 @@ void launch_adamw_chunks(const OptSeg* segs, const OptChunk* chunks, const int32
     c.bc2 = a.bc2;
     c.rbc1 = 1.0 / a.bc1;
     c.rbc2 = 1.0 / a.bc2;
-    static int impl = -1;  // B2_ADAMW_IMPL=regs: the register-pipelined kernel (A/B hook)
+    static int impl = -1;  // B2_ADAMW_IMPL=stream: the TMA-streamed kernel (A/B hook)
     if (impl < 0) {
         const char* env = getenv("B2_ADAMW_IMPL");
-        impl = env && std::string(env) == "regs" ? 0 : 1;
+        impl = env && std::string(env) == "stream" ? 1 : 0;
     }
     if (impl == 1) {
         static int sms = 0;

@@ -20,7 +20,8 @@ def main():
     torch.cuda.set_stream(stream)
     ctx = b2.Context(0, stream=stream)
     n = int(args.gelems * 1e9)
-    sizes = [n // 3, n // 3, n - 2 * (n // 3)]
+    third = (n // 3) // 64 * 64  # multiples of 64: every slot takes the vectorised path, as the Mula set does
+    sizes = [third, third, n - 2 * third]
     ws = [(torch.randn(k, device="cuda") * 0.02).bfloat16() for k in sizes]
     gs = [(torch.randn(k, device="cuda") * 1e-3).bfloat16() for k in sizes]
     opt = b2.ShardedOptimizer(ctx, b2.AdamWConfig(warmup_steps=0), [(w, g, 1, 0) for w, g in zip(ws, gs)], b2.EPSO)

@@ -32,7 +32,7 @@ for w in $WHAT; do case $w in
  adamw) timeout 300 python tools/adamw_probe.py --gelems 2 > $OUT/adamw.txt 2>&1; cat $OUT/adamw.txt
       timeout 600 ncu --set full --clock-control none -k regex:"adamw_chunks|adamw_stream|sumsq_chunks" --launch-skip 2 -c 2 -o $OUT/adamw_full python tools/adamw_probe.py --gelems 0.5 --steps 1 > $OUT/ncu_adamw.log 2>&1; echo "adamw ncu rc=$?" ;;
  adamwab) for impl in regs stream regs stream; do echo "== B2_ADAMW_IMPL=$impl"; B2_ADAMW_IMPL=$impl timeout 300 python tools/adamw_probe.py --gelems ${GELEMS:-2}; done
-      timeout 600 python -m pytest tests/test_gpu_optim.py -x -q > $OUT/optim_tests.log 2>&1; echo "optim tests rc=$?"; tail -3 $OUT/optim_tests.log ;;
+      for impl in regs stream; do B2_ADAMW_IMPL=$impl timeout 600 python -m pytest tests/test_gpu_optim.py tests/test_gpu_ckpt.py -x -q > $OUT/optim_tests_$impl.log 2>&1; echo "optim tests ($impl) rc=$?"; tail -2 $OUT/optim_tests_$impl.log; done ;;
  pdl) for i in 1 2; do for v in 1 0; do echo "== B2_PDL=$v"; B2_PDL=$v timeout 300 python tools/timeline.py --graph 2>&1 | grep -E "event-timed|span"; done; done ;;
  ab) for opt in "--graph" "--graph --tma-gather"; do echo "== timeline $opt"; timeout 300 python tools/timeline.py $opt 2>&1 | grep -v Warn | head -24; done ;;
  gtest) timeout 600 python -m pytest tests -m gpu -x -q -k "${GTEST_K}" > $OUT/gtest.log 2>&1; echo "gtest rc=$?"; tail -15 $OUT/gtest.log ;;
