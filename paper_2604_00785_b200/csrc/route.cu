@@ -10,6 +10,9 @@
 // follow kernels.hpp:201-212 in fp64 with the sequential sum order, and top-k uses
 // the same strict '>' (ties to the lower expert index). Given identical scores the
 // selections are bit-exact.
+#include <cstdlib>
+#include <string>
+
 #include "b2_common.cuh"
 #include "kernels.h"
 
@@ -305,6 +308,144 @@ __global__ void __launch_bounds__(128) router_logits_bf16_kernel(const __nv_bflo
     }
 }
 
+// ---- logits, bf16 inputs, 8 x 8 register tiles ----------------------------------------
+// One warp per CTA, 32 tokens x 64 experts; each lane owns 8 tokens x 8 experts (64 fp32
+// accumulators as 32 float2). Per p step a lane loads its 8 x values and 8 W values (4
+// conflict-free 128-bit shared loads), duplicates each x into an (x, x) pair in registers and
+// issues 32 fma.rn.f32x2 that pair two EXPERTS against one token: 2x the FMAs per shared byte
+// of the token-paired kernel above, whose 4 loads feed 16 FMA pairs. The order of every
+// accumulator is still p = 0, 1, ... with one rounding per step, and bf16 x bf16 products are
+// exact in fp32, so the logits stay bit-identical to the reference's multiply-then-add.
+constexpr int kL3Tok = 32, kL3Exp = 64, kL3P = 32, kL3Stages = 4;
+struct Logits3Smem {
+    uint16_t xraw[kL3Stages][kL3Tok][kL3P];  // 64 B rows, 16 B units swizzled by (t >> 1) & 3
+    uint16_t wraw[kL3Stages][kL3P][kL3Exp];  // 128 B rows, 16 B units swizzled by p & 7
+    float xs[2][kL3P][kL3Tok];               // transposed [p][token]
+    float ws[2][kL3P][kL3Exp];               // 16 B units (4 experts) swizzled by p & 15
+};
+
+__global__ void __launch_bounds__(32) router_logits_bf16_t88_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                    const __nv_bfloat16* __restrict__ w,
+                                                                    float* __restrict__ logits, int S, int H, int N) {
+    pdl_wait();
+    pdl_launch();
+    extern __shared__ __align__(128) uint8_t l3_smem[];
+    Logits3Smem& sm = *reinterpret_cast<Logits3Smem*>(l3_smem);
+    const int lane = threadIdx.x;
+    const int t0 = blockIdx.x * kL3Tok, e0 = blockIdx.y * kL3Exp;
+    const int nchunks = H / kL3P;
+    auto issue = [&](int c) {
+        if (c < nchunks) {
+            const int s = c % kL3Stages, p0 = c * kL3P;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {  // x: 32 rows x 4 units
+                const int idx = lane + 32 * q, t = idx / 4, u = idx % 4;
+                const bool ok = t0 + t < S;
+                const __nv_bfloat16* src = x + (int64_t)(ok ? t0 + t : 0) * H + p0 + 8 * u;
+                cp_async16(&sm.xraw[s][t][8 * (u ^ ((t >> 1) & 3))], src, ok);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {  // W: 32 rows x 8 units
+                const int idx = lane + 32 * q, pp = idx / 8, u = idx % 8;
+                const bool ok = e0 + 8 * u < N;
+                const __nv_bfloat16* src = w + (int64_t)(p0 + pp) * N + (ok ? e0 + 8 * u : 0);
+                cp_async16(&sm.wraw[s][pp][8 * (u ^ (pp & 7))], src, ok);
+            }
+        }
+        cp_async_commit();
+    };
+    auto widen = [&](int c) {
+        const int s = c % kL3Stages, b = c & 1;
+        {  // x: lane = token, its 32 p values -> column `lane` of xs (consecutive lanes, no conflicts)
+            const int t = lane;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint4 r = *reinterpret_cast<const uint4*>(&sm.xraw[s][t][8 * (u ^ ((t >> 1) & 3))]);
+                const uint32_t v[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    sm.xs[b][8 * u + 2 * j][t] = __uint_as_float(v[j] << 16);
+                    sm.xs[b][8 * u + 2 * j + 1][t] = __uint_as_float(v[j] & 0xFFFF0000u);
+                }
+            }
+        }
+        {  // W: lane = row p, 64 experts -> 16 units of 4 floats, unit k stored at k ^ (p & 15)
+            const int pp = lane;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint4 r = *reinterpret_cast<const uint4*>(&sm.wraw[s][pp][8 * (u ^ (pp & 7))]);
+                const uint32_t v[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int k = 2 * u + h;  // experts 4k .. 4k+3
+                    *reinterpret_cast<float4*>(&sm.ws[b][pp][4 * (k ^ (pp & 15))]) =
+                        make_float4(__uint_as_float(v[2 * h] << 16), __uint_as_float(v[2 * h] & 0xFFFF0000u),
+                                    __uint_as_float(v[2 * h + 1] << 16), __uint_as_float(v[2 * h + 1] & 0xFFFF0000u));
+                }
+            }
+        }
+    };
+
+    float2 acc[8][4];  // [token][expert pair]
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+
+#pragma unroll
+    for (int c = 0; c < kL3Stages; ++c) issue(c);
+    cp_async_wait<kL3Stages - 1>();
+    __syncwarp();
+    widen(0);
+    const int tg = lane % 4, eg = lane / 4;  // tokens 8*tg .. +7, experts 8*eg .. +7
+    for (int c = 0; c < nchunks; ++c) {
+        cp_async_wait<kL3Stages - 2>();
+        __syncwarp();  // chunk c widened; chunk c+1 landed; ring slot c free
+        if (c + 1 < nchunks) widen(c + 1);
+        issue(c + kL3Stages);
+        const int b = c & 1;
+        float4 op[2][4];
+        auto ld = [&](float4 (&o)[4], int pp) {
+            o[0] = *reinterpret_cast<const float4*>(&sm.xs[b][pp][8 * tg]);
+            o[1] = *reinterpret_cast<const float4*>(&sm.xs[b][pp][8 * tg + 4]);
+            o[2] = *reinterpret_cast<const float4*>(&sm.ws[b][pp][4 * ((2 * eg) ^ (pp & 15))]);
+            o[3] = *reinterpret_cast<const float4*>(&sm.ws[b][pp][4 * ((2 * eg + 1) ^ (pp & 15))]);
+        };
+        ld(op[0], 0);
+#pragma unroll
+        for (int pp = 0; pp < kL3P; ++pp) {
+            if (pp + 1 < kL3P) ld(op[(pp + 1) & 1], pp + 1);
+            const float4 a0 = op[pp & 1][0], a1 = op[pp & 1][1], b0 = op[pp & 1][2], b1 = op[pp & 1][3];
+            const float xv[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float2 wp[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
+                                  make_float2(b1.z, b1.w)};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float2 xd = make_float2(xv[i], xv[i]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = __ffma2_rn(xd, wp[j], acc[i][j]);
+            }
+        }
+    }
+    const int e = e0 + 8 * eg;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int t = t0 + 8 * tg + i;
+        if (t >= S) continue;
+        float* dst = logits + (int64_t)t * N + e;
+        if (e + 7 < N) {
+            *reinterpret_cast<float4*>(dst) = make_float4(acc[i][0].x, acc[i][0].y, acc[i][1].x, acc[i][1].y);
+            *reinterpret_cast<float4*>(dst + 4) = make_float4(acc[i][2].x, acc[i][2].y, acc[i][3].x, acc[i][3].y);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (e + 2 * j < N) dst[2 * j] = acc[i][j].x;
+                if (e + 2 * j + 1 < N) dst[2 * j + 1] = acc[i][j].y;
+            }
+        }
+    }
+}
+
 // ---- softmax + top-k: one warp per token -------------------------------------------
 
 constexpr int kMaxExpertsPerLane = 8;  // N <= 256
@@ -583,6 +724,23 @@ template <typename T>
 void launch_router_logits(const T* x, const T* w, float* logits, int S, int H, int N, cudaStream_t st) {
     if (S == 0) return;
     if constexpr (sizeof(T) == 2) {
+        static int impl = -1;  // B2_LOGITS_IMPL=t42: the token-paired 8 x 4 kernel (A/B hook)
+        if (impl < 0) {
+            const char* env = getenv("B2_LOGITS_IMPL");
+            impl = env && std::string(env) == "t42" ? 0 : 1;
+        }
+        if (impl == 1 && H % kL3P == 0 && N % 8 == 0 && ((uintptr_t)x & 15) == 0 && ((uintptr_t)w & 15) == 0) {
+            static bool attr3 = false;
+            if (!attr3) {
+                B2_CUDA(cudaFuncSetAttribute(router_logits_bf16_t88_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sizeof(Logits3Smem)));
+                attr3 = true;
+            }
+            dim3 grid((unsigned)ceil_div(S, kL3Tok), (unsigned)ceil_div(N, kL3Exp));
+            launch_k(router_logits_bf16_t88_kernel, dim3(grid), dim3(32), sizeof(Logits3Smem), st, x, w, logits, S, H, N);
+            B2_LAUNCH_CHECK();
+            return;
+        }
         if (H % kL2P == 0 && N % 8 == 0 && ((uintptr_t)x & 15) == 0 && ((uintptr_t)w & 15) == 0) {
             static bool attr = false;
             if (!attr) {
