@@ -15,6 +15,8 @@ METRICS = [
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "%"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "%"),
     ("launch__registers_per_thread", ""),
+    ("sm__cycles_elapsed.avg.per_second", "GHz"),
+    ("l1tex__m_xbar2l1tex_read_bytes.sum", "bytes"),
 ]
 
 
