@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -199,6 +200,16 @@ __device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap*
         "l"((uint64_t)map), "r"(leader_bar), "r"(c0), "r"(c1)
         : "memory");
 }
+// 2-CTA load multicast to the CTAs in `mask` (same smem offset in each); every destination
+// pair's bytes complete_tx on that pair's LEADER barrier (the leader address is passed)
+__device__ __forceinline__ void tma_load_2d_cg2_mc(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                   int c1, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+        "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+        "l"((uint64_t)map), "r"(leader_bar), "r"(c0), "r"(c1), "h"(mask)
+        : "memory");
+}
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -263,6 +274,12 @@ __device__ __forceinline__ void umma_commit_cg2(uint32_t bar) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
         "h"((uint16_t)0x3)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_cg2_mask(uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+        "h"(mask)
         : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -466,18 +483,29 @@ __device__ __forceinline__ TileInfo tile_info(const Params& p, const int32_t* ps
 // producer: one stage of A and B for (tile, kb). `m_own` is the first A row this CTA
 // holds (the pair's tile base + 128 * rank); with CG = 2 each CTA loads B columns
 // [128 * rank, 128 * rank + 128) of the tile and signals the leader's barrier.
-template <GemmKind KIND, int CG>
+// MC = 2: the cluster holds two CTA pairs working on the same M rows (adjacent N tiles), so
+// each CTA loads HALF of its A tile (64 rows, or one of the two 64-column boxes of the MN-major
+// wgrad A) and multicasts it to the same-rank CTA of the other pair: A crosses L2 -> SM once
+// per cluster instead of once per pair.
+template <GemmKind KIND, int CG, int MC = 1>
 __device__ __forceinline__ void load_stage(const Params& p, const TileInfo& ti, int kb, int m_own, uint32_t rank,
-                                           uint32_t sA, uint32_t sB, uint32_t bar) {
+                                           uint32_t sA, uint32_t sB, uint32_t bar, int pair = 0) {
     const int k0 = kb * BK;
     auto ld = [&](uint32_t dst, const CUtensorMap* map, int c0, int c1) {
         if constexpr (CG == 1) tma_load_2d(dst, map, bar, c0, c1);
         else tma_load_2d_cg2(dst, map, bar, c0, c1);
     };
+    // A of the by-row kinds: [m_own, m_own + 128) x [k0, k0 + 64), K-major
+    auto ldA_rows = [&]() {
+        if constexpr (MC == 2)
+            tma_load_2d_cg2_mc(sA + 8192u * pair, &p.mapA, bar, k0, m_own + 64 * pair, (uint16_t)(0x5u << rank));
+        else
+            ld(sA, &p.mapA, k0, m_own);
+    };
     constexpr int BC = Cfg<CG>::B_COLS;
     const int nb = ti.n0 + BC * (int)rank;  // this CTA's first B column of the tile
     if constexpr (KIND == GemmKind::FwdGateUp) {
-        if (!p.gather_rows) ld(sA, &p.mapA, k0, m_own);
+        if (!p.gather_rows) ldA_rows();
         const int row = ti.e * p.H + k0;
         const int n0 = ti.n0 / 2;  // 128 gate columns + 128 up columns per tile
         if (CG == 1 || rank == 0) {
@@ -490,15 +518,15 @@ __device__ __forceinline__ void load_stage(const Params& p, const TileInfo& ti, 
             ld(sB + o + 8192, &p.mapB1, n0 + 64, row);
         }
     } else if constexpr (KIND == GemmKind::FwdDown) {
-        ld(sA, &p.mapA, k0, m_own);
+        ldA_rows();
         const int row = ti.e * p.I + k0;
 #pragma unroll
         for (int c = 0; c < BC / 64; ++c) ld(sB + c * 8192, &p.mapB0, nb + 64 * c, row);
     } else if constexpr (KIND == GemmKind::BwdDownDgrad) {
-        ld(sA, &p.mapA, k0, m_own);
+        ldA_rows();
         ld(sB, &p.mapB0, k0, ti.e * p.I + nb);
     } else if constexpr (KIND == GemmKind::BwdDx) {
-        ld(sA, &p.mapA, k0, m_own);
+        ldA_rows();
         if (k0 < p.I) ld(sB, &p.mapB0, k0, ti.e * p.H + nb);
         else ld(sB, &p.mapB1, k0 - p.I, ti.e * p.H + nb);
     } else if constexpr (KIND == GemmKind::RouterDx) {
@@ -512,8 +540,12 @@ __device__ __forceinline__ void load_stage(const Params& p, const TileInfo& ti, 
     } else {  // wgrad: K runs over the expert's rows; both operands MN-major
         const int row = ti.krow0 + k0;
         if (KIND != GemmKind::WgradGateUp || !p.gather_rows) {
-            ld(sA + 0, &p.mapA, m_own, row);
-            ld(sA + 8192, &p.mapA, m_own + 64, row);
+            if constexpr (MC == 2) {
+                tma_load_2d_cg2_mc(sA + 8192u * pair, &p.mapA, bar, m_own + 64 * pair, row, (uint16_t)(0x5u << rank));
+            } else {
+                ld(sA + 0, &p.mapA, m_own, row);
+                ld(sA + 8192, &p.mapA, m_own + 64, row);
+            }
         }
 #pragma unroll
         for (int c = 0; c < BC / 64; ++c) ld(sB + c * 8192, &p.mapB0, nb + 64 * c, row);
@@ -687,7 +719,7 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const TileInfo& t
     }
 }
 
-template <GemmKind KIND, int CG>
+template <GemmKind KIND, int CG, int MC>
 __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __grid_constant__ Params p) {
     using C = Cfg<CG>;
     using KC = KCfg<KIND, CG>;
@@ -709,15 +741,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
 
     pdl_launch();  // the next kernel may be scheduled (it waits for this grid's completion)
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+    // cluster = MC CTA pairs: crank = pair * 2 + rank; each pair's leader (rank 0) issues its MMAs
+    const uint32_t crank = CG == 2 ? cluster_rank() : 0u;
+    const uint32_t rank = crank & 1u, lead = crank & ~1u;
+    const int pair = (int)(crank >> 1);
     const bool leader = rank == 0;
+    const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pair));
     if (warp == 0 && lane == 0) {
         prefetch_map(&p.mapA);
         prefetch_map(&p.mapB0);
         prefetch_map(&p.mapB1);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full_bar(s), 1);
-            mbar_init(empty_bar(s), 1);
+            mbar_init(empty_bar(s), MC);  // MC = 2: both pairs' MMAs must be done with the stage
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull_bar(a), 1);
@@ -756,7 +792,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
     const int32_t* ps = p.pad_start;
     const int ntiles = total_tiles<KIND, CG>(p, ps);
     const uint32_t idesc = p.idesc;
-    const int unit = blockIdx.x / CG, nunits = gridDim.x / CG;  // tile scheduler over CTA pairs
+    // tile scheduler over clusters: pair `pair` of cluster `unit` takes tiles unit*MC + pair,
+    // + nunits*MC, ... (MC = 2: the two pairs share M rows and K extent, adjacent N tiles)
+    const int unit = blockIdx.x / (CG * MC), nunits = gridDim.x / (CG * MC);
+    const int tfirst = unit * MC + pair, tstride = nunits * MC;
 
     if (warp == 0) {
         constexpr bool kGatherKind = KIND == GemmKind::FwdGateUp || KIND == GemmKind::WgradGateUp;
@@ -765,7 +804,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
             // issues the 4-row pieces of the A tile (32 per stage), lane 0 the barrier and B
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = unit; t < ntiles; t += nunits) {
+            for (int t = tfirst; t < ntiles; t += tstride) {
                 const TileInfo ti = tile_info<KIND, CG>(p, ps, t);
                 const int m_own = ti.m0 + BM * (int)rank;
                 int4 rows_fwd = make_int4(0, 0, 0, 0);
@@ -775,10 +814,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                     mbar_wait(empty_bar(stage), phase ^ 1u, 0);
                     const uint32_t sA = base + stage * C::STAGE_BYTES, sB = sA + A_BYTES;
                     uint32_t fb = full_bar(stage);
-                    if constexpr (CG == 2) fb = map_to_rank(fb, 0);
+                    if constexpr (CG == 2) fb = map_to_rank(fb, lead);
                     if (lane == 0) {
                         if (leader) mbar_expect_tx(full_bar(stage), p.stage_tx);
-                        load_stage<KIND, CG>(p, ti, kb, m_own, rank, sA, sB, fb);  // B only in gather mode
+                        load_stage<KIND, CG>(p, ti, kb, m_own, rank, sA, sB, fb);  // B only in gather mode (MC = 1)
                     }
                     const int k0 = kb * BK;
                     if constexpr (KIND == GemmKind::FwdGateUp) {
@@ -798,16 +837,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
         } else if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = unit; t < ntiles; t += nunits) {
+            for (int t = tfirst; t < ntiles; t += tstride) {
                 const TileInfo ti = tile_info<KIND, CG>(p, ps, t);
                 const int m_own = ti.m0 + BM * (int)rank;
                 for (int kb = 0; kb < ti.kb; ++kb) {
                     mbar_wait(empty_bar(stage), phase ^ 1u, 0);
                     const uint32_t sA = base + stage * C::STAGE_BYTES, sB = sA + A_BYTES;
                     uint32_t fb = full_bar(stage);
-                    if constexpr (CG == 2) fb = map_to_rank(fb, 0);
+                    if constexpr (CG == 2) fb = map_to_rank(fb, lead);
                     if (leader) mbar_expect_tx(full_bar(stage), p.stage_tx);
-                    load_stage<KIND, CG>(p, ti, kb, m_own, rank, sA, sB, fb);
+                    load_stage<KIND, CG, MC>(p, ti, kb, m_own, rank, sA, sB, fb, pair);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
+            if constexpr (MC == 2) {
+                // tail: every stage's last release (from both pairs' MMAs) has landed in this CTA's
+                // barriers before the CTA can leave the cluster
+                for (int i = 0; i < STAGES; ++i) {
+                    mbar_wait(empty_bar(stage), phase ^ 1u, 4);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1u;
@@ -820,7 +870,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int t = unit; t < ntiles; t += nunits, ++it) {
+            for (int t = tfirst; t < ntiles; t += tstride, ++it) {
                 const TileInfo ti = tile_info<KIND, CG>(p, ps, t);
                 const int acc = it & 1;
                 const uint32_t acc_phase = (it >> 1) & 1;
@@ -842,6 +892,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                         else umma_f16_cg2(tacc, ad, bd, idesc, (kb | k) ? 1u : 0u);
                     }
                     if constexpr (CG == 1) umma_commit(empty_bar(stage));
+                    else if constexpr (MC == 2) umma_commit_cg2_mask(empty_bar(stage), (uint16_t)0xF);
                     else umma_commit_cg2(empty_bar(stage));
                     if (++stage == STAGES) {
                         stage = 0;
@@ -850,17 +901,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                 }
                 if (ti.kb > 0) {
                     if constexpr (CG == 1) umma_commit(tfull_bar(acc));
-                    else umma_commit_cg2(tfull_bar(acc));
+                    else umma_commit_cg2_mask(tfull_bar(acc), pair_mask);
                 } else {  // empty K range: nothing to wait for, the epilogues store zeros
                     mbar_arrive(tfull_bar(acc));
-                    if constexpr (CG == 2) mbar_arrive_cluster(map_to_rank(tfull_bar(acc), 1));
+                    if constexpr (CG == 2) mbar_arrive_cluster(map_to_rank(tfull_bar(acc), crank | 1u));
                 }
             }
         }
     } else if (warp >= 4) {
         const int quad = warp % 4;        // TMEM lanes 32*quad .. 32*quad+31 (hardware rule: warp id % 4)
         const int half = (warp - 4) / 4;  // column half of the tile
-        const uint32_t tempty0 = CG == 2 ? map_to_rank(tempty_bar(0), 0) : tempty_bar(0);
+        const uint32_t tempty0 = CG == 2 ? map_to_rank(tempty_bar(0), lead) : tempty_bar(0);
         // BwdDownDgrad: per-warp G/U staging buffer + mbarrier, one chunk ahead
         const int ew = warp - 4;
         const uint32_t gu_s = epi_base + (uint32_t)(ew * KC::WARP_EPI_BYTES);
@@ -879,14 +930,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
             }
         };
         if constexpr (KIND == GemmKind::BwdDownDgrad) {
-            if (unit < ntiles) {
-                TileInfo t0i = tile_info<KIND, CG>(p, ps, unit);
+            if (tfirst < ntiles) {
+                TileInfo t0i = tile_info<KIND, CG>(p, ps, tfirst);
                 t0i.m0 += BM * (int)rank;
                 gu_issue(t0i, half * (BN / 2));
             }
         }
         int it = 0;
-        for (int t = unit; t < ntiles; t += nunits, ++it) {
+        for (int t = tfirst; t < ntiles; t += tstride, ++it) {
             TileInfo ti = tile_info<KIND, CG>(p, ps, t);
             ti.m0 += BM * (int)rank;  // this CTA's 128 rows of the pair's tile
             const int acc = it & 1;
@@ -924,8 +975,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                     // the staging buffer is free again: fetch the next chunk (or the next tile's first)
                     if (c + 32 < (half + 1) * (BN / 2)) {
                         gu_issue(ti, c + 32);
-                    } else if (t + nunits < ntiles) {
-                        TileInfo tn = tile_info<KIND, CG>(p, ps, t + nunits);
+                    } else if (t + tstride < ntiles) {
+                        TileInfo tn = tile_info<KIND, CG>(p, ps, t + tstride);
                         tn.m0 += BM * (int)rank;
                         gu_issue(tn, half * (BN / 2));
                     }
@@ -1110,15 +1161,39 @@ static CUtensorMap make_store_map(const void* ptr, int64_t cols, int64_t rows) {
     return make_map(ptr, cols, rows, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
-template <GemmKind KIND, int CG>
+template <GemmKind KIND, int CG, int MC = 1>
 static void launch_kind(const Params& p, int grid, cudaStream_t st) {
     static std::once_flag once;
+    static int max_clusters = 0;  // co-resident clusters of CG * MC CTAs (GPC packing)
     constexpr int smem = KCfg<KIND, CG>::SMEM;
+    constexpr int CS = CG * MC;
     std::call_once(once, [] {
-        B2_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<KIND, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        B2_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<KIND, CG, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      smem));
+        cudaLaunchConfig_t q{};
+        q.gridDim = dim3(148);
+        q.blockDim = dim3(NUM_THREADS);
+        q.dynamicSmemBytes = smem;
+        cudaLaunchAttribute ca[1];
+        ca[0].id = cudaLaunchAttributeClusterDimension;
+        ca[0].val.clusterDim.x = CS;
+        ca[0].val.clusterDim.y = 1;
+        ca[0].val.clusterDim.z = 1;
+        q.attrs = ca;
+        q.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&max_clusters, grouped_gemm_kernel<KIND, CG, MC>, &q) != cudaSuccess) {
+            cudaGetLastError();
+            max_clusters = 0;
+        }
     });
-    grid = std::max(CG, grid / CG * CG);
+    if (max_clusters > 0) grid = std::min(grid, max_clusters * CS);
+    grid = std::max(CS, grid / CS * CS);
+    static bool said = false;
+    if (!said && getenv("B2_GEMM_DEBUG")) {
+        said = true;
+        fprintf(stderr, "b2 gemm kind %d: cluster %d, max active clusters %d, grid %d\n", (int)KIND, CS, max_clusters,
+                grid);
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(NUM_THREADS);
@@ -1126,14 +1201,14 @@ static void launch_kind(const Params& p, int grid, cudaStream_t st) {
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.x = CS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    B2_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<KIND, CG>, p));
+    B2_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<KIND, CG, MC>, p));
 }
 
 }  // namespace sm100
@@ -1151,6 +1226,21 @@ bool sm100_available() {
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
     cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
     return major == 10 && minor == 0;
+}
+
+// Opt-in (B2_GEMM_MC=2): clusters of two CTA pairs sharing the A operand by TMA multicast
+// (MC = 2) for the six expert kinds whose N tiles come in pairs. Correct (all GPU parity tests
+// pass under it) but not faster on B200: only 33 four-CTA clusters are co-resident (132 of 148
+// SMs), the GEMMs run power-limited (SM clock 1.45 GHz with 148 SMs, 1.6 GHz with 132), and the
+// per-kind times came out within -2 .. +2 % of the single-pair kernels (ncu, round 1 session 3)
+// while the step was 6 % slower on the same box. Single-pair clusters stay the default.
+static bool gemm_mc_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("B2_GEMM_MC");
+        v = (e && atoi(e) == 2) ? 1 : 0;
+    }
+    return v == 1;
 }
 
 void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
@@ -1191,8 +1281,10 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
     p.S = a.S;
     p.N = a.N;
     p.counts = a.counts;
-    // the six expert GEMMs run as 256 x 256 tiles on CTA pairs (cta_group::2)
+    // the six expert GEMMs run as 256 x 256 tiles on CTA pairs (cta_group::2); opt-in: two
+    // pairs per cluster sharing A by multicast where the N tiles pair up
     constexpr int G = 2;
+    const bool mc_ok = gemm_mc_enabled();
     using C2 = Cfg<G>;
     p.stage_tx = G * C2::STAGE_BYTES;
     switch (a.kind) {
@@ -1213,47 +1305,59 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             break;
     }
     switch (a.kind) {
-        case GemmKind::FwdGateUp:
-            p.mapA = a.gather_rows ? make_map(a.x, H, a.gather_tokens, 64, 1) : make_map(a.x, H, P, 64, BM);
+        case GemmKind::FwdGateUp: {
+            p.n_tiles = (int)ceil_div(I, BN / 2);
+            const bool mc = mc_ok && !a.gather_rows && p.n_tiles % 2 == 0;
+            p.mapA = a.gather_rows ? make_map(a.x, H, a.gather_tokens, 64, 1) : make_map(a.x, H, P, 64, mc ? 64 : BM);
             p.mapB0 = make_map(a.wg, I, nr * H, 64, 64);
             p.mapB1 = make_map(a.wu, I, nr * H, 64, 64);
             p.mapO0 = make_store_map(a.out0, I, P);
             p.mapO1 = make_store_map(a.out1, I, P);
             p.mapO2 = make_store_map(a.out2, I, P);
-            p.n_tiles = (int)ceil_div(I, BN / 2);
             p.num_kb_fixed = (int)ceil_div(H, BK);
-            launch_kind<GemmKind::FwdGateUp, G>(p, grid, st);
+            if (mc) launch_kind<GemmKind::FwdGateUp, G, 2>(p, grid, st);
+            else launch_kind<GemmKind::FwdGateUp, G>(p, grid, st);
             break;
-        case GemmKind::FwdDown:
-            p.mapA = make_map(a.h, I, P, 64, BM);
+        }
+        case GemmKind::FwdDown: {
+            p.n_tiles = (int)ceil_div(H, BN);
+            const bool mc = mc_ok && p.n_tiles % 2 == 0;
+            p.mapA = make_map(a.h, I, P, 64, mc ? 64 : BM);
             p.mapB0 = make_map(a.wd, H, nr * I, 64, 64);
             p.mapB1 = p.mapB0;
             p.mapO0 = make_store_map(a.out0, H, P);
-            p.n_tiles = (int)ceil_div(H, BN);
             p.num_kb_fixed = (int)ceil_div(I, BK);
-            launch_kind<GemmKind::FwdDown, G>(p, grid, st);
+            if (mc) launch_kind<GemmKind::FwdDown, G, 2>(p, grid, st);
+            else launch_kind<GemmKind::FwdDown, G>(p, grid, st);
             break;
-        case GemmKind::BwdDownDgrad:
-            p.mapA = make_map(a.dy, H, P, 64, BM);
+        }
+        case GemmKind::BwdDownDgrad: {
+            p.n_tiles = (int)ceil_div(I, BN);
+            const bool mc = mc_ok && p.n_tiles % 2 == 0;
+            p.mapA = make_map(a.dy, H, P, 64, mc ? 64 : BM);
             p.mapB0 = make_map(a.wd, H, nr * I, 64, C2::B_COLS);
             p.mapB1 = p.mapB0;
             p.mapG = make_map(a.g, I, P, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
             p.mapU = make_map(a.u, I, P, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
             p.mapO0 = make_store_map(a.out0, 2 * I, P);
-            p.n_tiles = (int)ceil_div(I, BN);
             p.num_kb_fixed = (int)ceil_div(H, BK);
-            launch_kind<GemmKind::BwdDownDgrad, G>(p, grid, st);
+            if (mc) launch_kind<GemmKind::BwdDownDgrad, G, 2>(p, grid, st);
+            else launch_kind<GemmKind::BwdDownDgrad, G>(p, grid, st);
             break;
-        case GemmKind::BwdDx:
-            p.mapA = make_map(a.dgu, 2 * I, P, 64, BM);
+        }
+        case GemmKind::BwdDx: {
+            p.n_tiles = (int)ceil_div(H, BN);
+            const bool mc = mc_ok && p.n_tiles % 2 == 0;
+            p.mapA = make_map(a.dgu, 2 * I, P, 64, mc ? 64 : BM);
             p.mapB0 = make_map(a.wg, I, nr * H, 64, C2::B_COLS);
             p.mapB1 = make_map(a.wu, I, nr * H, 64, C2::B_COLS);
             p.mapO0 = make_store_map(a.out0, H, P);
-            p.n_tiles = (int)ceil_div(H, BN);
             p.num_kb_fixed = (int)ceil_div(2 * I, BK);
-            launch_kind<GemmKind::BwdDx, G>(p, grid, st);
+            if (mc) launch_kind<GemmKind::BwdDx, G, 2>(p, grid, st);
+            else launch_kind<GemmKind::BwdDx, G>(p, grid, st);
             break;
-        case GemmKind::WgradDown:
+        }
+        case GemmKind::WgradDown: {
             check(a.counts != nullptr, "wgrad: expert row counts required");
             p.mapA = make_map(a.h, I, P, 64, 64);
             p.mapB0 = make_map(a.dy, H, P, 64, 64);
@@ -1262,9 +1366,11 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.m_tiles_fixed = (int)ceil_div(I, BM * G);
             p.n_tiles = (int)ceil_div(H, BN);
             grid = (int)std::min<int64_t>(grid, G * nr * p.m_tiles_fixed * p.n_tiles);
-            launch_kind<GemmKind::WgradDown, G>(p, grid, st);
+            if (mc_ok && p.n_tiles % 2 == 0) launch_kind<GemmKind::WgradDown, G, 2>(p, grid, st);
+            else launch_kind<GemmKind::WgradDown, G>(p, grid, st);
             break;
-        case GemmKind::WgradGateUp:
+        }
+        case GemmKind::WgradGateUp: {
             check(a.counts != nullptr, "wgrad: expert row counts required");
             p.mapA = a.gather_rows ? make_map(a.x, H, a.gather_tokens, 64, 1) : make_map(a.x, H, P, 64, 64);
             p.mapB0 = make_map(a.dgu, 2 * I, P, 64, 64);
@@ -1274,8 +1380,10 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.m_tiles_fixed = (int)ceil_div(H, BM * G);
             p.n_tiles = (int)ceil_div(2 * I, BN);
             grid = (int)std::min<int64_t>(grid, G * nr * p.m_tiles_fixed * p.n_tiles);
-            launch_kind<GemmKind::WgradGateUp, G>(p, grid, st);
+            if (mc_ok && !a.gather_rows && p.n_tiles % 2 == 0) launch_kind<GemmKind::WgradGateUp, G, 2>(p, grid, st);
+            else launch_kind<GemmKind::WgradGateUp, G>(p, grid, st);
             break;
+        }
         case GemmKind::RouterDx: {
             check(a.N % 8 == 0 && a.N <= 256, "router dx GEMM: n_experts must be a multiple of 8, <= 256");
             const int64_t S = a.S;
