@@ -345,6 +345,84 @@ void launch_ep_table_pull(const int32_t* const* peer_ids, const float* const* pe
     B2_LAUNCH_CHECK();
 }
 
+// ---- visiting order of the m-tiles for the fused pull (GEMM-side dispatch overlap) ----------
+// bucket[tile] = latest rotated gathered token among the tile's rows * nb / (E * S); rows are
+// pulled in rotated order (this rank's own tokens first), so a tile's bucket says when its last
+// row lands
+__global__ void ep_tile_bucket_kernel(const int32_t* __restrict__ prow_src, const int32_t* __restrict__ p_total,
+                                      int S, int E, int me, int nb, int max_tiles, int32_t* __restrict__ bucket) {
+    pdl_wait();
+    pdl_launch();
+    const int lane = threadIdx.x % 32;
+    const int ntiles = min(max_tiles, p_total[0] / kRowAlign);
+    const int nw = gridDim.x * blockDim.x / 32;
+    for (int tile = (blockIdx.x * blockDim.x + threadIdx.x) / 32; tile < ntiles; tile += nw) {
+        int key = -1;
+        for (int r = lane; r < kRowAlign; r += 32) {
+            const int gid = prow_src[(int64_t)tile * kRowAlign + r];
+            if (gid >= 0) key = max(key, ((gid / S - me + E) % E) * S + gid % S);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
+        if (lane == 0) bucket[tile] = key < 0 ? 0 : (int)((int64_t)key * nb / ((int64_t)E * S));
+    }
+}
+
+// one block: the buckets staged in shared memory, then thread b = bucket b counts, an exclusive
+// scan, and each bucket writes its tiles in ascending order (stable)
+__global__ void __launch_bounds__(256) ep_tile_order_kernel(const int32_t* __restrict__ bucket,
+                                                            const int32_t* __restrict__ p_total, int nb, int max_tiles,
+                                                            int32_t* __restrict__ order) {
+    pdl_wait();
+    pdl_launch();
+    extern __shared__ int32_t sbk[];
+    __shared__ int cnt[256];
+    const int b = threadIdx.x;
+    const int ntiles = min(max_tiles, p_total[0] / kRowAlign);
+    for (int i = b; i < ntiles; i += blockDim.x) sbk[i] = bucket[i];
+    __syncthreads();
+    int c = 0;
+    if (b < nb)
+        for (int i = 0; i < ntiles; ++i) c += sbk[i] == b;
+    cnt[b] = c;
+    __syncthreads();
+    if (b == 0) {
+        int run = 0;
+        for (int q = 0; q < nb; ++q) {
+            const int v = cnt[q];
+            cnt[q] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    if (b < nb) {
+        int at = cnt[b];
+        for (int i = 0; i < ntiles; ++i)
+            if (sbk[i] == b) order[at++] = i;
+    }
+}
+
+void launch_ep_tile_order(const int32_t* prow_src, const int32_t* p_total, int S, int E, int me, int max_tiles,
+                          int32_t* bucket, int32_t* order, cudaStream_t st) {
+    if (max_tiles <= 0) return;
+    // one bucket per source: within a bucket the tiles stay in padded-row (expert-major) order,
+    // so each expert's weights are streamed once per source pass instead of once per m-tile
+    // (8 buckets per source interleaved the experts and re-read every weight tile from HBM)
+    const int nb = std::min(256, E);
+    check((size_t)max_tiles * 4 <= 200 * 1024, "ep tile order: too many m-tiles for one block");
+    static int smem_set = 0;
+    if (smem_set < max_tiles * 4 && max_tiles * 4 > 48 * 1024) {
+        B2_CUDA(cudaFuncSetAttribute(ep_tile_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_tiles * 4));
+        smem_set = max_tiles * 4;
+    }
+    launch_k(ep_tile_bucket_kernel, dim3((unsigned)std::min<int64_t>(1184, ceil_div(max_tiles, 8))), dim3(256), 0, st,
+             prow_src, p_total, S, E, me, nb, max_tiles, bucket);
+    B2_LAUNCH_CHECK();
+    launch_k(ep_tile_order_kernel, dim3(1), dim3(256), (size_t)max_tiles * 4, st, bucket, p_total, nb, max_tiles,
+             order);
+    B2_LAUNCH_CHECK();
+}
+
 static unsigned ep_grid(int64_t warps) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(148 * 16, ceil_div(warps, 8))); }
 
 template <typename T>

@@ -115,6 +115,22 @@ struct Params {
     int ep_S, ep_K;
     const int32_t* gather_rows;  // FwdGateUp / WgradGateUp: padded row -> token (gather4 mode)
     int gather_oob;              // the zero-filled row index used for pad rows (-1 entries)
+    // EP > 1 fused dispatch (FwdGateUp: token rows; BwdDownDgrad: dout rows + the output-reduction
+    // backward): warps 2-3 of every CTA pull the gathered tokens' rows over NVLink, in the rotated
+    // source order me, me+1, ..., write them to the A operand's padded rows and count them per
+    // 128-row block; the producer waits for its block's count before the tile's TMA loads, and the
+    // m-tiles are visited in `tile_order` (sorted by when their rows arrive)
+    const int32_t* tile_order;
+    int32_t* ready;                      // [P / 128] rows landed per block; null: no fused pull
+    const __nv_bfloat16* const* peer_rows;  // [E] x (FwdGateUp) or dout (BwdDownDgrad) of every rank
+    int ep_E, ep_me, ep_T;
+    const int32_t* pull_cec;             // cum_expert_counts [T + 1]
+    const int32_t* pull_slot_prow;       // slot -> padded row
+    const int32_t* pull_selk;            // BwdDownDgrad: slot -> top-k index
+    const float* pull_gw;                // BwdDownDgrad: gathered routing weights [T, K]
+    const __nv_bfloat16* pull_y;         // BwdDownDgrad: mlp_out rows (the weight-gradient dots)
+    __nv_bfloat16* pull_dst;             // mlp_in / dY rows
+    float* pull_wgrad;                   // BwdDownDgrad: top-k weight gradients [T, K]
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -464,7 +480,7 @@ __device__ __forceinline__ TileInfo tile_info(const Params& p, const int32_t* ps
         ti.krow0 = ps[ti.e];
         ti.kb = (p.counts[ti.e] + BK - 1) / BK;  // pad rows past the count are zero: skip them
     } else {
-        const int mt = t / p.n_tiles;
+        const int mt = p.tile_order ? p.tile_order[t / p.n_tiles] : t / p.n_tiles;
         ti.n0 = (t % p.n_tiles) * BN;
         ti.m0 = mt * TM;
         int lo = 0, hi = p.nr - 1;  // last expert whose padded start <= m0
@@ -719,6 +735,119 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const TileInfo& t
     }
 }
 
+__device__ __forceinline__ int ld_acquire(const int32_t* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// producer side of the fused pull: wait until the valid rows of this CTA's 128-row block have
+// landed (bounded: traps after ~20 s instead of hanging the GPU), then order the async-proxy
+// (TMA) reads after them
+__device__ __forceinline__ void wait_rows_ready(const Params& p, const TileInfo& ti, int m_own) {
+    const int32_t* ps = p.pad_start;
+    const int need = max(0, min(BM, ps[ti.e] + p.counts[ti.e] - m_own));
+    if (need == 0) return;
+    const int32_t* flag = p.ready + (m_own >> 7);
+    uint32_t spins = 0;
+    uint64_t t0 = 0;
+    while (ld_acquire(flag) < need) {
+        __nanosleep(64);
+        if ((++spins & 0x3FFFu) == 0) {
+            const uint64_t now = global_ns();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 20000000000ull) {
+                printf("b2 gemm: fused pull never delivered block %d (%d rows)\n", m_own >> 7, need);
+                __trap();
+            }
+        }
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// the pull itself (warps 2-3 of every CTA): gathered tokens in the rotated source order, one
+// token per warp, its remote row read once (8 x 16 B in flight per lane) and written to each of
+// its local padded rows; BwdDownDgrad scales by the routing weight and forms the weight-gradient
+// dots against mlp_out (output_reduction_backward, moe.hpp:271-298). Each written row bumps its
+// block's counter after a gpu-scope fence.
+template <GemmKind KIND>
+__device__ __forceinline__ void fused_pull(const Params& p, int pw, int npw, int lane) {
+    const int S = p.ep_S, E = p.ep_E, H = p.H, K = p.ep_K;
+    const int nv = H / 8;  // 16-byte vectors per row
+    for (int i = pw; i < p.ep_T; i += npw) {
+        const int src = (p.ep_me + i / S) % E, t = i % S;
+        const int gid = src * S + t;
+        const int j0 = p.pull_cec[gid], j1 = p.pull_cec[gid + 1];
+        if constexpr (KIND == GemmKind::BwdDownDgrad)
+            for (int k = lane; k < K; k += 32) p.pull_wgrad[(int64_t)gid * K + k] = 0.f;
+        if (j0 == j1) continue;
+        const int4* row = reinterpret_cast<const int4*>(p.peer_rows[src] + (int64_t)t * H);
+        constexpr int B = 8;
+        if constexpr (KIND == GemmKind::FwdGateUp) {
+            for (int v0 = 0; v0 < nv; v0 += 32 * B) {
+                int4 val[B];
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    const int v = v0 + lane + 32 * b;
+                    if (v < nv) val[b] = __ldcv(row + v);
+                }
+                for (int j = j0; j < j1; ++j) {
+                    int4* dst = reinterpret_cast<int4*>(p.pull_dst + (int64_t)p.pull_slot_prow[j] * H);
+#pragma unroll
+                    for (int b = 0; b < B; ++b) {
+                        const int v = v0 + lane + 32 * b;
+                        if (v < nv) dst[v] = val[b];
+                    }
+                }
+            }
+        } else {  // dY[r] = w * dout[t]; wgrad[t, k] = dout[t] . y[r] (fp32: bf16 products are exact)
+            for (int j = j0; j < j1; ++j) {
+                const int64_t r = p.pull_slot_prow[j];
+                const int k = p.pull_selk[j];
+                const float wv = p.pull_gw[(int64_t)gid * K + k];
+                const int4* yr = reinterpret_cast<const int4*>(p.pull_y + r * H);
+                int4* dst = reinterpret_cast<int4*>(p.pull_dst + r * H);
+                float dot = 0.f;
+                for (int v0 = 0; v0 < nv; v0 += 32 * B) {
+                    int4 g[B], yv[B];
+#pragma unroll
+                    for (int b = 0; b < B; ++b) {
+                        const int v = v0 + lane + 32 * b;
+                        if (v < nv) {
+                            g[b] = __ldcv(row + v);
+                            yv[b] = __ldg(yr + v);
+                        }
+                    }
+#pragma unroll
+                    for (int b = 0; b < B; ++b) {
+                        const int v = v0 + lane + 32 * b;
+                        if (v >= nv) continue;
+                        const uint32_t gw4[4] = {(uint32_t)g[b].x, (uint32_t)g[b].y, (uint32_t)g[b].z, (uint32_t)g[b].w};
+                        const uint32_t yw4[4] = {(uint32_t)yv[b].x, (uint32_t)yv[b].y, (uint32_t)yv[b].z,
+                                                 (uint32_t)yv[b].w};
+                        uint32_t o[4];
+#pragma unroll
+                        for (int z = 0; z < 4; ++z) {
+                            const float g0 = bf16_lo(gw4[z]), g1 = bf16_hi(gw4[z]);
+                            dot = __fmaf_rn(g0, bf16_lo(yw4[z]), dot);
+                            dot = __fmaf_rn(g1, bf16_hi(yw4[z]), dot);
+                            o[z] = pack_bf16(__fmul_rn(wv, g0), __fmul_rn(wv, g1));
+                        }
+                        dst[v] = make_int4((int)o[0], (int)o[1], (int)o[2], (int)o[3]);
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+                if (lane == 0) p.pull_wgrad[(int64_t)gid * K + k] = dot;
+            }
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0)
+            for (int j = j0; j < j1; ++j) atomicAdd(p.ready + (p.pull_slot_prow[j] >> 7), 1);
+    }
+}
+
 template <GemmKind KIND, int CG, int MC>
 __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __grid_constant__ Params p) {
     using C = Cfg<CG>;
@@ -840,6 +969,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
             for (int t = tfirst; t < ntiles; t += tstride) {
                 const TileInfo ti = tile_info<KIND, CG>(p, ps, t);
                 const int m_own = ti.m0 + BM * (int)rank;
+                if constexpr (KIND == GemmKind::FwdGateUp || KIND == GemmKind::BwdDownDgrad)
+                    if (p.ready) wait_rows_ready(p, ti, m_own);
                 for (int kb = 0; kb < ti.kb; ++kb) {
                     mbar_wait(empty_bar(stage), phase ^ 1u, 0);
                     const uint32_t sA = base + stage * C::STAGE_BYTES, sB = sA + A_BYTES;
@@ -908,6 +1039,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                 }
             }
         }
+    } else if (warp == 2 || warp == 3) {
+        if constexpr (KIND == GemmKind::FwdGateUp || KIND == GemmKind::BwdDownDgrad)
+            if (p.ready) fused_pull<KIND>(p, (int)blockIdx.x * 2 + (warp - 2), (int)gridDim.x * 2, lane);
     } else if (warp >= 4) {
         const int quad = warp % 4;        // TMEM lanes 32*quad .. 32*quad+31 (hardware rule: warp id % 4)
         const int half = (warp - 4) / 4;  // column half of the tile
@@ -1262,6 +1396,25 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
     p.out2 = (__nv_bfloat16*)a.out2;
     p.gather_rows = a.gather_rows;
     p.gather_oob = a.gather_tokens;
+    p.tile_order = a.tile_order;
+    p.ready = a.ready;
+    p.peer_rows = reinterpret_cast<const __nv_bfloat16* const*>(a.peer_rows);
+    p.ep_E = a.ep_E;
+    p.ep_me = a.ep_me;
+    p.ep_T = a.ep_T;
+    p.pull_cec = a.pull_cec;
+    p.pull_slot_prow = a.pull_slot_prow;
+    p.pull_selk = a.pull_selk;
+    p.pull_gw = a.pull_gw;
+    p.pull_y = (const __nv_bfloat16*)a.pull_y;
+    p.pull_dst = (__nv_bfloat16*)a.pull_dst;
+    p.pull_wgrad = a.pull_wgrad;
+    if (a.ready)
+        check((a.kind == GemmKind::FwdGateUp || a.kind == GemmKind::BwdDownDgrad) && a.tile_order && a.peer_rows &&
+                  a.ep_E > 1 && a.ep_S > 0 && a.ep_T == a.ep_E * a.ep_S && a.pull_cec && a.pull_slot_prow &&
+                  a.pull_dst && a.counts && !a.gather_rows &&
+                  (a.kind == GemmKind::FwdGateUp || (a.pull_selk && a.pull_gw && a.pull_y && a.pull_wgrad)),
+              "fused pull: FwdGateUp / BwdDownDgrad with the EP tables");
     p.peer_kslab = a.peer_kslab;
     p.prow_src = a.prow_src;
     p.prow_k = a.prow_k;

@@ -171,8 +171,26 @@ struct Sm100GemmArgs {
     const float* gw;             // [T, K] gathered routing weights (FwdDown)
     int ep_S, ep_K;              // tokens per rank, top-k
     int max_ctas;                // > 0: cap the persistent grid (SMs left to concurrent comm kernels)
+    // FwdGateUp / BwdDownDgrad at EP > 1: the fused pull (sm100::Params). Warps 2-3 of every CTA
+    // pull the gathered tokens' x (dout) rows over NVLink into mlp_in (dY) and count them per
+    // 128-row block in `ready`; the producer waits for its block; m-tiles visit in `tile_order`
+    const int32_t* tile_order;
+    int32_t* ready;
+    const void* const* peer_rows;
+    int ep_E, ep_me, ep_T;
+    const int32_t* pull_cec;
+    const int32_t* pull_slot_prow;
+    const int32_t* pull_selk;
+    const float* pull_gw;
+    const void* pull_y;
+    void* pull_dst;
+    float* pull_wgrad;
 };
 void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st);
+// EP fused pull: the visiting order of the 256-row m-tiles, by the latest rotated gathered token
+// ((src - me) mod E) * S + t among each tile's rows, one bucket per source (stable)
+void launch_ep_tile_order(const int32_t* prow_src, const int32_t* p_total, int S, int E, int me, int max_tiles,
+                          int32_t* bucket, int32_t* order, cudaStream_t st);
 // number of S splits the RouterDw kind uses (its partial buffer holds splits*H*N floats)
 int router_dw_splits(int64_t S, int64_t H, int num_sms);
 // sums RouterDw partials in split order into dW (T = bf16)

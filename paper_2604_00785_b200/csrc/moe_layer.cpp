@@ -14,6 +14,7 @@
 #include "moe_layer.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "comm.h"
@@ -95,6 +96,8 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
         for (int64_t n : {tmax_ * K, tmax_ * K, smax_ * K}) acc(4 * (size_t)std::max<int64_t>(n, 1));
         acc(es * (size_t)std::max<int64_t>(smax_ * H, 1));
         acc(es * (size_t)std::max<int64_t>(tmax_ * H, 1));  // x_all (copy-engine dispatch)
+        for (int64_t n : {pmax_ / 128 + 1, pmax_ / kRowAlign + 1, pmax_ / kRowAlign + 1})  // fused pull
+            acc(4 * (size_t)n);
     }
     B2_CUDA(cudaSetDevice(ctx_.device));
     if (share_ws) {
@@ -156,6 +159,11 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
         gw_all_ = w.take<float>(tmax_ * K);
         wgrad_local_ = w.take<float>(smax_ * K);
         dx_exp_ = w.take_bytes(es * (size_t)std::max<int64_t>(smax_ * H, 1));
+        max_mtiles_ = pmax_ / kRowAlign;
+        ready_ = w.take<int32_t>(pmax_ / 128 + 1);
+        tile_bucket_ = w.take<int32_t>(max_mtiles_ + 1);
+        tile_order_ = w.take<int32_t>(max_mtiles_ + 1);
+        if (const char* e = getenv("B2_EP_FUSED_PULL")) fused_pull_opt_ = atoi(e) != 0;
         x_all_ = w.take_bytes(es * (size_t)std::max<int64_t>(tmax_ * H, 1));
         ep_setup();
         B2_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
@@ -254,6 +262,24 @@ void MoeLayer::ep_setup() {
 }
 
 // every rank's preceding stream work (and its peer stores) is complete once this returns
+bool MoeLayer::fused_pull() const {
+    return dtype_ == BF16 && cfg_.ep > 1 && fused_pull_opt_ && !ce_dispatch_opt_ && !gather_in_gemm() && ready_;
+}
+
+void MoeLayer::set_pull_args(Sm100GemmArgs& ga, const void* const* peer_rows, void* dst, int S, int K, int Tt) const {
+    ga.ready = ready_;
+    ga.tile_order = tile_order_;
+    ga.peer_rows = peer_rows;
+    ga.ep_E = cfg_.ep;
+    ga.ep_me = ctx_.coord_ep;
+    ga.ep_S = S;
+    ga.ep_K = K;
+    ga.ep_T = Tt;
+    ga.pull_cec = cec_;
+    ga.pull_slot_prow = slot_prow_;
+    ga.pull_dst = dst;
+}
+
 void MoeLayer::ep_barrier(cudaStream_t st) {
     launch_ep_flag_barrier((int* const*)peer_tab_ + 6 * cfg_.ep, flags_, bar_, cfg_.ep, ctx_.coord_ep,
                            st ? st : ctx_.stream);
@@ -497,6 +523,13 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
             B2_CUDA(cudaStreamWaitEvent(st, ev_xall_, 0));
             launch_gather_rows<T>((const T*)x_all_, prow_src_, p_total, (T*)mlp_in_, H, pmax_, st);
             launches_ += 1;
+        } else if (fused_pull()) {
+            // the FwdGateUp kernel pulls the rows itself; pads first, counters zeroed, tile order
+            launch_zero_pad_rows<T>((T*)mlp_in_, prow_src_, p_total, H, pmax_, st);
+            B2_CUDA(cudaMemsetAsync(ready_, 0, 4 * (size_t)(pmax_ / 128 + 1), st));
+            launch_ep_tile_order(prow_src_, p_total, S, E, ctx_.coord_ep, (int)max_mtiles_, tile_bucket_, tile_order_,
+                                 st);
+            launches_ += 3;
         } else {
             launch_ep_gather_pull<T>((const T* const*)peer_tab_, S, Tt, H, cec_, slot_prow_, (T*)mlp_in_, st);
             launch_zero_pad_rows<T>((T*)mlp_in_, prow_src_, p_total, H, pmax_, st);
@@ -525,9 +558,12 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
         ga.out0 = g_;
         ga.out1 = u_;
         ga.out2 = h_;
+        if (E > 1 && fused_pull()) set_pull_args(ga, (const void* const*)peer_tab_, mlp_in_, S, K, Tt);
         mark(kGemmGateUp, false);
         launch_sm100_gemm(ga, st);
         mark(kGemmGateUp, true);
+        ga.ready = nullptr;
+        ga.tile_order = nullptr;
         ga.kind = GemmKind::FwdDown;
         ga.gather_rows = nullptr;
         if (fused_combine()) {  // w * y rows go straight into the sources' slabs over NVLink
@@ -662,10 +698,17 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
     }
     // EP > 1: the top-k weight gradients go straight into this rank's symmetric slab, where
     // the sources pull them from
-    launch_out_reduction_bwd<T>(dout, peer_dout, S, (const T*)y_, slot_prow_, selected_k_, cec_, gw_, (T*)dy_,
-                                E > 1 ? wret_ : wgrad_, Tt, H, K, st);
-    launch_zero_pad_rows<T>((T*)dy_, prow_src_, p_total, H, pmax_, st);
-    launches_ += 2;
+    const bool fpull = E > 1 && fused_pull();
+    if (fpull) {  // the dgrad GEMM pulls dout and forms dY / the weight-gradient dots itself
+        launch_zero_pad_rows<T>((T*)dy_, prow_src_, p_total, H, pmax_, st);
+        B2_CUDA(cudaMemsetAsync(ready_, 0, 4 * (size_t)(pmax_ / 128 + 1), st));
+        launches_ += 1;
+    } else {
+        launch_out_reduction_bwd<T>(dout, peer_dout, S, (const T*)y_, slot_prow_, selected_k_, cec_, gw_, (T*)dy_,
+                                    E > 1 ? wret_ : wgrad_, Tt, H, K, st);
+        launch_zero_pad_rows<T>((T*)dy_, prow_src_, p_total, H, pmax_, st);
+        launches_ += 2;
+    }
     mark(kOutRedBwd, true);
     if (dtype_ == BF16) {
         Sm100GemmArgs ga{};
@@ -688,9 +731,18 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         ga.scale = inv_ep;
         ga.kind = GemmKind::BwdDownDgrad;  // 406 + silu_glu_backward 409
         ga.out0 = dgu_;
+        if (fpull) {
+            set_pull_args(ga, (const void* const*)peer_tab_ + E, dy_, S, K, Tt);
+            ga.pull_selk = selected_k_;
+            ga.pull_gw = gw_;
+            ga.pull_y = y_;
+            ga.pull_wgrad = wret_;
+        }
         mark(kGemmDgrad, false);
         launch_sm100_gemm(ga, st);
         mark(kGemmDgrad, true);
+        ga.ready = nullptr;
+        ga.tile_order = nullptr;
         if (overlap_return()) {
             // EP > 1: dX first, then its return to the source ranks (owner combine, barrier,
             // NVLink pull-sums: the reducescatters of moe.hpp:427-428) runs on a side stream

@@ -12,6 +12,8 @@
 
 namespace b2 {
 
+struct Sm100GemmArgs;
+
 struct MoeConfig {  // moe.hpp:13-31
     int64_t n_experts = 8, top_k = 2, hidden = 64, intermediate = 128;
     int ep = 1;
@@ -154,6 +156,17 @@ class MoeLayer {
     // slower (7.65 vs 5.32 ms per EP=2 step): each lane's 64-byte remote stores to scattered
     // rows make the epilogue NVLink-bound; the owner-local combine + coalesced pull is default
     bool fused_combine() const;
+    // bf16, EP > 1, opt-in (B2_EP_FUSED_PULL=1): the dispatch pull of x rows and the dout pull +
+    // output-reduction backward run inside the FwdGateUp / dgrad GEMM kernels (warps 2-3 of every
+    // CTA), tile by tile ahead of the MMAs that consume them (per-128-row arrival counters, m-tiles
+    // visited by source). Correct (EP parity tests pass under it) but measured slower at EP=2
+    // (6.36 vs 5.29 ms per step): 296 pulling warps keep too few NVLink bytes in flight to feed the
+    // GEMM, which then waits on its rows; the standalone pull kernels (~19k warps) stay default
+    bool fused_pull() const;
+    void set_pull_args(Sm100GemmArgs& ga, const void* const* peer_rows, void* dst, int S, int K, int Tt) const;
+    bool fused_pull_opt_ = false;
+    int32_t *ready_ = nullptr, *tile_bucket_ = nullptr, *tile_order_ = nullptr;
+    int64_t max_mtiles_ = 0;
     bool fused_combine_opt_ = false;  // bf16, EP = 1, opted in: GEMMs gather X rows by TMA gather4
     bool tma_gather_ = false;     // off by default: measured 1.9x slower GEMMs (32 TMA ops/stage)
 
