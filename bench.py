@@ -524,7 +524,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded randn tokens, random-init weights)",
             "config": {"workload": WORKLOAD, "global_batch_tokens": world * S,
-                       "parallelism": f"ep{world} (all-to-all dispatch/combine over NCCL)" if world > 1 else "ep1",
+                       "parallelism": f"ep{world} (dispatch/combine over NVLink peer memory)" if world > 1 else "ep1",
                        "l2": "working set (weights 0.8 GB + activations ~4 GB) >> 126 MB L2; no flush needed",
                        "host_cpus_bound": numa},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
