@@ -32,8 +32,10 @@ def run_world(world, case):
     port = free_port()
     with tempfile.TemporaryDirectory() as td:
         res = os.path.join(td, "res.json")
+        case = dict(case)
+        env = dict(os.environ, **case.pop("env", {}))  # opt-in kernel variants (A/B hooks)
         procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "ep_worker.py"), str(r), str(world), str(port),
-                                   json.dumps(case), res]) for r in range(world)]
+                                   json.dumps(case), res], env=env) for r in range(world)]
         for p in procs:
             assert p.wait(timeout=600) == 0
         with open(res) as f:
@@ -51,12 +53,19 @@ CASES = [
          graph=True),
     dict(n_experts=64, top_k=8, hidden=256, intermediate=128, token_block=8, s=512, dtype="bf16", fused=True),
     dict(n_experts=16, top_k=4, hidden=256, intermediate=128, token_block=8, s=300, dtype="bf16", ce=True),
+    # opt-in variants: the dispatch / dout pulls fused into the GEMM kernels (captured in graphs),
+    # and the A-operand multicast across two CTA pairs (N tiles pair up at H=512, I=256)
+    dict(n_experts=64, top_k=8, hidden=256, intermediate=128, token_block=8, s=512, dtype="bf16", graph=True,
+         env={"B2_EP_FUSED_PULL": "1"}),
+    dict(n_experts=16, top_k=4, hidden=512, intermediate=256, token_block=8, s=300, dtype="bf16",
+         env={"B2_GEMM_MC": "2"}),
 ]
 
 
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c['dtype']}-n{c['n_experts']}k{c['top_k']}"
-                         + ("-ckpt-graph" if c.get("ckpt") else "") + ("-fused" if c.get("fused") else "") + ("-ce" if c.get("ce") else ""))
+                         + ("-ckpt-graph" if c.get("ckpt") else "") + ("-fused" if c.get("fused") else "") + ("-ce" if c.get("ce") else "")
+                         + "".join(f"-{k}={v}" for k, v in c.get("env", {}).items()))
 def test_ep_matches_oracle(world, case):
     if case["n_experts"] % world:
         pytest.skip("experts do not divide")
