@@ -340,7 +340,9 @@ __global__ void __launch_bounds__(1024) norm_final_kernel(const double* __restri
 
 // 256 threads x 4 blocks per SM: the fp64 divide / sqrt chains are long, so occupancy (not the
 // FP64 pipe, ~28 % busy at 3 blocks) is what keeps enough bytes in flight
-template <int MINB>
+// VW = elements per thread-iteration of the vectorised path (4: float4 / 8-byte grads; 2: float2
+// / 4-byte grads, fewer registers -> more resident warps)
+template <int MINB, int VW = 4>
 __global__ void __launch_bounds__(256, MINB) adamw_chunks_kernel(const OptSeg* __restrict__ segs,
                                                            const OptChunk* __restrict__ chunks,
                                                            const int32_t* __restrict__ ids, int nids, AdamWDev c,
@@ -357,7 +359,37 @@ __global__ void __launch_bounds__(256, MINB) adamw_chunks_kernel(const OptSeg* _
     for (int q = blockIdx.x; q < nids; q += gridDim.x) {
         const OptChunk ch = chunks[ids[q]];
         const OptSeg sg = segs[ch.seg];
-        if (sg.vec) {
+        if (VW == 2 && sg.vec) {
+            float2* ms = reinterpret_cast<float2*>(sg.master + ch.begin);
+            float2* mo = reinterpret_cast<float2*>(sg.m + ch.begin);
+            float2* ve = reinterpret_cast<float2*>(sg.v + ch.begin);
+            const uint32_t* gr =
+                reinterpret_cast<const uint32_t*>(static_cast<const __nv_bfloat16*>(sg.grad) + ch.begin);
+            uint32_t* wo = reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(sg.wout) + ch.begin);
+            const int64_t n2 = ch.len / 2;
+            for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) {
+                const uint32_t gb = __ldcs(gr + i);
+                float2 m0 = __ldcs(ms + i), a0 = __ldcs(mo + i), v0 = __ldcs(ve + i);
+                const float g[2] = {__uint_as_float(gb << 16), __uint_as_float(gb & 0xFFFF0000u)};
+                float* fm = &m0.x;
+                float* fa = &a0.x;
+                float* fv = &v0.x;
+                uint32_t wb[2];
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    float gq = g[k];
+                    if (sg.scale != 1.f) gq = __fmul_rn(gq, sg.scale);
+                    if (clip != 1.0) gq = (float)__dmul_rn((double)gq, clip);
+                    float wf;
+                    adamw_elem(fm[k], fa[k], fv[k], gq, c, wf);
+                    wb[k] = bf16_bits_rne(wf);
+                }
+                __stcs(ms + i, m0);
+                __stcs(mo + i, a0);
+                __stcs(ve + i, v0);
+                __stcs(wo + i, wb[0] | (wb[1] << 16));
+            }
+        } else if (sg.vec) {
             float4* ms = reinterpret_cast<float4*>(sg.master + ch.begin);
             float4* mo = reinterpret_cast<float4*>(sg.m + ch.begin);
             float4* ve = reinterpret_cast<float4*>(sg.v + ch.begin);
@@ -663,17 +695,24 @@ void launch_adamw_chunks(const OptSeg* segs, const OptChunk* chunks, const int32
     }
     static int minb = 0, grid_cap = 0;  // resident blocks on the whole GPU (persistent grid)
     if (grid_cap == 0) {
-        const char* env = getenv("B2_ADAMW_MINB");  // A/B hook: 3 (no spills) or 4 (more warps)
-        minb = env && atoi(env) == 3 ? 3 : 4;
+        // A/B hook: 3 (no spills), 4 (default: more warps), 6 (pairs of elements, 48 warps/SM)
+        const char* env = getenv("B2_ADAMW_MINB");
+        minb = env ? atoi(env) : 4;
+        if (minb != 3 && minb != 6) minb = 4;
         int dev = 0, sms = 148, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (minb == 3) B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adamw_chunks_kernel<3>, 256, 0));
+        else if (minb == 6)
+            B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adamw_chunks_kernel<6, 2>, 256, 0));
         else B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adamw_chunks_kernel<4>, 256, 0));
         grid_cap = sms * std::max(1, per_sm);
     }
     const int grid = std::min(nids, grid_cap);
     if (minb == 3) launch_k(adamw_chunks_kernel<3>, dim3(grid), dim3(256), 0, st, segs, chunks, ids, nids, c, a, norm_sq, nonfinite);
+    else if (minb == 6)
+        launch_k(adamw_chunks_kernel<6, 2>, dim3(grid), dim3(256), 0, st, segs, chunks, ids, nids, c, a, norm_sq,
+                 nonfinite);
     else launch_k(adamw_chunks_kernel<4>, dim3(grid), dim3(256), 0, st, segs, chunks, ids, nids, c, a, norm_sq, nonfinite);
     B2_LAUNCH_CHECK();
 }
