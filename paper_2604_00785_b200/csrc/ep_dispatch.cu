@@ -423,6 +423,71 @@ void launch_ep_tile_order(const int32_t* prow_src, const int32_t* p_total, int S
     B2_LAUNCH_CHECK();
 }
 
+// The dispatch pull as a kernel that runs NEXT TO the FwdGateUp GEMM: one 256-thread block per
+// SM fits beside a GEMM CTA (<= 48 registers per thread: 12 K registers next to the GEMM's 52 K,
+// no shared memory), so 8 pulling warps per SM stream the gathered tokens' rows in rotated source
+// order (own rows first) while the GEMM's producers wait on the per-128-row arrival counters and
+// visit the m-tiles source by source. Each row is pulled once (8 x 16 B in flight per lane) and
+// written to all of its local padded rows, then counted after a gpu-scope fence.
+__global__ void __launch_bounds__(256, 5) ep_pull_rows_kernel(const __nv_bfloat16* const* __restrict__ peer_src,
+                                                              int S, int E, int me, int H,
+                                                              const int32_t* __restrict__ cec,
+                                                              const int32_t* __restrict__ slot_prow,
+                                                              __nv_bfloat16* __restrict__ out,
+                                                              int32_t* __restrict__ ready) {
+    pdl_wait();
+    pdl_launch();
+    const int lane = threadIdx.x % 32;
+    const int nw = gridDim.x * blockDim.x / 32;
+    const int T = E * S, nv = H / 8;
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) / 32; i < T; i += nw) {
+        const int src = (me + i / S) % E, t = i % S;
+        const int gid = src * S + t;
+        const int j0 = cec[gid], j1 = cec[gid + 1];
+        if (j0 == j1) continue;
+        const int4* row = reinterpret_cast<const int4*>(peer_src[src] + (int64_t)t * H);
+        constexpr int B = 8;
+        for (int v0 = 0; v0 < nv; v0 += 32 * B) {
+            int4 val[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const int v = v0 + lane + 32 * b;
+                if (v < nv) val[b] = __ldcv(row + v);
+            }
+            for (int j = j0; j < j1; ++j) {
+                int4* dst = reinterpret_cast<int4*>(out + (int64_t)slot_prow[j] * H);
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    const int v = v0 + lane + 32 * b;
+                    if (v < nv) dst[v] = val[b];
+                }
+            }
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0)
+            for (int j = j0; j < j1; ++j) atomicAdd(ready + (slot_prow[j] >> 7), 1);
+    }
+}
+
+void launch_ep_pull_rows(const void* const* peer_src, int S, int E, int me, int H, const int32_t* cec,
+                         const int32_t* slot_prow, void* out, int32_t* ready, int num_sms, cudaStream_t st) {
+    if (S <= 0) return;
+    check(H % 8 == 0, "ep pull: rows must be 16-byte multiples");
+    static bool carve = false;
+    if (!carve) {
+        // the SM's shared-memory carveout can only change while it is idle: ask for the full
+        // carveout (as the GEMM does), or a pull block landing first would keep the GEMM CTA out
+        B2_CUDA(cudaFuncSetAttribute(ep_pull_rows_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     (int)cudaSharedmemCarveoutMaxShared));
+        carve = true;
+    }
+    launch_k(ep_pull_rows_kernel, dim3((unsigned)std::max(1, num_sms)), dim3(256), 0, st,
+             reinterpret_cast<const __nv_bfloat16* const*>(peer_src), S, E, me, H, cec, slot_prow,
+             static_cast<__nv_bfloat16*>(out), ready);
+    B2_LAUNCH_CHECK();
+}
+
 static unsigned ep_grid(int64_t warps) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(148 * 16, ceil_div(warps, 8))); }
 
 template <typename T>

@@ -1041,7 +1041,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
         }
     } else if (warp == 2 || warp == 3) {
         if constexpr (KIND == GemmKind::FwdGateUp || KIND == GemmKind::BwdDownDgrad)
-            if (p.ready) fused_pull<KIND>(p, (int)blockIdx.x * 2 + (warp - 2), (int)gridDim.x * 2, lane);
+            if (p.ready && p.pull_dst) fused_pull<KIND>(p, (int)blockIdx.x * 2 + (warp - 2), (int)gridDim.x * 2, lane);
     } else if (warp >= 4) {
         const int quad = warp % 4;        // TMEM lanes 32*quad .. 32*quad+31 (hardware rule: warp id % 4)
         const int half = (warp - 4) / 4;  // column half of the tile
@@ -1409,7 +1409,11 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
     p.pull_y = (const __nv_bfloat16*)a.pull_y;
     p.pull_dst = (__nv_bfloat16*)a.pull_dst;
     p.pull_wgrad = a.pull_wgrad;
-    if (a.ready)
+    if (a.ready && !a.pull_dst)  // rows arrive from a concurrent pull kernel: wait only
+        check((a.kind == GemmKind::FwdGateUp || a.kind == GemmKind::BwdDownDgrad) && a.tile_order && a.counts &&
+                  !a.gather_rows,
+              "overlapped pull: FwdGateUp / BwdDownDgrad with a tile order");
+    else if (a.ready)
         check((a.kind == GemmKind::FwdGateUp || a.kind == GemmKind::BwdDownDgrad) && a.tile_order && a.peer_rows &&
                   a.ep_E > 1 && a.ep_S > 0 && a.ep_T == a.ep_E * a.ep_S && a.pull_cec && a.pull_slot_prow &&
                   a.pull_dst && a.counts && !a.gather_rows &&

@@ -189,6 +189,9 @@ struct Sm100GemmArgs {
 void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st);
 // EP fused pull: the visiting order of the 256-row m-tiles, by the latest rotated gathered token
 // ((src - me) mod E) * S + t among each tile's rows, one bucket per source (stable)
+// the dispatch pull beside the FwdGateUp GEMM (one block per SM, arrival counters per 128 rows)
+void launch_ep_pull_rows(const void* const* peer_src, int S, int E, int me, int H, const int32_t* cec,
+                         const int32_t* slot_prow, void* out, int32_t* ready, int num_sms, cudaStream_t st);
 void launch_ep_tile_order(const int32_t* prow_src, const int32_t* p_total, int S, int E, int me, int max_tiles,
                           int32_t* bucket, int32_t* order, cudaStream_t st);
 // number of S splits the RouterDw kind uses (its partial buffer holds splits*H*N floats)

@@ -164,6 +164,7 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
         tile_bucket_ = w.take<int32_t>(max_mtiles_ + 1);
         tile_order_ = w.take<int32_t>(max_mtiles_ + 1);
         if (const char* e = getenv("B2_EP_FUSED_PULL")) fused_pull_opt_ = atoi(e) != 0;
+        if (const char* e = getenv("B2_EP_OVERLAP_PULL")) overlap_pull_opt_ = atoi(e) != 0;
         x_all_ = w.take_bytes(es * (size_t)std::max<int64_t>(tmax_ * H, 1));
         ep_setup();
         B2_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
@@ -262,6 +263,11 @@ void MoeLayer::ep_setup() {
 }
 
 // every rank's preceding stream work (and its peer stores) is complete once this returns
+bool MoeLayer::overlap_pull() const {
+    return dtype_ == BF16 && cfg_.ep > 1 && overlap_pull_opt_ && !ce_dispatch_opt_ && !gather_in_gemm() && ready_ &&
+           side_ != nullptr;
+}
+
 bool MoeLayer::fused_pull() const {
     return dtype_ == BF16 && cfg_.ep > 1 && fused_pull_opt_ && !ce_dispatch_opt_ && !gather_in_gemm() && ready_;
 }
@@ -523,7 +529,7 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
             B2_CUDA(cudaStreamWaitEvent(st, ev_xall_, 0));
             launch_gather_rows<T>((const T*)x_all_, prow_src_, p_total, (T*)mlp_in_, H, pmax_, st);
             launches_ += 1;
-        } else if (fused_pull()) {
+        } else if (fused_pull() || overlap_pull()) {
             // the FwdGateUp kernel pulls the rows itself; pads first, counters zeroed, tile order
             launch_zero_pad_rows<T>((T*)mlp_in_, prow_src_, p_total, H, pmax_, st);
             B2_CUDA(cudaMemsetAsync(ready_, 0, 4 * (size_t)(pmax_ / 128 + 1), st));
@@ -559,9 +565,21 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
         ga.out1 = u_;
         ga.out2 = h_;
         if (E > 1 && fused_pull()) set_pull_args(ga, (const void* const*)peer_tab_, mlp_in_, S, K, Tt);
+        const bool opull = E > 1 && !fused_pull() && overlap_pull();
+        if (opull) {  // the pull kernel beside the GEMM, on the side stream
+            ga.ready = ready_;
+            ga.tile_order = tile_order_;
+            B2_CUDA(cudaEventRecord(ev_fork_, st));
+            B2_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+            launch_ep_pull_rows((const void* const*)peer_tab_, S, E, ctx_.coord_ep, H, cec_, slot_prow_, mlp_in_,
+                                ready_, ctx_.num_sms, side_);
+            B2_CUDA(cudaEventRecord(ev_join_, side_));
+            launches_ += 1;
+        }
         mark(kGemmGateUp, false);
         launch_sm100_gemm(ga, st);
         mark(kGemmGateUp, true);
+        if (opull) B2_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
         ga.ready = nullptr;
         ga.tile_order = nullptr;
         ga.kind = GemmKind::FwdDown;

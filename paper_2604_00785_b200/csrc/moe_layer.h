@@ -165,6 +165,13 @@ class MoeLayer {
     bool fused_pull() const;
     void set_pull_args(Sm100GemmArgs& ga, const void* const* peer_rows, void* dst, int S, int K, int Tt) const;
     bool fused_pull_opt_ = false;
+    // bf16, EP > 1, opt-in (B2_EP_OVERLAP_PULL=1): the forward's dispatch pull as a kernel
+    // co-resident with the FwdGateUp GEMM (one 8-warp block per SM beside each GEMM CTA, side
+    // stream), the GEMM waiting on per-block arrival counters. Correct, measured slower at EP=4
+    // (6.19-6.21 vs 6.04-6.06 ms): the pull slows to ~435 GB/s beside the GEMM, below the rate the
+    // GEMM consumes its A rows, and the source-major tile order costs weight locality
+    bool overlap_pull() const;
+    bool overlap_pull_opt_ = false;
     int32_t *ready_ = nullptr, *tile_bucket_ = nullptr, *tile_order_ = nullptr;
     int64_t max_mtiles_ = 0;
     bool fused_combine_opt_ = false;  // bf16, EP = 1, opted in: GEMMs gather X rows by TMA gather4

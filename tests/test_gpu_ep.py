@@ -59,6 +59,8 @@ CASES = [
          env={"B2_EP_FUSED_PULL": "1"}),
     dict(n_experts=16, top_k=4, hidden=512, intermediate=256, token_block=8, s=300, dtype="bf16",
          env={"B2_GEMM_MC": "2"}),
+    dict(n_experts=64, top_k=8, hidden=256, intermediate=128, token_block=8, s=512, dtype="bf16", graph=True,
+         env={"B2_EP_OVERLAP_PULL": "1"}),
 ]
 
 

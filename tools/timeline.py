@@ -89,10 +89,17 @@ def main():
         for _ in range(args.steps):
             step()
         torch.cuda.synchronize()
-    if rank != 0:
-        return
     ev = [e for e in prof.events() if e.device_type.name == "CUDA" and e.time_range.elapsed_us() > 0]
     ev.sort(key=lambda e: e.time_range.start)
+    if world > 1:  # per-rank view of the EP barriers (time spent waiting = skew between ranks)
+        bars = [e.time_range.elapsed_us() for e in ev if "flag_barrier" in e.name]
+        gemm = sum(e.time_range.elapsed_us() for e in ev if "grouped_gemm" in e.name) / args.steps
+        nb = max(1, len(bars) // args.steps)
+        per = [sum(bars[i::nb]) / args.steps for i in range(nb)]
+        print(f"rank {rank}: barrier waits per step (in order) {' '.join(f'{b:7.1f}' for b in per)} us; "
+              f"GEMMs {gemm / 1e3:.3f} ms/step", flush=True)
+    if rank != 0:
+        return
     agg = collections.defaultdict(list)
     for e in ev:
         agg[e.name.split("(")[0][:70]].append(e.time_range.elapsed_us())
