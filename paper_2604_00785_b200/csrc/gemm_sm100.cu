@@ -644,16 +644,28 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const TileInfo& t
 #pragma unroll
             for (int j = 0; j < 32; ++j) base[j] = 0.f;
             if (p.cec) {
-                for (int j = j0; j < j1; ++j) {
-                    const __nv_bfloat16* sp = p.src + (int64_t)p.slot_prow[j] * p.H + col;
+                // the token's slot rows, up to 4 at a time with all their 64-byte pieces in flight,
+                // summed in slot order (the scatter-add of moe.hpp:418-423)
+                for (int jb = j0; jb < j1; jb += 4) {
+                    uint4 w4[4][4];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(sp) + q);
-                        const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+                        if (jb + q >= j1) break;
+                        const uint4* sp = reinterpret_cast<const uint4*>(p.src + (int64_t)p.slot_prow[jb + q] * p.H + col);
 #pragma unroll
-                        for (int h = 0; h < 4; ++h) {
-                            base[8 * q + 2 * h] += bf16_lo(w[h]);
-                            base[8 * q + 2 * h + 1] += bf16_hi(w[h]);
+                        for (int u = 0; u < 4; ++u) w4[q][u] = __ldg(sp + u);
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (jb + q >= j1) break;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const uint32_t w[4] = {w4[q][u].x, w4[q][u].y, w4[q][u].z, w4[q][u].w};
+#pragma unroll
+                            for (int h = 0; h < 4; ++h) {
+                                base[8 * u + 2 * h] += bf16_lo(w[h]);
+                                base[8 * u + 2 * h + 1] += bf16_hi(w[h]);
+                            }
                         }
                     }
                 }

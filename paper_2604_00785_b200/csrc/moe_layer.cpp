@@ -951,13 +951,23 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         launch_router_dw_reduce_bf16(dw_part_, drouter, router_dw_splits(S, H, ctx_.num_sms), (int64_t)H * N, st);
         // scatter-add to tokens (418-423), then + matmul_nt(dlogits, router) (454) as a GEMM whose
         // epilogue adds the scattered rows
-        if (!dx_rows) {
+        // EP = 1: a combine kernel sums each token's slot rows of dXperm, the RouterDx epilogue
+        // adds them. Opt-in (B2_ROUTERDX_FUSED=1): the RouterDx epilogue gathers the slot rows
+        // itself — measured slower (5.08-5.12 vs 4.85 ms per step: 148 one-CTA tiles' epilogues
+        // read 512 MB of scattered rows with too few bytes in flight)
+        static const bool fused_dx = [] {
+            const char* e = getenv("B2_ROUTERDX_FUSED");
+            return e && atoi(e) == 1;
+        }();
+        const bool fuse = !dx_rows && fused_dx;
+        if (!dx_rows && !fuse) {
             launch_combine<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, dx, S, H, K, st);
             dx_rows = dx;
         }
         ga.kind = GemmKind::RouterDx;
-        ga.cec = nullptr;
-        ga.src = dx_rows;
+        ga.cec = fuse ? cec_ : nullptr;
+        ga.slot_prow = slot_prow_;
+        ga.src = fuse ? dxp_ : dx_rows;
         ga.out0 = dx;
         launch_sm100_gemm(ga, st);
         launches_ += 5;
