@@ -661,7 +661,8 @@ void launch_norm_final(const double* partials, int n, double* norm_sq, cudaStrea
 }
 
 void launch_adamw_chunks(const OptSeg* segs, const OptChunk* chunks, const int32_t* ids, int nids,
-                         const OptStepArgs& a, const double* norm_sq, const int32_t* nonfinite, cudaStream_t st) {
+                         const OptStepArgs& a, const double* norm_sq, const int32_t* nonfinite, cudaStream_t st,
+                         int sm_reserve) {
     if (nids <= 0) return;
     AdamWDev c;
     c.lr = a.lr;
@@ -693,7 +694,7 @@ void launch_adamw_chunks(const OptSeg* segs, const OptChunk* chunks, const int32
         B2_LAUNCH_CHECK();
         return;
     }
-    static int minb = 0, grid_cap = 0;  // resident blocks on the whole GPU (persistent grid)
+    static int minb = 0, grid_cap = 0, per_sm_blocks = 1;  // resident blocks (persistent grid)
     if (grid_cap == 0) {
         // A/B hook: 3 (no spills), 4 (default: more warps), 6 (pairs of elements, 48 warps/SM)
         const char* env = getenv("B2_ADAMW_MINB");
@@ -706,9 +707,10 @@ void launch_adamw_chunks(const OptSeg* segs, const OptChunk* chunks, const int32
         else if (minb == 6)
             B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adamw_chunks_kernel<6, 2>, 256, 0));
         else B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adamw_chunks_kernel<4>, 256, 0));
-        grid_cap = sms * std::max(1, per_sm);
+        per_sm_blocks = std::max(1, per_sm);
+        grid_cap = sms * per_sm_blocks;
     }
-    const int grid = std::min(nids, grid_cap);
+    const int grid = std::max(1, std::min(nids, grid_cap - std::max(0, sm_reserve) * per_sm_blocks));
     if (minb == 3) launch_k(adamw_chunks_kernel<3>, dim3(grid), dim3(256), 0, st, segs, chunks, ids, nids, c, a, norm_sq, nonfinite);
     else if (minb == 6)
         launch_k(adamw_chunks_kernel<6, 2>, dim3(grid), dim3(256), 0, st, segs, chunks, ids, nids, c, a, norm_sq,

@@ -256,8 +256,10 @@ void launch_sumsq_chunks(const OptSeg* segs, const OptChunk* chunks, const int32
 void launch_norm_final(const double* partials, int n, double* norm_sq, cudaStream_t st);
 // fused unscale + clip (from *norm_sq) + AdamW + bf16 recast over the listed chunks; a set
 // *nonfinite leaves every state untouched
+// sm_reserve > 0: the persistent grid leaves that many SMs free (for concurrent NCCL kernels)
 void launch_adamw_chunks(const OptSeg* segs, const OptChunk* chunks, const int32_t* ids, int nids,
-                         const OptStepArgs& a, const double* norm_sq, const int32_t* nonfinite, cudaStream_t st);
+                         const OptStepArgs& a, const double* norm_sq, const int32_t* nonfinite, cudaStream_t st,
+                         int sm_reserve = 0);
 // any non-finite element in the n-element buffer -> *flag = 1
 void launch_nonfinite_scan(const void* g, int dtype, int64_t n, int32_t* flag, cudaStream_t st);
 

@@ -100,6 +100,15 @@ class ShardedOptimizer {
     std::vector<char> pre_;  // param needs a collective before its update
     cudaStream_t comm_stream_ = nullptr;
     cudaEvent_t ev_start_ = nullptr, ev_synced_ = nullptr, ev_pre_done_ = nullptr, ev_ag_ = nullptr;
+    // the synced parameters' update + re-share in buckets (consecutive params, ~equal owned
+    // elements): bucket b's all-gather on the comm stream overlaps bucket b+1's update
+    struct Bucket {
+        int id0 = 0, id1 = 0;     // range in ids_pre_
+        std::vector<int> params;  // params whose re-share follows this bucket's update
+        cudaEvent_t ev = nullptr;
+    };
+    std::vector<Bucket> buckets_;
+    static constexpr int kCommSMs = 16;
     int64_t step_count_ = 0;
     int launches_ = 0;
 };
