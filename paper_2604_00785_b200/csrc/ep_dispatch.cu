@@ -142,12 +142,9 @@ __global__ void ep_combine_slots_kernel(const T* __restrict__ y, const int32_t* 
 // the reducescatter of moe.hpp:378 / 427-428 in member order, as remote loads with up to
 // 8 owners' 16-byte vectors in flight per lane
 template <typename T>
-__global__ void ep_pull_sum_kernel(const T* const* __restrict__ peer_slab, const int32_t* __restrict__ gi_local,
-                                   int S, int K, int E, int NR, int W, int me, T* __restrict__ out) {
-    pdl_wait();
-    pdl_launch();
-    const int t = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
-    if (t >= S) return;
+__device__ __forceinline__ void ep_pull_sum_token(const T* const* __restrict__ peer_slab,
+                                                  const int32_t* __restrict__ gi_local, int S, int K, int E, int NR,
+                                                  int W, int me, T* __restrict__ out, int t, int lane) {
     unsigned mask = 0;
     for (int k = 0; k < K; ++k) mask |= 1u << (gi_local[(int64_t)t * K + k] / NR);
     const int64_t row = (int64_t)me * S + t;
@@ -215,6 +212,16 @@ __global__ void ep_pull_sum_kernel(const T* const* __restrict__ peer_slab, const
             out[(int64_t)t * W + c] = Elem<T>::from_f(acc);
         }
     }
+}
+
+template <typename T>
+__global__ void ep_pull_sum_kernel(const T* const* __restrict__ peer_slab, const int32_t* __restrict__ gi_local,
+                                   int S, int K, int E, int NR, int W, int me, T* __restrict__ out) {
+    pdl_wait();
+    pdl_launch();
+    const int lane = threadIdx.x % 32, nw = gridDim.x * blockDim.x / 32;
+    for (int t = (blockIdx.x * blockDim.x + threadIdx.x) / 32; t < S; t += nw)  // grid-stride: any grid size
+        ep_pull_sum_token<T>(peer_slab, gi_local, S, K, E, NR, W, me, out, t, lane);
 }
 
 // source side of the GEMM-fused combine: out[t] = sum_k slab[k][t] in k order (every (t, k)
@@ -500,19 +507,22 @@ void launch_ep_gather_pull(const T* const* peer_src, int S, int T_tot, int H, co
 
 template <typename T>
 void launch_ep_combine_local(const T* y, const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec,
-                             const float* gw, int K, int S, int T_tot, int H, T* own_slab, cudaStream_t st) {
+                             const float* gw, int K, int S, int T_tot, int H, T* own_slab, cudaStream_t st,
+                             int max_blocks) {
     if (T_tot <= 0) return;
     check(((int64_t)H * sizeof(T)) % 16 == 0, "ep combine: rows must be 16-byte multiples");
-    launch_k(ep_combine_slots_kernel<T>, dim3(ep_grid(T_tot)), dim3(256), 0, st, y, slot_prow, selected_k, cec, gw, K, S, T_tot, H,
+    const unsigned grid = max_blocks > 0 ? std::min<unsigned>(ep_grid(T_tot), (unsigned)max_blocks) : ep_grid(T_tot);
+    launch_k(ep_combine_slots_kernel<T>, dim3(grid), dim3(256), 0, st, y, slot_prow, selected_k, cec, gw, K, S, T_tot, H,
                                                                   0, nullptr, own_slab);
     B2_LAUNCH_CHECK();
 }
 
 template <typename T>
 void launch_ep_pull_sum(const T* const* peer_slab, const int32_t* gi_local, int S, int K, int E, int NR, int W, int me,
-                        T* out, cudaStream_t st) {
+                        T* out, cudaStream_t st, int max_blocks) {
     if (S <= 0) return;
-    launch_k(ep_pull_sum_kernel<T>, dim3((unsigned)ceil_div(S, 8)), dim3(256), 0, st, peer_slab, gi_local, S, K, E, NR, W, me, out);
+    const unsigned full = (unsigned)ceil_div(S, 8);
+    launch_k(ep_pull_sum_kernel<T>, dim3(max_blocks > 0 ? std::min<unsigned>(full, (unsigned)max_blocks) : full), dim3(256), 0, st, peer_slab, gi_local, S, K, E, NR, W, me, out);
     B2_LAUNCH_CHECK();
 }
 
@@ -520,9 +530,9 @@ void launch_ep_pull_sum(const T* const* peer_slab, const int32_t* gi_local, int 
     template void launch_ep_gather_pull<T>(const T* const*, int, int, int, const int32_t*, const int32_t*, T*,    \
                                            cudaStream_t);                                                         \
     template void launch_ep_combine_local<T>(const T*, const int32_t*, const int32_t*, const int32_t*, const float*, \
-                                             int, int, int, int, T*, cudaStream_t);                              \
+                                             int, int, int, int, T*, cudaStream_t, int);                         \
     template void launch_ep_pull_sum<T>(const T* const*, const int32_t*, int, int, int, int, int, int, T*,        \
-                                        cudaStream_t);                                                            \
+                                        cudaStream_t, int);                                                       \
     template void launch_kslab_sum<T>(const T*, int, int, int, T*, cudaStream_t);
 B2_EP_INST(float)
 B2_EP_INST(__nv_bfloat16)

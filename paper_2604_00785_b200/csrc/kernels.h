@@ -82,11 +82,13 @@ void launch_ep_gather_pull(const T* const* peer_src, int S, int T_tot, int H, co
 // OWN slab row [gid]; sources pull them after a barrier (launch_ep_pull_sum)
 template <typename T>
 void launch_ep_combine_local(const T* y, const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec,
-                             const float* gw, int K, int S, int T_tot, int H, T* own_slab, cudaStream_t st);
+                             const float* gw, int K, int S, int T_tot, int H, T* own_slab, cudaStream_t st,
+                             int max_blocks = 0);
 // out[t] = sum over t's owner ranks (in rank order) of peer_slab[r][(me*S + t)*W ..]
 template <typename T>
+// max_blocks > 0 caps the grid (a side-stream launch that must stay inside its reserved SMs)
 void launch_ep_pull_sum(const T* const* peer_slab, const int32_t* gi_local, int S, int K, int E, int NR, int W, int me,
-                        T* out, cudaStream_t st);
+                        T* out, cudaStream_t st, int max_blocks = 0);
 // out[t] = sum over k (in k order) of slab[k][t] — the source side of the GEMM-fused
 // combine: every (t, k) row was stored into this rank's [K][S][W] slab by its owner's
 // FwdDown / BwdDx epilogue over NVLink

@@ -165,6 +165,7 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
         tile_order_ = w.take<int32_t>(max_mtiles_ + 1);
         if (const char* e = getenv("B2_EP_FUSED_PULL")) fused_pull_opt_ = atoi(e) != 0;
         if (const char* e = getenv("B2_EP_OVERLAP_PULL")) overlap_pull_opt_ = atoi(e) != 0;
+        if (const char* e = getenv("B2_COMM_SMS")) comm_sms_ = std::max(2, std::min(ctx_.num_sms / 2, atoi(e)));
         x_all_ = w.take_bytes(es * (size_t)std::max<int64_t>(tmax_ * H, 1));
         ep_setup();
         B2_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
@@ -772,15 +773,23 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
             mark(kGemmDx, true);
             B2_CUDA(cudaEventRecord(ev_fork_, st));
             B2_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+            // side-stream grids capped to the reserved SMs (8 resident 256-thread blocks each), so
+            // they never hold SMs the weight-gradient GEMM's CTAs are waiting for
+            // (B2_EP_SIDE_CAP=0: uncapped grids)
+            static const bool side_cap_on = [] {
+                const char* e = getenv("B2_EP_SIDE_CAP");
+                return !(e && atoi(e) == 0);
+            }();
+            const int side_cap = side_cap_on ? comm_sms_ * 8 : 0;
             launch_ep_combine_local<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, K, S, Tt, H,
-                                       (T*)ret_b_, side_);
+                                       (T*)ret_b_, side_, side_cap);
             ep_barrier(side_);
             launch_ep_pull_sum<T>((const T* const*)peer_tab_ + 3 * E, gi_local_, S, K, E, nr, H, ctx_.coord_ep,
-                                  (T*)dx_exp_, side_);
+                                  (T*)dx_exp_, side_, side_cap);
             launch_ep_pull_sum<float>((const float* const*)peer_tab_ + 4 * E, gi_local_, S, K, E, nr, K,
-                                      ctx_.coord_ep, wgrad_local_, side_);
+                                      ctx_.coord_ep, wgrad_local_, side_, side_cap);
             B2_CUDA(cudaEventRecord(ev_join_, side_));
-            ga.max_ctas = ctx_.num_sms - kCommSMs;
+            ga.max_ctas = ctx_.num_sms - comm_sms_;
         }
         ga.kind = GemmKind::WgradDown;  // 407
         ga.out0 = ddown;

@@ -229,7 +229,7 @@ class MoeLayer {
     // bf16, EP > 1: the backward returns dX / top-k weight gradients on a side stream while
     // the weight-gradient GEMMs run on num_sms - kCommSMs SMs
     bool overlap_return() const;
-    static constexpr int kCommSMs = 16;
+    int comm_sms_ = 16;  // B2_COMM_SMS overrides (A/B hook)
     bool overlap_opt_ = true;
     cudaStream_t side_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_xall_ = nullptr;
