@@ -1,7 +1,7 @@
 """Multi-GPU worker for the expert-parallel parity tests (one process per GPU).
 
 Each rank runs the B200 MoE layer on its S-token slice with its N/EP experts
-(dispatch/combine over NCCL all-to-all); rank 0 gathers every rank's outputs and
+(dispatch/combine over NVLink peer memory); rank 0 gathers every rank's outputs and
 gradients and compares them with the oracle's EP world (oracle/moe_oracle.c, itself
 pinned bitwise to the reference's fast_moe_forward/backward at EP > 1).
 """

@@ -1,4 +1,4 @@
-"""Expert parallelism across GPUs: all-to-all dispatch/combine vs the oracle's EP world.
+"""Expert parallelism across GPUs: dispatch/combine over NVLink peer memory vs the oracle's EP world.
 
 Runs tests/ep_worker.py as one process per GPU (needs >= 2 GPUs; skipped otherwise).
 Bars as in test_gpu_moe.py: fp32 within 1e-4 rel_err; bf16 outputs/dx within 2e-2
@@ -48,7 +48,7 @@ CASES = [
     dict(n_experts=16, top_k=4, hidden=256, intermediate=128, token_block=8, s=300, dtype="bf16"),
     dict(n_experts=64, top_k=8, hidden=256, intermediate=128, token_block=8, s=512, dtype="bf16"),
     # activation checkpointing (the backward replays the forward, EP collectives included) and
-    # CUDA-graph capture of the NCCL + peer-memory path
+    # CUDA-graph capture of the peer-memory path (flag barriers, pulls)
     dict(n_experts=16, top_k=4, hidden=256, intermediate=128, token_block=8, s=300, dtype="bf16", ckpt=True,
          graph=True),
     dict(n_experts=64, top_k=8, hidden=256, intermediate=128, token_block=8, s=512, dtype="bf16", fused=True),
