@@ -66,6 +66,24 @@ class ClockSampler:
         self._t.start()
 
     def _run(self):
+        # NVML directly (every 5 ms: a 100 ms timed region gets ~20 samples); nvidia-smi as fallback
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            import torch
+            p = torch.cuda.get_device_properties(self.device)  # matched by PCI bus id (visible-device safe)
+            h = pynvml.nvmlDeviceGetHandleByPciBusId(f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0")
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            bits = [pynvml.nvmlClocksThrottleReasonHwSlowdown, pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
+                    pynvml.nvmlClocksThrottleReasonSwThermalSlowdown, pynvml.nvmlClocksThrottleReasonSwPowerCap]
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.samples.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits])
+                self._stop.wait(0.005)
+            return
+        except Exception:
+            self.samples = []
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         while not self._stop.is_set():
@@ -88,7 +106,7 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(self.samples)}
+                "sm_min_mhz": sm[0] if sm else None, "samples": len(self.samples)}
 
 
 def bind_numa_local(torch, gpu: int):
