@@ -24,7 +24,8 @@ import os
 from dataclasses import dataclass
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libb2moe.so")
+# B2_LIB: an alternative build of the same library for A/B measurements (tools/build_alt.sh)
+LIB_PATH = os.environ.get("B2_LIB") or os.path.join(PKG, "libb2moe.so")
 
 F32, BF16 = 0, 1
 DDP, SO, EPSO = 0, 1, 2

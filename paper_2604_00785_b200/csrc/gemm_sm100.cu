@@ -60,6 +60,14 @@ constexpr int NUM_THREADS = 128 + 32 * NUM_EPI_WARPS;
 // dgrad epilogue (BwdDownDgrad): each epilogue warp stages the G and U operands of its
 // next 32-row x 32-column chunk by TMA (SWIZZLE_64B boxes) while it works on the current one
 constexpr int EPI_GU_BYTES = 2 * 32 * 32 * 2;  // g box + u box
+// dgrad epilogue: G/U read straight from global into registers (ld.global.nc, L1-cached) instead
+// of TMA-staged boxes: the staging's shared-memory writes + reads compete with the MMA operand
+// traffic, and dropping them frees the smem for a sixth stage
+#ifdef B2_DGRAD_STAGED_GU  // A/B build of the TMA-staged variant (tools/build_alt.sh)
+constexpr bool kDgradDirectGU = false;
+#else
+constexpr bool kDgradDirectGU = true;
+#endif
 // TMA-store epilogue of the six expert kinds: each epilogue warp owns SLOTS 2 KB staging
 // slots, each one 32-row x 32-column bf16 box in the SWIZZLE_64B layout
 constexpr int EPI_SLOT_BYTES = 32 * 32 * 2;
@@ -69,9 +77,9 @@ struct KCfg {
     // two staging slots everywhere (FwdGateUp's three boxes per chunk rotate through them),
     // so every kind but the dgrad (which also stages its G/U operands) keeps 6 stages
     static constexpr int SLOTS = 2;
-    static constexpr int STAGES = CG == 1 ? 4 : (K == GemmKind::BwdDownDgrad ? 5 : 6);
-    static constexpr int WARP_EPI_BYTES =
-        TMA_EPI ? SLOTS * EPI_SLOT_BYTES + (K == GemmKind::BwdDownDgrad ? EPI_GU_BYTES : 0) : 0;
+    static constexpr bool GU_STAGED = K == GemmKind::BwdDownDgrad && !kDgradDirectGU;
+    static constexpr int STAGES = CG == 1 ? 4 : (GU_STAGED ? 5 : 6);
+    static constexpr int WARP_EPI_BYTES = TMA_EPI ? SLOTS * EPI_SLOT_BYTES + (GU_STAGED ? EPI_GU_BYTES : 0) : 0;
     static constexpr int SMEM =
         STAGES * Cfg<CG>::STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + NUM_EPI_WARPS * WARP_EPI_BYTES;
     static_assert(SMEM <= 232448, "kernel exceeds 227 KB of shared memory");
@@ -1062,14 +1070,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
         const int ew = warp - 4;
         const uint32_t gu_s = epi_base + (uint32_t)(ew * KC::WARP_EPI_BYTES);
         EpiStage<KC::SLOTS> stg;
-        stg.s0 = gu_s + (KIND == GemmKind::BwdDownDgrad ? EPI_GU_BYTES : 0);
+        stg.s0 = gu_s + (KC::GU_STAGED ? EPI_GU_BYTES : 0);
         stg.g0 = gbase + (stg.s0 - base);
         stg.slot = 0;
         const int row0 = 32 * quad;  // first row of this warp inside the CTA's 128
         const uint32_t gu_bar = epi_bar(ew);
         uint32_t gu_phase = 0;
         auto gu_issue = [&](const TileInfo& tn, int c) {
-            if (lane == 0 && tn.n0 + c < p.I) {
+            if (KC::GU_STAGED && lane == 0 && tn.n0 + c < p.I) {
                 mbar_expect_tx(gu_bar, EPI_GU_BYTES);
                 tma_load_2d(gu_s, &p.mapG, gu_bar, tn.n0 + c, tn.m0 + 32 * quad);
                 tma_load_2d(gu_s + EPI_GU_BYTES / 2, &p.mapU, gu_bar, tn.n0 + c, tn.m0 + 32 * quad);
@@ -1100,7 +1108,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                     const int col = ti.n0 + c;
                     const bool live = col < p.I;  // I % 64 == 0: a chunk is all in or all out
                     float gv[32], uv[32];
-                    if (live) {
+                    if (live && !KC::GU_STAGED) {
+                        // this lane's row, 32 columns of G and U (64 B each), straight to registers
+                        const int64_t grow = (int64_t)(ti.m0 + row0 + lane) * p.I + col;
+                        const uint4* g4p = reinterpret_cast<const uint4*>(p.g + grow);
+                        const uint4* u4p = reinterpret_cast<const uint4*>(p.u + grow);
+                        uint4 g4[4], u4[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            g4[q] = __ldg(g4p + q);
+                            u4[q] = __ldg(u4p + q);
+                        }
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint32_t gw[4] = {g4[q].x, g4[q].y, g4[q].z, g4[q].w},
+                                           uw[4] = {u4[q].x, u4[q].y, u4[q].z, u4[q].w};
+#pragma unroll
+                            for (int h = 0; h < 4; ++h) {
+                                gv[8 * q + 2 * h] = bf16_lo(gw[h]);
+                                gv[8 * q + 2 * h + 1] = bf16_hi(gw[h]);
+                                uv[8 * q + 2 * h] = bf16_lo(uw[h]);
+                                uv[8 * q + 2 * h + 1] = bf16_hi(uw[h]);
+                            }
+                        }
+                    } else if (live) {
                         mbar_wait(gu_bar, gu_phase, 100 + ew);
                         gu_phase ^= 1u;
 #pragma unroll
