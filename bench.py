@@ -220,17 +220,24 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def mula7b_param_set(ep=1):
-    """Mula-7B-A1B ParamSlots of one rank (model.cpp:189-229, preset model.cpp:43-45):
-    (numel, expert?, tp_sharded?); the rank holds 64/ep experts per MoE layer."""
-    hid, layers, vocab, inter = 2048, 16, 50304, 1024
-    nexp = 64 // ep
+def mula_param_set(layers, hid, heads, head_size, inter, experts, vocab, ep=1):
+    """ParamSlots of one rank of an MoE preset in Model::param_slots order (model.cpp:189-229):
+    (numel, expert?, tp_sharded?); the rank holds experts/ep experts per MoE layer. Pinned to
+    the reference's own Model::param_slots / count_params by tests/test_param_set.py."""
+    hd = heads * head_size
+    nexp = experts // ep
     slots = [(vocab * hid, False, False)]
     for _ in range(layers):
-        slots += [(hid, False, False)] + [(hid * hid, False, True)] * 4 + [(hid, False, False)]
-        slots += [(hid * nexp, False, False)] + [(nexp * hid * inter, True, False)] * 3
+        slots += [(hid, False, False)] + [(hid * hd, False, True)] * 3 + [(hd * hid, False, True)]
+        slots += [(hid, False, False), (hid * experts, False, False)] + [(nexp * hid * inter, True, False)] * 3
     slots += [(hid, False, False), (hid * vocab, False, False)]
     return slots
+
+
+def mula7b_param_set(ep=1):
+    """Mula-7B-A1B (preset model.cpp:43-45): 16 layers, hidden 2048, 16 x 128 heads, 64 experts
+    of ffn 1024, vocab 50304."""
+    return mula_param_set(16, 2048, 16, 128, 1024, 64, 50304, ep)
 
 
 def bench_adamw(torch, b2, ctx, dev, steps, warmup, world, rank, hbm_peak, dp=1):

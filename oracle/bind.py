@@ -298,6 +298,21 @@ class Oracle:
             self._check(f(path.encode(), C.byref(cnt), C.byref(tot), _p(out), I64(out.size)))
         return cnt.value, out[:tot.value]
 
+    # ---- the model's parameter set (reference only: src/model.cpp:31-91, 189-229) ----
+    def count_params(self, preset: str):
+        tot, act = I64(), I64()
+        self._check(self._f("count_params")(preset.encode(), C.byref(tot), C.byref(act)))
+        return tot.value, act.value
+
+    def param_slots(self, preset: str, ep: int = 1, ep_coord: int = 0):
+        """Model::param_slots of one rank: list of (numel, expert?, tp_sharded?) in slot order."""
+        cap = 4096
+        numel, ex, tp = np.zeros(cap, np.int64), np.zeros(cap, np.int32), np.zeros(cap, np.int32)
+        n = C.c_int()
+        self._check(self._f("param_slots")(preset.encode(), ep, ep_coord, _p(numel), _p(ex), _p(tp), cap,
+                                           C.byref(n)))
+        return [(int(numel[i]), bool(ex[i]), bool(tp[i])) for i in range(min(n.value, cap))]
+
 
 _CACHE: dict = {}
 

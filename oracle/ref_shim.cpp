@@ -15,6 +15,8 @@
 //   lr_at_step             src/optim.cpp:17-24
 //   shard_slice            src/optim.cpp:43-50
 //   ShardedOptimizer::step src/optim.cpp:130-194
+//   Model::param_slots     src/model.cpp:189-229 (the EPSO parameter set of bench.py)
+//   count_params / preset  src/model.cpp:31-91
 // The rank threads are the reference's own World (src/comm.cpp:80-124).
 #include <chrono>
 #include <cstring>
@@ -23,6 +25,7 @@
 #include <vector>
 
 #include "optimus/comm.hpp"
+#include "optimus/model.hpp"
 #include "optimus/moe.hpp"
 #include "optimus/optim.hpp"
 
@@ -498,4 +501,38 @@ int ref_record_file_read(const char* path, int64_t* count, int64_t* total, float
         *total = tot;
     });
 }
+}  // extern "C"
+
+// ---- the model's parameter slots (bench.py's EPSO parameter set is pinned to these) ----------
+extern "C" {
+
+// the preset's parameter count (model.cpp:70-91)
+int ref_count_params(const char* preset_name, int64_t* total, int64_t* active) {
+    return guard([&] {
+        const ParamCount pc = count_params(preset(preset_name));
+        *total = pc.total;
+        *active = pc.active;
+    });
+}
+
+// Model::param_slots of the rank at EP coordinate ep_coord (Topology{ep}) for a preset;
+// writes up to cap slots (numel, expert?, tp_sharded?) and returns the slot count in *n
+int ref_param_slots(const char* preset_name, int ep, int ep_coord, int64_t* numel, int32_t* expert, int32_t* tp,
+                    int cap, int* n) {
+    return guard([&] {
+        Topology topo;
+        topo.ep = ep;
+        RankCoord coord;
+        coord.ep = ep_coord;
+        Model m(preset(preset_name), topo, coord, 1234);
+        const std::vector<ParamSlot> slots = m.param_slots();
+        *n = (int)slots.size();
+        for (int i = 0; i < (int)slots.size() && i < cap; ++i) {
+            numel[i] = slots[(size_t)i].weight->numel();
+            expert[i] = slots[(size_t)i].cls == ReplicationClass::expert ? 1 : 0;
+            tp[i] = slots[(size_t)i].tp_sharded ? 1 : 0;
+        }
+    });
+}
+
 }  // extern "C"
