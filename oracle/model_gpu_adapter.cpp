@@ -1,0 +1,154 @@
+// TEST INFRASTRUCTURE ONLY — the model-level integration check of SURVEY §8(f)3.
+//
+// Linked into oracle/_ref/model_parity_gpu with -Wl,--wrap on the reference's two MoE block
+// entry points, so the UNMODIFIED reference model (src/model.cpp chunk_forward /
+// chunk_backward, src/blocks.cpp, the pipeline schedule, attention, norms, CE loss) runs with
+// every MoE layer on the B200 through the C-ABI (include/b2moe.h) instead of
+// fast_moe_forward / fast_moe_backward:
+//   moe_block_forward   blocks.cpp:339-355  -> b2_moe_forward + b2_moe_aux_loss + artifacts
+//   moe_block_backward  blocks.cpp:357-377  -> b2_moe_aux_probs_grad + b2_moe_backward
+// This is exactly the adapter INTEGRATION.md describes for a maintainer (fp32 layer, EP = 1,
+// one GPU state per MoeRec = per (layer, microbatch), host Tensor in / Tensor out).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "optimus/blocks.hpp"
+#include "optimus/kernels.hpp"
+#include "../include/b2moe.h"
+
+using namespace optimus;
+
+namespace {
+
+void ok(int rc, const char* what) {
+    if (rc != B2_OK) throw std::runtime_error(std::string("b2 adapter: ") + what + ": " + b2_last_error());
+}
+void cu(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string("b2 adapter: ") + what + ": " + cudaGetErrorString(e));
+}
+
+struct Dev {
+    float* p = nullptr;
+    int64_t n = 0;
+    void need(int64_t k) {
+        if (k <= n) return;
+        if (p) cudaFree(p);
+        cu(cudaMalloc((void**)&p, sizeof(float) * (size_t)std::max<int64_t>(k, 1)), "cudaMalloc");
+        n = k;
+    }
+    void up(const TensorF& t) {
+        need(t.numel());
+        cu(cudaMemcpy(p, t.data(), sizeof(float) * (size_t)t.numel(), cudaMemcpyHostToDevice), "H2D");
+    }
+    void down(TensorF& t) const {
+        cu(cudaMemcpy(t.data(), p, sizeof(float) * (size_t)t.numel(), cudaMemcpyDeviceToHost), "D2H");
+    }
+};
+
+struct GpuLayer {
+    b2_moe* m = nullptr;
+    int64_t cap = 0;
+    Dev x, router, gate, up, down, out, dy, dx, dr, dg, du, dd, apg;
+};
+
+b2_ctx* g_ctx = nullptr;
+std::map<const MoeRec*, GpuLayer> g_layers;  // one GPU state per (layer, microbatch) record
+
+GpuLayer& layer_for(const MoeRec* rec, const MoeConfig& cfg, int64_t S) {
+    if (!g_ctx) ok(b2_ctx_create(0, nullptr, 0, 1, 1, 1, 1, nullptr, &g_ctx), "ctx");
+    GpuLayer& L = g_layers[rec];
+    if (!L.m || L.cap < S) {
+        if (L.m) b2_moe_destroy(L.m);
+        b2_moe_cfg c{cfg.n_experts, cfg.top_k, cfg.hidden, cfg.intermediate, (int32_t)cfg.ep,
+                     cfg.normalize_topk ? 1 : 0, cfg.token_block};
+        ok(b2_moe_create(g_ctx, &c, B2_F32, S, &L.m), "create");
+        L.cap = S;
+    }
+    return L;
+}
+
+void upload_weights(GpuLayer& L, const ExpertWeights<float>& w) {
+    L.router.up(w.router);
+    L.gate.up(w.gate);
+    L.up.up(w.up);
+    L.down.up(w.down);
+}
+
+}  // namespace
+
+extern "C" {
+
+// moe_block_forward (blocks.cpp:339-355) on the B200
+TensorF __wrap__ZN7optimus17moe_block_forwardERNS_7RankCtxERKNS_12ProcessGroupERKNS_6TensorIfEERKNS_13ExpertWeightsIfEERKNS_9MoeConfigEbbRNS_6MoeRecEPNS_9ActLedgerEPNS_11ExpertTallyE(
+    RankCtx&, const ProcessGroup& ep_group, const TensorF& x, const ExpertWeights<float>& w, const MoeConfig& cfg,
+    bool fur, bool ckpt, MoeRec& rec, ActLedger* led, ExpertTally* tally) {
+    check(ep_group.size() == 1, "b2 adapter: the GPU MoE block runs at EP = 1 in this harness");
+    const int64_t S = x.dim(0), H = cfg.hidden;
+    GpuLayer& L = layer_for(&rec, cfg, S);
+    rec.ckpt = ckpt;
+    upload_weights(L, w);
+    L.x.up(x);
+    L.out.need(S * H);
+    ok(b2_moe_forward(L.m, L.x.p, L.router.p, L.gate.p, L.up.p, L.down.p, S, fur ? 1 : 0, L.out.p), "forward");
+    TensorF out({S, H});
+    L.out.down(out);
+    ok(b2_moe_aux_loss(L.m, &rec.aux), "aux loss");
+    if (tally) {  // routed tokens per local expert (RoutingArtifacts::token_counts)
+        const int64_t nr = cfg.n_experts / cfg.ep, T = S * cfg.ep, K = cfg.top_k;
+        const int64_t th = (T + cfg.token_block - 1) / cfg.token_block;
+        int64_t sizes[4];
+        std::vector<int64_t> tc((size_t)nr), ptc((size_t)(nr * th + 1)), pc((size_t)(nr * th + 1)),
+            ctc((size_t)nr + 1), ec((size_t)T), cec((size_t)T + 1), ii((size_t)(T * K)), oi((size_t)(T * K)),
+            sk((size_t)(T * K)), cnt((size_t)(nr * th + 1));
+        ok(b2_moe_artifacts(L.m, sizes, tc.data(), ptc.data(), pc.data(), ctc.data(), ec.data(), cec.data(), ii.data(),
+                            oi.data(), sk.data(), cnt.data()),
+           "artifacts");
+        TensorI t({nr});
+        std::memcpy(t.data(), tc.data(), sizeof(int64_t) * (size_t)nr);
+        tally->accumulate(t);
+    }
+    rec.held = b2_moe_held_bytes(L.m);
+    detail::led_charge(led, rec.held);
+    return out;
+}
+
+// moe_block_backward (blocks.cpp:357-377) on the B200; grads accumulate into g like the reference
+TensorF __wrap__ZN7optimus18moe_block_backwardERNS_7RankCtxERKNS_12ProcessGroupERKNS_13ExpertWeightsIfEERKNS_9MoeConfigEbdRNS_6MoeRecERKNS_6TensorIfEERNS_13MoeParamGradsEPNS_9ActLedgerE(
+    RankCtx&, const ProcessGroup& ep_group, const ExpertWeights<float>& w, const MoeConfig& cfg, bool, double aux_coeff,
+    MoeRec& rec, const TensorF& dy, MoeParamGrads& g, ActLedger* led) {
+    check(ep_group.size() == 1, "b2 adapter: the GPU MoE block runs at EP = 1 in this harness");
+    const int64_t S = dy.dim(0), H = cfg.hidden;
+    GpuLayer& L = layer_for(&rec, cfg, S);
+    upload_weights(L, w);
+    L.apg.need(S * cfg.n_experts);
+    ok(b2_moe_aux_probs_grad(L.m, aux_coeff, L.apg.p), "aux probs grad");
+    L.dy.up(dy);
+    L.dx.need(S * H);
+    L.dr.need(w.router.numel());
+    L.dg.need(w.gate.numel());
+    L.du.need(w.up.numel());
+    L.dd.need(w.down.numel());
+    ok(b2_moe_backward(L.m, L.router.p, L.gate.p, L.up.p, L.down.p, L.dy.p, L.apg.p, L.dx.p, L.dr.p, L.dg.p, L.du.p,
+                       L.dd.p),
+       "backward");
+    TensorF dx({S, H}), dr(w.router.shape()), dg(w.gate.shape()), du(w.up.shape()), dd(w.down.shape());
+    L.dx.down(dx);
+    L.dr.down(dr);
+    L.dg.down(dg);
+    L.du.down(du);
+    L.dd.down(dd);
+    add_inplace(g.router, dr);
+    add_inplace(g.gate, dg);
+    add_inplace(g.up, du);
+    add_inplace(g.down, dd);
+    detail::led_release(led, rec.held);
+    rec = MoeRec{};
+    return dx;
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+// TEST INFRASTRUCTURE ONLY — the model-level integration check of SURVEY §8(f)3.
+//
+// One serial training pass of the UNMODIFIED reference model: the multi-rank equivalence
+// config of test_model.cpp:86-99 (4 layers, hidden 32, 4 x 8 heads, 4 experts top-2, ffn 48,
+// vocab 64, context 8, aux coeff 0.01), batch random_tokens(8, 8, 64, 8000)
+// (test_model.cpp:19-24), seed 23, gpipe with M microbatches, through pp_forward_backward
+// (model.cpp:271-382 chunk_forward / chunk_backward inside). Built twice by oracle/Makefile:
+//   model_parity_ref  as is (every MoE block on the reference's fast_moe_forward/backward)
+//   model_parity_gpu  linked with model_gpu_adapter.cpp and -Wl,--wrap on moe_block_forward /
+//                     moe_block_backward: every MoE block on the B200 (libb2moe.so)
+// Output (argv[1]): "<ce_sum> <aux_sum> <n_slots>\n" then per slot "<name> <numel>\n" and the
+// gradient as raw float32. tests/test_gpu_model_parity.py compares the two.
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "optimus/comm.hpp"
+#include "optimus/model.hpp"
+#include "optimus/schedule.hpp"
+
+using namespace optimus;
+
+int main(int argc, char** argv) {
+    if (argc < 2) {
+        std::fprintf(stderr, "usage: %s out.bin [microbatches]\n", argv[0]);
+        return 2;
+    }
+    const int m = argc > 2 ? std::atoi(argv[2]) : 1;
+    ModelConfig cfg;
+    cfg.layers = 4;
+    cfg.hidden = 32;
+    cfg.heads = 4;
+    cfg.head_size = 8;
+    cfg.intermediate = 48;
+    cfg.experts = 4;
+    cfg.top_k = 2;
+    cfg.vocab = 64;
+    cfg.context = 8;
+    cfg.aux_loss_coeff = 0.01;
+    TensorI batch({8, cfg.context});
+    for (int64_t i = 0; i < batch.numel(); ++i) batch.data()[i] = (int64_t)(hash_mix(8000, (uint64_t)i) % (uint64_t)cfg.vocab);
+    Topology serial;
+    World w(serial);
+    int rc = 0;
+    w.run([&](RankCtx& ctx) {
+        Model mdl(cfg, serial, ctx.coord(), 23, 1);
+        PipelineSchedule sched = pp_build_schedule(ScheduleKind::gpipe, 1, m, 1);
+        ActLedger led;
+        PpLossParts parts = pp_forward_backward(ctx, mdl, sched, batch, &led);
+        std::vector<ParamSlot> slots = mdl.param_slots();
+        FILE* f = std::fopen(argv[1], "wb");
+        if (!f) {
+            rc = 1;
+            return;
+        }
+        std::fprintf(f, "%.17g %.17g %d\n", parts.ce_sum, parts.aux_sum, (int)slots.size());
+        for (const ParamSlot& s : slots) {
+            std::fprintf(f, "%s %lld\n", s.name.c_str(), (long long)s.grad->numel());
+            std::fwrite(s.grad->data(), sizeof(float), (size_t)s.grad->numel(), f);
+        }
+        std::fclose(f);
+    });
+    return rc;
+}
