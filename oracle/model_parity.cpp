@@ -9,7 +9,10 @@
 //   model_parity_gpu  linked with model_gpu_adapter.cpp and -Wl,--wrap on moe_block_forward /
 //                     moe_block_backward: every MoE block on the B200 (libb2moe.so)
 // Output (argv[1]): "<ce_sum> <aux_sum> <n_slots>\n" then per slot "<name> <numel>\n" and the
-// gradient as raw float32. tests/test_gpu_model_parity.py compares the two.
+// gradient as raw float32. With argv[3] = K > 0 the pass is K end-to-end train_step calls instead
+// (model.cpp:538-565: forward/backward + the reference's EPSO AdamW step, warmup 0): the header
+// carries the K per-step losses and the slots hold the final weights.
+// tests/test_gpu_model_parity.py compares the two builds.
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -17,6 +20,7 @@
 
 #include "optimus/comm.hpp"
 #include "optimus/model.hpp"
+#include "optimus/optim.hpp"
 #include "optimus/schedule.hpp"
 
 using namespace optimus;
@@ -27,6 +31,7 @@ int main(int argc, char** argv) {
         return 2;
     }
     const int m = argc > 2 ? std::atoi(argv[2]) : 1;
+    const int steps = argc > 3 ? std::atoi(argv[3]) : 0;
     ModelConfig cfg;
     cfg.layers = 4;
     cfg.hidden = 32;
@@ -47,17 +52,29 @@ int main(int argc, char** argv) {
         Model mdl(cfg, serial, ctx.coord(), 23, 1);
         PipelineSchedule sched = pp_build_schedule(ScheduleKind::gpipe, 1, m, 1);
         ActLedger led;
-        PpLossParts parts = pp_forward_backward(ctx, mdl, sched, batch, &led);
+        std::vector<double> losses;
+        PpLossParts parts;
+        if (steps > 0) {
+            AdamWConfig ac;
+            ac.warmup_steps = 0;
+            ShardedOptimizer opt(ctx, ac, mdl.param_slots(), ShardMode::epso);
+            for (int k = 0; k < steps; ++k) losses.push_back(train_step(ctx, mdl, opt, sched, batch, &led).loss);
+        } else {
+            parts = pp_forward_backward(ctx, mdl, sched, batch, &led);
+        }
         std::vector<ParamSlot> slots = mdl.param_slots();
         FILE* f = std::fopen(argv[1], "wb");
         if (!f) {
             rc = 1;
             return;
         }
-        std::fprintf(f, "%.17g %.17g %d\n", parts.ce_sum, parts.aux_sum, (int)slots.size());
+        std::fprintf(f, "%.17g %.17g %d", parts.ce_sum, parts.aux_sum, (int)slots.size());
+        for (double l : losses) std::fprintf(f, " %.17g", l);
+        std::fprintf(f, "\n");
         for (const ParamSlot& s : slots) {
-            std::fprintf(f, "%s %lld\n", s.name.c_str(), (long long)s.grad->numel());
-            std::fwrite(s.grad->data(), sizeof(float), (size_t)s.grad->numel(), f);
+            const TensorF* t = steps > 0 ? s.weight : s.grad;
+            std::fprintf(f, "%s %lld\n", s.name.c_str(), (long long)t->numel());
+            std::fwrite(t->data(), sizeof(float), (size_t)t->numel(), f);
         }
         std::fclose(f);
     });

@@ -19,16 +19,23 @@ REF = os.path.join(ROOT, "oracle", "_ref", "model_parity_ref")
 GPU = os.path.join(ROOT, "oracle", "_ref", "model_parity_gpu")
 
 
-def run(binary, m, td):
-    out = os.path.join(td, f"{os.path.basename(binary)}_{m}.bin")
-    subprocess.run([binary, out, str(m)], check=True, timeout=600)
+def run(binary, m, td, steps=0):
+    out = os.path.join(td, f"{os.path.basename(binary)}_{m}_{steps}.bin")
+    subprocess.run([binary, out, str(m), str(steps)], check=True, timeout=600)
     with open(out, "rb") as f:
-        ce, aux, n = f.readline().split()
-        slots = {}
-        for _ in range(int(n)):
-            name, numel = f.readline().split()
-            slots[name.decode()] = np.frombuffer(f.read(4 * int(numel)), np.float32)
-    return float(ce), float(aux), slots
+        head = f.readline().split()
+        ce, aux, n = head[:3]
+        if steps:
+            return [float(v) for v in head[3:]], None, read_slots(f, int(n))
+        return float(ce), float(aux), read_slots(f, int(n))
+
+
+def read_slots(f, n):
+    slots = {}
+    for _ in range(n):
+        name, numel = f.readline().split()
+        slots[name.decode()] = np.frombuffer(f.read(4 * int(numel)), np.float32)
+    return slots
 
 
 def rel_err(a, b):
@@ -48,4 +55,20 @@ def test_model_with_b200_moe_matches_reference(m):
     assert set(g_g) == set(g_r)
     assert any(".moe." in k for k in g_r)
     worst = max(((rel_err(g_g[k], g_r[k]), k) for k in g_r))
+    print(f"m={m}: ce {ce_g:.9f} vs {ce_r:.9f}, aux {aux_g:.9f} vs {aux_r:.9f}, worst grad rel_err {worst}")
+    assert worst[0] <= 1e-4, worst
+
+
+def test_train_steps_with_b200_moe_match_reference():
+    """five end-to-end train_step calls (model.cpp:538-565): GPU MoE blocks + the reference's
+    EPSO AdamW on the CPU; per-step losses and the final weights of every parameter."""
+    if not (os.path.exists(REF) and os.path.exists(GPU)):
+        pytest.skip("oracle/_ref/model_parity_* not built (make -C oracle model_parity)")
+    with tempfile.TemporaryDirectory() as td:
+        l_r, _, w_r = run(REF, 2, td, steps=5)
+        l_g, _, w_g = run(GPU, 2, td, steps=5)
+    assert len(l_r) == len(l_g) == 5
+    assert max(abs(a - b) / abs(b) for a, b in zip(l_g, l_r)) <= 1e-5, (l_g, l_r)
+    worst = max(((rel_err(w_g[k], w_r[k]), k) for k in w_r))
+    print(f"train_step x5: losses {l_g} vs {l_r}; worst final-weight rel_err {worst}")
     assert worst[0] <= 1e-4, worst
