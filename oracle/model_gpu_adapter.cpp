@@ -7,10 +7,12 @@
 // fast_moe_forward / fast_moe_backward:
 //   moe_block_forward   blocks.cpp:339-355  -> b2_moe_forward + b2_moe_aux_loss + artifacts
 //   moe_block_backward  blocks.cpp:357-377  -> b2_moe_aux_probs_grad + b2_moe_backward
-// This is exactly the adapter INTEGRATION.md describes for a maintainer (fp32 layer, EP = 1,
-// one GPU state per MoeRec = per (layer, microbatch), host Tensor in / Tensor out).
+// This is exactly the adapter INTEGRATION.md describes for a maintainer (fp32 layer — or the
+// bf16 tensor-core layer with B2_ADAPTER_BF16=1 — EP = 1, one GPU state per MoeRec = per
+// (layer, microbatch), host Tensor in / Tensor out).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -32,28 +34,62 @@ void cu(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw std::runtime_error(std::string("b2 adapter: ") + what + ": " + cudaGetErrorString(e));
 }
 
+// B2_ADAPTER_BF16=1: the bf16 layer (tcgen05 tensor-core GEMMs) instead of the fp32 one; the
+// adapter rounds the fp32 tensors to bf16 (RNE) at the boundary and widens the results
+bool bf16_mode() {
+    static const bool on = [] {
+        const char* e = std::getenv("B2_ADAPTER_BF16");
+        return e && std::atoi(e) == 1;
+    }();
+    return on;
+}
+uint16_t to_bf16(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40u);
+    return (uint16_t)((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+}
+
 struct Dev {
-    float* p = nullptr;
+    void* p = nullptr;
     int64_t n = 0;
+    size_t es() const { return bf16_mode() ? 2 : 4; }
     void need(int64_t k) {
         if (k <= n) return;
         if (p) cudaFree(p);
-        cu(cudaMalloc((void**)&p, sizeof(float) * (size_t)std::max<int64_t>(k, 1)), "cudaMalloc");
+        cu(cudaMalloc(&p, es() * (size_t)std::max<int64_t>(k, 1)), "cudaMalloc");
         n = k;
     }
     void up(const TensorF& t) {
         need(t.numel());
-        cu(cudaMemcpy(p, t.data(), sizeof(float) * (size_t)t.numel(), cudaMemcpyHostToDevice), "H2D");
+        if (!bf16_mode()) {
+            cu(cudaMemcpy(p, t.data(), 4 * (size_t)t.numel(), cudaMemcpyHostToDevice), "H2D");
+            return;
+        }
+        std::vector<uint16_t> h((size_t)t.numel());
+        for (int64_t i = 0; i < t.numel(); ++i) h[(size_t)i] = to_bf16(t.data()[i]);
+        cu(cudaMemcpy(p, h.data(), 2 * h.size(), cudaMemcpyHostToDevice), "H2D");
     }
     void down(TensorF& t) const {
-        cu(cudaMemcpy(t.data(), p, sizeof(float) * (size_t)t.numel(), cudaMemcpyDeviceToHost), "D2H");
+        if (!bf16_mode()) {
+            cu(cudaMemcpy(t.data(), p, 4 * (size_t)t.numel(), cudaMemcpyDeviceToHost), "D2H");
+            return;
+        }
+        std::vector<uint16_t> h((size_t)t.numel());
+        cu(cudaMemcpy(h.data(), p, 2 * h.size(), cudaMemcpyDeviceToHost), "D2H");
+        for (int64_t i = 0; i < t.numel(); ++i) {
+            const uint32_t u = (uint32_t)h[(size_t)i] << 16;
+            std::memcpy(&t.data()[i], &u, 4);
+        }
     }
 };
 
 struct GpuLayer {
     b2_moe* m = nullptr;
     int64_t cap = 0;
-    Dev x, router, gate, up, down, out, dy, dx, dr, dg, du, dd, apg;
+    Dev x, router, gate, up, down, out, dy, dx, dr, dg, du, dd;
+    float* apg = nullptr;  // [S, N] fp32 in both modes
+    int64_t apg_n = 0;
 };
 
 b2_ctx* g_ctx = nullptr;
@@ -66,7 +102,7 @@ GpuLayer& layer_for(const MoeRec* rec, const MoeConfig& cfg, int64_t S) {
         if (L.m) b2_moe_destroy(L.m);
         b2_moe_cfg c{cfg.n_experts, cfg.top_k, cfg.hidden, cfg.intermediate, (int32_t)cfg.ep,
                      cfg.normalize_topk ? 1 : 0, cfg.token_block};
-        ok(b2_moe_create(g_ctx, &c, B2_F32, S, &L.m), "create");
+        ok(b2_moe_create(g_ctx, &c, bf16_mode() ? B2_BF16 : B2_F32, S, &L.m), "create");
         L.cap = S;
     }
     return L;
@@ -125,15 +161,19 @@ TensorF __wrap__ZN7optimus18moe_block_backwardERNS_7RankCtxERKNS_12ProcessGroupE
     const int64_t S = dy.dim(0), H = cfg.hidden;
     GpuLayer& L = layer_for(&rec, cfg, S);
     upload_weights(L, w);
-    L.apg.need(S * cfg.n_experts);
-    ok(b2_moe_aux_probs_grad(L.m, aux_coeff, L.apg.p), "aux probs grad");
+    if (L.apg_n < S * cfg.n_experts) {
+        if (L.apg) cudaFree(L.apg);
+        cu(cudaMalloc((void**)&L.apg, 4 * (size_t)(S * cfg.n_experts)), "cudaMalloc");
+        L.apg_n = S * cfg.n_experts;
+    }
+    ok(b2_moe_aux_probs_grad(L.m, aux_coeff, L.apg), "aux probs grad");
     L.dy.up(dy);
     L.dx.need(S * H);
     L.dr.need(w.router.numel());
     L.dg.need(w.gate.numel());
     L.du.need(w.up.numel());
     L.dd.need(w.down.numel());
-    ok(b2_moe_backward(L.m, L.router.p, L.gate.p, L.up.p, L.down.p, L.dy.p, L.apg.p, L.dx.p, L.dr.p, L.dg.p, L.du.p,
+    ok(b2_moe_backward(L.m, L.router.p, L.gate.p, L.up.p, L.down.p, L.dy.p, L.apg, L.dx.p, L.dr.p, L.dg.p, L.du.p,
                        L.dd.p),
        "backward");
     TensorF dx({S, H}), dr(w.router.shape()), dg(w.gate.shape()), du(w.up.shape()), dd(w.down.shape());

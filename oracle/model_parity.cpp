@@ -12,6 +12,7 @@
 // gradient as raw float32. With argv[3] = K > 0 the pass is K end-to-end train_step calls instead
 // (model.cpp:538-565: forward/backward + the reference's EPSO AdamW step, warmup 0): the header
 // carries the K per-step losses and the slots hold the final weights.
+// argv[4] = "wide": hidden 128, 4 x 32 heads, 8 experts of ffn 128 (the bf16 layer's shapes).
 // tests/test_gpu_model_parity.py compares the two builds.
 #include <cstdio>
 #include <cstdlib>
@@ -43,6 +44,13 @@ int main(int argc, char** argv) {
     cfg.vocab = 64;
     cfg.context = 8;
     cfg.aux_loss_coeff = 0.01;
+    if (argc > 4 && std::string(argv[4]) == "wide") {  // dims the bf16 tensor-core layer takes (H, I % 64 == 0)
+        cfg.hidden = 128;
+        cfg.heads = 4;
+        cfg.head_size = 32;
+        cfg.intermediate = 128;
+        cfg.experts = 8;
+    }
     TensorI batch({8, cfg.context});
     for (int64_t i = 0; i < batch.numel(); ++i) batch.data()[i] = (int64_t)(hash_mix(8000, (uint64_t)i) % (uint64_t)cfg.vocab);
     Topology serial;
