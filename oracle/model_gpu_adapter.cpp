@@ -7,6 +7,9 @@
 // fast_moe_forward / fast_moe_backward:
 //   moe_block_forward   blocks.cpp:339-355  -> b2_moe_forward + b2_moe_aux_loss + artifacts
 //   moe_block_backward  blocks.cpp:357-377  -> b2_moe_aux_probs_grad + b2_moe_backward
+//   ShardedOptimizer::step  optim.cpp:130-194 -> b2_opt_step (when the driver registers the
+//                           model's slots with b2_adapter_use_gpu_optimizer: grads up, the fused
+//                           EPSO AdamW on the device, bf16-rounded weights back)
 // This is exactly the adapter INTEGRATION.md describes for a maintainer (fp32 layer — or the
 // bf16 tensor-core layer with B2_ADAPTER_BF16=1 — EP = 1, one GPU state per MoeRec = per
 // (layer, microbatch), host Tensor in / Tensor out).
@@ -21,6 +24,7 @@
 
 #include "optimus/blocks.hpp"
 #include "optimus/kernels.hpp"
+#include "optimus/optim.hpp"
 #include "../include/b2moe.h"
 
 using namespace optimus;
@@ -191,4 +195,62 @@ TensorF __wrap__ZN7optimus18moe_block_backwardERNS_7RankCtxERKNS_12ProcessGroupE
     return dx;
 }
 
+}  // extern "C"
+
+// ---- the optimizer step on the B200 (optional: registered by the driver) ---------------------
+namespace {
+struct GpuOpt {
+    b2_opt* o = nullptr;
+    std::vector<ParamSlot> slots;
+    std::vector<float*> w, g;
+};
+GpuOpt* g_opt = nullptr;
+}  // namespace
+
+// the driver hands over the model's slots and the AdamW config; masters come from the current
+// weights, moments start at zero (optim.cpp:109-122)
+void b2_adapter_use_gpu_optimizer(const std::vector<ParamSlot>& slots, const AdamWConfig& c) {
+    if (!g_ctx) ok(b2_ctx_create(0, nullptr, 0, 1, 1, 1, 1, nullptr, &g_ctx), "ctx");
+    g_opt = new GpuOpt;
+    g_opt->slots = slots;
+    std::vector<b2_param> ps;
+    for (const ParamSlot& s : slots) {
+        float *w = nullptr, *g = nullptr;
+        const int64_t n = s.weight->numel();
+        cu(cudaMalloc((void**)&w, 4 * (size_t)n), "cudaMalloc");
+        cu(cudaMalloc((void**)&g, 4 * (size_t)n), "cudaMalloc");
+        cu(cudaMemcpy(w, s.weight->data(), 4 * (size_t)n, cudaMemcpyHostToDevice), "H2D");
+        g_opt->w.push_back(w);
+        g_opt->g.push_back(g);
+        ps.push_back(b2_param{w, g, n, s.cls == ReplicationClass::expert ? 1 : 0, s.tp_sharded ? 1 : 0});
+    }
+    b2_adamw_cfg ac{c.beta1, c.beta2, c.eps, c.weight_decay, c.peak_lr, c.min_lr, c.warmup_steps, c.total_steps,
+                    c.clip_norm, c.clip_after_warmup_only ? 1 : 0, c.round_weights_bf16 ? 1 : 0};
+    ok(b2_opt_create(g_ctx, &ac, ps.data(), (int)ps.size(), B2_EPSO, B2_F32, B2_F32, &g_opt->o), "opt create");
+}
+
+extern "C" {
+StepStats __real__ZN7optimus16ShardedOptimizer4stepEv(ShardedOptimizer* self);
+
+// ShardedOptimizer::step (optim.cpp:130-194); the reference's own step when no GPU optimizer
+// was registered
+StepStats __wrap__ZN7optimus16ShardedOptimizer4stepEv(ShardedOptimizer* self) {
+    if (!g_opt) return __real__ZN7optimus16ShardedOptimizer4stepEv(self);
+    for (size_t i = 0; i < g_opt->slots.size(); ++i) {
+        const TensorF& gr = *g_opt->slots[i].grad;
+        cu(cudaMemcpy(g_opt->g[i], gr.data(), 4 * (size_t)gr.numel(), cudaMemcpyHostToDevice), "H2D");
+    }
+    b2_step_stats st{};
+    ok(b2_opt_step(g_opt->o, &st), "opt step");
+    for (size_t i = 0; i < g_opt->slots.size(); ++i) {
+        TensorF& w = *g_opt->slots[i].weight;
+        cu(cudaMemcpy(w.data(), g_opt->w[i], 4 * (size_t)w.numel(), cudaMemcpyDeviceToHost), "D2H");
+    }
+    StepStats out;
+    out.step = st.step;
+    out.lr = st.lr;
+    out.grad_norm = st.grad_norm;
+    out.clip_scale = st.clip_scale;
+    return out;
+}
 }  // extern "C"

@@ -10,8 +10,9 @@
 //                     moe_block_backward: every MoE block on the B200 (libb2moe.so)
 // Output (argv[1]): "<ce_sum> <aux_sum> <n_slots>\n" then per slot "<name> <numel>\n" and the
 // gradient as raw float32. With argv[3] = K > 0 the pass is K end-to-end train_step calls instead
-// (model.cpp:538-565: forward/backward + the reference's EPSO AdamW step, warmup 0): the header
-// carries the K per-step losses and the slots hold the final weights.
+// (model.cpp:538-565: forward/backward + the reference's EPSO AdamW step, warmup 0; with
+// B2_ADAPTER_GPU_OPT=1 the GPU build runs that step on the B200 too): the header carries the K
+// per-step losses and the slots hold the final weights.
 // argv[4] = "wide": hidden 128, 4 x 32 heads, 8 experts of ffn 128 (the bf16 layer's shapes).
 // tests/test_gpu_model_parity.py compares the two builds.
 #include <cstdio>
@@ -25,6 +26,9 @@
 #include "optimus/schedule.hpp"
 
 using namespace optimus;
+
+// model_gpu_adapter.cpp (model_parity_gpu only): route ShardedOptimizer::step to the B200
+void b2_adapter_use_gpu_optimizer(const std::vector<ParamSlot>& slots, const AdamWConfig& c) __attribute__((weak));
 
 int main(int argc, char** argv) {
     if (argc < 2) {
@@ -66,6 +70,9 @@ int main(int argc, char** argv) {
             AdamWConfig ac;
             ac.warmup_steps = 0;
             ShardedOptimizer opt(ctx, ac, mdl.param_slots(), ShardMode::epso);
+            const char* gopt = std::getenv("B2_ADAPTER_GPU_OPT");
+            if (gopt && std::atoi(gopt) == 1 && b2_adapter_use_gpu_optimizer)
+                b2_adapter_use_gpu_optimizer(mdl.param_slots(), ac);
             for (int k = 0; k < steps; ++k) losses.push_back(train_step(ctx, mdl, opt, sched, batch, &led).loss);
         } else {
             parts = pp_forward_backward(ctx, mdl, sched, batch, &led);

@@ -60,18 +60,20 @@ def test_model_with_b200_moe_matches_reference(m):
     assert worst[0] <= 1e-4, worst
 
 
-def test_train_steps_with_b200_moe_match_reference():
-    """five end-to-end train_step calls (model.cpp:538-565): GPU MoE blocks + the reference's
-    EPSO AdamW on the CPU; per-step losses and the final weights of every parameter."""
+@pytest.mark.parametrize("gpu_opt", [0, 1], ids=["cpu-adamw", "b200-adamw"])
+def test_train_steps_with_b200_moe_match_reference(gpu_opt):
+    """five end-to-end train_step calls (model.cpp:538-565): GPU MoE blocks with the reference's
+    EPSO AdamW on the CPU, or (b200-adamw) with ShardedOptimizer::step on the B200 too
+    (b2_opt_step through the same link-time wrap); per-step losses and final weights."""
     if not (os.path.exists(REF) and os.path.exists(GPU)):
         pytest.skip("oracle/_ref/model_parity_* not built (make -C oracle model_parity)")
     with tempfile.TemporaryDirectory() as td:
         l_r, _, w_r = run(REF, 2, td, steps=5)
-        l_g, _, w_g = run(GPU, 2, td, steps=5)
+        l_g, _, w_g = run(GPU, 2, td, steps=5, env={"B2_ADAPTER_GPU_OPT": str(gpu_opt)})
     assert len(l_r) == len(l_g) == 5
     assert max(abs(a - b) / abs(b) for a, b in zip(l_g, l_r)) <= 1e-5, (l_g, l_r)
     worst = max(((rel_err(w_g[k], w_r[k]), k) for k in w_r))
-    print(f"train_step x5: losses {l_g} vs {l_r}; worst final-weight rel_err {worst}")
+    print(f"train_step x5 (gpu_opt={gpu_opt}): losses {l_g} vs {l_r}; worst final-weight rel_err {worst}")
     assert worst[0] <= 1e-4, worst
 
 
