@@ -11,13 +11,15 @@
 //                           model's slots with b2_adapter_use_gpu_optimizer: grads up, the fused
 //                           EPSO AdamW on the device, bf16-rounded weights back)
 // This is exactly the adapter INTEGRATION.md describes for a maintainer (fp32 layer — or the
-// bf16 tensor-core layer with B2_ADAPTER_BF16=1 — EP = 1, one GPU state per MoeRec = per
-// (layer, microbatch), host Tensor in / Tensor out).
+// bf16 tensor-core layer with B2_ADAPTER_BF16=1 — one GPU state per MoeRec = per (layer,
+// microbatch), host Tensor in / Tensor out; at EP > 1 each rank thread of the reference's World
+// drives the GPU of its EP coordinate).
 #include <cuda_runtime.h>
 
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -96,11 +98,26 @@ struct GpuLayer {
     int64_t apg_n = 0;
 };
 
-b2_ctx* g_ctx = nullptr;
-std::map<const MoeRec*, GpuLayer> g_layers;  // one GPU state per (layer, microbatch) record
+// EP > 1: the reference's rank threads each drive their own GPU (device = EP coordinate); the
+// layer's EP exchange then runs over direct peer access between the threads' devices, its
+// NCCL communicators from one id shared through this process
+thread_local b2_ctx* g_ctx = nullptr;
+thread_local std::map<const MoeRec*, GpuLayer> g_layers;  // one GPU state per (layer, microbatch)
+std::once_flag g_id_once;
+uint8_t g_nccl_id[128];
+
+void ensure_ctx(const RankCtx& rc, int E) {
+    if (g_ctx) return;
+    if (E <= 1) {
+        ok(b2_ctx_create(0, nullptr, 0, 1, 1, 1, 1, nullptr, &g_ctx), "ctx");
+        return;
+    }
+    std::call_once(g_id_once, [] { ok(b2_nccl_unique_id(g_nccl_id), "nccl id"); });
+    const int ep = rc.coord().ep;
+    ok(b2_ctx_create(ep, nullptr, ep, 1, E, 1, 1, g_nccl_id, &g_ctx), "ctx (EP)");
+}
 
 GpuLayer& layer_for(const MoeRec* rec, const MoeConfig& cfg, int64_t S) {
-    if (!g_ctx) ok(b2_ctx_create(0, nullptr, 0, 1, 1, 1, 1, nullptr, &g_ctx), "ctx");
     GpuLayer& L = g_layers[rec];
     if (!L.m || L.cap < S) {
         if (L.m) b2_moe_destroy(L.m);
@@ -125,9 +142,10 @@ extern "C" {
 
 // moe_block_forward (blocks.cpp:339-355) on the B200
 TensorF __wrap__ZN7optimus17moe_block_forwardERNS_7RankCtxERKNS_12ProcessGroupERKNS_6TensorIfEERKNS_13ExpertWeightsIfEERKNS_9MoeConfigEbbRNS_6MoeRecEPNS_9ActLedgerEPNS_11ExpertTallyE(
-    RankCtx&, const ProcessGroup& ep_group, const TensorF& x, const ExpertWeights<float>& w, const MoeConfig& cfg,
+    RankCtx& rctx, const ProcessGroup& ep_group, const TensorF& x, const ExpertWeights<float>& w, const MoeConfig& cfg,
     bool fur, bool ckpt, MoeRec& rec, ActLedger* led, ExpertTally* tally) {
-    check(ep_group.size() == 1, "b2 adapter: the GPU MoE block runs at EP = 1 in this harness");
+    check(ep_group.size() == cfg.ep, "b2 adapter: cfg.ep must match the EP group");
+    ensure_ctx(rctx, ep_group.size());
     const int64_t S = x.dim(0), H = cfg.hidden;
     GpuLayer& L = layer_for(&rec, cfg, S);
     rec.ckpt = ckpt;
@@ -159,9 +177,10 @@ TensorF __wrap__ZN7optimus17moe_block_forwardERNS_7RankCtxERKNS_12ProcessGroupER
 
 // moe_block_backward (blocks.cpp:357-377) on the B200; grads accumulate into g like the reference
 TensorF __wrap__ZN7optimus18moe_block_backwardERNS_7RankCtxERKNS_12ProcessGroupERKNS_13ExpertWeightsIfEERKNS_9MoeConfigEbdRNS_6MoeRecERKNS_6TensorIfEERNS_13MoeParamGradsEPNS_9ActLedgerE(
-    RankCtx&, const ProcessGroup& ep_group, const ExpertWeights<float>& w, const MoeConfig& cfg, bool, double aux_coeff,
-    MoeRec& rec, const TensorF& dy, MoeParamGrads& g, ActLedger* led) {
-    check(ep_group.size() == 1, "b2 adapter: the GPU MoE block runs at EP = 1 in this harness");
+    RankCtx& rctx, const ProcessGroup& ep_group, const ExpertWeights<float>& w, const MoeConfig& cfg, bool,
+    double aux_coeff, MoeRec& rec, const TensorF& dy, MoeParamGrads& g, ActLedger* led) {
+    check(ep_group.size() == cfg.ep, "b2 adapter: cfg.ep must match the EP group");
+    ensure_ctx(rctx, ep_group.size());
     const int64_t S = dy.dim(0), H = cfg.hidden;
     GpuLayer& L = layer_for(&rec, cfg, S);
     upload_weights(L, w);
@@ -210,7 +229,7 @@ GpuOpt* g_opt = nullptr;
 // the driver hands over the model's slots and the AdamW config; masters come from the current
 // weights, moments start at zero (optim.cpp:109-122)
 void b2_adapter_use_gpu_optimizer(const std::vector<ParamSlot>& slots, const AdamWConfig& c) {
-    if (!g_ctx) ok(b2_ctx_create(0, nullptr, 0, 1, 1, 1, 1, nullptr, &g_ctx), "ctx");
+    if (!g_ctx) ok(b2_ctx_create(0, nullptr, 0, 1, 1, 1, 1, nullptr, &g_ctx), "ctx");  // EP = 1 only
     g_opt = new GpuOpt;
     g_opt->slots = slots;
     std::vector<b2_param> ps;

@@ -14,6 +14,8 @@
 // B2_ADAPTER_GPU_OPT=1 the GPU build runs that step on the B200 too): the header carries the K
 // per-step losses and the slots hold the final weights.
 // argv[4] = "wide": hidden 128, 4 x 32 heads, 8 experts of ffn 128 (the bf16 layer's shapes).
+// argv[5] = EP: that many rank threads (Topology{ep}), each on the strided rows of
+// test_model.cpp:30-37 and (GPU build) on the GPU of its EP coordinate; one output file per rank.
 // tests/test_gpu_model_parity.py compares the two builds.
 #include <cstdio>
 #include <cstdlib>
@@ -57,7 +59,9 @@ int main(int argc, char** argv) {
     }
     TensorI batch({8, cfg.context});
     for (int64_t i = 0; i < batch.numel(); ++i) batch.data()[i] = (int64_t)(hash_mix(8000, (uint64_t)i) % (uint64_t)cfg.vocab);
+    const int ep = argc > 5 ? std::atoi(argv[5]) : 1;  // EP ranks (threads of the reference's World)
     Topology serial;
+    serial.ep = ep;
     World w(serial);
     int rc = 0;
     w.run([&](RankCtx& ctx) {
@@ -66,6 +70,11 @@ int main(int argc, char** argv) {
         ActLedger led;
         std::vector<double> losses;
         PpLossParts parts;
+        // strided rows per EP replica (test_model.cpp:30-37)
+        const int64_t rows = batch.dim(0) / ep, c = batch.dim(1);
+        TensorI local({rows, c});
+        for (int64_t r = 0; r < rows; ++r)
+            for (int64_t j = 0; j < c; ++j) local.data()[r * c + j] = batch.data()[(r * ep + ctx.coord().ep) * c + j];
         if (steps > 0) {
             AdamWConfig ac;
             ac.warmup_steps = 0;
@@ -73,12 +82,13 @@ int main(int argc, char** argv) {
             const char* gopt = std::getenv("B2_ADAPTER_GPU_OPT");
             if (gopt && std::atoi(gopt) == 1 && b2_adapter_use_gpu_optimizer)
                 b2_adapter_use_gpu_optimizer(mdl.param_slots(), ac);
-            for (int k = 0; k < steps; ++k) losses.push_back(train_step(ctx, mdl, opt, sched, batch, &led).loss);
+            for (int k = 0; k < steps; ++k) losses.push_back(train_step(ctx, mdl, opt, sched, local, &led).loss);
         } else {
-            parts = pp_forward_backward(ctx, mdl, sched, batch, &led);
+            parts = pp_forward_backward(ctx, mdl, sched, local, &led);
         }
         std::vector<ParamSlot> slots = mdl.param_slots();
-        FILE* f = std::fopen(argv[1], "wb");
+        const std::string path = ep > 1 ? std::string(argv[1]) + ".rank" + std::to_string(ctx.coord().ep) : argv[1];
+        FILE* f = std::fopen(path.c_str(), "wb");
         if (!f) {
             rc = 1;
             return;

@@ -17,6 +17,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <unistd.h>
+
 #include "comm.h"
 #include "kernels.h"
 
@@ -194,7 +196,8 @@ MoeLayer::~MoeLayer() {
     if (sym_) {
         cudaStreamSynchronize(ctx_.stream);
         for (int p = 0; p < (int)peer_base_.size(); ++p)
-            if (p != ctx_.coord_ep && peer_base_[(size_t)p]) cudaIpcCloseMemHandle(peer_base_[(size_t)p]);
+            if (p != ctx_.coord_ep && peer_base_[(size_t)p] && peer_ipc_[(size_t)p])
+                cudaIpcCloseMemHandle(peer_base_[(size_t)p]);
         cudaFree(sym_);
         cudaFree(peer_tab_);
     }
@@ -216,25 +219,46 @@ void MoeLayer::ep_setup() {
     // this rank's handle contribution on the same stream
     B2_CUDA(cudaMemsetAsync(sym_ + o_f, 0, 4 * (size_t)E, ctx_.stream));
     B2_CUDA(cudaMemsetAsync(bar_, 0, 4, ctx_.stream));
-    cudaIpcMemHandle_t h;
-    B2_CUDA(cudaIpcGetMemHandle(&h, sym_));
+    // per rank: the IPC handle (other processes) plus process id, device and raw address (ranks
+    // that are threads of one process — the reference's World — map peers directly instead)
+    struct Pub {
+        cudaIpcMemHandle_t h;
+        int64_t pid;
+        int64_t dev;
+        uint64_t addr;
+    };
     static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+    Pub mine{};
+    B2_CUDA(cudaIpcGetMemHandle(&mine.h, sym_));
+    mine.pid = (int64_t)getpid();
+    mine.dev = ctx_.device;
+    mine.addr = (uint64_t)(uintptr_t)sym_;
     char* dh = nullptr;
-    B2_CUDA(cudaMalloc(&dh, 64 * (size_t)E));
-    B2_CUDA(cudaMemcpyAsync(dh + 64 * me, &h, 64, cudaMemcpyHostToDevice, ctx_.stream));
-    B2_NCCL(ncclAllGather(dh + 64 * me, dh, 64, ncclUint8, ctx_.comm->ep.comm, ctx_.stream));
-    std::vector<cudaIpcMemHandle_t> hs((size_t)E);
-    B2_CUDA(cudaMemcpyAsync(hs.data(), dh, 64 * (size_t)E, cudaMemcpyDeviceToHost, ctx_.stream));
+    B2_CUDA(cudaMalloc(&dh, sizeof(Pub) * (size_t)E));
+    B2_CUDA(cudaMemcpyAsync(dh + sizeof(Pub) * me, &mine, sizeof(Pub), cudaMemcpyHostToDevice, ctx_.stream));
+    B2_NCCL(ncclAllGather(dh + sizeof(Pub) * me, dh, sizeof(Pub), ncclUint8, ctx_.comm->ep.comm, ctx_.stream));
+    std::vector<Pub> pubs((size_t)E);
+    B2_CUDA(cudaMemcpyAsync(pubs.data(), dh, sizeof(Pub) * (size_t)E, cudaMemcpyDeviceToHost, ctx_.stream));
     B2_CUDA(cudaStreamSynchronize(ctx_.stream));
     B2_CUDA(cudaFree(dh));
     peer_base_.assign((size_t)E, nullptr);
+    peer_ipc_.assign((size_t)E, 0);
     for (int p = 0; p < E; ++p) {
+        const Pub& q = pubs[(size_t)p];
         if (p == me) {
             peer_base_[(size_t)p] = sym_;
+        } else if (q.pid == mine.pid) {  // same process: direct peer access (UVA address)
+            if (q.dev != ctx_.device) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess((int)q.dev, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else B2_CUDA(e);
+            }
+            peer_base_[(size_t)p] = (char*)(uintptr_t)q.addr;
         } else {
             void* ptr = nullptr;
-            B2_CUDA(cudaIpcOpenMemHandle(&ptr, hs[(size_t)p], cudaIpcMemLazyEnablePeerAccess));
+            B2_CUDA(cudaIpcOpenMemHandle(&ptr, q.h, cudaIpcMemLazyEnablePeerAccess));
             peer_base_[(size_t)p] = (char*)ptr;
+            peer_ipc_[(size_t)p] = 1;
         }
     }
     std::vector<void*> tab((size_t)9 * E);

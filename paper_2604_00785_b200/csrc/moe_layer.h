@@ -242,6 +242,7 @@ class MoeLayer {
     const int32_t* gi_local_ = nullptr;  // this rank's dispatch table [S,K] (learned or FUR)
     char* sym_ = nullptr;
     std::vector<char*> peer_base_;
+    std::vector<char> peer_ipc_;  // 1: mapped through CUDA IPC (another process), 0: same process
     void** peer_tab_ = nullptr;  // device: tables of E pointers: x, dout, ret_f, ret_b, wret
     void *x_sh_ = nullptr, *dout_sh_ = nullptr, *ret_f_ = nullptr, *ret_b_ = nullptr;
     float* wret_ = nullptr;

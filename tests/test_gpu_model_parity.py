@@ -31,6 +31,18 @@ def run(binary, m, td, steps=0, wide=False, env=None):
         return float(ce), float(aux), read_slots(f, int(n))
 
 
+def run_ep(binary, ep, m, td):
+    """EP rank threads (the reference's World): one result file per rank."""
+    out = os.path.join(td, f"{os.path.basename(binary)}_ep{ep}.bin")
+    subprocess.run([binary, out, str(m), "0", "-", str(ep)], check=True, timeout=600)
+    res = []
+    for r in range(ep):
+        with open(f"{out}.rank{r}", "rb") as f:
+            ce, aux, n = f.readline().split()[:3]
+            res.append((float(ce), float(aux), read_slots(f, int(n))))
+    return res
+
+
 def read_slots(f, n):
     slots = {}
     for _ in range(n):
@@ -96,3 +108,22 @@ def test_model_with_bf16_tensor_core_moe_near_reference():
     print(f"bf16: ce {ce_g:.6f} vs {ce_r:.6f}, aux {aux_g:.6f} vs {aux_r:.6f}, worst grad scale err {worst}")
     assert abs(ce_g - ce_r) <= 1e-3 * abs(ce_r) and abs(aux_g - aux_r) <= 1e-3 * abs(aux_r)
     assert worst[0] <= 2e-2, worst
+
+
+def test_model_at_ep2_with_b200_moe_matches_reference():
+    """EP = 2: the reference's two rank threads each drive their own B200 (the layer's EP
+    exchange over direct peer access between the threads' devices, NCCL communicators from one
+    shared id); every rank's loss parts and gradients against the reference's EP = 2 run."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    if not (os.path.exists(REF) and os.path.exists(GPU)):
+        pytest.skip("oracle/_ref/model_parity_* not built (make -C oracle model_parity)")
+    with tempfile.TemporaryDirectory() as td:
+        ref = run_ep(REF, 2, 2, td)
+        gpu = run_ep(GPU, 2, 2, td)
+    for r, ((ce_r, aux_r, g_r), (ce_g, aux_g, g_g)) in enumerate(zip(ref, gpu)):
+        worst = max(((rel_err(g_g[k], g_r[k]), k) for k in g_r))
+        print(f"EP2 rank {r}: ce {ce_g:.9f} vs {ce_r:.9f}, aux {aux_g:.9f} vs {aux_r:.9f}, worst grad rel_err {worst}")
+        assert abs(ce_g - ce_r) <= 1e-5 * abs(ce_r) and abs(aux_g - aux_r) <= 1e-5 * abs(aux_r)
+        assert worst[0] <= 1e-4, (r, worst)
