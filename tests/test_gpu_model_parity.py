@@ -110,20 +110,21 @@ def test_model_with_bf16_tensor_core_moe_near_reference():
     assert worst[0] <= 2e-2, worst
 
 
-def test_model_at_ep2_with_b200_moe_matches_reference():
-    """EP = 2: the reference's two rank threads each drive their own B200 (the layer's EP
+@pytest.mark.parametrize("ep", [2, 4])
+def test_model_at_ep_with_b200_moe_matches_reference(ep):
+    """EP = 2 / 4: the reference's rank threads each drive their own B200 (the layer's EP
     exchange over direct peer access between the threads' devices, NCCL communicators from one
-    shared id); every rank's loss parts and gradients against the reference's EP = 2 run."""
+    shared id); every rank's loss parts and gradients against the reference's EP run."""
     import torch
-    if torch.cuda.device_count() < 2:
-        pytest.skip("needs 2 GPUs")
+    if torch.cuda.device_count() < ep:
+        pytest.skip(f"needs {ep} GPUs")
     if not (os.path.exists(REF) and os.path.exists(GPU)):
         pytest.skip("oracle/_ref/model_parity_* not built (make -C oracle model_parity)")
     with tempfile.TemporaryDirectory() as td:
-        ref = run_ep(REF, 2, 2, td)
-        gpu = run_ep(GPU, 2, 2, td)
+        ref = run_ep(REF, ep, 2, td)
+        gpu = run_ep(GPU, ep, 2, td)
     for r, ((ce_r, aux_r, g_r), (ce_g, aux_g, g_g)) in enumerate(zip(ref, gpu)):
         worst = max(((rel_err(g_g[k], g_r[k]), k) for k in g_r))
-        print(f"EP2 rank {r}: ce {ce_g:.9f} vs {ce_r:.9f}, aux {aux_g:.9f} vs {aux_r:.9f}, worst grad rel_err {worst}")
+        print(f"EP{ep} rank {r}: ce {ce_g:.9f} vs {ce_r:.9f}, aux {aux_g:.9f} vs {aux_r:.9f}, worst grad rel_err {worst}")
         assert abs(ce_g - ce_r) <= 1e-5 * abs(ce_r) and abs(aux_g - aux_r) <= 1e-5 * abs(aux_r)
         assert worst[0] <= 1e-4, (r, worst)
