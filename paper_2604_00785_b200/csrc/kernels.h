@@ -12,8 +12,9 @@ void launch_router_logits(const T* x, const T* w, float* logits, int S, int H, i
 void launch_softmax_topk(const float* logits, float* probs, float* topw, int32_t* topi, int S, int N, int K,
                          bool normalize, cudaStream_t st);
 void launch_fur_route(float* w, int32_t* idx, int S, int N, int K, cudaStream_t st);
+// partial: [ceil(S/128), N] scratch; ctr: one int32, zero before the first call (left zero)
 void launch_aux_stats(const float* probs, int S, int N, const int32_t* gidx, int64_t n_gidx, float* partial,
-                      float* mean_probs, int32_t* sel, cudaStream_t st);
+                      int32_t* ctr, float* mean_probs, int32_t* sel, cudaStream_t st);
 // dl_bf16 (optional): a bf16 copy of dlogits for the tensor-core router GEMMs
 void launch_router_dlogits(const float* probs, const float* wgrad, const int32_t* topi, const float* topw,
                            const float* aux_grad, float* dlogits, void* dl_bf16, int S, int N, int K, bool normalize,

@@ -113,11 +113,12 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     }
     ws_arena_.adopt(ws_->base, ws_->cap);
     // persistent per-layer state
-    arena_.reserve(4 * 256 + 4 * (size_t)N * 2 + 64);
+    arena_.reserve(5 * 256 + 4 * (size_t)N * 2 + 64);
     mean_probs_ = arena_.take<float>(N);
     sel_ = arena_.take<int32_t>(N);
     err_ = arena_.take<int32_t>(1);
     bar_ = arena_.take<int32_t>(8);
+    colsum_ctr_ = arena_.take<int32_t>(1);
     Arena& w = ws_arena_;
     logits_ = w.take<float>(smax_ * N);
     probs_ = w.take<float>(smax_ * N);
@@ -176,6 +177,7 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
         B2_CUDA(cudaEventCreateWithFlags(&ev_xall_, cudaEventDisableTiming));
     }
     B2_CUDA(cudaMemsetAsync(err_, 0, 4, ctx_.stream));
+    B2_CUDA(cudaMemsetAsync(colsum_ctr_, 0, 4, ctx_.stream));
     B2_CUDA(cudaMemsetAsync(pad_start_, 0, 4 * (nr + 1), ctx_.stream));
 }
 
@@ -512,8 +514,8 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     }
     // balancing statistics (381-386): mean_probs over the local rows, sel_counts over the
     // gathered table
-    launch_aux_stats(probs_, S, N, gi_, (int64_t)Tt * K, colsum_, mean_probs_, sel_, st);
-    launches_ += 3;
+    launch_aux_stats(probs_, S, N, gi_, (int64_t)Tt * K, colsum_, colsum_ctr_, mean_probs_, sel_, st);
+    launches_ += 2;
     mark(kRoute, true);
     mark(kIndex, false);
     // stages 2+3 (370-371)

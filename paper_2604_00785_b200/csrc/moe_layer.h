@@ -253,6 +253,7 @@ class MoeLayer {
     int32_t* gi_all_ = nullptr;
     float* gw_all_ = nullptr;
     int32_t* bar_ = nullptr;
+    int32_t* colsum_ctr_ = nullptr;  // arrival counter of the fused mean_probs reduction (self-resetting)
     float* wgrad_local_ = nullptr;
     void* dx_exp_ = nullptr;
 };

@@ -546,28 +546,52 @@ __global__ void fur_route_kernel(float* __restrict__ w, int32_t* __restrict__ id
 // ---- balancing statistics: mean_probs over local rows, sel_counts over the gathered
 // table (moe.hpp:381-386). Column sums use a fixed two-level order (deterministic).
 
-__global__ void prob_colsum_partial_kernel(const float* __restrict__ probs, float* __restrict__ partial,
-                                           int S, int N, int rows_per_block) {
+// One block per 128-row slice writes that slice's column sums; the last block to arrive
+// (arrival counter, self-resetting) adds the slices in slice order. Both levels keep the
+// fixed order of the former two-kernel version, so mean_probs is bitwise unchanged.
+__global__ void prob_colsum_kernel(const float* __restrict__ probs, float* __restrict__ partial,
+                                   int32_t* __restrict__ ctr, float* __restrict__ mean_probs, int S, int N,
+                                   int rows_per_block) {
     pdl_wait();
     pdl_launch();
+    constexpr int U = 16;
     const int r0 = blockIdx.x * rows_per_block;
+    const int r1 = min(S, r0 + rows_per_block);
     for (int e = threadIdx.x; e < N; e += blockDim.x) {
         float acc = 0.f;
-        const int r1 = min(S, r0 + rows_per_block);
-        for (int r = r0; r < r1; ++r) acc += probs[(int64_t)r * N + e];
+        int r = r0;
+        for (; r + U <= r1; r += U) {  // U independent loads in flight, then the sums in row order
+            float v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = __ldg(probs + (int64_t)(r + u) * N + e);
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc += v[u];
+        }
+        for (; r < r1; ++r) acc += probs[(int64_t)r * N + e];
         partial[(int64_t)blockIdx.x * N + e] = acc;
     }
-}
-
-__global__ void prob_colsum_final_kernel(const float* __restrict__ partial, float* __restrict__ mean_probs,
-                                         int nparts, int N, int S) {
-    pdl_wait();
-    pdl_launch();
+    __threadfence();
+    __syncthreads();
+    __shared__ int last;
+    if (threadIdx.x == 0) last = atomicAdd(ctr, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int nparts = gridDim.x;
     for (int e = threadIdx.x; e < N; e += blockDim.x) {
         float acc = 0.f;
-        for (int b = 0; b < nparts; ++b) acc += partial[(int64_t)b * N + e];
+        int b = 0;
+        for (; b + U <= nparts; b += U) {
+            float v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = __ldcg(partial + (int64_t)(b + u) * N + e);
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc += v[u];
+        }
+        for (; b < nparts; ++b) acc += __ldcg(partial + (int64_t)b * N + e);
         mean_probs[e] = acc * (float)(1.0 / (double)S);
     }
+    if (threadIdx.x == 0) *ctr = 0;
 }
 
 __global__ void sel_count_kernel(const int32_t* __restrict__ idx, int64_t n, int32_t* __restrict__ sel, int N) {
@@ -782,14 +806,12 @@ void launch_fur_route(float* w, int32_t* idx, int S, int N, int K, cudaStream_t 
 }
 
 void launch_aux_stats(const float* probs, int S, int N, const int32_t* gidx, int64_t n_gidx, float* partial,
-                      float* mean_probs, int32_t* sel, cudaStream_t st) {
+                      int32_t* ctr, float* mean_probs, int32_t* sel, cudaStream_t st) {
     B2_CUDA(cudaMemsetAsync(sel, 0, sizeof(int32_t) * N, st));
     if (S > 0) {
         const int rpb = 128;
         const int nparts = (int)ceil_div(S, rpb);
-        launch_k(prob_colsum_partial_kernel, dim3(nparts), dim3(128), 0, st, probs, partial, S, N, rpb);
-        B2_LAUNCH_CHECK();
-        launch_k(prob_colsum_final_kernel, dim3(1), dim3(256), 0, st, partial, mean_probs, nparts, N, S);
+        launch_k(prob_colsum_kernel, dim3(nparts), dim3(128), 0, st, probs, partial, ctr, mean_probs, S, N, rpb);
         B2_LAUNCH_CHECK();
     } else {
         B2_CUDA(cudaMemsetAsync(mean_probs, 0, sizeof(float) * N, st));
