@@ -106,21 +106,14 @@ __global__ void zero_pad_rows_kernel(T* __restrict__ buf, const int32_t* __restr
     const int lane = threadIdx.x % 32;
     const int64_t warps = (int64_t)gridDim.x * blockDim.x / 32;
     const bool vec = vec_ok<T>(W) && ((uintptr_t)buf & 15) == 0;
-    // a warp scans 32 rows' prow_src at once and zeroes the pad rows among them
-    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
-    for (int64_t c = gw * 32; c < P; c += warps * 32) {
-        const int64_t rl = c + lane;
-        unsigned pad = __ballot_sync(0xffffffffu, rl < P && prow_src[rl] < 0);
-        while (pad) {
-            const int64_t r = c + __ffs(pad) - 1;
-            pad &= pad - 1;
-            if (vec) {  // 16-byte stores: a warp writes 512 contiguous bytes per instruction
-                int4* d4 = reinterpret_cast<int4*>(buf + r * W);
-                const int nv = (int)((int64_t)W * sizeof(T) / 16);
-                for (int q = lane; q < nv; q += 32) d4[q] = make_int4(0, 0, 0, 0);
-            } else {
-                for (int q = lane; q < W; q += 32) buf[r * W + q] = Elem<T>::from_f(0.f);
-            }
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; r < P; r += warps) {
+        if (prow_src[r] >= 0) continue;
+        if (vec) {  // 16-byte stores: a warp writes 512 contiguous bytes per instruction
+            int4* d4 = reinterpret_cast<int4*>(buf + r * W);
+            const int nv = (int)((int64_t)W * sizeof(T) / 16);
+            for (int c = lane; c < nv; c += 32) d4[c] = make_int4(0, 0, 0, 0);
+        } else {
+            for (int c = lane; c < W; c += 32) buf[r * W + c] = Elem<T>::from_f(0.f);
         }
     }
 }

@@ -628,7 +628,34 @@ __global__ void router_dlogits_kernel(const float* __restrict__ probs, const flo
         dp[i] = 0.f;
         pr[i] = j < N ? probs[(int64_t)row * N + j] : 0.f;
     }
-    if (!fur) {
+    if (!fur && K <= 32) {
+        // lane k holds the row's k-th selection: the gathers and the per-k divisions run in
+        // parallel across lanes; raw_sum / dot still accumulate in k order (shuffled), and the
+        // selected experts are distinct, so every dp element receives exactly one add
+        const bool act = lane < K;
+        const int64_t ik = (int64_t)row * K + lane;
+        const int ek = act ? topi[ik] : 0;
+        const float gk = act ? wgrad[ik] : 0.f;
+        float addk = gk;
+        if (normalize) {
+            const float pk = act ? probs[(int64_t)row * N + ek] : 0.f;
+            const float wk = act ? topw[ik] : 0.f;
+            double raw_sum = 0, dot = 0;
+            for (int k = 0; k < K; ++k) raw_sum += (double)__shfl_sync(0xffffffffu, pk, k);
+            for (int k = 0; k < K; ++k)
+                dot += (double)__shfl_sync(0xffffffffu, gk, k) * (double)__shfl_sync(0xffffffffu, wk, k);
+            addk = (float)(((double)gk - dot) / raw_sum);
+        }
+        for (int k = 0; k < K; ++k) {
+            const int e = __shfl_sync(0xffffffffu, ek, k);
+            const float add = __shfl_sync(0xffffffffu, addk, k);
+            if (e % 32 == lane) {
+#pragma unroll
+                for (int i = 0; i < kMaxExpertsPerLane; ++i)
+                    if (i == e / 32) dp[i] += add;
+            }
+        }
+    } else if (!fur) {
         double raw_sum = 0, dot = 0;
         if (normalize) {
             for (int k = 0; k < K; ++k) raw_sum += (double)probs[(int64_t)row * N + topi[(int64_t)row * K + k]];

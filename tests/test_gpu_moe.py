@@ -170,6 +170,8 @@ F32_CASES = [
     dict(n_experts=8, top_k=2, hidden=16, intermediate=24, token_block=4, s=16, fur=True),
     dict(n_experts=64, top_k=8, hidden=128, intermediate=64, token_block=8, s=256),
     dict(n_experts=1, top_k=1, hidden=5, intermediate=7, token_block=8, s=6),
+    # top_k > 32: the router backward's serial per-k path (router_dlogits_kernel)
+    dict(n_experts=40, top_k=34, hidden=16, intermediate=8, token_block=4, s=24, normalize_topk=True),
 ]
 
 
