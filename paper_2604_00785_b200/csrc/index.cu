@@ -75,15 +75,24 @@ __device__ __forceinline__ int warp_incl_scan(int x, int lane) {
     return x;
 }
 
-// tiled exclusive block scan (coalesced), fixed order; returns the total
+// exclusive block scan (R consecutive elements per thread and round); returns the total
 template <class Get, class Put>
 __device__ int64_t block_scan(int64_t n, Get get, Put put, int* wsum) {
+    // each thread owns R consecutive elements per round: a serial local scan, one block
+    // scan of the thread totals, then the R exclusive prefixes (integer: order-independent)
+    constexpr int R = 16;
     const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nw = blockDim.x / 32;
     int64_t carry = 0;
-    for (int64_t base = 0; base < n; base += blockDim.x) {
-        const int64_t i = base + threadIdx.x;
-        const int v = i < n ? get(i) : 0;
-        const int x = warp_incl_scan(v, lane);
+    for (int64_t base = 0; base < n; base += (int64_t)blockDim.x * R) {
+        const int64_t i0 = base + (int64_t)threadIdx.x * R;
+        int v[R];
+        int tsum = 0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            v[r] = i0 + r < n ? get(i0 + r) : 0;
+            tsum += v[r];
+        }
+        const int x = warp_incl_scan(tsum, lane);
         if (lane == 31) wsum[warp] = x;
         __syncthreads();
         if (warp == 0) {
@@ -92,8 +101,12 @@ __device__ int64_t block_scan(int64_t n, Get get, Put put, int* wsum) {
             if (lane < nw) wsum[lane] = si;
         }
         __syncthreads();
-        const int64_t excl = carry + (warp > 0 ? wsum[warp - 1] : 0) + x - v;
-        if (i < n) put(i, excl);
+        int64_t excl = carry + (warp > 0 ? wsum[warp - 1] : 0) + x - tsum;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (i0 + r < n) put(i0 + r, excl);
+            excl += v[r];
+        }
         carry += wsum[nw - 1];
         __syncthreads();
     }
@@ -119,12 +132,21 @@ __global__ void __launch_bounds__(1024) scan_kernel(const int32_t* __restrict__ 
         int carry = 0;
         const int32_t* hrow = whist + (int64_t)ln * nchunks;
         int32_t* brow = wbase + (int64_t)ln * nchunks;
-        for (int c0 = 0; c0 < nchunks; c0 += 32) {
-            const int c = c0 + lane;
-            const int v = c < nchunks ? hrow[c] : 0;
-            const int x = warp_incl_scan(v, lane);
-            if (c < nchunks) brow[c] = carry + x - v;
-            carry += __shfl_sync(0xffffffffu, x, 31);
+        constexpr int P = 8;  // 8 x 32 chunk counts loaded together, then scanned in order
+        for (int cb = 0; cb < nchunks; cb += 32 * P) {
+            int vv[P];
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                const int c = cb + 32 * q + lane;
+                vv[q] = c < nchunks ? hrow[c] : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                const int c = cb + 32 * q + lane;
+                const int x = warp_incl_scan(vv[q], lane);
+                if (c < nchunks) brow[c] = carry + x - vv[q];
+                carry += __shfl_sync(0xffffffffu, x, 31);
+            }
         }
         if (lane == 0) tot[ln] = carry;
     }
