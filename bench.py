@@ -129,18 +129,23 @@ def bind_numa_local(torch, gpu: int):
     return "unbound"
 
 
+# the committed `ncu --set full` capture whose DRAM bytes back roofline.traffic (named, not globbed)
+GEMM_TRAFFIC_FILE = os.path.join("profiles", "r01s3_ncu_traffic.json")
+ADAMW_TRAFFIC_FILE = os.path.join("profiles", "r01_ncu_adamw_traffic.json")
+DATASHEET_BF16_TFLOPS = 2250.0  # dense bf16, B200 datasheet
+
+
 def ncu_traffic():
     """DRAM bytes (read + write) per step of the six expert-GEMM launches, from the committed
-    `ncu --set full` capture (tools/ncu_summary.py -> profiles/*_ncu_traffic.json)."""
-    import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_traffic.json")))
-    if not files:
+    `ncu --set full` capture GEMM_TRAFFIC_FILE (tools/ncu_summary.py writes it)."""
+    path = os.path.join(ROOT, GEMM_TRAFFIC_FILE)
+    if not os.path.exists(path):
         return None, None
-    with open(files[-1]) as f:
+    with open(path) as f:
         d = json.load(f)
     tot = sum(v["dram_bytes"] for k, v in d["kernels"].items()
               if "grouped_gemm_kernel" in k and k.split("<")[1][0] in "012345")
-    return tot, os.path.relpath(files[-1], ROOT)
+    return tot, GEMM_TRAFFIC_FILE
 
 
 def cpu_info():
@@ -210,7 +215,8 @@ def run_reference_arm(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD + f" (CPU sample: {ep * s_local} gathered tokens/step, EP={ep} rank threads)",
+        "config": {"workload": WORKLOAD.replace(", bf16", "") + f" (CPU sample: {ep * s_local} gathered tokens/step, "
+                               f"EP={ep} rank threads, f32 - the reference computes in f32)",
                    "parallelism": f"ep{ep} threads (reference World)"},
         "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": ep, "kind": which,
                          "sample": f"fast_moe_forward+backward, OLMoE shape, {ep}x{s_local} tokens per step, "
@@ -240,10 +246,13 @@ def mula7b_param_set(ep=1):
     return mula_param_set(16, 2048, 16, 128, 1024, 64, 50304, ep)
 
 
-def bench_adamw(torch, b2, ctx, dev, steps, warmup, world, rank, hbm_peak, dp=1):
+def bench_adamw(torch, b2, ctx, dev, steps, warmup, world, rank, hbm_peak, dp=1, mode=None):
     """EPSO step on the Mula-7B-A1B set. dp=1: DP=1 x EP=world (the EP axis, strong scaling);
     dp=world: DP=world x EP=1 (the DP axis: every rank holds all experts, expert grads are
-    reduce-scattered too — NVLink-bound by construction)."""
+    reduce-scattered too — NVLink-bound by construction). mode=SO runs the
+    reference's plain sharded optimizer (ShardMode::so, optim.hpp:37) on the same grid: non-expert
+    grads all-reduced over EP and every EP rank updates all of them."""
+    mode = b2.EPSO if mode is None else mode
     assert sum(n for n, _, _ in mula7b_param_set()) == 6_919_096_320
     per_rank = mula7b_param_set(world // dp)
     total = 6_919_096_320
@@ -254,7 +263,7 @@ def bench_adamw(torch, b2, ctx, dev, steps, warmup, world, rank, hbm_peak, dp=1)
              for n, _, _ in per_rank]
     cfg = b2.AdamWConfig(warmup_steps=0)
     opt = b2.ShardedOptimizer(ctx, cfg, [(w, g, int(e), int(t)) for (w, g, (n, e, t)) in zip(weights, grads, per_rank)],
-                              b2.EPSO)
+                              mode)
     for _ in range(warmup):
         opt.step(stats=False)
     torch.cuda.synchronize()
@@ -279,7 +288,7 @@ def bench_adamw(torch, b2, ctx, dev, steps, warmup, world, rank, hbm_peak, dp=1)
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
     traffic = None
-    tf = os.path.join(ROOT, "profiles", "r01_ncu_adamw_traffic.json")
+    tf = os.path.join(ROOT, ADAMW_TRAFFIC_FILE)
     if os.path.exists(tf):  # DRAM bytes per element of the capture (0.5 G elements), scaled to this step
         with open(tf) as f:
             k = json.load(f)["kernels"]
@@ -292,29 +301,31 @@ def bench_adamw(torch, b2, ctx, dev, steps, warmup, world, rank, hbm_peak, dp=1)
     ne_el = sum(n for n, e, _ in per_rank if not e)
     nvl = 2 * 2 * exp_el * (dp - 1) / dp + 2 * 2 * ne_el * (world - 1) / world
     t_roof = byt / (hbm_peak * 1e9) * 1e3 + nvl / 765e9 * 1e3
-    return {"metric": "sharded AdamW step ms (EPSO, Mula-7B-A1B param set, bf16 grads/weights, fp32 state)",
+    mname = {b2.EPSO: "EPSO", b2.SO: "SO", b2.DDP: "DDP"}[mode]
+    return {"metric": f"sharded AdamW step ms ({mname}, Mula-7B-A1B param set, bf16 grads/weights, fp32 state)",
             "parallelism": f"dp{dp} x ep{ep}", "scaling": "strong",
             "nvlink_bytes_per_rank": nvl, "t_roofline_ms": t_roof, "roofline_over_measured": t_roof / ms,
             "ms": ms, "params": total, "owned_params_per_rank": owned, "launches_per_step": launches,
             "grad_norm": st["grad_norm"],
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
-                         "traffic": traffic, "traffic_source": "profiles/r01_ncu_adamw_traffic.json (sumsq + update, "
-                                                               "per element x owned elements)",
+                         "traffic": traffic, "traffic_source": ADAMW_TRAFFIC_FILE + " (sumsq + update, per element x owned "
+                                                                        "elements)",
                          "algorithmic_bytes_per_step": byt}}
 
 
 def zipf_tokens(torch, dev, S, Hd, N, s, seed):
-    """Config E routing: logits[t,e] = log z_e + Gumbel(t,e), z_e ∝ (e+1)^-s,
-    identity expert permutation (the hottest experts on rank 0). Realised through the
-    layer's own router: x[:, :N] carries the logits and Wr = [I_N; 0]."""
+    """Config E routing (logits[t,e] = log z_e + noise, z_e ∝ (e+1)^-s, identity
+    expert permutation, the hottest experts on rank 0) through a router of realistic magnitude:
+    x ~ N(1, 1), Wr = column-centred N(0, 1.2825/sqrt(H)) + log z_e / H, so x·Wr = mean(x_t) ·
+    log z_e + N(0, 1.28²) (the Gumbel noise's std). Same construction as the parity test
+    (tests/test_gpu_bench_shapes.py::zipf_inputs)."""
     g = torch.Generator(device=dev).manual_seed(seed)
     z = (torch.arange(N, device=dev, dtype=torch.float64) + 1.0) ** -s
     z = z / z.sum()
-    u = torch.rand((S, N), device=dev, generator=g, dtype=torch.float64).clamp_(1e-12, 1.0)
-    x = torch.randn((S, Hd), device=dev, generator=g)
-    x[:, :N] = (torch.log(z)[None, :] - torch.log(-torch.log(u))).float()
-    router = torch.zeros((Hd, N), device=dev)
-    router[torch.arange(N), torch.arange(N)] = 1.0
+    x = torch.randn((S, Hd), device=dev, generator=g) + 1.0
+    wn = torch.randn((Hd, N), device=dev, generator=g, dtype=torch.float64) * (1.2825 / Hd ** 0.5)
+    wn -= wn.mean(0, keepdim=True)
+    router = (wn + torch.log(z)[None, :] / Hd).float()
     return x.bfloat16(), router.bfloat16()
 
 
@@ -326,6 +337,8 @@ def bench_zipf(torch, b2, ctx, dev, stream, world, rank, zipf_s, steps, warmup):
     cfg = b2.MoeConfig(n_experts=Nz, top_k=K, hidden=H, intermediate=I, ep=world, token_block=8)
     NR = Nz // world
     x, router = zipf_tokens(torch, dev, S, H, Nz, zipf_s, 4242 + rank)
+    if world > 1:  # one router for every rank (the tokens differ per rank)
+        dist.broadcast(router, src=0)
     gen = torch.Generator(device=dev).manual_seed(99 + rank)
     mk = lambda shape, std: (torch.randn(shape, device=dev, generator=gen) * std).bfloat16()
     gate, up, down, dout = mk((NR, H, I), 0.02), mk((NR, H, I), 0.02), mk((NR, I, H), 0.02), mk((S, H), 1.0)
@@ -375,6 +388,107 @@ def layer_rt(layer):
     return int(layer.artifacts()["rt"])
 
 
+def parity_check(torch, b2, dev, stream, router, gate, up, down, x, dout, world, S_par=256):
+    """Post-timing parity of the benchmarked configuration: the first
+    S_par tokens of this run's x/dout through a fresh EP=1 layer with this run's weights (the
+    full expert set; all-gathered over the EP ranks at N>1), against the CPU oracle
+    (oracle/liboracle.so, the C restatement pinned bitwise to the reference) on the same
+    bf16 values. Bars (north_star): routing indices and artifacts bit-exact; out / dX within
+    2e-2 rel_err elementwise; weight and router grads within 2e-2 of the tensor scale."""
+    import numpy as np
+    import torch.distributed as dist
+    from oracle import bind  # the checker only; the measured path never touches it
+    if world > 1:
+        full = []
+        for w in (gate, up, down):
+            buf = torch.empty((w.shape[0] * world,) + tuple(w.shape[1:]), dtype=w.dtype, device=dev)
+            dist.all_gather_into_tensor(buf, w.contiguous())
+            full.append(buf)
+        gate, up, down = full
+        if dist.get_rank() != 0:
+            return None
+    t0 = time.perf_counter()
+    Nf = gate.shape[0]
+    ctx1 = b2.Context(dev.index, stream=stream)
+    cfg = b2.MoeConfig(n_experts=Nf, top_k=K, hidden=H, intermediate=I)
+    xs, ds = x[:S_par].contiguous(), dout[:S_par].contiguous()
+    layer = b2.MoeLayer(ctx1, cfg, torch.bfloat16, S_par)
+    out = layer.forward(xs, router, gate, up, down)
+    g = layer.backward(router, gate, up, down, ds, layer.aux_probs_grad(0.01))
+    torch.cuda.synchronize()
+    _, wts, idx = layer.routing()
+    arts = layer.artifacts()
+    got = {k: v.float().cpu().numpy() for k, v in g.items()}
+    got["out"] = out.float().cpu().numpy()
+    layer.close()
+    ctx1.close()
+    orc = bind.get("orc")
+    ocfg = bind.moe_cfg(n_experts=Nf, top_k=K, hidden=H, intermediate=I)
+    f = lambda t: t.float().cpu().numpy()
+    ref = orc.moe_layer(ocfg, S_par, f(xs), f(router), f(gate), f(up), f(down), f(ds), aux_coeff=0.01)
+    oart = orc.artifacts(ocfg, ref["indices"], 0)
+
+    def rel(a, b):
+        return float(np.max(np.abs(a.astype(np.float64) - b) / np.maximum(1.0, np.maximum(np.abs(a), np.abs(b)))))
+
+    def scl(a, b):
+        return float(np.max(np.abs(a.astype(np.float64) - b)) / max(float(np.max(np.abs(b))), 1e-30))
+
+    art_keys = ("cum_token_counts", "cum_expert_counts", "input_indices", "output_indices", "selected_k")
+    res = {"tokens": S_par, "config": f"B dims (H {H}, N {Nf}, K {K}, I {I}), this run's weights and first "
+                                      f"{S_par} tokens", "oracle": "oracle/liboracle.so (C restatement, pinned "
+                                                                   "bitwise to the reference)",
+           "indices_bit_exact": bool(np.array_equal(idx, ref["indices"])),
+           "weights_bit_exact": bool(np.array_equal(wts, ref["weights"])),
+           "artifacts_bit_exact": bool(all(np.array_equal(np.asarray(arts[k]), oart[k]) for k in art_keys)),
+           "out_rel_err": rel(got["out"], ref["out"]), "dx_rel_err": rel(got["input"], ref["dx"]),
+           "drouter_scale_err": scl(got["router"], ref["drouter"][0]), "dgate_scale_err": scl(got["gate"], ref["dgate"]),
+           "dup_scale_err": scl(got["up"], ref["dup"]), "ddown_scale_err": scl(got["down"], ref["ddown"]),
+           "tol": 2e-2}
+    res["pass"] = bool(res["indices_bit_exact"] and res["weights_bit_exact"] and res["artifacts_bit_exact"] and
+                       all(v <= res["tol"] for k, v in res.items() if k.endswith("_err")))
+    res["seconds"] = round(time.perf_counter() - t0, 1)
+    return res
+
+
+def optimizer_cpu_baseline():
+    """ShardedOptimizer::step of the reference (oracle/_ref) on the host cores: SO and EPSO at
+    DP x EP = 1x1 and 2x2 (the reference's own rank threads), 8 M expert + 8 M non-expert
+    elements per rank (SURVEY §8d CPU baseline). ns per logical parameter element per step."""
+    from oracle import bind  # cpu_baseline leg only
+    import ctypes as C
+    if not bind.have_ref():
+        return None
+    ref = bind.get("ref")
+    fn = ref.lib.ref_bench_optim
+    fn.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int, C.POINTER(C.c_double)]
+    ne = nn = 8 << 20
+    out = []
+    for dp, ep in ((1, 1), (2, 2)):
+        for mode, name in ((1, "SO"), (2, "EPSO")):
+            sec = C.c_double()
+            if fn(dp, ep, mode, ne, nn, 2, C.byref(sec)) != 0:
+                raise RuntimeError(ref.lib.ref_last_error())
+            logical = ep * ne + nn  # expert elements differ per EP rank; non-expert ones are replicas
+            out.append({"mode": name, "dp": dp, "ep": ep, "threads": dp * ep, "step_ms": sec.value * 1e3,
+                        "ns_per_element": sec.value * 1e9 / logical, "logical_elements": logical})
+    return out
+
+
+def self_launch(args) -> bool:
+    """`bench.py --gpus N` without torchrun: re-launch this script as N ranks (one process per
+    GPU, torch.distributed.run over 127.0.0.1) so the JSON line always reports n_gpus = N."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return False
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -384,11 +498,13 @@ def main():
     ap.add_argument("--profile", action="store_true", help="print per-stage times to stderr")
     ap.add_argument("--no-adamw", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the post-timing oracle check")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA-graph replay")
     ap.add_argument("--zipf", type=float, default=1.2,
                     help="Zipf exponent of the config-E load-imbalance line (96 experts); 0 disables it")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    self_launch(args)
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
@@ -400,6 +516,8 @@ def main():
 
     import paper_2604_00785_b200 as b2
 
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; refusing to report n_gpus={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     all_cpus = set(os.sched_getaffinity(0))
@@ -516,10 +634,18 @@ def main():
 
     del layer
     torch.cuda.empty_cache()
+    parity = None
+    if not args.no_parity:
+        try:
+            parity = parity_check(torch, b2, dev, stream, router, gate, up, down, x, dout, world)
+        except Exception as e:  # reported in the line, never silently dropped
+            parity = {"pass": False, "error": f"{type(e).__name__}: {e}"}
+        if world > 1:
+            dist.barrier()
     zipf = None
     if args.zipf > 0:
         zipf = bench_zipf(torch, b2, ctx, dev, stream, world, rank, args.zipf, max(2, args.steps // 2), 2)
-    adamw = adamw_dp = None
+    adamw = adamw_dp = adamw_so = None
     if not args.no_adamw:
         adamw = bench_adamw(torch, b2, ctx, dev, 5, 2, world, rank, hbm_peak)
         if world > 1:  # the DP axis of config D on its own communicators
@@ -528,6 +654,7 @@ def main():
             ctx_dp = b2.Context(local, rank=rank, dp=world, ep=1, nccl_id=ids[0], stream=stream)
             adamw_dp = bench_adamw(torch, b2, ctx_dp, dev, 3, 1, world, rank, hbm_peak, dp=world)
             ctx_dp.close()
+            adamw_so = bench_adamw(torch, b2, ctx, dev, 3, 1, world, rank, hbm_peak, mode=b2.SO)
 
     cpu = None
     os.sched_setaffinity(0, all_cpus)  # the CPU reference leg may use every host core
@@ -541,6 +668,10 @@ def main():
                              f"(EP={ep} rank threads, f32) in {secs:.1f} s on {model} ({ncpu} cpus)"}
         except Exception as e:  # reported, never fatal for the GPU number
             cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+        try:
+            cpu["optimizer"] = optimizer_cpu_baseline()
+        except Exception as e:
+            cpu["optimizer"] = f"failed: {e}"
 
     traffic, traffic_src = ncu_traffic()
     if rank == 0:
@@ -558,17 +689,22 @@ def main():
                          "peak_kind": peak_kind,
                          "kernel": "tcgen05 grouped GEMMs (6 kinds, 9 expert GEMMs)",
                          "flop_per_step": gemm_flop, "gemm_ms_per_step": gemm_ms,
-                         "frac_of_sustained": achieved / bf16_sust if bf16_sust else None},
+                         "frac_of_sustained": achieved / bf16_sust if bf16_sust else None,
+                         "frac_of_datasheet": achieved / DATASHEET_BF16_TFLOPS},
             "stage_ms": {k: round(v, 4) for k, v in st.items()},
             "ep_rows_max_over_mean": ep_balance,
             "model_flop_per_token": FLOP_PER_TOKEN,
             "model_tflops": value * FLOP_PER_TOKEN / 1e12 / world,
+            "model_frac_of_measured_peak": value * FLOP_PER_TOKEN / 1e12 / world / bf16_peak,
+            "model_frac_of_datasheet": value * FLOP_PER_TOKEN / 1e12 / world / DATASHEET_BF16_TFLOPS,
+            "parity": parity,
             "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": 2 * tok_bytes,
                     "d2h_bytes_per_step": 2 * tok_bytes},
             "gpu_launches": launches,
             "clocks": clk,
             "adamw": adamw,
             "adamw_dp_axis": adamw_dp,
+            "adamw_so": adamw_so,
             "zipf": zipf,
             "cpu_baseline": cpu,
         }

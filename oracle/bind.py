@@ -205,6 +205,16 @@ class Oracle:
         self._check(rc)
         return r
 
+    def dense_moe_forward(self, cfg: MoeCfg, x, gate, up, down, weights, indices):
+        """reference_moe_forward (moe.hpp:471-497): the dense per-token oracle, full expert set."""
+        cv = lambda a: np.ascontiguousarray(a, np.float32)
+        x, gate, up, down, weights = map(cv, (x, gate, up, down, weights))
+        indices = np.ascontiguousarray(indices, np.int64)
+        out = np.zeros_like(x)
+        self._check(self._f("dense_moe_forward_f32")(C.byref(cfg), I64(x.shape[0]), _p(x), _p(gate), _p(up),
+                                                     _p(down), _p(weights), _p(indices), _p(out)))
+        return out
+
     # ---- optimizer ----
     def adamw_cfg(self, **kw) -> AdamWCfg:
         c = AdamWCfg()

@@ -9,7 +9,8 @@
  *   moe.hpp:13-31        MoeConfig::validate
  *   moe.hpp:122-164      count_tokens
  *   moe.hpp:167-197      generate_indices
- *   moe_oracle_impl.h    route / expert MLP / reductions / backward (moe.hpp:58-466)
+ *   moe_oracle_impl.h    route / expert MLP / reductions / backward (moe.hpp:58-466),
+ *                        dense per-token reference_moe_forward (moe.hpp:471-497)
  *   optim.cpp:17-24      lr_at_step
  *   optim.cpp:43-50      shard_slice
  *   optim.cpp:52-86      build_shard_plan / counts_toward_norm
@@ -69,9 +70,11 @@ double orc_normal_at(uint64_t seed, uint64_t tag, uint64_t i) {
     return sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
 }
 void orc_normal_init_f32(float* out, int64_t n, uint64_t seed, uint64_t tag, double stddev) {
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) out[i] = (float)(orc_normal_at(seed, tag, (uint64_t)i) * stddev);
 }
 void orc_normal_init_f64(double* out, int64_t n, uint64_t seed, uint64_t tag, double stddev) {
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) out[i] = orc_normal_at(seed, tag, (uint64_t)i) * stddev;
 }
 /* rng.next_below used by the reference tests (common.hpp:90-100) */
@@ -294,6 +297,18 @@ int orc_moe_layer_f64(const orc_moe_cfg* c, int64_t s, const double* x, const do
                       double* probs, double* aux) {
     return moe_layer_f64(c, s, x, router, gate, up, down, dout, fur, aux_coeff, do_backward, out, dx,
                          drouter, dgate, dup, ddown, weights, idx, probs, aux);
+}
+
+/* moe.hpp:471-497 reference_moe_forward (dense per-token oracle), full expert set [N,...] */
+int orc_dense_moe_forward_f32(const orc_moe_cfg* c, int64_t t_total, const float* x, const float* gate,
+                              const float* up, const float* down, const float* weights,
+                              const int64_t* indices, float* out) {
+    if (orc_validate(c)) return 1;
+    if (dense_forward_f32(c, t_total, x, gate, up, down, weights, indices, out)) {
+        strcpy(g_err, "reference_moe: expert id out of range");
+        return 1;
+    }
+    return 0;
 }
 
 /* ---- optimizer (optim.cpp) ------------------------------------------------------------- */

@@ -12,6 +12,7 @@
 
 /* kernels.hpp:16-49 matmul, non-f64 path: out[i,j] += a[i,p] * b[p,j], p outer */
 static void SFX(matmul)(const T* a, const T* b, T* out, int64_t m, int64_t k, int64_t n) {
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < m; ++i) {
         T* op = out + i * n;
         for (int64_t j = 0; j < n; ++j) op[j] = (T)0;
@@ -25,13 +26,15 @@ static void SFX(matmul)(const T* a, const T* b, T* out, int64_t m, int64_t k, in
 
 /* kernels.hpp:52-72 matmul_tn: a [K,M], b [K,N] -> [M,N] (accumulates into zeroed out) */
 static void SFX(matmul_tn)(const T* a, const T* b, T* out, int64_t k, int64_t m, int64_t n) {
-    for (int64_t i = 0; i < m * n; ++i) out[i] = (T)0;
-    for (int64_t p = 0; p < k; ++p) {
-        const T* ap = a + p * m;
-        const T* bp = b + p * n;
-        for (int64_t i = 0; i < m; ++i) {
-            const T av = ap[i];
-            T* op = out + i * n;
+    /* the reference runs p outer, i inner; every out[i,j] still accumulates p = 0..k-1 in
+     * order here (i outer, split across threads), so the result is bitwise the same */
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < m; ++i) {
+        T* op = out + i * n;
+        for (int64_t j = 0; j < n; ++j) op[j] = (T)0;
+        for (int64_t p = 0; p < k; ++p) {
+            const T av = a[p * m + i];
+            const T* bp = b + p * n;
             for (int64_t j = 0; j < n; ++j) op[j] += av * bp[j];
         }
     }
@@ -39,6 +42,7 @@ static void SFX(matmul_tn)(const T* a, const T* b, T* out, int64_t k, int64_t m,
 
 /* kernels.hpp:75-96 matmul_nt: a [M,K], b [N,K] -> [M,N] */
 static void SFX(matmul_nt)(const T* a, const T* b, T* out, int64_t m, int64_t k, int64_t n) {
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < m; ++i) {
         const T* ap = a + i * k;
         T* op = out + i * n;
@@ -57,6 +61,7 @@ static void SFX(grouped_mm)(const T* in, const T* w, const int64_t* bnd, int64_t
     for (int64_t i = 0; i < rows * k2; ++i) out[i] = (T)0;
     for (int64_t g = 0; g < groups; ++g) {
         const T* wg = w + g * k1 * k2;
+#pragma omp parallel for schedule(static)
         for (int64_t i = bnd[g]; i < bnd[g + 1]; ++i) {
             T* op = out + i * k2;
             const T* ip = in + i * k1;
@@ -75,6 +80,7 @@ static void SFX(grouped_mm_nt)(const T* in, const T* w, const int64_t* bnd, int6
     for (int64_t i = 0; i < rows * k1; ++i) out[i] = (T)0;
     for (int64_t g = 0; g < groups; ++g) {
         const T* wg = w + g * k1 * k2;
+#pragma omp parallel for schedule(static)
         for (int64_t i = bnd[g]; i < bnd[g + 1]; ++i) {
             const T* ip = in + i * k2;
             T* op = out + i * k1;
@@ -91,15 +97,17 @@ static void SFX(grouped_mm_nt)(const T* in, const T* w, const int64_t* bnd, int6
 /* kernels.hpp:165-189 grouped_mm_weight_grad: x [R,K1], dy [R,K2] -> [G,K1,K2] */
 static void SFX(grouped_wgrad)(const T* x, const T* dy, const int64_t* bnd, int64_t groups,
                                int64_t k1, int64_t k2, T* out) {
+    /* the reference runs rows i outer, p inner; every out[g,p,j] still accumulates its
+     * group's rows in ascending order here (p rows split across threads) -> bitwise equal */
     for (int64_t i = 0; i < groups * k1 * k2; ++i) out[i] = (T)0;
     for (int64_t g = 0; g < groups; ++g) {
         T* wg = out + g * k1 * k2;
-        for (int64_t i = bnd[g]; i < bnd[g + 1]; ++i) {
-            const T* xp = x + i * k1;
-            const T* dp = dy + i * k2;
-            for (int64_t p = 0; p < k1; ++p) {
-                const T xv = xp[p];
-                T* wp = wg + p * k2;
+#pragma omp parallel for schedule(static)
+        for (int64_t p = 0; p < k1; ++p) {
+            T* wp = wg + p * k2;
+            for (int64_t i = bnd[g]; i < bnd[g + 1]; ++i) {
+                const T xv = x[i * k1 + p];
+                const T* dp = dy + i * k2;
                 for (int64_t j = 0; j < k2; ++j) wp[j] += xv * dp[j];
             }
         }
@@ -426,5 +434,54 @@ static int SFX(moe_layer)(const orc_moe_cfg* c, int64_t S, const T* x_full, cons
     free(i_g);
     free(r_w);
     free(r_i);
+    return 0;
+}
+
+/* moe.hpp:471-497 reference_moe_forward: the dense per-token oracle. For each token and
+ * each of its K selections (k order), y = matmul(silu_glu(matmul(x, Wg_e), matmul(x, Wu_e)),
+ * Wd_e) with matmul's non-f64 p-outer order (kernels.hpp:37-46) and silu_glu in fp64
+ * (kernels.hpp:262-275); out[t] += w[t,k] * y. Tokens are independent (split across
+ * threads); every element keeps the reference's order, so the result is bitwise its own. */
+static int SFX(dense_forward)(const orc_moe_cfg* c, int64_t t_total, const T* input, const T* gate,
+                              const T* up, const T* down, const T* weights, const int64_t* indices,
+                              T* out) {
+    const int64_t H = c->hidden, I = c->intermediate, K = c->top_k, N = c->n_experts;
+    for (int64_t i = 0; i < t_total * K; ++i)
+        if (indices[i] < 0 || indices[i] >= N) return 1;
+#pragma omp parallel
+    {
+        T* g = (T*)malloc(sizeof(T) * (size_t)(3 * I + H));
+        T *u = g + I, *hm = u + I, *y = hm + I;
+#pragma omp for schedule(dynamic, 4)
+        for (int64_t t = 0; t < t_total; ++t) {
+            const T* xp = input + t * H;
+            T* op = out + t * H;
+            for (int64_t cc = 0; cc < H; ++cc) op[cc] = (T)0;
+            for (int64_t k = 0; k < K; ++k) {
+                const int64_t e = indices[t * K + k];
+                const T* wg = gate + e * H * I;
+                const T* wu = up + e * H * I;
+                const T* wd = down + e * I * H;
+                for (int64_t j = 0; j < I; ++j) g[j] = u[j] = (T)0;
+                for (int64_t p = 0; p < H; ++p) {
+                    const T av = xp[p];
+                    for (int64_t j = 0; j < I; ++j) g[j] += av * wg[p * I + j];
+                }
+                for (int64_t p = 0; p < H; ++p) {
+                    const T av = xp[p];
+                    for (int64_t j = 0; j < I; ++j) u[j] += av * wu[p * I + j];
+                }
+                for (int64_t j = 0; j < I; ++j) hm[j] = (T)(SFX(silu_scalar)((double)g[j]) * (double)u[j]);
+                for (int64_t cc = 0; cc < H; ++cc) y[cc] = (T)0;
+                for (int64_t p = 0; p < I; ++p) {
+                    const T av = hm[p];
+                    for (int64_t cc = 0; cc < H; ++cc) y[cc] += av * wd[p * H + cc];
+                }
+                const T wv = weights[t * K + k];
+                for (int64_t cc = 0; cc < H; ++cc) op[cc] += wv * y[cc];
+            }
+        }
+        free(g);
+    }
     return 0;
 }

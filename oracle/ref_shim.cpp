@@ -11,6 +11,7 @@
 //   fast_moe_forward       include/optimus/moe.hpp:344-390
 //   fast_moe_backward      include/optimus/moe.hpp:392-466
 //   moe_aux_probs_grad     include/optimus/moe.hpp:331-342
+//   reference_moe_forward  include/optimus/moe.hpp:471-497 (dense per-token oracle)
 //   adamw_update           src/optim.cpp:88-107
 //   lr_at_step             src/optim.cpp:17-24
 //   shard_slice            src/optim.cpp:43-50
@@ -202,6 +203,29 @@ static int moe_layer_impl(const ref_moe_cfg* c, int64_t s_local, const T* x_full
         });
     });
 }
+
+extern "C" {
+// reference_moe_forward (include/optimus/moe.hpp:471-497): the dense per-token oracle over the
+// full expert set; weights/indices are the routing of the same tokens ([T,K]).
+int ref_dense_moe_forward_f32(const ref_moe_cfg* c, int64_t t_total, const float* x,
+                              const float* gate, const float* up, const float* down,
+                              const float* weights, const int64_t* indices, float* out) {
+    return guard([&] {
+        MoeConfig cfg = to_cfg(c);
+        cfg.validate();
+        const int64_t H = cfg.hidden, I = cfg.intermediate, N = cfg.n_experts, K = cfg.top_k;
+        ExpertWeights<float> w;
+        w.gate = Tensor<float>({N, H, I}, std::vector<float>(gate, gate + N * H * I));
+        w.up = Tensor<float>({N, H, I}, std::vector<float>(up, up + N * H * I));
+        w.down = Tensor<float>({N, I, H}, std::vector<float>(down, down + N * I * H));
+        Tensor<float> in({t_total, H}, std::vector<float>(x, x + t_total * H));
+        Tensor<float> wt({t_total, K}, std::vector<float>(weights, weights + t_total * K));
+        TensorI idx({t_total, K}, std::vector<int64_t>(indices, indices + t_total * K));
+        Tensor<float> o = reference_moe_forward<float>(in, w, wt, idx, cfg);
+        std::memcpy(out, o.data(), o.bytes());
+    });
+}
+}  // extern "C"
 
 extern "C" {
 int ref_moe_layer_f32(const ref_moe_cfg* c, int64_t s_local, const float* x, const float* router,

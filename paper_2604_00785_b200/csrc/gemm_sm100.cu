@@ -87,6 +87,7 @@ struct KCfg {
 
 struct Params {
     CUtensorMap mapA;
+    CUtensorMap mapA1;  // RouterDx: the low bf16 half of dlogits (K blocks past num_kb_fixed / 2)
     CUtensorMap mapB0;
     CUtensorMap mapB1;
     CUtensorMap mapG;  // BwdDownDgrad epilogue operands (32 x 32 boxes, SWIZZLE_64B)
@@ -554,8 +555,11 @@ __device__ __forceinline__ void load_stage(const Params& p, const TileInfo& ti, 
         if (k0 < p.I) ld(sB, &p.mapB0, k0, ti.e * p.H + nb);
         else ld(sB, &p.mapB1, k0 - p.I, ti.e * p.H + nb);
     } else if constexpr (KIND == GemmKind::RouterDx) {
-        ld(sA, &p.mapA, k0, ti.m0);
-        ld(sB, &p.mapB0, k0, ti.n0);
+        // K runs twice over the experts: dl_hi · Wrᵀ, then dl_lo · Wrᵀ into the same accumulator
+        const int kh = (p.num_kb_fixed / 2) * BK;
+        if (k0 < kh) ld(sA, &p.mapA, k0, ti.m0);
+        else ld(sA, &p.mapA1, k0 - kh, ti.m0);
+        ld(sB, &p.mapB0, k0 < kh ? k0 : k0 - kh, ti.n0);
     } else if constexpr (KIND == GemmKind::RouterDw) {
         const int row = ti.krow0 + k0;
         ld(sA + 0, &p.mapA, ti.m0, row);
@@ -1588,11 +1592,13 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             check(a.N % 8 == 0 && a.N <= 256, "router dx GEMM: n_experts must be a multiple of 8, <= 256");
             const int64_t S = a.S;
             if (S <= 0) return;
+            check(a.dl_lo != nullptr, "router dx GEMM: needs the low half of the dlogits split");
             p.mapA = make_map(a.dl, a.N, S, 64, BM);
+            p.mapA1 = make_map(a.dl_lo, a.N, S, 64, BM);
             p.mapB0 = make_map(a.wr, a.N, H, 64, BN);
             p.mapB1 = p.mapB0;
             p.n_tiles = (int)ceil_div(H, BN);
-            p.num_kb_fixed = (int)ceil_div(a.N, BK);
+            p.num_kb_fixed = 2 * (int)ceil_div(a.N, BK);  // hi then lo
             p.cec = a.cec;
             p.slot_prow = a.slot_prow;
             p.src = (const __nv_bfloat16*)a.src;

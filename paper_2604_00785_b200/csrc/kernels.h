@@ -15,10 +15,11 @@ void launch_fur_route(float* w, int32_t* idx, int S, int N, int K, cudaStream_t 
 // partial: [ceil(S/128), N] scratch; ctr: one int32, zero before the first call (left zero)
 void launch_aux_stats(const float* probs, int S, int N, const int32_t* gidx, int64_t n_gidx, float* partial,
                       int32_t* ctr, float* mean_probs, int32_t* sel, cudaStream_t st);
-// dl_bf16 (optional): a bf16 copy of dlogits for the tensor-core router GEMMs
+// dl_bf16 (optional): bf16(dlogits) for the tensor-core router GEMMs; dl_lo (optional):
+// bf16(dlogits - dl_bf16), the low half of a two-term split (RouterDx)
 void launch_router_dlogits(const float* probs, const float* wgrad, const int32_t* topi, const float* topw,
-                           const float* aux_grad, float* dlogits, void* dl_bf16, int S, int N, int K, bool normalize,
-                           bool fur, cudaStream_t st);
+                           const float* aux_grad, float* dlogits, void* dl_bf16, void* dl_lo, int S, int N, int K,
+                           bool normalize, bool fur, cudaStream_t st);
 void launch_aux_probs_grad(const int32_t* sel, float* out, int S, int N, double coeff, double total,
                            cudaStream_t st);
 // dWr = x^T dlogits with a deterministic split over S; part holds max_splits*H*N floats
@@ -154,7 +155,8 @@ struct Sm100GemmArgs {
     // router kinds
     int S, N;                    // local tokens, experts
     const void* wr;              // router weight [H, N] bf16
-    const void* dl;              // dlogits [S, N] bf16
+    const void* dl;              // dlogits [S, N] bf16 (RouterDx: the high half of the split)
+    const void* dl_lo;           // RouterDx: bf16(dlogits - dl) [S, N]
     const int32_t* cec;          // RouterDx: cum_expert_counts [S+1] (null: add `base` rows instead)
     const int32_t* slot_prow;    // RouterDx: slot -> padded row of dXperm
     const void* src;             // RouterDx: dXperm [P, H] (slots) or base [S, H]

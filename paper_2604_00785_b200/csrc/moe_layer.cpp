@@ -92,7 +92,8 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     for (int64_t n : {pmax_ * H, pmax_ * I, pmax_ * I, pmax_ * I, pmax_ * H, pmax_ * H, pmax_ * I, pmax_ * 2 * I,
                       pmax_ * H, smax_ * H})
         acc(es * (size_t)std::max<int64_t>(n, 1));
-    acc(2 * (size_t)std::max<int64_t>(smax_ * N, 1));
+    acc(2 * (size_t)std::max<int64_t>(smax_ * N, 1));  // dl_bf16_
+    acc(2 * (size_t)std::max<int64_t>(smax_ * N, 1));  // dl_lo_
     const int E = cfg_.ep;
     if (E > 1) {
         for (int64_t n : {tmax_ * K, tmax_ * K, smax_ * K}) acc(4 * (size_t)std::max<int64_t>(n, 1));
@@ -155,6 +156,7 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     dgu_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * 2 * I, 1));
     dxp_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
     dl_bf16_ = w.take_bytes(2 * (size_t)std::max<int64_t>(smax_ * N, 1));
+    dl_lo_ = w.take_bytes(2 * (size_t)std::max<int64_t>(smax_ * N, 1));
     replay_out_ = w.take_bytes(es * (size_t)std::max<int64_t>(smax_ * H, 1));
     if (E > 1) {
         check(ctx_.comm != nullptr && ctx_.comm->ep.size == E, "fast_moe: EP > 1 needs the EP communicator");
@@ -965,9 +967,10 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
     }
     const bool tc_router = dtype_ == BF16 && N % 8 == 0 && N <= 256;
     launch_router_dlogits(probs_, wgrad_local, topi_, topw_, aux_probs_grad, dlogits_, tc_router ? dl_bf16_ : nullptr,
-                          S, N, K, cfg_.normalize_topk, fur_, st);
+                          tc_router ? dl_lo_ : nullptr, S, N, K, cfg_.normalize_topk, fur_, st);
     if (tc_router) {
-        // router dW and dx on the tensor cores (bf16 dlogits, fp32 accumulation)
+        // router dW and dx on the tensor cores (fp32 accumulation; dW from bf16 dlogits, dx from the
+        // two-term hi + lo split so the O(1) router weights of a real model keep dx fp32-accurate)
         Sm100GemmArgs ga{};
         ga.H = H;
         ga.I = I;
@@ -979,6 +982,7 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         ga.N = N;
         ga.x = x_;
         ga.dl = dl_bf16_;
+        ga.dl_lo = dl_lo_;
         ga.wr = router;
         ga.part = dw_part_;
         ga.kind = GemmKind::RouterDw;

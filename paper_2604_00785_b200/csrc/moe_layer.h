@@ -221,6 +221,7 @@ class MoeLayer {
     // dtype buffers (padded row space)
     void *mlp_in_, *g_, *u_, *h_, *y_, *dy_, *dh_, *dgu_, *dxp_;
     void* dl_bf16_ = nullptr;  // bf16 dlogits for the tensor-core router GEMMs
+    void* dl_lo_ = nullptr;    // bf16(dlogits - dl_bf16_): low half of RouterDx's two-term split
     // expert parallelism (ep > 1) over NVLink peer memory: a symmetric CUDA-IPC buffer per
     // rank holds x / dout (pulled by the expert owners) and the return slabs the owners
     // store into; only the [S,K] routing table goes through an NCCL all-gather

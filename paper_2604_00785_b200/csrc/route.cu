@@ -615,8 +615,9 @@ __global__ void sel_count_kernel(const int32_t* __restrict__ idx, int64_t n, int
 __global__ void router_dlogits_kernel(const float* __restrict__ probs, const float* __restrict__ wgrad,
                                       const int32_t* __restrict__ topi, const float* __restrict__ topw,
                                       const float* __restrict__ aux_grad /*[S,N] or null*/,
-                                      float* __restrict__ dlogits, __nv_bfloat16* __restrict__ dl_bf16, int S,
-                                      int N, int K, int normalize, int fur) {
+                                      float* __restrict__ dlogits, __nv_bfloat16* __restrict__ dl_bf16,
+                                      __nv_bfloat16* __restrict__ dl_lo, int S, int N, int K, int normalize,
+                                      int fur) {
     pdl_wait();
     pdl_launch();
     const int row = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
@@ -691,7 +692,13 @@ __global__ void router_dlogits_kernel(const float* __restrict__ probs, const flo
         if (j < N) {
             const float v = (float)((double)pr[i] * ((double)dp[i] - dot));
             dlogits[(int64_t)row * N + j] = v;
-            if (dl_bf16) dl_bf16[(int64_t)row * N + j] = __float2bfloat16_rn(v);
+            if (dl_bf16) {
+                // two-term bf16 split for the tensor-core router GEMMs: hi + lo carries ~16
+                // mantissa bits, so dlogits · Wrᵀ keeps fp32-level accuracy when |Wr| is O(1)
+                const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+                dl_bf16[(int64_t)row * N + j] = hi;
+                if (dl_lo) dl_lo[(int64_t)row * N + j] = __float2bfloat16_rn(v - __bfloat162float(hi));
+            }
         }
     }
 }
@@ -851,12 +858,11 @@ void launch_aux_stats(const float* probs, int S, int N, const int32_t* gidx, int
 }
 
 void launch_router_dlogits(const float* probs, const float* wgrad, const int32_t* topi, const float* topw,
-                           const float* aux_grad, float* dlogits, void* dl_bf16, int S, int N, int K, bool normalize,
-                           bool fur, cudaStream_t st) {
+                           const float* aux_grad, float* dlogits, void* dl_bf16, void* dl_lo, int S, int N, int K,
+                           bool normalize, bool fur, cudaStream_t st) {
     if (S == 0) return;
-    launch_k(router_dlogits_kernel, dim3((unsigned)ceil_div(S, 8)), dim3(256), 0, st, probs, wgrad, topi, topw, aux_grad, dlogits,
-                                                                      (__nv_bfloat16*)dl_bf16, S, N, K,
-                                                                      normalize ? 1 : 0, fur ? 1 : 0);
+    launch_k(router_dlogits_kernel, dim3((unsigned)ceil_div(S, 8)), dim3(256), 0, st, probs, wgrad, topi, topw, aux_grad,
+             dlogits, (__nv_bfloat16*)dl_bf16, (__nv_bfloat16*)dl_lo, S, N, K, normalize ? 1 : 0, fur ? 1 : 0);
     B2_LAUNCH_CHECK();
 }
 

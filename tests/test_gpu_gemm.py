@@ -4,6 +4,11 @@ Reference ops: grouped_mm / grouped_mm_nt / grouped_mm_weight_grad
 (include/optimus/kernels.hpp:111-189) with silu_glu(_backward) (kernels.hpp:262-295)
 fused into the epilogues. bf16 operands, fp32 accumulation: tolerance 1e-2 of the
 tensor scale (max|d| / max|ref|), written here.
+
+Two shapes: a small one (5 experts, H=320, I=192) and the benchmarked one (config B's
+H=2048, I=1024) with a skewed count vector — one expert of more than 16k rows (many
+256-row tiles per expert, a 16,900-deep ragged reduction in the weight-gradient kinds),
+several empty experts and single-row / exactly-aligned groups.
 """
 import ctypes as C
 
@@ -35,16 +40,21 @@ def scale_err(got, ref):
     return ((got - ref).abs().max() / ref.abs().max().clamp_min(1e-30)).item()
 
 
-@pytest.fixture(scope="module")
-def setup():
+SHAPES = {
+    "small": (320, 192, [200, 0, 77, 300, 256]),
+    "olmoe": (2048, 1024, [16900, 0, 1, 0, 255, 257, 3000, 0, 512]),
+}
+
+
+@pytest.fixture(scope="module", params=list(SHAPES))
+def setup(request):
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     b2, fn = _lib()
     ctx = b2.Context(0)
     torch.manual_seed(0)
-    counts = [200, 0, 77, 300, 256]
+    H, I, counts = SHAPES[request.param]
     nr = len(counts)
-    H, I = 320, 192
     starts = [0]
     for c in counts:
         starts.append(starts[-1] + (c + 255) // 256 * 256)

@@ -209,6 +209,29 @@ def test_moe_layer_bitwise_vs_reference(orc, ref, case, dtype):
         assert np.array_equal(a[key], b[key]), key
 
 
+@pytest.mark.parametrize("n,k,h,i,t", [(8, 2, 32, 48, 40), (64, 8, 64, 32, 97), (6, 6, 16, 8, 5)])
+def test_dense_forward_bitwise_vs_reference_and_close_to_fast(orc, ref, n, k, h, i, t):
+    """reference_moe_forward (moe.hpp:471-497): restatement == reference bitwise; fast path
+    == dense within 1e-5 (the reference's own bar, test_moe.cpp:451-490)."""
+    cfg = bind.moe_cfg(n_experts=n, top_k=k, hidden=h, intermediate=i)
+    rw, g, u, d = orc.expert_weights(cfg, 1234, 0.2)
+    x = orc.normal((t, h), 77, 0, 0.7)
+    fast = orc.moe_layer(cfg, t, x, rw, g, u, d)
+    a = orc.dense_moe_forward(cfg, x, g, u, d, fast["weights"], fast["indices"])
+    b = ref.dense_moe_forward(cfg, x, g, u, d, fast["weights"], fast["indices"])
+    assert np.array_equal(a, b)
+    err = np.max(np.abs(a - fast["out"]) / np.maximum(1.0, np.maximum(np.abs(a), np.abs(fast["out"]))))
+    assert err <= 1e-5
+
+
+def test_dense_forward_rejects_bad_ids(orc):
+    cfg = bind.moe_cfg(n_experts=4, top_k=2, hidden=4, intermediate=4)
+    z = np.zeros((1, 4), np.float32)
+    w = np.zeros((4, 4, 4), np.float32)
+    with pytest.raises(RuntimeError, match="out of range"):
+        orc.dense_moe_forward(cfg, z, w, w, w, np.ones((1, 2), np.float32), np.array([[0, 4]]))
+
+
 @pytest.mark.parametrize("dp,ep,mode,bf16", [(1, 1, 1, True), (4, 1, 0, True), (4, 1, 1, True),
                                               (2, 2, 1, False), (2, 2, 2, False), (2, 2, 2, True),
                                               (1, 4, 2, True), (2, 1, 2, True)])
