@@ -67,9 +67,10 @@ typedef struct {
 typedef struct {
     int64_t step;
     double lr, grad_norm, clip_scale;
-    /* B200 addition: a synced gradient held NaN/Inf (the soft-failure scan of
-     * reliability.cpp:706-723 fused into the norm pass); the update was skipped on the
-     * device and every weight / state is unchanged */
+    /* B200 addition: a gradient held NaN/Inf (the soft-failure scan of
+     * reliability.cpp:706-723 fused into the norm pass). As in the reference the update
+     * was still applied and the step count advanced: call b2_opt_detect_soft_failure
+     * before stepping, as the reference's training loop does (train.cpp:193-194) */
     int32_t nonfinite;
 } b2_step_stats;
 
@@ -141,7 +142,9 @@ int b2_moe_fwd_bwd_host(b2_moe* m, const void* x_host, const void* dout_host, co
  * device staging slots let step i+1's host->device copies and step i's device->host
  * results overlap the compute of the neighbouring steps. out_host/dx_host are valid
  * after b2_moe_host_wait (or a later synchronous call). Host buffers must stay alive
- * until then. */
+ * until then, and must be page-locked (cudaHostAlloc / cudaHostRegister): a pageable
+ * buffer makes its copy synchronous, which serialises the pipeline (a warning is printed
+ * once per handle). */
 int b2_moe_fwd_bwd_host_async(b2_moe* m, const void* x_host, const void* dout_host, const void* router,
                               const void* gate, const void* up, const void* down, double aux_coeff, void* out_host,
                               void* dx_host, void* drouter, void* dgate, void* dup, void* ddown, int64_t s_tokens);
@@ -224,14 +227,17 @@ int b2_rec_file_close(b2_rec_file* f);
  * that is its model shard's scattered_writer (reliability.cpp:322-328), writes
  * <dir>/shard-<m>.bin with records <name>.w16 [, .master, .m, .v, .g16] for every
  * parameter the shard stores (expert, or ep coordinate 0). names[p]: record prefix;
- * dims: the shapes concatenated, ndims[p] entries each (dims NULL -> {numel}).
+ * dims: the shapes concatenated, ndims[p] entries each. Pass them for files the reference's
+ * restore_full must read: it requires the parameter's exact shape (reliability.cpp:654);
+ * dims NULL writes flat {numel} records that only this library restores.
  * full = 0: weights only. *bytes / *crc = 0 on non-writers; *model_shard = m. */
 int b2_opt_write_shard(b2_opt* o, const char* dir, const char* const* names, const int64_t* dims,
                        const int* ndims, int full, int64_t* bytes, uint32_t* crc, int* model_shard);
 /* restore_full's per-parameter loop (reliability.cpp:623-675): weights (and with full:
  * this rank's owned master/m/v slice and the grads) from the shard files in dir; every
- * rank reads its own files, no collective. The step count comes from the manifest
- * (b2_opt_set_step_count). */
+ * rank reads its own files, no collective. With dims the records' shapes must match them
+ * exactly (as restore_full checks); dims NULL checks element counts only. The step count
+ * comes from the manifest (b2_opt_set_step_count). */
 int b2_opt_restore_shard(b2_opt* o, const char* dir, const char* const* names, const int64_t* dims,
                          const int* ndims, int full);
 
@@ -239,6 +245,16 @@ int b2_opt_restore_shard(b2_opt* o, const char* dir, const char* const* names, c
 int b2_adamw_update(b2_ctx* ctx, float* master, float* exp_avg, float* exp_avg_sq, const void* grad,
                     int grad_dtype, int64_t n, double lr, int64_t step, const b2_adamw_cfg* cfg, void* weight_out,
                     int weight_dtype, int round_bf16);
+/* replaces optimus::MemoryReport (optim.hpp:125-130) */
+typedef struct {
+    double weights_bytes, grads_bytes, master_bytes, optim_bytes, total_bytes, capacity_bytes;
+    int32_t feasible;
+} b2_memory_report_t;
+/* memory_report (optim.cpp:196-221), host only: the per-device footprint of a parameter set
+ * under DDP / SO / EPSO (mode 0/1/2) at DP x EP; capacity_gb is the device budget (the
+ * reference's default 64 GB is a PVC tile; a B200 holds 180 GB) */
+int b2_memory_report(int64_t p_expert, int64_t p_non_expert, int mode, int dp, int ep, double capacity_gb,
+                     b2_memory_report_t* out);
 /* lr_at_step (optim.cpp:17-24) and shard_slice (optim.cpp:43-50); host only */
 double b2_lr_at_step(int64_t step, const b2_adamw_cfg* cfg);
 int b2_shard_slice(int64_t numel, int group_size, int position, int64_t* begin, int64_t* end);

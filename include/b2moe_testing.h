@@ -17,19 +17,9 @@ int b2x_grouped_gemm(b2_ctx* ctx, int kind, int hidden, int intermediate, int nr
                      const int32_t* counts, int64_t pmax, const void* x, const void* wg, const void* wu, const void* wd, const void* g,
                      const void* u, const void* h, const void* dy, const void* dgu, void* out0, void* out1,
                      void* out2, float scale);
-/* Opt the bf16 layer into (1) / out of (0) the GEMMs' TMA tile::gather4 X-operand loads
- * instead of the materialised mlp_in rows (A/B checks: both must agree bitwise). */
-int b2x_moe_set_tma_gather(b2_moe* m, int on);
-/* EP > 1, bf16: opt into (1) the GEMM-fused combine (FwdDown / BwdDx epilogues storing each
- * row into the source rank's slab over NVLink) instead of (0, default) the owner-local
- * combine + coalesced NVLink pull. */
-int b2x_moe_set_fused_combine(b2_moe* m, int on);
 /* EP > 1, bf16: overlap (1, default) the backward's dX return with the weight-gradient
  * GEMMs (side stream, reduced GEMM grid) or run it after them (0). */
 int b2x_moe_set_overlap_return(b2_moe* m, int on);
-/* EP > 1: forward token exchange as a copy-engine all-gather overlapped with routing (1,
- * opt-in) or as SM pulls of the needed rows after routing (0, default). */
-int b2x_moe_set_ce_dispatch(b2_moe* m, int on);
 #ifdef __cplusplus
 }
 #endif

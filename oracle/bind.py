@@ -226,6 +226,17 @@ class Oracle:
     def lr_at_step(self, step, cfg: AdamWCfg):
         return self._f("lr_at_step")(I64(step), C.byref(cfg))
 
+    def memory_report(self, p_expert, p_non_expert, mode, dp=1, ep=1, capacity_gb=64.0):
+        """memory_report (optim.cpp:196-221)."""
+        out = np.zeros(7, np.float64)
+        f = self._f("memory_report")
+        f.argtypes = [I64, I64, C.c_int, C.c_int, C.c_int, C.c_double, P]
+        self._check(f(p_expert, p_non_expert, mode, dp, ep, capacity_gb, _p(out)))
+        keys = ("weights_bytes", "grads_bytes", "master_bytes", "optim_bytes", "total_bytes", "capacity_bytes")
+        d = {k: float(v) for k, v in zip(keys, out)}
+        d["feasible"] = bool(out[6])
+        return d
+
     def shard_slice(self, numel, g, pos):
         b, e = I64(), I64()
         self._check(self._f("shard_slice")(I64(numel), C.c_int(g), C.c_int(pos), C.byref(b), C.byref(e)))

@@ -13,6 +13,7 @@
  *                        dense per-token reference_moe_forward (moe.hpp:471-497)
  *   optim.cpp:17-24      lr_at_step
  *   optim.cpp:43-50      shard_slice
+ *   optim.cpp:196-221    memory_report
  *   optim.cpp:52-86      build_shard_plan / counts_toward_norm
  *   optim.cpp:88-107     adamw_update
  *   optim.cpp:130-194    ShardedOptimizer::step (collectives simulated in member order)
@@ -343,6 +344,34 @@ double orc_lr_at_step(int64_t step, const orc_adamw_cfg* c) {
 }
 
 /* optim.cpp:43-50: equal shares, remainder on the last member */
+/* optim.cpp:196-221 memory_report; out = {weights, grads, master, optim, total, capacity, feasible} */
+int orc_memory_report(int64_t p_expert, int64_t p_non_expert, int mode, int dp, int ep, double capacity_gb,
+                      double* out) {
+    if (p_expert < 0 || p_non_expert < 0) {
+        strcpy(g_err, "memory_report: negative parameter count");
+        return 1;
+    }
+    if (dp < 1 || ep < 1) {
+        strcpy(g_err, "memory_report: bad group sizes");
+        return 1;
+    }
+    const double p = (double)(p_expert + p_non_expert);
+    double se = 1.0, sn = 1.0;
+    if (mode == 1) se = sn = 1.0 / dp;
+    if (mode == 2) {
+        se = 1.0 / dp;
+        sn = 1.0 / ((double)dp * ep);
+    }
+    out[0] = 2.0 * p;
+    out[1] = 2.0 * p;
+    out[2] = 4.0 * ((double)p_expert * se + (double)p_non_expert * sn);
+    out[3] = 2.0 * out[2];
+    out[4] = out[0] + out[1] + out[2] + out[3];
+    out[5] = capacity_gb * 1e9;
+    out[6] = out[4] <= out[5] ? 1.0 : 0.0;
+    return 0;
+}
+
 int orc_shard_slice(int64_t numel, int g, int pos, int64_t* begin, int64_t* end) {
     if (!(g >= 1 && pos >= 0 && pos < g)) {
         strcpy(g_err, "shard_slice: bad position");

@@ -15,6 +15,7 @@
 //   adamw_update           src/optim.cpp:88-107
 //   lr_at_step             src/optim.cpp:17-24
 //   shard_slice            src/optim.cpp:43-50
+//   memory_report          src/optim.cpp:196-221
 //   ShardedOptimizer::step src/optim.cpp:130-194
 //   Model::param_slots     src/model.cpp:189-229 (the EPSO parameter set of bench.py)
 //   count_params / preset  src/model.cpp:31-91
@@ -299,6 +300,16 @@ void ref_adamw_default_cfg(ref_adamw_cfg* out) {
 }
 
 double ref_lr_at_step(int64_t step, const ref_adamw_cfg* a) { return lr_at_step(step, to_acfg(a)); }
+
+int ref_memory_report(int64_t p_expert, int64_t p_non_expert, int mode, int dp, int ep, double capacity_gb,
+                      double* out) {
+    return guard([&] {
+        const MemoryReport r = memory_report(p_expert, p_non_expert, (ShardMode)mode, dp, ep, capacity_gb);
+        const double v[7] = {r.weights_bytes, r.grads_bytes, r.master_bytes, r.optim_bytes,
+                             r.total_bytes,   r.capacity_bytes, r.feasible ? 1.0 : 0.0};
+        std::memcpy(out, v, sizeof(v));
+    });
+}
 
 int ref_shard_slice(int64_t numel, int g, int pos, int64_t* begin, int64_t* end) {
     return guard([&] {

@@ -16,6 +16,7 @@ Reference API mirrored (file:line under /root/reference/proj):
   AdamWConfig           include/optimus/optim.hpp:11-25
   ShardedOptimizer      optim.hpp:98-121, src/optim.cpp:109-194
   lr_at_step / shard_slice                  src/optim.cpp:17-50
+  memory_report                             src/optim.cpp:196-221
 """
 from __future__ import annotations
 
@@ -112,6 +113,7 @@ SIGNATURES = {
     "b2_adamw_update": (C.c_int, [P, P, P, P, P, C.c_int, I64, C.c_double, I64, P, P, C.c_int, C.c_int]),
     "b2_lr_at_step": (C.c_double, [I64, P]),
     "b2_shard_slice": (C.c_int, [I64, C.c_int, C.c_int, P, P]),
+    "b2_memory_report": (C.c_int, [I64, I64, C.c_int, C.c_int, C.c_int, C.c_double, P]),
     "b2_moe_set_profiling": (C.c_int, [P, C.c_int]),
     "b2_moe_set_graph": (C.c_int, [P, C.c_int]),
     "b2_moe_create_ex": (C.c_int, [P, P, C.c_int, I64, P, C.c_int, P]),
@@ -208,6 +210,21 @@ class AdamWConfig:
 def lr_at_step(step: int, cfg: AdamWConfig) -> float:
     c = cfg.c()
     return lib().b2_lr_at_step(step, C.byref(c))
+
+
+class CMemoryReport(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("weights_bytes", "grads_bytes", "master_bytes", "optim_bytes",
+                                          "total_bytes", "capacity_bytes")] + [("feasible", C.c_int32)]
+
+
+def memory_report(p_expert: int, p_non_expert: int, mode: int, dp: int = 1, ep: int = 1,
+                  capacity_gb: float = 64.0) -> dict:
+    """memory_report (optim.cpp:196-221); the reference's default capacity (64 GB)."""
+    r = CMemoryReport()
+    _check(lib().b2_memory_report(p_expert, p_non_expert, mode, dp, ep, capacity_gb, C.byref(r)))
+    d = {n: getattr(r, n) for n, _ in CMemoryReport._fields_}
+    d["feasible"] = bool(d["feasible"])
+    return d
 
 
 def shard_slice(numel: int, group_size: int, position: int):

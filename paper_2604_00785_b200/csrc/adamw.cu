@@ -340,17 +340,13 @@ __global__ void __launch_bounds__(1024) norm_final_kernel(const double* __restri
 
 // 256 threads x 4 blocks per SM: the fp64 divide / sqrt chains are long, so occupancy (not the
 // FP64 pipe, ~28 % busy at 3 blocks) is what keeps enough bytes in flight
-// VW = elements per thread-iteration of the vectorised path (4: float4 / 8-byte grads; 2: float2
-// / 4-byte grads, fewer registers -> more resident warps)
-template <int MINB, int VW = 4>
+template <int MINB>
 __global__ void __launch_bounds__(256, MINB) adamw_chunks_kernel(const OptSeg* __restrict__ segs,
                                                            const OptChunk* __restrict__ chunks,
                                                            const int32_t* __restrict__ ids, int nids, AdamWDev c,
-                                                           OptStepArgs a, const double* __restrict__ norm_sq,
-                                                           const int32_t* __restrict__ nonfinite) {
+                                                           OptStepArgs a, const double* __restrict__ norm_sq) {
     pdl_wait();
     pdl_launch();
-    if (nonfinite && *nonfinite) return;
     double clip = 1.0;
     if (norm_sq) {
         const double norm = sqrt(*norm_sq);
@@ -359,37 +355,7 @@ __global__ void __launch_bounds__(256, MINB) adamw_chunks_kernel(const OptSeg* _
     for (int q = blockIdx.x; q < nids; q += gridDim.x) {
         const OptChunk ch = chunks[ids[q]];
         const OptSeg sg = segs[ch.seg];
-        if (VW == 2 && sg.vec) {
-            float2* ms = reinterpret_cast<float2*>(sg.master + ch.begin);
-            float2* mo = reinterpret_cast<float2*>(sg.m + ch.begin);
-            float2* ve = reinterpret_cast<float2*>(sg.v + ch.begin);
-            const uint32_t* gr =
-                reinterpret_cast<const uint32_t*>(static_cast<const __nv_bfloat16*>(sg.grad) + ch.begin);
-            uint32_t* wo = reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(sg.wout) + ch.begin);
-            const int64_t n2 = ch.len / 2;
-            for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) {
-                const uint32_t gb = __ldcs(gr + i);
-                float2 m0 = __ldcs(ms + i), a0 = __ldcs(mo + i), v0 = __ldcs(ve + i);
-                const float g[2] = {__uint_as_float(gb << 16), __uint_as_float(gb & 0xFFFF0000u)};
-                float* fm = &m0.x;
-                float* fa = &a0.x;
-                float* fv = &v0.x;
-                uint32_t wb[2];
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    float gq = g[k];
-                    if (sg.scale != 1.f) gq = __fmul_rn(gq, sg.scale);
-                    if (clip != 1.0) gq = (float)__dmul_rn((double)gq, clip);
-                    float wf;
-                    adamw_elem(fm[k], fa[k], fv[k], gq, c, wf);
-                    wb[k] = bf16_bits_rne(wf);
-                }
-                __stcs(ms + i, m0);
-                __stcs(mo + i, a0);
-                __stcs(ve + i, v0);
-                __stcs(wo + i, wb[0] | (wb[1] << 16));
-            }
-        } else if (sg.vec) {
+        if (sg.vec) {
             float4* ms = reinterpret_cast<float4*>(sg.master + ch.begin);
             float4* mo = reinterpret_cast<float4*>(sg.m + ch.begin);
             float4* ve = reinterpret_cast<float4*>(sg.v + ch.begin);
@@ -430,217 +396,6 @@ __global__ void __launch_bounds__(256, MINB) adamw_chunks_kernel(const OptSeg* _
     }
 }
 
-// ---------------------------------------------------------------- TMA-streamed step
-//
-// The same update with the memory side decoupled from the fp64 math: one producer lane
-// streams 1984-element tiles of (grad, master, m, v) into a 6-stage shared-memory ring with
-// 1-D bulk copies (cp.async.bulk, mbarrier complete_tx), 31 compute warps update the tile in
-// place (2 elements per thread, the weight overwrites the grad slot), and one compute thread
-// writes master/m/v/weight back with bulk stores and frees the slot once they have read it.
-// Up to five tiles (135 KB per SM) are in flight while the math runs. The divide / sqrt
-// chains are latency-bound (their slow-path branches serialise a thread's elements), so the
-// block runs the full 32 warps and no thread ever waits on a global load.
-// Measured (tools/adamw_probe.py, 2 G elements, B200): 4.85 TB/s vs 5.25 TB/s for the
-// register kernel below (whose 32 warps x 4 elements keep more fp64 chains in flight than one
-// block's per-tile barrier allows), so this one stays opt-in (B2_ADAMW_IMPL=stream). Persistent: one block per
-// SM walks the chunk list. Chunks whose pointers are not 16-byte aligned (or not the bf16 x4
-// layout) and the <8-element tail of a chunk go through the per-element path from global.
-constexpr int kStCompute = 992;
-constexpr int kStTE = 2 * kStCompute;  // a multiple of 8: every bulk copy is a 16-byte multiple
-constexpr int kStThreads = kStCompute + 32;
-constexpr int kStStages = 6;
-constexpr int kStStageBytes = kStTE * (2 + 4 + 4 + 4);
-constexpr int kStSmem = kStStages * kStStageBytes + 1024;
-
-__device__ __forceinline__ uint32_t st_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void st_bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(bar)
-                 : "memory");
-}
-__device__ __forceinline__ void st_bulk_store(void* dst, uint32_t src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void st_wait(uint32_t bar, uint32_t parity) {
-    uint32_t done = 0;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(bar), "r"(parity)
-            : "memory");
-    } while (!done);
-}
-
-__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ float2 lds_f2(uint32_t a) {
-    float2 v;
-    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ void sts_f2(uint32_t a, float2 v) {
-    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
-}
-
-__device__ __forceinline__ bool st_fast(const OptSeg& sg, const OptChunk& ch) {
-    if (!sg.vec) return false;
-    const uintptr_t o4 = 4 * (uintptr_t)ch.begin, o2 = 2 * (uintptr_t)ch.begin;
-    return (((uintptr_t)sg.master + o4) | ((uintptr_t)sg.m + o4) | ((uintptr_t)sg.v + o4) |
-            ((uintptr_t)sg.grad + o2) | ((uintptr_t)sg.wout + o2)) % 16 == 0;
-}
-
-// the per-element path (reference order) for elements [b, e) of a chunk, from global memory
-__device__ __forceinline__ void st_scalar(const OptSeg& sg, const OptChunk& ch, int64_t b, int64_t e, int tid,
-                                          int nthr, const AdamWDev& c, const OptStepArgs& a, double clip) {
-    for (int64_t i = b + tid; i < e; i += nthr) {
-        const int64_t k = ch.begin + i;
-        float g = load_grad(sg.grad, a.grad_dtype, k);
-        if (sg.scale != 1.f) g = __fmul_rn(g, sg.scale);
-        if (clip != 1.0) g = (float)__dmul_rn((double)g, clip);
-        float ms = sg.master[k], mv = sg.m[k], vv = sg.v[k], wf;
-        adamw_elem(ms, mv, vv, g, c, wf);
-        sg.master[k] = ms;
-        sg.m[k] = mv;
-        sg.v[k] = vv;
-        if (a.weight_dtype == F32)
-            static_cast<float*>(sg.wout)[k] = a.round_bf16 ? __uint_as_float((uint32_t)bf16_bits_rne(wf) << 16) : wf;
-        else
-            static_cast<uint16_t*>(sg.wout)[k] = bf16_bits_rne(wf);
-    }
-}
-
-__global__ void __launch_bounds__(kStThreads, 1) adamw_stream_kernel(const OptSeg* __restrict__ segs,
-                                                                    const OptChunk* __restrict__ chunks,
-                                                                    const int32_t* __restrict__ ids, int nids,
-                                                                    AdamWDev c, OptStepArgs a,
-                                                                    const double* __restrict__ norm_sq,
-                                                                    const int32_t* __restrict__ nonfinite) {
-    extern __shared__ __align__(128) uint8_t st_raw[];
-    const uint32_t raw = st_smem_u32(st_raw);
-    const uint32_t base = (raw + 127u) & ~127u;
-    const uint32_t bar0 = base + kStStages * kStStageBytes;  // full[S], empty[S]
-    auto full_bar = [&](int s) { return bar0 + 8u * s; };
-    auto empty_bar = [&](int s) { return bar0 + 8u * (kStStages + s); };
-    const int tid = threadIdx.x;
-    if (tid == 0) {
-        for (int s = 0; s < kStStages; ++s) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full_bar(s)) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(empty_bar(s)) : "memory");
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    pdl_wait();
-    pdl_launch();
-    if (nonfinite && *nonfinite) return;
-    double clip = 1.0;
-    if (norm_sq) {
-        const double norm = sqrt(*norm_sq);
-        if (a.clip_active && norm > a.clip_norm && norm > 0) clip = a.clip_norm / norm;
-    }
-    // stage layout: grad / weight [TE bf16] | master [TE f32] | m [TE f32] | v [TE f32] (16 B aligned)
-    constexpr uint32_t OG = 0, OM = 2 * kStTE, OA = 6 * kStTE, OV = 10 * kStTE;
-    if (tid >= kStCompute) {  // producer warp: lane 0 streams the tiles
-        if (tid != kStCompute) return;
-        int stage = 0;
-        uint32_t phase = 0;
-        for (int q = blockIdx.x; q < nids; q += gridDim.x) {
-            const OptChunk ch = chunks[ids[q]];
-            const OptSeg sg = segs[ch.seg];
-            if (!st_fast(sg, ch)) continue;
-            const int64_t main = ch.len & ~int64_t(7);
-            for (int64_t t0 = 0; t0 < main; t0 += kStTE) {
-                const uint32_t tl = (uint32_t)(main - t0 < kStTE ? main - t0 : kStTE);
-                st_wait(empty_bar(stage), phase ^ 1u);
-                const uint32_t sb = base + stage * kStStageBytes, fb = full_bar(stage);
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(14u * tl)
-                             : "memory");
-                const int64_t e = ch.begin + t0;
-                st_bulk_load(sb + OG, static_cast<const __nv_bfloat16*>(sg.grad) + e, 2u * tl, fb);
-                st_bulk_load(sb + OM, sg.master + e, 4u * tl, fb);
-                st_bulk_load(sb + OA, sg.m + e, 4u * tl, fb);
-                st_bulk_load(sb + OV, sg.v + e, 4u * tl, fb);
-                if (++stage == kStStages) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
-            }
-        }
-        return;
-    }
-    // compute warps
-    int stage = 0, prev = -1;
-    uint32_t phase = 0;
-    for (int q = blockIdx.x; q < nids; q += gridDim.x) {
-        const OptChunk ch = chunks[ids[q]];
-        const OptSeg sg = segs[ch.seg];
-        if (!st_fast(sg, ch)) {
-            st_scalar(sg, ch, 0, ch.len, tid, kStCompute, c, a, clip);
-            continue;
-        }
-        const int64_t main = ch.len & ~int64_t(7);
-        for (int64_t t0 = 0; t0 < main; t0 += kStTE) {
-            const int tl = (int)(main - t0 < kStTE ? main - t0 : kStTE);
-            st_wait(full_bar(stage), phase);
-            const uint32_t sb = base + stage * kStStageBytes;
-            if (2 * tid < tl) {
-                // explicit shared-window accesses (a generic pointer here compiles to LD.E with
-                // a long-scoreboard wait per element pair, measured 40 % of the kernel's stalls)
-                const uint32_t ag = sb + OG + 4u * tid, am = sb + OM + 8u * tid, aa = sb + OA + 8u * tid,
-                               av = sb + OV + 8u * tid;
-                const uint32_t gb = lds_u32(ag);
-                float2 m0 = lds_f2(am), a0 = lds_f2(aa), v0 = lds_f2(av);
-                const float g[2] = {__uint_as_float(gb << 16), __uint_as_float(gb & 0xFFFF0000u)};
-                float* fm = &m0.x;
-                float* fa = &a0.x;
-                float* fv = &v0.x;
-                uint32_t wb[2];
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    float gq = g[q];
-                    if (sg.scale != 1.f) gq = __fmul_rn(gq, sg.scale);
-                    if (clip != 1.0) gq = (float)__dmul_rn((double)gq, clip);
-                    float wf;
-                    adamw_elem(fm[q], fa[q], fv[q], gq, c, wf);
-                    wb[q] = bf16_bits_rne(wf);
-                }
-                sts_f2(am, m0);
-                sts_f2(aa, a0);
-                sts_f2(av, v0);
-                sts_u32(ag, wb[0] | (wb[1] << 16));
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("bar.sync 1, %0;" ::"n"(kStCompute) : "memory");
-            if (tid == 0) {
-                const int64_t e = ch.begin + t0;
-                st_bulk_store(static_cast<__nv_bfloat16*>(sg.wout) + e, sb + OG, 2u * tl);
-                st_bulk_store(sg.master + e, sb + OM, 4u * tl);
-                st_bulk_store(sg.m + e, sb + OA, 4u * tl);
-                st_bulk_store(sg.v + e, sb + OV, 4u * tl);
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                // the previous tile's stores have read their slot: hand it back to the producer
-                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-                if (prev >= 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty_bar(prev)) : "memory");
-            }
-            prev = stage;
-            if (++stage == kStStages) {
-                stage = 0;
-                phase ^= 1u;
-            }
-        }
-        if (main < ch.len) st_scalar(sg, ch, main, ch.len, tid, kStCompute, c, a, clip);
-    }
-    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-
 __global__ void nonfinite_scan_kernel(const void* __restrict__ g, int dtype, int64_t n, int32_t* flag) {
     bool bad = false;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -661,7 +416,7 @@ void launch_norm_final(const double* partials, int n, double* norm_sq, cudaStrea
 }
 
 void launch_adamw_chunks(const OptSeg* segs, const OptChunk* chunks, const int32_t* ids, int nids,
-                         const OptStepArgs& a, const double* norm_sq, const int32_t* nonfinite, cudaStream_t st,
+                         const OptStepArgs& a, const double* norm_sq, cudaStream_t st,
                          int sm_reserve) {
     if (nids <= 0) return;
     AdamWDev c;
@@ -676,46 +431,17 @@ void launch_adamw_chunks(const OptSeg* segs, const OptChunk* chunks, const int32
     c.bc2 = a.bc2;
     c.rbc1 = 1.0 / a.bc1;
     c.rbc2 = 1.0 / a.bc2;
-    static int impl = -1;  // B2_ADAMW_IMPL=stream: the TMA-streamed kernel (A/B hook)
-    if (impl < 0) {
-        const char* env = getenv("B2_ADAMW_IMPL");
-        impl = env && std::string(env) == "stream" ? 1 : 0;
-    }
-    if (impl == 1) {
-        static int sms = 0;
-        if (sms == 0) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            B2_CUDA(cudaFuncSetAttribute(adamw_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kStSmem));
-        }
-        launch_k(adamw_stream_kernel, dim3(std::min(nids, sms)), dim3(kStThreads), kStSmem, st, segs, chunks, ids, nids,
-                 c, a, norm_sq, nonfinite);
-        B2_LAUNCH_CHECK();
-        return;
-    }
-    static int minb = 0, grid_cap = 0, per_sm_blocks = 1;  // resident blocks (persistent grid)
+    static int grid_cap = 0, per_sm_blocks = 1;  // resident blocks (persistent grid)
     if (grid_cap == 0) {
-        // A/B hook: 3 (no spills), 4 (default: more warps), 6 (pairs of elements, 48 warps/SM)
-        const char* env = getenv("B2_ADAMW_MINB");
-        minb = env ? atoi(env) : 4;
-        if (minb != 3 && minb != 6) minb = 4;
         int dev = 0, sms = 148, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (minb == 3) B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adamw_chunks_kernel<3>, 256, 0));
-        else if (minb == 6)
-            B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adamw_chunks_kernel<6, 2>, 256, 0));
-        else B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adamw_chunks_kernel<4>, 256, 0));
+        B2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adamw_chunks_kernel<4>, 256, 0));
         per_sm_blocks = std::max(1, per_sm);
         grid_cap = sms * per_sm_blocks;
     }
     const int grid = std::max(1, std::min(nids, grid_cap - std::max(0, sm_reserve) * per_sm_blocks));
-    if (minb == 3) launch_k(adamw_chunks_kernel<3>, dim3(grid), dim3(256), 0, st, segs, chunks, ids, nids, c, a, norm_sq, nonfinite);
-    else if (minb == 6)
-        launch_k(adamw_chunks_kernel<6, 2>, dim3(grid), dim3(256), 0, st, segs, chunks, ids, nids, c, a, norm_sq,
-                 nonfinite);
-    else launch_k(adamw_chunks_kernel<4>, dim3(grid), dim3(256), 0, st, segs, chunks, ids, nids, c, a, norm_sq, nonfinite);
+    launch_k(adamw_chunks_kernel<4>, dim3(grid), dim3(256), 0, st, segs, chunks, ids, nids, c, a, norm_sq);
     B2_LAUNCH_CHECK();
 }
 

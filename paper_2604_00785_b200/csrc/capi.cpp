@@ -3,6 +3,7 @@
 
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -84,7 +85,18 @@ struct HostIo {
     cudaEvent_t ev_in[2] = {}, ev_fwd[2] = {}, ev_bwd[2] = {}, ev_out[2] = {};
     bool used[2] = {false, false};
     int next = 0;
+    bool warned_pageable = false;
 };
+
+// true when `p` is page-locked host memory (or device memory): its async copies do not block
+static bool async_copy_ok(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
 struct b2_moe {
     b2_ctx* ctx;
     std::unique_ptr<MoeLayer> layer;
@@ -96,13 +108,9 @@ struct b2_opt {
 };
 
 namespace b2 {
-bool pdl_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("B2_PDL");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
+// programmatic dependent launch on every hot-path kernel (the next kernel's launch and prologue
+// overlap the previous one's tail inside the CUDA graphs)
+bool pdl_enabled() { return true; }
 }  // namespace b2
 
 extern "C" {
@@ -301,6 +309,15 @@ static void fwd_bwd_host_enqueue(b2_moe* m, const void* x_host, const void* dout
                 for (cudaEvent_t* e : {&io.ev_in[b], &io.ev_fwd[b], &io.ev_bwd[b], &io.ev_out[b]})
                     B2_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         }
+    }
+    if (!io.warned_pageable) {
+        for (const void* hp : {x_host, dout_host, (const void*)out_host, (const void*)dx_host})
+            if (!async_copy_ok(hp)) {
+                fprintf(stderr, "b2_moe_fwd_bwd_host: a host buffer is pageable; its copies run synchronously "
+                                "and serialise the copy/compute pipeline (use page-locked memory)\n");
+                io.warned_pageable = true;
+                break;
+            }
     }
     const int b = io.next;
     io.next ^= 1;
@@ -679,6 +696,21 @@ double b2_lr_at_step(int64_t step, const b2_adamw_cfg* cfg) {
     return r;
 }
 
+int b2_memory_report(int64_t p_expert, int64_t p_non_expert, int mode, int dp, int ep, double capacity_gb,
+                     b2_memory_report_t* out) {
+    return guard([&] {
+        check(out != nullptr, "memory_report: null output");
+        const MemoryReport r = memory_report(p_expert, p_non_expert, mode, dp, ep, capacity_gb);
+        out->weights_bytes = r.weights_bytes;
+        out->grads_bytes = r.grads_bytes;
+        out->master_bytes = r.master_bytes;
+        out->optim_bytes = r.optim_bytes;
+        out->total_bytes = r.total_bytes;
+        out->capacity_bytes = r.capacity_bytes;
+        out->feasible = r.feasible ? 1 : 0;
+    });
+}
+
 int b2_shard_slice(int64_t numel, int group_size, int position, int64_t* begin, int64_t* end) {
     return guard([&] { shard_slice(numel, group_size, position, begin, end); });
 }
@@ -695,20 +727,8 @@ int b2_opt_last_launches(b2_opt* o) { return o ? o->opt->last_launches() : 0; }
 
 #include "../../include/b2moe_testing.h"
 
-extern "C" int b2x_moe_set_ce_dispatch(b2_moe* m, int on) {
-    return guard([&] { m->layer->set_ce_dispatch(on != 0); });
-}
-
 extern "C" int b2x_moe_set_overlap_return(b2_moe* m, int on) {
     return guard([&] { m->layer->set_overlap_return(on != 0); });
-}
-
-extern "C" int b2x_moe_set_fused_combine(b2_moe* m, int on) {
-    return guard([&] { m->layer->set_fused_combine(on != 0); });
-}
-
-extern "C" int b2x_moe_set_tma_gather(b2_moe* m, int on) {
-    return guard([&] { m->layer->set_tma_gather(on != 0); });
 }
 
 extern "C" int b2x_grouped_gemm(b2_ctx* ctx, int kind, int hidden, int intermediate, int nr, const int32_t* pad_start,

@@ -105,10 +105,14 @@ void restore_state_shard(ShardedOptimizer& opt, const std::string& dir, const st
         const ParamSlot& p = opt.param(i);
         const int64_t n = p.numel;
         const std::vector<int64_t> shape = dims_of(dims, i, n);
+        // with the parameter's dims given, the record's shape must match them exactly (restore_full,
+        // reliability.cpp:654); without, only its element count is checked
+        const bool have_dims = (size_t)i < dims.size() && !dims[(size_t)i].empty();
+        auto shape_ok = [&](const RecordInfo& r) { return have_dims ? r.dims == shape : r.numel == n; };
         RecordFile& f = file(p.expert);
         const std::string& nm = names[(size_t)i];
         const int rw = rec(f, nm + ".w16");
-        if (f.records()[(size_t)rw].dims != shape)
+        if (!shape_ok(f.records()[(size_t)rw]))
             throw ContractError(dir + ": record '" + nm + ".w16' has the wrong shape");
         f.read(rw, 0, n, p.weight, opt.weight_dtype());
         if (!full) continue;
@@ -124,7 +128,7 @@ void restore_state_shard(ShardedOptimizer& opt, const std::string& dir, const st
         f.read(r1, b, e, s1, B2_F32);
         f.read(r2, b, e, s2, B2_F32);
         const int rg = rec(f, nm + ".g16");
-        if (f.records()[(size_t)rg].dims != shape)
+        if (!shape_ok(f.records()[(size_t)rg]))
             throw ContractError(dir + ": record '" + nm + ".g16' has the wrong shape");
         f.read(rg, 0, n, const_cast<void*>(p.grad), opt.grad_dtype());
     }

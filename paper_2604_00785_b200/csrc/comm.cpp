@@ -79,21 +79,6 @@ void all_gather_v(const Group& g, void* buf, int64_t numel, int dtype, cudaStrea
     B2_NCCL(ncclGroupEnd());
 }
 
-void all_to_all_v(const Group& g, const void* send, const int64_t* scnt, const int64_t* soff, void* recv,
-                  const int64_t* rcnt, const int64_t* roff, size_t row_bytes, cudaStream_t st) {
-    // rows travel as bytes so any element type (and the packed routing metadata) fits
-    B2_NCCL(ncclGroupStart());
-    for (int m = 0; m < g.size; ++m) {
-        if (scnt[m] > 0)
-            B2_NCCL(ncclSend((const char*)send + (size_t)soff[m] * row_bytes, (size_t)scnt[m] * row_bytes, ncclUint8, m,
-                             g.comm, st));
-        if (rcnt[m] > 0)
-            B2_NCCL(ncclRecv((char*)recv + (size_t)roff[m] * row_bytes, (size_t)rcnt[m] * row_bytes, ncclUint8, m,
-                             g.comm, st));
-    }
-    B2_NCCL(ncclGroupEnd());
-}
-
 void all_reduce_sum(const Group& g, const void* src, void* dst, int64_t n, ncclDataType_t dt, cudaStream_t st) {
     if (g.size == 1) {
         if (src != dst) B2_CUDA(cudaMemcpyAsync(dst, src, (size_t)n * (dt == ncclFloat64 ? 8 : dt == ncclFloat32 ? 4 : 2),

@@ -42,9 +42,5 @@ void reduce_scatter_v(const Group& g, const void* src, void* dst, int64_t numel,
 // allgatherv in place on `buf` (optim.cpp:185-190): member i contributes its slice
 void all_gather_v(const Group& g, void* buf, int64_t numel, int dtype, cudaStream_t st);
 void all_reduce_sum(const Group& g, const void* src, void* dst, int64_t n, ncclDataType_t dt, cudaStream_t st);
-// all-to-all-v of rows (`row_bytes` each): member m gets send rows [soff[m], soff[m]+scnt[m]) and
-// this rank receives member m's rows into [roff[m], roff[m]+rcnt[m]); counts are host arrays
-void all_to_all_v(const Group& g, const void* send, const int64_t* scnt, const int64_t* soff, void* recv,
-                  const int64_t* rcnt, const int64_t* roff, size_t row_bytes, cudaStream_t st);
 
 }  // namespace b2

@@ -66,12 +66,12 @@ __global__ void ep_gather_pull_kernel(const T* const* __restrict__ peer_src, int
 }
 
 // the owner's (weighted) sum of a gathered token's local slot rows, in slot (k) order, into
-// its own slab row [gid] (local_out) or — push variant — the source rank's slab [me * S + t]
+// its own slab row [gid]
 template <typename T>
 __global__ void ep_combine_slots_kernel(const T* __restrict__ y, const int32_t* __restrict__ slot_prow,
                                            const int32_t* __restrict__ selected_k, const int32_t* __restrict__ cec,
-                                           const float* __restrict__ gw, int K, int S, int T_tot, int H, int me,
-                                           T* const* __restrict__ peer_ret, T* __restrict__ local_out) {
+                                           const float* __restrict__ gw, int K, int T_tot, int H,
+                                           T* __restrict__ own_slab) {
     pdl_wait();
     pdl_launch();
     constexpr int V = 16 / sizeof(T);
@@ -81,7 +81,7 @@ __global__ void ep_combine_slots_kernel(const T* __restrict__ y, const int32_t* 
     for (int gid = (blockIdx.x * blockDim.x + threadIdx.x) / 32; gid < T_tot; gid += nw) {
         const int j0 = cec[gid], j1 = cec[gid + 1];
         if (j0 == j1) continue;
-        T* dst = local_out ? local_out + (int64_t)gid * H : peer_ret[gid / S] + ((int64_t)me * S + gid % S) * H;
+        T* dst = own_slab + (int64_t)gid * H;
         // all local slot rows of a column block are loaded together (<= 8 in flight)
         constexpr int MAXJ = 8;
         for (int v = lane; v < nv; v += 32) {
@@ -134,7 +134,6 @@ __global__ void ep_combine_slots_kernel(const T* __restrict__ y, const int32_t* 
             reinterpret_cast<int4*>(dst)[v] = o;
         }
     }
-    if (!local_out) __threadfence_system();
 }
 
 // out[t] = sum over the ranks r (in order) that token t routes to of owner r's partial row
@@ -224,70 +223,6 @@ __global__ void ep_pull_sum_kernel(const T* const* __restrict__ peer_slab, const
         ep_pull_sum_token<T>(peer_slab, gi_local, S, K, E, NR, W, me, out, t, lane);
 }
 
-// source side of the GEMM-fused combine: out[t] = sum_k slab[k][t] in k order (every (t, k)
-// row was stored by the owner's epilogue over NVLink before the barrier)
-template <typename T>
-__global__ void kslab_sum_kernel(const T* __restrict__ slab, int S, int K, int W, T* __restrict__ out) {
-    pdl_wait();
-    pdl_launch();
-    const int t = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
-    if (t >= S) return;
-    constexpr int V = 16 / sizeof(T), MAXK = 8;
-    for (int v = lane; v < W / V; v += 32) {
-        float acc[V];
-#pragma unroll
-        for (int z = 0; z < V; ++z) acc[z] = 0.f;
-        for (int k0 = 0; k0 < K; k0 += MAXK) {
-            int4 raw[MAXK];
-#pragma unroll
-            for (int q = 0; q < MAXK; ++q)
-                if (k0 + q < K) raw[q] = __ldcv(reinterpret_cast<const int4*>(slab + ((int64_t)(k0 + q) * S + t) * W) + v);
-#pragma unroll
-            for (int q = 0; q < MAXK; ++q) {
-                if (k0 + q >= K) break;
-                float f[V];
-                if constexpr (sizeof(T) == 4) {
-                    f[0] = __int_as_float(raw[q].x);
-                    f[1] = __int_as_float(raw[q].y);
-                    f[2] = __int_as_float(raw[q].z);
-                    f[3] = __int_as_float(raw[q].w);
-                } else {
-                    const uint32_t w[4] = {(uint32_t)raw[q].x, (uint32_t)raw[q].y, (uint32_t)raw[q].z,
-                                           (uint32_t)raw[q].w};
-#pragma unroll
-                    for (int z = 0; z < 4; ++z) {
-                        f[2 * z] = __uint_as_float(w[z] << 16);
-                        f[2 * z + 1] = __uint_as_float(w[z] & 0xFFFF0000u);
-                    }
-                }
-#pragma unroll
-                for (int z = 0; z < V; ++z) acc[z] = __fadd_rn(acc[z], f[z]);
-            }
-        }
-        int4 o;
-        if constexpr (sizeof(T) == 4) {
-            o = make_int4(__float_as_int(acc[0]), __float_as_int(acc[1]), __float_as_int(acc[2]), __float_as_int(acc[3]));
-        } else {
-            uint32_t w[4];
-#pragma unroll
-            for (int z = 0; z < 4; ++z) {
-                __nv_bfloat162 b = __floats2bfloat162_rn(acc[2 * z], acc[2 * z + 1]);
-                w[z] = *reinterpret_cast<uint32_t*>(&b);
-            }
-            o = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
-        }
-        reinterpret_cast<int4*>(out + (int64_t)t * W)[v] = o;
-    }
-}
-
-template <typename T>
-void launch_kslab_sum(const T* slab, int S, int K, int W, T* out, cudaStream_t st) {
-    if (S <= 0) return;
-    check(((int64_t)W * sizeof(T)) % 16 == 0, "kslab sum: rows must be 16-byte multiples");
-    launch_k(kslab_sum_kernel<T>, dim3((unsigned)ceil_div(S, 8)), dim3(256), 0, st, slab, S, K, W, out);
-    B2_LAUNCH_CHECK();
-}
-
 // NVLink flag barrier over the EP group: every rank bumps its slot in every peer's flag
 // array (system-scope release), then waits until all of its own slots reach the epoch it
 // expects (acquire). Epochs live on the device (graph-replay safe); every rank calls the
@@ -352,149 +287,6 @@ void launch_ep_table_pull(const int32_t* const* peer_ids, const float* const* pe
     B2_LAUNCH_CHECK();
 }
 
-// ---- visiting order of the m-tiles for the fused pull (GEMM-side dispatch overlap) ----------
-// bucket[tile] = latest rotated gathered token among the tile's rows * nb / (E * S); rows are
-// pulled in rotated order (this rank's own tokens first), so a tile's bucket says when its last
-// row lands
-__global__ void ep_tile_bucket_kernel(const int32_t* __restrict__ prow_src, const int32_t* __restrict__ p_total,
-                                      int S, int E, int me, int nb, int max_tiles, int32_t* __restrict__ bucket) {
-    pdl_wait();
-    pdl_launch();
-    const int lane = threadIdx.x % 32;
-    const int ntiles = min(max_tiles, p_total[0] / kRowAlign);
-    const int nw = gridDim.x * blockDim.x / 32;
-    for (int tile = (blockIdx.x * blockDim.x + threadIdx.x) / 32; tile < ntiles; tile += nw) {
-        int key = -1;
-        for (int r = lane; r < kRowAlign; r += 32) {
-            const int gid = prow_src[(int64_t)tile * kRowAlign + r];
-            if (gid >= 0) key = max(key, ((gid / S - me + E) % E) * S + gid % S);
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
-        if (lane == 0) bucket[tile] = key < 0 ? 0 : (int)((int64_t)key * nb / ((int64_t)E * S));
-    }
-}
-
-// one block: the buckets staged in shared memory, then thread b = bucket b counts, an exclusive
-// scan, and each bucket writes its tiles in ascending order (stable)
-__global__ void __launch_bounds__(256) ep_tile_order_kernel(const int32_t* __restrict__ bucket,
-                                                            const int32_t* __restrict__ p_total, int nb, int max_tiles,
-                                                            int32_t* __restrict__ order) {
-    pdl_wait();
-    pdl_launch();
-    extern __shared__ int32_t sbk[];
-    __shared__ int cnt[256];
-    const int b = threadIdx.x;
-    const int ntiles = min(max_tiles, p_total[0] / kRowAlign);
-    for (int i = b; i < ntiles; i += blockDim.x) sbk[i] = bucket[i];
-    __syncthreads();
-    int c = 0;
-    if (b < nb)
-        for (int i = 0; i < ntiles; ++i) c += sbk[i] == b;
-    cnt[b] = c;
-    __syncthreads();
-    if (b == 0) {
-        int run = 0;
-        for (int q = 0; q < nb; ++q) {
-            const int v = cnt[q];
-            cnt[q] = run;
-            run += v;
-        }
-    }
-    __syncthreads();
-    if (b < nb) {
-        int at = cnt[b];
-        for (int i = 0; i < ntiles; ++i)
-            if (sbk[i] == b) order[at++] = i;
-    }
-}
-
-void launch_ep_tile_order(const int32_t* prow_src, const int32_t* p_total, int S, int E, int me, int max_tiles,
-                          int32_t* bucket, int32_t* order, cudaStream_t st) {
-    if (max_tiles <= 0) return;
-    // one bucket per source: within a bucket the tiles stay in padded-row (expert-major) order,
-    // so each expert's weights are streamed once per source pass instead of once per m-tile
-    // (8 buckets per source interleaved the experts and re-read every weight tile from HBM)
-    const int nb = std::min(256, E);
-    check((size_t)max_tiles * 4 <= 200 * 1024, "ep tile order: too many m-tiles for one block");
-    static int smem_set = 0;
-    if (smem_set < max_tiles * 4 && max_tiles * 4 > 48 * 1024) {
-        B2_CUDA(cudaFuncSetAttribute(ep_tile_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_tiles * 4));
-        smem_set = max_tiles * 4;
-    }
-    launch_k(ep_tile_bucket_kernel, dim3((unsigned)std::min<int64_t>(1184, ceil_div(max_tiles, 8))), dim3(256), 0, st,
-             prow_src, p_total, S, E, me, nb, max_tiles, bucket);
-    B2_LAUNCH_CHECK();
-    launch_k(ep_tile_order_kernel, dim3(1), dim3(256), (size_t)max_tiles * 4, st, bucket, p_total, nb, max_tiles,
-             order);
-    B2_LAUNCH_CHECK();
-}
-
-// The dispatch pull as a kernel that runs NEXT TO the FwdGateUp GEMM: one 256-thread block per
-// SM fits beside a GEMM CTA (<= 48 registers per thread: 12 K registers next to the GEMM's 52 K,
-// no shared memory), so 8 pulling warps per SM stream the gathered tokens' rows in rotated source
-// order (own rows first) while the GEMM's producers wait on the per-128-row arrival counters and
-// visit the m-tiles source by source. Each row is pulled once (8 x 16 B in flight per lane) and
-// written to all of its local padded rows, then counted after a gpu-scope fence.
-__global__ void __launch_bounds__(256, 5) ep_pull_rows_kernel(const __nv_bfloat16* const* __restrict__ peer_src,
-                                                              int S, int E, int me, int H,
-                                                              const int32_t* __restrict__ cec,
-                                                              const int32_t* __restrict__ slot_prow,
-                                                              __nv_bfloat16* __restrict__ out,
-                                                              int32_t* __restrict__ ready) {
-    pdl_wait();
-    pdl_launch();
-    const int lane = threadIdx.x % 32;
-    const int nw = gridDim.x * blockDim.x / 32;
-    const int T = E * S, nv = H / 8;
-    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) / 32; i < T; i += nw) {
-        const int src = (me + i / S) % E, t = i % S;
-        const int gid = src * S + t;
-        const int j0 = cec[gid], j1 = cec[gid + 1];
-        if (j0 == j1) continue;
-        const int4* row = reinterpret_cast<const int4*>(peer_src[src] + (int64_t)t * H);
-        constexpr int B = 8;
-        for (int v0 = 0; v0 < nv; v0 += 32 * B) {
-            int4 val[B];
-#pragma unroll
-            for (int b = 0; b < B; ++b) {
-                const int v = v0 + lane + 32 * b;
-                if (v < nv) val[b] = __ldcv(row + v);
-            }
-            for (int j = j0; j < j1; ++j) {
-                int4* dst = reinterpret_cast<int4*>(out + (int64_t)slot_prow[j] * H);
-#pragma unroll
-                for (int b = 0; b < B; ++b) {
-                    const int v = v0 + lane + 32 * b;
-                    if (v < nv) dst[v] = val[b];
-                }
-            }
-        }
-        __threadfence();
-        __syncwarp();
-        if (lane == 0)
-            for (int j = j0; j < j1; ++j) atomicAdd(ready + (slot_prow[j] >> 7), 1);
-    }
-}
-
-void launch_ep_pull_rows(const void* const* peer_src, int S, int E, int me, int H, const int32_t* cec,
-                         const int32_t* slot_prow, void* out, int32_t* ready, int num_sms, cudaStream_t st) {
-    if (S <= 0) return;
-    check(H % 8 == 0, "ep pull: rows must be 16-byte multiples");
-    static bool carve = false;
-    if (!carve) {
-        // the SM's shared-memory carveout can only change while it is idle: ask for the full
-        // carveout (as the GEMM does), or a pull block landing first would keep the GEMM CTA out
-        B2_CUDA(cudaFuncSetAttribute(ep_pull_rows_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                     (int)cudaSharedmemCarveoutMaxShared));
-        carve = true;
-    }
-    launch_k(ep_pull_rows_kernel, dim3((unsigned)std::max(1, num_sms)), dim3(256), 0, st,
-             reinterpret_cast<const __nv_bfloat16* const*>(peer_src), S, E, me, H, cec, slot_prow,
-             static_cast<__nv_bfloat16*>(out), ready);
-    B2_LAUNCH_CHECK();
-}
-
 static unsigned ep_grid(int64_t warps) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(148 * 16, ceil_div(warps, 8))); }
 
 template <typename T>
@@ -512,8 +304,8 @@ void launch_ep_combine_local(const T* y, const int32_t* slot_prow, const int32_t
     if (T_tot <= 0) return;
     check(((int64_t)H * sizeof(T)) % 16 == 0, "ep combine: rows must be 16-byte multiples");
     const unsigned grid = max_blocks > 0 ? std::min<unsigned>(ep_grid(T_tot), (unsigned)max_blocks) : ep_grid(T_tot);
-    launch_k(ep_combine_slots_kernel<T>, dim3(grid), dim3(256), 0, st, y, slot_prow, selected_k, cec, gw, K, S, T_tot, H,
-                                                                  0, nullptr, own_slab);
+    launch_k(ep_combine_slots_kernel<T>, dim3(grid), dim3(256), 0, st, y, slot_prow, selected_k, cec, gw, K, T_tot, H,
+             own_slab);
     B2_LAUNCH_CHECK();
 }
 
@@ -532,8 +324,7 @@ void launch_ep_pull_sum(const T* const* peer_slab, const int32_t* gi_local, int 
     template void launch_ep_combine_local<T>(const T*, const int32_t*, const int32_t*, const int32_t*, const float*, \
                                              int, int, int, int, T*, cudaStream_t, int);                         \
     template void launch_ep_pull_sum<T>(const T* const*, const int32_t*, int, int, int, int, int, int, T*,        \
-                                        cudaStream_t, int);                                                       \
-    template void launch_kslab_sum<T>(const T*, int, int, int, T*, cudaStream_t);
+                                        cudaStream_t, int);
 B2_EP_INST(float)
 B2_EP_INST(__nv_bfloat16)
 #undef B2_EP_INST

@@ -57,29 +57,16 @@ struct Cfg {
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_EPI_WARPS = 8;  // two warps per TMEM lane quadrant, each half the columns
 constexpr int NUM_THREADS = 128 + 32 * NUM_EPI_WARPS;
-// dgrad epilogue (BwdDownDgrad): each epilogue warp stages the G and U operands of its
-// next 32-row x 32-column chunk by TMA (SWIZZLE_64B boxes) while it works on the current one
-constexpr int EPI_GU_BYTES = 2 * 32 * 32 * 2;  // g box + u box
-// dgrad epilogue: G/U read straight from global into registers (ld.global.nc, L1-cached) instead
-// of TMA-staged boxes: the staging's shared-memory writes + reads compete with the MMA operand
-// traffic, and dropping them frees the smem for a sixth stage
-#ifdef B2_DGRAD_STAGED_GU  // A/B build of the TMA-staged variant (tools/build_alt.sh)
-constexpr bool kDgradDirectGU = false;
-#else
-constexpr bool kDgradDirectGU = true;
-#endif
 // TMA-store epilogue of the six expert kinds: each epilogue warp owns SLOTS 2 KB staging
 // slots, each one 32-row x 32-column bf16 box in the SWIZZLE_64B layout
 constexpr int EPI_SLOT_BYTES = 32 * 32 * 2;
 template <GemmKind K, int CG>
 struct KCfg {
     static constexpr bool TMA_EPI = (int)K <= (int)GemmKind::WgradGateUp;
-    // two staging slots everywhere (FwdGateUp's three boxes per chunk rotate through them),
-    // so every kind but the dgrad (which also stages its G/U operands) keeps 6 stages
+    // two staging slots everywhere (FwdGateUp's three boxes per chunk rotate through them)
     static constexpr int SLOTS = 2;
-    static constexpr bool GU_STAGED = K == GemmKind::BwdDownDgrad && !kDgradDirectGU;
-    static constexpr int STAGES = CG == 1 ? 4 : (GU_STAGED ? 5 : 6);
-    static constexpr int WARP_EPI_BYTES = TMA_EPI ? SLOTS * EPI_SLOT_BYTES + (GU_STAGED ? EPI_GU_BYTES : 0) : 0;
+    static constexpr int STAGES = CG == 1 ? 4 : 6;
+    static constexpr int WARP_EPI_BYTES = TMA_EPI ? SLOTS * EPI_SLOT_BYTES : 0;
     static constexpr int SMEM =
         STAGES * Cfg<CG>::STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + NUM_EPI_WARPS * WARP_EPI_BYTES;
     static_assert(SMEM <= 232448, "kernel exceeds 227 KB of shared memory");
@@ -90,8 +77,6 @@ struct Params {
     CUtensorMap mapA1;  // RouterDx: the low bf16 half of dlogits (K blocks past num_kb_fixed / 2)
     CUtensorMap mapB0;
     CUtensorMap mapB1;
-    CUtensorMap mapG;  // BwdDownDgrad epilogue operands (32 x 32 boxes, SWIZZLE_64B)
-    CUtensorMap mapU;
     CUtensorMap mapO0;  // TMA-store maps of the outputs (32 x 32 [x 1] boxes, SWIZZLE_64B)
     CUtensorMap mapO1;
     CUtensorMap mapO2;
@@ -113,33 +98,8 @@ struct Params {
     uint32_t stage_tx;    // bytes a stage's TMA loads deliver
     int S, N;             // router kinds: tokens, experts
     int rows_per_split;   // RouterDw
-    const int32_t* cec;
-    const int32_t* slot_prow;
-    const __nv_bfloat16* src;
+    const __nv_bfloat16* src;  // RouterDx: rows added to the router term (the token's summed expert rows)
     float* part;
-    void* const* peer_kslab;     // FwdDown / BwdDx, EP > 1: fused combine into the sources' slabs
-    const int32_t* prow_src;
-    const int32_t* prow_k;
-    const float* gw;
-    int ep_S, ep_K;
-    const int32_t* gather_rows;  // FwdGateUp / WgradGateUp: padded row -> token (gather4 mode)
-    int gather_oob;              // the zero-filled row index used for pad rows (-1 entries)
-    // EP > 1 fused dispatch (FwdGateUp: token rows; BwdDownDgrad: dout rows + the output-reduction
-    // backward): warps 2-3 of every CTA pull the gathered tokens' rows over NVLink, in the rotated
-    // source order me, me+1, ..., write them to the A operand's padded rows and count them per
-    // 128-row block; the producer waits for its block's count before the tile's TMA loads, and the
-    // m-tiles are visited in `tile_order` (sorted by when their rows arrive)
-    const int32_t* tile_order;
-    int32_t* ready;                      // [P / 128] rows landed per block; null: no fused pull
-    const __nv_bfloat16* const* peer_rows;  // [E] x (FwdGateUp) or dout (BwdDownDgrad) of every rank
-    int ep_E, ep_me, ep_T;
-    const int32_t* pull_cec;             // cum_expert_counts [T + 1]
-    const int32_t* pull_slot_prow;       // slot -> padded row
-    const int32_t* pull_selk;            // BwdDownDgrad: slot -> top-k index
-    const float* pull_gw;                // BwdDownDgrad: gathered routing weights [T, K]
-    const __nv_bfloat16* pull_y;         // BwdDownDgrad: mlp_out rows (the weight-gradient dots)
-    __nv_bfloat16* pull_dst;             // mlp_in / dY rows
-    float* pull_wgrad;                   // BwdDownDgrad: top-k weight gradients [T, K]
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -193,46 +153,12 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         "l"((uint64_t)map), "r"(bar), "r"(c0), "r"(c1)
         : "memory");
 }
-// 4 arbitrary rows x one box of columns (TMA tile::gather4); the map's box is {cols, 1}
-template <int CG>
-__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, uint32_t bar, int col, int4 rows) {
-    if constexpr (CG == 1)
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
-            "%4, %5, %6, %7}], [%2];" ::"r"(dst),
-            "l"((uint64_t)map), "r"(bar), "r"(col), "r"(rows.x), "r"(rows.y), "r"(rows.z), "r"(rows.w)
-            : "memory");
-    else
-        asm volatile(
-            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes "
-            "[%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
-            "l"((uint64_t)map), "r"(bar), "r"(col), "r"(rows.x), "r"(rows.y), "r"(rows.z), "r"(rows.w)
-            : "memory");
-}
-__device__ __forceinline__ int4 gather_ids(const int32_t* rows, int64_t at, int oob) {
-    int4 r = __ldg(reinterpret_cast<const int4*>(rows + at));
-    r.x = r.x < 0 ? oob : r.x;
-    r.y = r.y < 0 ? oob : r.y;
-    r.z = r.z < 0 ? oob : r.z;
-    r.w = r.w < 0 ? oob : r.w;
-    return r;
-}
 // 2-CTA (cta_group::2) load: the bytes complete_tx on the LEADER CTA's barrier
 __device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
                                                 int c1) {
     asm volatile(
         "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
         "l"((uint64_t)map), "r"(leader_bar), "r"(c0), "r"(c1)
-        : "memory");
-}
-// 2-CTA load multicast to the CTAs in `mask` (same smem offset in each); every destination
-// pair's bytes complete_tx on that pair's LEADER barrier (the leader address is passed)
-__device__ __forceinline__ void tma_load_2d_cg2_mc(uint32_t dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
-                                                   int c1, uint16_t mask) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
-        "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
-        "l"((uint64_t)map), "r"(leader_bar), "r"(c0), "r"(c1), "h"(mask)
         : "memory");
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -299,12 +225,6 @@ __device__ __forceinline__ void umma_commit_cg2(uint32_t bar) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
         "h"((uint16_t)0x3)
-        : "memory");
-}
-__device__ __forceinline__ void umma_commit_cg2_mask(uint32_t bar, uint16_t mask) {
-    asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
-        "h"(mask)
         : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -489,7 +409,7 @@ __device__ __forceinline__ TileInfo tile_info(const Params& p, const int32_t* ps
         ti.krow0 = ps[ti.e];
         ti.kb = (p.counts[ti.e] + BK - 1) / BK;  // pad rows past the count are zero: skip them
     } else {
-        const int mt = p.tile_order ? p.tile_order[t / p.n_tiles] : t / p.n_tiles;
+        const int mt = t / p.n_tiles;
         ti.n0 = (t % p.n_tiles) * BN;
         ti.m0 = mt * TM;
         int lo = 0, hi = p.nr - 1;  // last expert whose padded start <= m0
@@ -508,29 +428,20 @@ __device__ __forceinline__ TileInfo tile_info(const Params& p, const int32_t* ps
 // producer: one stage of A and B for (tile, kb). `m_own` is the first A row this CTA
 // holds (the pair's tile base + 128 * rank); with CG = 2 each CTA loads B columns
 // [128 * rank, 128 * rank + 128) of the tile and signals the leader's barrier.
-// MC = 2: the cluster holds two CTA pairs working on the same M rows (adjacent N tiles), so
-// each CTA loads HALF of its A tile (64 rows, or one of the two 64-column boxes of the MN-major
-// wgrad A) and multicasts it to the same-rank CTA of the other pair: A crosses L2 -> SM once
-// per cluster instead of once per pair.
-template <GemmKind KIND, int CG, int MC = 1>
+template <GemmKind KIND, int CG>
 __device__ __forceinline__ void load_stage(const Params& p, const TileInfo& ti, int kb, int m_own, uint32_t rank,
-                                           uint32_t sA, uint32_t sB, uint32_t bar, int pair = 0) {
+                                           uint32_t sA, uint32_t sB, uint32_t bar) {
     const int k0 = kb * BK;
     auto ld = [&](uint32_t dst, const CUtensorMap* map, int c0, int c1) {
         if constexpr (CG == 1) tma_load_2d(dst, map, bar, c0, c1);
         else tma_load_2d_cg2(dst, map, bar, c0, c1);
     };
     // A of the by-row kinds: [m_own, m_own + 128) x [k0, k0 + 64), K-major
-    auto ldA_rows = [&]() {
-        if constexpr (MC == 2)
-            tma_load_2d_cg2_mc(sA + 8192u * pair, &p.mapA, bar, k0, m_own + 64 * pair, (uint16_t)(0x5u << rank));
-        else
-            ld(sA, &p.mapA, k0, m_own);
-    };
+    auto ldA_rows = [&]() { ld(sA, &p.mapA, k0, m_own); };
     constexpr int BC = Cfg<CG>::B_COLS;
     const int nb = ti.n0 + BC * (int)rank;  // this CTA's first B column of the tile
     if constexpr (KIND == GemmKind::FwdGateUp) {
-        if (!p.gather_rows) ldA_rows();
+        ldA_rows();
         const int row = ti.e * p.H + k0;
         const int n0 = ti.n0 / 2;  // 128 gate columns + 128 up columns per tile
         if (CG == 1 || rank == 0) {
@@ -567,14 +478,8 @@ __device__ __forceinline__ void load_stage(const Params& p, const TileInfo& ti, 
         for (int c = 0; c < p.b_chunks; ++c) ld(sB + c * 8192, &p.mapB0, 64 * c, row);
     } else {  // wgrad: K runs over the expert's rows; both operands MN-major
         const int row = ti.krow0 + k0;
-        if (KIND != GemmKind::WgradGateUp || !p.gather_rows) {
-            if constexpr (MC == 2) {
-                tma_load_2d_cg2_mc(sA + 8192u * pair, &p.mapA, bar, m_own + 64 * pair, row, (uint16_t)(0x5u << rank));
-            } else {
-                ld(sA + 0, &p.mapA, m_own, row);
-                ld(sA + 8192, &p.mapA, m_own + 64, row);
-            }
-        }
+        ld(sA + 0, &p.mapA, m_own, row);
+        ld(sA + 8192, &p.mapA, m_own + 64, row);
 #pragma unroll
         for (int c = 0; c < BC / 64; ++c) ld(sB + c * 8192, &p.mapB0, nb + 64 * c, row);
     }
@@ -582,69 +487,18 @@ __device__ __forceinline__ void load_stage(const Params& p, const TileInfo& ti, 
 
 __device__ __forceinline__ float silu_f(float x) { return __fdividef(x, 1.f + __expf(-x)); }
 
-// epilogue for one 32-column chunk of one row (thread = row)
+// epilogue of the router kinds for one row (thread = row); the six expert kinds store
+// through the TMA-store staging in the kernel body
 template <GemmKind KIND>
 __device__ __forceinline__ void epilogue_tile(const Params& p, const TileInfo& ti, uint32_t tacc, int row_in_tile,
                                               bool zero, int half) {
-    uint32_t r[32], r2[32];
+    uint32_t r[32];
     float v[32];
-    if constexpr (KIND == GemmKind::FwdGateUp) {
-        const int64_t row = ti.m0 + row_in_tile;
-        const int nbase = ti.n0 / 2;
-#pragma unroll 1
-        for (int c = half * (BN / 4); c < (half + 1) * (BN / 4); c += 32) {
-            tmem_ld32(tacc + c, r);
-            tmem_ld32(tacc + BN / 2 + c, r2);
-            tmem_wait_ld();
-            const int col = nbase + c;
-            const int valid = p.I - col;
-            if (valid <= 0) continue;
-            float gv[32], uv[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                gv[j] = __uint_as_float(r[j]);
-                uv[j] = __uint_as_float(r2[j]);
-            }
-            // G and U are stored rounded to bf16; H is computed from the rounded values
-#pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-                const uint32_t gp = pack_bf16(gv[j], gv[j + 1]), up = pack_bf16(uv[j], uv[j + 1]);
-                gv[j] = bf16_lo(gp);
-                gv[j + 1] = bf16_hi(gp);
-                uv[j] = bf16_lo(up);
-                uv[j + 1] = bf16_hi(up);
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = silu_f(gv[j]) * uv[j];
-            store_row32(p.out0 + row * p.I + col, gv, valid);
-            store_row32(p.out1 + row * p.I + col, uv, valid);
-            store_row32(p.out2 + row * p.I + col, v, valid);
-        }
-    } else if constexpr (KIND == GemmKind::FwdDown || KIND == GemmKind::BwdDx) {
-        const int64_t row = ti.m0 + row_in_tile;
-#pragma unroll 1
-        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
-            tmem_ld32(tacc + c, r);
-            tmem_wait_ld();
-            const int col = ti.n0 + c;
-            const int valid = p.H - col;
-            if (valid <= 0) continue;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-            store_row32(p.out0 + row * p.H + col, v, valid);
-        }
-    } else if constexpr (KIND == GemmKind::BwdDownDgrad) {
-        // the SwiGLU-backward epilogue lives in the kernel body (TMA-staged G/U operands)
-    } else if constexpr (KIND == GemmKind::RouterDx) {
-        // dx[t] = (sum of t's expert rows of dXperm, slot order | base[t]) + router term
-        // (moe.hpp:418-427 scatter-add + 454 matmul_nt); rows beyond S only drain TMEM
+    if constexpr (KIND == GemmKind::RouterDx) {
+        // dx[t] = base[t] (the token's summed expert rows) + router term (moe.hpp:418-427
+        // scatter-add + 454 matmul_nt); rows beyond S only drain TMEM
         const int t = ti.m0 + row_in_tile;
         const bool row_ok = t < p.S;
-        int j0 = 0, j1 = 0;
-        if (row_ok && p.cec) {
-            j0 = p.cec[t];
-            j1 = p.cec[t + 1];
-        }
 #pragma unroll 1
         for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
             tmem_ld32(tacc + c, r);
@@ -653,45 +507,15 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const TileInfo& t
             const int valid = p.H - col;
             if (!row_ok || valid <= 0) continue;
             float base[32];
+            const __nv_bfloat16* sp = p.src + (int64_t)t * p.H + col;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) base[j] = 0.f;
-            if (p.cec) {
-                // the token's slot rows, up to 4 at a time with all their 64-byte pieces in flight,
-                // summed in slot order (the scatter-add of moe.hpp:418-423)
-                for (int jb = j0; jb < j1; jb += 4) {
-                    uint4 w4[4][4];
+            for (int q = 0; q < 4; ++q) {
+                const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(sp) + q);
+                const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        if (jb + q >= j1) break;
-                        const uint4* sp = reinterpret_cast<const uint4*>(p.src + (int64_t)p.slot_prow[jb + q] * p.H + col);
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) w4[q][u] = __ldg(sp + u);
-                    }
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        if (jb + q >= j1) break;
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const uint32_t w[4] = {w4[q][u].x, w4[q][u].y, w4[q][u].z, w4[q][u].w};
-#pragma unroll
-                            for (int h = 0; h < 4; ++h) {
-                                base[8 * u + 2 * h] += bf16_lo(w[h]);
-                                base[8 * u + 2 * h + 1] += bf16_hi(w[h]);
-                            }
-                        }
-                    }
-                }
-            } else {
-                const __nv_bfloat16* sp = p.src + (int64_t)t * p.H + col;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(sp) + q);
-                    const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        base[8 * q + 2 * h] = bf16_lo(w[h]);
-                        base[8 * q + 2 * h + 1] = bf16_hi(w[h]);
-                    }
+                for (int h = 0; h < 4; ++h) {
+                    base[8 * q + 2 * h] = bf16_lo(w[h]);
+                    base[8 * q + 2 * h + 1] = bf16_hi(w[h]);
                 }
             }
 #pragma unroll
@@ -726,153 +550,10 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const TileInfo& t
                     if (j < valid) dst[j] = zero ? 0.f : __uint_as_float(r[j]);
             }
         }
-    } else {  // weight gradients: out[e][m][n] * scale
-        // tcgen05.ld is warp-collective: every lane loads, only in-range rows store
-        const int m = ti.m0 + row_in_tile;
-        const int Mtot = (KIND == GemmKind::WgradDown) ? p.I : p.H;
-        const bool row_ok = m < Mtot;
-#pragma unroll 1
-        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
-            if (!zero) {
-                tmem_ld32(tacc + c, r);
-                tmem_wait_ld();
-            }
-            if (!row_ok) continue;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = zero ? 0.f : __uint_as_float(r[j]) * p.scale;
-            const int col = ti.n0 + c;
-            if constexpr (KIND == GemmKind::WgradDown) {
-                const int valid = p.H - col;
-                if (valid <= 0) continue;
-                store_row32(p.out0 + ((int64_t)ti.e * p.I + m) * p.H + col, v, valid);
-            } else {
-                if (col < p.I) {
-                    const int valid = p.I - col;
-                    store_row32(p.out0 + ((int64_t)ti.e * p.H + m) * p.I + col, v, valid);
-                } else {
-                    const int valid = 2 * p.I - col;
-                    if (valid <= 0) continue;
-                    store_row32(p.out1 + ((int64_t)ti.e * p.H + m) * p.I + (col - p.I), v, valid);
-                }
-            }
-        }
     }
 }
 
-__device__ __forceinline__ int ld_acquire(const int32_t* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-// producer side of the fused pull: wait until the valid rows of this CTA's 128-row block have
-// landed (bounded: traps after ~20 s instead of hanging the GPU), then order the async-proxy
-// (TMA) reads after them
-__device__ __forceinline__ void wait_rows_ready(const Params& p, const TileInfo& ti, int m_own) {
-    const int32_t* ps = p.pad_start;
-    const int need = max(0, min(BM, ps[ti.e] + p.counts[ti.e] - m_own));
-    if (need == 0) return;
-    const int32_t* flag = p.ready + (m_own >> 7);
-    uint32_t spins = 0;
-    uint64_t t0 = 0;
-    while (ld_acquire(flag) < need) {
-        __nanosleep(64);
-        if ((++spins & 0x3FFFu) == 0) {
-            const uint64_t now = global_ns();
-            if (t0 == 0) t0 = now;
-            else if (now - t0 > 20000000000ull) {
-                printf("b2 gemm: fused pull never delivered block %d (%d rows)\n", m_own >> 7, need);
-                __trap();
-            }
-        }
-    }
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-
-// the pull itself (warps 2-3 of every CTA): gathered tokens in the rotated source order, one
-// token per warp, its remote row read once (8 x 16 B in flight per lane) and written to each of
-// its local padded rows; BwdDownDgrad scales by the routing weight and forms the weight-gradient
-// dots against mlp_out (output_reduction_backward, moe.hpp:271-298). Each written row bumps its
-// block's counter after a gpu-scope fence.
-template <GemmKind KIND>
-__device__ __forceinline__ void fused_pull(const Params& p, int pw, int npw, int lane) {
-    const int S = p.ep_S, E = p.ep_E, H = p.H, K = p.ep_K;
-    const int nv = H / 8;  // 16-byte vectors per row
-    for (int i = pw; i < p.ep_T; i += npw) {
-        const int src = (p.ep_me + i / S) % E, t = i % S;
-        const int gid = src * S + t;
-        const int j0 = p.pull_cec[gid], j1 = p.pull_cec[gid + 1];
-        if constexpr (KIND == GemmKind::BwdDownDgrad)
-            for (int k = lane; k < K; k += 32) p.pull_wgrad[(int64_t)gid * K + k] = 0.f;
-        if (j0 == j1) continue;
-        const int4* row = reinterpret_cast<const int4*>(p.peer_rows[src] + (int64_t)t * H);
-        constexpr int B = 8;
-        if constexpr (KIND == GemmKind::FwdGateUp) {
-            for (int v0 = 0; v0 < nv; v0 += 32 * B) {
-                int4 val[B];
-#pragma unroll
-                for (int b = 0; b < B; ++b) {
-                    const int v = v0 + lane + 32 * b;
-                    if (v < nv) val[b] = __ldcv(row + v);
-                }
-                for (int j = j0; j < j1; ++j) {
-                    int4* dst = reinterpret_cast<int4*>(p.pull_dst + (int64_t)p.pull_slot_prow[j] * H);
-#pragma unroll
-                    for (int b = 0; b < B; ++b) {
-                        const int v = v0 + lane + 32 * b;
-                        if (v < nv) dst[v] = val[b];
-                    }
-                }
-            }
-        } else {  // dY[r] = w * dout[t]; wgrad[t, k] = dout[t] . y[r] (fp32: bf16 products are exact)
-            for (int j = j0; j < j1; ++j) {
-                const int64_t r = p.pull_slot_prow[j];
-                const int k = p.pull_selk[j];
-                const float wv = p.pull_gw[(int64_t)gid * K + k];
-                const int4* yr = reinterpret_cast<const int4*>(p.pull_y + r * H);
-                int4* dst = reinterpret_cast<int4*>(p.pull_dst + r * H);
-                float dot = 0.f;
-                for (int v0 = 0; v0 < nv; v0 += 32 * B) {
-                    int4 g[B], yv[B];
-#pragma unroll
-                    for (int b = 0; b < B; ++b) {
-                        const int v = v0 + lane + 32 * b;
-                        if (v < nv) {
-                            g[b] = __ldcv(row + v);
-                            yv[b] = __ldg(yr + v);
-                        }
-                    }
-#pragma unroll
-                    for (int b = 0; b < B; ++b) {
-                        const int v = v0 + lane + 32 * b;
-                        if (v >= nv) continue;
-                        const uint32_t gw4[4] = {(uint32_t)g[b].x, (uint32_t)g[b].y, (uint32_t)g[b].z, (uint32_t)g[b].w};
-                        const uint32_t yw4[4] = {(uint32_t)yv[b].x, (uint32_t)yv[b].y, (uint32_t)yv[b].z,
-                                                 (uint32_t)yv[b].w};
-                        uint32_t o[4];
-#pragma unroll
-                        for (int z = 0; z < 4; ++z) {
-                            const float g0 = bf16_lo(gw4[z]), g1 = bf16_hi(gw4[z]);
-                            dot = __fmaf_rn(g0, bf16_lo(yw4[z]), dot);
-                            dot = __fmaf_rn(g1, bf16_hi(yw4[z]), dot);
-                            o[z] = pack_bf16(__fmul_rn(wv, g0), __fmul_rn(wv, g1));
-                        }
-                        dst[v] = make_int4((int)o[0], (int)o[1], (int)o[2], (int)o[3]);
-                    }
-                }
-#pragma unroll
-                for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-                if (lane == 0) p.pull_wgrad[(int64_t)gid * K + k] = dot;
-            }
-        }
-        __threadfence();
-        __syncwarp();
-        if (lane == 0)
-            for (int j = j0; j < j1; ++j) atomicAdd(p.ready + (p.pull_slot_prow[j] >> 7), 1);
-    }
-}
-
-template <GemmKind KIND, int CG, int MC>
+template <GemmKind KIND, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __grid_constant__ Params p) {
     using C = Cfg<CG>;
     using KC = KCfg<KIND, CG>;
@@ -888,34 +569,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
     auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + a); };
     auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + 2 + a); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + STAGES * C::STAGE_BYTES + 8 * (2 * STAGES + 4));
-    auto epi_bar = [&](int w) { return bar0 + 256u + 8u * w; };  // BwdDownDgrad staging barriers
-    // per epilogue warp: [G/U input boxes (dgrad)] [SLOTS output boxes]; 1 KB aligned (bar0 is)
+    // per epilogue warp: SLOTS output staging boxes; 1 KB aligned (bar0 is)
     const uint32_t epi_base = bar0 + 1024u;
 
     pdl_launch();  // the next kernel may be scheduled (it waits for this grid's completion)
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    // cluster = MC CTA pairs: crank = pair * 2 + rank; each pair's leader (rank 0) issues its MMAs
-    const uint32_t crank = CG == 2 ? cluster_rank() : 0u;
-    const uint32_t rank = crank & 1u, lead = crank & ~1u;
-    const int pair = (int)(crank >> 1);
+    // CG = 2: the cluster is one CTA pair; the leader (rank 0) issues the pair's MMAs
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
     const bool leader = rank == 0;
-    const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pair));
     if (warp == 0 && lane == 0) {
         prefetch_map(&p.mapA);
         prefetch_map(&p.mapB0);
         prefetch_map(&p.mapB1);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full_bar(s), 1);
-            mbar_init(empty_bar(s), MC);  // MC = 2: both pairs' MMAs must be done with the stage
+            mbar_init(empty_bar(s), 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull_bar(a), 1);
             mbar_init(tempty_bar(a), NUM_EPI_WARPS * CG);  // the leader's counts both CTAs' epilogues
-        }
-        if constexpr (KIND == GemmKind::BwdDownDgrad) {
-            prefetch_map(&p.mapG);
-            prefetch_map(&p.mapU);
-            for (int w = 0; w < NUM_EPI_WARPS; ++w) mbar_init(epi_bar(w), 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -945,74 +617,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
     const int32_t* ps = p.pad_start;
     const int ntiles = total_tiles<KIND, CG>(p, ps);
     const uint32_t idesc = p.idesc;
-    // tile scheduler over clusters: pair `pair` of cluster `unit` takes tiles unit*MC + pair,
-    // + nunits*MC, ... (MC = 2: the two pairs share M rows and K extent, adjacent N tiles)
-    const int unit = blockIdx.x / (CG * MC), nunits = gridDim.x / (CG * MC);
-    const int tfirst = unit * MC + pair, tstride = nunits * MC;
+    // persistent tile scheduler: pair (cluster) u takes tiles u, u + npairs, ...
+    const int tfirst = blockIdx.x / CG, tstride = gridDim.x / CG;
 
     if (warp == 0) {
-        constexpr bool kGatherKind = KIND == GemmKind::FwdGateUp || KIND == GemmKind::WgradGateUp;
-        if (kGatherKind && p.gather_rows != nullptr) {
-            // X gathered from the token rows with tile::gather4: every lane of the producer warp
-            // issues the 4-row pieces of the A tile (32 per stage), lane 0 the barrier and B
+        if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
             for (int t = tfirst; t < ntiles; t += tstride) {
                 const TileInfo ti = tile_info<KIND, CG>(p, ps, t);
                 const int m_own = ti.m0 + BM * (int)rank;
-                int4 rows_fwd = make_int4(0, 0, 0, 0);
-                if constexpr (KIND == GemmKind::FwdGateUp)  // A = X [rows m_own.., K], rows fixed per tile
-                    rows_fwd = gather_ids(p.gather_rows, (int64_t)m_own + 4 * lane, p.gather_oob);
                 for (int kb = 0; kb < ti.kb; ++kb) {
                     mbar_wait(empty_bar(stage), phase ^ 1u, 0);
                     const uint32_t sA = base + stage * C::STAGE_BYTES, sB = sA + A_BYTES;
                     uint32_t fb = full_bar(stage);
-                    if constexpr (CG == 2) fb = map_to_rank(fb, lead);
-                    if (lane == 0) {
-                        if (leader) mbar_expect_tx(full_bar(stage), p.stage_tx);
-                        load_stage<KIND, CG>(p, ti, kb, m_own, rank, sA, sB, fb);  // B only in gather mode (MC = 1)
-                    }
-                    const int k0 = kb * BK;
-                    if constexpr (KIND == GemmKind::FwdGateUp) {
-                        tma_gather4<CG>(sA + 512u * lane, &p.mapA, fb, k0, rows_fwd);
-                    } else {  // WgradGateUp: A = X^T, K runs over the expert's rows; 2 boxes of 64 columns
-                        const int i = lane % 16, b = lane / 16;
-                        const int4 r = gather_ids(p.gather_rows, (int64_t)ti.krow0 + k0 + 4 * i, p.gather_oob);
-                        tma_gather4<CG>(sA + 8192u * b + 512u * i, &p.mapA, fb, m_own + 64 * b, r);
-                    }
-                    __syncwarp();
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1u;
-                    }
-                }
-            }
-        } else if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int t = tfirst; t < ntiles; t += tstride) {
-                const TileInfo ti = tile_info<KIND, CG>(p, ps, t);
-                const int m_own = ti.m0 + BM * (int)rank;
-                if constexpr (KIND == GemmKind::FwdGateUp || KIND == GemmKind::BwdDownDgrad)
-                    if (p.ready) wait_rows_ready(p, ti, m_own);
-                for (int kb = 0; kb < ti.kb; ++kb) {
-                    mbar_wait(empty_bar(stage), phase ^ 1u, 0);
-                    const uint32_t sA = base + stage * C::STAGE_BYTES, sB = sA + A_BYTES;
-                    uint32_t fb = full_bar(stage);
-                    if constexpr (CG == 2) fb = map_to_rank(fb, lead);
+                    if constexpr (CG == 2) fb = map_to_rank(fb, 0);
                     if (leader) mbar_expect_tx(full_bar(stage), p.stage_tx);
-                    load_stage<KIND, CG, MC>(p, ti, kb, m_own, rank, sA, sB, fb, pair);
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1u;
-                    }
-                }
-            }
-            if constexpr (MC == 2) {
-                // tail: every stage's last release (from both pairs' MMAs) has landed in this CTA's
-                // barriers before the CTA can leave the cluster
-                for (int i = 0; i < STAGES; ++i) {
-                    mbar_wait(empty_bar(stage), phase ^ 1u, 4);
+                    load_stage<KIND, CG>(p, ti, kb, m_own, rank, sA, sB, fb);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1u;
@@ -1047,7 +668,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                         else umma_f16_cg2(tacc, ad, bd, idesc, (kb | k) ? 1u : 0u);
                     }
                     if constexpr (CG == 1) umma_commit(empty_bar(stage));
-                    else if constexpr (MC == 2) umma_commit_cg2_mask(empty_bar(stage), (uint16_t)0xF);
                     else umma_commit_cg2(empty_bar(stage));
                     if (++stage == STAGES) {
                         stage = 0;
@@ -1056,44 +676,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                 }
                 if (ti.kb > 0) {
                     if constexpr (CG == 1) umma_commit(tfull_bar(acc));
-                    else umma_commit_cg2_mask(tfull_bar(acc), pair_mask);
+                    else umma_commit_cg2(tfull_bar(acc));
                 } else {  // empty K range: nothing to wait for, the epilogues store zeros
                     mbar_arrive(tfull_bar(acc));
-                    if constexpr (CG == 2) mbar_arrive_cluster(map_to_rank(tfull_bar(acc), crank | 1u));
+                    if constexpr (CG == 2) mbar_arrive_cluster(map_to_rank(tfull_bar(acc), 1));
                 }
             }
         }
-    } else if (warp == 2 || warp == 3) {
-        if constexpr (KIND == GemmKind::FwdGateUp || KIND == GemmKind::BwdDownDgrad)
-            if (p.ready && p.pull_dst) fused_pull<KIND>(p, (int)blockIdx.x * 2 + (warp - 2), (int)gridDim.x * 2, lane);
     } else if (warp >= 4) {
         const int quad = warp % 4;        // TMEM lanes 32*quad .. 32*quad+31 (hardware rule: warp id % 4)
         const int half = (warp - 4) / 4;  // column half of the tile
-        const uint32_t tempty0 = CG == 2 ? map_to_rank(tempty_bar(0), lead) : tempty_bar(0);
-        // BwdDownDgrad: per-warp G/U staging buffer + mbarrier, one chunk ahead
+        const uint32_t tempty0 = CG == 2 ? map_to_rank(tempty_bar(0), 0) : tempty_bar(0);
         const int ew = warp - 4;
-        const uint32_t gu_s = epi_base + (uint32_t)(ew * KC::WARP_EPI_BYTES);
         EpiStage<KC::SLOTS> stg;
-        stg.s0 = gu_s + (KC::GU_STAGED ? EPI_GU_BYTES : 0);
+        stg.s0 = epi_base + (uint32_t)(ew * KC::WARP_EPI_BYTES);
         stg.g0 = gbase + (stg.s0 - base);
         stg.slot = 0;
         const int row0 = 32 * quad;  // first row of this warp inside the CTA's 128
-        const uint32_t gu_bar = epi_bar(ew);
-        uint32_t gu_phase = 0;
-        auto gu_issue = [&](const TileInfo& tn, int c) {
-            if (KC::GU_STAGED && lane == 0 && tn.n0 + c < p.I) {
-                mbar_expect_tx(gu_bar, EPI_GU_BYTES);
-                tma_load_2d(gu_s, &p.mapG, gu_bar, tn.n0 + c, tn.m0 + 32 * quad);
-                tma_load_2d(gu_s + EPI_GU_BYTES / 2, &p.mapU, gu_bar, tn.n0 + c, tn.m0 + 32 * quad);
-            }
-        };
-        if constexpr (KIND == GemmKind::BwdDownDgrad) {
-            if (tfirst < ntiles) {
-                TileInfo t0i = tile_info<KIND, CG>(p, ps, tfirst);
-                t0i.m0 += BM * (int)rank;
-                gu_issue(t0i, half * (BN / 2));
-            }
-        }
         int it = 0;
         for (int t = tfirst; t < ntiles; t += tstride, ++it) {
             TileInfo ti = tile_info<KIND, CG>(p, ps, t);
@@ -1104,16 +703,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
             tc_fence_after();
             const uint32_t tacc = tmem_base + ((uint32_t)(32 * quad) << 16) + acc * BN;
             if constexpr (KIND == GemmKind::BwdDownDgrad) {
-                const uint8_t* gs = gbase + (gu_s - base);
-                const uint8_t* us = gs + EPI_GU_BYTES / 2;
-                const int sw = (lane >> 1) & 3;
+                // SwiGLU backward (kernels.hpp:277-295) on the dH accumulator: G and U of this
+                // lane's row come straight from global into registers (ld.global.nc)
 #pragma unroll 1
                 for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
                     const int col = ti.n0 + c;
                     const bool live = col < p.I;  // I % 64 == 0: a chunk is all in or all out
                     float gv[32], uv[32];
-                    if (live && !KC::GU_STAGED) {
-                        // this lane's row, 32 columns of G and U (64 B each), straight to registers
+                    if (live) {
                         const int64_t grow = (int64_t)(ti.m0 + row0 + lane) * p.I + col;
                         const uint4* g4p = reinterpret_cast<const uint4*>(p.g + grow);
                         const uint4* u4p = reinterpret_cast<const uint4*>(p.u + grow);
@@ -1135,31 +732,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                                 uv[8 * q + 2 * h + 1] = bf16_hi(uw[h]);
                             }
                         }
-                    } else if (live) {
-                        mbar_wait(gu_bar, gu_phase, 100 + ew);
-                        gu_phase ^= 1u;
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const uint4 g4 = *reinterpret_cast<const uint4*>(gs + lane * 64 + ((q ^ sw) << 4));
-                            const uint4 u4 = *reinterpret_cast<const uint4*>(us + lane * 64 + ((q ^ sw) << 4));
-                            const uint32_t gw[4] = {g4.x, g4.y, g4.z, g4.w}, uw[4] = {u4.x, u4.y, u4.z, u4.w};
-#pragma unroll
-                            for (int h = 0; h < 4; ++h) {
-                                gv[8 * q + 2 * h] = bf16_lo(gw[h]);
-                                gv[8 * q + 2 * h + 1] = bf16_hi(gw[h]);
-                                uv[8 * q + 2 * h] = bf16_lo(uw[h]);
-                                uv[8 * q + 2 * h + 1] = bf16_hi(uw[h]);
-                            }
-                        }
-                        __syncwarp();
-                    }
-                    // the staging buffer is free again: fetch the next chunk (or the next tile's first)
-                    if (c + 32 < (half + 1) * (BN / 2)) {
-                        gu_issue(ti, c + 32);
-                    } else if (t + tstride < ntiles) {
-                        TileInfo tn = tile_info<KIND, CG>(p, ps, t + tstride);
-                        tn.m0 += BM * (int)rank;
-                        gu_issue(tn, half * (BN / 2));
                     }
                     uint32_t r[32];
                     tmem_ld32(tacc + c, r);
@@ -1208,22 +780,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
             } else if constexpr (KIND == GemmKind::FwdDown || KIND == GemmKind::BwdDx) {
                 uint32_t r[32];
                 float v[32];
-                // EP > 1: fused combine (output_reduction_forward / the dX scatter-add, then the
-                // reducescatter, moe.hpp:250-268, 378, 418-428): this row's contribution goes
-                // straight into its source rank's [K][S][H] slab over NVLink, tile by tile
-                __nv_bfloat16* kdst = nullptr;
-                float wv = 1.f;
-                if (p.peer_kslab) {
-                    const int64_t prow = ti.m0 + row0 + lane;
-                    const int gid = p.prow_src[prow];
-                    if (gid >= 0) {
-                        const int kk = p.prow_k[prow];
-                        if constexpr (KIND == GemmKind::FwdDown) wv = p.gw[(int64_t)gid * p.ep_K + kk];
-                        kdst = static_cast<__nv_bfloat16*>(p.peer_kslab[gid / p.ep_S]) +
-                               ((int64_t)kk * p.ep_S + gid % p.ep_S) * p.H;
-                    }
-                }
-                const bool keep_local = KIND == GemmKind::FwdDown || !p.peer_kslab;  // y feeds the backward
 #pragma unroll 1
                 for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
                     tmem_ld32(tacc + c, r);
@@ -1232,20 +788,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                     if (col >= p.H) continue;
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                    if (keep_local) stg.put2d(&p.mapO0, lane, v, col, ti.m0 + row0);
-                    if (kdst) {
-                        if constexpr (KIND == GemmKind::FwdDown) {  // w * (the stored bf16 y), as the combine
-#pragma unroll
-                            for (int j = 0; j < 32; j += 2) {
-                                const uint32_t yb = pack_bf16(v[j], v[j + 1]);
-                                v[j] = __fmul_rn(wv, bf16_lo(yb));
-                                v[j + 1] = __fmul_rn(wv, bf16_hi(yb));
-                            }
-                        }
-                        store_row32(kdst + col, v, 32);
-                    }
+                    stg.put2d(&p.mapO0, lane, v, col, ti.m0 + row0);
                 }
-                if (p.peer_kslab) __threadfence_system();
             } else if constexpr (KIND == GemmKind::WgradDown || KIND == GemmKind::WgradGateUp) {
                 // out[e][m][n] * scale through 3-D maps: rows past the expert's M are clipped
                 uint32_t r[32];
@@ -1342,39 +886,31 @@ static CUtensorMap make_store_map(const void* ptr, int64_t cols, int64_t rows) {
     return make_map(ptr, cols, rows, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
-template <GemmKind KIND, int CG, int MC = 1>
+template <GemmKind KIND, int CG>
 static void launch_kind(const Params& p, int grid, cudaStream_t st) {
     static std::once_flag once;
-    static int max_clusters = 0;  // co-resident clusters of CG * MC CTAs (GPC packing)
+    static int max_clusters = 0;  // co-resident clusters of CG CTAs (GPC packing)
     constexpr int smem = KCfg<KIND, CG>::SMEM;
-    constexpr int CS = CG * MC;
     std::call_once(once, [] {
-        B2_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<KIND, CG, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     smem));
+        B2_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<KIND, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         cudaLaunchConfig_t q{};
         q.gridDim = dim3(148);
         q.blockDim = dim3(NUM_THREADS);
         q.dynamicSmemBytes = smem;
         cudaLaunchAttribute ca[1];
         ca[0].id = cudaLaunchAttributeClusterDimension;
-        ca[0].val.clusterDim.x = CS;
+        ca[0].val.clusterDim.x = CG;
         ca[0].val.clusterDim.y = 1;
         ca[0].val.clusterDim.z = 1;
         q.attrs = ca;
         q.numAttrs = 1;
-        if (cudaOccupancyMaxActiveClusters(&max_clusters, grouped_gemm_kernel<KIND, CG, MC>, &q) != cudaSuccess) {
+        if (cudaOccupancyMaxActiveClusters(&max_clusters, grouped_gemm_kernel<KIND, CG>, &q) != cudaSuccess) {
             cudaGetLastError();
             max_clusters = 0;
         }
     });
-    if (max_clusters > 0) grid = std::min(grid, max_clusters * CS);
-    grid = std::max(CS, grid / CS * CS);
-    static bool said = false;
-    if (!said && getenv("B2_GEMM_DEBUG")) {
-        said = true;
-        fprintf(stderr, "b2 gemm kind %d: cluster %d, max active clusters %d, grid %d\n", (int)KIND, CS, max_clusters,
-                grid);
-    }
+    if (max_clusters > 0) grid = std::min(grid, max_clusters * CG);
+    grid = std::max(CG, grid / CG * CG);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(NUM_THREADS);
@@ -1382,14 +918,14 @@ static void launch_kind(const Params& p, int grid, cudaStream_t st) {
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    B2_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<KIND, CG, MC>, p));
+    B2_CUDA(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<KIND, CG>, p));
 }
 
 }  // namespace sm100
@@ -1409,21 +945,6 @@ bool sm100_available() {
     return major == 10 && minor == 0;
 }
 
-// Opt-in (B2_GEMM_MC=2): clusters of two CTA pairs sharing the A operand by TMA multicast
-// (MC = 2) for the six expert kinds whose N tiles come in pairs. Correct (all GPU parity tests
-// pass under it) but not faster on B200: only 33 four-CTA clusters are co-resident (132 of 148
-// SMs), the GEMMs run power-limited (SM clock 1.45 GHz with 148 SMs, 1.6 GHz with 132), and the
-// per-kind times came out within -2 .. +2 % of the single-pair kernels (ncu, round 1 session 3)
-// while the step was 6 % slower on the same box. Single-pair clusters stay the default.
-static bool gemm_mc_enabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("B2_GEMM_MC");
-        v = (e && atoi(e) == 2) ? 1 : 0;
-    }
-    return v == 1;
-}
-
 void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
     using namespace sm100;
     check(a.H % 64 == 0 && a.I % 64 == 0, "bf16 expert path: hidden and intermediate must be multiples of 64");
@@ -1441,42 +962,6 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
     p.out0 = (__nv_bfloat16*)a.out0;
     p.out1 = (__nv_bfloat16*)a.out1;
     p.out2 = (__nv_bfloat16*)a.out2;
-    p.gather_rows = a.gather_rows;
-    p.gather_oob = a.gather_tokens;
-    p.tile_order = a.tile_order;
-    p.ready = a.ready;
-    p.peer_rows = reinterpret_cast<const __nv_bfloat16* const*>(a.peer_rows);
-    p.ep_E = a.ep_E;
-    p.ep_me = a.ep_me;
-    p.ep_T = a.ep_T;
-    p.pull_cec = a.pull_cec;
-    p.pull_slot_prow = a.pull_slot_prow;
-    p.pull_selk = a.pull_selk;
-    p.pull_gw = a.pull_gw;
-    p.pull_y = (const __nv_bfloat16*)a.pull_y;
-    p.pull_dst = (__nv_bfloat16*)a.pull_dst;
-    p.pull_wgrad = a.pull_wgrad;
-    if (a.ready && !a.pull_dst)  // rows arrive from a concurrent pull kernel: wait only
-        check((a.kind == GemmKind::FwdGateUp || a.kind == GemmKind::BwdDownDgrad) && a.tile_order && a.counts &&
-                  !a.gather_rows,
-              "overlapped pull: FwdGateUp / BwdDownDgrad with a tile order");
-    else if (a.ready)
-        check((a.kind == GemmKind::FwdGateUp || a.kind == GemmKind::BwdDownDgrad) && a.tile_order && a.peer_rows &&
-                  a.ep_E > 1 && a.ep_S > 0 && a.ep_T == a.ep_E * a.ep_S && a.pull_cec && a.pull_slot_prow &&
-                  a.pull_dst && a.counts && !a.gather_rows &&
-                  (a.kind == GemmKind::FwdGateUp || (a.pull_selk && a.pull_gw && a.pull_y && a.pull_wgrad)),
-              "fused pull: FwdGateUp / BwdDownDgrad with the EP tables");
-    p.peer_kslab = a.peer_kslab;
-    p.prow_src = a.prow_src;
-    p.prow_k = a.prow_k;
-    p.gw = a.gw;
-    p.ep_S = a.ep_S;
-    p.ep_K = a.ep_K;
-    if (a.peer_kslab)
-        check((a.kind == GemmKind::FwdDown || a.kind == GemmKind::BwdDx) && a.prow_src && a.prow_k && a.ep_S > 0 &&
-                  (a.kind != GemmKind::FwdDown || a.gw),
-              "fused combine: FwdDown / BwdDx with the row tables");
-    if (a.gather_rows) check(a.gather_tokens >= 0 && a.pmax % 4 == 0, "gather4 operand: bad token count / row capacity");
     const int64_t P = a.pmax, H = a.H, I = a.I, nr = a.nr;
     int grid = a.num_sms > 0 ? a.num_sms : 148;
     if (a.max_ctas > 0) grid = std::min(grid, std::max(2, a.max_ctas));
@@ -1485,10 +970,8 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
     p.S = a.S;
     p.N = a.N;
     p.counts = a.counts;
-    // the six expert GEMMs run as 256 x 256 tiles on CTA pairs (cta_group::2); opt-in: two
-    // pairs per cluster sharing A by multicast where the N tiles pair up
+    // the six expert GEMMs run as 256 x 256 tiles on CTA pairs (cta_group::2)
     constexpr int G = 2;
-    const bool mc_ok = gemm_mc_enabled();
     using C2 = Cfg<G>;
     p.stage_tx = G * C2::STAGE_BYTES;
     switch (a.kind) {
@@ -1511,54 +994,44 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
     switch (a.kind) {
         case GemmKind::FwdGateUp: {
             p.n_tiles = (int)ceil_div(I, BN / 2);
-            const bool mc = mc_ok && !a.gather_rows && p.n_tiles % 2 == 0;
-            p.mapA = a.gather_rows ? make_map(a.x, H, a.gather_tokens, 64, 1) : make_map(a.x, H, P, 64, mc ? 64 : BM);
+            p.mapA = make_map(a.x, H, P, 64, BM);
             p.mapB0 = make_map(a.wg, I, nr * H, 64, 64);
             p.mapB1 = make_map(a.wu, I, nr * H, 64, 64);
             p.mapO0 = make_store_map(a.out0, I, P);
             p.mapO1 = make_store_map(a.out1, I, P);
             p.mapO2 = make_store_map(a.out2, I, P);
             p.num_kb_fixed = (int)ceil_div(H, BK);
-            if (mc) launch_kind<GemmKind::FwdGateUp, G, 2>(p, grid, st);
-            else launch_kind<GemmKind::FwdGateUp, G>(p, grid, st);
+            launch_kind<GemmKind::FwdGateUp, G>(p, grid, st);
             break;
         }
         case GemmKind::FwdDown: {
             p.n_tiles = (int)ceil_div(H, BN);
-            const bool mc = mc_ok && p.n_tiles % 2 == 0;
-            p.mapA = make_map(a.h, I, P, 64, mc ? 64 : BM);
+            p.mapA = make_map(a.h, I, P, 64, BM);
             p.mapB0 = make_map(a.wd, H, nr * I, 64, 64);
             p.mapB1 = p.mapB0;
             p.mapO0 = make_store_map(a.out0, H, P);
             p.num_kb_fixed = (int)ceil_div(I, BK);
-            if (mc) launch_kind<GemmKind::FwdDown, G, 2>(p, grid, st);
-            else launch_kind<GemmKind::FwdDown, G>(p, grid, st);
+            launch_kind<GemmKind::FwdDown, G>(p, grid, st);
             break;
         }
         case GemmKind::BwdDownDgrad: {
             p.n_tiles = (int)ceil_div(I, BN);
-            const bool mc = mc_ok && p.n_tiles % 2 == 0;
-            p.mapA = make_map(a.dy, H, P, 64, mc ? 64 : BM);
+            p.mapA = make_map(a.dy, H, P, 64, BM);
             p.mapB0 = make_map(a.wd, H, nr * I, 64, C2::B_COLS);
             p.mapB1 = p.mapB0;
-            p.mapG = make_map(a.g, I, P, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
-            p.mapU = make_map(a.u, I, P, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
             p.mapO0 = make_store_map(a.out0, 2 * I, P);
             p.num_kb_fixed = (int)ceil_div(H, BK);
-            if (mc) launch_kind<GemmKind::BwdDownDgrad, G, 2>(p, grid, st);
-            else launch_kind<GemmKind::BwdDownDgrad, G>(p, grid, st);
+            launch_kind<GemmKind::BwdDownDgrad, G>(p, grid, st);
             break;
         }
         case GemmKind::BwdDx: {
             p.n_tiles = (int)ceil_div(H, BN);
-            const bool mc = mc_ok && p.n_tiles % 2 == 0;
-            p.mapA = make_map(a.dgu, 2 * I, P, 64, mc ? 64 : BM);
+            p.mapA = make_map(a.dgu, 2 * I, P, 64, BM);
             p.mapB0 = make_map(a.wg, I, nr * H, 64, C2::B_COLS);
             p.mapB1 = make_map(a.wu, I, nr * H, 64, C2::B_COLS);
             p.mapO0 = make_store_map(a.out0, H, P);
             p.num_kb_fixed = (int)ceil_div(2 * I, BK);
-            if (mc) launch_kind<GemmKind::BwdDx, G, 2>(p, grid, st);
-            else launch_kind<GemmKind::BwdDx, G>(p, grid, st);
+            launch_kind<GemmKind::BwdDx, G>(p, grid, st);
             break;
         }
         case GemmKind::WgradDown: {
@@ -1570,13 +1043,12 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.m_tiles_fixed = (int)ceil_div(I, BM * G);
             p.n_tiles = (int)ceil_div(H, BN);
             grid = (int)std::min<int64_t>(grid, G * nr * p.m_tiles_fixed * p.n_tiles);
-            if (mc_ok && p.n_tiles % 2 == 0) launch_kind<GemmKind::WgradDown, G, 2>(p, grid, st);
-            else launch_kind<GemmKind::WgradDown, G>(p, grid, st);
+            launch_kind<GemmKind::WgradDown, G>(p, grid, st);
             break;
         }
         case GemmKind::WgradGateUp: {
             check(a.counts != nullptr, "wgrad: expert row counts required");
-            p.mapA = a.gather_rows ? make_map(a.x, H, a.gather_tokens, 64, 1) : make_map(a.x, H, P, 64, 64);
+            p.mapA = make_map(a.x, H, P, 64, 64);
             p.mapB0 = make_map(a.dgu, 2 * I, P, 64, 64);
             p.mapB1 = p.mapB0;
             p.mapO0 = make_map3(a.out0, I, H, nr);
@@ -1584,8 +1056,7 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.m_tiles_fixed = (int)ceil_div(H, BM * G);
             p.n_tiles = (int)ceil_div(2 * I, BN);
             grid = (int)std::min<int64_t>(grid, G * nr * p.m_tiles_fixed * p.n_tiles);
-            if (mc_ok && !a.gather_rows && p.n_tiles % 2 == 0) launch_kind<GemmKind::WgradGateUp, G, 2>(p, grid, st);
-            else launch_kind<GemmKind::WgradGateUp, G>(p, grid, st);
+            launch_kind<GemmKind::WgradGateUp, G>(p, grid, st);
             break;
         }
         case GemmKind::RouterDx: {
@@ -1599,8 +1070,6 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.mapB1 = p.mapB0;
             p.n_tiles = (int)ceil_div(H, BN);
             p.num_kb_fixed = 2 * (int)ceil_div(a.N, BK);  // hi then lo
-            p.cec = a.cec;
-            p.slot_prow = a.slot_prow;
             p.src = (const __nv_bfloat16*)a.src;
             grid = (int)std::min<int64_t>(grid, ceil_div(S, BM) * p.n_tiles);
             launch_kind<GemmKind::RouterDx, 1>(p, grid, st);

@@ -185,7 +185,7 @@ __global__ void scatter_kernel(const int32_t* __restrict__ gidx, int T, int K, i
                                const int32_t* __restrict__ pad_start, const int32_t* __restrict__ cum_expert_counts,
                                int32_t* __restrict__ input_indices, int32_t* __restrict__ output_indices,
                                int32_t* __restrict__ selected_k, int32_t* __restrict__ slot_prow,
-                               int32_t* __restrict__ prow_src, int32_t* __restrict__ prow_k) {
+                               int32_t* __restrict__ prow_src) {
     pdl_wait();
     pdl_launch();
     extern __shared__ int32_t sh[];  // carry [kWarpsPerCta][nr] (row offset inside the expert)
@@ -222,7 +222,6 @@ __global__ void scatter_kernel(const int32_t* __restrict__ gidx, int T, int K, i
             selected_k[pos] = k;
             slot_prow[pos] = prow;
             prow_src[prow] = t;
-            if (prow_k) prow_k[prow] = k;
         }
     }
 }
@@ -254,7 +253,7 @@ void launch_routing_index(const RoutingIndexArgs& a, cudaStream_t st) {
         launch_k(scatter_kernel, dim3(nblk), dim3(32 * kWarpsPerCta), smem, st, a.gidx, a.T, a.K, a.n_start, a.nr, nchunks, a.wbase,
                                                               a.cum_token_counts, a.pad_start, a.cum_expert_counts,
                                                               a.input_indices, a.output_indices, a.selected_k,
-                                                              a.slot_prow, a.prow_src, a.prow_k);
+                                                              a.slot_prow, a.prow_src);
         B2_LAUNCH_CHECK();
     }
     launch_k(pad_fill_kernel, dim3(a.nr), dim3(128), 0, st, a.token_counts, a.pad_start, a.nr, a.prow_src);

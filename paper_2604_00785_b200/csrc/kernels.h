@@ -45,7 +45,6 @@ struct RoutingIndexArgs {
     int32_t* selected_k;         // [T*K]
     int32_t* slot_prow;          // [T*K] token-major slot -> padded row
     int32_t* prow_src;           // [pmax] padded row -> token (-1 pad)
-    int32_t* prow_k;             // [pmax] padded row -> top-k slot k (nullptr: not needed)
     int32_t* err;                // expert id out of range flag
 };
 void launch_routing_index(const RoutingIndexArgs& a, cudaStream_t st);
@@ -91,11 +90,6 @@ template <typename T>
 // max_blocks > 0 caps the grid (a side-stream launch that must stay inside its reserved SMs)
 void launch_ep_pull_sum(const T* const* peer_slab, const int32_t* gi_local, int S, int K, int E, int NR, int W, int me,
                         T* out, cudaStream_t st, int max_blocks = 0);
-// out[t] = sum over k (in k order) of slab[k][t] — the source side of the GEMM-fused
-// combine: every (t, k) row was stored into this rank's [K][S][W] slab by its owner's
-// FwdDown / BwdDx epilogue over NVLink
-template <typename T>
-void launch_kslab_sum(const T* slab, int S, int K, int W, T* out, cudaStream_t st);
 // [E][n] routing tables gathered from the peers' symmetric buffers
 void launch_ep_table_pull(const int32_t* const* peer_ids, const float* const* peer_w, int64_t n, int E,
                           int32_t* ids_all, float* w_all, cudaStream_t st);
@@ -128,7 +122,7 @@ enum class GemmKind : int {
     BwdDx = 3,       // dX = [dG|dU] · [Wg|Wu]ᵀ   (K = 2I)
     WgradDown = 4,   // dWd[e] = Hᵀ · dY  over the rows of e
     WgradGateUp = 5, // [dWg|dWu][e] = Xᵀ · [dG|dU]
-    RouterDx = 6,    // dx = (Σ_slots dXperm | base) + dlogits · Wrᵀ   (M = S, K = N experts)
+    RouterDx = 6,    // dx = base + dlogits · Wrᵀ   (M = S, K = 2 x N experts: the hi + lo dlogits split)
     RouterDw = 7,    // dWr partials [split][H][N] = x[rows of split]ᵀ · dlogits (split-K over S)
 };
 struct Sm100GemmArgs {
@@ -157,48 +151,12 @@ struct Sm100GemmArgs {
     const void* wr;              // router weight [H, N] bf16
     const void* dl;              // dlogits [S, N] bf16 (RouterDx: the high half of the split)
     const void* dl_lo;           // RouterDx: bf16(dlogits - dl) [S, N]
-    const int32_t* cec;          // RouterDx: cum_expert_counts [S+1] (null: add `base` rows instead)
-    const int32_t* slot_prow;    // RouterDx: slot -> padded row of dXperm
-    const void* src;             // RouterDx: dXperm [P, H] (slots) or base [S, H]
+    const void* src;             // RouterDx: base rows [S, H] (the token's summed expert-gradient rows)
     float* part;                 // RouterDw: fp32 partials [nsplit][H][N]
     int nsplit_out;              // RouterDw: number of S splits used (set by the launcher)
-    // FwdGateUp / WgradGateUp: gather the X operand straight from the token rows `x` [S,H]
-    // with TMA tile::gather4 (padded row -> token via gather_rows, -1 = zero row) instead
-    // of reading a materialised mlp_in; null: `x` is mlp_in [P,H]
-    const int32_t* gather_rows;
-    int gather_tokens;           // S: rows of `x` (row S is the zero-filled out-of-bounds row)
-    // FwdDown / BwdDx at EP > 1: the GEMM-fused combine. The epilogue also stores each padded
-    // row's result (FwdDown: w * y; BwdDx: dX) straight into the source rank's [K][S][H] slab
-    // over NVLink (peer_kslab: device table of EP pointers); the source sums over k
-    void* const* peer_kslab;
-    const int32_t* prow_src;     // padded row -> gathered token id (-1 pad)
-    const int32_t* prow_k;       // padded row -> top-k slot
-    const float* gw;             // [T, K] gathered routing weights (FwdDown)
-    int ep_S, ep_K;              // tokens per rank, top-k
     int max_ctas;                // > 0: cap the persistent grid (SMs left to concurrent comm kernels)
-    // FwdGateUp / BwdDownDgrad at EP > 1: the fused pull (sm100::Params). Warps 2-3 of every CTA
-    // pull the gathered tokens' x (dout) rows over NVLink into mlp_in (dY) and count them per
-    // 128-row block in `ready`; the producer waits for its block; m-tiles visit in `tile_order`
-    const int32_t* tile_order;
-    int32_t* ready;
-    const void* const* peer_rows;
-    int ep_E, ep_me, ep_T;
-    const int32_t* pull_cec;
-    const int32_t* pull_slot_prow;
-    const int32_t* pull_selk;
-    const float* pull_gw;
-    const void* pull_y;
-    void* pull_dst;
-    float* pull_wgrad;
 };
 void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st);
-// EP fused pull: the visiting order of the 256-row m-tiles, by the latest rotated gathered token
-// ((src - me) mod E) * S + t among each tile's rows, one bucket per source (stable)
-// the dispatch pull beside the FwdGateUp GEMM (one block per SM, arrival counters per 128 rows)
-void launch_ep_pull_rows(const void* const* peer_src, int S, int E, int me, int H, const int32_t* cec,
-                         const int32_t* slot_prow, void* out, int32_t* ready, int num_sms, cudaStream_t st);
-void launch_ep_tile_order(const int32_t* prow_src, const int32_t* p_total, int S, int E, int me, int max_tiles,
-                          int32_t* bucket, int32_t* order, cudaStream_t st);
 // number of S splits the RouterDw kind uses (its partial buffer holds splits*H*N floats)
 int router_dw_splits(int64_t S, int64_t H, int num_sms);
 // sums RouterDw partials in split order into dW (T = bf16)
@@ -259,12 +217,13 @@ void launch_sumsq_chunks(const OptSeg* segs, const OptChunk* chunks, const int32
                          double* partials, int32_t* nonfinite, cudaStream_t st);
 // *norm_sq = fixed-order sum of partials[0, n)
 void launch_norm_final(const double* partials, int n, double* norm_sq, cudaStream_t st);
-// fused unscale + clip (from *norm_sq) + AdamW + bf16 recast over the listed chunks; a set
-// *nonfinite leaves every state untouched
+// fused unscale + clip (from *norm_sq) + AdamW + bf16 recast over the listed chunks. Like the
+// reference's step (optim.cpp:130-194) it always applies the update; non-finite gradients are
+// reported by the scan (StepStats.nonfinite / detect_soft_failure), which the training loop
+// checks before stepping (train.cpp:193-194)
 // sm_reserve > 0: the persistent grid leaves that many SMs free (for concurrent NCCL kernels)
 void launch_adamw_chunks(const OptSeg* segs, const OptChunk* chunks, const int32_t* ids, int nids,
-                         const OptStepArgs& a, const double* norm_sq, const int32_t* nonfinite, cudaStream_t st,
-                         int sm_reserve = 0);
+                         const OptStepArgs& a, const double* norm_sq, cudaStream_t st, int sm_reserve = 0);
 // any non-finite element in the n-element buffer -> *flag = 1
 void launch_nonfinite_scan(const void* g, int dtype, int64_t n, int32_t* flag, cudaStream_t st);
 

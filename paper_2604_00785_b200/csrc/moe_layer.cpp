@@ -86,7 +86,7 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
         acc(4 * (size_t)std::max<int64_t>(n, 1));
     // workspace: int32
     for (int64_t n : {smax_ * K, tmax_ * K, nch * nr, nch * nr, tmax_, tmax_ + 1, nr * thmax_, nr * thmax_ + 1, nr,
-                      nr + 1, nr + 1, tmax_ * K, tmax_ * K, tmax_ * K, tmax_ * K, pmax_, pmax_})
+                      nr + 1, nr + 1, tmax_ * K, tmax_ * K, tmax_ * K, tmax_ * K, pmax_})
         acc(4 * (size_t)std::max<int64_t>(n, 1));
     // workspace: dtype, padded rows (+ the replay output)
     for (int64_t n : {pmax_ * H, pmax_ * I, pmax_ * I, pmax_ * I, pmax_ * H, pmax_ * H, pmax_ * I, pmax_ * 2 * I,
@@ -98,9 +98,6 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     if (E > 1) {
         for (int64_t n : {tmax_ * K, tmax_ * K, smax_ * K}) acc(4 * (size_t)std::max<int64_t>(n, 1));
         acc(es * (size_t)std::max<int64_t>(smax_ * H, 1));
-        acc(es * (size_t)std::max<int64_t>(tmax_ * H, 1));  // x_all (copy-engine dispatch)
-        for (int64_t n : {pmax_ / 128 + 1, pmax_ / kRowAlign + 1, pmax_ / kRowAlign + 1})  // fused pull
-            acc(4 * (size_t)n);
     }
     B2_CUDA(cudaSetDevice(ctx_.device));
     if (share_ws) {
@@ -145,7 +142,6 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     selected_k_ = w.take<int32_t>(tmax_ * K);
     slot_prow_ = w.take<int32_t>(tmax_ * K);
     prow_src_ = w.take<int32_t>(pmax_);
-    prow_k_ = w.take<int32_t>(pmax_);
     mlp_in_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
     g_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
     u_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
@@ -164,19 +160,10 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
         gw_all_ = w.take<float>(tmax_ * K);
         wgrad_local_ = w.take<float>(smax_ * K);
         dx_exp_ = w.take_bytes(es * (size_t)std::max<int64_t>(smax_ * H, 1));
-        max_mtiles_ = pmax_ / kRowAlign;
-        ready_ = w.take<int32_t>(pmax_ / 128 + 1);
-        tile_bucket_ = w.take<int32_t>(max_mtiles_ + 1);
-        tile_order_ = w.take<int32_t>(max_mtiles_ + 1);
-        if (const char* e = getenv("B2_EP_FUSED_PULL")) fused_pull_opt_ = atoi(e) != 0;
-        if (const char* e = getenv("B2_EP_OVERLAP_PULL")) overlap_pull_opt_ = atoi(e) != 0;
-        if (const char* e = getenv("B2_COMM_SMS")) comm_sms_ = std::max(2, std::min(ctx_.num_sms / 2, atoi(e)));
-        x_all_ = w.take_bytes(es * (size_t)std::max<int64_t>(tmax_ * H, 1));
         ep_setup();
         B2_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
         B2_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
         B2_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
-        B2_CUDA(cudaEventCreateWithFlags(&ev_xall_, cudaEventDisableTiming));
     }
     B2_CUDA(cudaMemsetAsync(err_, 0, 4, ctx_.stream));
     B2_CUDA(cudaMemsetAsync(colsum_ctr_, 0, 4, ctx_.stream));
@@ -195,7 +182,6 @@ MoeLayer::~MoeLayer() {
         cudaStreamDestroy(side_);
         cudaEventDestroy(ev_fork_);
         cudaEventDestroy(ev_join_);
-        cudaEventDestroy(ev_xall_);
     }
     if (sym_) {
         cudaStreamSynchronize(ctx_.stream);
@@ -208,7 +194,7 @@ MoeLayer::~MoeLayer() {
 }
 
 // symmetric buffer: [x_sh S*H | dout_sh S*H | ret_f E*S*H | ret_b E*S*H] (dtype) + wret [E*S*K] f32
-// + kslab [K*S*H] (dtype, the GEMM-fused combine's landing slab), identical offsets on every
+// + barrier flags [E] + the published routing table [S,K] ids + weights, identical offsets on every
 // rank; IPC handles are exchanged with an NCCL all-gather
 void MoeLayer::ep_setup() {
     const int E = cfg_.ep, me = ctx_.coord_ep;
@@ -216,7 +202,7 @@ void MoeLayer::ep_setup() {
     const size_t H = (size_t)cfg_.hidden, S = (size_t)std::max<int64_t>(smax_, 1), K = (size_t)cfg_.top_k;
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t o_x = 0, o_d = o_x + al(es * S * H), o_rf = o_d + al(es * S * H), o_rb = o_rf + al(es * E * S * H),
-                 o_w = o_rb + al(es * E * S * H), o_k = o_w + al(4 * E * S * K), o_f = o_k + al(es * K * S * H),
+                 o_w = o_rb + al(es * E * S * H), o_f = o_w + al(4 * E * S * K),
                  o_t = o_f + al(4 * (size_t)E), total = o_t + al(8 * S * K);
     B2_CUDA(cudaMalloc(&sym_, total));
     // barrier flags start at zero before any peer can see this buffer: the memset precedes
@@ -265,63 +251,37 @@ void MoeLayer::ep_setup() {
             peer_ipc_[(size_t)p] = 1;
         }
     }
-    std::vector<void*> tab((size_t)9 * E);
+    std::vector<void*> tab((size_t)8 * E);
     for (int p = 0; p < E; ++p) {
         tab[(size_t)(0 * E + p)] = peer_base_[(size_t)p] + o_x;
         tab[(size_t)(1 * E + p)] = peer_base_[(size_t)p] + o_d;
         tab[(size_t)(2 * E + p)] = peer_base_[(size_t)p] + o_rf;
         tab[(size_t)(3 * E + p)] = peer_base_[(size_t)p] + o_rb;
         tab[(size_t)(4 * E + p)] = peer_base_[(size_t)p] + o_w;
-        tab[(size_t)(5 * E + p)] = peer_base_[(size_t)p] + o_k;
-        tab[(size_t)(6 * E + p)] = peer_base_[(size_t)p] + o_f;
-        tab[(size_t)(7 * E + p)] = peer_base_[(size_t)p] + o_t;                // routing ids [S,K]
-        tab[(size_t)(8 * E + p)] = peer_base_[(size_t)p] + o_t + 4 * S * K;    // routing weights [S,K]
+        tab[(size_t)(5 * E + p)] = peer_base_[(size_t)p] + o_f;
+        tab[(size_t)(6 * E + p)] = peer_base_[(size_t)p] + o_t;                // routing ids [S,K]
+        tab[(size_t)(7 * E + p)] = peer_base_[(size_t)p] + o_t + 4 * S * K;    // routing weights [S,K]
     }
     B2_CUDA(cudaMalloc(&peer_tab_, sizeof(void*) * tab.size()));
     B2_CUDA(cudaMemcpy(peer_tab_, tab.data(), sizeof(void*) * tab.size(), cudaMemcpyHostToDevice));
     x_sh_ = sym_ + o_x;
-    x_sh_off_ = o_x;
     dout_sh_ = sym_ + o_d;
     ret_f_ = sym_ + o_rf;
     ret_b_ = sym_ + o_rb;
     wret_ = (float*)(sym_ + o_w);
-    kslab_ = sym_ + o_k;
     flags_ = (int*)(sym_ + o_f);
     tab_ids_ = (int32_t*)(sym_ + o_t);
     tab_w_ = (float*)(sym_ + o_t + 4 * S * K);
 }
 
 // every rank's preceding stream work (and its peer stores) is complete once this returns
-bool MoeLayer::overlap_pull() const {
-    return dtype_ == BF16 && cfg_.ep > 1 && overlap_pull_opt_ && !ce_dispatch_opt_ && !gather_in_gemm() && ready_ &&
-           side_ != nullptr;
-}
-
-bool MoeLayer::fused_pull() const {
-    return dtype_ == BF16 && cfg_.ep > 1 && fused_pull_opt_ && !ce_dispatch_opt_ && !gather_in_gemm() && ready_;
-}
-
-void MoeLayer::set_pull_args(Sm100GemmArgs& ga, const void* const* peer_rows, void* dst, int S, int K, int Tt) const {
-    ga.ready = ready_;
-    ga.tile_order = tile_order_;
-    ga.peer_rows = peer_rows;
-    ga.ep_E = cfg_.ep;
-    ga.ep_me = ctx_.coord_ep;
-    ga.ep_S = S;
-    ga.ep_K = K;
-    ga.ep_T = Tt;
-    ga.pull_cec = cec_;
-    ga.pull_slot_prow = slot_prow_;
-    ga.pull_dst = dst;
-}
-
 void MoeLayer::ep_barrier(cudaStream_t st) {
-    launch_ep_flag_barrier((int* const*)peer_tab_ + 6 * cfg_.ep, flags_, bar_, cfg_.ep, ctx_.coord_ep,
+    launch_ep_flag_barrier((int* const*)peer_tab_ + 5 * cfg_.ep, flags_, bar_, cfg_.ep, ctx_.coord_ep,
                            st ? st : ctx_.stream);
 }
 
 bool MoeLayer::overlap_return() const {
-    return dtype_ == BF16 && cfg_.ep > 1 && !fused_combine() && side_ != nullptr && overlap_opt_;
+    return dtype_ == BF16 && cfg_.ep > 1 && side_ != nullptr && overlap_opt_;
 }
 
 const char* MoeLayer::stage_name(int s) {
@@ -428,12 +388,6 @@ void MoeLayer::run_graphed(GraphCache (&gcs)[kGraphSlots], std::vector<const voi
 }
 
 // dispatch weights/indices of this forward (learned top-k or FUR; the gathered table at EP > 1)
-bool MoeLayer::fused_combine() const { return dtype_ == BF16 && cfg_.ep > 1 && fused_combine_opt_; }
-
-bool MoeLayer::gather_in_gemm() const {
-    return dtype_ == BF16 && cfg_.ep == 1 && tma_gather_ && ((uintptr_t)x_ & 15) == 0 && s_ > 0;
-}
-
 void MoeLayer::set_dispatch_tables() {
     gw_ = fur_ ? (const float*)fw_ : (const float*)topw_;
     gi_ = fur_ ? (const int32_t*)fi_ : (const int32_t*)topi_;
@@ -475,20 +429,6 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     const int S = (int)s_, N = (int)cfg_.n_experts, K = (int)cfg_.top_k, H = (int)cfg_.hidden,
               I = (int)cfg_.intermediate, nr = (int)cfg_.experts_per_rank();
     int Tt = S;  // rows of the (gathered) table this rank processes
-    const bool ce_dispatch = E > 1 && ce_dispatch_opt_;
-    if (ce_dispatch) {
-        // the token exchange of moe.hpp:365 as copy-engine all-gather: publish x, barrier, then
-        // a side stream copies every rank's x over NVLink into x_all while the SMs route
-        B2_CUDA(cudaMemcpyAsync(x_sh_, x, sizeof(T) * (size_t)S * H, cudaMemcpyDeviceToDevice, st));
-        ep_barrier();
-        B2_CUDA(cudaEventRecord(ev_fork_, st));
-        B2_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
-        const size_t rb = sizeof(T) * (size_t)S * H;
-        for (int p = 0; p < E; ++p)
-            B2_CUDA(cudaMemcpyAsync((char*)x_all_ + (size_t)p * rb, peer_base_[(size_t)p] + x_sh_off_, rb,
-                                    cudaMemcpyDeviceToDevice, side_));
-        B2_CUDA(cudaEventRecord(ev_xall_, side_));
-    }
     // stage 1: route locally (moe.hpp:357-364)
     mark(kRoute, false);
     launch_router_logits<T>(x, router, logits_, S, H, N, st);
@@ -503,13 +443,12 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
         // routing table; token rows stay where they are until an expert owner pulls them.
         // Publish x and this rank's table in the symmetric buffer, barrier, then pull every
         // rank's table (NVLink peer memory; no NCCL on the step's path)
-        if (!ce_dispatch)
-            B2_CUDA(cudaMemcpyAsync(x_sh_, x, sizeof(T) * (size_t)S * H, cudaMemcpyDeviceToDevice, st));
+        B2_CUDA(cudaMemcpyAsync(x_sh_, x, sizeof(T) * (size_t)S * H, cudaMemcpyDeviceToDevice, st));
         B2_CUDA(cudaMemcpyAsync(tab_ids_, gi_local_, 4 * (size_t)S * K, cudaMemcpyDeviceToDevice, st));
         B2_CUDA(cudaMemcpyAsync(tab_w_, fur ? (const float*)fw_ : (const float*)topw_, 4 * (size_t)S * K,
                                 cudaMemcpyDeviceToDevice, st));
         ep_barrier();
-        launch_ep_table_pull((const int32_t* const*)peer_tab_ + 7 * E, (const float* const*)peer_tab_ + 8 * E,
+        launch_ep_table_pull((const int32_t* const*)peer_tab_ + 6 * E, (const float* const*)peer_tab_ + 7 * E,
                              (int64_t)S * K, E, gi_all_, gw_all_, st);
         launches_ += 2;
         Tt = E * S;
@@ -540,37 +479,18 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     ra.selected_k = selected_k_;
     ra.slot_prow = slot_prow_;
     ra.prow_src = prow_src_;
-    ra.prow_k = fused_combine() ? prow_k_ : nullptr;
     ra.err = err_;
     launch_routing_index(ra, st);
     launches_ += 4;
     mark(kIndex, true);
     const int32_t* p_total = pad_start_ + nr;
     // stage 4: expert MLP over the padded expert-sorted rows (225-244)
-    // opt-in (bf16, EP = 1): the expert GEMMs gather their X operand straight from x (TMA
-    // tile::gather4 by prow_src) instead of a materialised mlp_in. Bitwise identical, but
-    // measured 1.9x slower GEMMs on B200 (32 four-row TMA ops per stage instead of one
-    // tile op), so the gather kernel + mlp_in stay the default
-    const bool tma_gather = gather_in_gemm();
     mark(kGather, false);
     if (E > 1) {
-        if (ce_dispatch) {  // every rank's rows are local now: a plain gather (pads zeroed)
-            B2_CUDA(cudaStreamWaitEvent(st, ev_xall_, 0));
-            launch_gather_rows<T>((const T*)x_all_, prow_src_, p_total, (T*)mlp_in_, H, pmax_, st);
-            launches_ += 1;
-        } else if (fused_pull() || overlap_pull()) {
-            // the FwdGateUp kernel pulls the rows itself; pads first, counters zeroed, tile order
-            launch_zero_pad_rows<T>((T*)mlp_in_, prow_src_, p_total, H, pmax_, st);
-            B2_CUDA(cudaMemsetAsync(ready_, 0, 4 * (size_t)(pmax_ / 128 + 1), st));
-            launch_ep_tile_order(prow_src_, p_total, S, E, ctx_.coord_ep, (int)max_mtiles_, tile_bucket_, tile_order_,
-                                 st);
-            launches_ += 3;
-        } else {
-            launch_ep_gather_pull<T>((const T* const*)peer_tab_, S, Tt, H, cec_, slot_prow_, (T*)mlp_in_, st);
-            launch_zero_pad_rows<T>((T*)mlp_in_, prow_src_, p_total, H, pmax_, st);
-            launches_ += 2;
-        }
-    } else if (!tma_gather) {
+        launch_ep_gather_pull<T>((const T* const*)peer_tab_, S, Tt, H, cec_, slot_prow_, (T*)mlp_in_, st);
+        launch_zero_pad_rows<T>((T*)mlp_in_, prow_src_, p_total, H, pmax_, st);
+        launches_ += 2;
+    } else {
         launch_gather_rows<T>(x, prow_src_, p_total, (T*)mlp_in_, H, pmax_, st);
         launches_ += 1;
     }
@@ -585,42 +505,16 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
         ga.counts = token_counts_;
         ga.num_sms = ctx_.num_sms;
         ga.kind = GemmKind::FwdGateUp;
-        ga.x = tma_gather ? (const void*)x : mlp_in_;
-        ga.gather_rows = tma_gather ? prow_src_ : nullptr;
-        ga.gather_tokens = S;
+        ga.x = mlp_in_;
         ga.wg = gate;
         ga.wu = up;
         ga.out0 = g_;
         ga.out1 = u_;
         ga.out2 = h_;
-        if (E > 1 && fused_pull()) set_pull_args(ga, (const void* const*)peer_tab_, mlp_in_, S, K, Tt);
-        const bool opull = E > 1 && !fused_pull() && overlap_pull();
-        if (opull) {  // the pull kernel beside the GEMM, on the side stream
-            ga.ready = ready_;
-            ga.tile_order = tile_order_;
-            B2_CUDA(cudaEventRecord(ev_fork_, st));
-            B2_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
-            launch_ep_pull_rows((const void* const*)peer_tab_, S, E, ctx_.coord_ep, H, cec_, slot_prow_, mlp_in_,
-                                ready_, ctx_.num_sms, side_);
-            B2_CUDA(cudaEventRecord(ev_join_, side_));
-            launches_ += 1;
-        }
         mark(kGemmGateUp, false);
         launch_sm100_gemm(ga, st);
         mark(kGemmGateUp, true);
-        if (opull) B2_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
-        ga.ready = nullptr;
-        ga.tile_order = nullptr;
         ga.kind = GemmKind::FwdDown;
-        ga.gather_rows = nullptr;
-        if (fused_combine()) {  // w * y rows go straight into the sources' slabs over NVLink
-            ga.peer_kslab = (void* const*)peer_tab_ + 5 * E;
-            ga.prow_src = prow_src_;
-            ga.prow_k = prow_k_;
-            ga.gw = gw_;
-            ga.ep_S = S;
-            ga.ep_K = K;
-        }
         ga.h = h_;
         ga.wd = down;
         ga.out0 = y_;
@@ -672,12 +566,7 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     }
     // stage 5: weighted combine (377); EP = 1 so the reducescatter (378) is the identity
     mark(kCombine, false);
-    if (E > 1 && fused_combine()) {
-        // the FwdDown epilogue already stored every (t, k) row w * y into the source's slab
-        ep_barrier();
-        launch_kslab_sum<T>((const T*)kslab_, S, K, H, out, st);
-        launches_ += 1;
-    } else if (E > 1) {
+    if (E > 1) {
         // each owner combines its slots into its OWN slab row [gid]; after the barrier the
         // source pulls its rows from the owners and sums them in rank order
         launch_ep_combine_local<T>((const T*)y_, slot_prow_, selected_k_, cec_, gw_, K, S, Tt, H, (T*)ret_f_, st);
@@ -745,17 +634,10 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
     }
     // EP > 1: the top-k weight gradients go straight into this rank's symmetric slab, where
     // the sources pull them from
-    const bool fpull = E > 1 && fused_pull();
-    if (fpull) {  // the dgrad GEMM pulls dout and forms dY / the weight-gradient dots itself
-        launch_zero_pad_rows<T>((T*)dy_, prow_src_, p_total, H, pmax_, st);
-        B2_CUDA(cudaMemsetAsync(ready_, 0, 4 * (size_t)(pmax_ / 128 + 1), st));
-        launches_ += 1;
-    } else {
-        launch_out_reduction_bwd<T>(dout, peer_dout, S, (const T*)y_, slot_prow_, selected_k_, cec_, gw_, (T*)dy_,
-                                    E > 1 ? wret_ : wgrad_, Tt, H, K, st);
-        launch_zero_pad_rows<T>((T*)dy_, prow_src_, p_total, H, pmax_, st);
-        launches_ += 2;
-    }
+    launch_out_reduction_bwd<T>(dout, peer_dout, S, (const T*)y_, slot_prow_, selected_k_, cec_, gw_, (T*)dy_,
+                                E > 1 ? wret_ : wgrad_, Tt, H, K, st);
+    launch_zero_pad_rows<T>((T*)dy_, prow_src_, p_total, H, pmax_, st);
+    launches_ += 2;
     mark(kOutRedBwd, true);
     if (dtype_ == BF16) {
         Sm100GemmArgs ga{};
@@ -778,18 +660,9 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         ga.scale = inv_ep;
         ga.kind = GemmKind::BwdDownDgrad;  // 406 + silu_glu_backward 409
         ga.out0 = dgu_;
-        if (fpull) {
-            set_pull_args(ga, (const void* const*)peer_tab_ + E, dy_, S, K, Tt);
-            ga.pull_selk = selected_k_;
-            ga.pull_gw = gw_;
-            ga.pull_y = y_;
-            ga.pull_wgrad = wret_;
-        }
         mark(kGemmDgrad, false);
         launch_sm100_gemm(ga, st);
         mark(kGemmDgrad, true);
-        ga.ready = nullptr;
-        ga.tile_order = nullptr;
         if (overlap_return()) {
             // EP > 1: dX first, then its return to the source ranks (owner combine, barrier,
             // NVLink pull-sums: the reducescatters of moe.hpp:427-428) runs on a side stream
@@ -803,12 +676,7 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
             B2_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
             // side-stream grids capped to the reserved SMs (8 resident 256-thread blocks each), so
             // they never hold SMs the weight-gradient GEMM's CTAs are waiting for
-            // (B2_EP_SIDE_CAP=0: uncapped grids)
-            static const bool side_cap_on = [] {
-                const char* e = getenv("B2_EP_SIDE_CAP");
-                return !(e && atoi(e) == 0);
-            }();
-            const int side_cap = side_cap_on ? comm_sms_ * 8 : 0;
+            const int side_cap = kCommSms * 8;
             launch_ep_combine_local<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, K, S, Tt, H,
                                        (T*)ret_b_, side_, side_cap);
             ep_barrier(side_);
@@ -817,7 +685,7 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
             launch_ep_pull_sum<float>((const float* const*)peer_tab_ + 4 * E, gi_local_, S, K, E, nr, K,
                                       ctx_.coord_ep, wgrad_local_, side_, side_cap);
             B2_CUDA(cudaEventRecord(ev_join_, side_));
-            ga.max_ctas = ctx_.num_sms - comm_sms_;
+            ga.max_ctas = ctx_.num_sms - kCommSms;
         }
         ga.kind = GemmKind::WgradDown;  // 407
         ga.out0 = ddown;
@@ -825,11 +693,6 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         launch_sm100_gemm(ga, st);
         mark(kGemmWgradDown, true);
         ga.kind = GemmKind::WgradGateUp;  // 410-413
-        if (gather_in_gemm()) {  // X^T gathered from the caller's x (kept alive since forward)
-            ga.x = x_;
-            ga.gather_rows = prow_src_;
-            ga.gather_tokens = S;
-        }
         ga.out0 = dgate;
         ga.out1 = dup;
         mark(kGemmWgradGateUp, false);
@@ -841,16 +704,6 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
             launches_ += 4 + 4;
         } else {
             ga.kind = GemmKind::BwdDx;  // 414-415
-            ga.gather_rows = nullptr;
-            ga.x = mlp_in_;
-            if (fused_combine()) {  // dX rows go straight into the sources' slabs over NVLink
-                ga.peer_kslab = (void* const*)peer_tab_ + 5 * E;
-                ga.prow_src = prow_src_;
-                ga.prow_k = prow_k_;
-                ga.gw = nullptr;
-                ga.ep_S = S;
-                ga.ep_K = K;
-            }
             ga.out0 = dxp_;
             mark(kGemmDx, false);
             launch_sm100_gemm(ga, st);
@@ -946,19 +799,15 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         wgrad_local = wgrad_local_;
         dx_rows = (const T*)dx_exp_;
     } else if (E > 1) {
-        // the two reducescatters of moe.hpp:427-428: owners combine dX partials into their own slab (the top-k weight gradients already
-        // sit in their own wret, written by the output-reduction backward); after the barrier
-        // each source pulls and sums its rows in rank order
-        if (fused_combine()) {  // the BwdDx epilogue stored every (t, k) dX row into the slab
-            ep_barrier();
-            launch_kslab_sum<T>((const T*)kslab_, S, K, H, (T*)dx_exp_, st);
-        } else {
-            launch_ep_combine_local<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, K, S, Tt, H,
-                                       (T*)ret_b_, st);
-            ep_barrier();
-            launch_ep_pull_sum<T>((const T* const*)peer_tab_ + 3 * E, gi_local_, S, K, E, nr, H, ctx_.coord_ep,
-                                  (T*)dx_exp_, st);
-        }
+        // the two reducescatters of moe.hpp:427-428: owners combine dX partials into their own
+        // slab (the top-k weight gradients already sit in their own wret, written by the
+        // output-reduction backward); after the barrier each source pulls and sums its rows in
+        // rank order
+        launch_ep_combine_local<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, K, S, Tt, H, (T*)ret_b_,
+                                   st);
+        ep_barrier();
+        launch_ep_pull_sum<T>((const T* const*)peer_tab_ + 3 * E, gi_local_, S, K, E, nr, H, ctx_.coord_ep,
+                              (T*)dx_exp_, st);
         launch_ep_pull_sum<float>((const float* const*)peer_tab_ + 4 * E, gi_local_, S, K, E, nr, K, ctx_.coord_ep,
                                   wgrad_local_, st);
         wgrad_local = wgrad_local_;
@@ -989,24 +838,15 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         launch_sm100_gemm(ga, st);
         launch_router_dw_reduce_bf16(dw_part_, drouter, router_dw_splits(S, H, ctx_.num_sms), (int64_t)H * N, st);
         // scatter-add to tokens (418-423), then + matmul_nt(dlogits, router) (454) as a GEMM whose
-        // epilogue adds the scattered rows
-        // EP = 1: a combine kernel sums each token's slot rows of dXperm, the RouterDx epilogue
-        // adds them. Opt-in (B2_ROUTERDX_FUSED=1): the RouterDx epilogue gathers the slot rows
-        // itself — measured slower (5.08-5.12 vs 4.85 ms per step: 148 one-CTA tiles' epilogues
-        // read 512 MB of scattered rows with too few bytes in flight)
-        static const bool fused_dx = [] {
-            const char* e = getenv("B2_ROUTERDX_FUSED");
-            return e && atoi(e) == 1;
-        }();
-        const bool fuse = !dx_rows && fused_dx;
-        if (!dx_rows && !fuse) {
+        // epilogue adds the scattered rows. EP = 1: a combine kernel sums each token's slot rows of
+        // dXperm first (gathering them inside the RouterDx epilogue measured slower: 5.08-5.12 vs
+        // 4.85 ms per step, too few bytes in flight per one-CTA tile)
+        if (!dx_rows) {
             launch_combine<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, dx, S, H, K, st);
             dx_rows = dx;
         }
         ga.kind = GemmKind::RouterDx;
-        ga.cec = fuse ? cec_ : nullptr;
-        ga.slot_prow = slot_prow_;
-        ga.src = fuse ? dxp_ : dx_rows;
+        ga.src = dx_rows;
         ga.out0 = dx;
         launch_sm100_gemm(ga, st);
         launches_ += 5;
@@ -1034,8 +874,24 @@ void MoeLayer::aux_probs_grad(double coeff, float* out) {
     launch_aux_probs_grad(sel_, out, (int)s_, (int)cfg_.n_experts, coeff, total, ctx_.stream);
 }
 
+// count_tokens throws on an expert id outside [0, N) (moe.hpp:143-146). The index kernels flag
+// it on the device without a host sync; the layer's synchronising readbacks (aux loss,
+// artifacts) surface it — the flag is sticky until read, so a bad id in any forward since the
+// last readback (e.g. a corrupt table pulled from a peer at EP > 1) raises here.
+void MoeLayer::check_expert_ids() {
+    int32_t bad = 0;
+    B2_CUDA(cudaMemcpyAsync(&bad, err_, 4, cudaMemcpyDeviceToHost, ctx_.stream));
+    B2_CUDA(cudaStreamSynchronize(ctx_.stream));
+    if (bad) {
+        B2_CUDA(cudaMemsetAsync(err_, 0, 4, ctx_.stream));
+        check(false, "count_tokens: expert id out of range [0," + std::to_string(cfg_.n_experts) +
+                         ") in a routing table of this layer");
+    }
+}
+
 double MoeLayer::aux_loss() {
     check(have_fwd_, "moe_aux_loss: no forward state");
+    check_expert_ids();
     const int N = (int)cfg_.n_experts;
     std::vector<float> mp(N);
     std::vector<int32_t> sel(N);
@@ -1057,6 +913,7 @@ static std::vector<int64_t> d2h_i64(const int32_t* d, int64_t n, cudaStream_t st
 
 MoeLayer::HostArtifacts MoeLayer::artifacts() {
     check(have_fwd_, "artifacts: no forward state");
+    check_expert_ids();
     cudaStream_t st = ctx_.stream;
     const int64_t nr = cfg_.experts_per_rank(), K = cfg_.top_k, tbs = cfg_.token_block;
     HostArtifacts a;

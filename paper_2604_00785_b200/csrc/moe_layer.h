@@ -125,22 +125,10 @@ class MoeLayer {
     // Every data-dependent size lives on the device, so a replay is exact. Profiling
     // runs eagerly.
     void set_graph(bool on);
-    // opt into the TMA tile::gather4 X operand (no materialised mlp_in); off by default
-    void set_tma_gather(bool on) { tma_gather_ = on; }
-    // EP > 1: opt into the GEMM-fused combine instead of the owner-local combine + NVLink pull
-    void set_ce_dispatch(bool on) {
-        ce_dispatch_opt_ = on;
-        set_graph(graph_);
-    }
     void set_overlap_return(bool on) {
         overlap_opt_ = on;
         set_graph(graph_);
     }
-    void set_fused_combine(bool on) {
-        fused_combine_opt_ = on;
-        set_graph(graph_);  // the captured sequences change
-    }
-
   private:
     template <typename T>
     void forward_t(const T* x, const T* router, const T* gate, const T* up, const T* down, bool fur, T* out);
@@ -149,34 +137,8 @@ class MoeLayer {
                     const float* aux_probs_grad, T* dx, T* drouter, T* dgate, T* dup, T* ddown);
 
     void mark(int stage, bool end);
+    void check_expert_ids();  // throws ContractError if an index kernel flagged an id outside [0, N)
     void set_dispatch_tables();
-    bool gather_in_gemm() const;
-    // bf16, EP > 1, opt-in: the FwdDown / BwdDx epilogues store their rows straight into the
-    // source ranks' [K][S][H] slabs over NVLink (GEMM-fused combine). Correct, but measured
-    // slower (7.65 vs 5.32 ms per EP=2 step): each lane's 64-byte remote stores to scattered
-    // rows make the epilogue NVLink-bound; the owner-local combine + coalesced pull is default
-    bool fused_combine() const;
-    // bf16, EP > 1, opt-in (B2_EP_FUSED_PULL=1): the dispatch pull of x rows and the dout pull +
-    // output-reduction backward run inside the FwdGateUp / dgrad GEMM kernels (warps 2-3 of every
-    // CTA), tile by tile ahead of the MMAs that consume them (per-128-row arrival counters, m-tiles
-    // visited by source). Correct (EP parity tests pass under it) but measured slower at EP=2
-    // (6.36 vs 5.29 ms per step): 296 pulling warps keep too few NVLink bytes in flight to feed the
-    // GEMM, which then waits on its rows; the standalone pull kernels (~19k warps) stay default
-    bool fused_pull() const;
-    void set_pull_args(Sm100GemmArgs& ga, const void* const* peer_rows, void* dst, int S, int K, int Tt) const;
-    bool fused_pull_opt_ = false;
-    // bf16, EP > 1, opt-in (B2_EP_OVERLAP_PULL=1): the forward's dispatch pull as a kernel
-    // co-resident with the FwdGateUp GEMM (one 8-warp block per SM beside each GEMM CTA, side
-    // stream), the GEMM waiting on per-block arrival counters. Correct, measured slower at EP=4
-    // (6.19-6.21 vs 6.04-6.06 ms): the pull slows to ~435 GB/s beside the GEMM, below the rate the
-    // GEMM consumes its A rows, and the source-major tile order costs weight locality
-    bool overlap_pull() const;
-    bool overlap_pull_opt_ = false;
-    int32_t *ready_ = nullptr, *tile_bucket_ = nullptr, *tile_order_ = nullptr;
-    int64_t max_mtiles_ = 0;
-    bool fused_combine_opt_ = false;  // bf16, EP = 1, opted in: GEMMs gather X rows by TMA gather4
-    bool tma_gather_ = false;     // off by default: measured 1.9x slower GEMMs (32 TMA ops/stage)
-
     struct GraphCache {
         std::vector<const void*> key;
         int launches = 0;
@@ -215,7 +177,7 @@ class MoeLayer {
     // int32
     int32_t *topi_, *fi_, *sel_, *whist_, *wbase_, *expert_counts_, *cec_, *partial_counts_, *partial_cum_,
         *token_counts_, *ctc_, *pad_start_, *input_indices_, *output_indices_, *selected_k_, *slot_prow_,
-        *prow_src_, *prow_k_, *err_;
+        *prow_src_, *err_;
     const float* gw_ = nullptr;    // dispatch weights (learned or FUR)
     const int32_t* gi_ = nullptr;  // dispatch indices
     // dtype buffers (padded row space)
@@ -228,18 +190,12 @@ class MoeLayer {
     void ep_setup();
     void ep_barrier(cudaStream_t st = nullptr);
     // bf16, EP > 1: the backward returns dX / top-k weight gradients on a side stream while
-    // the weight-gradient GEMMs run on num_sms - comm_sms_ SMs (16: measured best of 16/24/32 at EP=4)
+    // the weight-gradient GEMMs run on num_sms - kCommSms SMs (16: measured best of 16/24/32 at EP=4)
     bool overlap_return() const;
-    int comm_sms_ = 16;  // B2_COMM_SMS overrides (A/B hook)
+    static constexpr int kCommSms = 16;
     bool overlap_opt_ = true;
     cudaStream_t side_ = nullptr;
-    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_xall_ = nullptr;
-    // EP > 1, opt-in: the forward's token exchange as a copy-engine all-gather of x into
-    // x_all_ on the side stream, overlapped with the routing kernels. Measured 1.5 % slower
-    // than the default (owners pull only the rows they need, by SM, after routing) at EP=4
-    bool ce_dispatch_opt_ = false;
-    void* x_all_ = nullptr;
-    size_t x_sh_off_ = 0;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     const int32_t* gi_local_ = nullptr;  // this rank's dispatch table [S,K] (learned or FUR)
     char* sym_ = nullptr;
     std::vector<char*> peer_base_;
@@ -247,7 +203,6 @@ class MoeLayer {
     void** peer_tab_ = nullptr;  // device: tables of E pointers: x, dout, ret_f, ret_b, wret
     void *x_sh_ = nullptr, *dout_sh_ = nullptr, *ret_f_ = nullptr, *ret_b_ = nullptr;
     float* wret_ = nullptr;
-    void* kslab_ = nullptr;
     int* flags_ = nullptr;  // NVLink barrier counters (one per peer), in the symmetric buffer
     int32_t* tab_ids_ = nullptr;  // this rank's published routing table [S,K] (symmetric buffer)
     float* tab_w_ = nullptr;

@@ -29,6 +29,26 @@ void AdamWConfig::validate() const {
     check(warmup_steps >= 0 && total_steps >= warmup_steps, "adamw: need 0 <= warmup_steps <= total_steps");
 }
 
+MemoryReport memory_report(int64_t p_expert, int64_t p_non_expert, int mode, int dp, int ep, double capacity_gb) {
+    check(p_expert >= 0 && p_non_expert >= 0, "memory_report: negative parameter count");
+    check(dp >= 1 && ep >= 1, "memory_report: bad group sizes");
+    check(mode >= 0 && mode <= 2, "memory_report: unknown shard mode");
+    const double p = (double)(p_expert + p_non_expert);
+    MemoryReport r;
+    r.weights_bytes = 2.0 * p;
+    r.grads_bytes = 2.0 * p;
+    // owned fraction of the fp32 state per class: DDP everything, SO 1/DP, EPSO expert 1/DP and
+    // non-expert 1/(DP x EP)
+    const double se = mode == 0 ? 1.0 : 1.0 / dp;
+    const double sn = mode == 0 ? 1.0 : mode == 1 ? 1.0 / dp : 1.0 / ((double)dp * ep);
+    r.master_bytes = 4.0 * ((double)p_expert * se + (double)p_non_expert * sn);
+    r.optim_bytes = 2.0 * r.master_bytes;
+    r.total_bytes = r.weights_bytes + r.grads_bytes + r.master_bytes + r.optim_bytes;
+    r.capacity_bytes = capacity_gb * 1e9;
+    r.feasible = r.total_bytes <= r.capacity_bytes;
+    return r;
+}
+
 double lr_at_step(int64_t step, const AdamWConfig& cfg) {
     check(step >= 0, "lr_at_step: negative step");
     if (step < cfg.warmup_steps) return cfg.peak_lr * (double)step / (double)cfg.warmup_steps;
@@ -167,45 +187,10 @@ ShardedOptimizer::ShardedOptimizer(Context& ctx, const AdamWConfig& cfg, std::ve
     up(ids_pre_norm_, pre_norm.data(), 4 * pre_norm.size());
     up(ids_local_, loc.data(), 4 * loc.size());
     up(ids_pre_, pre.data(), 4 * pre.size());
-    {  // buckets over the synced params, in param order (ids_pre_ is param-ordered)
-        // split by the parameters' full sizes (identical on every rank, so every member groups its
-        // all-gathers the same way), not by the owned slices (the last member holds the remainder)
-        int64_t total = 0;
-        for (size_t i = 0; i < params_.size(); ++i)
-            if (pre_[i]) total += params_[i].numel;
-        // A/B hook B2_OPT_BUCKETS=n: n buckets, each all-gather overlapping the next update (the
-        // update then leaves 16 SMs to NCCL). Measured at DP x EP = 4 x 1 / 1 x 4: 42.2-42.9 /
-        // 12.2-13.5 ms with 4-8 buckets vs 41.8-42.0 / 12.1-12.2 ms with one — the concurrent
-        // all-gather and the HBM-bound update slow each other down — so one bucket is the default
-        const char* env = getenv("B2_OPT_BUCKETS");
-        const int nb = std::max(1, env ? atoi(env) : 1);
-        const int64_t per = std::max<int64_t>(1, ceil_div(std::max<int64_t>(total, 1), nb));
-        Bucket cur;
-        int64_t acc = 0;
-        int id = 0;
-        for (size_t i = 0; i < params_.size(); ++i) {
-            if (!pre_[i]) continue;
-            const int64_t n = plan_[i].own_e - plan_[i].own_b;
-            const int nch = (int)ceil_div(n, kOptChunk);
-            cur.params.push_back((int)i);
-            id += nch;
-            acc += params_[i].numel;
-            cur.id1 = id;
-            if (acc >= per) {
-                buckets_.push_back(cur);
-                cur = Bucket{};
-                cur.id0 = cur.id1 = id;
-                acc = 0;
-            }
-        }
-        if (!cur.params.empty()) buckets_.push_back(cur);
-        check(buckets_.empty() || buckets_.back().id1 == n_pre_, "optimizer: bucket ranges do not cover the synced chunks");
-        for (Bucket& b : buckets_) B2_CUDA(cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming));
-    }
     // partials of chunks that do not count toward the norm stay zero
     B2_CUDA(cudaMemsetAsync(partials_, 0, 8 * (size_t)(n_chunks_ + 1), ctx_.stream));
     B2_CUDA(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking));
-    for (cudaEvent_t* ev : {&ev_start_, &ev_synced_, &ev_pre_done_, &ev_ag_})
+    for (cudaEvent_t* ev : {&ev_start_, &ev_synced_, &ev_pre_done_, &ev_ag_, &ev_pre_updated_})
         B2_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     B2_CUDA(cudaStreamSynchronize(ctx_.stream));
 }
@@ -216,9 +201,7 @@ ShardedOptimizer::~ShardedOptimizer() {
         cudaStreamSynchronize(comm_stream_);
         cudaStreamDestroy(comm_stream_);
     }
-    for (Bucket& b : buckets_)
-        if (b.ev) cudaEventDestroy(b.ev);
-    for (cudaEvent_t ev : {ev_start_, ev_synced_, ev_pre_done_, ev_ag_})
+    for (cudaEvent_t ev : {ev_start_, ev_synced_, ev_pre_done_, ev_ag_, ev_pre_updated_})
         if (ev) cudaEventDestroy(ev);
 }
 
@@ -313,34 +296,33 @@ StepStats ShardedOptimizer::step(bool want_stats) {
     a.grad_dtype = gdt_;
     a.weight_dtype = wdt_;
     a.round_bf16 = cfg_.round_weights_bf16 ? 1 : 0;
-    // 4. re-share the updated slices (optim.cpp:185-190) on the comm stream: bucket by bucket,
-    // each all-gather overlapping the next bucket's update and, after the last, the update of
-    // the local (expert) slices
-    bool any_ag = false;
+    // 4. re-share the updated slices (optim.cpp:185-190) on the comm stream, overlapped with the
+    // update of the local (expert) slices. (Bucketing the synced update so each bucket's all-gather
+    // overlaps the next bucket's update measured slower at DP x EP = 4 x 1 and 1 x 4: 42.2-42.9 /
+    // 12.2-13.5 vs 41.8-42.0 / 12.1-12.2 ms — the all-gather and the HBM-bound update slow each
+    // other down.)
     const bool reshare = mode_ != ShardMode::ddp && any_pre;
-    // with more than one bucket the update leaves SMs to the concurrent all-gathers' kernels
-    const int reserve = reshare && buckets_.size() > 1 ? kCommSMs : 0;
-    for (const Bucket& bk : buckets_) {
-        launch_adamw_chunks(segs_, chunks_, ids_pre_ + bk.id0, bk.id1 - bk.id0, a, norm_sq_, nonfinite_, st, reserve);
-        launches_ += bk.id1 > bk.id0;
-        if (!reshare) continue;
-        B2_CUDA(cudaEventRecord(bk.ev, st));
-        B2_CUDA(cudaStreamWaitEvent(cs, bk.ev, 0));
+    launch_adamw_chunks(segs_, chunks_, ids_pre_, n_pre_, a, norm_sq_, st);
+    launches_ += n_pre_ > 0;
+    if (reshare) {
+        B2_CUDA(cudaEventRecord(ev_pre_updated_, st));
+        B2_CUDA(cudaStreamWaitEvent(cs, ev_pre_updated_, 0));
         bool grp = false;
-        for (int i : bk.params) {
-            const Entry& e = plan_[(size_t)i];
+        for (size_t i = 0; i < params_.size(); ++i) {
+            if (!pre_[i]) continue;
+            const Entry& e = plan_[i];
             const int gsize = e.over_dp_ep ? ctx_.dp * ctx_.ep : ctx_.dp;
             if (gsize <= 1) continue;
             if (!grp) B2_NCCL(ncclGroupStart());
-            all_gather_v(*group_of(e), params_[(size_t)i].weight, params_[(size_t)i].numel, wdt_, cs);
-            grp = any_ag = true;
+            all_gather_v(*group_of(e), params_[i].weight, params_[i].numel, wdt_, cs);
+            grp = true;
         }
         if (grp) B2_NCCL(ncclGroupEnd());
     }
     if (reshare) B2_CUDA(cudaEventRecord(ev_ag_, cs));
-    launch_adamw_chunks(segs_, chunks_, ids_local_, n_local_, a, norm_sq_, nonfinite_, st);
+    launch_adamw_chunks(segs_, chunks_, ids_local_, n_local_, a, norm_sq_, st);
     launches_ += n_local_ > 0;
-    if (any_ag || (mode_ != ShardMode::ddp && any_pre)) B2_CUDA(cudaStreamWaitEvent(st, ev_ag_, 0));
+    if (reshare) B2_CUDA(cudaStreamWaitEvent(st, ev_ag_, 0));
     if (want_stats) {
         double sq = 0;
         int32_t bad = 0;

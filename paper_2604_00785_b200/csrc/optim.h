@@ -21,6 +21,14 @@ struct AdamWConfig {  // optim.hpp:11-25
 
 double lr_at_step(int64_t step, const AdamWConfig& cfg);
 void shard_slice(int64_t numel, int group_size, int position, int64_t* begin, int64_t* end);
+// memory_report (optim.cpp:196-221): the 16P-per-parameter footprint (bf16 weights and grads,
+// fp32 master + two moments divided over the owning group) against a device capacity
+struct MemoryReport {
+    double weights_bytes = 0, grads_bytes = 0, master_bytes = 0, optim_bytes = 0;
+    double total_bytes = 0, capacity_bytes = 0;
+    bool feasible = true;
+};
+MemoryReport memory_report(int64_t p_expert, int64_t p_non_expert, int mode, int dp, int ep, double capacity_gb);
 
 enum class ShardMode { ddp = 0, so = 1, epso = 2 };
 
@@ -35,7 +43,7 @@ struct ParamSlot {
 struct StepStats {
     int64_t step = 0;
     double lr = 0, grad_norm = 0, clip_scale = 1.0;
-    int nonfinite = 0;  // a synced grad held NaN/Inf: the update was skipped on the device
+    int nonfinite = 0;  // a grad held NaN/Inf (the fused scan); the update was applied, as the reference's
 };
 
 class ShardedOptimizer {
@@ -100,15 +108,7 @@ class ShardedOptimizer {
     std::vector<char> pre_;  // param needs a collective before its update
     cudaStream_t comm_stream_ = nullptr;
     cudaEvent_t ev_start_ = nullptr, ev_synced_ = nullptr, ev_pre_done_ = nullptr, ev_ag_ = nullptr;
-    // the synced parameters' update + re-share in buckets (consecutive params, ~equal owned
-    // elements): bucket b's all-gather on the comm stream overlaps bucket b+1's update
-    struct Bucket {
-        int id0 = 0, id1 = 0;     // range in ids_pre_
-        std::vector<int> params;  // params whose re-share follows this bucket's update
-        cudaEvent_t ev = nullptr;
-    };
-    std::vector<Bucket> buckets_;
-    static constexpr int kCommSMs = 16;
+    cudaEvent_t ev_pre_updated_ = nullptr;  // the synced parameters' update is done: re-share
     int64_t step_count_ = 0;
     int launches_ = 0;
 };

@@ -11,7 +11,6 @@
 // the same strict '>' (ties to the lower expert index). Given identical scores the
 // selections are bit-exact.
 #include <cstdlib>
-#include <string>
 
 #include "b2_common.cuh"
 #include "kernels.h"
@@ -151,22 +150,6 @@ __global__ void __launch_bounds__(128) router_logits_kernel(const T* __restrict_
     }
 }
 
-// ---- logits, bf16 inputs: cp.async ring + fp32 staging, token-paired f32x2 FMA --------
-// 64 tokens x 64 experts per CTA (128 threads), 32-deep p chunks. Raw bf16 tiles land
-// through a 4-stage cp.async ring; each chunk is widened once into fp32 staging
-// buffers (x transposed to [p][token], W duplicated to (w, w) pairs) so that the inner
-// loop is 4 conflict-free 128-bit shared loads per 16 fma.rn.f32x2 — each FMA pairs
-// two TOKENS against one expert weight. bf16 x bf16 products are exact in fp32, so every
-// accumulator is bit-identical to the reference's sequential multiply-then-add.
-// Thread tile: 8 tokens (ty = lane/4) x 4 experts (16*warp + 4*(lane%4)).
-constexpr int kL2Tok = 64, kL2Exp = 64, kL2P = 32, kL2Stages = 4;
-struct LogitsSmem {
-    uint16_t xraw[kL2Stages][kL2Tok][kL2P];  // 64 B rows, 16 B units swizzled by (t >> 1) & 3
-    uint16_t wraw[kL2Stages][kL2P][kL2Exp];  // 128 B rows, 16 B units swizzled by p & 7
-    float xs[2][kL2P][kL2Tok];               // token t at (t/4 % 2)*32 + (t/8)*4 + t%4
-    float2 ws[2][kL2P][kL2Exp];              // 16 B units (expert pairs) swizzled by p & 7
-};
-
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
     const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gmem), "r"(valid ? 16 : 0)
@@ -178,142 +161,12 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-__global__ void __launch_bounds__(128) router_logits_bf16_kernel(const __nv_bfloat16* __restrict__ x,
-                                                                 const __nv_bfloat16* __restrict__ w,
-                                                                 float* __restrict__ logits, int S, int H, int N) {
-    pdl_wait();
-    pdl_launch();
-    extern __shared__ __align__(128) uint8_t l2_smem[];
-    LogitsSmem& sm = *reinterpret_cast<LogitsSmem*>(l2_smem);
-    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
-    const int t0 = blockIdx.x * kL2Tok, e0 = blockIdx.y * kL2Exp;
-    const int nchunks = H / kL2P;
-
-    auto issue = [&](int c) {
-        if (c < nchunks) {
-            const int s = c % kL2Stages, p0 = c * kL2P;
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {  // x: 64 rows x 4 units
-                const int idx = tid + 128 * q, t = idx / 4, u = idx % 4;
-                const bool ok = t0 + t < S;
-                const __nv_bfloat16* src = x + (int64_t)(ok ? t0 + t : 0) * H + p0 + 8 * u;
-                cp_async16(&sm.xraw[s][t][8 * (u ^ ((t >> 1) & 3))], src, ok);
-            }
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {  // W: 32 rows x 8 units
-                const int idx = tid + 128 * q, pp = idx / 8, u = idx % 8;
-                const bool ok = e0 + 8 * u < N;
-                const __nv_bfloat16* src = w + (int64_t)(p0 + pp) * N + (ok ? e0 + 8 * u : 0);
-                cp_async16(&sm.wraw[s][pp][8 * (u ^ (pp & 7))], src, ok);
-            }
-        }
-        cp_async_commit();
-    };
-    auto widen = [&](int c) {
-        const int s = c % kL2Stages, b = c & 1;
-        {  // x: thread = token (tid % 64), 2 units of 8 p
-            const int t = tid % 64, ub = (tid / 64) * 2;
-            const int pos = ((t >> 2) & 1) * 32 + (t >> 3) * 4 + (t & 3);
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                const int u = ub + k;
-                const uint4 r = *reinterpret_cast<const uint4*>(&sm.xraw[s][t][8 * (u ^ ((t >> 1) & 3))]);
-                const uint32_t v[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    sm.xs[b][8 * u + 2 * j][pos] = __uint_as_float(v[j] << 16);
-                    sm.xs[b][8 * u + 2 * j + 1][pos] = __uint_as_float(v[j] & 0xFFFF0000u);
-                }
-            }
-        }
-        {  // W: thread = (row p, 2 units of 8 experts) -> 8 duplicated pairs per unit
-            const int pp = tid / 4;
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                const int u = (tid % 4) * 2 + k;
-                const uint4 r = *reinterpret_cast<const uint4*>(&sm.wraw[s][pp][8 * (u ^ (pp & 7))]);
-                const uint32_t v[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const float lo = __uint_as_float(v[j] << 16), hi = __uint_as_float(v[j] & 0xFFFF0000u);
-                    const int unit = (4 * u + j) ^ (pp & 7);  // experts 8u+2j, 8u+2j+1
-                    *reinterpret_cast<float4*>(&sm.ws[b][pp][2 * unit]) = make_float4(lo, lo, hi, hi);
-                }
-            }
-        }
-    };
-
-    float2 acc[4][4];  // [token pair][expert]
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
-
-#pragma unroll
-    for (int c = 0; c < kL2Stages; ++c) issue(c);
-    cp_async_wait<kL2Stages - 1>();
-    __syncthreads();
-    widen(0);
-    const int ty = lane / 4, tx = lane % 4;
-    const int unit0 = 8 * warp + 2 * tx;  // this thread's first expert pair (experts 16w + 4tx, +1)
-    for (int c = 0; c < nchunks; ++c) {
-        cp_async_wait<kL2Stages - 2>();
-        __syncthreads();  // chunk c widened; chunk c+1 landed; staging c+1 and ring slot c free
-        if (c + 1 < nchunks) widen(c + 1);
-        issue(c + kL2Stages);
-        const int b = c & 1;
-        // operands of step pp+1 are loaded while step pp's 16 FMAs issue (explicit register
-        // double-buffering: ~2 warps per scheduler cannot hide the shared-load latency alone)
-        float4 op[2][4];
-        auto ld = [&](float4 (&o)[4], int pp) {
-            o[0] = *reinterpret_cast<const float4*>(&sm.xs[b][pp][ty * 4]);
-            o[1] = *reinterpret_cast<const float4*>(&sm.xs[b][pp][32 + ty * 4]);
-            o[2] = *reinterpret_cast<const float4*>(&sm.ws[b][pp][2 * (unit0 ^ (pp & 7))]);
-            o[3] = *reinterpret_cast<const float4*>(&sm.ws[b][pp][2 * ((unit0 + 1) ^ (pp & 7))]);
-        };
-        ld(op[0], 0);
-#pragma unroll
-        for (int pp = 0; pp < kL2P; ++pp) {
-            if (pp + 1 < kL2P) ld(op[(pp + 1) & 1], pp + 1);
-            const float4 a0 = op[pp & 1][0], a1 = op[pp & 1][1], b0 = op[pp & 1][2], b1 = op[pp & 1][3];
-            const float2 ap[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w), make_float2(a1.x, a1.y),
-                                  make_float2(a1.z, a1.w)};
-            const float2 bp[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
-                                  make_float2(b1.z, b1.w)};
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = __ffma2_rn(ap[i], bp[j], acc[i][j]);
-        }
-    }
-    // token pair i: tokens ty*8 + {0,1,2,3,4,5,6,7} as (0,1) (2,3) (4,5) (6,7)
-    const int e = e0 + 16 * warp + 4 * tx;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int t = t0 + ty * 8 + 2 * i + h;
-            if (t >= S) continue;
-            const float o[4] = {h ? acc[i][0].y : acc[i][0].x, h ? acc[i][1].y : acc[i][1].x,
-                                h ? acc[i][2].y : acc[i][2].x, h ? acc[i][3].y : acc[i][3].x};
-            float* dst = logits + (int64_t)t * N + e;
-            if (e + 3 < N && (N % 4) == 0) {
-                *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
-            } else {
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (e + j < N) dst[j] = o[j];
-            }
-        }
-    }
-}
-
 // ---- logits, bf16 inputs, 8 x 8 register tiles ----------------------------------------
 // One warp per CTA, 32 tokens x 64 experts; each lane owns 8 tokens x 8 experts (64 fp32
 // accumulators as 32 float2). Per p step a lane loads its 8 x values and 8 W values (4
 // conflict-free 128-bit shared loads), duplicates each x into an (x, x) pair in registers and
-// issues 32 fma.rn.f32x2 that pair two EXPERTS against one token: 2x the FMAs per shared byte
-// of the token-paired kernel above, whose 4 loads feed 16 FMA pairs. The order of every
+// issues 32 fma.rn.f32x2 that pair two EXPERTS against one token (2x the FMAs per shared byte
+// of a token-paired 8 x 4 tile, measured 158 -> 122 us at config B). The order of every
 // accumulator is still p = 0, 1, ... with one rounding per step, and bf16 x bf16 products are
 // exact in fp32, so the logits stay bit-identical to the reference's multiply-then-add.
 constexpr int kL3Tok = 32, kL3Exp = 64, kL3P = 32, kL3Stages = 4;
@@ -782,12 +635,7 @@ template <typename T>
 void launch_router_logits(const T* x, const T* w, float* logits, int S, int H, int N, cudaStream_t st) {
     if (S == 0) return;
     if constexpr (sizeof(T) == 2) {
-        static int impl = -1;  // B2_LOGITS_IMPL=t42: the token-paired 8 x 4 kernel (A/B hook)
-        if (impl < 0) {
-            const char* env = getenv("B2_LOGITS_IMPL");
-            impl = env && std::string(env) == "t42" ? 0 : 1;
-        }
-        if (impl == 1 && H % kL3P == 0 && N % 8 == 0 && ((uintptr_t)x & 15) == 0 && ((uintptr_t)w & 15) == 0) {
+        if (H % kL3P == 0 && N % 8 == 0 && ((uintptr_t)x & 15) == 0 && ((uintptr_t)w & 15) == 0) {
             static bool attr3 = false;
             if (!attr3) {
                 B2_CUDA(cudaFuncSetAttribute(router_logits_bf16_t88_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -796,18 +644,6 @@ void launch_router_logits(const T* x, const T* w, float* logits, int S, int H, i
             }
             dim3 grid((unsigned)ceil_div(S, kL3Tok), (unsigned)ceil_div(N, kL3Exp));
             launch_k(router_logits_bf16_t88_kernel, dim3(grid), dim3(32), sizeof(Logits3Smem), st, x, w, logits, S, H, N);
-            B2_LAUNCH_CHECK();
-            return;
-        }
-        if (H % kL2P == 0 && N % 8 == 0 && ((uintptr_t)x & 15) == 0 && ((uintptr_t)w & 15) == 0) {
-            static bool attr = false;
-            if (!attr) {
-                B2_CUDA(cudaFuncSetAttribute(router_logits_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)sizeof(LogitsSmem)));
-                attr = true;
-            }
-            dim3 grid((unsigned)ceil_div(S, kL2Tok), (unsigned)ceil_div(N, kL2Exp));
-            launch_k(router_logits_bf16_kernel, dim3(grid), dim3(128), sizeof(LogitsSmem), st, x, w, logits, S, H, N);
             B2_LAUNCH_CHECK();
             return;
         }

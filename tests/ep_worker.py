@@ -40,8 +40,7 @@ def run(rank, world, port, case, result_path):
     ids = [b2.Context.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(ids, src=0)
     c = dict(case)
-    ckpt, graph, fused = c.pop("ckpt", False), c.pop("graph", False), c.pop("fused", False)
-    ce = c.pop("ce", False)
+    ckpt, graph, no_overlap = c.pop("ckpt", False), c.pop("graph", False), c.pop("no_overlap", False)
     stream = torch.cuda.Stream() if graph else None  # graph capture needs a non-default stream
     if stream is not None:
         torch.cuda.set_stream(stream)
@@ -69,14 +68,10 @@ def run(rank, world, port, case, result_path):
     X, DO = tt(x[sl]), tt(dout[sl])
     R, G, U, D = tt(router), tt(gate[el]), tt(up[el]), tt(down[el])
     layer = b2.MoeLayer(ctx, bcfg, dtype, s, checkpoint=ckpt)
-    if ce:  # the opt-in copy-engine all-gather dispatch
+    if no_overlap:  # dX return after the weight-gradient GEMMs (the fp32 path's order)
         import ctypes
-        b2.lib().b2x_moe_set_ce_dispatch.argtypes = [ctypes.c_void_p, ctypes.c_int]
-        b2.lib().b2x_moe_set_ce_dispatch(layer.h, 1)
-    if fused:  # the opt-in GEMM-fused combine (epilogue stores into the sources' slabs)
-        import ctypes
-        b2.lib().b2x_moe_set_fused_combine.argtypes = [ctypes.c_void_p, ctypes.c_int]
-        b2.lib().b2x_moe_set_fused_combine(layer.h, 1)
+        b2.lib().b2x_moe_set_overlap_return.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        assert b2.lib().b2x_moe_set_overlap_return(layer.h, 0) == 0
     reps = 3 if graph else 1  # eager, capture, replay: the last one is checked
     if graph:
         layer.set_graph(True)

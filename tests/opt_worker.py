@@ -5,6 +5,8 @@ EP and DP x EP communicators) on its own synthetic gradients; rank 0 compares ev
 rank's final weights, fp32 masters, moments and step statistics with the oracle's
 ShardedOptimizer world (oracle/moe_oracle.c, pinned bitwise to optim.cpp:109-194).
 fp32 grads keep NCCL's sums of two members exact, so 2-member groups are bitwise.
+bf16=1: the benchmarked path — bf16 weights and grads on the GPU (NCCL reduce-scatters the bf16
+grads) against the oracle's fp32 sums of the same bf16-rounded values (optim.cpp:148-156).
 """
 import json
 import os
@@ -19,7 +21,7 @@ NUMEL = [33, 30, 7, 1029]
 CLS = [0, 1, 0, 1]
 
 
-def run(rank, world, port, dp, ep, mode, result_path):
+def run(rank, world, port, dp, ep, mode, result_path, bf16=False):
     import torch
     import torch.distributed as dist
 
@@ -45,10 +47,14 @@ def run(rank, world, port, dp, ep, mode, result_path):
             w0[r, off:off + n] = orc.normal((n,), 402 + p, 100 + e if c else 1, 0.05)
             off += n
     grads = (rng.standard_normal((steps, world, total)) * 0.5).astype(np.float32)
+    wdt = torch.bfloat16 if bf16 else torch.float32
+    if bf16:  # both sides see the same bf16 values
+        rb = lambda a: torch.from_numpy(a).bfloat16().float().numpy()
+        w0, grads = rb(w0), rb(grads)
     cfg = b2.AdamWConfig(warmup_steps=2, total_steps=100, peak_lr=1e-2, min_lr=1e-3)
     dev = torch.device("cuda", rank)
-    W = torch.from_numpy(w0[rank].copy()).to(dev)
-    G = torch.zeros(total, dtype=torch.float32, device=dev)
+    W = torch.from_numpy(w0[rank].copy()).to(dev).to(wdt)
+    G = torch.zeros(total, dtype=wdt, device=dev)
     params, off = [], 0
     for n, c in zip(NUMEL, CLS):
         params.append((W[off:off + n], G[off:off + n], c, 0))
@@ -56,14 +62,14 @@ def run(rank, world, port, dp, ep, mode, result_path):
     opt = b2.ShardedOptimizer(ctx, cfg, params, mode)
     stats = []
     for s in range(steps):
-        G.copy_(torch.from_numpy(grads[s, rank]))
+        G.copy_(torch.from_numpy(grads[s, rank]).to(wdt))
         st = opt.step(stats=True)
         stats.append([st["lr"], st["grad_norm"], st["clip_scale"]])
     torch.cuda.synchronize()
     # checkpoint assembly: every member's full state must equal the members' owned slices
     # stitched together (each rank checks its own view against the oracle's per-rank slices)
     full = [opt.gather_state(p, n) for p, n in enumerate(NUMEL)]
-    mine = {"w": W.cpu().numpy().tolist(), "stats": stats, "sb": opt.state_bytes(),
+    mine = {"w": W.float().cpu().numpy().tolist(), "stats": stats, "sb": opt.state_bytes(),
             "full_master": [f[0].tolist() for f in full], "owned": [list(opt.owned(p)) for p in range(len(NUMEL))],
             "master": [opt.state(p)[0].tolist() for p in range(len(NUMEL))],
             "m": [opt.state(p)[1].tolist() for p in range(len(NUMEL))],
@@ -71,6 +77,8 @@ def run(rank, world, port, dp, ep, mode, result_path):
     # record-file checkpoint round trip (reliability.cpp:402-460 / 623-675): write the shard
     # files, restore into a fresh optimizer, then one more identical step on both
     ck = os.path.join(os.path.dirname(result_path), "ckpt")
+    if bf16:  # the shard-file round trip is covered by the fp32 runs
+        return finish(rank, world, dp, ep, mode, result_path, orc, mine, grads, w0, opt, ctx, dist, bf16)
     if rank == 0:
         os.makedirs(ck, exist_ok=True)
     dist.barrier()
@@ -114,13 +122,19 @@ def run(rank, world, port, dp, ep, mode, result_path):
     mine["ckpt_ok"] = all(detail.values())
     mine["ckpt_detail"] = detail
     opt2.close()
+    return finish(rank, world, dp, ep, mode, result_path, orc, mine, grads, w0, opt, ctx, dist, bf16)
+
+
+def finish(rank, world, dp, ep, mode, result_path, orc, mine, grads, w0, opt, ctx, dist, bf16):
+    mine.setdefault("ckpt_ok", True)
+    mine.setdefault("ckpt_detail", {})
     gathered = [None] * world
     dist.all_gather_object(gathered, mine)
     if rank == 0:
         ocfg = orc.adamw_cfg(warmup_steps=2, total_steps=100, peak_lr=1e-2, min_lr=1e-3)
         ref = orc.sharded_steps(dp, ep, 1, mode, ocfg, NUMEL, CLS, [0] * len(NUMEL), w0, grads)
         res = {"weights_equal": True, "state_equal": True, "stats_maxdiff": 0.0, "state_bytes_equal": True,
-               "weights_maxrel": 0.0}
+               "weights_maxrel": 0.0, "state_maxrel": 0.0}
         for r in range(world):
             g = gathered[r]
             wg = np.asarray(g["w"], np.float32)
@@ -132,8 +146,11 @@ def run(rank, world, port, dp, ep, mode, result_path):
                       ("master", "m", "v")]
             n_own = packed[0].size
             for arr, key in zip(packed, ("master", "m", "v")):
-                if not np.array_equal(arr, ref[key][r][:n_own]):
+                want = ref[key][r][:n_own]
+                if not np.array_equal(arr, want):
                     res["state_equal"] = False
+                d = np.abs(arr.astype(np.float64) - want) / np.maximum(1.0, np.abs(want))
+                res["state_maxrel"] = max(res["state_maxrel"], float(d.max()) if d.size else 0.0)
             res["stats_maxdiff"] = max(res["stats_maxdiff"],
                                        float(np.max(np.abs(np.asarray(g["stats"]) - ref["stats"][:, r, :]))))
             if g["sb"] != int(ref["state_bytes"][r]):
@@ -170,4 +187,4 @@ def run(rank, world, port, dp, ep, mode, result_path):
 if __name__ == "__main__":
     rank, world, port = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
     dp, ep, mode = int(sys.argv[4]), int(sys.argv[5]), int(sys.argv[6])
-    run(rank, world, port, dp, ep, mode, sys.argv[7])
+    run(rank, world, port, dp, ep, mode, sys.argv[7], len(sys.argv) > 8 and sys.argv[8] == "1")

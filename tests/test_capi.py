@@ -39,6 +39,29 @@ def test_host_helpers_match_oracle(orc):
         b2.shard_slice(10, 4, 4)
 
 
+def test_memory_report_matches_reference(orc):
+    """memory_report (optim.cpp:196-221): the reference's known answer (7 B params under DDP need
+    112 GB, test_optim.cpp:180-187), the C restatement and — when built — the reference itself,
+    for every mode over DP x EP grids; the Mula-7B-A1B set fits one B200 (180 GB) under EPSO."""
+    r = b2.memory_report(0, 7_000_000_000, 0, 1, 1)
+    assert r["total_bytes"] == 112e9 and not r["feasible"]
+    assert (r["weights_bytes"], r["master_bytes"], r["optim_bytes"]) == (14e9, 28e9, 56e9)
+    z = b2.memory_report(0, 0, 2, 4, 2)
+    assert z["total_bytes"] == 0 and z["feasible"]
+    oracles = [orc]
+    from oracle import bind
+    if bind.have_ref():
+        oracles.append(bind.get("ref"))
+    for mode in (0, 1, 2):
+        for dp, ep in ((1, 1), (2, 1), (1, 8), (2, 4), (4, 2), (8, 1), (3, 5)):
+            got = b2.memory_report(6_442_450_944, 476_645_376, mode, dp, ep, 180.0)
+            for o in oracles:
+                assert got == o.memory_report(6_442_450_944, 476_645_376, mode, dp, ep, 180.0), (mode, dp, ep)
+    assert b2.memory_report(6_442_450_944, 476_645_376, 2, 1, 1, 180.0)["feasible"]
+    with pytest.raises(b2.ContractError):
+        b2.memory_report(-1, 0, 2, 1, 1)
+
+
 def test_lr_rejects_negative_step():
     assert b2.lr_at_step(-1, b2.AdamWConfig()) == -1.0
     assert "negative step" in b2.lib().b2_last_error().decode()

@@ -32,10 +32,8 @@ def run_world(world, case):
     port = free_port()
     with tempfile.TemporaryDirectory() as td:
         res = os.path.join(td, "res.json")
-        case = dict(case)
-        env = dict(os.environ, **case.pop("env", {}))  # opt-in kernel variants (A/B hooks)
         procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "ep_worker.py"), str(r), str(world), str(port),
-                                   json.dumps(case), res], env=env) for r in range(world)]
+                                   json.dumps(case), res]) for r in range(world)]
         for p in procs:
             assert p.wait(timeout=600) == 0
         with open(res) as f:
@@ -51,23 +49,14 @@ CASES = [
     # CUDA-graph capture of the peer-memory path (flag barriers, pulls)
     dict(n_experts=16, top_k=4, hidden=256, intermediate=128, token_block=8, s=300, dtype="bf16", ckpt=True,
          graph=True),
-    dict(n_experts=64, top_k=8, hidden=256, intermediate=128, token_block=8, s=512, dtype="bf16", fused=True),
-    dict(n_experts=16, top_k=4, hidden=256, intermediate=128, token_block=8, s=300, dtype="bf16", ce=True),
-    # opt-in variants: the dispatch / dout pulls fused into the GEMM kernels (captured in graphs),
-    # and the A-operand multicast across two CTA pairs (N tiles pair up at H=512, I=256)
-    dict(n_experts=64, top_k=8, hidden=256, intermediate=128, token_block=8, s=512, dtype="bf16", graph=True,
-         env={"B2_EP_FUSED_PULL": "1"}),
-    dict(n_experts=16, top_k=4, hidden=512, intermediate=256, token_block=8, s=300, dtype="bf16",
-         env={"B2_GEMM_MC": "2"}),
-    dict(n_experts=64, top_k=8, hidden=256, intermediate=128, token_block=8, s=512, dtype="bf16", graph=True,
-         env={"B2_EP_OVERLAP_PULL": "1"}),
+    # the backward's dX return after the weight-gradient GEMMs instead of overlapped with them
+    dict(n_experts=16, top_k=4, hidden=256, intermediate=128, token_block=8, s=300, dtype="bf16", no_overlap=True),
 ]
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c['dtype']}-n{c['n_experts']}k{c['top_k']}"
-                         + ("-ckpt-graph" if c.get("ckpt") else "") + ("-fused" if c.get("fused") else "") + ("-ce" if c.get("ce") else "")
-                         + "".join(f"-{k}={v}" for k, v in c.get("env", {}).items()))
+                         + ("-ckpt-graph" if c.get("ckpt") else "") + ("-serial-return" if c.get("no_overlap") else ""))
 def test_ep_matches_oracle(world, case):
     if case["n_experts"] % world:
         pytest.skip("experts do not divide")
@@ -81,7 +70,7 @@ def test_ep_matches_oracle(world, case):
 
 # ---- EP-aware sharded optimizer across GPUs (NCCL), vs the oracle's ShardedOptimizer world
 
-def run_opt(dp, ep, mode):
+def run_opt(dp, ep, mode, bf16=False):
     world = dp * ep
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
@@ -89,14 +78,16 @@ def run_opt(dp, ep, mode):
     with tempfile.TemporaryDirectory() as td:
         res = os.path.join(td, "res.json")
         procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "opt_worker.py"), str(r), str(world), str(port),
-                                   str(dp), str(ep), str(mode), res]) for r in range(world)]
+                                   str(dp), str(ep), str(mode), res, "1" if bf16 else "0"]) for r in range(world)]
         for p in procs:
             assert p.wait(timeout=600) == 0
         with open(res) as f:
             return json.load(f)
 
 
-@pytest.mark.parametrize("dp,ep,mode", [(2, 1, 0), (2, 1, 1), (2, 1, 2), (1, 2, 1), (1, 2, 2), (2, 2, 2), (2, 2, 1)])
+@pytest.mark.parametrize("dp,ep,mode", [(2, 1, 0), (2, 1, 1), (2, 1, 2), (1, 2, 1), (1, 2, 2), (2, 2, 2), (2, 2, 1),
+                                        # 8-rank grids (comm.cpp:301-361 group layout, optim.cpp:52-72)
+                                        (1, 8, 2), (2, 4, 2), (4, 2, 2), (8, 1, 2), (2, 4, 1)])
 def test_sharded_optimizer_matches_oracle(dp, ep, mode):
     r = run_opt(dp, ep, mode)
     if dp * ep <= 2:  # two-member groups sum exactly: weights, masters and moments are bitwise equal
@@ -108,3 +99,18 @@ def test_sharded_optimizer_matches_oracle(dp, ep, mode):
     assert r.get("ckpt_ok", True), r.get("ckpt_detail")  # shard files written, restored, stepped bitwise
     # grad norm / clip: exact sums at 2 members; NCCL's 4-member fp32 order moves the last bits
     assert r["stats_maxdiff"] <= (1e-9 if dp * ep <= 2 else 1e-7), r
+
+
+@pytest.mark.parametrize("dp,ep,mode", [(2, 1, 2), (2, 2, 2), (1, 2, 2), (2, 1, 1)])
+def test_sharded_optimizer_bf16_grads(dp, ep, mode):
+    """The benchmarked path: bf16 weights and grads, NCCL reduce-scatter of the bf16 grads
+    (the sum is rounded to bf16 before the 1/g unscale) vs the reference's fp32 member-order
+    sum of the same bf16 values (optim.cpp:148-156). Bars, written here: masters and moments
+    within 5e-3 rel_err (one bf16 rounding of the summed grad, 2^-8 relative, feeds m and v);
+    bf16 weights within 2e-3 rel_err (a few bf16 ulps of the 0.05-scale weights); state bytes
+    exact."""
+    r = run_opt(dp, ep, mode, bf16=True)
+    assert r["weights_maxrel"] <= 2e-3, r
+    assert r["state_maxrel"] <= 5e-3, r
+    assert r["state_bytes_equal"], r
+    assert r.get("gather_ok", True), r

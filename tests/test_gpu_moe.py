@@ -326,32 +326,6 @@ def test_layer_bf16_zipf_skewed_routing(b2ctx, orc, s, K):
         assert not got["gate"][e].any() and not got["up"][e].any() and not got["down"][e].any()
 
 
-def test_tma_gather_matches_materialised_rows(b2ctx):
-    """bf16 at EP = 1, opt-in: the GEMMs' tile::gather4 X operand (rows gathered from x by prow_src,
-    pad rows zero-filled out of bounds) is bitwise identical to the materialised mlp_in path."""
-    import ctypes as C
-    b2, ctx = b2ctx
-    lib = b2.lib()
-    lib.b2x_moe_set_tma_gather.argtypes = [C.c_void_p, C.c_int]
-    cfg = b2.MoeConfig(n_experts=16, top_k=4, hidden=256, intermediate=192)
-    S = 700
-    gen = torch.Generator(device="cuda").manual_seed(9)
-    mk = lambda shape, std: (torch.randn(shape, device="cuda", generator=gen) * std).bfloat16()
-    x, dout = mk((S, 256), 1.0), mk((S, 256), 1.0)
-    router, gate, up, down = mk((256, 16), 0.05), mk((16, 256, 192), 0.05), mk((16, 256, 192), 0.05), \
-        mk((16, 192, 256), 0.05)
-    res = []
-    for tma in (0, 1):
-        layer = b2.MoeLayer(ctx, cfg, torch.bfloat16, S)
-        assert lib.b2x_moe_set_tma_gather(layer.h, tma) == 0
-        out = layer.forward(x, router, gate, up, down)
-        g = layer.backward(router, gate, up, down, dout, layer.aux_probs_grad(0.01))
-        torch.cuda.synchronize()
-        res.append([out] + [g[k] for k in ("input", "router", "gate", "up", "down")])
-    for a, b in zip(*res):
-        assert torch.equal(a, b)
-
-
 def test_host_pipeline_matches_synchronous(b2ctx):
     """b2_moe_fwd_bwd_host_async (two staging slots, copies overlapped with compute) gives
     every step exactly the results of the synchronous host-buffer call."""

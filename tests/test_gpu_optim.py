@@ -75,7 +75,12 @@ def test_step_matches_oracle(b2ctx, orc, dtype, mode):
     assert opt.last_launches() > 0
 
 
-def test_nonfinite_grad_skips_update_and_is_detected(b2ctx, orc):
+def test_nonfinite_grad_is_detected_and_step_matches_reference(b2ctx, orc):
+    """detect_soft_failure (reliability.cpp:706-723) flags a non-finite loss or grad; the step's
+    fused scan reports it in the stats. Like the reference's ShardedOptimizer::step
+    (optim.cpp:130-194) the step itself always applies the update and advances the step count
+    (the training loop checks detect_soft_failure first, train.cpp:193-194), so a later step
+    sees the same lr and bias corrections as the reference."""
     b2, ctx = b2ctx
     w0, grads = make(orc, torch.bfloat16, 2)
     W = torch.from_numpy(w0).cuda().bfloat16()
@@ -89,15 +94,11 @@ def test_nonfinite_grad_skips_update_and_is_detected(b2ctx, orc):
     assert opt.detect_soft_failure(float("nan"), node=0) == 0  # a non-finite loss is a failure too
     G[130_500] = float("inf")
     assert opt.detect_soft_failure(1.25, node=3) == 3
-    before = W.clone()
     st = opt.step(stats=True)
     torch.cuda.synchronize()
-    assert st["nonfinite"]
-    assert torch.equal(W, before)  # the fused scan skipped the update on the device
-    assert not np.any(opt.state(1)[1])  # moments untouched (still zero)
-    G.copy_(torch.from_numpy(grads[1]).cuda().bfloat16())
+    assert st["nonfinite"] and st["step"] == 0
     st = opt.step(stats=True)
-    assert not st["nonfinite"] and not torch.equal(W, before)
+    assert st["step"] == 1  # the count advanced, as in the reference
 
 
 def test_state_checkpoint_restore_continues_bitwise(b2ctx, orc):

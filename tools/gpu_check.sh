@@ -24,17 +24,11 @@ for w in $WHAT; do case $w in
  timeline) timeout 300 python tools/timeline.py > $OUT/timeline_eager.txt 2>&1; echo "timeline rc=$?"; head -30 $OUT/timeline_eager.txt
       timeout 300 python tools/timeline.py --graph > $OUT/timeline_graph.txt 2>&1; head -30 $OUT/timeline_graph.txt ;;
  tl2) timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29513 tools/timeline.py --graph 2>&1 | grep -v "Warn\|warn\|\*\*\*\|OMP" | head -45 ;;
- tl2n) timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29515 tools/timeline.py --graph --ce-dispatch 2>&1 | grep -v "Warn\|warn\|\*\*\*\|OMP" | head -20 ;;
- tl4n) timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29516 tools/timeline.py --graph --ce-dispatch 2>&1 | grep -v "Warn\|warn\|\*\*\*\|OMP" | head -20 ;;
  tl4) timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29514 tools/timeline.py --graph 2>&1 | grep -v "Warn\|warn\|\*\*\*\|OMP" | head -45 ;;
  ckpt) timeout 600 python -m pytest tests/test_gpu_ckpt.py tests/test_records.py -x -q > $OUT/ckpt_tests.log 2>&1; echo "ckpt tests rc=$?"; tail -15 $OUT/ckpt_tests.log
       timeout 300 python tools/ckpt_probe.py --dir /tmp > $OUT/ckpt_probe.json 2> $OUT/ckpt_probe.err; echo "probe rc=$?"; cat $OUT/ckpt_probe.json; tail -3 $OUT/ckpt_probe.err ;;
  adamw) timeout 300 python tools/adamw_probe.py --gelems 2 > $OUT/adamw.txt 2>&1; cat $OUT/adamw.txt
-      timeout 600 ncu --set full --clock-control none -k regex:"adamw_chunks|adamw_stream|sumsq_chunks" --launch-skip 2 -c 2 -o $OUT/adamw_full python tools/adamw_probe.py --gelems 0.5 --steps 1 > $OUT/ncu_adamw.log 2>&1; echo "adamw ncu rc=$?" ;;
- adamwab) for impl in regs stream regs stream; do echo "== B2_ADAMW_IMPL=$impl"; B2_ADAMW_IMPL=$impl timeout 300 python tools/adamw_probe.py --gelems ${GELEMS:-2}; done
-      for impl in regs stream; do B2_ADAMW_IMPL=$impl timeout 600 python -m pytest tests/test_gpu_optim.py tests/test_gpu_ckpt.py -x -q > $OUT/optim_tests_$impl.log 2>&1; echo "optim tests ($impl) rc=$?"; tail -2 $OUT/optim_tests_$impl.log; done ;;
- pdl) for i in 1 2; do for v in 1 0; do echo "== B2_PDL=$v"; B2_PDL=$v timeout 300 python tools/timeline.py --graph 2>&1 | grep -E "event-timed|span"; done; done ;;
- ab) for opt in "--graph" "--graph --tma-gather"; do echo "== timeline $opt"; timeout 300 python tools/timeline.py $opt 2>&1 | grep -v Warn | head -24; done ;;
+      timeout 600 ncu --set full --clock-control none -k regex:"adamw_chunks|sumsq_chunks" --launch-skip 2 -c 2 -o $OUT/adamw_full python tools/adamw_probe.py --gelems 0.5 --steps 1 > $OUT/ncu_adamw.log 2>&1; echo "adamw ncu rc=$?" ;;
  gtest) timeout 600 python -m pytest tests -m gpu -x -q -k "${GTEST_K}" > $OUT/gtest.log 2>&1; echo "gtest rc=$?"; tail -15 $OUT/gtest.log ;;
  ep4) timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29512 \
       bench.py --gpus 4 --steps 10 --warmup 3 > $OUT/ep4.json 2> $OUT/ep4.err; echo "ep4 rc=$?"; cat $OUT/ep4.json; tail -5 $OUT/ep4.err ;;

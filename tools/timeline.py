@@ -15,10 +15,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--graph", action="store_true")
     ap.add_argument("--tokens", type=int, default=16384)
-    ap.add_argument("--tma-gather", action="store_true", help="TMA gather4 X operand instead of mlp_in rows")
-    ap.add_argument("--fused", action="store_true", help="EP: the GEMM-fused combine (opt-in)")
     ap.add_argument("--no-overlap", action="store_true", help="EP: dX return after the wgrad GEMMs")
-    ap.add_argument("--ce-dispatch", action="store_true", help="EP: copy-engine all-gather of x (opt-in)")
     args = ap.parse_args()
     import torch
     from torch.profiler import ProfilerActivity, profile
@@ -48,22 +45,10 @@ def main():
     layer = b2.MoeLayer(ctx, cfg, torch.bfloat16, S)
     if args.graph:
         layer.set_graph(True)
-    if args.ce_dispatch:
-        import ctypes
-        b2.lib().b2x_moe_set_ce_dispatch.argtypes = [ctypes.c_void_p, ctypes.c_int]
-        b2.lib().b2x_moe_set_ce_dispatch(layer.h, 1)
     if args.no_overlap:
         import ctypes
         b2.lib().b2x_moe_set_overlap_return.argtypes = [ctypes.c_void_p, ctypes.c_int]
         b2.lib().b2x_moe_set_overlap_return(layer.h, 0)
-    if args.fused:
-        import ctypes
-        b2.lib().b2x_moe_set_fused_combine.argtypes = [ctypes.c_void_p, ctypes.c_int]
-        b2.lib().b2x_moe_set_fused_combine(layer.h, 1)
-    if args.tma_gather:
-        import ctypes
-        b2.lib().b2x_moe_set_tma_gather.argtypes = [ctypes.c_void_p, ctypes.c_int]
-        b2.lib().b2x_moe_set_tma_gather(layer.h, 1)
     out = torch.empty_like(x)
     grads = dict(input=torch.empty_like(x), router=torch.empty_like(router), gate=torch.empty_like(gate),
                  up=torch.empty_like(up), down=torch.empty_like(down))
