@@ -92,6 +92,8 @@ struct Params {
     __nv_bfloat16* out1;
     __nv_bfloat16* out2;
     float scale;
+    const float* row_w;   // FwdGateUp / BwdDownDgrad: per padded row routing weight (weighted-H scheme)
+    float* wpart;         // BwdDownDgrad with row_w: [P, 2 * n_tiles] partial weight-gradient dots
     uint32_t idesc;       // instruction descriptor (runtime N for the router kinds)
     int umma_n;           // accumulator columns in use
     int b_chunks;         // 64-column B boxes per stage (MN-major B)
@@ -294,14 +296,19 @@ struct EpiStage {
     uint8_t* g0;  // generic address of slot 0
     int slot;
     __device__ __forceinline__ uint32_t begin(int lane, const float* v) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
+        return begin_packed(lane, pk);
+    }
+    // pk: the row's 32 bf16 values packed in pairs
+    __device__ __forceinline__ uint32_t begin_packed(int lane, const uint32_t* pk) {
         if (lane == 0) bulk_wait_read<SLOTS - 1>();
         __syncwarp();
         uint4* row = reinterpret_cast<uint4*>(g0 + slot * EPI_SLOT_BYTES + lane * 64);
         const int sw = (lane >> 1) & 3;
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-            row[q ^ sw] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
-                                     pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+        for (int q = 0; q < 4; ++q) row[q ^ sw] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
         fence_async_smem();
         __syncwarp();
         const uint32_t src = s0 + slot * EPI_SLOT_BYTES;
@@ -310,6 +317,13 @@ struct EpiStage {
     }
     __device__ __forceinline__ void put2d(const CUtensorMap* map, int lane, const float* v, int c0, int c1) {
         const uint32_t src = begin(lane, v);
+        if (lane == 0) {
+            tma_store_2d(map, src, c0, c1);
+            bulk_commit();
+        }
+    }
+    __device__ __forceinline__ void put2d_packed(const CUtensorMap* map, int lane, const uint32_t* pk, int c0, int c1) {
+        const uint32_t src = begin_packed(lane, pk);
         if (lane == 0) {
             tma_store_2d(map, src, c0, c1);
             bulk_commit();
@@ -486,6 +500,17 @@ __device__ __forceinline__ void load_stage(const Params& p, const TileInfo& ti, 
 }
 
 __device__ __forceinline__ float silu_f(float x) { return __fdividef(x, 1.f + __expf(-x)); }
+
+// dgrad epilogue operands: 32 bf16 columns of one row of G and of U (64 B each)
+__device__ __forceinline__ void load_gu(const Params& p, int64_t off, uint4 (&g4)[4], uint4 (&u4)[4]) {
+    const uint4* gp = reinterpret_cast<const uint4*>(p.g + off);
+    const uint4* up = reinterpret_cast<const uint4*>(p.u + off);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        g4[q] = __ldg(gp + q);
+        u4[q] = __ldg(up + q);
+    }
+}
 
 // epilogue of the router kinds for one row (thread = row); the six expert kinds store
 // through the TMA-store staging in the kernel body
@@ -699,57 +724,74 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
             ti.m0 += BM * (int)rank;  // this CTA's 128 rows of the pair's tile
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
+            // this lane's row weight and (dgrad) G/U operands of the first chunk load while the
+            // MMAs still run
+            float wrow = 1.f;
+            if constexpr (KIND == GemmKind::FwdGateUp || KIND == GemmKind::BwdDownDgrad)
+                if (p.row_w) wrow = __ldg(p.row_w + ti.m0 + row0 + lane);
+            uint4 gq[4], uq[4];
+            if constexpr (KIND == GemmKind::BwdDownDgrad) {
+                const int col = ti.n0 + half * (BN / 2);
+                if (col < p.I) load_gu(p, (int64_t)(ti.m0 + row0 + lane) * p.I + col, gq, uq);
+            }
             mbar_wait(tfull_bar(acc), acc_phase, 3);
             tc_fence_after();
             const uint32_t tacc = tmem_base + ((uint32_t)(32 * quad) << 16) + acc * BN;
             if constexpr (KIND == GemmKind::BwdDownDgrad) {
-                // SwiGLU backward (kernels.hpp:277-295) on the dH accumulator: G and U of this
-                // lane's row come straight from global into registers (ld.global.nc)
+                // SwiGLU backward (kernels.hpp:277-295) on the dH accumulator. G and U of this lane's
+                // row come straight from global into registers (ld.global.nc), one 32-column chunk
+                // ahead of the math (the first one before the accumulator wait). Weighted-H scheme
+                // (row_w): the accumulator is dH' = dout . Wd^T; dmul = w * dH', and the row's
+                // top-k weight-gradient partial dH' . silu(G) * U (= dout . y) goes to wpart
+                const bool wscheme = p.row_w != nullptr;
+                const int64_t grow = (int64_t)(ti.m0 + row0 + lane) * p.I;
+                float wdot = 0.f;
 #pragma unroll 1
                 for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
                     const int col = ti.n0 + c;
                     const bool live = col < p.I;  // I % 64 == 0: a chunk is all in or all out
-                    float gv[32], uv[32];
-                    if (live) {
-                        const int64_t grow = (int64_t)(ti.m0 + row0 + lane) * p.I + col;
-                        const uint4* g4p = reinterpret_cast<const uint4*>(p.g + grow);
-                        const uint4* u4p = reinterpret_cast<const uint4*>(p.u + grow);
-                        uint4 g4[4], u4[4];
+                    uint4 g4[4], u4[4];
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            g4[q] = __ldg(g4p + q);
-                            u4[q] = __ldg(u4p + q);
-                        }
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const uint32_t gw[4] = {g4[q].x, g4[q].y, g4[q].z, g4[q].w},
-                                           uw[4] = {u4[q].x, u4[q].y, u4[q].z, u4[q].w};
-#pragma unroll
-                            for (int h = 0; h < 4; ++h) {
-                                gv[8 * q + 2 * h] = bf16_lo(gw[h]);
-                                gv[8 * q + 2 * h + 1] = bf16_hi(gw[h]);
-                                uv[8 * q + 2 * h] = bf16_lo(uw[h]);
-                                uv[8 * q + 2 * h + 1] = bf16_hi(uw[h]);
-                            }
-                        }
+                    for (int q = 0; q < 4; ++q) {
+                        g4[q] = gq[q];
+                        u4[q] = uq[q];
                     }
+                    if (c + 32 < (half + 1) * (BN / 2) && col + 32 < p.I) load_gu(p, grow + col + 32, gq, uq);
                     uint32_t r[32];
                     tmem_ld32(tacc + c, r);
                     tmem_wait_ld();
                     if (!live) continue;
-                    float dgv[32], duv[32];
+                    uint32_t dgp[16], dup[16];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const float x = gv[j], uu = uv[j], d = __uint_as_float(r[j]);
-                        const float sg = __fdividef(1.f, 1.f + __expf(-x));
-                        duv[j] = x * sg * d;
-                        dgv[j] = uu * d * (sg * (1.f + x * (1.f - sg)));
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t gw[4] = {g4[q].x, g4[q].y, g4[q].z, g4[q].w},
+                                       uw[4] = {u4[q].x, u4[q].y, u4[q].z, u4[q].w};
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            float dg2[2], du2[2];
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const float x = e ? bf16_hi(gw[h]) : bf16_lo(gw[h]);
+                                const float uu = e ? bf16_hi(uw[h]) : bf16_lo(uw[h]);
+                                const float a = __uint_as_float(r[8 * q + 2 * h + e]);
+                                const float sg = __fdividef(1.f, 1.f + __expf(-x));
+                                const float xs = x * sg;  // silu(g)
+                                wdot = __fmaf_rn(a, xs * uu, wdot);
+                                const float d = a * wrow;
+                                du2[e] = xs * d;
+                                dg2[e] = uu * d * (sg * (1.f + x * (1.f - sg)));
+                            }
+                            dgp[4 * q + h] = pack_bf16(dg2[0], dg2[1]);
+                            dup[4 * q + h] = pack_bf16(du2[0], du2[1]);
+                        }
                     }
                     // (measured: TMA-staged stores beat direct register->global stores here,
                     // 0.57 vs 0.61 ms per dgrad at config B)
-                    stg.put2d(&p.mapO0, lane, dgv, col, ti.m0 + row0);
-                    stg.put2d(&p.mapO0, lane, duv, p.I + col, ti.m0 + row0);
+                    stg.put2d_packed(&p.mapO0, lane, dgp, col, ti.m0 + row0);
+                    stg.put2d_packed(&p.mapO0, lane, dup, p.I + col, ti.m0 + row0);
                 }
+                if (wscheme)
+                    p.wpart[(int64_t)(ti.m0 + row0 + lane) * (2 * p.n_tiles) + 2 * (ti.n0 / BN) + half] = wdot;
             } else if constexpr (KIND == GemmKind::FwdGateUp) {
                 const int nbase = ti.n0 / 2;  // 128 gate + 128 up columns per tile
                 uint32_t r[32], r2[32];
@@ -772,7 +814,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                         uv[j + 1] = bf16_hi(up);
                     }
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) hv[j] = silu_f(gv[j]) * uv[j];
+                    for (int j = 0; j < 32; ++j) hv[j] = silu_f(gv[j]) * uv[j] * wrow;
                     stg.put2d(&p.mapO0, lane, gv, col, ti.m0 + row0);
                     stg.put2d(&p.mapO1, lane, uv, col, ti.m0 + row0);
                     stg.put2d(&p.mapO2, lane, hv, col, ti.m0 + row0);
@@ -962,6 +1004,9 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
     p.out0 = (__nv_bfloat16*)a.out0;
     p.out1 = (__nv_bfloat16*)a.out1;
     p.out2 = (__nv_bfloat16*)a.out2;
+    p.row_w = a.row_w;
+    p.wpart = a.wpart;
+    if (a.kind == GemmKind::BwdDownDgrad && a.row_w) check(a.wpart != nullptr, "dgrad: row weights need wpart");
     const int64_t P = a.pmax, H = a.H, I = a.I, nr = a.nr;
     int grid = a.num_sms > 0 ? a.num_sms : 148;
     if (a.max_ctas > 0) grid = std::min(grid, std::max(2, a.max_ctas));

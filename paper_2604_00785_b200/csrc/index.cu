@@ -185,7 +185,8 @@ __global__ void scatter_kernel(const int32_t* __restrict__ gidx, int T, int K, i
                                const int32_t* __restrict__ pad_start, const int32_t* __restrict__ cum_expert_counts,
                                int32_t* __restrict__ input_indices, int32_t* __restrict__ output_indices,
                                int32_t* __restrict__ selected_k, int32_t* __restrict__ slot_prow,
-                               int32_t* __restrict__ prow_src) {
+                               int32_t* __restrict__ prow_src, const float* __restrict__ gw,
+                               float* __restrict__ prow_w) {
     pdl_wait();
     pdl_launch();
     extern __shared__ int32_t sh[];  // carry [kWarpsPerCta][nr] (row offset inside the expert)
@@ -222,18 +223,22 @@ __global__ void scatter_kernel(const int32_t* __restrict__ gidx, int T, int K, i
             selected_k[pos] = k;
             slot_prow[pos] = prow;
             prow_src[prow] = t;
+            if (prow_w) prow_w[prow] = gw[(int64_t)t * K + k];
         }
     }
 }
 
 // pad rows of each expert group read as zero tokens
 __global__ void pad_fill_kernel(const int32_t* __restrict__ token_counts, const int32_t* __restrict__ pad_start,
-                                int nr, int32_t* __restrict__ prow_src) {
+                                int nr, int32_t* __restrict__ prow_src, float* __restrict__ prow_w) {
     pdl_wait();
     pdl_launch();
     const int ln = blockIdx.x;
     const int b = pad_start[ln] + token_counts[ln], e = pad_start[ln + 1];
-    for (int r = b + threadIdx.x; r < e; r += blockDim.x) prow_src[r] = -1;
+    for (int r = b + threadIdx.x; r < e; r += blockDim.x) {
+        prow_src[r] = -1;
+        if (prow_w) prow_w[r] = 0.f;
+    }
 }
 
 void launch_routing_index(const RoutingIndexArgs& a, cudaStream_t st) {
@@ -253,10 +258,10 @@ void launch_routing_index(const RoutingIndexArgs& a, cudaStream_t st) {
         launch_k(scatter_kernel, dim3(nblk), dim3(32 * kWarpsPerCta), smem, st, a.gidx, a.T, a.K, a.n_start, a.nr, nchunks, a.wbase,
                                                               a.cum_token_counts, a.pad_start, a.cum_expert_counts,
                                                               a.input_indices, a.output_indices, a.selected_k,
-                                                              a.slot_prow, a.prow_src);
+                                                              a.slot_prow, a.prow_src, a.gw, a.prow_w);
         B2_LAUNCH_CHECK();
     }
-    launch_k(pad_fill_kernel, dim3(a.nr), dim3(128), 0, st, a.token_counts, a.pad_start, a.nr, a.prow_src);
+    launch_k(pad_fill_kernel, dim3(a.nr), dim3(128), 0, st, a.token_counts, a.pad_start, a.nr, a.prow_src, a.prow_w);
     B2_LAUNCH_CHECK();
 }
 

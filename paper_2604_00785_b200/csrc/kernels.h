@@ -45,6 +45,8 @@ struct RoutingIndexArgs {
     int32_t* selected_k;         // [T*K]
     int32_t* slot_prow;          // [T*K] token-major slot -> padded row
     int32_t* prow_src;           // [pmax] padded row -> token (-1 pad)
+    const float* gw;             // [T, K] dispatch weights (with prow_w)
+    float* prow_w;               // [pmax] padded row -> its routing weight (0 pad); nullptr: not needed
     int32_t* err;                // expert id out of range flag
 };
 void launch_routing_index(const RoutingIndexArgs& a, cudaStream_t st);
@@ -66,6 +68,9 @@ template <typename T>
 void launch_out_reduction_bwd(const T* dout, const T* const* peer_dout, int s_local, const T* y,
                               const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec, const float* gw,
                               T* dy, float* wgrad, int T_tok, int H, int K, cudaStream_t st);
+// bf16 path: wgrad[t, k] from the dgrad epilogue's np partial dots per padded row
+void launch_wgrad_from_parts(const float* part, int np, const int32_t* slot_prow, const int32_t* selected_k,
+                             const int32_t* cec, float* wgrad, int T_tok, int K, cudaStream_t st);
 template <typename T>
 void launch_dx_finalize(const T* src, bool from_slots, const int32_t* slot_prow, const int32_t* cec, const float* dl,
                         const T* wr, T* dx, int S, int H, int N, cudaStream_t st);
@@ -145,6 +150,12 @@ struct Sm100GemmArgs {
     void* out1;
     void* out2;
     float scale;        // wgrad: 1/EP
+    // bf16 layer (weighted-H scheme): row_w [P] = each padded row's routing weight. FwdGateUp
+    // stores H' = w * silu(G) * U; BwdDownDgrad takes the UNweighted dout rows as dY, scales its
+    // accumulator by w and leaves the top-k weight-gradient partial dots acc . silu(G) * U in
+    // wpart [P, 2 * ceil(I / 256)] (null row_w: plain semantics, dY already weighted)
+    const float* row_w;
+    float* wpart;
     int num_sms;
     // router kinds
     int S, N;                    // local tokens, experts

@@ -82,7 +82,7 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     auto acc = [&](size_t b) { bytes += ((b + 255) & ~size_t(255)) + 256; };
     // workspace: fp32
     for (int64_t n : {smax_ * N, smax_ * N, smax_ * K, tmax_ * K, (ceil_div(smax_, 128) + 1) * N, tmax_ * K,
-                      smax_ * N, (int64_t)kRouterDwMaxSplits * H * N})
+                      smax_ * N, (int64_t)kRouterDwMaxSplits * H * N, pmax_, pmax_ * wparts()})
         acc(4 * (size_t)std::max<int64_t>(n, 1));
     // workspace: int32
     for (int64_t n : {smax_ * K, tmax_ * K, nch * nr, nch * nr, tmax_, tmax_ + 1, nr * thmax_, nr * thmax_ + 1, nr,
@@ -142,6 +142,8 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     selected_k_ = w.take<int32_t>(tmax_ * K);
     slot_prow_ = w.take<int32_t>(tmax_ * K);
     prow_src_ = w.take<int32_t>(pmax_);
+    prow_w_ = w.take<float>(pmax_);
+    wpart_ = w.take<float>(pmax_ * wparts());
     mlp_in_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
     g_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
     u_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
@@ -479,6 +481,8 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     ra.selected_k = selected_k_;
     ra.slot_prow = slot_prow_;
     ra.prow_src = prow_src_;
+    ra.gw = gw_;
+    ra.prow_w = dtype_ == BF16 ? prow_w_ : nullptr;  // weighted-H scheme of the tensor-core path
     ra.err = err_;
     launch_routing_index(ra, st);
     launches_ += 4;
@@ -510,7 +514,8 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
         ga.wu = up;
         ga.out0 = g_;
         ga.out1 = u_;
-        ga.out2 = h_;
+        ga.out2 = h_;  // H' = w * silu(G) * U (weighted-H scheme: row_w)
+        ga.row_w = prow_w_;
         mark(kGemmGateUp, false);
         launch_sm100_gemm(ga, st);
         mark(kGemmGateUp, true);
@@ -569,12 +574,15 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     if (E > 1) {
         // each owner combines its slots into its OWN slab row [gid]; after the barrier the
         // source pulls its rows from the owners and sums them in rank order
-        launch_ep_combine_local<T>((const T*)y_, slot_prow_, selected_k_, cec_, gw_, K, S, Tt, H, (T*)ret_f_, st);
+        // bf16: the rows are already weighted (y' = H' . Wd = w * y), fp32: weight here
+        launch_ep_combine_local<T>((const T*)y_, slot_prow_, selected_k_, cec_, dtype_ == BF16 ? nullptr : gw_, K, S,
+                                   Tt, H, (T*)ret_f_, st);
         ep_barrier();
         launch_ep_pull_sum<T>((const T* const*)peer_tab_ + 2 * E, gi_local_, S, K, E, nr, H, ctx_.coord_ep, out, st);
         launches_ += 2;
     } else {
-        launch_combine<T>((const T*)y_, slot_prow_, selected_k_, cec_, gw_, out, Tt, H, K, st);
+        launch_combine<T>((const T*)y_, slot_prow_, selected_k_, cec_, dtype_ == BF16 ? nullptr : gw_, out, Tt, H, K,
+                          st);
         launches_ += 1;
     }
     mark(kCombine, true);
@@ -634,10 +642,24 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
     }
     // EP > 1: the top-k weight gradients go straight into this rank's symmetric slab, where
     // the sources pull them from
-    launch_out_reduction_bwd<T>(dout, peer_dout, S, (const T*)y_, slot_prow_, selected_k_, cec_, gw_, (T*)dy_,
-                                E > 1 ? wret_ : wgrad_, Tt, H, K, st);
-    launch_zero_pad_rows<T>((T*)dy_, prow_src_, p_total, H, pmax_, st);
-    launches_ += 2;
+    if (dtype_ == BF16) {
+        // weighted-H scheme: dY is just the token's dout row in each of its padded rows (the
+        // routing weight is applied inside the dgrad epilogue, and the weight gradient comes out
+        // of that epilogue's dot products) — a plain gather, no mlp_out read
+        if (E > 1) {
+            launch_ep_gather_pull<T>(peer_dout, S, Tt, H, cec_, slot_prow_, (T*)dy_, st);
+            launch_zero_pad_rows<T>((T*)dy_, prow_src_, p_total, H, pmax_, st);
+            launches_ += 2;
+        } else {
+            launch_gather_rows<T>(dout, prow_src_, p_total, (T*)dy_, H, pmax_, st);
+            launches_ += 1;
+        }
+    } else {
+        launch_out_reduction_bwd<T>(dout, peer_dout, S, (const T*)y_, slot_prow_, selected_k_, cec_, gw_, (T*)dy_,
+                                    E > 1 ? wret_ : wgrad_, Tt, H, K, st);
+        launch_zero_pad_rows<T>((T*)dy_, prow_src_, p_total, H, pmax_, st);
+        launches_ += 2;
+    }
     mark(kOutRedBwd, true);
     if (dtype_ == BF16) {
         Sm100GemmArgs ga{};
@@ -660,8 +682,15 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         ga.scale = inv_ep;
         ga.kind = GemmKind::BwdDownDgrad;  // 406 + silu_glu_backward 409
         ga.out0 = dgu_;
+        ga.row_w = prow_w_;
+        ga.wpart = wpart_;
         mark(kGemmDgrad, false);
         launch_sm100_gemm(ga, st);
+        ga.row_w = nullptr;
+        ga.wpart = nullptr;
+        launch_wgrad_from_parts(wpart_, (int)wparts(), slot_prow_, selected_k_, cec_, E > 1 ? wret_ : wgrad_, Tt, K,
+                                st);
+        launches_ += 1;
         mark(kGemmDgrad, true);
         if (overlap_return()) {
             // EP > 1: dX first, then its return to the source ranks (owner combine, barrier,

@@ -137,7 +137,10 @@ class MoeLayer {
                     const float* aux_probs_grad, T* dx, T* drouter, T* dgate, T* dup, T* ddown);
 
     void mark(int stage, bool end);
-    void check_expert_ids();  // throws ContractError if an index kernel flagged an id outside [0, N)
+    void check_expert_ids();
+    // partial weight-gradient dots per padded row left by the dgrad epilogue (two per 256-column
+    // n-tile of I)
+    int64_t wparts() const { return 2 * ceil_div(cfg_.intermediate, (int64_t)256); }  // throws ContractError if an index kernel flagged an id outside [0, N)
     void set_dispatch_tables();
     struct GraphCache {
         std::vector<const void*> key;
@@ -178,6 +181,8 @@ class MoeLayer {
     int32_t *topi_, *fi_, *sel_, *whist_, *wbase_, *expert_counts_, *cec_, *partial_counts_, *partial_cum_,
         *token_counts_, *ctc_, *pad_start_, *input_indices_, *output_indices_, *selected_k_, *slot_prow_,
         *prow_src_, *err_;
+    float* prow_w_ = nullptr;  // bf16: padded row -> routing weight (0 pad), the weighted-H scheme
+    float* wpart_ = nullptr;   // bf16: [pmax, wparts()] dgrad-epilogue partial dots
     const float* gw_ = nullptr;    // dispatch weights (learned or FUR)
     const int32_t* gi_ = nullptr;  // dispatch indices
     // dtype buffers (padded row space)

@@ -440,6 +440,38 @@ void launch_combine(const T* y, const int32_t* slot_prow, const int32_t* selecte
     B2_LAUNCH_CHECK();
 }
 
+// top-k weight gradients from the dgrad epilogue's row partials (bf16 path): the reference's
+// weights_grad[t, k] = dout[t] . mlp_out[r] (moe.hpp:283-294) equals dH'[r] . h[r] with
+// dH' = dout . Wd^T, which the dgrad GEMM accumulates anyway; its epilogue leaves np partial
+// dots per padded row (one per 128-column half tile), summed here in a fixed order. Tokens
+// without a local slot get zeros, like the reference's zero-initialised weights_grad.
+__global__ void wgrad_from_parts_kernel(const float* __restrict__ part, int np, const int32_t* __restrict__ slot_prow,
+                                        const int32_t* __restrict__ selected_k, const int32_t* __restrict__ cec,
+                                        float* __restrict__ wgrad, int T_tok, int K) {
+    pdl_wait();
+    pdl_launch();
+    // one thread per (token, k): find the token's local slot holding k (if any)
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)T_tok * K) return;
+    const int t = (int)(i / K), k = (int)(i % K);
+    float acc = 0.f;
+    for (int j = cec[t], j1 = cec[t + 1]; j < j1; ++j) {
+        if (selected_k[j] != k) continue;
+        const float* pr = part + (int64_t)slot_prow[j] * np;
+        for (int q = 0; q < np; ++q) acc += pr[q];
+        break;
+    }
+    wgrad[i] = acc;
+}
+
+void launch_wgrad_from_parts(const float* part, int np, const int32_t* slot_prow, const int32_t* selected_k,
+                             const int32_t* cec, float* wgrad, int T_tok, int K, cudaStream_t st) {
+    if (T_tok <= 0) return;
+    launch_k(wgrad_from_parts_kernel, dim3((unsigned)ceil_div((int64_t)T_tok * K, 256)), dim3(256), 0, st, part, np,
+             slot_prow, selected_k, cec, wgrad, T_tok, K);
+    B2_LAUNCH_CHECK();
+}
+
 template <typename T>
 void launch_out_reduction_bwd(const T* dout, const T* const* peer_dout, int s_local, const T* y,
                               const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec, const float* gw,
