@@ -477,16 +477,28 @@ def optimizer_cpu_baseline():
 
 def self_launch(args) -> bool:
     """`bench.py --gpus N` without torchrun: re-launch this script as N ranks (one process per
-    GPU, torch.distributed.run over 127.0.0.1) so the JSON line always reports n_gpus = N."""
+    GPU, torch.distributed.run over 127.0.0.1) so the JSON line always reports n_gpus = N. The
+    rendezvous port is probed free first; a lost race for it (EADDRINUSE) is retried."""
     if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
         return False
+    import random
     import socket
-    with socket.socket() as so:
-        so.bind(("127.0.0.1", 0))
-        port = so.getsockname()[1]
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
-    sys.exit(subprocess.call(cmd))
+    rc = 1
+    for attempt in range(4):
+        port = random.randint(20000, 60000)
+        with socket.socket() as so:
+            try:
+                so.bind(("127.0.0.1", port))
+            except OSError:
+                continue
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        p = subprocess.run(cmd, stderr=subprocess.PIPE, text=True)
+        sys.stderr.write(p.stderr)
+        rc = p.returncode
+        if rc == 0 or "EADDRINUSE" not in p.stderr and "address already in use" not in p.stderr:
+            break
+    sys.exit(rc)
 
 
 def main():
