@@ -60,15 +60,37 @@ constexpr int NUM_THREADS = 128 + 32 * NUM_EPI_WARPS;
 // TMA-store epilogue of the six expert kinds: each epilogue warp owns SLOTS 2 KB staging
 // slots, each one 32-row x 32-column bf16 box in the SWIZZLE_64B layout
 constexpr int EPI_SLOT_BYTES = 32 * 32 * 2;
+// Wide tiles: 256 x 512 per CTA pair — two N = 256 MMAs per k-step into one 512-column TMEM
+// accumulator. Per SM a k-block then brings 16 KB of A and 32 KB of B for 128 x 512 x 64 MACs
+// instead of 16 + 16 KB for 128 x 256 x 64: a quarter fewer L2 -> SM bytes per FLOP, the limit of
+// the 256-wide kernels (with the operand loads removed the same MMAs run at the measured bf16
+// peak: tools/gemm_tile_probe.py, noload experiment). No accumulator double-buffering is left, so
+// the epilogue frees the two 256-column halves separately and the next tile's MMAs start on the
+// first half while the second drains.
+// Measured per kind at config B (tools/gemm_tile_probe.py, same box): FwdGateUp 837 -> 803 us,
+// FwdDown 424 -> 397, BwdDx 819 -> 751, WgradDown 417 -> 394, WgradGateUp 806 -> 756; the dgrad,
+// whose epilogue also loads G/U and computes the SwiGLU backward, got slower without the
+// double-buffered accumulator (503 -> 562 us) and stays 256 wide.
+template <GemmKind K>
+struct WideKind {
+    static constexpr bool value = K == GemmKind::FwdGateUp || K == GemmKind::FwdDown || K == GemmKind::BwdDx ||
+                                  K == GemmKind::WgradDown || K == GemmKind::WgradGateUp;
+};
 template <GemmKind K, int CG>
 struct KCfg {
+    static constexpr bool WIDE = CG == 2 && WideKind<K>::value;
+    static constexpr int TN = WIDE ? 2 * BN : BN;  // N columns of a tile
+    static constexpr int REGIONS = TN / BN;        // N = 256 MMAs per k-step
+    static constexpr int B_COLS = TN / CG;         // B columns held per CTA
+    static constexpr int REGION_BYTES = (B_COLS / REGIONS) * BK * 2;
+    static constexpr int STAGE_BYTES = A_BYTES + B_COLS * BK * 2;
     static constexpr bool TMA_EPI = (int)K <= (int)GemmKind::WgradGateUp;
     // two staging slots everywhere (FwdGateUp's three boxes per chunk rotate through them)
     static constexpr int SLOTS = 2;
-    static constexpr int STAGES = CG == 1 ? 4 : 6;
+    static constexpr int STAGES = CG == 1 ? 4 : (WIDE ? 4 : 6);
     static constexpr int WARP_EPI_BYTES = TMA_EPI ? SLOTS * EPI_SLOT_BYTES : 0;
     static constexpr int SMEM =
-        STAGES * Cfg<CG>::STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + NUM_EPI_WARPS * WARP_EPI_BYTES;
+        STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + NUM_EPI_WARPS * WARP_EPI_BYTES;
     static_assert(SMEM <= 232448, "kernel exceeds 227 KB of shared memory");
 };
 
@@ -329,6 +351,14 @@ struct EpiStage {
             bulk_commit();
         }
     }
+    __device__ __forceinline__ void put3d_packed(const CUtensorMap* map, int lane, const uint32_t* pk, int c0, int c1,
+                                                 int c2) {
+        const uint32_t src = begin_packed(lane, pk);
+        if (lane == 0) {
+            tma_store_3d(map, src, c0, c1, c2);
+            bulk_commit();
+        }
+    }
     __device__ __forceinline__ void put3d(const CUtensorMap* map, int lane, const float* v, int c0, int c1, int c2) {
         const uint32_t src = begin(lane, v);
         if (lane == 0) {
@@ -419,12 +449,12 @@ __device__ __forceinline__ TileInfo tile_info(const Params& p, const int32_t* ps
         ti.e = t / per_e;
         const int r = t % per_e;
         ti.m0 = (r / p.n_tiles) * TM;
-        ti.n0 = (r % p.n_tiles) * BN;
+        ti.n0 = (r % p.n_tiles) * KCfg<KIND, CG>::TN;
         ti.krow0 = ps[ti.e];
         ti.kb = (p.counts[ti.e] + BK - 1) / BK;  // pad rows past the count are zero: skip them
     } else {
         const int mt = t / p.n_tiles;
-        ti.n0 = (t % p.n_tiles) * BN;
+        ti.n0 = (t % p.n_tiles) * KCfg<KIND, CG>::TN;
         ti.m0 = mt * TM;
         int lo = 0, hi = p.nr - 1;  // last expert whose padded start <= m0
         while (lo < hi) {
@@ -452,33 +482,43 @@ __device__ __forceinline__ void load_stage(const Params& p, const TileInfo& ti, 
     };
     // A of the by-row kinds: [m_own, m_own + 128) x [k0, k0 + 64), K-major
     auto ldA_rows = [&]() { ld(sA, &p.mapA, k0, m_own); };
-    constexpr int BC = Cfg<CG>::B_COLS;
-    const int nb = ti.n0 + BC * (int)rank;  // this CTA's first B column of the tile
+    constexpr int BC = KCfg<KIND, CG>::B_COLS;
+    const int nb = ti.n0 + BC * (int)rank;  // this CTA's first B column of the tile (one region)
     if constexpr (KIND == GemmKind::FwdGateUp) {
         ldA_rows();
         const int row = ti.e * p.H + k0;
-        const int n0 = ti.n0 / 2;  // 128 gate columns + 128 up columns per tile
-        if (CG == 1 || rank == 0) {
-            ld(sB + 0 * 8192, &p.mapB0, n0, row);
-            ld(sB + 1 * 8192, &p.mapB0, n0 + 64, row);
-        }
-        if (CG == 1 || rank == 1) {
-            const uint32_t o = CG == 1 ? 2 * 8192 : 0;
-            ld(sB + o, &p.mapB1, n0, row);
-            ld(sB + o + 8192, &p.mapB1, n0 + 64, row);
+        // region q: [gate 128 | up 128] columns of I columns n0/2 + 128 q ..; CTA 0 loads the gate
+        // half of every region, CTA 1 the up half
+        static_assert(CG == 2, "FwdGateUp runs on CTA pairs");
+#pragma unroll
+        for (int q = 0; q < KCfg<KIND, CG>::REGIONS; ++q) {
+            const int n0 = ti.n0 / 2 + (BN / 2) * q;
+            const uint32_t d = sB + q * KCfg<KIND, CG>::REGION_BYTES;
+            const CUtensorMap* m = rank == 0 ? &p.mapB0 : &p.mapB1;
+            ld(d, m, n0, row);
+            ld(d + 8192, m, n0 + 64, row);
         }
     } else if constexpr (KIND == GemmKind::FwdDown) {
         ldA_rows();
         const int row = ti.e * p.I + k0;
+        // region q (MMA q) holds tile columns 256 q + 128 rank .. of this CTA, 2 boxes of 64
 #pragma unroll
-        for (int c = 0; c < BC / 64; ++c) ld(sB + c * 8192, &p.mapB0, nb + 64 * c, row);
+        for (int c = 0; c < BC / 64; ++c)
+            ld(sB + c * 8192, &p.mapB0, ti.n0 + BN * (c / 2) + (BN / 2) * (int)rank + 64 * (c % 2), row);
     } else if constexpr (KIND == GemmKind::BwdDownDgrad) {
         ldA_rows();
-        ld(sB, &p.mapB0, k0, ti.e * p.I + nb);
+#pragma unroll
+        for (int q = 0; q < KCfg<KIND, CG>::REGIONS; ++q)
+            ld(sB + q * KCfg<KIND, CG>::REGION_BYTES, &p.mapB0, k0, ti.e * p.I + ti.n0 + BN * q + (BN / 2) * (int)rank);
     } else if constexpr (KIND == GemmKind::BwdDx) {
         ldA_rows();
-        if (k0 < p.I) ld(sB, &p.mapB0, k0, ti.e * p.H + nb);
-        else ld(sB, &p.mapB1, k0 - p.I, ti.e * p.H + nb);
+#pragma unroll
+        for (int q = 0; q < KCfg<KIND, CG>::REGIONS; ++q) {  // region q: tile rows 256 q + 128 rank ..
+            const int r = ti.e * p.H + ti.n0 + BN * q + (BN / 2) * (int)rank;
+            const uint32_t d = sB + q * KCfg<KIND, CG>::REGION_BYTES;
+            if (k0 < p.I) ld(d, &p.mapB0, k0, r);
+            else ld(d, &p.mapB1, k0 - p.I, r);
+        }
     } else if constexpr (KIND == GemmKind::RouterDx) {
         // K runs twice over the experts: dl_hi · Wrᵀ, then dl_lo · Wrᵀ into the same accumulator
         const int kh = (p.num_kb_fixed / 2) * BK;
@@ -495,7 +535,8 @@ __device__ __forceinline__ void load_stage(const Params& p, const TileInfo& ti, 
         ld(sA + 0, &p.mapA, m_own, row);
         ld(sA + 8192, &p.mapA, m_own + 64, row);
 #pragma unroll
-        for (int c = 0; c < BC / 64; ++c) ld(sB + c * 8192, &p.mapB0, nb + 64 * c, row);
+        for (int c = 0; c < BC / 64; ++c)
+            ld(sB + c * 8192, &p.mapB0, ti.n0 + BN * (c / 2) + (BN / 2) * (int)rank + 64 * (c % 2), row);
     }
 }
 
@@ -587,13 +628,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* gbase = smem_raw + (base - raw);
-    const uint32_t bar0 = base + STAGES * C::STAGE_BYTES;
+    const uint32_t bar0 = base + STAGES * KC::STAGE_BYTES;
     // barrier layout: full[S], empty[S], tfull[2], tempty[2], then the TMEM address slot
     auto full_bar = [&](int s) { return bar0 + 8u * s; };
     auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
     auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + a); };
     auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + 2 + a); };
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + STAGES * C::STAGE_BYTES + 8 * (2 * STAGES + 4));
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + STAGES * KC::STAGE_BYTES + 8 * (2 * STAGES + 4));
     // per epilogue warp: SLOTS output staging boxes; 1 KB aligned (bar0 is)
     const uint32_t epi_base = bar0 + 1024u;
 
@@ -654,7 +695,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                 const int m_own = ti.m0 + BM * (int)rank;
                 for (int kb = 0; kb < ti.kb; ++kb) {
                     mbar_wait(empty_bar(stage), phase ^ 1u, 0);
-                    const uint32_t sA = base + stage * C::STAGE_BYTES, sB = sA + A_BYTES;
+                    const uint32_t sA = base + stage * KC::STAGE_BYTES, sB = sA + A_BYTES;
                     uint32_t fb = full_bar(stage);
                     if constexpr (CG == 2) fb = map_to_rank(fb, 0);
                     if (leader) mbar_expect_tx(full_bar(stage), p.stage_tx);
@@ -673,15 +714,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
             int it = 0;
             for (int t = tfirst; t < ntiles; t += tstride, ++it) {
                 const TileInfo ti = tile_info<KIND, CG>(p, ps, t);
-                const int acc = it & 1;
-                const uint32_t acc_phase = (it >> 1) & 1;
-                mbar_wait(tempty_bar(acc), acc_phase ^ 1u, 2);
-                tc_fence_after();
-                const uint32_t tacc = tmem_base + acc * BN;
-                for (int kb = 0; kb < ti.kb; ++kb) {
-                    mbar_wait(full_bar(stage), phase, 1);
+                // two double-buffered 256-column accumulators, or (wide) one 512-column accumulator
+                // whose halves are freed separately (tempty[0], tempty[1])
+                const int acc = KC::WIDE ? 0 : it & 1;
+                const uint32_t acc_phase = KC::WIDE ? it & 1 : (it >> 1) & 1;
+                if (!KC::WIDE || ti.kb == 0) {
+                    mbar_wait(tempty_bar(acc), acc_phase ^ 1u, 2);
+                    if (KC::WIDE) mbar_wait(tempty_bar(1), acc_phase ^ 1u, 2);
                     tc_fence_after();
-                    const uint32_t sA = base + stage * C::STAGE_BYTES, sB = sA + A_BYTES;
+                }
+                const uint32_t tacc = tmem_base + acc * BN;
+                // MMAs of k-block kb into region q (N = 256 columns each)
+                auto issue = [&](int stg, int kb, int q) {
+                    const uint32_t sA = base + stg * KC::STAGE_BYTES, sB = sA + A_BYTES + q * KC::REGION_BYTES;
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k) {
                         uint64_t ad, bd;
@@ -689,15 +734,54 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                         else ad = umma_desc(sA + k * 32, 16, 1024);
                         if (Traits<KIND>::b_mn) bd = umma_desc(sB + k * 2048, 8192, 1024);
                         else bd = umma_desc(sB + k * 32, 16, 1024);
-                        if constexpr (CG == 1) umma_f16(tacc, ad, bd, idesc, (kb | k) ? 1u : 0u);
-                        else umma_f16_cg2(tacc, ad, bd, idesc, (kb | k) ? 1u : 0u);
+                        if constexpr (CG == 1) umma_f16(tacc + q * BN, ad, bd, idesc, (kb | k) ? 1u : 0u);
+                        else umma_f16_cg2(tacc + q * BN, ad, bd, idesc, (kb | k) ? 1u : 0u);
                     }
+                };
+                auto release_stage = [&]() {
                     if constexpr (CG == 1) umma_commit(empty_bar(stage));
                     else umma_commit_cg2(empty_bar(stage));
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1u;
                     }
+                };
+                int kb0 = 0;
+                if constexpr (KC::WIDE) {
+                    // the first k-blocks' region-0 MMAs (every loaded stage) run while the epilogue
+                    // still drains region 1 of the previous tile; their region-1 MMAs follow
+                    const int na = ti.kb < STAGES ? ti.kb : STAGES;
+                    if (na > 0) {
+                        mbar_wait(tempty_bar(0), acc_phase ^ 1u, 2);
+                        tc_fence_after();
+                    }
+                    int sj = stage;
+                    uint32_t pj = phase;
+                    for (int j = 0; j < na; ++j) {
+                        mbar_wait(full_bar(sj), pj, 1);
+                        tc_fence_after();
+                        issue(sj, j, 0);
+                        if (++sj == STAGES) {
+                            sj = 0;
+                            pj ^= 1u;
+                        }
+                    }
+                    if (na > 0) {
+                        mbar_wait(tempty_bar(1), acc_phase ^ 1u, 2);
+                        tc_fence_after();
+                    }
+                    for (int j = 0; j < na; ++j) {
+                        issue(stage, j, 1);
+                        release_stage();
+                    }
+                    kb0 = na;
+                }
+                for (int kb = kb0; kb < ti.kb; ++kb) {
+                    mbar_wait(full_bar(stage), phase, 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int q = 0; q < KC::REGIONS; ++q) issue(stage, kb, q);
+                    release_stage();
                 }
                 if (ti.kb > 0) {
                     if constexpr (CG == 1) umma_commit(tfull_bar(acc));
@@ -722,8 +806,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
         for (int t = tfirst; t < ntiles; t += tstride, ++it) {
             TileInfo ti = tile_info<KIND, CG>(p, ps, t);
             ti.m0 += BM * (int)rank;  // this CTA's 128 rows of the pair's tile
-            const int acc = it & 1;
-            const uint32_t acc_phase = (it >> 1) & 1;
+            const int acc = KC::WIDE ? 0 : it & 1;
+            const uint32_t acc_phase = KC::WIDE ? it & 1 : (it >> 1) & 1;
             // this lane's row weight and (dgrad) G/U operands of the first chunk load while the
             // MMAs still run
             float wrow = 1.f;
@@ -736,132 +820,197 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
             }
             mbar_wait(tfull_bar(acc), acc_phase, 3);
             tc_fence_after();
-            const uint32_t tacc = tmem_base + ((uint32_t)(32 * quad) << 16) + acc * BN;
-            if constexpr (KIND == GemmKind::BwdDownDgrad) {
-                // SwiGLU backward (kernels.hpp:277-295) on the dH accumulator. G and U of this lane's
-                // row come straight from global into registers (ld.global.nc), one 32-column chunk
-                // ahead of the math (the first one before the accumulator wait). Weighted-H scheme
-                // (row_w): the accumulator is dH' = dout . Wd^T; dmul = w * dH', and the row's
-                // top-k weight-gradient partial dH' . silu(G) * U (= dout . y) goes to wpart
-                const bool wscheme = p.row_w != nullptr;
-                const int64_t grow = (int64_t)(ti.m0 + row0 + lane) * p.I;
-                float wdot = 0.f;
-#pragma unroll 1
-                for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
-                    const int col = ti.n0 + c;
-                    const bool live = col < p.I;  // I % 64 == 0: a chunk is all in or all out
-                    uint4 g4[4], u4[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        g4[q] = gq[q];
-                        u4[q] = uq[q];
-                    }
-                    if (c + 32 < (half + 1) * (BN / 2) && col + 32 < p.I) load_gu(p, grow + col + 32, gq, uq);
-                    uint32_t r[32];
-                    tmem_ld32(tacc + c, r);
-                    tmem_wait_ld();
-                    if (!live) continue;
-                    uint32_t dgp[16], dup[16];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t gw[4] = {g4[q].x, g4[q].y, g4[q].z, g4[q].w},
-                                       uw[4] = {u4[q].x, u4[q].y, u4[q].z, u4[q].w};
-#pragma unroll
-                        for (int h = 0; h < 4; ++h) {
-                            float dg2[2], du2[2];
-#pragma unroll
-                            for (int e = 0; e < 2; ++e) {
-                                const float x = e ? bf16_hi(gw[h]) : bf16_lo(gw[h]);
-                                const float uu = e ? bf16_hi(uw[h]) : bf16_lo(uw[h]);
-                                const float a = __uint_as_float(r[8 * q + 2 * h + e]);
-                                const float sg = __fdividef(1.f, 1.f + __expf(-x));
-                                const float xs = x * sg;  // silu(g)
-                                wdot = __fmaf_rn(a, xs * uu, wdot);
-                                const float d = a * wrow;
-                                du2[e] = xs * d;
-                                dg2[e] = uu * d * (sg * (1.f + x * (1.f - sg)));
-                            }
-                            dgp[4 * q + h] = pack_bf16(dg2[0], dg2[1]);
-                            dup[4 * q + h] = pack_bf16(du2[0], du2[1]);
+            const uint32_t tacc0 = tmem_base + ((uint32_t)(32 * quad) << 16) + acc * BN;
+            // drain one 256-column accumulator (`tacc`) holding tile columns ti.n0 ..
+            // next_n0 >= 0: the tile column base of the region drained after this one (wide dgrad:
+            // its first G/U chunk is prefetched at the end of this region)
+            auto drain = [&](const uint32_t tacc, const TileInfo& ti, int next_n0) {
+                if constexpr (KIND == GemmKind::BwdDownDgrad) {
+                    // SwiGLU backward (kernels.hpp:277-295) on the dH accumulator. G and U of this lane's
+                    // row come straight from global into registers (ld.global.nc), one 32-column chunk
+                    // ahead of the math (the first one before the accumulator wait). Weighted-H scheme
+                    // (row_w): the accumulator is dH' = dout . Wd^T; dmul = w * dH', and the row's
+                    // top-k weight-gradient partial dH' . silu(G) * U (= dout . y) goes to wpart
+                    const bool wscheme = p.row_w != nullptr;
+                    const int64_t grow = (int64_t)(ti.m0 + row0 + lane) * p.I;
+                    float wdot = 0.f;
+    #pragma unroll 1
+                    for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+                        const int col = ti.n0 + c;
+                        const bool live = col < p.I;  // I % 64 == 0: a chunk is all in or all out
+                        uint4 g4[4], u4[4];
+    #pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            g4[q] = gq[q];
+                            u4[q] = uq[q];
                         }
-                    }
-                    // (measured: TMA-staged stores beat direct register->global stores here,
-                    // 0.57 vs 0.61 ms per dgrad at config B)
-                    stg.put2d_packed(&p.mapO0, lane, dgp, col, ti.m0 + row0);
-                    stg.put2d_packed(&p.mapO0, lane, dup, p.I + col, ti.m0 + row0);
-                }
-                if (wscheme)
-                    p.wpart[(int64_t)(ti.m0 + row0 + lane) * (2 * p.n_tiles) + 2 * (ti.n0 / BN) + half] = wdot;
-            } else if constexpr (KIND == GemmKind::FwdGateUp) {
-                const int nbase = ti.n0 / 2;  // 128 gate + 128 up columns per tile
-                uint32_t r[32], r2[32];
-#pragma unroll 1
-                for (int c = half * (BN / 4); c < (half + 1) * (BN / 4); c += 32) {
-                    tmem_ld32(tacc + c, r);
-                    tmem_ld32(tacc + BN / 2 + c, r2);
-                    tmem_wait_ld();
-                    const int col = nbase + c;
-                    if (col >= p.I) continue;  // I % 64 == 0: all in or all out
-                    float gv[32], uv[32], hv[32];
-                    // G and U are stored rounded to bf16; H is computed from the rounded values
-#pragma unroll
-                    for (int j = 0; j < 32; j += 2) {
-                        const uint32_t gp = pack_bf16(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
-                        const uint32_t up = pack_bf16(__uint_as_float(r2[j]), __uint_as_float(r2[j + 1]));
-                        gv[j] = bf16_lo(gp);
-                        gv[j + 1] = bf16_hi(gp);
-                        uv[j] = bf16_lo(up);
-                        uv[j + 1] = bf16_hi(up);
-                    }
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) hv[j] = silu_f(gv[j]) * uv[j] * wrow;
-                    stg.put2d(&p.mapO0, lane, gv, col, ti.m0 + row0);
-                    stg.put2d(&p.mapO1, lane, uv, col, ti.m0 + row0);
-                    stg.put2d(&p.mapO2, lane, hv, col, ti.m0 + row0);
-                }
-            } else if constexpr (KIND == GemmKind::FwdDown || KIND == GemmKind::BwdDx) {
-                uint32_t r[32];
-                float v[32];
-#pragma unroll 1
-                for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
-                    tmem_ld32(tacc + c, r);
-                    tmem_wait_ld();
-                    const int col = ti.n0 + c;
-                    if (col >= p.H) continue;
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                    stg.put2d(&p.mapO0, lane, v, col, ti.m0 + row0);
-                }
-            } else if constexpr (KIND == GemmKind::WgradDown || KIND == GemmKind::WgradGateUp) {
-                // out[e][m][n] * scale through 3-D maps: rows past the expert's M are clipped
-                uint32_t r[32];
-                float v[32];
-                const bool zero = ti.kb == 0;
-#pragma unroll 1
-                for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
-                    if (!zero) {
+                        if (c + 32 < (half + 1) * (BN / 2)) {
+                            if (col + 32 < p.I) load_gu(p, grow + col + 32, gq, uq);
+                        } else if (next_n0 >= 0 && next_n0 + half * (BN / 2) < p.I) {
+                            load_gu(p, grow + next_n0 + half * (BN / 2), gq, uq);
+                        }
+                        uint32_t r[32];
                         tmem_ld32(tacc + c, r);
                         tmem_wait_ld();
+                        if (!live) continue;
+                        uint32_t dgp[16], dup[16];
+    #pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint32_t gw[4] = {g4[q].x, g4[q].y, g4[q].z, g4[q].w},
+                                           uw[4] = {u4[q].x, u4[q].y, u4[q].z, u4[q].w};
+    #pragma unroll
+                            for (int h = 0; h < 4; ++h) {
+                                float dg2[2], du2[2];
+    #pragma unroll
+                                for (int e = 0; e < 2; ++e) {
+                                    const float x = e ? bf16_hi(gw[h]) : bf16_lo(gw[h]);
+                                    const float uu = e ? bf16_hi(uw[h]) : bf16_lo(uw[h]);
+                                    const float a = __uint_as_float(r[8 * q + 2 * h + e]);
+                                    const float sg = __fdividef(1.f, 1.f + __expf(-x));
+                                    const float xs = x * sg;  // silu(g)
+                                    wdot = __fmaf_rn(a, xs * uu, wdot);
+                                    const float d = a * wrow;
+                                    du2[e] = xs * d;
+                                    dg2[e] = uu * d * (sg * (1.f + x * (1.f - sg)));
+                                }
+                                dgp[4 * q + h] = pack_bf16(dg2[0], dg2[1]);
+                                dup[4 * q + h] = pack_bf16(du2[0], du2[1]);
+                            }
+                        }
+                        // (measured: TMA-staged stores beat direct register->global stores here,
+                        // 0.57 vs 0.61 ms per dgrad at config B)
+                        stg.put2d_packed(&p.mapO0, lane, dgp, col, ti.m0 + row0);
+                        stg.put2d_packed(&p.mapO0, lane, dup, p.I + col, ti.m0 + row0);
                     }
+                    if (wscheme)
+                        p.wpart[(int64_t)(ti.m0 + row0 + lane) * (2 * ((p.I + BN - 1) / BN)) + 2 * (ti.n0 / BN) + half] = wdot;
+                } else if constexpr (KIND == GemmKind::FwdGateUp) {
+                    const int nbase = ti.n0 / 2;  // 128 gate + 128 up columns per tile
+                    uint32_t r[32], r2[32];
+    #pragma unroll 1
+                    for (int c = half * (BN / 4); c < (half + 1) * (BN / 4); c += 32) {
+                        tmem_ld32(tacc + c, r);
+                        tmem_ld32(tacc + BN / 2 + c, r2);
+                        tmem_wait_ld();
+                        const int col = nbase + c;
+                        if (col >= p.I) continue;  // I % 64 == 0: all in or all out
+                        float gv[32], uv[32], hv[32];
+                        // G and U are stored rounded to bf16; H is computed from the rounded values
+    #pragma unroll
+                        for (int j = 0; j < 32; j += 2) {
+                            const uint32_t gp = pack_bf16(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
+                            const uint32_t up = pack_bf16(__uint_as_float(r2[j]), __uint_as_float(r2[j + 1]));
+                            gv[j] = bf16_lo(gp);
+                            gv[j + 1] = bf16_hi(gp);
+                            uv[j] = bf16_lo(up);
+                            uv[j + 1] = bf16_hi(up);
+                        }
+    #pragma unroll
+                        for (int j = 0; j < 32; ++j) hv[j] = silu_f(gv[j]) * uv[j] * wrow;
+                        stg.put2d(&p.mapO0, lane, gv, col, ti.m0 + row0);
+                        stg.put2d(&p.mapO1, lane, uv, col, ti.m0 + row0);
+                        stg.put2d(&p.mapO2, lane, hv, col, ti.m0 + row0);
+                    }
+                } else if constexpr (KIND == GemmKind::FwdDown || KIND == GemmKind::BwdDx) {
+                    uint32_t r[32];
+                    float v[32];
+    #pragma unroll 1
+                    for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+                        tmem_ld32(tacc + c, r);
+                        tmem_wait_ld();
+                        const int col = ti.n0 + c;
+                        if (col >= p.H) continue;
+    #pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                        stg.put2d(&p.mapO0, lane, v, col, ti.m0 + row0);
+                    }
+                } else if constexpr (KIND == GemmKind::WgradDown || KIND == GemmKind::WgradGateUp) {
+                    // out[e][m][n] * scale through 3-D maps: rows past the expert's M are clipped
+                    uint32_t r[32];
+                    float v[32];
+                    const bool zero = ti.kb == 0;
+    #pragma unroll 1
+                    for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+                        if (!zero) {
+                            tmem_ld32(tacc + c, r);
+                            tmem_wait_ld();
+                        }
+    #pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] = zero ? 0.f : __uint_as_float(r[j]) * p.scale;
+                        const int col = ti.n0 + c;
+                        if constexpr (KIND == GemmKind::WgradDown) {
+                            if (col < p.H) stg.put3d(&p.mapO0, lane, v, col, ti.m0 + row0, ti.e);
+                        } else {
+                            if (col < p.I) stg.put3d(&p.mapO0, lane, v, col, ti.m0 + row0, ti.e);
+                            else if (col < 2 * p.I) stg.put3d(&p.mapO1, lane, v, col - p.I, ti.m0 + row0, ti.e);
+                        }
+                    }
+                } else {
+                    epilogue_tile<KIND>(p, ti, tacc, 32 * quad + lane, ti.kb == 0, half);
+                }
+            };
+            auto release = [&](int a) {  // this warp is done reading accumulator (half) a
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 1) mbar_arrive(tempty_bar(a));
+                    else mbar_arrive_cluster(tempty0 + 8u * a);
+                }
+            };
+            if constexpr (KC::WIDE && (KIND == GemmKind::FwdDown || KIND == GemmKind::BwdDx ||
+                                       KIND == GemmKind::WgradDown || KIND == GemmKind::WgradGateUp)) {
+                // a half leaves TMEM first (this warp's 32 rows x 128 columns, packed to bf16 in
+                // registers), is released to the next tile's MMAs, and only then goes out through the
+                // staging slots — the stores no longer hold the accumulator
+                constexpr bool kWgrad = KIND == GemmKind::WgradDown || KIND == GemmKind::WgradGateUp;
+                const bool zero = kWgrad && ti.kb == 0;  // empty expert: zero weight gradient
+                const float sc = kWgrad ? p.scale : 1.f;
+#pragma unroll 1
+                for (int hh = 0; hh < KC::REGIONS; ++hh) {
+                    uint32_t pk[4][16];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = zero ? 0.f : __uint_as_float(r[j]) * p.scale;
-                    const int col = ti.n0 + c;
-                    if constexpr (KIND == GemmKind::WgradDown) {
-                        if (col < p.H) stg.put3d(&p.mapO0, lane, v, col, ti.m0 + row0, ti.e);
-                    } else {
-                        if (col < p.I) stg.put3d(&p.mapO0, lane, v, col, ti.m0 + row0, ti.e);
-                        else if (col < 2 * p.I) stg.put3d(&p.mapO1, lane, v, col - p.I, ti.m0 + row0, ti.e);
+                    for (int ch = 0; ch < 4; ch += 2) {
+                        uint32_t r0[32], r1[32];
+                        if (!zero) {
+                            tmem_ld32(tacc0 + BN * hh + half * (BN / 2) + 32 * ch, r0);
+                            tmem_ld32(tacc0 + BN * hh + half * (BN / 2) + 32 * (ch + 1), r1);
+                            tmem_wait_ld();
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            pk[ch][j] = zero ? 0u : pack_bf16(__uint_as_float(r0[2 * j]) * sc, __uint_as_float(r0[2 * j + 1]) * sc);
+                            pk[ch + 1][j] =
+                                zero ? 0u : pack_bf16(__uint_as_float(r1[2 * j]) * sc, __uint_as_float(r1[2 * j + 1]) * sc);
+                        }
+                    }
+                    release(hh);
+#pragma unroll
+                    for (int ch = 0; ch < 4; ++ch) {
+                        const int col = ti.n0 + BN * hh + half * (BN / 2) + 32 * ch;
+                        if constexpr (KIND == GemmKind::FwdDown || KIND == GemmKind::BwdDx) {
+                            if (col < p.H) stg.put2d_packed(&p.mapO0, lane, pk[ch], col, ti.m0 + row0);
+                        } else if constexpr (KIND == GemmKind::WgradDown) {
+                            if (col < p.H) stg.put3d_packed(&p.mapO0, lane, pk[ch], col, ti.m0 + row0, ti.e);
+                        } else {
+                            if (col < p.I) stg.put3d_packed(&p.mapO0, lane, pk[ch], col, ti.m0 + row0, ti.e);
+                            else if (col < 2 * p.I)
+                                stg.put3d_packed(&p.mapO1, lane, pk[ch], col - p.I, ti.m0 + row0, ti.e);
+                        }
                     }
                 }
+            } else if constexpr (KC::WIDE) {
+#pragma unroll 1
+                for (int hh = 0; hh < KC::REGIONS; ++hh) {
+                    TileInfo th = ti;
+                    th.n0 += BN * hh;
+                    drain(tacc0 + BN * hh, th, hh + 1 < KC::REGIONS ? th.n0 + BN : -1);
+                    release(hh);
+                }
             } else {
-                epilogue_tile<KIND>(p, ti, tacc, 32 * quad + lane, ti.kb == 0, half);
+                drain(tacc0, ti, -1);
+                release(acc);
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                if constexpr (CG == 1) mbar_arrive(tempty_bar(acc));
-                else mbar_arrive_cluster(tempty0 + 8u * acc);
-            }
+
         }
         if constexpr (KC::TMA_EPI) stg.drain(lane);  // the bulk stores have left shared memory
     }
@@ -1038,7 +1187,9 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
     }
     switch (a.kind) {
         case GemmKind::FwdGateUp: {
-            p.n_tiles = (int)ceil_div(I, BN / 2);
+            using K0 = KCfg<GemmKind::FwdGateUp, G>;
+            p.n_tiles = (int)ceil_div(I, K0::TN / 2);
+            p.stage_tx = G * K0::STAGE_BYTES;
             p.mapA = make_map(a.x, H, P, 64, BM);
             p.mapB0 = make_map(a.wg, I, nr * H, 64, 64);
             p.mapB1 = make_map(a.wu, I, nr * H, 64, 64);
@@ -1050,7 +1201,9 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             break;
         }
         case GemmKind::FwdDown: {
-            p.n_tiles = (int)ceil_div(H, BN);
+            using K1 = KCfg<GemmKind::FwdDown, G>;
+            p.n_tiles = (int)ceil_div(H, K1::TN);
+            p.stage_tx = G * K1::STAGE_BYTES;
             p.mapA = make_map(a.h, I, P, 64, BM);
             p.mapB0 = make_map(a.wd, H, nr * I, 64, 64);
             p.mapB1 = p.mapB0;
@@ -1060,7 +1213,9 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             break;
         }
         case GemmKind::BwdDownDgrad: {
-            p.n_tiles = (int)ceil_div(I, BN);
+            using K2 = KCfg<GemmKind::BwdDownDgrad, G>;
+            p.n_tiles = (int)ceil_div(I, K2::TN);
+            p.stage_tx = G * K2::STAGE_BYTES;
             p.mapA = make_map(a.dy, H, P, 64, BM);
             p.mapB0 = make_map(a.wd, H, nr * I, 64, C2::B_COLS);
             p.mapB1 = p.mapB0;
@@ -1070,7 +1225,9 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             break;
         }
         case GemmKind::BwdDx: {
-            p.n_tiles = (int)ceil_div(H, BN);
+            using K3 = KCfg<GemmKind::BwdDx, G>;
+            p.n_tiles = (int)ceil_div(H, K3::TN);
+            p.stage_tx = G * K3::STAGE_BYTES;
             p.mapA = make_map(a.dgu, 2 * I, P, 64, BM);
             p.mapB0 = make_map(a.wg, I, nr * H, 64, C2::B_COLS);
             p.mapB1 = make_map(a.wu, I, nr * H, 64, C2::B_COLS);
@@ -1086,7 +1243,8 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.mapB1 = p.mapB0;
             p.mapO0 = make_map3(a.out0, H, I, nr);
             p.m_tiles_fixed = (int)ceil_div(I, BM * G);
-            p.n_tiles = (int)ceil_div(H, BN);
+            p.n_tiles = (int)ceil_div(H, KCfg<GemmKind::WgradDown, G>::TN);
+            p.stage_tx = G * KCfg<GemmKind::WgradDown, G>::STAGE_BYTES;
             grid = (int)std::min<int64_t>(grid, G * nr * p.m_tiles_fixed * p.n_tiles);
             launch_kind<GemmKind::WgradDown, G>(p, grid, st);
             break;
@@ -1099,7 +1257,8 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.mapO0 = make_map3(a.out0, I, H, nr);
             p.mapO1 = make_map3(a.out1, I, H, nr);
             p.m_tiles_fixed = (int)ceil_div(H, BM * G);
-            p.n_tiles = (int)ceil_div(2 * I, BN);
+            p.n_tiles = (int)ceil_div(2 * I, KCfg<GemmKind::WgradGateUp, G>::TN);
+            p.stage_tx = G * KCfg<GemmKind::WgradGateUp, G>::STAGE_BYTES;
             grid = (int)std::min<int64_t>(grid, G * nr * p.m_tiles_fixed * p.n_tiles);
             launch_kind<GemmKind::WgradGateUp, G>(p, grid, st);
             break;
