@@ -998,6 +998,43 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                         }
                     }
                 }
+            } else if constexpr (KC::WIDE && KIND == GemmKind::FwdGateUp) {
+                // per region: this warp's two gate chunks and their up chunks leave TMEM rounded to
+                // bf16 (what is stored; H is computed from the rounded values), the region is released,
+                // then G, U and H' = w * silu(G) * U go out through the staging slots
+#pragma unroll 1
+                for (int hh = 0; hh < KC::REGIONS; ++hh) {
+                    uint32_t gp[2][16], up[2][16];
+#pragma unroll
+                    for (int ch = 0; ch < 2; ++ch) {
+                        uint32_t r[32], r2[32];
+                        const int c = half * (BN / 4) + 32 * ch;
+                        tmem_ld32(tacc0 + BN * hh + c, r);
+                        tmem_ld32(tacc0 + BN * hh + BN / 2 + c, r2);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            gp[ch][j] = pack_bf16(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+                            up[ch][j] = pack_bf16(__uint_as_float(r2[2 * j]), __uint_as_float(r2[2 * j + 1]));
+                        }
+                    }
+                    release(hh);
+#pragma unroll
+                    for (int ch = 0; ch < 2; ++ch) {
+                        const int col = (ti.n0 + BN * hh) / 2 + half * (BN / 4) + 32 * ch;
+                        if (col >= p.I) continue;  // I % 64 == 0: all in or all out
+                        uint32_t hp[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const float g0 = bf16_lo(gp[ch][j]), g1 = bf16_hi(gp[ch][j]);
+                            const float u0 = bf16_lo(up[ch][j]), u1 = bf16_hi(up[ch][j]);
+                            hp[j] = pack_bf16(silu_f(g0) * u0 * wrow, silu_f(g1) * u1 * wrow);
+                        }
+                        stg.put2d_packed(&p.mapO0, lane, gp[ch], col, ti.m0 + row0);
+                        stg.put2d_packed(&p.mapO1, lane, up[ch], col, ti.m0 + row0);
+                        stg.put2d_packed(&p.mapO2, lane, hp, col, ti.m0 + row0);
+                    }
+                }
             } else if constexpr (KC::WIDE) {
 #pragma unroll 1
                 for (int hh = 0; hh < KC::REGIONS; ++hh) {
