@@ -130,8 +130,8 @@ def bind_numa_local(torch, gpu: int):
 
 
 # the committed `ncu --set full` capture whose DRAM bytes back roofline.traffic (named, not globbed)
-GEMM_TRAFFIC_FILE = os.path.join("profiles", "r01s3_ncu_traffic.json")
-ADAMW_TRAFFIC_FILE = os.path.join("profiles", "r01_ncu_adamw_traffic.json")
+GEMM_TRAFFIC_FILE = os.path.join("profiles", "r02_ncu_gemm_traffic.json")
+ADAMW_TRAFFIC_FILE = os.path.join("profiles", "r02_ncu_adamw_traffic.json")
 DATASHEET_BF16_TFLOPS = 2250.0  # dense bf16, B200 datasheet
 
 
