@@ -76,11 +76,20 @@ struct WideKind {
     static constexpr bool value = K == GemmKind::FwdGateUp || K == GemmKind::FwdDown || K == GemmKind::BwdDx ||
                                   K == GemmKind::WgradDown || K == GemmKind::WgradGateUp;
 };
+// (the dgrad was also measured wide as four N = 128 regions released one by one, its epilogue
+// holding 64 accumulator columns per warp: 475 -> 597 us)
+template <GemmKind K>
+struct RegionN {
+    static constexpr int value = 256;
+};
+constexpr int MAX_REGIONS = 2;
 template <GemmKind K, int CG>
 struct KCfg {
     static constexpr bool WIDE = CG == 2 && WideKind<K>::value;
     static constexpr int TN = WIDE ? 2 * BN : BN;  // N columns of a tile
-    static constexpr int REGIONS = TN / BN;        // N = 256 MMAs per k-step
+    static constexpr int RN = WIDE ? RegionN<K>::value : BN;  // N columns per MMA
+    static constexpr int REGIONS = TN / RN;        // MMAs per k-step (accumulator regions)
+    static_assert(REGIONS <= MAX_REGIONS, "too many accumulator regions");
     static constexpr int B_COLS = TN / CG;         // B columns held per CTA
     static constexpr int REGION_BYTES = (B_COLS / REGIONS) * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_COLS * BK * 2;
@@ -509,12 +518,13 @@ __device__ __forceinline__ void load_stage(const Params& p, const TileInfo& ti, 
         ldA_rows();
 #pragma unroll
         for (int q = 0; q < KCfg<KIND, CG>::REGIONS; ++q)
-            ld(sB + q * KCfg<KIND, CG>::REGION_BYTES, &p.mapB0, k0, ti.e * p.I + ti.n0 + BN * q + (BN / 2) * (int)rank);
+            ld(sB + q * KCfg<KIND, CG>::REGION_BYTES, &p.mapB0, k0,
+               ti.e * p.I + ti.n0 + KCfg<KIND, CG>::RN * q + (KCfg<KIND, CG>::RN / 2) * (int)rank);
     } else if constexpr (KIND == GemmKind::BwdDx) {
         ldA_rows();
 #pragma unroll
         for (int q = 0; q < KCfg<KIND, CG>::REGIONS; ++q) {  // region q: tile rows 256 q + 128 rank ..
-            const int r = ti.e * p.H + ti.n0 + BN * q + (BN / 2) * (int)rank;
+            const int r = ti.e * p.H + ti.n0 + KCfg<KIND, CG>::RN * q + (KCfg<KIND, CG>::RN / 2) * (int)rank;
             const uint32_t d = sB + q * KCfg<KIND, CG>::REGION_BYTES;
             if (k0 < p.I) ld(d, &p.mapB0, k0, r);
             else ld(d, &p.mapB1, k0 - p.I, r);
@@ -634,7 +644,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
     auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
     auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + a); };
     auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + 2 + a); };
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + STAGES * KC::STAGE_BYTES + 8 * (2 * STAGES + 4));
+    uint32_t* tmem_slot =
+        reinterpret_cast<uint32_t*>(gbase + STAGES * KC::STAGE_BYTES + 8 * (2 * STAGES + 2 + MAX_REGIONS));
     // per epilogue warp: SLOTS output staging boxes; 1 KB aligned (bar0 is)
     const uint32_t epi_base = bar0 + 1024u;
 
@@ -651,10 +662,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
             mbar_init(full_bar(s), 1);
             mbar_init(empty_bar(s), 1);
         }
-        for (int a = 0; a < 2; ++a) {
-            mbar_init(tfull_bar(a), 1);
+        for (int a = 0; a < 2; ++a) mbar_init(tfull_bar(a), 1);
+        for (int a = 0; a < MAX_REGIONS; ++a)
             mbar_init(tempty_bar(a), NUM_EPI_WARPS * CG);  // the leader's counts both CTAs' epilogues
-        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -720,7 +730,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                 const uint32_t acc_phase = KC::WIDE ? it & 1 : (it >> 1) & 1;
                 if (!KC::WIDE || ti.kb == 0) {
                     mbar_wait(tempty_bar(acc), acc_phase ^ 1u, 2);
-                    if (KC::WIDE) mbar_wait(tempty_bar(1), acc_phase ^ 1u, 2);
+                    if (KC::WIDE)
+                        for (int q = 1; q < KC::REGIONS; ++q) mbar_wait(tempty_bar(q), acc_phase ^ 1u, 2);
                     tc_fence_after();
                 }
                 const uint32_t tacc = tmem_base + acc * BN;
@@ -734,8 +745,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                         else ad = umma_desc(sA + k * 32, 16, 1024);
                         if (Traits<KIND>::b_mn) bd = umma_desc(sB + k * 2048, 8192, 1024);
                         else bd = umma_desc(sB + k * 32, 16, 1024);
-                        if constexpr (CG == 1) umma_f16(tacc + q * BN, ad, bd, idesc, (kb | k) ? 1u : 0u);
-                        else umma_f16_cg2(tacc + q * BN, ad, bd, idesc, (kb | k) ? 1u : 0u);
+                        if constexpr (CG == 1) umma_f16(tacc + q * KC::RN, ad, bd, idesc, (kb | k) ? 1u : 0u);
+                        else umma_f16_cg2(tacc + q * KC::RN, ad, bd, idesc, (kb | k) ? 1u : 0u);
                     }
                 };
                 auto release_stage = [&]() {
@@ -749,31 +760,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                 int kb0 = 0;
                 if constexpr (KC::WIDE) {
                     // the first k-blocks' region-0 MMAs (every loaded stage) run while the epilogue
-                    // still drains region 1 of the previous tile; their region-1 MMAs follow
+                    // still drains the later regions of the previous tile; each later region's MMAs
+                    // follow as soon as it is released
                     const int na = ti.kb < STAGES ? ti.kb : STAGES;
-                    if (na > 0) {
-                        mbar_wait(tempty_bar(0), acc_phase ^ 1u, 2);
+#pragma unroll 1
+                    for (int q = 0; q < KC::REGIONS && na > 0; ++q) {
+                        mbar_wait(tempty_bar(q), acc_phase ^ 1u, 2);
                         tc_fence_after();
-                    }
-                    int sj = stage;
-                    uint32_t pj = phase;
-                    for (int j = 0; j < na; ++j) {
-                        mbar_wait(full_bar(sj), pj, 1);
-                        tc_fence_after();
-                        issue(sj, j, 0);
-                        if (++sj == STAGES) {
-                            sj = 0;
-                            pj ^= 1u;
+                        int sj = stage;
+                        uint32_t pj = phase;
+                        for (int j = 0; j < na; ++j) {
+                            if (q == 0) {
+                                mbar_wait(full_bar(sj), pj, 1);
+                                tc_fence_after();
+                            }
+                            issue(sj, j, q);
+                            if (++sj == STAGES) {
+                                sj = 0;
+                                pj ^= 1u;
+                            }
                         }
                     }
-                    if (na > 0) {
-                        mbar_wait(tempty_bar(1), acc_phase ^ 1u, 2);
-                        tc_fence_after();
-                    }
-                    for (int j = 0; j < na; ++j) {
-                        issue(stage, j, 1);
-                        release_stage();
-                    }
+                    for (int j = 0; j < na; ++j) release_stage();
                     kb0 = na;
                 }
                 for (int kb = kb0; kb < ti.kb; ++kb) {
@@ -881,9 +889,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                         // 0.57 vs 0.61 ms per dgrad at config B)
                         stg.put2d_packed(&p.mapO0, lane, dgp, col, ti.m0 + row0);
                         stg.put2d_packed(&p.mapO0, lane, dup, p.I + col, ti.m0 + row0);
+                        if (wscheme && (col & 63) == 32) {  // end of a 64-column weight-gradient slot
+                            p.wpart[(int64_t)(ti.m0 + row0 + lane) * (p.I / 64) + col / 64] = wdot;
+                            wdot = 0.f;
+                        }
                     }
-                    if (wscheme)
-                        p.wpart[(int64_t)(ti.m0 + row0 + lane) * (2 * ((p.I + BN - 1) / BN)) + 2 * (ti.n0 / BN) + half] = wdot;
                 } else if constexpr (KIND == GemmKind::FwdGateUp) {
                     const int nbase = ti.n0 / 2;  // 128 gate + 128 up columns per tile
                     uint32_t r[32], r2[32];
@@ -1254,7 +1264,7 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.n_tiles = (int)ceil_div(I, K2::TN);
             p.stage_tx = G * K2::STAGE_BYTES;
             p.mapA = make_map(a.dy, H, P, 64, BM);
-            p.mapB0 = make_map(a.wd, H, nr * I, 64, C2::B_COLS);
+            p.mapB0 = make_map(a.wd, H, nr * I, 64, K2::RN / 2);
             p.mapB1 = p.mapB0;
             p.mapO0 = make_store_map(a.out0, 2 * I, P);
             p.num_kb_fixed = (int)ceil_div(H, BK);

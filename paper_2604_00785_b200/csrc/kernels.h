@@ -153,7 +153,7 @@ struct Sm100GemmArgs {
     // bf16 layer (weighted-H scheme): row_w [P] = each padded row's routing weight. FwdGateUp
     // stores H' = w * silu(G) * U; BwdDownDgrad takes the UNweighted dout rows as dY, scales its
     // accumulator by w and leaves the top-k weight-gradient partial dots acc . silu(G) * U in
-    // wpart [P, 2 * ceil(I / 256)] (null row_w: plain semantics, dY already weighted)
+    // wpart [P, I / 64] (null row_w: plain semantics, dY already weighted)
     const float* row_w;
     float* wpart;
     int num_sms;

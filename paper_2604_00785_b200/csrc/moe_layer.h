@@ -137,10 +137,9 @@ class MoeLayer {
                     const float* aux_probs_grad, T* dx, T* drouter, T* dgate, T* dup, T* ddown);
 
     void mark(int stage, bool end);
-    void check_expert_ids();
-    // partial weight-gradient dots per padded row left by the dgrad epilogue (two per 256-column
-    // n-tile of I)
-    int64_t wparts() const { return 2 * ceil_div(cfg_.intermediate, (int64_t)256); }  // throws ContractError if an index kernel flagged an id outside [0, N)
+    void check_expert_ids();  // throws ContractError if an index kernel flagged an id outside [0, N)
+    // partial weight-gradient dots per padded row left by the dgrad epilogue (one per 64 columns of I)
+    int64_t wparts() const { return ceil_div(cfg_.intermediate, (int64_t)64); }
     void set_dispatch_tables();
     struct GraphCache {
         std::vector<const void*> key;
