@@ -17,8 +17,9 @@ int b2x_grouped_gemm(b2_ctx* ctx, int kind, int hidden, int intermediate, int nr
                      const int32_t* counts, int64_t pmax, const void* x, const void* wg, const void* wu, const void* wd, const void* g,
                      const void* u, const void* h, const void* dy, const void* dgu, void* out0, void* out1,
                      void* out2, float scale);
-/* EP > 1, bf16: overlap (1, default) the backward's dX return with the weight-gradient
- * GEMMs (side stream, reduced GEMM grid) or run it after them (0). */
+/* EP >= 4, bf16: overlap (1, default) the backward's dX return with the weight-gradient
+ * GEMMs (side stream, GEMM grid reduced by 32 SMs) or run it after them (0); at EP 2 the
+ * return always runs after them (measured faster). */
 int b2x_moe_set_overlap_return(b2_moe* m, int on);
 #ifdef __cplusplus
 }

@@ -283,7 +283,7 @@ void MoeLayer::ep_barrier(cudaStream_t st) {
 }
 
 bool MoeLayer::overlap_return() const {
-    return dtype_ == BF16 && cfg_.ep > 1 && side_ != nullptr && overlap_opt_;
+    return dtype_ == BF16 && cfg_.ep >= kOverlapMinEp && side_ != nullptr && overlap_opt_;
 }
 
 const char* MoeLayer::stage_name(int s) {

@@ -194,9 +194,13 @@ class MoeLayer {
     void ep_setup();
     void ep_barrier(cudaStream_t st = nullptr);
     // bf16, EP > 1: the backward returns dX / top-k weight gradients on a side stream while
-    // the weight-gradient GEMMs run on num_sms - kCommSms SMs (16: measured best of 16/24/32 at EP=4)
+    // the weight-gradient GEMMs run on num_sms - kCommSms SMs. Measured with the wide GEMM tiles
+    // (tools/timeline.py --graph, same 4-GPU box): EP 4: 8 / 16 / 32 / 48 / 64 SMs 6.41 / 6.05 /
+    // 5.66 / 5.77 / 5.98 ms per step, serial return 5.76; EP 2: serial 5.04-5.06 against 5.17-5.29
+    // with 32 SMs — so the return overlaps from EP 4 up and runs after the GEMMs at EP 2
     bool overlap_return() const;
-    static constexpr int kCommSms = 16;
+    static constexpr int kCommSms = 32;
+    static constexpr int kOverlapMinEp = 4;
     bool overlap_opt_ = true;
     cudaStream_t side_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
