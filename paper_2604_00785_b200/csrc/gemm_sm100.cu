@@ -78,17 +78,12 @@ struct WideKind {
 };
 // (the dgrad was also measured wide as four N = 128 regions released one by one, its epilogue
 // holding 64 accumulator columns per warp: 475 -> 597 us)
-template <GemmKind K>
-struct RegionN {
-    static constexpr int value = 256;
-};
 constexpr int MAX_REGIONS = 2;
 template <GemmKind K, int CG>
 struct KCfg {
     static constexpr bool WIDE = CG == 2 && WideKind<K>::value;
     static constexpr int TN = WIDE ? 2 * BN : BN;  // N columns of a tile
-    static constexpr int RN = WIDE ? RegionN<K>::value : BN;  // N columns per MMA
-    static constexpr int REGIONS = TN / RN;        // MMAs per k-step (accumulator regions)
+    static constexpr int REGIONS = TN / BN;        // N = 256 MMAs per k-step (accumulator regions)
     static_assert(REGIONS <= MAX_REGIONS, "too many accumulator regions");
     static constexpr int B_COLS = TN / CG;         // B columns held per CTA
     static constexpr int REGION_BYTES = (B_COLS / REGIONS) * BK * 2;
@@ -519,12 +514,12 @@ __device__ __forceinline__ void load_stage(const Params& p, const TileInfo& ti, 
 #pragma unroll
         for (int q = 0; q < KCfg<KIND, CG>::REGIONS; ++q)
             ld(sB + q * KCfg<KIND, CG>::REGION_BYTES, &p.mapB0, k0,
-               ti.e * p.I + ti.n0 + KCfg<KIND, CG>::RN * q + (KCfg<KIND, CG>::RN / 2) * (int)rank);
+               ti.e * p.I + ti.n0 + BN * q + (BN / 2) * (int)rank);
     } else if constexpr (KIND == GemmKind::BwdDx) {
         ldA_rows();
 #pragma unroll
         for (int q = 0; q < KCfg<KIND, CG>::REGIONS; ++q) {  // region q: tile rows 256 q + 128 rank ..
-            const int r = ti.e * p.H + ti.n0 + KCfg<KIND, CG>::RN * q + (KCfg<KIND, CG>::RN / 2) * (int)rank;
+            const int r = ti.e * p.H + ti.n0 + BN * q + (BN / 2) * (int)rank;
             const uint32_t d = sB + q * KCfg<KIND, CG>::REGION_BYTES;
             if (k0 < p.I) ld(d, &p.mapB0, k0, r);
             else ld(d, &p.mapB1, k0 - p.I, r);
@@ -745,8 +740,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                         else ad = umma_desc(sA + k * 32, 16, 1024);
                         if (Traits<KIND>::b_mn) bd = umma_desc(sB + k * 2048, 8192, 1024);
                         else bd = umma_desc(sB + k * 32, 16, 1024);
-                        if constexpr (CG == 1) umma_f16(tacc + q * KC::RN, ad, bd, idesc, (kb | k) ? 1u : 0u);
-                        else umma_f16_cg2(tacc + q * KC::RN, ad, bd, idesc, (kb | k) ? 1u : 0u);
+                        if constexpr (CG == 1) umma_f16(tacc + q * BN, ad, bd, idesc, (kb | k) ? 1u : 0u);
+                        else umma_f16_cg2(tacc + q * BN, ad, bd, idesc, (kb | k) ? 1u : 0u);
                     }
                 };
                 auto release_stage = [&]() {
@@ -830,9 +825,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
             tc_fence_after();
             const uint32_t tacc0 = tmem_base + ((uint32_t)(32 * quad) << 16) + acc * BN;
             // drain one 256-column accumulator (`tacc`) holding tile columns ti.n0 ..
-            // next_n0 >= 0: the tile column base of the region drained after this one (wide dgrad:
-            // its first G/U chunk is prefetched at the end of this region)
-            auto drain = [&](const uint32_t tacc, const TileInfo& ti, int next_n0) {
+            auto drain = [&](const uint32_t tacc, const TileInfo& ti) {
                 if constexpr (KIND == GemmKind::BwdDownDgrad) {
                     // SwiGLU backward (kernels.hpp:277-295) on the dH accumulator. G and U of this lane's
                     // row come straight from global into registers (ld.global.nc), one 32-column chunk
@@ -852,11 +845,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                             g4[q] = gq[q];
                             u4[q] = uq[q];
                         }
-                        if (c + 32 < (half + 1) * (BN / 2)) {
-                            if (col + 32 < p.I) load_gu(p, grow + col + 32, gq, uq);
-                        } else if (next_n0 >= 0 && next_n0 + half * (BN / 2) < p.I) {
-                            load_gu(p, grow + next_n0 + half * (BN / 2), gq, uq);
-                        }
+                        if (c + 32 < (half + 1) * (BN / 2) && col + 32 < p.I) load_gu(p, grow + col + 32, gq, uq);
                         uint32_t r[32];
                         tmem_ld32(tacc + c, r);
                         tmem_wait_ld();
@@ -1050,11 +1039,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) grouped_gemm_kernel(const __gr
                 for (int hh = 0; hh < KC::REGIONS; ++hh) {
                     TileInfo th = ti;
                     th.n0 += BN * hh;
-                    drain(tacc0 + BN * hh, th, hh + 1 < KC::REGIONS ? th.n0 + BN : -1);
+                    drain(tacc0 + BN * hh, th);
                     release(hh);
                 }
             } else {
-                drain(tacc0, ti, -1);
+                drain(tacc0, ti);
                 release(acc);
             }
 
@@ -1264,7 +1253,7 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
             p.n_tiles = (int)ceil_div(I, K2::TN);
             p.stage_tx = G * K2::STAGE_BYTES;
             p.mapA = make_map(a.dy, H, P, 64, BM);
-            p.mapB0 = make_map(a.wd, H, nr * I, 64, K2::RN / 2);
+            p.mapB0 = make_map(a.wd, H, nr * I, 64, C2::B_COLS);
             p.mapB1 = p.mapB0;
             p.mapO0 = make_store_map(a.out0, 2 * I, P);
             p.num_kb_fixed = (int)ceil_div(H, BK);
