@@ -29,6 +29,7 @@ __device__ __forceinline__ uint16_t bf16_bits_rne(float f) {
 struct AdamWDev {
     double lr, b1, b2, omb1, omb2, eps, lr_wd, bc1, bc2;
     double rbc1, rbc2;  // RN(1/bc1), RN(1/bc2), computed on the host
+    double lr_rbc1;     // lr * rbc1 (the fast path's estimate only)
 };
 
 // a / b, correctly rounded, for the step constants b = bc1, bc2 with y = RN(1/b): q0 = a*y is
@@ -43,6 +44,26 @@ __device__ __forceinline__ double div_const(double a, double b, double y) {
     return a == 0.0 ? a : (isfinite(a) ? q2 : q0);
 }
 
+// The update term U = RN(RN(lr * RN(m / bc1)) / RN(RN(sqrt(RN(v / bc2))) + eps)) in the
+// reference's correctly rounded steps (div_const, __dsqrt_rn, __ddiv_rn).
+__device__ __forceinline__ double update_exact(double md, double vd, const AdamWDev& c) {
+    const double num = __dmul_rn(c.lr, div_const(md, c.bc1, c.rbc1));
+    const double den = __dadd_rn(__dsqrt_rn(div_const(vd, c.bc2, c.rbc2)), c.eps);
+    return __ddiv_rn(num, den);
+}
+
+// Fast path with an exactness certificate. U' comes from the MUFU rsqrt / rcp seeds of the fp64
+// values (rsqrt.approx.f64 / rcp.approx.f64: measured within 2^-19.9, tools/adamw_seed_probe.cu)
+// and one fp64 Newton step each, so |U' - U| <= 2^-36 |U| even for seeds 2x worse (the step
+// squares the seed error; ~12 fp64 roundings and the reference's own 6 ulp add 2^-49). Hence
+// W1 - U lies within tol = 2^-30 |U'| + 2^-50 |W'| of W' = W1 - U' (margins 64x / 4x). Float
+// rounding is monotonic: when W' - tol and W' + tol round to the same float, so does W1 - U,
+// and that float is the reference's master. Otherwise (W' within tol of a rounding boundary:
+// ~1e-4 of the elements at training scale) and for inputs outside the seeds' normal range,
+// non-finite values included, the exact sequence runs — bitwise the reference's either way.
+// Against the exact sequence alone: 0.59 -> 0.37 G fp64 instructions per 0.5 G elements and
+// 5.59-5.70 -> 5.25-5.29 ms per G elements (tools/adamw_probe.py), where a kernel with the
+// same loads and stores and no fp64 math takes 5.08 ms.
 __device__ __forceinline__ void adamw_elem(float& master, float& m, float& v, float g, const AdamWDev& c,
                                            float& wout_f) {
     double w = (double)master;
@@ -52,10 +73,29 @@ __device__ __forceinline__ void adamw_elem(float& master, float& m, float& v, fl
     const double vv = __dadd_rn(__dmul_rn(c.b2, (double)v), __dmul_rn(__dmul_rn(c.omb2, gd), gd));
     m = (float)mm;
     v = (float)vv;
-    const double num = __dmul_rn(c.lr, div_const((double)m, c.bc1, c.rbc1));
-    const double den = __dadd_rn(__dsqrt_rn(div_const((double)v, c.bc2, c.rbc2)), c.eps);
-    w = __dsub_rn(w, __ddiv_rn(num, den));
-    master = (float)w;
+    const double md = (double)m, vd = (double)v;
+    const double np = __dmul_rn(md, c.lr_rbc1);  // ~ lr * (m / bc1)
+    const double bp = __dmul_rn(vd, c.rbc2);     // ~ v / bc2
+    double y0, r0;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y0) : "d"(bp));
+    const double s0 = __dmul_rn(bp, y0);
+    const double sq = __fma_rn(__fma_rn(-s0, s0, bp), __dmul_rn(0.5, y0), s0);  // ~ sqrt(v / bc2)
+    const double den = __dadd_rn(sq, c.eps);
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(den));
+    const double q0 = __dmul_rn(np, r0);
+    // m == +-0 with a positive denominator (v > 0, or v == 0 and eps > 0): U = +-0 exactly, with
+    // m's sign, which matters when W1 is a zero too
+    const bool mzero = md == 0.0 && (vd > 0.0 || (vd == 0.0 && c.eps > 0.0));
+    const double up = mzero ? np : __fma_rn(__fma_rn(-den, q0, np), r0, q0);
+    const double wn = __dsub_rn(w, up);
+    const double tol = __fma_rn(fabs(up), 0x1p-30, __dmul_rn(fabs(wn), 0x1p-50));
+    const float lo = __double2float_rn(__dsub_rn(wn, tol)), hi = __double2float_rn(__dadd_rn(wn, tol));
+    const bool ok = mzero || (bp >= 0x1p-120 && bp <= 0x1p120 && __float_as_uint(lo) == __float_as_uint(hi));
+    if (__builtin_expect(ok, 1)) {
+        master = mzero ? (float)wn : lo;
+    } else {
+        master = (float)__dsub_rn(w, update_exact(md, vd, c));
+    }
     wout_f = master;
 }
 
@@ -197,6 +237,7 @@ void launch_adamw_full(const AdamWKernelArgs& a, const double* norm_sq, double c
     c.bc2 = a.bc2;
     c.rbc1 = 1.0 / a.bc1;
     c.rbc2 = 1.0 / a.bc2;
+    c.lr_rbc1 = a.lr * c.rbc1;
     const float gs = (float)a.grad_scale;
     const bool vec = a.grad_dtype == BF16 && a.weight_dtype == BF16 && a.round_bf16 && a.n % 4 == 0 &&
                      ((uintptr_t)a.master % 16 == 0) && ((uintptr_t)a.m % 16 == 0) && ((uintptr_t)a.v % 16 == 0) &&
@@ -431,6 +472,7 @@ void launch_adamw_chunks(const OptSeg* segs, const OptChunk* chunks, const int32
     c.bc2 = a.bc2;
     c.rbc1 = 1.0 / a.bc1;
     c.rbc2 = 1.0 / a.bc2;
+    c.lr_rbc1 = a.lr * c.rbc1;
     static int grid_cap = 0, per_sm_blocks = 1;  // resident blocks (persistent grid)
     if (grid_cap == 0) {
         int dev = 0, sms = 148, per_sm = 0;

@@ -137,3 +137,56 @@ def test_state_checkpoint_restore_continues_bitwise(b2ctx, orc):
     for p, n in enumerate(NUMEL):
         for a, b in zip(opt.gather_state(p, n), opt2.gather_state(p, n)):
             assert np.array_equal(a, b)
+
+
+def _adversarial_state(n, seed):
+    """master / exp_avg / exp_avg_sq / grad covering the update's corner cases: signed zeros,
+    float subnormals, magnitudes from 1e-38 to 1e30, exact powers of two, v = 0 with m != 0,
+    and a few non-finite values, mixed with ordinary training-scale values."""
+    rng = np.random.default_rng(seed)
+
+    def mixed(scale):
+        x = (rng.standard_normal(n) * scale).astype(np.float32)
+        pick = rng.integers(0, 12, n)
+        x[pick == 0] = 0.0
+        x[pick == 1] = -0.0
+        x[pick == 2] = (rng.standard_normal((pick == 2).sum()) * 1e-40).astype(np.float32)  # subnormal
+        x[pick == 3] = (10.0 ** rng.uniform(-38, 30, (pick == 3).sum()) * rng.choice([-1, 1], (pick == 3).sum()))
+        x[pick == 4] = np.ldexp(1.0, rng.integers(-30, 10, (pick == 4).sum())).astype(np.float32)
+        return x
+
+    master = mixed(0.05)
+    m = mixed(1e-3)
+    v = np.abs(mixed(1e-6)).astype(np.float32)
+    g = mixed(0.02)
+    m[rng.integers(0, n, 8)] = 1e-3  # v stays 0 there when g is 0: the sqrt(0) branch
+    for arr, val in ((g, np.inf), (g, np.nan), (master, -np.inf), (v, np.nan)):
+        arr[rng.integers(0, n, 3)] = val
+    return master, m, v, g
+
+
+@pytest.mark.parametrize("wdt", ["f32", "bf16"])
+@pytest.mark.parametrize("step,lr", [(0, 4e-4), (7, 1e-2), (2500, 0.0)])
+def test_adamw_update_adversarial_bitwise(b2ctx, orc, wdt, step, lr):
+    """adamw_update (optim.cpp:88-107) on corner-case states: the kernel's fast path (MUFU
+    seeds + one Newton step, checked against the float rounding boundary) must fall back to
+    the exactly rounded sequence wherever that check is not conclusive, so master, moments
+    and weight are bit-identical to the reference's (NaN payloads aside)."""
+    b2, ctx = b2ctx
+    n = (1 << 20) + 4 if wdt == "bf16" else 200_003
+    master, m, v, g = _adversarial_state(n, seed=step + 11)
+    dt = torch.bfloat16 if wdt == "bf16" else torch.float32
+    G = torch.from_numpy(g).to(dt).cuda()
+    g_seen = G.float().cpu().numpy()
+    dM, dm, dv = (torch.from_numpy(a.copy()).cuda() for a in (master, m, v))
+    W = torch.empty(n, dtype=dt, device="cuda")
+    cfg = b2.AdamWConfig()
+    b2.adamw_update(ctx, dM, dm, dv, G, lr, step, cfg, W, round_bf16=True)
+    torch.cuda.synchronize()
+    rm, rmo, rv, rw = orc.adamw_update(master, m, v, g_seen, lr, step, orc.adamw_cfg(), round_bf16=True)
+    for got, want in ((dM, rm), (dm, rmo), (dv, rv), (W.float(), rw)):
+        got = got.cpu().numpy()
+        nan = np.isnan(want)
+        assert np.array_equal(np.isnan(got), nan)
+        bad = got.view(np.uint32)[~nan] != want.view(np.uint32)[~nan]
+        assert not bad.any(), f"{bad.sum()} of {n} differ"
