@@ -313,7 +313,7 @@ def bench_adamw(torch, b2, ctx, dev, steps, warmup, world, rank, hbm_peak, dp=1,
                          "algorithmic_bytes_per_step": byt}}
 
 
-def zipf_tokens(torch, dev, S, Hd, N, s, seed):
+def zipf_tokens(torch, dev, S, Hd, N, s, seed, perm_seed=None):
     """Config E routing (logits[t,e] = log z_e + noise, z_e ∝ (e+1)^-s, identity
     expert permutation, the hottest experts on rank 0) through a router of realistic magnitude:
     x ~ N(1, 1), Wr = column-centred N(0, 1.2825/sqrt(H)) + log z_e / H, so x·Wr = mean(x_t) ·
@@ -322,6 +322,9 @@ def zipf_tokens(torch, dev, S, Hd, N, s, seed):
     g = torch.Generator(device=dev).manual_seed(seed)
     z = (torch.arange(N, device=dev, dtype=torch.float64) + 1.0) ** -s
     z = z / z.sum()
+    if perm_seed is not None:  # a seeded expert permutation pi instead of the identity (worst case)
+        pg = torch.Generator().manual_seed(perm_seed)
+        z = z[torch.randperm(N, generator=pg).to(dev)]
     x = torch.randn((S, Hd), device=dev, generator=g) + 1.0
     wn = torch.randn((Hd, N), device=dev, generator=g, dtype=torch.float64) * (1.2825 / Hd ** 0.5)
     wn -= wn.mean(0, keepdim=True)
@@ -329,14 +332,14 @@ def zipf_tokens(torch, dev, S, Hd, N, s, seed):
     return x.bfloat16(), router.bfloat16()
 
 
-def bench_zipf(torch, b2, ctx, dev, stream, world, rank, zipf_s, steps, warmup):
+def bench_zipf(torch, b2, ctx, dev, stream, world, rank, zipf_s, steps, warmup, perm_seed=None):
     """Mula-20B-A2B-shaped layer (H 2048, 96 experts top-8, ffn 1024; model.cpp:46-48) under
     Zipf-skewed routing, EP = world (config E): the load-imbalance stress line."""
     import torch.distributed as dist
     Nz = 96
     cfg = b2.MoeConfig(n_experts=Nz, top_k=K, hidden=H, intermediate=I, ep=world, token_block=8)
     NR = Nz // world
-    x, router = zipf_tokens(torch, dev, S, H, Nz, zipf_s, 4242 + rank)
+    x, router = zipf_tokens(torch, dev, S, H, Nz, zipf_s, 4242 + rank, perm_seed)
     if world > 1:  # one router for every rank (the tokens differ per rank)
         dist.broadcast(router, src=0)
     gen = torch.Generator(device=dev).manual_seed(99 + rank)
@@ -378,7 +381,8 @@ def bench_zipf(torch, b2, ctx, dev, stream, world, rank, zipf_s, steps, warmup):
     return {"metric": METRIC + " (Zipf-skewed routing)", "value": world * S / (ms * 1e-3), "unit": "tokens/s",
             "ms_per_step": ms, "zipf_s": zipf_s, "experts": Nz, "ep": world,
             "workload": f"Mula-20B-A2B layer shape: hidden 2048, 96 experts top-8, ffn 1024, {S} tokens/GPU, bf16, "
-                        f"Zipf s={zipf_s}, identity expert permutation",
+                        f"Zipf s={zipf_s}, " + ("identity expert permutation" if perm_seed is None
+                                                 else f"expert permutation seed {perm_seed}"),
             "rows_per_rank_max_over_mean": float(rows_max.item()) / (float(rows_sum.item()) / world),
             "rank0_rows_per_expert_max_over_mean": float(max(counts)) / max(1e-9, sum(counts) / len(counts))}
 

@@ -119,7 +119,8 @@ struct Params {
     __nv_bfloat16* out2;
     float scale;
     const float* row_w;   // FwdGateUp / BwdDownDgrad: per padded row routing weight (weighted-H scheme)
-    float* wpart;         // BwdDownDgrad with row_w: [P, 2 * n_tiles] partial weight-gradient dots
+    float* wpart;         // BwdDownDgrad with row_w: [P, I / 64] partial weight-gradient dots
+    const int32_t* eorder;  // by_k kinds: expert of the i-th group of tiles (null: i), longest first
     uint32_t idesc;       // instruction descriptor (runtime N for the router kinds)
     int umma_n;           // accumulator columns in use
     int b_chunks;         // 64-column B boxes per stage (MN-major B)
@@ -450,7 +451,7 @@ __device__ __forceinline__ TileInfo tile_info(const Params& p, const int32_t* ps
     }
     if (Traits<KIND>::by_k) {
         const int per_e = p.m_tiles_fixed * p.n_tiles;
-        ti.e = t / per_e;
+        ti.e = p.eorder ? p.eorder[t / per_e] : t / per_e;
         const int r = t % per_e;
         ti.m0 = (r / p.n_tiles) * TM;
         ti.n0 = (r % p.n_tiles) * KCfg<KIND, CG>::TN;
@@ -1191,6 +1192,7 @@ void launch_sm100_gemm(const Sm100GemmArgs& a, cudaStream_t st) {
     p.out2 = (__nv_bfloat16*)a.out2;
     p.row_w = a.row_w;
     p.wpart = a.wpart;
+    p.eorder = a.expert_order;
     if (a.kind == GemmKind::BwdDownDgrad && a.row_w) check(a.wpart != nullptr, "dgrad: row weights need wpart");
     const int64_t P = a.pmax, H = a.H, I = a.I, nr = a.nr;
     int grid = a.num_sms > 0 ? a.num_sms : 148;

@@ -120,7 +120,8 @@ __global__ void __launch_bounds__(1024) scan_kernel(const int32_t* __restrict__ 
                                                     int32_t* __restrict__ token_counts,
                                                     int32_t* __restrict__ cum_token_counts,
                                                     int32_t* __restrict__ pad_start,
-                                                    int32_t* __restrict__ cum_expert_counts) {
+                                                    int32_t* __restrict__ cum_expert_counts,
+                                                    int32_t* __restrict__ expert_order) {
     pdl_wait();
     pdl_launch();
     extern __shared__ int32_t tot[];  // [nr]
@@ -172,6 +173,16 @@ __global__ void __launch_bounds__(1024) scan_kernel(const int32_t* __restrict__ 
             pad_start[nr] = pcarry;
         }
     }
+    // (b') the experts by descending row count, ties by index: the weight-gradient GEMMs take
+    //      their per-expert tiles (K extent = the expert's rows) in this order, so the persistent
+    //      CTAs' static tile stride spreads the longest tiles first (an LPT-like schedule)
+    if (expert_order)
+        for (int e = threadIdx.x; e < nr; e += blockDim.x) {
+            const int ce = tot[e];
+            int r = 0;
+            for (int j = 0; j < nr; ++j) r += (tot[j] > ce) || (tot[j] == ce && j < e);
+            expert_order[r] = e;
+        }
     // (c) cum_expert_counts: exclusive scan of the per-token local counts
     const int64_t te = block_scan(
         T, [&](int64_t i) { return expert_counts[i]; }, [&](int64_t i, int64_t v) { cum_expert_counts[i] = (int32_t)v; },
@@ -252,7 +263,7 @@ void launch_routing_index(const RoutingIndexArgs& a, cudaStream_t st) {
     }
     launch_k(scan_kernel, dim3(1), dim3(1024), sizeof(int32_t) * a.nr, st, a.whist, nchunks, a.nr, a.expert_counts, a.T, a.wbase,
                                                          a.token_counts, a.cum_token_counts, a.pad_start,
-                                                         a.cum_expert_counts);
+                                                         a.cum_expert_counts, a.expert_order);
     B2_LAUNCH_CHECK();
     if (a.T > 0) {
         launch_k(scatter_kernel, dim3(nblk), dim3(32 * kWarpsPerCta), smem, st, a.gidx, a.T, a.K, a.n_start, a.nr, nchunks, a.wbase,

@@ -48,6 +48,7 @@ struct RoutingIndexArgs {
     const float* gw;             // [T, K] dispatch weights (with prow_w)
     float* prow_w;               // [pmax] padded row -> its routing weight (0 pad); nullptr: not needed
     int32_t* err;                // expert id out of range flag
+    int32_t* expert_order;       // [nr] experts by descending row count (wgrad tile order); nullptr: none
 };
 void launch_routing_index(const RoutingIndexArgs& a, cudaStream_t st);
 // TBS-blocked diagnostics partial_token_counts [nr*th] / partial_cum [nr*th+1] (moe.hpp:148-158)
@@ -156,6 +157,7 @@ struct Sm100GemmArgs {
     // wpart [P, I / 64] (null row_w: plain semantics, dY already weighted)
     const float* row_w;
     float* wpart;
+    const int32_t* expert_order;  // wgrad kinds: expert of the i-th group of tiles (null: i)
     int num_sms;
     // router kinds
     int S, N;                    // local tokens, experts

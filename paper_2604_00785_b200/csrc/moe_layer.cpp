@@ -143,6 +143,7 @@ MoeLayer::MoeLayer(Context& ctx, const MoeConfig& cfg, int dtype, int64_t max_to
     slot_prow_ = w.take<int32_t>(tmax_ * K);
     prow_src_ = w.take<int32_t>(pmax_);
     prow_w_ = w.take<float>(pmax_);
+    expert_order_ = w.take<int32_t>(nr);
     wpart_ = w.take<float>(pmax_ * wparts());
     mlp_in_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * H, 1));
     g_ = w.take_bytes(es * (size_t)std::max<int64_t>(pmax_ * I, 1));
@@ -484,6 +485,7 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
     ra.gw = gw_;
     ra.prow_w = dtype_ == BF16 ? prow_w_ : nullptr;  // weighted-H scheme of the tensor-core path
     ra.err = err_;
+    ra.expert_order = dtype_ == BF16 ? expert_order_ : nullptr;  // wgrad tile order
     launch_routing_index(ra, st);
     launches_ += 4;
     mark(kIndex, true);
@@ -674,6 +676,7 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         ga.wg = gate;
         ga.wu = up;
         ga.wd = down;
+        ga.expert_order = expert_order_;
         ga.g = g_;
         ga.u = u_;
         ga.h = h_;

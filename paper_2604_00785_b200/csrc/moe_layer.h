@@ -182,6 +182,7 @@ class MoeLayer {
         *prow_src_, *err_;
     float* prow_w_ = nullptr;  // bf16: padded row -> routing weight (0 pad), the weighted-H scheme
     float* wpart_ = nullptr;   // bf16: [pmax, wparts()] dgrad-epilogue partial dots
+    int32_t* expert_order_ = nullptr;  // bf16: local experts by descending rows (wgrad tile order)
     const float* gw_ = nullptr;    // dispatch weights (learned or FUR)
     const int32_t* gi_ = nullptr;  // dispatch indices
     // dtype buffers (padded row space)
