@@ -62,6 +62,12 @@ void launch_gather_rows(const T* x, const int32_t* prow_src, const int32_t* p_to
 template <typename T>
 void launch_zero_pad_rows(T* buf, const int32_t* prow_src, const int32_t* p_total, int W, int64_t pmax,
                           cudaStream_t st);
+// the gather token-major (each x row read once, written to its padded rows slot_prow[cec[t]..]),
+// pad rows zeroed in the same launch
+template <typename T>
+void launch_gather_tokens(const T* x, const int32_t* cec, const int32_t* slot_prow, int T_tok,
+                          const int32_t* prow_src, const int32_t* p_total, T* out, int H, int64_t pmax,
+                          cudaStream_t st);
 template <typename T>
 void launch_combine(const T* y, const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec,
                     const float* gw, T* out, int T_tok, int H, int K, cudaStream_t st);

@@ -497,7 +497,7 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
         launch_zero_pad_rows<T>((T*)mlp_in_, prow_src_, p_total, H, pmax_, st);
         launches_ += 2;
     } else {
-        launch_gather_rows<T>(x, prow_src_, p_total, (T*)mlp_in_, H, pmax_, st);
+        launch_gather_tokens<T>(x, cec_, slot_prow_, S, prow_src_, p_total, (T*)mlp_in_, H, pmax_, st);
         launches_ += 1;
     }
     mark(kGather, true);
@@ -653,7 +653,7 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
             launch_zero_pad_rows<T>((T*)dy_, prow_src_, p_total, H, pmax_, st);
             launches_ += 2;
         } else {
-            launch_gather_rows<T>(dout, prow_src_, p_total, (T*)dy_, H, pmax_, st);
+            launch_gather_tokens<T>(dout, cec_, slot_prow_, S, prow_src_, p_total, (T*)dy_, H, pmax_, st);
             launches_ += 1;
         }
     } else {

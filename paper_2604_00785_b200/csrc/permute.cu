@@ -96,6 +96,52 @@ __global__ void gather_rows_kernel(const T* __restrict__ x, const int32_t* __res
     }
 }
 
+// The same rows written token-major: warp per token t reads x[t] ONCE (up to 8 x 16 B per lane
+// in flight) and writes it to each of its padded rows slot_prow[cec[t] .. cec[t+1]); then the
+// pad rows (prow_src < 0, rows < *p_total) are zeroed. The row-major gather above re-reads a
+// token's row for each of its K rows, which the streaming writes evict from L2 in between
+// (ncu, round 1: 849 MB of DRAM traffic for 604 MB of algorithmic bytes).
+template <typename T>
+__global__ void gather_tokens_kernel(const T* __restrict__ x, const int32_t* __restrict__ cec,
+                                     const int32_t* __restrict__ slot_prow, int T_tok,
+                                     const int32_t* __restrict__ prow_src, const int32_t* __restrict__ p_total,
+                                     T* __restrict__ out, int H, int64_t pmax) {
+    pdl_wait();
+    pdl_launch();
+    const int lane = threadIdx.x % 32;
+    const int64_t warps = (int64_t)gridDim.x * blockDim.x / 32;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    const int nv = (int)((int64_t)H * sizeof(T) / 16);  // launcher: rows are 16-byte multiples
+    constexpr int B = 8;
+    for (int64_t t = w0; t < T_tok; t += warps) {
+        const int j0 = cec[t], j1 = cec[t + 1];
+        if (j0 == j1) continue;
+        const int4* src = reinterpret_cast<const int4*>(x + t * H);
+        for (int v0 = 0; v0 < nv; v0 += 32 * B) {
+            int4 val[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const int v = v0 + lane + 32 * b;
+                if (v < nv) val[b] = __ldg(src + v);
+            }
+            for (int j = j0; j < j1; ++j) {
+                int4* dst = reinterpret_cast<int4*>(out + (int64_t)slot_prow[j] * H);
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    const int v = v0 + lane + 32 * b;
+                    if (v < nv) dst[v] = val[b];
+                }
+            }
+        }
+    }
+    const int64_t P = min((int64_t)*p_total, pmax);
+    for (int64_t r = w0; r < P; r += warps) {
+        if (prow_src[r] >= 0) continue;
+        int4* d4 = reinterpret_cast<int4*>(out + r * H);
+        for (int v = lane; v < nv; v += 32) d4[v] = make_int4(0, 0, 0, 0);
+    }
+}
+
 // zero the pad rows of a padded buffer (rows < *p_total whose prow_src < 0)
 template <typename T>
 __global__ void zero_pad_rows_kernel(T* __restrict__ buf, const int32_t* __restrict__ prow_src,
@@ -425,6 +471,19 @@ void launch_gather_rows(const T* x, const int32_t* prow_src, const int32_t* p_to
 }
 
 template <typename T>
+void launch_gather_tokens(const T* x, const int32_t* cec, const int32_t* slot_prow, int T_tok,
+                          const int32_t* prow_src, const int32_t* p_total, T* out, int H, int64_t pmax,
+                          cudaStream_t st) {
+    if (((int64_t)H * sizeof(T)) % 16 != 0 || ((uintptr_t)x & 15) || ((uintptr_t)out & 15)) {  // not 16-B rows
+        launch_gather_rows<T>(x, prow_src, p_total, out, H, pmax, st);
+        return;
+    }
+    launch_k(gather_tokens_kernel<T>, dim3(grid_for_rows(std::max<int64_t>(pmax, T_tok))), dim3(256), 0, st, x, cec,
+             slot_prow, T_tok, prow_src, p_total, out, H, pmax);
+    B2_LAUNCH_CHECK();
+}
+
+template <typename T>
 void launch_zero_pad_rows(T* buf, const int32_t* prow_src, const int32_t* p_total, int W, int64_t pmax,
                           cudaStream_t st) {
     if (pmax <= 0) return;
@@ -513,6 +572,8 @@ void launch_swiglu_bwd(const T* g, const T* u, const T* dh, T* dgu, const int32_
 #define B2_INST(T)                                                                                              \
     template void launch_gather_rows<T>(const T*, const int32_t*, const int32_t*, T*, int, int64_t, cudaStream_t); \
     template void launch_zero_pad_rows<T>(T*, const int32_t*, const int32_t*, int, int64_t, cudaStream_t);        \
+    template void launch_gather_tokens<T>(const T*, const int32_t*, const int32_t*, int, const int32_t*,          \
+                                          const int32_t*, T*, int, int64_t, cudaStream_t);                       \
     template void launch_combine<T>(const T*, const int32_t*, const int32_t*, const int32_t*, const float*, T*, int, \
                                     int, int, cudaStream_t);                                                       \
     template void launch_out_reduction_bwd<T>(const T*, const T* const*, int, const T*, const int32_t*,           \
