@@ -71,7 +71,8 @@ template <typename T>
 __global__ void ep_combine_slots_kernel(const T* __restrict__ y, const int32_t* __restrict__ slot_prow,
                                            const int32_t* __restrict__ selected_k, const int32_t* __restrict__ cec,
                                            const float* __restrict__ gw, int K, int T_tot, int H,
-                                           T* __restrict__ own_slab) {
+                                           T* __restrict__ own_slab, T* const* __restrict__ push_slab, int S,
+                                           int me) {
     pdl_wait();
     pdl_launch();
     constexpr int V = 16 / sizeof(T);
@@ -81,7 +82,8 @@ __global__ void ep_combine_slots_kernel(const T* __restrict__ y, const int32_t* 
     for (int gid = (blockIdx.x * blockDim.x + threadIdx.x) / 32; gid < T_tot; gid += nw) {
         const int j0 = cec[gid], j1 = cec[gid + 1];
         if (j0 == j1) continue;
-        T* dst = own_slab + (int64_t)gid * H;
+        // push: straight into the source rank's slab, row [me][token] (NVLink stores)
+        T* dst = push_slab ? push_slab[gid / S] + ((int64_t)me * S + gid % S) * H : own_slab + (int64_t)gid * H;
         // all local slot rows of a column block are loaded together (<= 8 in flight)
         constexpr int MAXJ = 8;
         for (int v = lane; v < nv; v += 32) {
@@ -143,10 +145,13 @@ __global__ void ep_combine_slots_kernel(const T* __restrict__ y, const int32_t* 
 template <typename T>
 __device__ __forceinline__ void ep_pull_sum_token(const T* const* __restrict__ peer_slab,
                                                   const int32_t* __restrict__ gi_local, int S, int K, int E, int NR,
-                                                  int W, int me, T* __restrict__ out, int t, int lane) {
+                                                  int W, int me, T* __restrict__ out, int t, int lane, bool pushed) {
     unsigned mask = 0;
     for (int k = 0; k < K; ++k) mask |= 1u << (gi_local[(int64_t)t * K + k] / NR);
-    const int64_t row = (int64_t)me * S + t;
+    // pulled: owner r's own slab, row [me][t]; pushed: this rank's slab, row [r][t]
+    auto src = [&](int r) -> const T* {
+        return pushed ? peer_slab[me] + ((int64_t)r * S + t) * W : peer_slab[r] + ((int64_t)me * S + t) * W;
+    };
     if (((int64_t)W * sizeof(T)) % 16 == 0) {
         constexpr int V = 16 / sizeof(T), MAXR = 8;
         for (int v = lane; v < W / V; v += 32) {
@@ -157,7 +162,7 @@ __device__ __forceinline__ void ep_pull_sum_token(const T* const* __restrict__ p
 #pragma unroll
                 for (int q = 0; q < MAXR; ++q)
                     if (r0 + q < E && (mask >> (r0 + q) & 1u))
-                        raw[q] = __ldcv(reinterpret_cast<const int4*>(peer_slab[r0 + q] + row * W) + v);
+                        raw[q] = __ldcv(reinterpret_cast<const int4*>(src(r0 + q)) + v);
 #pragma unroll
                 for (int q = 0; q < MAXR; ++q) {
                     if (!(r0 + q < E && (mask >> (r0 + q) & 1u))) continue;
@@ -204,7 +209,7 @@ __device__ __forceinline__ void ep_pull_sum_token(const T* const* __restrict__ p
             bool any = false;
             for (int r = 0; r < E; ++r) {
                 if (!(mask >> r & 1u)) continue;
-                const float v = Elem<T>::to_f(__ldcv(peer_slab[r] + row * W + c));
+                const float v = Elem<T>::to_f(__ldcv(src(r) + c));
                 acc = any ? __fadd_rn(acc, v) : v;
                 any = true;
             }
@@ -215,12 +220,12 @@ __device__ __forceinline__ void ep_pull_sum_token(const T* const* __restrict__ p
 
 template <typename T>
 __global__ void ep_pull_sum_kernel(const T* const* __restrict__ peer_slab, const int32_t* __restrict__ gi_local,
-                                   int S, int K, int E, int NR, int W, int me, T* __restrict__ out) {
+                                   int S, int K, int E, int NR, int W, int me, T* __restrict__ out, int pushed) {
     pdl_wait();
     pdl_launch();
     const int lane = threadIdx.x % 32, nw = gridDim.x * blockDim.x / 32;
     for (int t = (blockIdx.x * blockDim.x + threadIdx.x) / 32; t < S; t += nw)  // grid-stride: any grid size
-        ep_pull_sum_token<T>(peer_slab, gi_local, S, K, E, NR, W, me, out, t, lane);
+        ep_pull_sum_token<T>(peer_slab, gi_local, S, K, E, NR, W, me, out, t, lane, pushed != 0);
 }
 
 // NVLink flag barrier over the EP group: every rank bumps its slot in every peer's flag
@@ -300,21 +305,21 @@ void launch_ep_gather_pull(const T* const* peer_src, int S, int T_tot, int H, co
 template <typename T>
 void launch_ep_combine_local(const T* y, const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec,
                              const float* gw, int K, int S, int T_tot, int H, T* own_slab, cudaStream_t st,
-                             int max_blocks) {
+                             int max_blocks, T* const* push_slab, int me) {
     if (T_tot <= 0) return;
     check(((int64_t)H * sizeof(T)) % 16 == 0, "ep combine: rows must be 16-byte multiples");
     const unsigned grid = max_blocks > 0 ? std::min<unsigned>(ep_grid(T_tot), (unsigned)max_blocks) : ep_grid(T_tot);
     launch_k(ep_combine_slots_kernel<T>, dim3(grid), dim3(256), 0, st, y, slot_prow, selected_k, cec, gw, K, T_tot, H,
-             own_slab);
+             own_slab, push_slab, S, me);
     B2_LAUNCH_CHECK();
 }
 
 template <typename T>
 void launch_ep_pull_sum(const T* const* peer_slab, const int32_t* gi_local, int S, int K, int E, int NR, int W, int me,
-                        T* out, cudaStream_t st, int max_blocks) {
+                        T* out, cudaStream_t st, int max_blocks, bool pushed) {
     if (S <= 0) return;
     const unsigned full = (unsigned)ceil_div(S, 8);
-    launch_k(ep_pull_sum_kernel<T>, dim3(max_blocks > 0 ? std::min<unsigned>(full, (unsigned)max_blocks) : full), dim3(256), 0, st, peer_slab, gi_local, S, K, E, NR, W, me, out);
+    launch_k(ep_pull_sum_kernel<T>, dim3(max_blocks > 0 ? std::min<unsigned>(full, (unsigned)max_blocks) : full), dim3(256), 0, st, peer_slab, gi_local, S, K, E, NR, W, me, out, pushed ? 1 : 0);
     B2_LAUNCH_CHECK();
 }
 
@@ -322,9 +327,9 @@ void launch_ep_pull_sum(const T* const* peer_slab, const int32_t* gi_local, int 
     template void launch_ep_gather_pull<T>(const T* const*, int, int, int, const int32_t*, const int32_t*, T*,    \
                                            cudaStream_t);                                                         \
     template void launch_ep_combine_local<T>(const T*, const int32_t*, const int32_t*, const int32_t*, const float*, \
-                                             int, int, int, int, T*, cudaStream_t, int);                         \
+                                             int, int, int, int, T*, cudaStream_t, int, T* const*, int);        \
     template void launch_ep_pull_sum<T>(const T* const*, const int32_t*, int, int, int, int, int, int, T*,        \
-                                        cudaStream_t, int);
+                                        cudaStream_t, int, bool);
 B2_EP_INST(float)
 B2_EP_INST(__nv_bfloat16)
 #undef B2_EP_INST

@@ -91,17 +91,18 @@ void launch_swiglu_bwd(const T* g, const T* u, const T* dh, T* dgu, const int32_
 template <typename T>
 void launch_ep_gather_pull(const T* const* peer_src, int S, int T_tot, int H, const int32_t* cec,
                            const int32_t* slot_prow, T* out, cudaStream_t st);
-// owner side of the pull-based combine: the token's (weighted) partial row into the owner's
-// OWN slab row [gid]; sources pull them after a barrier (launch_ep_pull_sum)
+// owner side of the combine: the token's (weighted) partial row into the owner's OWN slab row
+// [gid] (sources pull them after a barrier), or with push_slab (the E slab pointers) straight
+// into the source rank's slab row [me][token] (the sources then sum locally, pushed = true)
 template <typename T>
 void launch_ep_combine_local(const T* y, const int32_t* slot_prow, const int32_t* selected_k, const int32_t* cec,
                              const float* gw, int K, int S, int T_tot, int H, T* own_slab, cudaStream_t st,
-                             int max_blocks = 0);
+                             int max_blocks = 0, T* const* push_slab = nullptr, int me = 0);
 // out[t] = sum over t's owner ranks (in rank order) of peer_slab[r][(me*S + t)*W ..]
 template <typename T>
 // max_blocks > 0 caps the grid (a side-stream launch that must stay inside its reserved SMs)
 void launch_ep_pull_sum(const T* const* peer_slab, const int32_t* gi_local, int S, int K, int E, int NR, int W, int me,
-                        T* out, cudaStream_t st, int max_blocks = 0);
+                        T* out, cudaStream_t st, int max_blocks = 0, bool pushed = false);
 // [E][n] routing tables gathered from the peers' symmetric buffers
 void launch_ep_table_pull(const int32_t* const* peer_ids, const float* const* peer_w, int64_t n, int E,
                           int32_t* ids_all, float* w_all, cudaStream_t st);

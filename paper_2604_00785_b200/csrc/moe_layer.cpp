@@ -578,9 +578,10 @@ void MoeLayer::forward_t(const T* x, const T* router, const T* gate, const T* up
         // source pulls its rows from the owners and sums them in rank order
         // bf16: the rows are already weighted (y' = H' . Wd = w * y), fp32: weight here
         launch_ep_combine_local<T>((const T*)y_, slot_prow_, selected_k_, cec_, dtype_ == BF16 ? nullptr : gw_, K, S,
-                                   Tt, H, (T*)ret_f_, st);
+                                   Tt, H, (T*)ret_f_, st, 0, (T* const*)peer_tab_ + 2 * E, ctx_.coord_ep);
         ep_barrier();
-        launch_ep_pull_sum<T>((const T* const*)peer_tab_ + 2 * E, gi_local_, S, K, E, nr, H, ctx_.coord_ep, out, st);
+        launch_ep_pull_sum<T>((const T* const*)peer_tab_ + 2 * E, gi_local_, S, K, E, nr, H, ctx_.coord_ep, out, st, 0,
+                              true);
         launches_ += 2;
     } else {
         launch_combine<T>((const T*)y_, slot_prow_, selected_k_, cec_, dtype_ == BF16 ? nullptr : gw_, out, Tt, H, K,
@@ -710,10 +711,10 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
             // they never hold SMs the weight-gradient GEMM's CTAs are waiting for
             const int side_cap = kCommSms * 8;
             launch_ep_combine_local<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, K, S, Tt, H,
-                                       (T*)ret_b_, side_, side_cap);
+                                       (T*)ret_b_, side_, side_cap, (T* const*)peer_tab_ + 3 * E, ctx_.coord_ep);
             ep_barrier(side_);
             launch_ep_pull_sum<T>((const T* const*)peer_tab_ + 3 * E, gi_local_, S, K, E, nr, H, ctx_.coord_ep,
-                                  (T*)dx_exp_, side_, side_cap);
+                                  (T*)dx_exp_, side_, side_cap, true);
             launch_ep_pull_sum<float>((const float* const*)peer_tab_ + 4 * E, gi_local_, S, K, E, nr, K,
                                       ctx_.coord_ep, wgrad_local_, side_, side_cap);
             B2_CUDA(cudaEventRecord(ev_join_, side_));
@@ -836,10 +837,10 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         // output-reduction backward); after the barrier each source pulls and sums its rows in
         // rank order
         launch_ep_combine_local<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, K, S, Tt, H, (T*)ret_b_,
-                                   st);
+                                   st, 0, (T* const*)peer_tab_ + 3 * E, ctx_.coord_ep);
         ep_barrier();
         launch_ep_pull_sum<T>((const T* const*)peer_tab_ + 3 * E, gi_local_, S, K, E, nr, H, ctx_.coord_ep,
-                              (T*)dx_exp_, st);
+                              (T*)dx_exp_, st, 0, true);
         launch_ep_pull_sum<float>((const float* const*)peer_tab_ + 4 * E, gi_local_, S, K, E, nr, K, ctx_.coord_ep,
                                   wgrad_local_, st);
         wgrad_local = wgrad_local_;
