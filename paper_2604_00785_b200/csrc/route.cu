@@ -169,29 +169,38 @@ __device__ __forceinline__ void cp_async_wait() {
 // of a token-paired 8 x 4 tile, measured 158 -> 122 us at config B). The order of every
 // accumulator is still p = 0, 1, ... with one rounding per step, and bf16 x bf16 products are
 // exact in fp32, so the logits stay bit-identical to the reference's multiply-then-add.
-constexpr int kL3Tok = 32, kL3Exp = 64, kL3P = 32, kL3Stages = 4;
+constexpr int kL3P = 32, kL3Exp = 64, kL3Stages = 4;
+constexpr int kLogitsTok = 16;  // tokens per warp (16 or 32)
+template <int TOK>
 struct Logits3Smem {
-    uint16_t xraw[kL3Stages][kL3Tok][kL3P];  // 64 B rows, 16 B units swizzled by (t >> 1) & 3
-    uint16_t wraw[kL3Stages][kL3P][kL3Exp];  // 128 B rows, 16 B units swizzled by p & 7
-    float xs[2][kL3P][kL3Tok];               // transposed [p][token]
-    float ws[2][kL3P][kL3Exp];               // 16 B units (4 experts) swizzled by p & 15
+    uint16_t xraw[kL3Stages][TOK][kL3P];      // 64 B rows, 16 B units swizzled by (t >> 1) & 3
+    uint16_t wraw[kL3Stages][kL3P][kL3Exp];   // 128 B rows, 16 B units swizzled by p & 7
+    float xs[2][kL3P][TOK];                   // x transposed to [p][token], fp32
 };
 
-__global__ void __launch_bounds__(32) router_logits_bf16_t88_kernel(const __nv_bfloat16* __restrict__ x,
-                                                                    const __nv_bfloat16* __restrict__ w,
-                                                                    float* __restrict__ logits, int S, int H, int N) {
+// One warp per TOK tokens x 64 experts; a lane owns TOK/4 tokens x 8 experts. W is read in its
+// raw bf16 form straight from the cp.async ring (one 16 B load per p step, widened in
+// registers); only x goes through a transposed fp32 copy, 4 tokens per 16 B store. TOK = 16
+// runs twice the warps of TOK = 32 (two per scheduler instead of one, which left the FMA pipe
+// idle half the time: ncu issue 42 %, FMA 50 %).
+template <int TOK>
+__global__ void __launch_bounds__(32) router_logits_bf16_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                const __nv_bfloat16* __restrict__ w,
+                                                                float* __restrict__ logits, int S, int H, int N) {
     pdl_wait();
     pdl_launch();
+    using Sm = Logits3Smem<TOK>;
+    constexpr int TPL = TOK / 4;  // tokens per lane
     extern __shared__ __align__(128) uint8_t l3_smem[];
-    Logits3Smem& sm = *reinterpret_cast<Logits3Smem*>(l3_smem);
+    Sm& sm = *reinterpret_cast<Sm*>(l3_smem);
     const int lane = threadIdx.x;
-    const int t0 = blockIdx.x * kL3Tok, e0 = blockIdx.y * kL3Exp;
+    const int t0 = blockIdx.x * TOK, e0 = blockIdx.y * kL3Exp;
     const int nchunks = H / kL3P;
     auto issue = [&](int c) {
         if (c < nchunks) {
             const int s = c % kL3Stages, p0 = c * kL3P;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {  // x: 32 rows x 4 units
+            for (int q = 0; q < TOK / 8; ++q) {  // x: TOK rows x 4 units
                 const int idx = lane + 32 * q, t = idx / 4, u = idx % 4;
                 const bool ok = t0 + t < S;
                 const __nv_bfloat16* src = x + (int64_t)(ok ? t0 + t : 0) * H + p0 + 8 * u;
@@ -207,73 +216,75 @@ __global__ void __launch_bounds__(32) router_logits_bf16_t88_kernel(const __nv_b
         }
         cp_async_commit();
     };
+    // x of chunk c -> xs[c & 1]: lane (tq, u) < TOK moves tokens 4tq .. 4tq+3, p 8u .. 8u+7
     auto widen = [&](int c) {
-        const int s = c % kL3Stages, b = c & 1;
-        {  // x: lane = token, its 32 p values -> column `lane` of xs (consecutive lanes, no conflicts)
-            const int t = lane;
+        if (lane >= TOK) return;
+        const int s = c % kL3Stages, b = c & 1, tq = lane / 4, u = lane % 4;
+        uint4 r[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint4 r = *reinterpret_cast<const uint4*>(&sm.xraw[s][t][8 * (u ^ ((t >> 1) & 3))]);
-                const uint32_t v[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    sm.xs[b][8 * u + 2 * j][t] = __uint_as_float(v[j] << 16);
-                    sm.xs[b][8 * u + 2 * j + 1][t] = __uint_as_float(v[j] & 0xFFFF0000u);
-                }
-            }
+        for (int i = 0; i < 4; ++i) {
+            const int t = 4 * tq + i;
+            r[i] = *reinterpret_cast<const uint4*>(&sm.xraw[s][t][8 * (u ^ ((t >> 1) & 3))]);
         }
-        {  // W: lane = row p, 64 experts -> 16 units of 4 floats, unit k stored at k ^ (p & 15)
-            const int pp = lane;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const uint4 r = *reinterpret_cast<const uint4*>(&sm.wraw[s][pp][8 * (u ^ (pp & 7))]);
-                const uint32_t v[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int k = 2 * u + h;  // experts 4k .. 4k+3
-                    *reinterpret_cast<float4*>(&sm.ws[b][pp][4 * (k ^ (pp & 15))]) =
-                        make_float4(__uint_as_float(v[2 * h] << 16), __uint_as_float(v[2 * h] & 0xFFFF0000u),
-                                    __uint_as_float(v[2 * h + 1] << 16), __uint_as_float(v[2 * h + 1] & 0xFFFF0000u));
-                }
-            }
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t v0 = (&r[0].x)[j], v1 = (&r[1].x)[j], v2 = (&r[2].x)[j], v3 = (&r[3].x)[j];
+            *reinterpret_cast<float4*>(&sm.xs[b][8 * u + 2 * j][4 * tq]) =
+                make_float4(__uint_as_float(v0 << 16), __uint_as_float(v1 << 16), __uint_as_float(v2 << 16),
+                            __uint_as_float(v3 << 16));
+            *reinterpret_cast<float4*>(&sm.xs[b][8 * u + 2 * j + 1][4 * tq]) =
+                make_float4(__uint_as_float(v0 & 0xFFFF0000u), __uint_as_float(v1 & 0xFFFF0000u),
+                            __uint_as_float(v2 & 0xFFFF0000u), __uint_as_float(v3 & 0xFFFF0000u));
         }
     };
 
-    float2 acc[8][4];  // [token][expert pair]
+    float2 acc[TPL][4];  // [token][expert pair]
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < TPL; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
 
 #pragma unroll
-    for (int c = 0; c < kL3Stages; ++c) issue(c);
-    cp_async_wait<kL3Stages - 1>();
+    for (int c = 0; c < kL3Stages - 1; ++c) issue(c);
+    cp_async_wait<kL3Stages - 2>();
     __syncwarp();
     widen(0);
-    const int tg = lane % 4, eg = lane / 4;  // tokens 8*tg .. +7, experts 8*eg .. +7
+    const int tg = lane % 4, eg = lane / 4;  // tokens TPL*tg .., experts 8*eg .. +7
     for (int c = 0; c < nchunks; ++c) {
-        cp_async_wait<kL3Stages - 2>();
-        __syncwarp();  // chunk c widened; chunk c+1 landed; ring slot c free
+        // chunk c+1 landed (chunk c's x is in xs[c & 1]); ring slot (c - 1) % stages is free
+        cp_async_wait<kL3Stages - 3>();
+        __syncwarp();
         if (c + 1 < nchunks) widen(c + 1);
-        issue(c + kL3Stages);
-        const int b = c & 1;
-        float4 op[2][4];
-        auto ld = [&](float4 (&o)[4], int pp) {
-            o[0] = *reinterpret_cast<const float4*>(&sm.xs[b][pp][8 * tg]);
-            o[1] = *reinterpret_cast<const float4*>(&sm.xs[b][pp][8 * tg + 4]);
-            o[2] = *reinterpret_cast<const float4*>(&sm.ws[b][pp][4 * ((2 * eg) ^ (pp & 15))]);
-            o[3] = *reinterpret_cast<const float4*>(&sm.ws[b][pp][4 * ((2 * eg + 1) ^ (pp & 15))]);
+        issue(c + kL3Stages - 1);
+        const int b = c & 1, s = c % kL3Stages;
+        float4 xa[2][TPL / 4];
+        uint4 wb[2];
+        auto ld = [&](int q, int pp) {
+#pragma unroll
+            for (int h = 0; h < TPL / 4; ++h)
+                xa[q][h] = *reinterpret_cast<const float4*>(&sm.xs[b][pp][TPL * tg + 4 * h]);
+            wb[q] = *reinterpret_cast<const uint4*>(&sm.wraw[s][pp][8 * (eg ^ (pp & 7))]);
         };
-        ld(op[0], 0);
+        ld(0, 0);
 #pragma unroll
         for (int pp = 0; pp < kL3P; ++pp) {
-            if (pp + 1 < kL3P) ld(op[(pp + 1) & 1], pp + 1);
-            const float4 a0 = op[pp & 1][0], a1 = op[pp & 1][1], b0 = op[pp & 1][2], b1 = op[pp & 1][3];
-            const float xv[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const float2 wp[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
-                                  make_float2(b1.z, b1.w)};
+            if (pp + 1 < kL3P) ld((pp + 1) & 1, pp + 1);
+            float xv[TPL];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int h = 0; h < TPL / 4; ++h) {
+                const float4 a = xa[pp & 1][h];
+                xv[4 * h] = a.x;
+                xv[4 * h + 1] = a.y;
+                xv[4 * h + 2] = a.z;
+                xv[4 * h + 3] = a.w;
+            }
+            const uint32_t wr[4] = {wb[pp & 1].x, wb[pp & 1].y, wb[pp & 1].z, wb[pp & 1].w};
+            float2 wp[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                wp[j] = make_float2(__uint_as_float(wr[j] << 16), __uint_as_float(wr[j] & 0xFFFF0000u));
+#pragma unroll
+            for (int i = 0; i < TPL; ++i) {
                 const float2 xd = make_float2(xv[i], xv[i]);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) acc[i][j] = __ffma2_rn(xd, wp[j], acc[i][j]);
@@ -282,8 +293,8 @@ __global__ void __launch_bounds__(32) router_logits_bf16_t88_kernel(const __nv_b
     }
     const int e = e0 + 8 * eg;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int t = t0 + 8 * tg + i;
+    for (int i = 0; i < TPL; ++i) {
+        const int t = t0 + TPL * tg + i;
         if (t >= S) continue;
         float* dst = logits + (int64_t)t * N + e;
         if (e + 7 < N) {
@@ -636,14 +647,15 @@ void launch_router_logits(const T* x, const T* w, float* logits, int S, int H, i
     if (S == 0) return;
     if constexpr (sizeof(T) == 2) {
         if (H % kL3P == 0 && N % 8 == 0 && ((uintptr_t)x & 15) == 0 && ((uintptr_t)w & 15) == 0) {
-            static bool attr3 = false;
-            if (!attr3) {
-                B2_CUDA(cudaFuncSetAttribute(router_logits_bf16_t88_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)sizeof(Logits3Smem)));
-                attr3 = true;
+            constexpr int TOK = kLogitsTok;
+            static bool attr = false;
+            if (!attr) {
+                B2_CUDA(cudaFuncSetAttribute(router_logits_bf16_kernel<TOK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sizeof(Logits3Smem<TOK>)));
+                attr = true;
             }
-            dim3 grid((unsigned)ceil_div(S, kL3Tok), (unsigned)ceil_div(N, kL3Exp));
-            launch_k(router_logits_bf16_t88_kernel, dim3(grid), dim3(32), sizeof(Logits3Smem), st, x, w, logits, S, H, N);
+            dim3 grid((unsigned)ceil_div(S, TOK), (unsigned)ceil_div(N, kL3Exp));
+            launch_k(router_logits_bf16_kernel<TOK>, grid, dim3(32), sizeof(Logits3Smem<TOK>), st, x, w, logits, S, H, N);
             B2_LAUNCH_CHECK();
             return;
         }
