@@ -59,7 +59,7 @@ __device__ __forceinline__ void pdl_launch() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
 }
-bool pdl_enabled();  // B2_PDL=0 turns the attribute off (A/B checks)
+bool pdl_enabled();  // programmatic dependent launch on every hot-path kernel (capi.cpp)
 
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
