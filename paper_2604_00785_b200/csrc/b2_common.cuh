@@ -59,7 +59,17 @@ __device__ __forceinline__ void pdl_launch() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
 }
-bool pdl_enabled();  // programmatic dependent launch on every hot-path kernel (capi.cpp)
+// programmatic dependent launch (the next kernel's launch and prologue overlap the previous
+// one's tail), per host thread (capi.cpp); MoeLayer scopes it per call (see PdlScope)
+bool pdl_enabled();
+void set_pdl_enabled(bool on);
+struct PdlScope {
+    bool prev;
+    explicit PdlScope(bool on) : prev(pdl_enabled()) { set_pdl_enabled(on); }
+    ~PdlScope() { set_pdl_enabled(prev); }
+    PdlScope(const PdlScope&) = delete;
+    PdlScope& operator=(const PdlScope&) = delete;
+};
 
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {

@@ -108,9 +108,11 @@ struct b2_opt {
 };
 
 namespace b2 {
-// programmatic dependent launch on every hot-path kernel (the next kernel's launch and prologue
-// overlap the previous one's tail inside the CUDA graphs)
-bool pdl_enabled() { return true; }
+// programmatic dependent launch, on by default (the optimizer); MoeLayer turns it off for its
+// single-GPU calls (b2_common.cuh PdlScope)
+static thread_local bool g_pdl = true;
+bool pdl_enabled() { return g_pdl; }
+void set_pdl_enabled(bool on) { g_pdl = on; }
 }  // namespace b2
 
 extern "C" {

@@ -405,6 +405,7 @@ void MoeLayer::forward(const void* x, const void* router, const void* gate, cons
                        int64_t s, bool fur, void* out) {
     check(s >= 0 && s <= smax_, "fast_moe: token count exceeds the layer's capacity");
     B2_CUDA(cudaSetDevice(ctx_.device));
+    const PdlScope pdl(pdl_for_layer());
     s_ = s;
     t_ = s * cfg_.ep;
     th_ = ceil_div(std::max<int64_t>(t_, 0), cfg_.token_block);
@@ -595,6 +596,7 @@ void MoeLayer::backward(const void* router, const void* gate, const void* up, co
                         const float* aux_probs_grad, void* dx, void* drouter, void* dgate, void* dup, void* ddown) {
     check(have_fwd_, "fast_moe_backward: no forward state");
     B2_CUDA(cudaSetDevice(ctx_.device));
+    const PdlScope pdl(pdl_for_layer());
     launches_ = 0;
     run_graphed(gbwd_,
                 {router, gate, up, down, dout, aux_probs_grad, dx, drouter, dgate, dup, ddown, x_,

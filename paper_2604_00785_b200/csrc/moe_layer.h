@@ -200,6 +200,11 @@ class MoeLayer {
     // 5.66 / 5.77 / 5.98 ms per step, serial return 5.76; EP 2: serial 5.04-5.06 against 5.17-5.29
     // with 32 SMs — so the return overlaps from EP 4 up and runs after the GEMMs at EP 2
     bool overlap_return() const;
+    // programmatic dependent launch inside the layer's graphs: on with EP (the NVLink kernels'
+    // early launch pays: EP 4 5.62-5.65 vs 5.71 ms per step), off on one GPU, where the early-
+    // resident dependents cost about what the hidden prologues save (17 alternated rounds on
+    // four boxes: -60 us per step on average, single rounds from -240 to +70 us)
+    bool pdl_for_layer() const { return cfg_.ep > 1; }
     static constexpr int kCommSms = 32;
     static constexpr int kOverlapMinEp = 4;
     bool overlap_opt_ = true;
