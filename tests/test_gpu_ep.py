@@ -11,6 +11,7 @@ import socket
 import subprocess
 import sys
 import tempfile
+import time
 
 import pytest
 
@@ -26,18 +27,51 @@ def free_port():
         return s.getsockname()[1]
 
 
+def wait_all(procs, timeout):
+    """Exit codes of the rank processes; once one fails (or time runs out) the others, which
+    would wait for it in a collective, are killed (our own children, by handle)."""
+    t_end = time.monotonic() + timeout
+    while True:
+        codes = [p.poll() for p in procs]
+        if all(c is not None for c in codes):
+            return codes
+        if any(c not in (None, 0) for c in codes) or time.monotonic() > t_end:
+            for p in procs:
+                if p.poll() is None:
+                    p.kill()
+            return [p.wait() for p in procs]
+        time.sleep(0.2)
+
+
+def launch_world(script, world, extra, tail=(), attempts=3):
+    """Runs `script rank world port *extra res *tail` on `world` ranks and returns the result JSON rank
+    0 wrote. The rendezvous port is picked free but can be taken before rank 0 binds it; a launch
+    whose ranks fail with EADDRINUSE is retried on a new port (any other failure is reported)."""
+    for attempt in range(attempts):
+        port = free_port()
+        with tempfile.TemporaryDirectory() as td:
+            res = os.path.join(td, "res.json")
+            errs = [open(os.path.join(td, f"err{r}.txt"), "w+") for r in range(world)]
+            procs = [subprocess.Popen([sys.executable, os.path.join(HERE, script), str(r), str(world), str(port),
+                                       *extra, res, *tail], stderr=errs[r]) for r in range(world)]
+            codes = wait_all(procs, timeout=600)
+            text = []
+            for e in errs:
+                e.seek(0)
+                text.append(e.read())
+                e.close()
+            if all(c == 0 for c in codes):
+                with open(res) as f:
+                    return json.load(f)
+            busy = any("EADDRINUSE" in t or "address already in use" in t for t in text)
+            if not busy or attempt == attempts - 1:
+                raise AssertionError(f"{script} ranks exited {codes}:\n" + "\n".join(t[-3000:] for t in text))
+
+
 def run_world(world, case):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
-    port = free_port()
-    with tempfile.TemporaryDirectory() as td:
-        res = os.path.join(td, "res.json")
-        procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "ep_worker.py"), str(r), str(world), str(port),
-                                   json.dumps(case), res]) for r in range(world)]
-        for p in procs:
-            assert p.wait(timeout=600) == 0
-        with open(res) as f:
-            return json.load(f)
+    return launch_world("ep_worker.py", world, [json.dumps(case)])
 
 
 CASES = [
@@ -74,15 +108,7 @@ def run_opt(dp, ep, mode, bf16=False):
     world = dp * ep
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
-    port = free_port()
-    with tempfile.TemporaryDirectory() as td:
-        res = os.path.join(td, "res.json")
-        procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "opt_worker.py"), str(r), str(world), str(port),
-                                   str(dp), str(ep), str(mode), res, "1" if bf16 else "0"]) for r in range(world)]
-        for p in procs:
-            assert p.wait(timeout=600) == 0
-        with open(res) as f:
-            return json.load(f)
+    return launch_world("opt_worker.py", world, [str(dp), str(ep), str(mode)], ["1" if bf16 else "0"])
 
 
 @pytest.mark.parametrize("dp,ep,mode", [(2, 1, 0), (2, 1, 1), (2, 1, 2), (1, 2, 1), (1, 2, 2), (2, 2, 2), (2, 2, 1),
