@@ -203,7 +203,8 @@ class MoeLayer {
     // programmatic dependent launch inside the layer's graphs: on with EP (the NVLink kernels'
     // early launch pays: EP 4 5.62-5.65 vs 5.71 ms per step), off on one GPU, where the early-
     // resident dependents cost about what the hidden prologues save (17 alternated rounds on
-    // four boxes: -60 us per step on average, single rounds from -240 to +70 us)
+    // four boxes: -60 us per step on average, single rounds from -240 to +70 us; in 100-step
+    // runs held at the power cap (~1.45 GHz) the two are within 15 us)
     bool pdl_for_layer() const { return cfg_.ep > 1; }
     static constexpr int kCommSms = 32;
     static constexpr int kOverlapMinEp = 4;
