@@ -260,7 +260,8 @@ double b2_lr_at_step(int64_t step, const b2_adamw_cfg* cfg);
 int b2_shard_slice(int64_t numel, int group_size, int position, int64_t* begin, int64_t* end);
 /* per-stage CUDA-event timing of the layer (route, index, gather, the six GEMMs,
  * combine, output-reduction backward, router backward): enable, run, then read
- * B2_MOE_NUM_STAGES floats in ms (synchronises). */
+ * B2_MOE_NUM_STAGES floats in ms (synchronises). on: 0 off; 1 eager launches, the mean over
+ * the profiled calls; 2 inside the CUDA graphs (graph mode), the last replayed call. */
 #define B2_MOE_NUM_STAGES 12
 int b2_moe_set_profiling(b2_moe* m, int on);
 int b2_moe_stage_times(b2_moe* m, float* ms_host);

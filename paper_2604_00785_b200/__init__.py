@@ -375,7 +375,9 @@ class MoeLayer:
 
     NUM_STAGES = 12
 
-    def set_profiling(self, on: bool = True):
+    def set_profiling(self, on=True):
+        """0 / False off; 1 / True eager per-stage events (mean over calls); 2 per-stage events
+        inside the CUDA graphs (graph mode; the last replayed call)."""
         _check(lib().b2_moe_set_profiling(self.h, int(on)))
 
     def stage_times(self) -> dict:

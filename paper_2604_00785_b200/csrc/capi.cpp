@@ -717,7 +717,7 @@ int b2_shard_slice(int64_t numel, int group_size, int position, int64_t* begin, 
     return guard([&] { shard_slice(numel, group_size, position, begin, end); });
 }
 
-int b2_moe_set_profiling(b2_moe* m, int on) { return guard([&] { m->layer->set_profiling(on != 0); }); }
+int b2_moe_set_profiling(b2_moe* m, int on) { return guard([&] { m->layer->set_profiling(on); }); }
 int b2_moe_set_graph(b2_moe* m, int on) { return guard([&] { m->layer->set_graph(on != 0); }); }
 int b2_moe_stage_times(b2_moe* m, float* ms_host) { return guard([&] { m->layer->stage_times(ms_host); }); }
 const char* b2_moe_stage_name(int stage) { return MoeLayer::stage_name(stage); }

@@ -298,9 +298,11 @@ const char* MoeLayer::stage_name(int s) {
 // (up to kMaxProfSteps); stage_times() returns the mean over the recorded steps.
 constexpr int kMaxProfSteps = 256;
 
-void MoeLayer::set_profiling(bool on) {
-    profiling_ = on;
+void MoeLayer::set_profiling(int mode) {
+    check(mode >= 0 && mode <= 2, "set_profiling: mode is 0, 1 or 2");
+    profiling_ = mode;
     prof_step_ = -1;
+    set_graph(graph_);  // graphs captured with (or without) the stage events must not be replayed
 }
 
 void MoeLayer::mark(int stage, bool end) {
@@ -310,7 +312,12 @@ void MoeLayer::mark(int stage, bool end) {
         for (cudaEvent_t& e : v) B2_CUDA(cudaEventCreate(&e));
         prof_ev_.push_back(std::move(v));
     }
-    B2_CUDA(cudaEventRecord(prof_ev_[(size_t)prof_step_][(size_t)(2 * stage + (end ? 1 : 0))], ctx_.stream));
+    cudaEvent_t ev = prof_ev_[(size_t)prof_step_][(size_t)(2 * stage + (end ? 1 : 0))];
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    B2_CUDA(cudaStreamIsCapturing(ctx_.stream, &cs));
+    // under capture (in-graph profiling) the record becomes an event-record node of the graph
+    if (cs == cudaStreamCaptureStatusActive) B2_CUDA(cudaEventRecordWithFlags(ev, ctx_.stream, cudaEventRecordExternal));
+    else B2_CUDA(cudaEventRecord(ev, ctx_.stream));
 }
 
 void MoeLayer::stage_times(float* ms) {
@@ -347,7 +354,7 @@ void MoeLayer::set_graph(bool on) {
 template <typename F>
 void MoeLayer::run_graphed(GraphCache (&gcs)[kGraphSlots], std::vector<const void*> key, F&& body) {
     cudaStream_t st = ctx_.stream;
-    if (!graph_ || profiling_ || st == nullptr) {  // the legacy default stream cannot be captured
+    if (!graph_ || profiling_ == 1 || st == nullptr) {  // the legacy default stream cannot be captured
         body();
         return;
     }
@@ -413,7 +420,8 @@ void MoeLayer::forward(const void* x, const void* router, const void* gate, cons
     x_ = x;
     set_dispatch_tables();
     launches_ = 0;
-    if (profiling_) ++prof_step_;
+    if (profiling_ == 1) ++prof_step_;
+    else if (profiling_ == 2) prof_step_ = 0;  // in-graph: one event set, rewritten by every replay
     run_graphed(gfwd_, {x, router, gate, up, down, out, (const void*)(intptr_t)s, (const void*)(intptr_t)fur}, [&] {
         if (dtype_ == F32)
             forward_t<float>((const float*)x, (const float*)router, (const float*)gate, (const float*)up,

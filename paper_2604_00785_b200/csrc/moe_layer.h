@@ -111,13 +111,15 @@ class MoeLayer {
     // number of kernels of this library launched by the last forward / backward
     int last_launches() const { return launches_; }
 
-    // per-stage CUDA-event timing of the last forward+backward (profiling mode)
+    // per-stage CUDA-event timing (profiling mode): 1 = eager launches, the mean over every
+    // forward+backward since enabling; 2 = inside the CUDA graphs (event-record nodes around
+    // each stage), the times of the last replayed forward+backward
     enum Stage {
         kRoute, kIndex, kGather, kGemmGateUp, kGemmDown, kCombine, kOutRedBwd, kGemmDgrad, kGemmWgradDown,
         kGemmWgradGateUp, kGemmDx, kRouterBwd, kNumStages
     };
     static const char* stage_name(int s);
-    void set_profiling(bool on);
+    void set_profiling(int mode);
     void stage_times(float* ms);  // synchronises
 
     // CUDA-graph mode: a forward (backward) whose arguments repeat the previous call's is
@@ -160,7 +162,7 @@ class MoeLayer {
 
     Context& ctx_;
     MoeConfig cfg_;
-    bool profiling_ = false;
+    int profiling_ = 0;
     int prof_step_ = -1;  // index of the profiled forward+backward being recorded
     std::vector<std::vector<cudaEvent_t>> prof_ev_;  // [step][stage*2 + end]
     int dtype_;
