@@ -82,7 +82,7 @@ struct HostIo {
     size_t slot_bytes = 0;
     int64_t cap_tokens = -1;
     cudaStream_t h2d = nullptr, d2h = nullptr;
-    cudaEvent_t ev_in[2] = {}, ev_fwd[2] = {}, ev_bwd[2] = {}, ev_out[2] = {};
+    cudaEvent_t ev_x[2] = {}, ev_in[2] = {}, ev_fwd[2] = {}, ev_bwd[2] = {}, ev_out[2] = {};
     bool used[2] = {false, false};
     int next = 0;
     bool warned_pageable = false;
@@ -216,7 +216,7 @@ int b2_moe_destroy(b2_moe* m) {
         if (io.d2h) cudaStreamSynchronize(io.d2h);
         if (io.dev) cudaFree(io.dev);
         for (int b = 0; b < 2; ++b)
-            for (cudaEvent_t e : {io.ev_in[b], io.ev_fwd[b], io.ev_bwd[b], io.ev_out[b]})
+            for (cudaEvent_t e : {io.ev_x[b], io.ev_in[b], io.ev_fwd[b], io.ev_bwd[b], io.ev_out[b]})
                 if (e) cudaEventDestroy(e);
         if (io.h2d) cudaStreamDestroy(io.h2d);
         if (io.d2h) cudaStreamDestroy(io.d2h);
@@ -280,9 +280,9 @@ int b2_moe_artifacts(b2_moe* m, int64_t* sizes_host, int64_t* token_counts, int6
 }
 
 // Enqueues one forward+backward over host buffers on a two-slot pipeline:
-//   h2d stream : [wait: slot's previous backward] x, dout -> slot          (ev_in)
-//   compute    : [wait ev_in, slot's previous out/dx read-back] forward (ev_fwd), aux grad,
-//                backward (ev_bwd)
+//   h2d stream : [wait: slot's previous backward] x (ev_x), dout -> slot (ev_in)
+//   compute    : [wait ev_x, slot's previous out/dx read-back] forward (ev_fwd), [wait ev_in]
+//                aux grad, backward (ev_bwd)
 //   d2h stream : [wait ev_fwd] out -> host, [wait ev_bwd] dx -> host       (ev_out)
 static void fwd_bwd_host_enqueue(b2_moe* m, const void* x_host, const void* dout_host, const void* router,
                                  const void* gate, const void* up, const void* down, double aux_coeff,
@@ -308,7 +308,7 @@ static void fwd_bwd_host_enqueue(b2_moe* m, const void* x_host, const void* dout
             B2_CUDA(cudaStreamCreateWithFlags(&io.h2d, cudaStreamNonBlocking));
             B2_CUDA(cudaStreamCreateWithFlags(&io.d2h, cudaStreamNonBlocking));
             for (int b = 0; b < 2; ++b)
-                for (cudaEvent_t* e : {&io.ev_in[b], &io.ev_fwd[b], &io.ev_bwd[b], &io.ev_out[b]})
+                for (cudaEvent_t* e : {&io.ev_x[b], &io.ev_in[b], &io.ev_fwd[b], &io.ev_bwd[b], &io.ev_out[b]})
                     B2_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         }
     }
@@ -329,12 +329,15 @@ static void fwd_bwd_host_enqueue(b2_moe* m, const void* x_host, const void* dout
     cudaStream_t st = cx.stream;
     // inputs: the slot's previous step must be done reading x / dout
     if (io.used[b]) B2_CUDA(cudaStreamWaitEvent(io.h2d, io.ev_bwd[b], 0));
+    // the forward waits for x only; dout lands while it runs (the backward waits for it)
     B2_CUDA(cudaMemcpyAsync(xd, x_host, tok_bytes, cudaMemcpyHostToDevice, io.h2d));
+    B2_CUDA(cudaEventRecord(io.ev_x[b], io.h2d));
     B2_CUDA(cudaMemcpyAsync(doutd, dout_host, tok_bytes, cudaMemcpyHostToDevice, io.h2d));
     B2_CUDA(cudaEventRecord(io.ev_in[b], io.h2d));
-    B2_CUDA(cudaStreamWaitEvent(st, io.ev_in[b], 0));
+    B2_CUDA(cudaStreamWaitEvent(st, io.ev_x[b], 0));
     if (io.used[b]) B2_CUDA(cudaStreamWaitEvent(st, io.ev_out[b], 0));  // out/dx of the slot read back
     L.forward(xd, router, gate, up, down, s_tokens, false, outd);
+    B2_CUDA(cudaStreamWaitEvent(st, io.ev_in[b], 0));
     B2_CUDA(cudaEventRecord(io.ev_fwd[b], st));
     const float* ag = nullptr;
     if (aux_coeff != 0.0) {
