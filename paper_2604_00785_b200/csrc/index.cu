@@ -113,6 +113,62 @@ __device__ int64_t block_scan(int64_t n, Get get, Put put, int* wsum) {
     return carry;
 }
 
+// block_scan over an int32 array with 16-byte loads and stores (in, out 16-byte aligned; the
+// last partial group of 16 element-wise)
+__device__ int64_t block_scan_i32(const int32_t* __restrict__ in, int32_t* __restrict__ out, int64_t n, int* wsum) {
+    constexpr int R = 16;
+    const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nw = blockDim.x / 32;
+    int64_t carry = 0;
+    for (int64_t base = 0; base < n; base += (int64_t)blockDim.x * R) {
+        const int64_t i0 = base + (int64_t)threadIdx.x * R;
+        int v[R];
+        if (i0 + R <= n) {
+#pragma unroll
+            for (int q = 0; q < R / 4; ++q) {
+                const int4 w = *reinterpret_cast<const int4*>(in + i0 + 4 * q);
+                v[4 * q] = w.x;
+                v[4 * q + 1] = w.y;
+                v[4 * q + 2] = w.z;
+                v[4 * q + 3] = w.w;
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[r] = i0 + r < n ? in[i0 + r] : 0;
+        }
+        int tsum = 0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) tsum += v[r];
+        const int x = warp_incl_scan(tsum, lane);
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            const int s = lane < nw ? wsum[lane] : 0;
+            const int si = warp_incl_scan(s, lane);
+            if (lane < nw) wsum[lane] = si;
+        }
+        __syncthreads();
+        int excl = (int)carry + (warp > 0 ? wsum[warp - 1] : 0) + x - tsum;
+        int o[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            o[r] = excl;
+            excl += v[r];
+        }
+        if (i0 + R <= n) {
+#pragma unroll
+            for (int q = 0; q < R / 4; ++q)
+                *reinterpret_cast<int4*>(out + i0 + 4 * q) = make_int4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (i0 + r < n) out[i0 + r] = o[r];
+        }
+        carry += wsum[nw - 1];
+        __syncthreads();
+    }
+    return carry;
+}
+
 // 2. scans, one CTA of 1024 threads
 __global__ void __launch_bounds__(1024) scan_kernel(const int32_t* __restrict__ whist, int nchunks, int nr,
                                                     const int32_t* __restrict__ expert_counts, int T,
@@ -128,28 +184,54 @@ __global__ void __launch_bounds__(1024) scan_kernel(const int32_t* __restrict__ 
     __shared__ int wsum[32];
     const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nw = blockDim.x / 32;
     // (a) within-expert chunk offsets (expert-major, chunk-minor == the reference's
-    //     partial_cum order restricted to whole chunks)
-    for (int ln = warp; ln < nr; ln += nw) {
+    //     partial_cum order restricted to whole chunks). With fewer experts than warps (EP:
+    //     nr = N / EP over a table EP times longer) each expert's chunks are split into
+    //     segments over wpe warps, then every segment adds the totals of the ones before it
+    __shared__ int segsum[32];
+    const int wpe = nr >= nw ? 1 : nw / nr;           // warps per expert
+    const int ngroups = nw / wpe;                     // experts in flight
+    const int seg = (int)ceil_div(nchunks, wpe);      // chunks per warp segment
+    for (int e0 = 0; e0 < nr; e0 += ngroups) {
+        const int ln = e0 + warp / wpe, sg = warp % wpe;
+        const bool active = warp < ngroups * wpe && ln < nr;
+        const int c0 = sg * seg, c1 = min(nchunks, c0 + seg);
         int carry = 0;
-        const int32_t* hrow = whist + (int64_t)ln * nchunks;
-        int32_t* brow = wbase + (int64_t)ln * nchunks;
-        constexpr int P = 8;  // 8 x 32 chunk counts loaded together, then scanned in order
-        for (int cb = 0; cb < nchunks; cb += 32 * P) {
-            int vv[P];
+        if (active) {
+            const int32_t* hrow = whist + (int64_t)ln * nchunks;
+            int32_t* brow = wbase + (int64_t)ln * nchunks;
+            constexpr int P = 8;  // 8 x 32 chunk counts loaded together, then scanned in order
+            for (int cb = c0; cb < c1; cb += 32 * P) {
+                int vv[P];
 #pragma unroll
-            for (int q = 0; q < P; ++q) {
-                const int c = cb + 32 * q + lane;
-                vv[q] = c < nchunks ? hrow[c] : 0;
-            }
+                for (int q = 0; q < P; ++q) {
+                    const int c = cb + 32 * q + lane;
+                    vv[q] = c < c1 ? hrow[c] : 0;
+                }
 #pragma unroll
-            for (int q = 0; q < P; ++q) {
-                const int c = cb + 32 * q + lane;
-                const int x = warp_incl_scan(vv[q], lane);
-                if (c < nchunks) brow[c] = carry + x - vv[q];
-                carry += __shfl_sync(0xffffffffu, x, 31);
+                for (int q = 0; q < P; ++q) {
+                    const int c = cb + 32 * q + lane;
+                    const int x = warp_incl_scan(vv[q], lane);
+                    if (c < c1) brow[c] = carry + x - vv[q];
+                    carry += __shfl_sync(0xffffffffu, x, 31);
+                }
             }
         }
-        if (lane == 0) tot[ln] = carry;
+        if (wpe > 1) {
+            if (lane == 0) segsum[warp] = active ? carry : 0;
+            __syncthreads();
+            if (active) {
+                int off = 0;
+                for (int q = 0; q < sg; ++q) off += segsum[warp - sg + q];
+                if (off) {
+                    int32_t* brow = wbase + (int64_t)ln * nchunks;
+                    for (int c = c0 + lane; c < c1; c += 32) brow[c] += off;
+                }
+                if (sg == wpe - 1 && lane == 0) tot[ln] = off + carry;
+            }
+            __syncthreads();
+        } else if (active && lane == 0) {
+            tot[ln] = carry;
+        }
     }
     __syncthreads();
     // (b) expert boundaries and padded starts (warp 0)
@@ -183,10 +265,9 @@ __global__ void __launch_bounds__(1024) scan_kernel(const int32_t* __restrict__ 
             for (int j = 0; j < nr; ++j) r += (tot[j] > ce) || (tot[j] == ce && j < e);
             expert_order[r] = e;
         }
-    // (c) cum_expert_counts: exclusive scan of the per-token local counts
-    const int64_t te = block_scan(
-        T, [&](int64_t i) { return expert_counts[i]; }, [&](int64_t i, int64_t v) { cum_expert_counts[i] = (int32_t)v; },
-        wsum);
+    // (c) cum_expert_counts: exclusive scan of the per-token local counts (16 per thread per
+    //     round, moved as 16-byte vectors: the table is EP times longer than the local tokens)
+    const int64_t te = block_scan_i32(expert_counts, cum_expert_counts, T, wsum);
     if (threadIdx.x == 0) cum_expert_counts[T] = (int32_t)te;
 }
 
