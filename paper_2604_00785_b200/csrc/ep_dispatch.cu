@@ -10,13 +10,13 @@
 //   gather   the expert owner PULLS each gathered token that has a local expert once
 //            from the source rank's x over NVLink (CUDA IPC mapping) and writes it to
 //            every padded row of that token (dedup per destination);
-//   combine  the owner combines the token's local slots (weighted, slot order) into its OWN
-//            slab row [gid]; after a barrier the source PULLS the rows of the ranks its
-//            token routed to and sums them in rank order (the reducescatter's member order,
-//            comm.hpp:391-394) — remote loads with many bytes in flight, fused with the sum.
-// The backward pulls dout rows the same way; dX partial rows and the top-k weight
-// gradients go back through the owners' slabs and the same pull-sum. No host
-// synchronisation, no staging copies.
+//   combine  the owner combines the token's local slots (weighted, slot order) and PUSHES the
+//            partial row into the source rank's slab, row [owner][token] (NVLink stores);
+//            after a barrier the source sums the rows of the ranks its token routed to in
+//            rank order (the reducescatter's member order, comm.hpp:391-394), locally.
+// The backward pulls dout rows the same way and returns dX partial rows by the same push +
+// sum; the top-k weight gradients stay in the owners' slabs and are pulled and summed (a
+// few KB). No host synchronisation, no staging copies.
 #include "b2_common.cuh"
 #include "kernels.h"
 
@@ -138,10 +138,10 @@ __global__ void ep_combine_slots_kernel(const T* __restrict__ y, const int32_t* 
     }
 }
 
-// out[t] = sum over the ranks r (in order) that token t routes to of owner r's partial row
-// [me * S + t], read over NVLink from r's own slab (written there before the barrier):
-// the reducescatter of moe.hpp:378 / 427-428 in member order, as remote loads with up to
-// 8 owners' 16-byte vectors in flight per lane
+// out[t] = sum over the ranks r (in order) that token t routes to of owner r's partial row:
+// pushed, row [r * S + t] of this rank's own slab; pulled, row [me * S + t] of r's slab over
+// NVLink (both written before the barrier) — the reducescatter of moe.hpp:378 / 427-428 in
+// member order, with up to 8 owners' 16-byte vectors in flight per lane
 template <typename T>
 __device__ __forceinline__ void ep_pull_sum_token(const T* const* __restrict__ peer_slab,
                                                   const int32_t* __restrict__ gi_local, int S, int K, int E, int NR,

@@ -707,8 +707,9 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         launches_ += 1;
         mark(kGemmDgrad, true);
         if (overlap_return()) {
-            // EP > 1: dX first, then its return to the source ranks (owner combine, barrier,
-            // NVLink pull-sums: the reducescatters of moe.hpp:427-428) runs on a side stream
+            // EP > 1: dX first, then its return to the source ranks (owner combine pushed into
+            // the sources' slabs, barrier, rank-order sums: the reducescatters of moe.hpp:427-428)
+            // runs on a side stream
             // while the weight-gradient GEMMs run on the SMs left to them
             ga.kind = GemmKind::BwdDx;  // 414-415
             ga.out0 = dxp_;
@@ -842,10 +843,10 @@ void MoeLayer::backward_t(const T* router, const T* gate, const T* up, const T* 
         wgrad_local = wgrad_local_;
         dx_rows = (const T*)dx_exp_;
     } else if (E > 1) {
-        // the two reducescatters of moe.hpp:427-428: owners combine dX partials into their own
-        // slab (the top-k weight gradients already sit in their own wret, written by the
-        // output-reduction backward); after the barrier each source pulls and sums its rows in
-        // rank order
+        // the two reducescatters of moe.hpp:427-428: owners combine dX partials and push them
+        // into the sources' slabs (the top-k weight gradients already sit in the owners' wret);
+        // after the barrier each source sums its dX rows and pulls and sums its weight
+        // gradients, in rank order
         launch_ep_combine_local<T>((const T*)dxp_, slot_prow_, selected_k_, cec_, nullptr, K, S, Tt, H, (T*)ret_b_,
                                    st, 0, (T* const*)peer_tab_ + 3 * E, ctx_.coord_ep);
         ep_barrier();
